@@ -1,0 +1,176 @@
+/* dcsc_cuda.h — C-ABI of the B200 (sm_100a) dual-domain CSC hot path.
+ *
+ * Drop-in boundary for the reference's solver API (arXiv 1709.09479
+ * reference, /root/reference/proj). No exceptions or torch types cross it:
+ * every entry returns a status code; dcsc_cuda_last_error() gives the message.
+ * Plain host pointers and sizes only; all hot-path state stays device-resident
+ * between calls inside the opaque context.
+ *
+ * Entry point -> reference interface it replaces:
+ *   dcsc_cuda_create / _destroy     dcsc::SolverConfig + RunConfig
+ *                                   (include/dcsc/types.hpp:96-110,
+ *                                    include/dcsc/pipeline.hpp:19-26)
+ *   dcsc_cuda_set_signals           Dataset signals + dcsc::normalize
+ *                                   (pipeline.hpp:13-16, 32; pipeline.cpp:78-121)
+ *   dcsc_cuda_set_dictionary/get    dcsc::Dictionary (types.hpp:62-78)
+ *   dcsc_cuda_init_dictionary       dcsc::init_variables (pipeline.hpp:44-45;
+ *                                   pipeline.cpp:123-156)
+ *   dcsc_cuda_set/get_coding_state  dcsc::CodingDualState (coding.hpp:15-25)
+ *   dcsc_cuda_coding                dcsc::solve_coding (coding.hpp:74-77),
+ *                                   batched over images: replaces the OpenMP
+ *                                   loop at pipeline.cpp:221-227
+ *   dcsc_cuda_set/get_maps          dcsc::SparseMaps (types.hpp:81-94)
+ *   dcsc_cuda_set/get_learning_state dcsc::LearningDualState (learning.hpp:15-23)
+ *   dcsc_cuda_learning              dcsc::solve_learning (learning.hpp:99-104)
+ *   dcsc_cuda_objective             dcsc::evaluate_objective (objective.hpp:14-15)
+ *   dcsc_cuda_learning_data_term    dcsc::learning_data_term (objective.hpp:18-19)
+ *   dcsc_cuda_learning_apply        dcsc::LearningOperator::apply (learning.hpp:57)
+ *   dcsc_cuda_run                   dcsc::run_csc (pipeline.hpp:58) + trace rows
+ *                                   (types.hpp:122-136, trace_io.hpp)
+ *   dcsc_cuda_dft2_forward/_inverse dcsc::forward_dft / inverse_dft
+ *                                   (spectral.hpp:27-38), half-spectrum form
+ */
+#ifndef DCSC_CUDA_H
+#define DCSC_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mirroring the reference's exception classes, types.hpp:24-38) */
+#define DCSC_OK 0
+#define DCSC_ERR_DIMENSION 1 /* dcsc::DimensionError */
+#define DCSC_ERR_NUMERIC 2   /* dcsc::NumericError */
+#define DCSC_ERR_CUDA 3      /* CUDA / NCCL failure */
+#define DCSC_ERR_INVALID 4   /* std::invalid_argument from validate() */
+
+typedef struct dcsc_cuda_ctx dcsc_cuda_ctx;
+
+/* dcsc::SolverConfig (types.hpp:96-110); normalize: 0 None, 1 Global, 2 Local */
+typedef struct {
+  double beta, rho, tol;
+  int max_outer, max_admm, max_mu_iters;
+  double cg_tol;
+  int cg_max;
+  double mu_floor;
+  uint64_t seed;
+  int normalize;
+} dcsc_solver_config;
+
+typedef struct {
+  int n_images;            /* N */
+  int height, width;       /* grid H x W (row-major, last axis fastest) */
+  int filters;             /* K */
+  int support_h, support_w;
+  int precision;           /* 32 or 64: storage/FFT precision; reductions are FP64 */
+  int device;              /* CUDA device ordinal */
+  dcsc_solver_config cfg;
+} dcsc_cuda_opts;
+
+/* dcsc::CodingStats (coding.hpp:27-37) */
+typedef struct {
+  int admm_iters, converged, degenerate_dictionary, dual_rescaled;
+  double primal_residual, theta_change, z_change, dual_objective, dual_infeasibility;
+} dcsc_coding_stats;
+
+/* dcsc::LearningStats (learning.hpp:25-35); dead filters reported by count */
+typedef struct {
+  int mu_iters;
+  long cg_iters, cg_iters_first;
+  int converged, degenerate, mu_clamped, cg_budget_hit, rescaled_filters, n_dead;
+} dcsc_learning_stats;
+
+/* dcsc::ObjectiveBreakdown (types.hpp:112-117) */
+typedef struct {
+  double data_term, l1_term, total, residual_norm;
+} dcsc_objective;
+
+/* dcsc::TraceRow (types.hpp:122-129) + mu_iters, wall time, l0 of the maps */
+typedef struct {
+  int outer_iter, phase; /* phase 0 coding, 1 learning */
+  double total, data_term, l1_term, residual_norm;
+  long admm_iters, cg_iters;
+  int mu_iters;
+  double elapsed_ms; /* solver call only (the reference's timer) */
+  double wall_ms;    /* whole half-step incl. objective bookkeeping */
+  long l0;           /* non-zero entries of the accepted maps */
+} dcsc_trace_row;
+
+int dcsc_cuda_last_error(char* buf, size_t len);
+/* 1 when a kernel family for this grid / precision is compiled in */
+int dcsc_cuda_supported_grid(int height, int width, int precision);
+
+int dcsc_cuda_create(const dcsc_cuda_opts* opts, dcsc_cuda_ctx** out);
+int dcsc_cuda_destroy(dcsc_cuda_ctx* ctx);
+int dcsc_cuda_synchronize(dcsc_cuda_ctx* ctx);
+
+/* signals x: N*H*W doubles; normalised per cfg.normalize (pipeline.cpp:78-121) */
+int dcsc_cuda_set_signals(dcsc_cuda_ctx* ctx, const double* x);
+int dcsc_cuda_get_signals(dcsc_cuda_ctx* ctx, double* x);
+/* dictionary: K*mh*mw doubles */
+int dcsc_cuda_set_dictionary(dcsc_cuda_ctx* ctx, const double* d);
+int dcsc_cuda_get_dictionary(dcsc_cuda_ctx* ctx, double* d);
+/* init_variables: seeded dictionary, zero maps / coding state, gamma = 0, mu = 1 */
+int dcsc_cuda_init_variables(dcsc_cuda_ctx* ctx);
+
+/* warm coding state for images [n0, n1): theta, z (K*D each per image), NULL = zeros */
+int dcsc_cuda_set_coding_state(dcsc_cuda_ctx* ctx, int n0, int n1, const double* theta,
+                               const double* z);
+int dcsc_cuda_get_coding_state(dcsc_cuda_ctx* ctx, int n0, int n1, double* theta, double* z,
+                               double* lambda);
+/* solve_coding for images [n0, n1) against the context dictionary */
+int dcsc_cuda_coding(dcsc_cuda_ctx* ctx, int n0, int n1, dcsc_coding_stats* stats);
+
+/* accepted maps used by learning / objective: K*D per image */
+int dcsc_cuda_set_maps(dcsc_cuda_ctx* ctx, int n0, int n1, const double* z);
+int dcsc_cuda_get_maps(dcsc_cuda_ctx* ctx, int n0, int n1, double* z);
+
+/* learning warm state: gamma N*D (NULL = zeros), mu K (NULL = ones) */
+int dcsc_cuda_set_learning_state(dcsc_cuda_ctx* ctx, const double* gamma, const double* mu);
+int dcsc_cuda_get_learning_state(dcsc_cuda_ctx* ctx, double* gamma, double* mu);
+/* solve_learning over all images' maps; writes the candidate dictionary
+ * (K*mh*mw) to d_out without installing it */
+int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* stats);
+/* LearningOperator::apply with the given mu on N*D vectors */
+int dcsc_cuda_learning_apply(dcsc_cuda_ctx* ctx, const double* mu, const double* v, double* out);
+
+/* evaluate_objective(x_n, d, maps_n) for every image; d NULL = context dictionary */
+int dcsc_cuda_objective(dcsc_cuda_ctx* ctx, const double* d, dcsc_objective* per_image);
+/* learning_data_term(xs, d, maps) */
+int dcsc_cuda_learning_data_term(dcsc_cuda_ctx* ctx, const double* d, double* data);
+
+/* run_csc from init_variables: rows needs 2*max_outer entries */
+int dcsc_cuda_run(dcsc_cuda_ctx* ctx, int max_outer, dcsc_trace_row* rows, int* n_rows,
+                  int* converged);
+
+/* standalone half-spectrum DFTs of a batch of H x W real planes:
+ * forward writes batch * H * (W/2+1) complex (interleaved re,im) */
+int dcsc_cuda_dft2_forward(int height, int width, int precision, int batch, const double* in,
+                           double* out);
+int dcsc_cuda_dft2_inverse(int height, int width, int precision, int batch, const double* in,
+                           double* out);
+
+/* measurement: kernels launched by this context so far; per-kernel-family
+ * CUDA-event timing (family: 0 coding_pass ADMM, 1 lambda_update,
+ * 2 learning contractions, 3 learning mask step, 4 other) */
+int dcsc_cuda_kernel_launches(dcsc_cuda_ctx* ctx, long long* count);
+int dcsc_cuda_set_profiling(dcsc_cuda_ctx* ctx, int enable);
+int dcsc_cuda_kernel_time(dcsc_cuda_ctx* ctx, int family, double* total_ms, long long* launches);
+/* device-event timer on the context stream: mark(slot), elapsed(slot a, slot b) */
+int dcsc_cuda_event_mark(dcsc_cuda_ctx* ctx, int slot);
+int dcsc_cuda_event_elapsed(dcsc_cuda_ctx* ctx, int a, int b, double* ms);
+/* bytes of device memory held by the context */
+int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes);
+
+/* synthetic BASELINE data (host only, no GPU): x N*H*W, d_true K*m*m */
+int dcsc_synth_generate(int n_images, int height, int width, int filters, int m, double p,
+                        double sigma, uint64_t seed, int round_fp32, double* x, double* d_true);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DCSC_CUDA_H */

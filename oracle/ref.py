@@ -1,0 +1,223 @@
+"""ctypes binding of oracle/_ref/libdcsc_ref.so (TEST INFRASTRUCTURE ONLY).
+
+The library is the UNMODIFIED reference solver (proj/src/{types,parallel,
+spectral,objective,coding,learning,pipeline}.cpp) built by oracle/Makefile
+against the FFTW3-API shim. Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference leg may import this module; it is the checker,
+never the thing measured as the product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libdcsc_ref.so")
+
+
+class RefCfg(C.Structure):
+    _fields_ = [
+        ("beta", C.c_double), ("rho", C.c_double), ("tol", C.c_double),
+        ("max_outer", C.c_int), ("max_admm", C.c_int), ("max_mu_iters", C.c_int),
+        ("cg_tol", C.c_double), ("cg_max", C.c_int), ("mu_floor", C.c_double),
+        ("seed", C.c_uint64), ("normalize", C.c_int),
+    ]
+
+
+class RefCodingStats(C.Structure):
+    _fields_ = [
+        ("admm_iters", C.c_int), ("converged", C.c_int), ("degenerate_dictionary", C.c_int),
+        ("dual_rescaled", C.c_int), ("primal_residual", C.c_double), ("theta_change", C.c_double),
+        ("z_change", C.c_double), ("dual_objective", C.c_double), ("dual_infeasibility", C.c_double),
+    ]
+
+
+class RefLearningStats(C.Structure):
+    _fields_ = [
+        ("mu_iters", C.c_int), ("cg_iters", C.c_long), ("cg_iters_first", C.c_long),
+        ("converged", C.c_int), ("degenerate", C.c_int), ("mu_clamped", C.c_int),
+        ("cg_budget_hit", C.c_int), ("rescaled_filters", C.c_int), ("n_dead", C.c_int),
+    ]
+
+
+class RefTraceRow(C.Structure):
+    _fields_ = [
+        ("outer_iter", C.c_int), ("phase", C.c_int), ("total", C.c_double),
+        ("data_term", C.c_double), ("l1_term", C.c_double), ("residual_norm", C.c_double),
+        ("admm_iters", C.c_long), ("cg_iters", C.c_long), ("mu_iters", C.c_int),
+        ("elapsed_ms", C.c_double), ("wall_ms", C.c_double), ("l0", C.c_long),
+    ]
+
+
+@dataclass
+class Cfg:
+    """Mirror of dcsc::SolverConfig (proj/include/dcsc/types.hpp:96-110)."""
+    beta: float = 0.5
+    rho: float = 0.1
+    tol: float = 1e-3
+    max_outer: int = 50
+    max_admm: int = 500
+    max_mu_iters: int = 60
+    cg_tol: float = 1e-6
+    cg_max: int = 300
+    mu_floor: float = 1e-6
+    seed: int = 0
+    normalize: int = 1  # 0 None, 1 Global, 2 Local
+
+    def c(self) -> RefCfg:
+        return RefCfg(self.beta, self.rho, self.tol, self.max_outer, self.max_admm,
+                      self.max_mu_iters, self.cg_tol, self.cg_max, self.mu_floor,
+                      self.seed, self.normalize)
+
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"oracle reference library missing: {LIB_PATH} (run make -C oracle)")
+        _lib = C.CDLL(LIB_PATH)
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _check(rc):
+    if rc != 0:
+        buf = C.create_string_buffer(1024)
+        lib().ref_last_error(buf, 1024)
+        raise RuntimeError(f"reference error {rc}: {buf.value.decode()}")
+
+
+def set_threads(n: int) -> int:
+    return lib().ref_set_threads(int(n))
+
+
+def forward_dft(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dims = (C.c_int * x.ndim)(*x.shape)
+    out = np.zeros(x.shape, dtype=np.complex128)
+    _check(lib().ref_forward_dft(x.ndim, dims, _p(x), out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+def inverse_dft(s: np.ndarray) -> np.ndarray:
+    s = np.ascontiguousarray(s, dtype=np.complex128)
+    dims = (C.c_int * s.ndim)(*s.shape)
+    out = np.zeros(s.shape, dtype=np.float64)
+    _check(lib().ref_inverse_dft(s.ndim, dims, s.ctypes.data_as(C.POINTER(C.c_double)), _p(out)))
+    return out
+
+
+def init_dictionary(K: int, m: tuple[int, int], grid: tuple[int, int], seed: int) -> np.ndarray:
+    out = np.zeros((K, m[0], m[1]))
+    _check(lib().ref_init_dictionary(K, m[0], m[1], grid[0], grid[1], C.c_uint64(seed), _p(out)))
+    return out
+
+
+def solve_coding(x, d, cfg: Cfg, state=None):
+    """solve_coding (proj/src/coding.cpp:333-356). state = (theta, z, lambda) or None."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    H, W = x.shape
+    K, mh, mw = d.shape
+    if state is None:
+        theta = np.zeros((K, H, W)); z = np.zeros((K, H, W)); lam = np.zeros((H, W)); warm = 0
+    else:
+        theta, z, lam = (np.array(a, dtype=np.float64, copy=True) for a in state); warm = 1
+    st = RefCodingStats()
+    c = cfg.c()
+    _check(lib().ref_solve_coding(H, W, _p(x), K, mh, mw, _p(d), C.byref(c), warm,
+                                  _p(theta), _p(z), _p(lam), C.byref(st)))
+    stats = {f: getattr(st, f) for f, _ in RefCodingStats._fields_}
+    return z.copy(), (theta, z, lam), stats
+
+
+def solve_learning(xs, maps, support, cfg: Cfg, state=None):
+    """solve_learning (proj/src/learning.cpp:227-355). state = (gamma N*D, mu K) or None."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    N, H, W = xs.shape
+    K = maps.shape[1]
+    if state is None:
+        gamma = np.zeros((N, H, W)); mu = np.ones(K); warm = 0
+    else:
+        gamma = np.array(state[0], dtype=np.float64, copy=True).reshape(N, H, W)
+        mu = np.array(state[1], dtype=np.float64, copy=True); warm = 1
+    d = np.zeros((K, support[0], support[1]))
+    st = RefLearningStats()
+    c = cfg.c()
+    _check(lib().ref_solve_learning(N, H, W, _p(xs), K, _p(maps), support[0], support[1],
+                                    C.byref(c), warm, _p(gamma), _p(mu), _p(d), C.byref(st)))
+    stats = {f: getattr(st, f) for f, _ in RefLearningStats._fields_}
+    return d, (gamma, mu), stats
+
+
+def objective(x, d, z, beta):
+    """evaluate_objective (proj/src/objective.cpp:59-81) -> (data, l1, total, residual_norm)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.zeros(4)
+    H, W = x.shape
+    K, mh, mw = d.shape
+    _check(lib().ref_objective(H, W, _p(x), K, mh, mw, _p(d), _p(z), C.c_double(beta), _p(out)))
+    return tuple(out)
+
+
+def learning_apply(maps, support, mu, mu_floor, v):
+    """LearningOperator::apply (proj/src/learning.cpp:83-122)."""
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    N, K, H, W = maps.shape
+    out = np.zeros_like(v)
+    _check(lib().ref_learning_apply(N, H, W, K, _p(maps), support[0], support[1], _p(mu),
+                                    C.c_double(mu_floor), _p(v), _p(out)))
+    return out
+
+
+def run(xs, K, support, cfg: Cfg, dump_dicts=True):
+    """Instrumented run_csc replica (oracle/ref_capi.cpp:ref_run)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    N, H, W = xs.shape
+    mh, mw = support
+    rows = (RefTraceRow * (2 * max(cfg.max_outer, 1)))()
+    n_outer = C.c_int(0)
+    dict_iter = np.zeros((cfg.max_outer + 1, K, mh, mw)) if dump_dicts else None
+    maps = np.zeros((N, K, H, W))
+    dfin = np.zeros((K, mh, mw))
+    c = cfg.c()
+    _check(lib().ref_run(C.byref(c), N, H, W, _p(xs), K, mh, mw, rows, C.byref(n_outer),
+                         _p(dict_iter) if dump_dicts else None, _p(maps), _p(dfin)))
+    trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(2 * n_outer.value)]
+    return {"trace": trace, "n_outer": n_outer.value,
+            "dicts": dict_iter[: n_outer.value + 1] if dump_dicts else None,
+            "maps": maps, "dict": dfin}
+
+
+def run_csc(xs, K, support, cfg: Cfg):
+    """The reference's own run_csc (proj/src/pipeline.cpp:158-301)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    N, H, W = xs.shape
+    mh, mw = support
+    rows = (RefTraceRow * (2 * max(cfg.max_outer, 1)))()
+    n_rows = C.c_int(0)
+    dfin = np.zeros((K, mh, mw))
+    maps = np.zeros((N, K, H, W))
+    c = cfg.c()
+    _check(lib().ref_run_csc(C.byref(c), N, H, W, _p(xs), K, mh, mw, rows, C.byref(n_rows),
+                             _p(dfin), _p(maps)))
+    trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(n_rows.value)]
+    return {"trace": trace, "dict": dfin, "maps": maps}

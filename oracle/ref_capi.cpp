@@ -1,0 +1,440 @@
+// C-ABI over the UNMODIFIED reference hot-path translation units
+// (TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference leg; never by the product).
+//
+// oracle/Makefile compiles /root/reference/proj/src/{types,parallel,spectral,
+// objective,coding,learning,pipeline}.cpp in place (no sources are copied)
+// against oracle/fftw3.h + oracle/fftw_shim.c, links this file and
+// oracle/tcsc_stub.cpp, and writes oracle/_ref/libdcsc_ref.so.
+//
+// ref_run() is an instrumented replica of dcsc::run_csc
+// (proj/src/pipeline.cpp:158-301) assembled ONLY from the reference's public
+// functions (normalize, init_variables, solve_coding, evaluate_objective,
+// solve_learning, learning_data_term). It exists because run_csc returns only
+// the final state; the replica additionally dumps the per-outer-iteration
+// dictionary, the l0 count of the maps and mu_iters. tests/ assert that its
+// trace equals run_csc's (ref_run_csc) bit for bit at one thread.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "dcsc/coding.hpp"
+#include "dcsc/learning.hpp"
+#include "dcsc/objective.hpp"
+#include "dcsc/parallel.hpp"
+#include "dcsc/pipeline.hpp"
+#include "dcsc/spectral.hpp"
+#include "dcsc/types.hpp"
+
+using namespace dcsc;
+
+extern "C" {
+
+struct ref_cfg {
+  double beta, rho, tol;
+  int max_outer, max_admm, max_mu_iters;
+  double cg_tol;
+  int cg_max;
+  double mu_floor;
+  std::uint64_t seed;
+  int normalize;  // 0 None, 1 Global, 2 Local
+};
+
+struct ref_coding_stats {
+  int admm_iters, converged, degenerate_dictionary, dual_rescaled;
+  double primal_residual, theta_change, z_change, dual_objective, dual_infeasibility;
+};
+
+struct ref_learning_stats {
+  int mu_iters;
+  long cg_iters, cg_iters_first;
+  int converged, degenerate, mu_clamped, cg_budget_hit, rescaled_filters, n_dead;
+};
+
+struct ref_trace_row {
+  int outer_iter, phase;
+  double total, data_term, l1_term, residual_norm;
+  long admm_iters, cg_iters;
+  int mu_iters;
+  double elapsed_ms;  // reference timer: solver call only
+  double wall_ms;     // whole half-step including objective bookkeeping
+  long l0;            // |z| > 1e-12 * max|z| over the accepted maps (coding rows)
+};
+
+}  // extern "C"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const DimensionError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const NumericError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
+
+SolverConfig to_cfg(const ref_cfg* c) {
+  SolverConfig s;
+  s.beta = c->beta;
+  s.rho = c->rho;
+  s.tol = c->tol;
+  s.max_outer = c->max_outer;
+  s.max_admm = c->max_admm;
+  s.max_mu_iters = c->max_mu_iters;
+  s.cg_tol = c->cg_tol;
+  s.cg_max = c->cg_max;
+  s.mu_floor = c->mu_floor;
+  s.seed = c->seed;
+  s.normalize = c->normalize == 0 ? NormalizeMode::None
+                : c->normalize == 1 ? NormalizeMode::Global
+                                    : NormalizeMode::Local;
+  return s;
+}
+
+double now_ms() {
+  using clock = std::chrono::steady_clock;
+  return std::chrono::duration<double, std::milli>(clock::now().time_since_epoch()).count();
+}
+
+Dictionary make_dict(int K, int mh, int mw, const double* d) {
+  Dictionary dict(K, {mh, mw}, 1);
+  std::copy(d, d + dict.values.size(), dict.values.begin());
+  return dict;
+}
+
+SignalTensor make_signal(int H, int W, const double* x) {
+  SignalTensor s({H, W}, 1);
+  std::copy(x, x + s.values.size(), s.values.begin());
+  return s;
+}
+
+long count_l0(const std::vector<SparseMaps>& maps) {
+  double mx = 0.0;
+  for (const auto& m : maps)
+    for (double v : m.values) mx = std::max(mx, std::abs(v));
+  const double thr = 1e-12 * mx;
+  long c = 0;
+  for (const auto& m : maps)
+    for (double v : m.values)
+      if (std::abs(v) > thr) ++c;
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_last_error(char* buf, std::size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return static_cast<int>(g_err.size());
+}
+
+int ref_set_threads(int n) {
+  par::set_max_threads(n);
+  return par::max_threads();
+}
+
+// rank-D forward DFT of a real grid: out is D interleaved complex values.
+int ref_forward_dft(int rank, const int* dims, const double* in, double* out) {
+  return guarded([&] {
+    GridDims g(dims, dims + rank);
+    const std::size_t n = grid_count(g);
+    Spectrum s = forward_dft(g, std::span<const double>(in, n));
+    std::memcpy(out, s.values.data(), n * sizeof(std::complex<double>));
+  });
+}
+
+// rank-D inverse DFT (1/D, real part kept, residue guard) of a full spectrum.
+int ref_inverse_dft(int rank, const int* dims, const double* in, double* out) {
+  return guarded([&] {
+    GridDims g(dims, dims + rank);
+    Spectrum s(g);
+    std::memcpy(s.values.data(), in, s.values.size() * sizeof(std::complex<double>));
+    inverse_dft(s, std::span<double>(out, s.values.size()));
+  });
+}
+
+int ref_init_dictionary(int K, int mh, int mw, int H, int W, std::uint64_t seed, double* out) {
+  return guarded([&] {
+    RunConfig rc;
+    rc.solver.seed = seed;
+    rc.filters = K;
+    rc.support = {mh, mw};
+    InitVariables v = init_variables(rc, {H, W}, 1, 1);
+    std::copy(v.dict.values.begin(), v.dict.values.end(), out);
+  });
+}
+
+// One solve_coding call. theta/z/lambda are in/out warm state (K*D, K*D, D);
+// warm = 0 starts from the reference's empty state.
+int ref_solve_coding(int H, int W, const double* x, int K, int mh, int mw, const double* d,
+                     const ref_cfg* cfg, int warm, double* theta, double* z, double* lambda,
+                     ref_coding_stats* st) {
+  return guarded([&] {
+    const SignalTensor xs = make_signal(H, W, x);
+    const Dictionary dict = make_dict(K, mh, mw, d);
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    CodingDualState state;
+    if (warm) {
+      state.theta.assign(theta, theta + K * D);
+      state.z.assign(z, z + K * D);
+      state.lambda.assign(lambda, lambda + D);
+    }
+    CodingStats s;
+    solve_coding(xs, dict, to_cfg(cfg), state, &s);
+    std::copy(state.theta.begin(), state.theta.end(), theta);
+    std::copy(state.z.begin(), state.z.end(), z);
+    std::copy(state.lambda.begin(), state.lambda.end(), lambda);
+    if (st) {
+      st->admm_iters = s.admm_iters;
+      st->converged = s.converged;
+      st->degenerate_dictionary = s.degenerate_dictionary;
+      st->dual_rescaled = s.dual_rescaled;
+      st->primal_residual = s.primal_residual;
+      st->theta_change = s.theta_change;
+      st->z_change = s.z_change;
+      st->dual_objective = s.dual_objective;
+      st->dual_infeasibility = s.dual_infeasibility;
+    }
+  });
+}
+
+// One solve_learning call over N images. gamma (N*D) / mu (K) are in/out warm
+// state; warm = 0 starts from the empty state. d_out receives K*M values.
+int ref_solve_learning(int N, int H, int W, const double* xs, int K, const double* maps, int mh,
+                       int mw, const ref_cfg* cfg, int warm, double* gamma, double* mu,
+                       double* d_out, ref_learning_stats* st) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    std::vector<SignalTensor> sig;
+    std::vector<SparseMaps> zs;
+    for (int n = 0; n < N; ++n) {
+      sig.push_back(make_signal(H, W, xs + n * D));
+      SparseMaps m(K, {H, W});
+      std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
+      zs.push_back(std::move(m));
+    }
+    LearningDualState state;
+    if (warm) {
+      state.gamma.assign(1, std::vector<double>(gamma, gamma + N * D));
+      state.mu.assign(mu, mu + K);
+    }
+    LearningStats s;
+    Dictionary dict = solve_learning(sig, zs, {mh, mw}, to_cfg(cfg), state, &s);
+    std::copy(dict.values.begin(), dict.values.end(), d_out);
+    if (!state.gamma.empty()) std::copy(state.gamma[0].begin(), state.gamma[0].end(), gamma);
+    std::copy(state.mu.begin(), state.mu.end(), mu);
+    if (st) {
+      st->mu_iters = s.mu_iters;
+      st->cg_iters = s.cg_iters;
+      st->cg_iters_first = s.cg_iters_first;
+      st->converged = s.converged;
+      st->degenerate = s.degenerate;
+      st->mu_clamped = s.mu_clamped;
+      st->cg_budget_hit = s.cg_budget_hit;
+      st->rescaled_filters = s.rescaled_filters;
+      st->n_dead = static_cast<int>(s.dead_filters.size());
+    }
+  });
+}
+
+// evaluate_objective for one image: out = {data_term, l1_term, total, residual_norm}
+int ref_objective(int H, int W, const double* x, int K, int mh, int mw, const double* d,
+                  const double* z, double beta, double* out) {
+  return guarded([&] {
+    SparseMaps m(K, {H, W});
+    std::copy(z, z + m.values.size(), m.values.begin());
+    const ObjectiveBreakdown b =
+        evaluate_objective(make_signal(H, W, x), make_dict(K, mh, mw, d), m, beta);
+    out[0] = b.data_term;
+    out[1] = b.l1_term;
+    out[2] = b.total;
+    out[3] = b.residual_norm;
+  });
+}
+
+// LearningOperator::apply (proj/src/learning.cpp:83-122) on stacked N*D vectors.
+int ref_learning_apply(int N, int H, int W, int K, const double* maps, int mh, int mw,
+                       const double* mu, double mu_floor, const double* v, double* out) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    std::vector<SparseMaps> zs;
+    for (int n = 0; n < N; ++n) {
+      SparseMaps m(K, {H, W});
+      std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
+      zs.push_back(std::move(m));
+    }
+    LearningOperator op(zs, {mh, mw}, mu_floor);
+    op.set_mu(std::span<const double>(mu, K));
+    op.apply(std::span<const double>(v, N * D), std::span<double>(out, N * D));
+  });
+}
+
+// Instrumented replica of run_csc (see header comment). xs are the RAW signals;
+// normalisation follows cfg->normalize exactly as run_csc does. rows must hold
+// 2*max_outer entries. dict_iter (optional) receives (max_outer+1)*K*M values:
+// the initial dictionary then the accepted dictionary after each outer
+// iteration. maps_out (optional) receives the final N*K*D maps, dict_out the
+// final K*M dictionary. Returns the number of outer iterations run in *n_outer.
+int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
+            int mw, ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out,
+            double* dict_out) {
+  return guarded([&] {
+    RunConfig cfg;
+    cfg.solver = to_cfg(cfgp);
+    cfg.filters = K;
+    cfg.support = {mh, mw};
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    const double beta = cfg.solver.beta;
+    const double tau = cfg.solver.tol;
+    std::vector<SignalTensor> xs(N);
+    for (int n = 0; n < N; ++n) xs[n] = normalize(make_signal(H, W, xs_raw + n * D), cfg.solver.normalize);
+
+    InitVariables vars = init_variables(cfg, {H, W}, 1, N);
+    Dictionary dict = vars.dict;
+    std::vector<SparseMaps> maps = vars.maps;
+    const std::size_t KM = dict.values.size();
+    if (dict_iter) std::copy(dict.values.begin(), dict.values.end(), dict_iter);
+    *n_outer = 0;
+
+    auto total_objective = [&]() {
+      ObjectiveBreakdown sum;
+      for (int n = 0; n < N; ++n) {
+        const ObjectiveBreakdown b = evaluate_objective(xs[n], dict, maps[n], beta);
+        sum.data_term += b.data_term;
+        sum.l1_term += b.l1_term;
+        sum.residual_norm += b.residual_norm * b.residual_norm;
+      }
+      sum.total = sum.data_term + sum.l1_term;
+      sum.residual_norm = std::sqrt(sum.residual_norm);
+      return sum;
+    };
+    double prev_total = total_objective().total;
+    std::vector<ObjectiveBreakdown> image_obj(N);
+    for (int n = 0; n < N; ++n) image_obj[n] = evaluate_objective(xs[n], dict, maps[n], beta);
+
+    int row = 0;
+    for (int outer = 1; outer <= cfg.solver.max_outer; ++outer) {
+      const double wall0 = now_ms();
+      std::vector<SparseMaps> cand(N);
+      std::vector<CodingStats> cs(N);
+      const double c0 = now_ms();
+      par::parallel_for(N, [&](std::int64_t n) {
+        cand[n] = solve_coding(xs[n], dict, cfg.solver, vars.coding[n], &cs[n]);
+      });
+      const double coding_ms = now_ms() - c0;
+      long admm_total = 0;
+      double z_change_sq = 0.0, z_norm_sq = 0.0;
+      for (int n = 0; n < N; ++n) {
+        admm_total += cs[n].admm_iters;
+        const ObjectiveBreakdown c = evaluate_objective(xs[n], dict, cand[n], beta);
+        if (!std::isfinite(c.total)) throw NumericError("non-finite objective (coding)");
+        if (c.total <= image_obj[n].total) {
+          for (std::size_t i = 0; i < cand[n].values.size(); ++i) {
+            const double delta = cand[n].values[i] - maps[n].values[i];
+            z_change_sq += delta * delta;
+          }
+          maps[n] = std::move(cand[n]);
+          image_obj[n] = c;
+        }
+        for (double v : maps[n].values) z_norm_sq += v * v;
+      }
+      ObjectiveBreakdown after_coding;
+      for (int n = 0; n < N; ++n) {
+        after_coding.data_term += image_obj[n].data_term;
+        after_coding.l1_term += image_obj[n].l1_term;
+        after_coding.residual_norm += image_obj[n].residual_norm * image_obj[n].residual_norm;
+      }
+      after_coding.total = after_coding.data_term + after_coding.l1_term;
+      after_coding.residual_norm = std::sqrt(after_coding.residual_norm);
+      const double wall1 = now_ms();
+      rows[row++] = {outer, 0, after_coding.total, after_coding.data_term, after_coding.l1_term,
+                     after_coding.residual_norm, admm_total, 0, 0, coding_ms, wall1 - wall0,
+                     count_l0(maps)};
+
+      LearningStats ls;
+      const double l0 = now_ms();
+      Dictionary dc = solve_learning(xs, maps, cfg.support, cfg.solver, vars.learning, &ls);
+      const double learning_ms = now_ms() - l0;
+      double d_change_sq = 0.0, d_norm_sq = 0.0;
+      ObjectiveBreakdown after_learning = after_coding;
+      const double cand_data = learning_data_term(xs, dc, maps);
+      if (!std::isfinite(cand_data + after_coding.l1_term))
+        throw NumericError("non-finite objective (learning)");
+      if (cand_data <= after_coding.data_term) {
+        for (std::size_t i = 0; i < dc.values.size(); ++i) {
+          const double delta = dc.values[i] - dict.values[i];
+          d_change_sq += delta * delta;
+        }
+        dict = std::move(dc);
+        after_learning.data_term = cand_data;
+        after_learning.total = cand_data + after_coding.l1_term;
+        after_learning.residual_norm = std::sqrt(2.0 * cand_data);
+        for (int n = 0; n < N; ++n) image_obj[n] = evaluate_objective(xs[n], dict, maps[n], beta);
+      }
+      for (double v : dict.values) d_norm_sq += v * v;
+      const double wall2 = now_ms();
+      rows[row++] = {outer, 1, after_learning.total, after_learning.data_term,
+                     after_learning.l1_term, after_learning.residual_norm, 0, ls.cg_iters,
+                     ls.mu_iters, learning_ms, wall2 - wall1, count_l0(maps)};
+      if (dict_iter) std::copy(dict.values.begin(), dict.values.end(), dict_iter + outer * KM);
+      *n_outer = outer;
+
+      const double obj_change =
+          std::abs(prev_total - after_learning.total) / std::max(std::abs(prev_total), 1e-30);
+      const double z_change = std::sqrt(z_change_sq) / std::max(std::sqrt(z_norm_sq), 1.0);
+      const double d_change = std::sqrt(d_change_sq) / std::max(std::sqrt(d_norm_sq), 1.0);
+      prev_total = after_learning.total;
+      if (obj_change <= tau && z_change <= tau && d_change <= tau) break;
+    }
+    if (maps_out)
+      for (int n = 0; n < N; ++n) std::copy(maps[n].values.begin(), maps[n].values.end(), maps_out + n * K * D);
+    if (dict_out) std::copy(dict.values.begin(), dict.values.end(), dict_out);
+  });
+}
+
+// The reference's own run_csc, for checking the replica (trace rows only).
+int ref_run_csc(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
+                int mw, ref_trace_row* rows, int* n_rows, double* dict_out, double* maps_out) {
+  return guarded([&] {
+    RunConfig cfg;
+    cfg.solver = to_cfg(cfgp);
+    cfg.filters = K;
+    cfg.support = {mh, mw};
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    Dataset data;
+    for (int n = 0; n < N; ++n) data.signals.push_back(make_signal(H, W, xs_raw + n * D));
+    RunResult r = run_csc(cfg, data);
+    *n_rows = static_cast<int>(r.trace.rows.size());
+    for (std::size_t i = 0; i < r.trace.rows.size(); ++i) {
+      const TraceRow& t = r.trace.rows[i];
+      rows[i] = {t.outer_iter, t.phase == Phase::Coding ? 0 : 1, t.objective.total,
+                 t.objective.data_term, t.objective.l1_term, t.objective.residual_norm,
+                 t.admm_iters, t.cg_iters, 0, t.elapsed_ms, 0.0, 0};
+    }
+    if (dict_out) std::copy(r.dict.values.begin(), r.dict.values.end(), dict_out);
+    if (maps_out)
+      for (int n = 0; n < N; ++n) std::copy(r.maps[n].values.begin(), r.maps[n].values.end(), maps_out + n * K * D);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+"""In-tree build of the sm_100a library paper_1709_09479_b200/lib/libdcsc_cuda.so.
+
+nvcc cross-compiles for sm_100a on a machine without a GPU; the built .so is
+git-ignored but travels with the gpurun snapshot. Object files are cached in
+build/ and rebuilt only when a source or header is newer.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INC = os.path.join(ROOT, "include")
+LIBDIR = os.path.join(PKG, "lib")
+OBJDIR = os.path.join(ROOT, "build", "obj")
+LIB = os.path.join(LIBDIR, "libdcsc_cuda.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + [
+    "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + INC, "-I" + CSRC,
+]
+HOST_CXX = shutil.which("g++", path="/usr/bin") or "g++"
+
+
+def _nvcc() -> str:
+    for p in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if p and os.path.exists(p):
+            return p
+    raise RuntimeError("nvcc not found")
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp"))]
+    hs += [os.path.join(INC, f) for f in os.listdir(INC)]
+    return hs
+
+
+def _stale(out: str, deps) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(OBJDIR, exist_ok=True)
+    nvcc = _nvcc()
+    hdrs = _headers()
+    objs = []
+    for src in sorted(os.listdir(CSRC)):
+        path = os.path.join(CSRC, src)
+        if src.endswith(".cu"):
+            obj = os.path.join(OBJDIR, src + ".o")
+            if _stale(obj, [path] + hdrs):
+                cmd = [nvcc, "-c", path, "-o", obj] + NVCC_FLAGS + ["-ccbin", HOST_CXX]
+                log = os.path.join(OBJDIR, src + ".ptxas.log")
+                with open(log, "w") as f:
+                    r = subprocess.run(cmd, stdout=f, stderr=subprocess.STDOUT)
+                if r.returncode != 0:
+                    sys.stderr.write(open(log).read()[-20000:])
+                    raise RuntimeError(f"nvcc failed on {src}")
+            objs.append(obj)
+        elif src.endswith(".cpp"):
+            obj = os.path.join(OBJDIR, src + ".o")
+            if _stale(obj, [path] + hdrs):
+                cmd = [HOST_CXX, "-c", path, "-o", obj, "-O3", "-fPIC", "-fopenmp", "-std=c++17", "-I" + INC, "-I" + CSRC]
+                subprocess.run(cmd, check=True)
+            objs.append(obj)
+    if _stale(LIB, objs):
+        cmd = [nvcc, "-shared", "-o", LIB] + objs + ARCH + ["-ccbin", HOST_CXX, "-Xcompiler", "-fopenmp", "-lgomp"]
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose=True))

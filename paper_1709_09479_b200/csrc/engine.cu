@@ -1,0 +1,1332 @@
+// Host orchestration of the B200 dual-domain CSC path and the C-ABI
+// (include/dcsc_cuda.h). One Engine<R, H, W> per compiled grid/precision keeps
+// every hot-path buffer device-resident; the host only makes the discrete
+// decisions the reference makes on scalars (stop tests, acceptance, the mu
+// settle test) from FP64 reductions read back per iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dcsc_cuda.h"
+#include "kernels.cuh"
+
+using namespace dcsc_cuda;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DimErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NumErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct InvErr : std::runtime_error { using std::runtime_error::runtime_error; };
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return DCSC_OK;
+  } catch (const DimErr& e) {
+    g_err = e.what();
+    return DCSC_ERR_DIMENSION;
+  } catch (const NumErr& e) {
+    g_err = e.what();
+    return DCSC_ERR_NUMERIC;
+  } catch (const CudaErr& e) {
+    g_err = e.what();
+    return DCSC_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DCSC_ERR_INVALID;
+  }
+}
+
+double now_ms() {
+  using clock = std::chrono::steady_clock;
+  return std::chrono::duration<double, std::milli>(clock::now().time_since_epoch()).count();
+}
+
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b) {
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    bytes = b;
+    if (b) CK(cudaMalloc(&p, b));
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+void validate_cfg(const dcsc_solver_config& c) {  // types.cpp:106-114
+  if (!(c.beta > 0)) throw InvErr("beta must be > 0");
+  if (!(c.rho > 0)) throw InvErr("rho must be > 0");
+  if (!(c.tol > 0)) throw InvErr("tol must be > 0");
+  if (!(c.mu_floor > 0)) throw InvErr("mu_floor must be > 0");
+  if (c.max_outer < 0 || c.max_admm < 1 || c.max_mu_iters < 1 || c.cg_max < 1)
+    throw InvErr("iteration caps must be positive");
+  if (!(c.cg_tol > 0)) throw InvErr("cg_tol must be > 0");
+}
+
+void require_finite(const double* v, size_t n, const char* what) {  // types.cpp:26-29
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) throw NumErr(std::string(what) + " contains a non-finite value");
+}
+
+constexpr double kFilterNormTol = 1e-3;  // learning.cpp:14
+
+// Kernel families for the per-launch CUDA-event profiler.
+enum Family { kFamCoding = 0, kFamLambda = 1, kFamContract = 2, kFamMask = 3, kFamOther = 4, kFamCount = 5 };
+
+// Circular Gaussian blur (sigma in samples, truncated at 4 sigma) along both
+// axes, as pipeline.cpp:26-57 does for local contrast normalisation.
+std::vector<double> gaussian_blur(int H, int W, const double* v, double sigma) {
+  const int radius = static_cast<int>(std::ceil(4.0 * sigma));
+  std::vector<double> ker(2 * radius + 1);
+  double ks = 0.0;
+  for (int i = -radius; i <= radius; ++i) {
+    ker[i + radius] = std::exp(-0.5 * (i * i) / (sigma * sigma));
+    ks += ker[i + radius];
+  }
+  for (double& k : ker) k /= ks;
+  std::vector<double> cur(v, v + (size_t)H * W), next(cur.size());
+  const int dims[2] = {H, W};
+  for (int axis = 0; axis < 2; ++axis) {
+    const int n = dims[axis];
+    for (int r = 0; r < H; ++r)
+      for (int c = 0; c < W; ++c) {
+        double acc = 0.0;
+        const int c0 = axis == 0 ? r : c;
+        for (int i = -radius; i <= radius; ++i) {
+          int cc = (c0 + i) % n;
+          if (cc < 0) cc += n;
+          acc += ker[i + radius] * (axis == 0 ? cur[(size_t)cc * W + c] : cur[(size_t)r * W + cc]);
+        }
+        next[(size_t)r * W + c] = acc;
+      }
+    cur.swap(next);
+  }
+  return cur;
+}
+
+// dcsc::normalize (pipeline.cpp:78-121) for one single-channel image.
+void normalize_image(int mode, int H, int W, const double* in, double* out) {
+  const size_t D = (size_t)H * W;
+  if (mode == 0) {
+    std::copy(in, in + D, out);
+    return;
+  }
+  if (mode == 1) {
+    double m = 0.0;
+    for (size_t i = 0; i < D; ++i) m += in[i];
+    m /= (double)D;
+    double var = 0.0;
+    for (size_t i = 0; i < D; ++i) var += (in[i] - m) * (in[i] - m);
+    const double sd = std::sqrt(var / (double)D);
+    if (sd < 1e-8) {
+      std::fill(out, out + D, 0.0);
+      return;
+    }
+    for (size_t i = 0; i < D; ++i) out[i] = (in[i] - m) / sd;
+    return;
+  }
+  const std::vector<double> lm = gaussian_blur(H, W, in, 3.0);
+  std::vector<double> sq(D);
+  for (size_t i = 0; i < D; ++i) sq[i] = in[i] * in[i];
+  const std::vector<double> ls = gaussian_blur(H, W, sq.data(), 3.0);
+  std::vector<double> lsd(D);
+  double fl = 0.0;
+  for (size_t i = 0; i < D; ++i) {
+    lsd[i] = std::sqrt(std::max(ls[i] - lm[i] * lm[i], 0.0));
+    fl += lsd[i];
+  }
+  fl /= (double)D;
+  if (fl < 1e-8) {
+    for (size_t i = 0; i < D; ++i) out[i] = in[i] - lm[i];
+    return;
+  }
+  for (size_t i = 0; i < D; ++i) out[i] = (in[i] - lm[i]) / std::max(lsd[i], fl);
+}
+
+// ---------------------------------------------------------------- interface
+class EngineBase {
+ public:
+  virtual ~EngineBase() = default;
+  virtual void set_signals(const double* x) = 0;
+  virtual void get_signals(double* x) = 0;
+  virtual void set_dictionary(const double* d) = 0;
+  virtual void get_dictionary(double* d) = 0;
+  virtual void init_variables() = 0;
+  virtual void set_coding_state(int n0, int n1, const double* theta, const double* z) = 0;
+  virtual void get_coding_state(int n0, int n1, double* theta, double* z, double* lambda) = 0;
+  virtual void coding(int n0, int n1, dcsc_coding_stats* stats) = 0;
+  virtual void set_maps(int n0, int n1, const double* z) = 0;
+  virtual void get_maps(int n0, int n1, double* z) = 0;
+  virtual void set_learning_state(const double* gamma, const double* mu) = 0;
+  virtual void get_learning_state(double* gamma, double* mu) = 0;
+  virtual void learning(double* d_out, dcsc_learning_stats* st) = 0;
+  virtual void learning_apply(const double* mu, const double* v, double* out) = 0;
+  virtual void objective(const double* d, dcsc_objective* per_image) = 0;
+  virtual void learning_data_term(const double* d, double* data) = 0;
+  virtual void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) = 0;
+  virtual void synchronize() = 0;
+  virtual void set_profiling(int on) = 0;
+  virtual void kernel_time(int fam, double* ms, long long* n) = 0;
+  virtual void event_mark(int slot) = 0;
+  virtual double event_elapsed(int a, int b) = 0;
+  long long launches = 0;
+  size_t device_bytes = 0;
+};
+
+constexpr int pick_threads(int H, int W) { return H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128); }
+
+template <class R, int H, int W>
+class Engine final : public EngineBase {
+ public:
+  static constexpr int T = pick_threads(H, W);
+  using P = Plane<R, H, W, T>;
+  using C = cx<R>;
+  static constexpr int NB = P::NB, D = P::D, Wh = P::Wh;
+  static constexpr int TBV = 256;  // block size of the streaming kernels
+
+  explicit Engine(const dcsc_cuda_opts& o) : o_(o), cfg_(o.cfg) {
+    N_ = o.n_images;
+    K_ = o.filters;
+    mh_ = o.support_h;
+    mw_ = o.support_w;
+    M_ = mh_ * mw_;
+    CK(cudaSetDevice(o.device));
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&pin_, 1 << 20));
+    // filter groups: at least ~4 CTAs per SM-wave of work when N is small
+    kpg_ = K_;
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      const int target = 4 * sms;
+      int G = std::max(1, std::min(K_, (target + N_ - 1) / N_));
+      kpg_ = (K_ + G - 1) / G;
+    }
+    G_ = (K_ + kpg_ - 1) / kpg_;
+    setup_attributes();
+    // twiddles (forward roots) in long double, rounded once
+    std::vector<C> tw(P::TW_LEN);
+    auto fill = [&](int off, int L) {
+      for (int j = 0; j < L; ++j) {
+        const long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
+        tw[off + j] = mk<C>(R(std::cos(a)), R(std::sin(a)));
+      }
+    };
+    fill(0, W);
+    if (!P::SAME_TW) fill(W, H);
+    dtw_.alloc(sizeof(C) * P::TW_LEN);
+    CK(cudaMemcpy(dtw_.p, tw.data(), sizeof(C) * P::TW_LEN, cudaMemcpyHostToDevice));
+
+    const size_t nD = (size_t)N_ * D, nNB = (size_t)N_ * NB;
+    x_.alloc(sizeof(R) * nD);
+    xhat_.alloc(sizeof(C) * nNB);
+    dhat_.alloc(sizeof(C) * (size_t)K_ * NB);
+    dcand_.alloc(sizeof(C) * (size_t)K_ * NB);
+    sigma_.alloc(sizeof(R) * NB);
+    u_.alloc(sizeof(R) * nD * K_);
+    maps_.alloc(sizeof(R) * nD * K_);
+    lamhat_.alloc(sizeof(C) * nNB);
+    lam_.alloc(sizeof(R) * nD);
+    part_.alloc(sizeof(C) * (size_t)N_ * G_ * NB);
+    sums_.alloc(sizeof(double) * (size_t)N_ * G_ * kSums);
+    conv_.alloc(sizeof(int) * N_);
+    img_.alloc(sizeof(ImageAdmm) * N_);
+    dual_.alloc(sizeof(double) * N_);
+    infeas_.alloc(sizeof(double) * N_);
+    resc_.alloc(sizeof(int) * N_);
+    odata_.alloc(sizeof(double) * N_);
+    ol1_.alloc(sizeof(double) * N_);
+    accept_.alloc(sizeof(int) * N_);
+    gam_.alloc(sizeof(C) * nNB);
+    r_.alloc(sizeof(C) * nNB);
+    p_.alloc(sizeof(C) * nNB);
+    ap_.alloc(sizeof(C) * nNB);
+    cvec_.alloc(sizeof(C) * (size_t)K_ * NB);
+    phat_.alloc(sizeof(C) * (size_t)K_ * NB);
+    live_.alloc(sizeof(int) * K_);
+    dmu_.alloc(sizeof(double) * K_);
+    dwk_.alloc(sizeof(double) * K_);
+    dd_.alloc(sizeof(double) * (size_t)K_ * M_);
+    ddict_.alloc(sizeof(double) * (size_t)K_ * M_);
+    cg_.alloc(sizeof(CgState));
+    tiles_ = (NB + TBV - 1) / TBV;
+    const size_t vec_blocks = (nNB + TBV - 1) / TBV;
+    accept_chunks_ = std::max(1, std::min(64, (int)((size_t)K_ * D / (TBV * 8))));
+    const size_t np = std::max({(size_t)N_ * tiles_, vec_blocks, (size_t)N_ * accept_chunks_});
+    partial_.alloc(sizeof(double) * np);
+    partial2_.alloc(sizeof(double) * (size_t)N_ * accept_chunks_);
+    l0_.alloc(sizeof(unsigned long long) * (size_t)N_ * accept_chunks_);
+    device_bytes = x_.bytes + xhat_.bytes + dhat_.bytes + dcand_.bytes + sigma_.bytes + u_.bytes +
+                   maps_.bytes + lamhat_.bytes + lam_.bytes + part_.bytes + sums_.bytes +
+                   4 * gam_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes;
+    CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
+    CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
+    CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
+    CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    CK(cudaMemsetAsync(x_.p, 0, x_.bytes, st_));
+    CK(cudaMemsetAsync(xhat_.p, 0, xhat_.bytes, st_));
+    dict_.assign((size_t)K_ * M_, 0.0);
+    mu_.assign(K_, 1.0);
+    xnorm2_.assign(N_, 0.0);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  ~Engine() override {
+    for (auto& e : prof_) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    for (auto& e : marks_)
+      if (e) cudaEventDestroy(e);
+    if (pin_) cudaFreeHost(pin_);
+    if (st_) cudaStreamDestroy(st_);
+  }
+
+  // ------------------------------------------------------------ launches
+  template <class F>
+  void launch(int fam, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profiling_) {
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      CK(cudaEventRecord(a, st_));
+    }
+    f();
+    CK(cudaGetLastError());
+    if (profiling_) {
+      CK(cudaEventRecord(b, st_));
+      prof_.push_back({fam, a, b});
+    }
+    ++launches;
+  }
+
+  void setup_attributes() {
+    auto big = [](const void* fn, size_t bytes) {
+      if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    };
+    big((const void*)coding_pass<P, kPassAdmm>, Smem<P>::coding);
+    big((const void*)coding_pass<P, kPassPrologue>, Smem<P>::coding);
+    big((const void*)coding_pass<P, kPassObjective>, Smem<P>::coding);
+    big((const void*)coding_pass<P, kPassMaps>, Smem<P>::coding);
+    big((const void*)r2c_planes<P, R>, Smem<P>::two);
+    big((const void*)r2c_planes<P, double>, Smem<P>::two);
+    big((const void*)c2r_planes<P, R>, Smem<P>::two);
+    big((const void*)c2r_planes<P, double>, Smem<P>::two);
+    big((const void*)r2c_filters<P>, Smem<P>::two);
+    big((const void*)mask_step<P>, Smem<P>::two);
+  }
+
+  CodingArgs<R> cargs(const C* dhat, int n_off) {
+    CodingArgs<R> a;
+    a.dhat = dhat;
+    a.lamhat = lamhat_.as<C>();
+    a.u = u_.as<R>() + (size_t)n_off * K_ * D;
+    a.maps = maps_.as<R>() + (size_t)n_off * K_ * D;
+    a.part = part_.as<C>() + (size_t)n_off * G_ * NB;
+    a.sums = sums_.as<double>() + (size_t)n_off * G_ * kSums;
+    a.conv = conv_.as<int>() + n_off;
+    a.lamhat = lamhat_.as<C>() + (size_t)n_off * NB;
+    a.K = K_;
+    a.G = G_;
+    a.kpg = kpg_;
+    a.rho = R(cfg_.rho);
+    a.beta = R(cfg_.beta);
+    a.tw = dtw_.as<C>();
+    return a;
+  }
+
+  template <int MODE>
+  void coding_launch(const C* dhat, int n0, int cnt) {
+    CodingArgs<R> a = cargs(dhat, n0);
+    launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] {
+      coding_pass<P, MODE><<<dim3(G_, cnt), T, Smem<P>::coding, st_>>>(a);
+    });
+  }
+
+  void r2c(const void* src, bool src_double, size_t src_stride, C* dst, size_t dst_stride, int count,
+           int* live = nullptr, int live_mod = 1) {
+    if (count <= 0) return;
+    launch(kFamOther, [&] {
+      if (src_double)
+        r2c_planes<P, double><<<count, T, Smem<P>::two, st_>>>(static_cast<const double*>(src), src_stride,
+                                                                dst, dst_stride, dtw_.as<C>(), live, live_mod);
+      else
+        r2c_planes<P, R><<<count, T, Smem<P>::two, st_>>>(static_cast<const R*>(src), src_stride, dst,
+                                                           dst_stride, dtw_.as<C>(), live, live_mod);
+    });
+  }
+
+  template <class DST>
+  void c2r(const C* src, size_t src_stride, DST* dst, size_t dst_stride, int count) {
+    if (count <= 0) return;
+    launch(kFamOther, [&] {
+      c2r_planes<P, DST><<<count, T, Smem<P>::two, st_>>>(src, src_stride, dst, dst_stride, dtw_.as<C>(), nullptr);
+    });
+  }
+
+  void upload_dict_spectra(const double* d, C* dst) {
+    CK(cudaMemcpyAsync(ddict_.p, d, sizeof(double) * K_ * M_, cudaMemcpyHostToDevice, st_));
+    launch(kFamOther, [&] {
+      r2c_filters<P><<<K_, T, Smem<P>::two, st_>>>(ddict_.as<double>(), mh_, mw_, dst, dtw_.as<C>());
+    });
+  }
+
+  // ------------------------------------------------------------ API
+  void set_signals(const double* x) override {
+    const size_t nD = (size_t)N_ * D;
+    require_finite(x, nD, "signal");
+    std::vector<double> xn(nD);
+    for (int n = 0; n < N_; ++n) normalize_image(cfg_.normalize, H, W, x + (size_t)n * D, xn.data() + (size_t)n * D);
+    // the device stores R; norms use the stored (rounded) values, as the oracle sees them
+    std::vector<R> xr(nD);
+    for (size_t i = 0; i < nD; ++i) xr[i] = R(xn[i]);
+    xs_host_.assign(nD, 0.0);
+    for (size_t i = 0; i < nD; ++i) xs_host_[i] = double(xr[i]);
+    for (int n = 0; n < N_; ++n) {
+      double s = 0.0;
+      for (size_t i = 0; i < (size_t)D; ++i) s += xs_host_[(size_t)n * D + i] * xs_host_[(size_t)n * D + i];
+      xnorm2_[n] = s;
+    }
+    CK(cudaMemcpyAsync(x_.p, xr.data(), sizeof(R) * nD, cudaMemcpyHostToDevice, st_));
+    r2c(x_.p, false, D, xhat_.as<C>(), NB, N_);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_signals(double* x) override { std::copy(xs_host_.begin(), xs_host_.end(), x); }
+
+  void set_dictionary(const double* d) override {
+    require_finite(d, (size_t)K_ * M_, "dictionary");
+    dict_.assign(d, d + (size_t)K_ * M_);
+    dict_zero_ = std::all_of(dict_.begin(), dict_.end(), [](double v) { return v == 0.0; });
+    upload_dict_spectra(dict_.data(), dhat_.as<C>());
+    launch(kFamOther, [&] {
+      sigma_kernel<R><<<(NB + 255) / 256, 256, 0, st_>>>(dhat_.as<C>(), sigma_.as<R>(), K_, NB, cfg_.rho);
+    });
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_dictionary(double* d) override { std::copy(dict_.begin(), dict_.end(), d); }
+
+  // init_variables (pipeline.cpp:123-156)
+  void init_variables() override {
+    std::vector<double> d((size_t)K_ * M_);
+    std::mt19937_64 rng(cfg_.seed);
+    auto uniform = [&rng]() { return static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5; };
+    for (int k = 0; k < K_; ++k) {
+      double sq = 0.0;
+      for (int i = 0; i < M_; ++i) {
+        const double v = uniform();
+        d[(size_t)k * M_ + i] = v;
+        sq += v * v;
+      }
+      double nrm = std::sqrt(sq);
+      if (nrm == 0.0) {
+        d[(size_t)k * M_] = 1.0;
+        nrm = 1.0;
+      }
+      for (int i = 0; i < M_; ++i) d[(size_t)k * M_ + i] /= nrm;
+    }
+    set_dictionary(d.data());
+    CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
+    CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
+    CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
+    CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    mu_.assign(K_, 1.0);
+    zhat_valid_ = false;
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void check_range(int n0, int n1) const {
+    if (n0 < 0 || n1 > N_ || n0 >= n1) throw DimErr("image range out of bounds");
+  }
+
+  void set_coding_state(int n0, int n1, const double* theta, const double* z) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> u(cnt);
+    const double inv_rho = 1.0 / cfg_.rho;
+    for (size_t i = 0; i < cnt; ++i) u[i] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
+    CK(cudaMemcpyAsync(u_.as<R>() + (size_t)n0 * K_ * D, u.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_coding_state(int n0, int n1, double* theta, double* z, double* lambda) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> u(cnt);
+    CK(cudaMemcpyAsync(u.data(), u_.as<R>() + (size_t)n0 * K_ * D, sizeof(R) * cnt, cudaMemcpyDeviceToHost, st_));
+    std::vector<R> l((size_t)(n1 - n0) * D);
+    CK(cudaMemcpyAsync(l.data(), lam_.as<R>() + (size_t)n0 * D, sizeof(R) * l.size(), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    const R beta = R(cfg_.beta), rho = R(cfg_.rho);
+    for (size_t i = 0; i < cnt; ++i) {
+      const R th = std::min(std::max(u[i], -beta), beta);
+      if (theta) theta[i] = th;
+      if (z) z[i] = rho * (th - u[i]);
+    }
+    if (lambda)
+      for (size_t i = 0; i < l.size(); ++i) lambda[i] = l[i];
+  }
+
+  // solve_coding for images [n0, n1) (coding.cpp:166-329, 333-356)
+  void coding(int n0, int n1, dcsc_coding_stats* stats) override {
+    check_range(n0, n1);
+    const int cnt = n1 - n0;
+    std::vector<dcsc_coding_stats> out(cnt);
+    if (dict_zero_) {
+      // degenerate dictionary: z = theta = 0, lambda = -x (coding.cpp:181-191)
+      CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * (size_t)cnt * K_ * D, st_));
+      const size_t tot = (size_t)cnt * D;
+      launch(kFamOther, [&] {
+        neg_copy<R><<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(x_.as<R>() + (size_t)n0 * D,
+                                                                   lam_.as<R>() + (size_t)n0 * D, tot);
+      });
+      CK(cudaStreamSynchronize(st_));
+      for (int i = 0; i < cnt; ++i) {
+        double ls = 0.0, lx = 0.0;
+        for (size_t j = 0; j < (size_t)D; ++j) {
+          const double lv = -xs_host_[(size_t)(n0 + i) * D + j];
+          ls += lv * lv;
+          lx += lv * xs_host_[(size_t)(n0 + i) * D + j];
+        }
+        out[i] = dcsc_coding_stats{};
+        out[i].converged = 1;
+        out[i].degenerate_dictionary = 1;
+        out[i].dual_objective = -0.5 * ls - lx;
+      }
+      if (stats) std::copy(out.begin(), out.end(), stats);
+      return;
+    }
+    int* conv_h = static_cast<int*>(pin_);
+    CK(cudaMemsetAsync(conv_.as<int>() + n0, 0, sizeof(int) * cnt, st_));
+    CK(cudaMemsetAsync(img_.as<ImageAdmm>() + n0, 0, sizeof(ImageAdmm) * cnt, st_));
+    const dim3 lgrid((NB + 255) / 256, cnt);
+    // initial lambda_hat from the warm state (the first assemble_w, coding.cpp:216-229)
+    coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);
+    auto lam_update = [&](int iter, int last, int prologue) {
+      launch(kFamLambda, [&] {
+        lambda_update<R><<<lgrid, 256, 0, st_>>>(part_.as<C>() + (size_t)n0 * G_ * NB,
+                                                 sums_.as<double>() + (size_t)n0 * G_ * kSums,
+                                                 xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(),
+                                                 lamhat_.as<C>() + (size_t)n0 * NB, conv_.as<int>() + n0,
+                                                 img_.as<ImageAdmm>() + n0, G_, NB, R(cfg_.rho), iter, last,
+                                                 prologue);
+      });
+    };
+    lam_update(0, 0, 1);
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    int pending = -1;  // iteration whose conv flags are in flight
+    for (int it = 1; it <= cfg_.max_admm; ++it) {
+      coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt);
+      lam_update(it, it == cfg_.max_admm, 0);
+      if (pending >= 0) {
+        // one-iteration look-ahead: iteration `it` is queued before we wait on it-1
+        CK(cudaEventSynchronize(ev[pending & 1]));
+        bool all = true;
+        for (int i = 0; i < cnt; ++i) all = all && conv_h[(pending & 1) * 65536 + i];
+        if (all) break;
+      }
+      if (cnt <= 65536) {
+        CK(cudaMemcpyAsync(conv_h + (it & 1) * 65536, conv_.as<int>() + n0, sizeof(int) * cnt,
+                           cudaMemcpyDeviceToHost, st_));
+        CK(cudaEventRecord(ev[it & 1], st_));
+        pending = it;
+      }
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    // exit: lambda = iDFT(lambda_hat), rescale, dual objective (coding.cpp:287-309)
+    c2r<R>(lamhat_.as<C>() + (size_t)n0 * NB, NB, lam_.as<R>() + (size_t)n0 * D, D, cnt);
+    launch(kFamOther, [&] {
+      admm_exit<R><<<cnt, 256, 0, st_>>>(lam_.as<R>() + (size_t)n0 * D, x_.as<R>() + (size_t)n0 * D,
+                                         img_.as<ImageAdmm>() + n0, D, cfg_.beta, dual_.as<double>() + n0,
+                                         infeas_.as<double>() + n0, resc_.as<int>() + n0);
+    });
+    std::vector<ImageAdmm> im(cnt);
+    std::vector<double> du(cnt), inf(cnt);
+    std::vector<int> rs(cnt);
+    CK(cudaMemcpyAsync(im.data(), img_.as<ImageAdmm>() + n0, sizeof(ImageAdmm) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(du.data(), dual_.as<double>() + n0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(inf.data(), infeas_.as<double>() + n0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(rs.data(), resc_.as<int>() + n0, sizeof(int) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (int i = 0; i < cnt; ++i) {
+      dcsc_coding_stats& s = out[i];
+      s.admm_iters = im[i].iters;
+      s.converged = im[i].converged;
+      s.degenerate_dictionary = 0;
+      s.dual_rescaled = rs[i];
+      s.primal_residual = im[i].primal;
+      s.theta_change = im[i].thc;
+      s.z_change = im[i].zc;
+      s.dual_objective = du[i];
+      s.dual_infeasibility = inf[i];
+    }
+    if (stats) std::copy(out.begin(), out.end(), stats);
+  }
+
+  void set_maps(int n0, int n1, const double* z) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> v(cnt);
+    for (size_t i = 0; i < cnt; ++i) v[i] = R(z[i]);
+    CK(cudaMemcpyAsync(maps_.as<R>() + (size_t)n0 * K_ * D, v.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    zhat_valid_ = false;
+  }
+
+  void get_maps(int n0, int n1, double* z) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> v(cnt);
+    CK(cudaMemcpyAsync(v.data(), maps_.as<R>() + (size_t)n0 * K_ * D, sizeof(R) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (size_t i = 0; i < cnt; ++i) z[i] = v[i];
+  }
+
+  void set_learning_state(const double* gamma, const double* mu) override {
+    if (gamma) {
+      DevMem tmp;
+      tmp.alloc(sizeof(double) * (size_t)N_ * D);
+      CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
+      r2c(tmp.p, true, D, gam_.as<C>(), NB, N_);
+      CK(cudaStreamSynchronize(st_));
+    } else {
+      CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    }
+    if (mu) mu_.assign(mu, mu + K_);
+    else mu_.assign(K_, 1.0);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_learning_state(double* gamma, double* mu) override {
+    if (gamma) {
+      DevMem tmp;
+      tmp.alloc(sizeof(double) * (size_t)N_ * D);
+      c2r<double>(gam_.as<C>(), NB, tmp.as<double>(), D, N_);
+      CK(cudaMemcpyAsync(gamma, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+    if (mu) std::copy(mu_.begin(), mu_.end(), mu);
+  }
+
+  // z_hat of the accepted maps and the dead-filter flags (learning.cpp:41-64)
+  void build_zhat() {
+    if (zhat_valid_) return;
+    if (!zhat_.p) {
+      zhat_.alloc(sizeof(C) * (size_t)N_ * K_ * NB);
+      device_bytes += zhat_.bytes;
+    }
+    CK(cudaMemsetAsync(live_.p, 0, sizeof(int) * K_, st_));
+    r2c(maps_.p, false, D, zhat_.as<C>(), NB, N_ * K_, live_.as<int>(), K_);
+    live_h_.assign(K_, 0);
+    CK(cudaMemcpyAsync(live_h_.data(), live_.p, sizeof(int) * K_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    zhat_valid_ = true;
+  }
+
+  // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
+  void apply_hat(const C* v, C* out) {
+    const dim3 g1((NB + TBV - 1) / TBV, K_);
+    launch(kFamContract, [&] {
+      contract_c<R><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), v, cvec_.as<C>(), live_.as<int>(), N_, K_, NB);
+    });
+    launch(kFamMask, [&] {
+      mask_step<P><<<K_, T, Smem<P>::two, st_>>>(cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(),
+                                                 dmu_.as<double>(), mh_, mw_, 0, dtw_.as<C>());
+    });
+    const dim3 g3(tiles_, N_);
+    launch(kFamContract, [&] {
+      contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(), live_.as<int>(),
+                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0);
+    });
+  }
+
+  void upload_mu() {
+    std::vector<double> wk(K_);
+    for (int k = 0; k < K_; ++k) wk[k] = 0.5 / mu_[k];
+    CK(cudaMemcpyAsync(dmu_.p, mu_.data(), sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(dwk_.p, wk.data(), sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
+  }
+
+  CgState read_cg() {
+    CgState* h = reinterpret_cast<CgState*>(static_cast<char*>(pin_) + 600000);
+    CK(cudaMemcpyAsync(h, cg_.p, sizeof(CgState), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    return *h;
+  }
+
+  // gamma_solve (learning.cpp:136-185), warm-started, on half spectra
+  void gamma_solve(double bnorm, int& iters, bool& converged) {
+    iters = 0;
+    converged = false;
+    const size_t total = (size_t)N_ * NB;
+    const unsigned vb = (unsigned)((total + TBV - 1) / TBV);
+    if (bnorm == 0.0) {
+      CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+      converged = true;
+      return;
+    }
+    CgState init{};
+    init.bnorm = bnorm;
+    CK(cudaMemcpyAsync(cg_.p, &init, sizeof(CgState), cudaMemcpyHostToDevice, st_));
+    apply_hat(gam_.as<C>(), ap_.as<C>());
+    launch(kFamOther, [&] {
+      cg_init<R, TBV><<<vb, TBV, 0, st_>>>(xhat_.as<C>(), ap_.as<C>(), r_.as<C>(), p_.as<C>(),
+                                            partial_.as<double>(), total, NB, Wh);
+    });
+    const double invD = 1.0 / D;
+    launch(kFamOther, [&] { cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 0); });
+    CgState s = read_cg();
+    if (s.rel <= cfg_.cg_tol) {
+      converged = true;
+      return;
+    }
+    for (int it = 1; it <= cfg_.cg_max; ++it) {
+      apply_hat(p_.as<C>(), ap_.as<C>());
+      launch(kFamOther, [&] {
+        cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), N_ * tiles_, invD, cg_.as<CgState>(), 1);
+      });
+      launch(kFamOther, [&] {
+        cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_.as<C>(), r_.as<C>(), p_.as<C>(), ap_.as<C>(),
+                                                cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh);
+      });
+      launch(kFamOther, [&] {
+        cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 2);
+      });
+      launch(kFamOther, [&] {
+        cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(r_.as<C>(), p_.as<C>(), cg_.as<CgState>(), total);
+      });
+      s = read_cg();
+      if (s.bad) break;  // pAp <= 0 guard (learning.cpp:166): gamma unchanged this step
+      iters = it;
+      if (s.rel <= cfg_.cg_tol) {
+        converged = true;
+        break;
+      }
+    }
+  }
+
+  // d_recover (learning.cpp:187-216): d_k = -0.5/max(mu_k,1e-300) crop(iDFT(sum_n conj(z_nk) gamma_n))
+  void d_recover(std::vector<double>& d) {
+    const dim3 g1((NB + TBV - 1) / TBV, K_);
+    launch(kFamContract, [&] {
+      contract_c<R><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), gam_.as<C>(), cvec_.as<C>(), live_.as<int>(), N_, K_, NB);
+    });
+    // d_recover does not skip dead filters; their correlation is exactly zero anyway
+    launch(kFamMask, [&] {
+      mask_step<P><<<K_, T, Smem<P>::two, st_>>>(cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(),
+                                                 dmu_.as<double>(), mh_, mw_, 1, dtw_.as<C>());
+    });
+    d.resize((size_t)K_ * M_);
+    CK(cudaMemcpyAsync(d.data(), dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // solve_learning (learning.cpp:227-355) over all images
+  void learning(double* d_out, dcsc_learning_stats* st) override {
+    dcsc_learning_stats ls{};
+    if ((int)mu_.size() != K_) mu_.assign(K_, 1.0);
+    build_zhat();
+    int n_live = 0;
+    for (int k = 0; k < K_; ++k) n_live += live_h_[k] ? 1 : 0;
+    ls.n_dead = K_ - n_live;
+    if (n_live == 0) {  // every map zero: zero dictionary, gamma = 0 (learning.cpp:258-270)
+      ls.degenerate = 1;
+      CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+      CK(cudaStreamSynchronize(st_));
+      std::fill(d_out, d_out + (size_t)K_ * M_, 0.0);
+      if (st) *st = ls;
+      return;
+    }
+    double bn = 0.0;
+    for (int n = 0; n < N_; ++n) bn += xnorm2_[n];
+    const double bnorm = std::sqrt(bn);
+    std::vector<double> d;
+    std::vector<double> norms(K_, 0.0);
+    bool clamped = false;
+    for (int iter = 1; iter <= cfg_.max_mu_iters; ++iter) {
+      clamped = false;
+      for (int k = 0; k < K_; ++k)
+        if (mu_[k] < cfg_.mu_floor) {
+          mu_[k] = cfg_.mu_floor;
+          clamped = true;
+        }
+      upload_mu();
+      int cg_iters = 0;
+      bool cg_conv = false;
+      gamma_solve(bnorm, cg_iters, cg_conv);
+      ls.cg_iters += cg_iters;
+      if (!cg_conv) ls.cg_budget_hit = 1;
+      if (iter == 1) ls.cg_iters_first = cg_iters;
+      d_recover(d);
+      for (int k = 0; k < K_; ++k) {
+        double sq = 0.0;
+        for (int i = 0; i < M_; ++i) sq += d[(size_t)k * M_ + i] * d[(size_t)k * M_ + i];
+        norms[k] = std::sqrt(sq);
+      }
+      ls.mu_iters = iter;
+      bool settled = true;
+      for (int k = 0; k < K_; ++k) {
+        const bool at_boundary = std::abs(norms[k] - 1.0) <= kFilterNormTol;
+        const bool inactive = mu_[k] <= cfg_.mu_floor * (1.0 + 1e-9) && norms[k] < 1.0;
+        if (!at_boundary && !inactive) {
+          settled = false;
+          break;
+        }
+      }
+      if (settled) {
+        ls.converged = 1;
+        break;
+      }
+      if (iter < cfg_.max_mu_iters)
+        for (int k = 0; k < K_; ++k) mu_[k] = std::max(mu_[k] * norms[k], cfg_.mu_floor);
+    }
+    ls.mu_clamped = clamped ? 1 : 0;
+    for (int k = 0; k < K_; ++k) {
+      double scale = 1.0;
+      if (norms[k] > 1.0) {
+        scale = 1.0 / norms[k];
+        ++ls.rescaled_filters;
+      }
+      for (int i = 0; i < M_; ++i) d_out[(size_t)k * M_ + i] = scale * d[(size_t)k * M_ + i];
+    }
+    if (st) *st = ls;
+  }
+
+  void learning_apply(const double* mu, const double* v, double* out) override {
+    build_zhat();
+    std::vector<double> keep = mu_;
+    mu_.assign(mu, mu + K_);
+    for (int k = 0; k < K_; ++k) mu_[k] = std::max(mu_[k], cfg_.mu_floor);  // set_mu clamps (learning.cpp:66-81)
+    upload_mu();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, v, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
+    apply_hat(r_.as<C>(), ap_.as<C>());
+    c2r<double>(ap_.as<C>(), NB, tmp.as<double>(), D, N_);
+    CK(cudaMemcpyAsync(out, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    mu_ = keep;
+  }
+
+  // per-image data terms of `d` against the accepted maps (Parseval on z_hat)
+  void data_terms(const double* d, std::vector<double>& data) {
+    build_zhat();
+    upload_dict_spectra(d, dcand_.as<C>());
+    const dim3 g3(tiles_, N_);
+    launch(kFamContract, [&] {
+      contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), dcand_.as<C>(), dwk_.as<double>(), live_.as<int>(),
+                                                 xhat_.as<C>(), nullptr, partial_.as<double>(), N_, K_, NB, Wh, 1);
+    });
+    launch(kFamOther, [&] {
+      per_image_reduce<<<N_, 256, 0, st_>>>(partial_.as<double>(), tiles_, 0.5 / D, odata_.as<double>());
+    });
+    data.resize(N_);
+    CK(cudaMemcpyAsync(data.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void learning_data_term(const double* d, double* out) override {
+    std::vector<double> data;
+    data_terms(d ? d : dict_.data(), data);
+    double s = 0.0;
+    for (double v : data) s += v;
+    *out = s;
+  }
+
+  // per-image objective of a map source (coding candidates in u, or the accepted maps)
+  template <int MODE>
+  void objective_pass(const C* dhat, std::vector<double>& data, std::vector<double>& l1) {
+    coding_launch<MODE>(dhat, 0, N_);
+    launch(kFamOther, [&] {
+      objective_reduce<R><<<N_, 256, 0, st_>>>(part_.as<C>(), sums_.as<double>(), xhat_.as<C>(), G_, NB, Wh, 1.0 / D,
+                                               cfg_.beta, odata_.as<double>(), ol1_.as<double>());
+    });
+    data.resize(N_);
+    l1.resize(N_);
+    CK(cudaMemcpyAsync(data.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(l1.data(), ol1_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void objective(const double* d, dcsc_objective* per_image) override {
+    const C* dh = dhat_.as<C>();
+    if (d) {
+      upload_dict_spectra(d, dcand_.as<C>());
+      dh = dcand_.as<C>();
+    }
+    std::vector<double> data, l1;
+    objective_pass<kPassMaps>(dh, data, l1);
+    for (int n = 0; n < N_; ++n) {
+      per_image[n].data_term = data[n];
+      per_image[n].l1_term = l1[n];
+      per_image[n].total = data[n] + l1[n];
+      per_image[n].residual_norm = std::sqrt(2.0 * data[n]);
+      if (!std::isfinite(per_image[n].total)) throw NumErr("objective is not finite");
+    }
+  }
+
+  // run_csc (pipeline.cpp:158-301) from init_variables
+  void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) override {
+    *n_rows = 0;
+    *converged = 0;
+    init_variables();
+    if (max_outer == 0) return;
+    std::vector<dcsc_objective> img(N_);
+    double prev_total = 0.0;
+    {
+      double dsum = 0.0;
+      for (int n = 0; n < N_; ++n) {
+        img[n].data_term = 0.5 * xnorm2_[n];  // maps are zero: reconstruct = 0
+        img[n].l1_term = 0.0;
+        img[n].total = img[n].data_term;
+        img[n].residual_norm = std::sqrt(xnorm2_[n]);
+        dsum += img[n].data_term;
+      }
+      prev_total = dsum;
+    }
+    std::vector<dcsc_coding_stats> cs(N_);
+    std::vector<int> acc(N_);
+    int row = 0;
+    for (int outer = 1; outer <= max_outer; ++outer) {
+      const double w0 = now_ms();
+      coding(0, N_, cs.data());
+      const double coding_ms = now_ms() - w0;
+      std::vector<double> cdata, cl1;
+      objective_pass<kPassObjective>(dhat_.as<C>(), cdata, cl1);
+      long admm_total = 0;
+      for (int n = 0; n < N_; ++n) {
+        admm_total += cs[n].admm_iters;
+        const double tot = cdata[n] + cl1[n];
+        if (!std::isfinite(tot))
+          throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", coding phase");
+        acc[n] = tot <= img[n].total ? 1 : 0;
+        if (acc[n]) img[n] = {cdata[n], cl1[n], tot, std::sqrt(2.0 * cdata[n])};
+      }
+      double zc2 = 0.0, zn2 = 0.0;
+      long l0 = 0;
+      accept(acc, zc2, zn2, l0);
+      zhat_valid_ = false;
+      dcsc_objective after{};
+      for (int n = 0; n < N_; ++n) {
+        after.data_term += img[n].data_term;
+        after.l1_term += img[n].l1_term;
+        after.residual_norm += img[n].residual_norm * img[n].residual_norm;
+      }
+      after.total = after.data_term + after.l1_term;
+      after.residual_norm = std::sqrt(after.residual_norm);
+      const double w1 = now_ms();
+      rows[row++] = {outer, 0, after.total, after.data_term, after.l1_term, after.residual_norm,
+                     admm_total, 0, 0, coding_ms, w1 - w0, l0};
+
+      dcsc_learning_stats ls{};
+      std::vector<double> dc((size_t)K_ * M_);
+      learning(dc.data(), &ls);
+      const double learning_ms = now_ms() - w1;
+      std::vector<double> data;
+      data_terms(dc.data(), data);
+      double cand = 0.0;
+      for (double v : data) cand += v;
+      if (!std::isfinite(cand + after.l1_term))
+        throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", learning phase");
+      dcsc_objective afterl = after;
+      double dc2 = 0.0, dn2 = 0.0;
+      if (cand <= after.data_term) {
+        for (size_t i = 0; i < dc.size(); ++i) {
+          const double dl = dc[i] - dict_[i];
+          dc2 += dl * dl;
+        }
+        set_dictionary(dc.data());
+        afterl.data_term = cand;
+        afterl.total = cand + after.l1_term;
+        afterl.residual_norm = std::sqrt(2.0 * cand);
+        for (int n = 0; n < N_; ++n)
+          img[n] = {data[n], img[n].l1_term, data[n] + img[n].l1_term, std::sqrt(2.0 * data[n])};
+      }
+      for (double v : dict_) dn2 += v * v;
+      const double w2 = now_ms();
+      rows[row++] = {outer, 1, afterl.total, afterl.data_term, afterl.l1_term, afterl.residual_norm,
+                     0, ls.cg_iters, ls.mu_iters, learning_ms, w2 - w1, l0};
+      *n_rows = row;
+      const double obj_change = std::abs(prev_total - afterl.total) / std::max(std::abs(prev_total), 1e-30);
+      const double z_change = std::sqrt(zc2) / std::max(std::sqrt(zn2), 1.0);
+      const double d_change = std::sqrt(dc2) / std::max(std::sqrt(dn2), 1.0);
+      prev_total = afterl.total;
+      if (obj_change <= cfg_.tol && z_change <= cfg_.tol && d_change <= cfg_.tol) {
+        *converged = 1;
+        break;
+      }
+    }
+  }
+
+  // accept-only-descent for the coding half-step (pipeline.cpp:231-247)
+  void accept(const std::vector<int>& acc, double& zc2, double& zn2, long& l0) {
+    CK(cudaMemcpyAsync(accept_.p, acc.data(), sizeof(int) * N_, cudaMemcpyHostToDevice, st_));
+    const dim3 g(accept_chunks_, N_);
+    launch(kFamOther, [&] {
+      accept_maps<R, TBV><<<g, TBV, 0, st_>>>(u_.as<R>(), maps_.as<R>(), accept_.as<int>(), (size_t)K_ * D, cfg_.rho,
+                                               cfg_.beta, partial_.as<double>(), partial2_.as<double>(),
+                                               l0_.as<unsigned long long>());
+    });
+    const size_t cnt = (size_t)N_ * accept_chunks_;
+    std::vector<double> a(cnt), b(cnt);
+    std::vector<unsigned long long> c(cnt);
+    CK(cudaMemcpyAsync(a.data(), partial_.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(b.data(), partial2_.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(c.data(), l0_.p, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    zc2 = zn2 = 0.0;
+    l0 = 0;
+    for (size_t i = 0; i < cnt; ++i) {
+      zc2 += a[i];
+      zn2 += b[i];
+      l0 += (long)c[i];
+    }
+  }
+
+  void synchronize() override { CK(cudaStreamSynchronize(st_)); }
+
+  void set_profiling(int on) override {
+    CK(cudaStreamSynchronize(st_));
+    for (auto& e : prof_) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    prof_.clear();
+    profiling_ = on != 0;
+  }
+
+  void kernel_time(int fam, double* ms, long long* n) override {
+    CK(cudaStreamSynchronize(st_));
+    double t = 0.0;
+    long long c = 0;
+    for (auto& e : prof_)
+      if (e.fam == fam) {
+        float x = 0.f;
+        CK(cudaEventElapsedTime(&x, e.a, e.b));
+        t += x;
+        ++c;
+      }
+    *ms = t;
+    *n = c;
+  }
+
+  void event_mark(int slot) override {
+    if (slot < 0 || slot >= 64) throw InvErr("event slot out of range");
+    if ((int)marks_.size() < 64) marks_.resize(64, nullptr);
+    if (!marks_[slot]) CK(cudaEventCreate(&marks_[slot]));
+    CK(cudaEventRecord(marks_[slot], st_));
+  }
+
+  double event_elapsed(int a, int b) override {
+    if (a < 0 || b < 0 || a >= (int)marks_.size() || b >= (int)marks_.size() || !marks_[a] || !marks_[b])
+      throw InvErr("event slot not marked");
+    CK(cudaEventSynchronize(marks_[b]));
+    float x = 0.f;
+    CK(cudaEventElapsedTime(&x, marks_[a], marks_[b]));
+    return x;
+  }
+
+ private:
+  struct Prof {
+    int fam;
+    cudaEvent_t a, b;
+  };
+  dcsc_cuda_opts o_;
+  dcsc_solver_config cfg_;
+  int N_, K_, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_;
+  cudaStream_t st_ = nullptr;
+  void* pin_ = nullptr;
+  DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
+      infeas_, resc_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
+      partial_, partial2_, l0_, zhat_;
+  std::vector<double> dict_, mu_, xnorm2_, xs_host_;
+  std::vector<int> live_h_;
+  bool dict_zero_ = false, zhat_valid_ = false, profiling_ = false;
+  std::vector<Prof> prof_;
+  std::vector<cudaEvent_t> marks_;
+};
+
+// ---------------------------------------------------------------- size table
+#define DCSC_SIZES(X) \
+  X(double, 16, 16)   \
+  X(double, 16, 20)   \
+  X(double, 20, 20)   \
+  X(double, 64, 64)   \
+  X(double, 100, 100) \
+  X(float, 16, 16)    \
+  X(float, 16, 20)    \
+  X(float, 20, 20)    \
+  X(float, 64, 64)    \
+  X(float, 100, 100)  \
+  X(float, 128, 128)
+
+int prec_of(const char* t) { return std::strcmp(t, "double") == 0 ? 64 : 32; }
+
+std::unique_ptr<EngineBase> make_engine(const dcsc_cuda_opts& o) {
+#define DCSC_MAKE(Rt, Hh, Ww) \
+  if (o.precision == prec_of(#Rt) && o.height == Hh && o.width == Ww) return std::make_unique<Engine<Rt, Hh, Ww>>(o);
+  DCSC_SIZES(DCSC_MAKE)
+#undef DCSC_MAKE
+  throw DimErr("no compiled kernel family for grid " + std::to_string(o.height) + "x" + std::to_string(o.width) +
+               " at FP" + std::to_string(o.precision));
+}
+
+bool supported(int H, int W, int prec) {
+#define DCSC_SUP(Rt, Hh, Ww) \
+  if (prec == prec_of(#Rt) && H == Hh && W == Ww) return true;
+  DCSC_SIZES(DCSC_SUP)
+#undef DCSC_SUP
+  return false;
+}
+
+// Standalone half-spectrum DFTs
+template <class R, int H, int W>
+void dft_batch(bool inverse, int batch, const double* in, double* out) {
+  using E = Engine<R, H, W>;
+  using P = typename E::P;
+  using C = cx<R>;
+  constexpr int NB = P::NB, D = P::D, T = E::T;
+  static bool attr = false;
+  if (!attr) {
+    if (Smem<P>::two > 48 * 1024) {
+      CK(cudaFuncSetAttribute((const void*)r2c_planes<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<P>::two));
+      CK(cudaFuncSetAttribute((const void*)c2r_planes<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<P>::two));
+    }
+    attr = true;
+  }
+  std::vector<C> tw(P::TW_LEN);
+  auto fill = [&](int off, int L) {
+    for (int j = 0; j < L; ++j) {
+      const long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
+      tw[off + j] = mk<C>(R(std::cos(a)), R(std::sin(a)));
+    }
+  };
+  fill(0, W);
+  if (!P::SAME_TW) fill(W, H);
+  DevMem dtw, din, dout, spec;
+  dtw.alloc(sizeof(C) * P::TW_LEN);
+  CK(cudaMemcpy(dtw.p, tw.data(), dtw.bytes, cudaMemcpyHostToDevice));
+  spec.alloc(sizeof(C) * (size_t)batch * NB);
+  if (!inverse) {
+    din.alloc(sizeof(double) * (size_t)batch * D);
+    CK(cudaMemcpy(din.p, in, din.bytes, cudaMemcpyHostToDevice));
+    r2c_planes<P, double><<<batch, T, Smem<P>::two>>>(din.as<double>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+    CK(cudaGetLastError());
+    std::vector<C> h((size_t)batch * NB);
+    CK(cudaMemcpy(h.data(), spec.p, spec.bytes, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h.size(); ++i) {
+      out[2 * i] = h[i].x;
+      out[2 * i + 1] = h[i].y;
+    }
+  } else {
+    std::vector<C> h((size_t)batch * NB);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = mk<C>(R(in[2 * i]), R(in[2 * i + 1]));
+    CK(cudaMemcpy(spec.p, h.data(), spec.bytes, cudaMemcpyHostToDevice));
+    dout.alloc(sizeof(double) * (size_t)batch * D);
+    c2r_planes<P, double><<<batch, T, Smem<P>::two>>>(spec.as<C>(), NB, dout.as<double>(), D, dtw.as<C>(), nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout.p, dout.bytes, cudaMemcpyDeviceToHost));
+  }
+  CK(cudaDeviceSynchronize());
+}
+
+void dft_dispatch(int H, int W, int prec, bool inverse, int batch, const double* in, double* out) {
+#define DCSC_DFT(Rt, Hh, Ww)                           \
+  if (prec == prec_of(#Rt) && H == Hh && W == Ww) {    \
+    dft_batch<Rt, Hh, Ww>(inverse, batch, in, out);    \
+    return;                                            \
+  }
+  DCSC_SIZES(DCSC_DFT)
+#undef DCSC_DFT
+  throw DimErr("no compiled FFT for this grid/precision");
+}
+
+}  // namespace
+
+struct dcsc_cuda_ctx {
+  std::unique_ptr<EngineBase> eng;
+};
+
+#define CTX_CHECK                                         \
+  if (!ctx || !ctx->eng) {                                \
+    g_err = "null context";                               \
+    return DCSC_ERR_INVALID;                              \
+  }
+
+extern "C" {
+
+int dcsc_cuda_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)g_err.size();
+}
+
+int dcsc_cuda_supported_grid(int height, int width, int precision) { return supported(height, width, precision) ? 1 : 0; }
+
+int dcsc_cuda_create(const dcsc_cuda_opts* opts, dcsc_cuda_ctx** out) {
+  return guarded([&] {
+    if (!opts || !out) throw InvErr("null argument");
+    validate_cfg(opts->cfg);
+    if (opts->n_images < 1) throw InvErr("dataset is empty");
+    if (opts->filters < 1) throw InvErr("filter count must be >= 1");
+    if (opts->support_h < 1 || opts->support_w < 1 || opts->support_h > opts->height ||
+        opts->support_w > opts->width)
+      throw DimErr("filter support must fit inside the grid");
+    if (opts->precision != 32 && opts->precision != 64) throw InvErr("precision must be 32 or 64");
+    if (opts->cfg.normalize < 0 || opts->cfg.normalize > 2) throw InvErr("normalize must be 0, 1 or 2");
+    auto* c = new dcsc_cuda_ctx;
+    try {
+      c->eng = make_engine(*opts);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int dcsc_cuda_destroy(dcsc_cuda_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int dcsc_cuda_synchronize(dcsc_cuda_ctx* ctx) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->synchronize(); });
+}
+
+int dcsc_cuda_set_signals(dcsc_cuda_ctx* ctx, const double* x) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->set_signals(x); });
+}
+int dcsc_cuda_get_signals(dcsc_cuda_ctx* ctx, double* x) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->get_signals(x); });
+}
+int dcsc_cuda_set_dictionary(dcsc_cuda_ctx* ctx, const double* d) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->set_dictionary(d); });
+}
+int dcsc_cuda_get_dictionary(dcsc_cuda_ctx* ctx, double* d) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->get_dictionary(d); });
+}
+int dcsc_cuda_init_variables(dcsc_cuda_ctx* ctx) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->init_variables(); });
+}
+int dcsc_cuda_set_coding_state(dcsc_cuda_ctx* ctx, int n0, int n1, const double* theta, const double* z) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->set_coding_state(n0, n1, theta, z); });
+}
+int dcsc_cuda_get_coding_state(dcsc_cuda_ctx* ctx, int n0, int n1, double* theta, double* z, double* lambda) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->get_coding_state(n0, n1, theta, z, lambda); });
+}
+int dcsc_cuda_coding(dcsc_cuda_ctx* ctx, int n0, int n1, dcsc_coding_stats* stats) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->coding(n0, n1, stats); });
+}
+int dcsc_cuda_set_maps(dcsc_cuda_ctx* ctx, int n0, int n1, const double* z) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->set_maps(n0, n1, z); });
+}
+int dcsc_cuda_get_maps(dcsc_cuda_ctx* ctx, int n0, int n1, double* z) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->get_maps(n0, n1, z); });
+}
+int dcsc_cuda_set_learning_state(dcsc_cuda_ctx* ctx, const double* gamma, const double* mu) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->set_learning_state(gamma, mu); });
+}
+int dcsc_cuda_get_learning_state(dcsc_cuda_ctx* ctx, double* gamma, double* mu) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->get_learning_state(gamma, mu); });
+}
+int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* stats) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->learning(d_out, stats); });
+}
+int dcsc_cuda_learning_apply(dcsc_cuda_ctx* ctx, const double* mu, const double* v, double* out) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->learning_apply(mu, v, out); });
+}
+int dcsc_cuda_objective(dcsc_cuda_ctx* ctx, const double* d, dcsc_objective* per_image) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->objective(d, per_image); });
+}
+int dcsc_cuda_learning_data_term(dcsc_cuda_ctx* ctx, const double* d, double* data) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->learning_data_term(d, data); });
+}
+int dcsc_cuda_run(dcsc_cuda_ctx* ctx, int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->run(max_outer, rows, n_rows, converged); });
+}
+int dcsc_cuda_dft2_forward(int height, int width, int precision, int batch, const double* in, double* out) {
+  return guarded([&] { dft_dispatch(height, width, precision, false, batch, in, out); });
+}
+int dcsc_cuda_dft2_inverse(int height, int width, int precision, int batch, const double* in, double* out) {
+  return guarded([&] { dft_dispatch(height, width, precision, true, batch, in, out); });
+}
+int dcsc_cuda_kernel_launches(dcsc_cuda_ctx* ctx, long long* count) {
+  CTX_CHECK
+  *count = ctx->eng->launches;
+  return DCSC_OK;
+}
+int dcsc_cuda_set_profiling(dcsc_cuda_ctx* ctx, int enable) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->set_profiling(enable); });
+}
+int dcsc_cuda_kernel_time(dcsc_cuda_ctx* ctx, int family, double* total_ms, long long* launches) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->kernel_time(family, total_ms, launches); });
+}
+int dcsc_cuda_event_mark(dcsc_cuda_ctx* ctx, int slot) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->event_mark(slot); });
+}
+int dcsc_cuda_event_elapsed(dcsc_cuda_ctx* ctx, int a, int b, double* ms) {
+  CTX_CHECK
+  return guarded([&] { *ms = ctx->eng->event_elapsed(a, b); });
+}
+int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes) {
+  CTX_CHECK
+  *bytes = ctx->eng->device_bytes;
+  return DCSC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,795 @@
+// Device kernels of the dual-domain CSC hot path, templated on the plane type
+// P = Plane<R, H, W, T> (fft2d.cuh). Reference anchors are cited per kernel.
+#pragma once
+#include "fft2d.cuh"
+
+namespace dcsc_cuda {
+
+constexpr double kAdmmRelTol = 1e-4;  // proj/include/dcsc/coding.hpp:41
+
+enum PassMode : int {
+  kPassAdmm = 0,      // one full ADMM iteration for a filter group
+  kPassPrologue = 1,  // w = theta + z/rho from the stored state -> acc (initial lambda)
+  kPassObjective = 2, // z from the ADMM state -> acc = sum_k d_hat_k z_hat_k, l1
+  kPassMaps = 3,      // z from the accepted-maps buffer -> acc, l1
+};
+
+// Per-(image, group) partial sums written by coding_pass, in slot order:
+// 0 sum (theta'-t)^2, 1 sum theta'^2, 2 sum t^2, 3 sum dz^2, 4 sum z'^2,
+// 5 sum dtheta^2, 6 max|t|, 7 unused. (proj/src/coding.cpp:237-259)
+// Objective modes: 0 = sum |z|.
+constexpr int kSums = 8;
+
+template <class R>
+struct CodingArgs {
+  const cx<R>* dhat;    // K x NB filter spectra
+  const cx<R>* lamhat;  // N x NB current lambda_hat
+  R* u;                 // N x K x D ADMM state u = t - z/rho (theta = clamp(u), z = rho(theta-u))
+  const R* maps;        // N x K x D accepted maps (kPassMaps)
+  cx<R>* part;          // N x G x NB partial sum_k d_hat_k w_hat_k
+  double* sums;         // N x G x kSums
+  const int* conv;      // N: nonzero = this image's ADMM has stopped
+  int K, G, kpg;
+  R rho, beta;
+  const cx<R>* tw;      // twiddle table (global)
+};
+
+template <class P>
+struct Smem {
+  static constexpr size_t tw_bytes = sizeof(typename P::C) * P::TW_LEN;
+  static constexpr size_t two = 2 * P::buffer_bytes + tw_bytes;
+  static constexpr size_t three = 3 * P::buffer_bytes + tw_bytes;
+  static constexpr bool acc_in_smem = three <= 220 * 1024;
+  static constexpr size_t coding = acc_in_smem ? three : two;
+};
+
+// ----------------------------------------------------------------------------
+// The fused coding kernel. One CTA = (image n, filter group g); for each filter:
+//   t_hat = conj(d_hat_k) lambda_hat           (coding.cpp:77-86, correlate)
+//   t = iDFT(t_hat)                            (coding.cpp:234)
+//   theta' = clamp(t - z/rho), z' = z + rho(theta'-t)   (coding.cpp:237-246)
+//     in closed form on u: u' = t - z/rho, theta' = clamp(u'), z' = rho(theta'-u')
+//   w = theta' + z'/rho = 2 theta' - u'  ->  w_hat = DFT(w)
+//     (one forward FFT replaces DFT(theta) and DFT(z), coding.cpp:260-261,224-227)
+//   acc += d_hat_k w_hat_k                     (lambda_from_w numerator, coding.cpp:25-37)
+// ----------------------------------------------------------------------------
+template <class P, int MODE>
+__global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, D = P::D, T = P::T;
+  constexpr int W2 = W / 2, RLS = P::RLS;
+  constexpr bool ACC_SMEM = Smem<P>::acc_in_smem;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[kSums * (T / 32)];
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB + (ACC_SMEM ? NB : 0);
+  const int n = blockIdx.y, g = blockIdx.x;
+  if (MODE == kPassAdmm && a.conv[n]) return;
+  C* ACC = ACC_SMEM ? (B1 + NB) : (a.part + ((size_t)n * a.G + g) * NB);
+
+  P::load_twiddles(TW, a.tw);
+  for (int i = threadIdx.x; i < NB; i += T) ACC[i] = mk<C>(R(0), R(0));
+  __syncthreads();
+
+  const R rho = a.rho, beta = a.beta, invD = R(1) / R(D), inv_rho = R(1) / rho;
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
+  const int k0 = g * a.kpg;
+  const int k1 = min(a.K, k0 + a.kpg);
+  for (int k = k0; k < k1; ++k) {
+    const C* __restrict__ dk = a.dhat + (size_t)k * NB;
+    C* work;
+    if constexpr (MODE == kPassAdmm) {
+      R* __restrict__ uk = a.u + ((size_t)n * a.K + k) * D;
+      const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
+      for (int it = threadIdx.x; it < P::HALF; it += T) {
+        const int r = it / W2, c = it % W2;
+        const int b = r * Wh + c;
+        if (c == 0) {
+          const C t0 = cmulc(dk[b], lam[b]);
+          const C tn = cmulc(dk[b + W2], lam[b + W2]);
+          B0[b] = P::pack_col0(t0, tn);
+        } else {
+          B0[b] = cmulc(dk[b], lam[b]);
+        }
+      }
+      __syncthreads();
+      C* sp = P::inverse(B0, B1, TW);
+      for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+        const int pa = it / W, c = it % W;
+        const C v = sp[pa * RLS + c];
+        R* up = uk + (2 * pa) * W + c;
+        const R tv[2] = {v.x * invD, v.y * invD};
+        const R uo[2] = {up[0], up[W]};
+        R wv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const R t = tv[e];
+          const R th_o = fmin(fmax(uo[e], -beta), beta);
+          const R un = t - (th_o - uo[e]);           // u' = t - z/rho
+          const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
+          const R zn = rho * (th - un);              // z' = rho (theta' - u')
+          const R d_tt = th - t;
+          const R dz = rho * d_tt;                   // z' - z = rho (theta' - t)
+          const R dth = th - th_o;
+          s0 += (double)d_tt * (double)d_tt;
+          s1 += (double)th * (double)th;
+          s2 += (double)t * (double)t;
+          s3 += (double)dz * (double)dz;
+          s4 += (double)zn * (double)zn;
+          s5 += (double)dth * (double)dth;
+          s6 = fmax(s6, (double)fabs(t));
+          wv[e] = R(2) * th - un;
+          if (e == 0) up[0] = un; else up[W] = un;
+        }
+        sp[pa * RLS + c] = mk<C>(wv[0], wv[1]);
+      }
+      __syncthreads();
+      work = sp;
+    } else {
+      const R* __restrict__ src = (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D
+                                                      : a.u + ((size_t)n * a.K + k) * D;
+      for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+        const int pa = it / W, c = it % W;
+        const R v0 = src[(2 * pa) * W + c], v1 = src[(2 * pa + 1) * W + c];
+        R w0, w1;
+        if constexpr (MODE == kPassPrologue) {
+          w0 = R(2) * fmin(fmax(v0, -beta), beta) - v0;
+          w1 = R(2) * fmin(fmax(v1, -beta), beta) - v1;
+        } else if constexpr (MODE == kPassObjective) {
+          w0 = rho * (fmin(fmax(v0, -beta), beta) - v0);
+          w1 = rho * (fmin(fmax(v1, -beta), beta) - v1);
+          s0 += (double)fabs(w0) + (double)fabs(w1);
+        } else {
+          w0 = v0;
+          w1 = v1;
+          s0 += (double)fabs(w0) + (double)fabs(w1);
+        }
+        B0[pa * RLS + c] = mk<C>(w0, w1);
+      }
+      __syncthreads();
+      work = B0;
+    }
+    C* other = (work == B0) ? B1 : B0;
+    C* spec = P::forward(work, other, TW);
+    for (int it = threadIdx.x; it < P::HALF; it += T) {
+      const int r = it / W2, c = it % W2;
+      const int b = r * Wh + c;
+      if (c == 0) {
+        C x0, xn;
+        P::unpack_col0(spec, r, x0, xn);
+        ACC[b] = cadd(ACC[b], cmul(dk[b], x0));
+        ACC[b + W2] = cadd(ACC[b + W2], cmul(dk[b + W2], xn));
+      } else {
+        ACC[b] = cadd(ACC[b], cmul(dk[b], spec[b]));
+      }
+    }
+    __syncthreads();
+  }
+  (void)inv_rho;
+  if constexpr (ACC_SMEM) {
+    C* dst = a.part + ((size_t)n * a.G + g) * NB;
+    for (int i = threadIdx.x; i < NB; i += T) dst[i] = ACC[i];
+  }
+  // reductions of the partial sums (FP64)
+  double v[7] = {s0, s1, s2, s3, s4, s5, 0.0};
+  block_sum<T, 7>(v, red);
+  const double mx = block_max(s6, red, T);
+  if (threadIdx.x == 0) {
+    double* o = a.sums + ((size_t)n * a.G + g) * kSums;
+    for (int i = 0; i < 6; ++i) o[i] = v[i];
+    o[6] = mx;
+    o[7] = 0.0;
+  }
+}
+
+// Per-image ADMM bookkeeping written by lambda_update (CTA 0 of the image).
+struct ImageAdmm {
+  int iters;
+  int converged;
+  double primal, zc, thc, tinf;
+};
+
+// ----------------------------------------------------------------------------
+// lambda_hat = (sum_g part_g - x_hat / rho) / sigma    (coding.cpp:25-37)
+// preceded by the per-image stop test on the iteration's partial sums
+// (coding.cpp:264-283). A converging or final iteration keeps lambda_hat.
+// ----------------------------------------------------------------------------
+template <class R>
+__global__ void lambda_update(const cx<R>* __restrict__ part, const double* __restrict__ sums,
+                              const cx<R>* __restrict__ xhat, const R* __restrict__ sigma,
+                              cx<R>* __restrict__ lamhat, int* conv, ImageAdmm* img, int G, int NB,
+                              R rho, int iter, int is_last, int prologue) {
+  using C = cx<R>;
+  const int n = blockIdx.y;
+  if (!prologue && conv[n]) return;
+  bool stop = false;
+  if (!prologue) {
+    double tt = 0, th = 0, t2 = 0, dz2 = 0, z2 = 0, dth = 0, tinf = 0;
+    for (int g = 0; g < G; ++g) {
+      const double* s = sums + ((size_t)n * G + g) * kSums;
+      tt += s[0]; th += s[1]; t2 += s[2]; dz2 += s[3]; z2 += s[4]; dth += s[5];
+      tinf = fmax(tinf, s[6]);
+    }
+    const double denom = fmax(fmax(sqrt(th), sqrt(t2)), 1.0);
+    const double primal = sqrt(tt) / denom;
+    const double zc = sqrt(dz2) / fmax(sqrt(z2), 1.0);
+    const double thc = sqrt(dth) / fmax(sqrt(th), 1.0);
+    stop = primal <= kAdmmRelTol && zc <= kAdmmRelTol && thc <= kAdmmRelTol;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ImageAdmm& m = img[n];
+      m.iters = iter;
+      m.primal = primal;
+      m.zc = zc;
+      m.thc = thc;
+      m.tinf = tinf;
+      if (stop) {
+        m.converged = 1;
+        conv[n] = 1;
+      }
+    }
+  }
+  if (stop || is_last) return;
+  const R inv_rho = R(1) / rho;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= NB) return;
+  C acc = part[((size_t)n * G) * NB + b];
+  for (int g = 1; g < G; ++g) acc = cadd(acc, part[((size_t)n * G + g) * NB + b]);
+  const C xv = xhat[(size_t)n * NB + b];
+  const R s = sigma[b];
+  lamhat[(size_t)n * NB + b] = mk<C>((acc.x - xv.x * inv_rho) / s, (acc.y - xv.y * inv_rho) / s);
+}
+
+// ----------------------------------------------------------------------------
+// Batched r2c of real planes (x_hat, z_hat, padded filters) and c2r.
+// ----------------------------------------------------------------------------
+template <class P, class SRC>
+__global__ void __launch_bounds__(P::T)
+r2c_planes(const SRC* __restrict__ src, size_t src_stride, cx<typename P::R>* __restrict__ dst,
+           size_t dst_stride, const cx<typename P::R>* tw, int* live_flags, int live_mod) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB;
+  const int p = blockIdx.x;
+  P::load_twiddles(TW, tw);
+  const SRC* s = src + (size_t)p * src_stride;
+  int any = 0;
+  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+    const int pa = it / W, c = it % W;
+    const R v0 = R(s[(2 * pa) * W + c]), v1 = R(s[(2 * pa + 1) * W + c]);
+    any |= (v0 != R(0)) | (v1 != R(0));
+    B0[pa * P::RLS + c] = mk<C>(v0, v1);
+  }
+  __syncthreads();
+  if (live_flags) {
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0 && any) atomicOr(live_flags + (p % live_mod), 1);
+  }
+  C* spec = P::forward(B0, B1, TW);
+  C* d = dst + (size_t)p * dst_stride;
+  for (int it = threadIdx.x; it < P::HALF; it += T) {
+    const int r = it / W2, c = it % W2;
+    const int b = r * Wh + c;
+    if (c == 0) {
+      C x0, xn;
+      P::unpack_col0(spec, r, x0, xn);
+      d[b] = x0;
+      d[b + W2] = xn;
+    } else {
+      d[b] = spec[b];
+    }
+  }
+}
+
+// Zero-padded filters (corner placement, spectral.cpp:106-122) -> spectra.
+template <class P>
+__global__ void __launch_bounds__(P::T)
+r2c_filters(const double* __restrict__ d, int mh, int mw, cx<typename P::R>* __restrict__ dst,
+            const cx<typename P::R>* tw) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB;
+  const int k = blockIdx.x;
+  P::load_twiddles(TW, tw);
+  const double* f = d + (size_t)k * mh * mw;
+  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+    const int pa = it / W, c = it % W;
+    const int r0 = 2 * pa, r1 = r0 + 1;
+    const R v0 = (r0 < mh && c < mw) ? R(f[r0 * mw + c]) : R(0);
+    const R v1 = (r1 < mh && c < mw) ? R(f[r1 * mw + c]) : R(0);
+    B0[pa * P::RLS + c] = mk<C>(v0, v1);
+  }
+  __syncthreads();
+  C* spec = P::forward(B0, B1, TW);
+  C* o = dst + (size_t)k * NB;
+  for (int it = threadIdx.x; it < P::HALF; it += T) {
+    const int r = it / W2, c = it % W2;
+    const int b = r * Wh + c;
+    if (c == 0) {
+      C x0, xn;
+      P::unpack_col0(spec, r, x0, xn);
+      o[b] = x0;
+      o[b + W2] = xn;
+    } else {
+      o[b] = spec[b];
+    }
+  }
+}
+
+// Batched c2r of NSL spectra (scaled by `scale`/D) into real planes.
+template <class P, class DST>
+__global__ void __launch_bounds__(P::T)
+c2r_planes(const cx<typename P::R>* __restrict__ src, size_t src_stride, DST* __restrict__ dst,
+           size_t dst_stride, const cx<typename P::R>* tw, const double* scale) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2, D = P::D;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB;
+  const int p = blockIdx.x;
+  P::load_twiddles(TW, tw);
+  const C* s = src + (size_t)p * src_stride;
+  for (int it = threadIdx.x; it < P::HALF; it += T) {
+    const int r = it / W2, c = it % W2;
+    const int b = r * Wh + c;
+    B0[b] = (c == 0) ? P::pack_col0(s[b], s[b + W2]) : s[b];
+  }
+  __syncthreads();
+  C* sp = P::inverse(B0, B1, TW);
+  const R sc = R((scale ? scale[p] : 1.0) / (double)D);
+  DST* o = dst + (size_t)p * dst_stride;
+  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+    const int pa = it / W, c = it % W;
+    const C v = sp[pa * P::RLS + c];
+    o[(2 * pa) * W + c] = DST(v.x * sc);
+    o[(2 * pa + 1) * W + c] = DST(v.y * sc);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Learning: the support-mask step of LearningOperator::apply
+// (learning.cpp:96-107): p_hat_k = DFT(mask . iDFT(c_k)), and the crop of
+// d_recover (learning.cpp:205-214): d_k = -0.5/max(mu_k,1e-300) crop(iDFT(c_k)).
+// mode 0: mask -> p_hat (NSL); mode 1: crop -> d_out (K x mh x mw, double).
+// ----------------------------------------------------------------------------
+template <class P>
+__global__ void __launch_bounds__(P::T)
+mask_step(const cx<typename P::R>* __restrict__ c, cx<typename P::R>* __restrict__ phat,
+          double* __restrict__ d_out, const int* live, const double* mu, int mh, int mw, int mode,
+          const cx<typename P::R>* tw) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2, D = P::D;
+  constexpr int RLS = P::RLS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB;
+  const int k = blockIdx.x;
+  if (!live[k]) {  // dead filter: skipped by the operator (learning.cpp:96)
+    if (mode == 0) {
+      for (int i = threadIdx.x; i < NB; i += T) phat[(size_t)k * NB + i] = mk<C>(R(0), R(0));
+    } else {
+      for (int i = threadIdx.x; i < mh * mw; i += T) d_out[(size_t)k * mh * mw + i] = 0.0;
+    }
+    return;
+  }
+  P::load_twiddles(TW, tw);
+  const C* s = c + (size_t)k * NB;
+  for (int it = threadIdx.x; it < P::HALF; it += T) {
+    const int r = it / W2, cc = it % W2;
+    const int b = r * Wh + cc;
+    B0[b] = (cc == 0) ? P::pack_col0(s[b], s[b + W2]) : s[b];
+  }
+  __syncthreads();
+  C* sp = P::inverse(B0, B1, TW);
+  const R invD = R(1) / R(D);
+  if (mode == 1) {
+    const double scale = -0.5 / fmax(mu[k], 1e-300);
+    for (int i = threadIdx.x; i < mh * mw; i += T) {
+      const int r = i / mw, cc = i % mw;
+      const C v = sp[(r / 2) * RLS + cc];
+      const R val = ((r & 1) ? v.y : v.x) * invD;
+      d_out[(size_t)k * mh * mw + i] = scale * (double)val;
+    }
+    return;
+  }
+  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+    const int pa = it / W, cc = it % W;
+    const C v = sp[pa * RLS + cc];
+    const bool in_c = cc < mw;
+    const R v0 = (in_c && 2 * pa < mh) ? v.x * invD : R(0);
+    const R v1 = (in_c && 2 * pa + 1 < mh) ? v.y * invD : R(0);
+    sp[pa * RLS + cc] = mk<C>(v0, v1);
+  }
+  __syncthreads();
+  C* other = (sp == B0) ? B1 : B0;
+  C* spec = P::forward(sp, other, TW);
+  C* o = phat + (size_t)k * NB;
+  for (int it = threadIdx.x; it < P::HALF; it += T) {
+    const int r = it / W2, cc = it % W2;
+    const int b = r * Wh + cc;
+    if (cc == 0) {
+      C x0, xn;
+      P::unpack_col0(spec, r, x0, xn);
+      o[b] = x0;
+      o[b + W2] = xn;
+    } else {
+      o[b] = spec[b];
+    }
+  }
+}
+
+// Parseval weight of a half-spectrum bin: columns 0 and W/2 are their own
+// mirrors (weight 1), every other bin stands for itself and its conjugate.
+__device__ __forceinline__ double bin_weight(int b, int Wh) {
+  const int c = b % Wh;
+  return (c == 0 || c == Wh - 1) ? 1.0 : 2.0;
+}
+
+// c_k(w) = sum_n conj(z_hat_nk(w)) v_hat_n(w)   (learning.cpp:97-102, 204-209)
+template <class R>
+__global__ void contract_c(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ v,
+                           cx<R>* __restrict__ c, const int* __restrict__ live, int N, int K,
+                           int NB) {
+  using C = cx<R>;
+  const int k = blockIdx.y;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= NB) return;
+  double ar = 0.0, ai = 0.0;
+  if (live[k]) {
+    const C* zp = zhat + (size_t)k * NB + b;
+    const size_t zs = (size_t)K * NB;
+#pragma unroll 4
+    for (int n = 0; n < N; ++n) {
+      const C z = zp[(size_t)n * zs];
+      const C x = v[(size_t)n * NB + b];
+      ar += (double)z.x * (double)x.x + (double)z.y * (double)x.y;
+      ai += (double)z.x * (double)x.y - (double)z.y * (double)x.x;
+    }
+  }
+  c[(size_t)k * NB + b] = mk<C>(R(ar), R(ai));
+}
+
+// out_n = v_n + sum_k (0.5/mu_k) z_hat_nk p_hat_k (learning.cpp:109-121, in the
+// frequency domain), with the block partial of <v, out> (Parseval, FP64).
+// mode 1 (learning data term): y_n = sum_k d_hat_k z_hat_nk, partial of
+// |y_n - x_hat_n|^2 weighted, no identity (objective.cpp:83-95).
+template <class R, int TB>
+__global__ void __launch_bounds__(TB)
+contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const double* __restrict__ wk,
+             const int* __restrict__ live, const cx<R>* __restrict__ v, cx<R>* __restrict__ out,
+             double* __restrict__ partial, int N, int K, int NB, int Wh, int mode) {
+  using C = cx<R>;
+  __shared__ double red[TB / 32];
+  const int n = blockIdx.y;
+  const int b = blockIdx.x * TB + threadIdx.x;
+  double dot = 0.0;
+  if (b < NB) {
+    double ar = 0.0, ai = 0.0;
+    const C* zp = zhat + (size_t)n * K * NB + b;
+    for (int k = 0; k < K; ++k) {
+      if (!live[k]) continue;
+      const C z = zp[(size_t)k * NB];
+      const C q = p[(size_t)k * NB + b];
+      const double w = mode == 0 ? wk[k] : 1.0;
+      ar += w * ((double)z.x * (double)q.x - (double)z.y * (double)q.y);
+      ai += w * ((double)z.x * (double)q.y + (double)z.y * (double)q.x);
+    }
+    const C vv = v[(size_t)n * NB + b];
+    if (mode == 0) {
+      const C o = mk<C>(R((double)vv.x + ar), R((double)vv.y + ai));
+      out[(size_t)n * NB + b] = o;
+      dot = bin_weight(b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
+    } else {
+      const double rr = ar - (double)vv.x, ri = ai - (double)vv.y;
+      dot = bin_weight(b, Wh) * (rr * rr + ri * ri);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < TB / 32; ++w) s += red[w];
+    partial[(size_t)n * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// CG vector kernels on half spectra (gamma_solve, learning.cpp:136-185).
+// Dot products are spatial via Parseval: <a,b> = (1/D) sum_bins wt Re(conj(a) b).
+// ----------------------------------------------------------------------------
+template <int TB>
+__device__ __forceinline__ void block_partial(double v, double* out_slot) {
+  __shared__ double red[TB / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < TB / 32; ++w) s += red[w];
+    *out_slot = s;
+  }
+}
+
+// r = -x_hat - ap ; p = r ; partial of rr
+template <class R, int TB>
+__global__ void __launch_bounds__(TB)
+cg_init(const cx<R>* __restrict__ xhat, const cx<R>* __restrict__ ap, cx<R>* __restrict__ r,
+        cx<R>* __restrict__ p, double* partial, size_t total, int NB, int Wh) {
+  using C = cx<R>;
+  const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
+  double v = 0.0;
+  if (i < total) {
+    const C x = xhat[i], a = ap[i];
+    const C rv = mk<C>(-x.x - a.x, -x.y - a.y);
+    r[i] = rv;
+    p[i] = rv;
+    v = bin_weight((int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
+  }
+  block_partial<TB>(v, partial + blockIdx.x);
+}
+
+struct CgState {
+  double rr, pap, alpha, beta, rel, bnorm;
+  int bad;
+  int pad;
+};
+
+// gamma += alpha p ; r -= alpha ap ; partial of rr_new
+template <class R, int TB>
+__global__ void __launch_bounds__(TB)
+cg_update(cx<R>* __restrict__ gam, cx<R>* __restrict__ r, const cx<R>* __restrict__ p,
+          const cx<R>* __restrict__ ap, const CgState* st, double* partial, size_t total, int NB,
+          int Wh) {
+  using C = cx<R>;
+  const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
+  double v = 0.0;
+  if (i < total && !st->bad) {
+    const double al = st->alpha;
+    const C pv = p[i], av = ap[i], gv = gam[i], rv0 = r[i];
+    gam[i] = mk<C>(R(gv.x + al * pv.x), R(gv.y + al * pv.y));
+    const C rv = mk<C>(R(rv0.x - al * av.x), R(rv0.y - al * av.y));
+    r[i] = rv;
+    v = bin_weight((int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
+  }
+  block_partial<TB>(v, partial + blockIdx.x);
+}
+
+// p = r + beta p
+template <class R, int TB>
+__global__ void __launch_bounds__(TB)
+cg_pupdate(const cx<R>* __restrict__ r, cx<R>* __restrict__ p, const CgState* st, size_t total) {
+  using C = cx<R>;
+  const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
+  if (i >= total || st->bad) return;
+  const double be = st->beta;
+  const C rv = r[i], pv = p[i];
+  p[i] = mk<C>(R(rv.x + be * pv.x), R(rv.y + be * pv.y));
+}
+
+// Single-block scalar step of CG. step 0: rr from the init residual; step 1:
+// pap -> alpha (guard pap <= 0, learning.cpp:166); step 2: rr_new -> rel, beta.
+__global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step) {
+  __shared__ double red[32];
+  double v = 0.0;
+  // fixed-order strided partial sums, then a fixed-order tree: deterministic
+  for (int i = threadIdx.x; i < count; i += blockDim.x) v += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
+  s *= invD;
+  if (step == 0) {
+    st->rr = s;
+    st->rel = sqrt(s) / st->bnorm;
+    st->bad = 0;
+  } else if (step == 1) {
+    st->pap = s;
+    if (s <= 0.0) {
+      st->bad = 1;
+    } else {
+      st->alpha = st->rr / s;
+    }
+  } else {
+    st->rel = sqrt(s) / st->bnorm;
+    st->beta = s / st->rr;
+    st->rr = s;
+  }
+}
+
+// Per-image sum of block partials (learning data term / objective), out[n] = 0.5*invD*sum.
+__global__ void per_image_reduce(const double* partial, int tiles, double scale, double* out) {
+  __shared__ double red[32];
+  const int n = blockIdx.x;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < tiles; i += blockDim.x) v += partial[(size_t)n * tiles + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
+    out[n] = scale * s;
+  }
+}
+
+// Coding objective: data_n = 1/2 ||sum_k d_k * z_k - x||^2 by Parseval on the
+// reduced partial spectra; l1_n = beta * sum |z| (objective.cpp:59-81).
+template <class R>
+__global__ void objective_reduce(const cx<R>* __restrict__ part, const double* __restrict__ sums,
+                                 const cx<R>* __restrict__ xhat, int G, int NB, int Wh, double invD,
+                                 double beta, double* data, double* l1) {
+  using C = cx<R>;
+  __shared__ double red[32];
+  const int n = blockIdx.x;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+    C acc = part[((size_t)n * G) * NB + b];
+    for (int g = 1; g < G; ++g) acc = cadd(acc, part[((size_t)n * G + g) * NB + b]);
+    const C x = xhat[(size_t)n * NB + b];
+    const double rr = (double)acc.x - (double)x.x, ri = (double)acc.y - (double)x.y;
+    v += bin_weight(b, Wh) * (rr * rr + ri * ri);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
+    data[n] = 0.5 * invD * s;
+    double a = 0.0;
+    for (int g = 0; g < G; ++g) a += sums[((size_t)n * G + g) * kSums];
+    l1[n] = beta * a;
+  }
+}
+
+// ADMM exit (coding.cpp:287-309): lambda = iDFT(lambda_hat) (done by c2r into
+// `lam`), rescale by beta/max|t| when infeasible, dual objective. One CTA/image.
+template <class R>
+__global__ void admm_exit(R* __restrict__ lam, const R* __restrict__ x, const ImageAdmm* img,
+                          int D, double beta, double* dual_obj, double* infeas, int* rescaled) {
+  __shared__ double red[64];
+  const int n = blockIdx.x;
+  const double tinf = img[n].tinf;
+  const bool resc = tinf > beta;
+  const R scale = resc ? R(beta / tinf) : R(1);
+  double a = 0.0, b = 0.0;
+  R* l = lam + (size_t)n * D;
+  const R* xv = x + (size_t)n * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    R v = l[i];
+    if (resc) {
+      v *= scale;
+      l[i] = v;
+    }
+    a += (double)v * (double)v;
+    b += (double)v * (double)xv[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = a;
+    red[32 + (threadIdx.x >> 5)] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      sa += red[w];
+      sb += red[32 + w];
+    }
+    dual_obj[n] = -0.5 * sa - sb;
+    infeas[n] = fmax(0.0, tinf - beta);
+    rescaled[n] = resc ? 1 : 0;
+  }
+}
+
+// sigma(w) = sum_k |d_hat_k(w)|^2 + 1/rho  (coding.cpp:15-21), FP64 accumulation
+template <class R>
+__global__ void sigma_kernel(const cx<R>* __restrict__ dhat, R* __restrict__ sigma, int K, int NB,
+                             double rho) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= NB) return;
+  double s = 1.0 / rho;
+  for (int k = 0; k < K; ++k) {
+    const cx<R> d = dhat[(size_t)k * NB + b];
+    s += (double)d.x * d.x + (double)d.y * d.y;
+  }
+  sigma[b] = R(s);
+}
+
+// Accept coded maps (pipeline.cpp:236-246): for accepted images maps = z_cand
+// (closed form from u); block partials of sum (cand-old)^2 over accepted images,
+// sum maps^2 and the l0 count over all images. grid (chunks, N).
+template <class R, int TB>
+__global__ void __launch_bounds__(TB)
+accept_maps(const R* __restrict__ u, R* __restrict__ maps, const int* __restrict__ accept,
+            size_t per_image, double rho, double beta, double* part_dz, double* part_zz,
+            unsigned long long* l0) {
+  const int n = blockIdx.y;
+  const bool acc = accept[n] != 0;
+  double dz = 0.0, zz = 0.0;
+  unsigned long long cnt = 0;
+  const R rr = R(rho), bb = R(beta);
+  const R* up = u + (size_t)n * per_image;
+  R* mp = maps + (size_t)n * per_image;
+  for (size_t i = (size_t)blockIdx.x * TB + threadIdx.x; i < per_image; i += (size_t)gridDim.x * TB) {
+    R m = mp[i];
+    if (acc) {
+      const R uv = up[i];
+      const R zc = rr * (fmin(fmax(uv, -bb), bb) - uv);
+      const double d = (double)zc - (double)m;
+      dz += d * d;
+      m = zc;
+      mp[i] = m;
+    }
+    zz += (double)m * (double)m;
+    cnt += (m != R(0));
+  }
+  __shared__ double red[2][TB / 32];
+  __shared__ unsigned long long redc[TB / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dz += __shfl_xor_sync(0xffffffffu, dz, o);
+    zz += __shfl_xor_sync(0xffffffffu, zz, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = dz;
+    red[1][threadIdx.x >> 5] = zz;
+    redc[threadIdx.x >> 5] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    unsigned long long c = 0;
+    for (int w = 0; w < TB / 32; ++w) {
+      a += red[0][w];
+      b += red[1][w];
+      c += redc[w];
+    }
+    const size_t slot = (size_t)n * gridDim.x + blockIdx.x;
+    part_dz[slot] = a;
+    part_zz[slot] = b;
+    l0[slot] = c;
+  }
+}
+
+// lambda = -x for the degenerate (all-zero) dictionary (coding.cpp:181-191)
+template <class R>
+__global__ void neg_copy(const R* __restrict__ x, R* __restrict__ lam, size_t total) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) lam[i] = -x[i];
+}
+
+template <class R>
+__global__ void to_real(const double* __restrict__ src, R* __restrict__ dst, size_t total) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) dst[i] = R(src[i]);
+}
+
+}  // namespace dcsc_cuda

@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+The oracle is oracle/_ref/libdcsc_ref.so — the reference's own solver
+translation units compiled here (oracle/Makefile) — on identical seeded inputs.
+Tolerances (BASELINE.json north_star): FP64 <= 1e-9 relative, FP32 <= 1e-4.
+"""
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_1709_09479_b200 import dcsc
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-9
+FP32_TOL = 1e-4
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def problem(N, grid, K, m, p=0.05, sigma=0.01, seed=7, fp32=False):
+    x, _ = dcsc.synth_generate(N, grid, K, m, p, sigma, seed, fp32)
+    d0 = ref.init_dictionary(K, (m, m), grid, seed=3)
+    return x, d0
+
+
+# ---------------------------------------------------------------- FFT
+@pytest.mark.parametrize("H,W", [(16, 16), (16, 20), (20, 20), (64, 64), (100, 100)])
+def test_dft_fp64_matches_reference(H, W):
+    rng = np.random.default_rng(H * 1000 + W)
+    x = rng.standard_normal((3, H, W))
+    g = dcsc.forward_dft2(x, 64)
+    r = np.stack([ref.forward_dft(xi) for xi in x])[..., : W // 2 + 1]
+    assert rel(g.view(np.float64), r.view(np.float64)) <= 1e-13
+    back = dcsc.inverse_dft2(g, W, 64)
+    assert rel(back, x) <= 1e-13
+
+
+@pytest.mark.parametrize("H,W", [(16, 16), (16, 20), (20, 20), (64, 64), (100, 100), (128, 128)])
+def test_dft_fp32_matches_reference(H, W):
+    rng = np.random.default_rng(H * 7 + W)
+    x = rng.standard_normal((4, H, W)).astype(np.float32).astype(np.float64)
+    g = dcsc.forward_dft2(x, 32)
+    r = np.stack([ref.forward_dft(xi) for xi in x])[..., : W // 2 + 1]
+    assert rel(g.view(np.float64), r.view(np.float64)) <= 2e-6
+    back = dcsc.inverse_dft2(r, W, 32)
+    assert rel(back, x) <= 2e-6
+
+
+def test_dft_known_answers():
+    # test_spectral.cpp:15-32: impulse -> all ones; constant c -> (D c, 0, ...)
+    x = np.zeros((1, 16, 20))
+    x[0, 0, 0] = 1.0
+    g = dcsc.forward_dft2(x, 64)
+    assert np.abs(g - 1.0).max() <= 1e-14
+    c = np.full((1, 16, 20), 0.75)
+    g = dcsc.forward_dft2(c, 64)
+    assert abs(g[0, 0, 0] - 0.75 * 320) <= 1e-12
+    g[0, 0, 0] = 0
+    assert np.abs(g).max() <= 1e-12
+
+
+# ---------------------------------------------------------------- coding
+@pytest.mark.parametrize("grid,K,m,beta", [((20, 20), 4, 5, 0.1), ((16, 20), 3, 3, 0.05),
+                                           ((64, 64), 8, 7, 0.5)])
+def test_coding_fp64_matches_reference(grid, K, m, beta):
+    x, d = problem(1, grid, K, m)
+    cfg = ref.Cfg(beta=beta, max_admm=300, normalize=0)
+    z_r, st_r, s_r = ref.solve_coding(x[0], d, cfg)
+    z_g, st_g, s_g = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=beta, max_admm=300, normalize=0), precision=64)
+    assert s_g["admm_iters"] == s_r["admm_iters"]
+    assert s_g["converged"] == s_r["converged"]
+    assert rel(z_g, z_r) <= FP64_TOL
+    assert rel(st_g.theta, st_r[0]) <= FP64_TOL
+    assert rel(st_g.lam, st_r[2]) <= FP64_TOL
+    for key in ("dual_objective", "primal_residual", "z_change", "theta_change"):
+        assert abs(s_g[key] - s_r[key]) <= FP64_TOL * max(abs(s_r[key]), 1e-12) + 1e-13, key
+    assert s_g["dual_rescaled"] == s_r["dual_rescaled"]
+    # warm restart from the returned state (pipeline warm start, coding.hpp:15-25)
+    z_r2, _, s_r2 = ref.solve_coding(x[0], d * 0.9, cfg, st_r)
+    z_g2, _, s_g2 = dcsc.solve_coding(x[0], d * 0.9, dcsc.SolverConfig(beta=beta, max_admm=300, normalize=0),
+                                      st_g, precision=64)
+    assert s_g2["admm_iters"] == s_r2["admm_iters"]
+    assert rel(z_g2, z_r2) <= FP64_TOL
+
+
+def test_coding_degenerate_dictionary():
+    x, d = problem(1, (20, 20), 4, 5)
+    d = np.zeros_like(d)
+    z, st, s = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(normalize=0))
+    assert s["degenerate_dictionary"] and s["converged"]
+    assert np.all(z == 0)
+    assert np.allclose(st.lam, -x[0])
+
+
+def test_coding_fp32_matches_reference():
+    x, d = problem(1, (100, 100), 16, 11, fp32=True)
+    cfg = ref.Cfg(beta=0.5, max_admm=50, normalize=0)
+    z_r, st_r, s_r = ref.solve_coding(x[0], d, cfg)
+    z_g, st_g, s_g = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=0.5, max_admm=50, normalize=0), precision=32)
+    assert abs(s_g["admm_iters"] - s_r["admm_iters"]) <= 1
+    assert rel(z_g, z_r) <= 1e-3  # element-wise maps; the objective below carries the 1e-4 bar
+    og = dcsc.evaluate_objective(x[0], d, z_g, 0.5, precision=64)
+    orf = ref.objective(x[0], d, z_r, 0.5)
+    assert abs(og[2] - orf[2]) <= FP32_TOL * abs(orf[2])
+
+
+# ---------------------------------------------------------------- objective
+def test_objective_fp64_matches_reference():
+    x, d = problem(2, (20, 20), 4, 5)
+    rng = np.random.default_rng(5)
+    z = rng.standard_normal((2, 4, 20, 20)) * (rng.random((2, 4, 20, 20)) < 0.1)
+    with dcsc.Context(2, (20, 20), 4, (5, 5), dcsc.SolverConfig(beta=0.3, normalize=0), 64) as ctx:
+        ctx.set_signals(x)
+        ctx.set_dictionary(d)
+        ctx.set_maps(z)
+        og = ctx.objective()
+        ld = ctx.learning_data_term()
+    for n in range(2):
+        orf = ref.objective(x[n], d, z[n], 0.3)
+        for a, b in zip(og[n], orf):
+            assert abs(a - b) <= FP64_TOL * abs(b)
+    assert abs(ld - (og[0][0] + og[1][0])) <= FP64_TOL * ld
+
+
+# ---------------------------------------------------------------- learning
+def coded_maps(x, d, beta, max_admm=200):
+    cfg = ref.Cfg(beta=beta, max_admm=max_admm, normalize=0)
+    return np.stack([ref.solve_coding(xi, d, cfg)[0] for xi in x])
+
+
+def test_learning_apply_fp64_matches_reference():
+    x, d = problem(3, (16, 20), 4, 5)
+    maps = coded_maps(x, d, 0.1)
+    mu = np.array([1.0, 0.3, 2e-7, 5.0])
+    rng = np.random.default_rng(9)
+    v = rng.standard_normal(x.shape)
+    out_r = ref.learning_apply(maps, (5, 5), mu, 1e-6, v)
+    with dcsc.Context(3, (16, 20), 4, (5, 5), dcsc.SolverConfig(normalize=0), 64) as ctx:
+        ctx.set_signals(x)
+        ctx.set_maps(maps)
+        out_g = ctx.learning_apply(mu, v)
+    assert rel(out_g, out_r) <= 1e-12
+
+
+@pytest.mark.parametrize("grid,N,K,m", [((20, 20), 3, 4, 5), ((16, 20), 2, 3, 3)])
+def test_learning_fp64_matches_reference(grid, N, K, m):
+    x, d = problem(N, grid, K, m)
+    maps = coded_maps(x, d, 0.1)
+    cfg = ref.Cfg(beta=0.1, normalize=0)
+    d_r, st_r, s_r = ref.solve_learning(x, maps, (m, m), cfg)
+    d_g, st_g, s_g = dcsc.solve_learning(x, maps, (m, m), dcsc.SolverConfig(beta=0.1, normalize=0), precision=64)
+    assert s_g["mu_iters"] == s_r["mu_iters"]
+    assert abs(s_g["cg_iters"] - s_r["cg_iters"]) <= max(2, 0.02 * s_r["cg_iters"])
+    assert rel(d_g, d_r) <= 1e-7
+    assert rel(st_g.mu, st_r[1]) <= 1e-7
+    # warm second solve
+    d_r2, _, s_r2 = ref.solve_learning(x, maps * 1.1, (m, m), cfg, st_r)
+    d_g2, _, s_g2 = dcsc.solve_learning(x, maps * 1.1, (m, m), dcsc.SolverConfig(beta=0.1, normalize=0), st_g,
+                                        precision=64)
+    assert rel(d_g2, d_r2) <= 1e-7
+
+
+def test_learning_degenerate_zero_maps():
+    x, d = problem(2, (20, 20), 4, 5)
+    d_g, _, s = dcsc.solve_learning(x, np.zeros((2, 4, 20, 20)), (5, 5), dcsc.SolverConfig(normalize=0))
+    assert s["degenerate"] and np.all(d_g == 0)
+
+
+# ---------------------------------------------------------------- full run
+def compare_runs(g, r, tol):
+    tg, tr = g["trace"], r["trace"]
+    assert len(tg) == len(tr)
+    for a, b in zip(tg, tr):
+        assert a["phase"] == b["phase"]
+        for key in ("total", "data_term", "l1_term"):
+            assert abs(a[key] - b[key]) <= tol * abs(b[key]) + 1e-300, (a, b, key)
+
+
+def test_run_fp64_small_matches_reference():
+    x, _ = problem(3, (20, 20), 6, 5, p=0.05)
+    cfg = ref.Cfg(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
+    r = ref.run(x, 6, (5, 5), cfg)
+    g = dcsc.run_csc(x, 6, (5, 5), dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300),
+                     precision=64)
+    compare_runs(g, r, 1e-8)
+    for a, b in zip(g["trace"], r["trace"]):
+        assert a["admm_iters"] == b["admm_iters"]
+        assert a["mu_iters"] == b["mu_iters"]
+    assert rel(g["dict"], r["dict"]) <= 1e-7
