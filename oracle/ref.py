@@ -221,3 +221,18 @@ def run_csc(xs, K, support, cfg: Cfg):
                              _p(dfin), _p(maps)))
     trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(n_rows.value)]
     return {"trace": trace, "dict": dfin, "maps": maps}
+
+
+def coding_batch(xs, d, cfg: Cfg, want_maps=False):
+    """solve_coding over all images, OpenMP-parallel over images (pipeline.cpp:221-227)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    N, H, W = xs.shape
+    K, mh, mw = d.shape
+    iters = np.zeros(N, dtype=np.int32)
+    maps = np.zeros((N, K, H, W)) if want_maps else None
+    c = cfg.c()
+    _check(lib().ref_coding_batch(N, H, W, _p(xs), K, mh, mw, _p(d), C.byref(c),
+                                  _p(maps) if want_maps else None,
+                                  iters.ctypes.data_as(C.POINTER(C.c_int))))
+    return iters, maps

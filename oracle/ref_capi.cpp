@@ -218,6 +218,28 @@ int ref_solve_coding(int H, int W, const double* x, int K, int mh, int mw, const
   });
 }
 
+// solve_coding over N images from the empty state, OpenMP-parallel over
+// images exactly as run_csc's coding half-step (pipeline.cpp:221-227).
+// Used by bench.py as the reference CPU arm. iters_out: per-image ADMM iterations.
+int ref_coding_batch(int N, int H, int W, const double* xs, int K, int mh, int mw,
+                     const double* d, const ref_cfg* cfg, double* maps_out, int* iters_out) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    const Dictionary dict = make_dict(K, mh, mw, d);
+    const SolverConfig sc = to_cfg(cfg);
+    std::vector<SignalTensor> sig;
+    for (int n = 0; n < N; ++n) sig.push_back(make_signal(H, W, xs + n * D));
+    std::vector<SparseMaps> out(N);
+    std::vector<CodingStats> st(N);
+    std::vector<CodingDualState> state(N);
+    par::parallel_for(N, [&](std::int64_t n) { out[n] = solve_coding(sig[n], dict, sc, state[n], &st[n]); });
+    for (int n = 0; n < N; ++n) {
+      if (iters_out) iters_out[n] = st[n].admm_iters;
+      if (maps_out) std::copy(out[n].values.begin(), out[n].values.end(), maps_out + n * K * D);
+    }
+  });
+}
+
 // One solve_learning call over N images. gamma (N*D) / mu (K) are in/out warm
 // state; warm = 0 starts from the empty state. d_out receives K*M values.
 int ref_solve_learning(int N, int H, int W, const double* xs, int K, const double* maps, int mh,

@@ -470,6 +470,11 @@ class Engine final : public EngineBase {
   void set_coding_state(int n0, int n1, const double* theta, const double* z) override {
     check_range(n0, n1);
     const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    if (!theta && !z) {  // the reference's empty state (coding.cpp:175-179): device-side reset
+      CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * cnt, st_));
+      CK(cudaMemsetAsync(lam_.as<R>() + (size_t)n0 * D, 0, sizeof(R) * (size_t)(n1 - n0) * D, st_));
+      return;
+    }
     std::vector<R> u(cnt);
     const double inv_rho = 1.0 / cfg_.rho;
     for (size_t i = 0; i < cnt; ++i) u[i] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
