@@ -254,6 +254,8 @@ def run_ours(args, cfg):
     ms = ctx.event_elapsed(0, 1)
     launches = ctx.kernel_launches() - l0
     cod_ms, cod_n = ctx.kernel_time(0)
+    fam_names = ["coding_pass_admm", "lambda_update", "learning_contract", "learning_mask", "other"]
+    fam_ms = {fam_names[f]: round(ctx.kernel_time(f)[0] / args.steps, 3) for f in range(5)}
     if dist:
         import torch
         t = torch.tensor([ms], device="cuda")
@@ -293,6 +295,7 @@ def run_ours(args, cfg):
         "config": config_block(cfg, args),
         "e2e": {"value": e2e * 1.0, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
+        "kernel_ms_per_step": fam_ms,
     }
     if cod_n:
         avg = cod_ms / cod_n

@@ -1,0 +1,228 @@
+// dcsc_cuda.hpp — header-only C++ wrapper that restores the reference solver
+// signatures (namespace dcsc, /root/reference/proj/include/dcsc/*.hpp) over the
+// C-ABI in dcsc_cuda.h, rethrowing the reference exception types.
+//
+// A reference user includes this after the reference headers and swaps
+//   dcsc::solve_coding   -> dcsc::cuda::solve_coding     (coding.hpp:74-77)
+//   dcsc::solve_learning -> dcsc::cuda::solve_learning   (learning.hpp:99-104)
+//   dcsc::run_csc        -> dcsc::cuda::run_csc          (pipeline.hpp:58)
+// Precision defaults to FP64 (the reference's arithmetic); FP32 is opt-in.
+// Grid support: 2-D, single channel (J = 1), sizes compiled into the library
+// (dcsc_cuda_supported_grid); anything else throws dcsc::DimensionError.
+#pragma once
+
+#include <cmath>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dcsc/coding.hpp"
+#include "dcsc/learning.hpp"
+#include "dcsc/pipeline.hpp"
+#include "dcsc/types.hpp"
+#include "dcsc_cuda.h"
+
+namespace dcsc::cuda {
+
+inline void check(int rc) {
+  if (rc == DCSC_OK) return;
+  char buf[2048];
+  dcsc_cuda_last_error(buf, sizeof(buf));
+  switch (rc) {
+    case DCSC_ERR_DIMENSION: throw DimensionError(buf);
+    case DCSC_ERR_NUMERIC: throw NumericError(buf);
+    case DCSC_ERR_INVALID: throw std::invalid_argument(buf);
+    default: throw std::runtime_error(std::string("CUDA: ") + buf);
+  }
+}
+
+inline dcsc_solver_config to_c(const SolverConfig& c) {
+  dcsc_solver_config o{};
+  o.beta = c.beta;
+  o.rho = c.rho;
+  o.tol = c.tol;
+  o.max_outer = c.max_outer;
+  o.max_admm = c.max_admm;
+  o.max_mu_iters = c.max_mu_iters;
+  o.cg_tol = c.cg_tol;
+  o.cg_max = c.cg_max;
+  o.mu_floor = c.mu_floor;
+  o.seed = c.seed;
+  o.normalize = c.normalize == NormalizeMode::None ? 0 : (c.normalize == NormalizeMode::Global ? 1 : 2);
+  return o;
+}
+
+struct Options {
+  int precision = 64;
+  int device = 0;
+};
+
+class Context {
+ public:
+  Context(int n_images, const GridDims& dims, int filters, const GridDims& support,
+          const SolverConfig& cfg, Options opt = {}) {
+    if (dims.size() != 2 || support.size() != 2)
+      throw DimensionError("dcsc::cuda supports 2-D grids only");
+    dcsc_cuda_opts o{};
+    o.n_images = n_images;
+    o.height = dims[0];
+    o.width = dims[1];
+    o.filters = filters;
+    o.support_h = support[0];
+    o.support_w = support[1];
+    o.precision = opt.precision;
+    o.device = opt.device;
+    o.cfg = to_c(cfg);
+    dcsc_cuda_ctx* c = nullptr;
+    check(dcsc_cuda_create(&o, &c));
+    ctx_.reset(c);
+  }
+  dcsc_cuda_ctx* get() const { return ctx_.get(); }
+
+ private:
+  struct Del {
+    void operator()(dcsc_cuda_ctx* c) const { dcsc_cuda_destroy(c); }
+  };
+  std::unique_ptr<dcsc_cuda_ctx, Del> ctx_;
+};
+
+inline CodingStats to_stats(const dcsc_coding_stats& s) {
+  CodingStats o;
+  o.admm_iters = s.admm_iters;
+  o.converged = s.converged != 0;
+  o.degenerate_dictionary = s.degenerate_dictionary != 0;
+  o.dual_rescaled = s.dual_rescaled != 0;
+  o.primal_residual = s.primal_residual;
+  o.theta_change = s.theta_change;
+  o.z_change = s.z_change;
+  o.dual_objective = s.dual_objective;
+  o.dual_infeasibility = s.dual_infeasibility;
+  return o;
+}
+
+// solve_coding (coding.hpp:74-77): one single-channel signal, warm state in/out.
+inline SparseMaps solve_coding(const SignalTensor& x, const Dictionary& d, const SolverConfig& cfg,
+                               CodingDualState& state, CodingStats* stats = nullptr,
+                               Options opt = {}) {
+  cfg.validate();
+  x.validate();
+  d.validate();
+  if (x.channels != 1)
+    throw DimensionError("solve_coding expects a single-channel signal; use the TCSC path");
+  if (d.channels != 1) throw DimensionError("solve_coding expects a single-channel dictionary");
+  SolverConfig c = cfg;
+  c.normalize = NormalizeMode::None;  // solve_coding never normalises
+  Context ctx(1, x.dims, d.filters, d.support, c, opt);
+  check(dcsc_cuda_set_signals(ctx.get(), x.values.data()));
+  check(dcsc_cuda_set_dictionary(ctx.get(), d.values.data()));
+  const std::size_t kd = static_cast<std::size_t>(d.filters) * x.grid_count();
+  if (state.z.size() == kd && state.theta.size() == kd)
+    check(dcsc_cuda_set_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data()));
+  dcsc_coding_stats s{};
+  check(dcsc_cuda_coding(ctx.get(), 0, 1, &s));
+  state.theta.assign(kd, 0.0);
+  state.z.assign(kd, 0.0);
+  state.lambda.assign(x.grid_count(), 0.0);
+  check(dcsc_cuda_get_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data(),
+                                   state.lambda.data()));
+  if (stats) *stats = to_stats(s);
+  SparseMaps maps(d.filters, x.dims);
+  maps.values = state.z;
+  return maps;
+}
+
+// solve_learning (learning.hpp:99-104), J = 1.
+inline Dictionary solve_learning(std::span<const SignalTensor> xs, std::span<const SparseMaps> zs,
+                                 const GridDims& support, const SolverConfig& cfg,
+                                 LearningDualState& state, LearningStats* stats = nullptr,
+                                 Options opt = {}) {
+  cfg.validate();
+  if (xs.empty() || xs.size() != zs.size())
+    throw DimensionError("solve_learning: need one sparse map set per image");
+  const int N = static_cast<int>(xs.size());
+  const int K = zs.front().maps;
+  const GridDims dims = xs.front().dims;
+  const std::size_t D = grid_count(dims);
+  SolverConfig c = cfg;
+  c.normalize = NormalizeMode::None;
+  Context ctx(N, dims, K, support, c, opt);
+  std::vector<double> x(N * D), z(static_cast<std::size_t>(N) * K * D);
+  for (int n = 0; n < N; ++n) {
+    if (xs[n].channels != 1) throw DimensionError("dcsc::cuda::solve_learning supports J = 1");
+    std::copy(xs[n].values.begin(), xs[n].values.end(), x.begin() + n * D);
+    std::copy(zs[n].values.begin(), zs[n].values.end(), z.begin() + static_cast<std::size_t>(n) * K * D);
+  }
+  check(dcsc_cuda_set_signals(ctx.get(), x.data()));
+  check(dcsc_cuda_set_maps(ctx.get(), 0, N, z.data()));
+  const bool warm_g = state.gamma.size() == 1 && state.gamma[0].size() == N * D;
+  const bool warm_m = state.mu.size() == static_cast<std::size_t>(K);
+  check(dcsc_cuda_set_learning_state(ctx.get(), warm_g ? state.gamma[0].data() : nullptr,
+                                     warm_m ? state.mu.data() : nullptr));
+  Dictionary dict(K, support, 1);
+  dcsc_learning_stats s{};
+  check(dcsc_cuda_learning(ctx.get(), dict.values.data(), &s));
+  state.gamma.assign(1, std::vector<double>(N * D));
+  state.mu.assign(K, 1.0);
+  check(dcsc_cuda_get_learning_state(ctx.get(), state.gamma[0].data(), state.mu.data()));
+  state.mu_iters_total += s.mu_iters;
+  state.cg_iters_total += s.cg_iters;
+  if (stats) {
+    LearningStats o;
+    o.mu_iters = s.mu_iters;
+    o.cg_iters = s.cg_iters;
+    o.cg_iters_first = s.cg_iters_first;
+    o.converged = s.converged != 0;
+    o.degenerate = s.degenerate != 0;
+    o.mu_clamped = s.mu_clamped != 0;
+    o.cg_budget_hit = s.cg_budget_hit != 0;
+    o.rescaled_filters = s.rescaled_filters;
+    *stats = o;
+  }
+  return dict;
+}
+
+// run_csc (pipeline.hpp:58): the whole alternating loop device-resident.
+inline RunResult run_csc(const RunConfig& cfg, const Dataset& data, Options opt = {}) {
+  if (data.signals.empty()) throw std::invalid_argument("dataset is empty");
+  const GridDims dims = data.signals.front().dims;
+  for (const SignalTensor& s : data.signals) {
+    s.validate();
+    if (s.dims != dims || s.channels != 1)
+      throw DimensionError("all dataset signals must share dims (J = 1 on the CUDA path)");
+  }
+  cfg.validate(dims, 1);
+  const int N = static_cast<int>(data.signals.size());
+  const std::size_t D = grid_count(dims);
+  Context ctx(N, dims, cfg.filters, cfg.support, cfg.solver, opt);
+  std::vector<double> x(N * D);
+  for (int n = 0; n < N; ++n) std::copy(data.signals[n].values.begin(), data.signals[n].values.end(), x.begin() + n * D);
+  check(dcsc_cuda_set_signals(ctx.get(), x.data()));
+  RunResult r;
+  std::vector<dcsc_trace_row> rows(2 * std::max(cfg.solver.max_outer, 1));
+  int n_rows = 0, conv = 0;
+  check(dcsc_cuda_run(ctx.get(), cfg.solver.max_outer, rows.data(), &n_rows, &conv));
+  for (int i = 0; i < n_rows; ++i) {
+    TraceRow t;
+    t.outer_iter = rows[i].outer_iter;
+    t.phase = rows[i].phase == 0 ? Phase::Coding : Phase::Learning;
+    t.objective = {rows[i].data_term, rows[i].l1_term, rows[i].total, rows[i].residual_norm};
+    t.admm_iters = rows[i].admm_iters;
+    t.cg_iters = rows[i].cg_iters;
+    t.elapsed_ms = rows[i].elapsed_ms;
+    r.trace.rows.push_back(t);
+  }
+  r.converged = conv != 0;
+  r.outer_iters = n_rows / 2;
+  r.dict = Dictionary(cfg.filters, cfg.support, 1);
+  check(dcsc_cuda_get_dictionary(ctx.get(), r.dict.values.data()));
+  r.maps.assign(N, SparseMaps(cfg.filters, dims));
+  std::vector<double> z(static_cast<std::size_t>(N) * cfg.filters * D);
+  check(dcsc_cuda_get_maps(ctx.get(), 0, N, z.data()));
+  for (int n = 0; n < N; ++n)
+    std::copy(z.begin() + static_cast<std::size_t>(n) * cfg.filters * D,
+              z.begin() + static_cast<std::size_t>(n + 1) * cfg.filters * D, r.maps[n].values.begin());
+  return r;
+}
+
+}  // namespace dcsc::cuda

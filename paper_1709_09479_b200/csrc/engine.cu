@@ -220,17 +220,30 @@ class Engine final : public EngineBase {
     CK(cudaSetDevice(o.device));
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     CK(cudaMallocHost(&pin_, 1 << 20));
-    // filter groups: at least ~4 CTAs per SM-wave of work when N is small
-    kpg_ = K_;
-    {
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
-      const int target = 4 * sms;
-      int G = std::max(1, std::min(K_, (target + N_ - 1) / N_));
-      kpg_ = (K_ + G - 1) / G;
-    }
-    G_ = (K_ + kpg_ - 1) / kpg_;
     setup_attributes();
+    // Filter groups per image: a CTA runs kpg filters; pick G minimising the
+    // makespan ceil(N*G / slots) * ceil(K/G) (wave quantisation), ties -> fewer
+    // groups (less partial-spectrum traffic).
+    {
+      int sms = 148, per_sm = 1;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coding_pass<P, kPassAdmm>, T, Smem<P>::coding));
+      const long slots = (long)sms * std::max(per_sm, 1);
+      long best = -1;
+      int bestG = 1;
+      for (int G = 1; G <= K_; ++G) {
+        const int kpg = (K_ + G - 1) / G;
+        if ((K_ + kpg - 1) / kpg != G) continue;  // G must be realisable
+        const long waves = ((long)N_ * G + slots - 1) / slots;
+        const long span = waves * kpg;
+        if (best < 0 || span < best) {
+          best = span;
+          bestG = G;
+        }
+      }
+      kpg_ = (K_ + bestG - 1) / bestG;
+      G_ = bestG;
+    }
     // twiddles (forward roots) in long double, rounded once
     std::vector<C> tw(P::TW_LEN);
     auto fill = [&](int off, int L) {
@@ -293,6 +306,7 @@ class Engine final : public EngineBase {
     CK(cudaMemsetAsync(x_.p, 0, x_.bytes, st_));
     CK(cudaMemsetAsync(xhat_.p, 0, xhat_.bytes, st_));
     dict_.assign((size_t)K_ * M_, 0.0);
+    u_zero_.assign(N_, 1);
     mu_.assign(K_, 1.0);
     xnorm2_.assign(N_, 0.0);
     CK(cudaStreamSynchronize(st_));
@@ -458,6 +472,7 @@ class Engine final : public EngineBase {
     CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
     CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
     CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    u_zero_.assign(N_, 1);
     mu_.assign(K_, 1.0);
     zhat_valid_ = false;
     CK(cudaStreamSynchronize(st_));
@@ -471,10 +486,12 @@ class Engine final : public EngineBase {
     check_range(n0, n1);
     const size_t cnt = (size_t)(n1 - n0) * K_ * D;
     if (!theta && !z) {  // the reference's empty state (coding.cpp:175-179): device-side reset
+      std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
       CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * cnt, st_));
       CK(cudaMemsetAsync(lam_.as<R>() + (size_t)n0 * D, 0, sizeof(R) * (size_t)(n1 - n0) * D, st_));
       return;
     }
+    std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
     std::vector<R> u(cnt);
     const double inv_rho = 1.0 / cfg_.rho;
     for (size_t i = 0; i < cnt; ++i) u[i] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
@@ -507,6 +524,7 @@ class Engine final : public EngineBase {
     std::vector<dcsc_coding_stats> out(cnt);
     if (dict_zero_) {
       // degenerate dictionary: z = theta = 0, lambda = -x (coding.cpp:181-191)
+      std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
       CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * (size_t)cnt * K_ * D, st_));
       const size_t tot = (size_t)cnt * D;
       launch(kFamOther, [&] {
@@ -533,8 +551,14 @@ class Engine final : public EngineBase {
     CK(cudaMemsetAsync(conv_.as<int>() + n0, 0, sizeof(int) * cnt, st_));
     CK(cudaMemsetAsync(img_.as<ImageAdmm>() + n0, 0, sizeof(ImageAdmm) * cnt, st_));
     const dim3 lgrid((NB + 255) / 256, cnt);
-    // initial lambda_hat from the warm state (the first assemble_w, coding.cpp:216-229)
-    coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);
+    // initial lambda_hat from the warm state (the first assemble_w, coding.cpp:216-229);
+    // a zero state has w_hat = 0, so the FFT pass is skipped and part is zeroed
+    const bool all_zero = std::all_of(u_zero_.begin() + n0, u_zero_.begin() + n1, [](char v) { return v != 0; });
+    if (all_zero)
+      CK(cudaMemsetAsync(part_.as<C>() + (size_t)n0 * G_ * NB, 0, sizeof(C) * (size_t)cnt * G_ * NB, st_));
+    else
+      coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);
+    std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
     auto lam_update = [&](int iter, int last, int prologue) {
       launch(kFamLambda, [&] {
         lambda_update<R><<<lgrid, 256, 0, st_>>>(part_.as<C>() + (size_t)n0 * G_ * NB,
@@ -1078,6 +1102,7 @@ class Engine final : public EngineBase {
       partial_, partial2_, l0_, zhat_;
   std::vector<double> dict_, mu_, xnorm2_, xs_host_;
   std::vector<int> live_h_;
+  std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero
   bool dict_zero_ = false, zhat_valid_ = false, profiling_ = false;
   std::vector<Prof> prof_;
   std::vector<cudaEvent_t> marks_;

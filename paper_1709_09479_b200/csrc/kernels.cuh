@@ -34,6 +34,11 @@ struct CodingArgs {
   const cx<R>* tw;      // twiddle table (global)
 };
 
+// Bulk prefetch of a contiguous global range into L2 (sm_90+ TMA engine op).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <class P>
 struct Smem {
   static constexpr size_t tw_bytes = sizeof(typename P::C) * P::TW_LEN;
@@ -84,25 +89,61 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     if constexpr (MODE == kPassAdmm) {
       R* __restrict__ uk = a.u + ((size_t)n * a.K + k) * D;
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
-      for (int it = threadIdx.x; it < P::HALF; it += T) {
-        const int r = it / W2, c = it % W2;
-        const int b = r * Wh + c;
-        if (c == 0) {
-          const C t0 = cmulc(dk[b], lam[b]);
-          const C tn = cmulc(dk[b + W2], lam[b + W2]);
-          B0[b] = P::pack_col0(t0, tn);
-        } else {
-          B0[b] = cmulc(dk[b], lam[b]);
+      if (threadIdx.x == 0) {
+        prefetch_l2_bulk(uk, sizeof(R) * D);  // this filter's state, consumed after the inverse FFT
+        if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
+      }
+      constexpr int U = 4;
+      for (int base = 0; base < P::HALF; base += T * U) {
+        C dv[U], lv[U], dn[U], ln[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int it = base + q * T + threadIdx.x;
+          if (it < P::HALF) {
+            const int r = it / W2, c = it % W2;
+            const int b = r * Wh + c;
+            dv[q] = __ldg(dk + b);
+            lv[q] = __ldg(lam + b);
+            if (c == 0) {
+              dn[q] = __ldg(dk + b + W2);
+              ln[q] = __ldg(lam + b + W2);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int it = base + q * T + threadIdx.x;
+          if (it < P::HALF) {
+            const int r = it / W2, c = it % W2;
+            const int b = r * Wh + c;
+            const C t0 = cmulc(dv[q], lv[q]);
+            B0[b] = (c == 0) ? P::pack_col0(t0, cmulc(dn[q], ln[q])) : t0;
+          }
         }
       }
       __syncthreads();
       C* sp = P::inverse(B0, B1, TW);
-      for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
+      constexpr int UP = 4;
+      for (int base = 0; base < (H / 2) * W; base += T * UP) {
+       R ua[UP], ub[UP];
+#pragma unroll
+       for (int q = 0; q < UP; ++q) {
+         const int it = base + q * T + threadIdx.x;
+         if (it < (H / 2) * W) {
+           const int pa = it / W, c = it % W;
+           ua[q] = uk[(2 * pa) * W + c];
+           ub[q] = uk[(2 * pa + 1) * W + c];
+         }
+       }
+#pragma unroll
+       for (int q = 0; q < UP; ++q) {
+        const int it = base + q * T + threadIdx.x;
+        if (it >= (H / 2) * W) continue;
         const int pa = it / W, c = it % W;
         const C v = sp[pa * RLS + c];
         R* up = uk + (2 * pa) * W + c;
         const R tv[2] = {v.x * invD, v.y * invD};
-        const R uo[2] = {up[0], up[W]};
+        const R uo[2] = {ua[q], ub[q]};
         R wv[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -125,6 +166,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
           if (e == 0) up[0] = un; else up[W] = un;
         }
         sp[pa * RLS + c] = mk<C>(wv[0], wv[1]);
+       }
       }
       __syncthreads();
       work = sp;
@@ -154,16 +196,33 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     }
     C* other = (work == B0) ? B1 : B0;
     C* spec = P::forward(work, other, TW);
-    for (int it = threadIdx.x; it < P::HALF; it += T) {
-      const int r = it / W2, c = it % W2;
-      const int b = r * Wh + c;
-      if (c == 0) {
-        C x0, xn;
-        P::unpack_col0(spec, r, x0, xn);
-        ACC[b] = cadd(ACC[b], cmul(dk[b], x0));
-        ACC[b + W2] = cadd(ACC[b + W2], cmul(dk[b + W2], xn));
-      } else {
-        ACC[b] = cadd(ACC[b], cmul(dk[b], spec[b]));
+    constexpr int UA = 4;
+    for (int base = 0; base < P::HALF; base += T * UA) {
+      C dv[UA], dn[UA];
+#pragma unroll
+      for (int q = 0; q < UA; ++q) {
+        const int it = base + q * T + threadIdx.x;
+        if (it < P::HALF) {
+          const int r = it / W2, c = it % W2;
+          const int b = r * Wh + c;
+          dv[q] = __ldg(dk + b);
+          if (c == 0) dn[q] = __ldg(dk + b + W2);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UA; ++q) {
+        const int it = base + q * T + threadIdx.x;
+        if (it >= P::HALF) continue;
+        const int r = it / W2, c = it % W2;
+        const int b = r * Wh + c;
+        if (c == 0) {
+          C x0, xn;
+          P::unpack_col0(spec, r, x0, xn);
+          ACC[b] = cadd(ACC[b], cmul(dv[q], x0));
+          ACC[b + W2] = cadd(ACC[b + W2], cmul(dn[q], xn));
+        } else {
+          ACC[b] = cadd(ACC[b], cmul(dv[q], spec[b]));
+        }
       }
     }
     __syncthreads();
