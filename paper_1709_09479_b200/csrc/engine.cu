@@ -222,8 +222,9 @@ class Engine final : public EngineBase {
     CK(cudaMallocHost(&pin_, 1 << 20));
     setup_attributes();
     // Filter groups per image: a CTA runs kpg filters; pick G minimising the
-    // makespan ceil(N*G / slots) * ceil(K/G) (wave quantisation), ties -> fewer
-    // groups (less partial-spectrum traffic).
+    // makespan ceil(N*G / slots) * (ceil(K/G) + 1): wave quantisation plus a
+    // per-CTA overhead of about one filter's worth (partial spectrum write and
+    // re-read, twiddles, the epilogue). Ties -> fewer groups.
     {
       int sms = 148, per_sm = 1;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
@@ -235,7 +236,7 @@ class Engine final : public EngineBase {
         const int kpg = (K_ + G - 1) / G;
         if ((K_ + kpg - 1) / kpg != G) continue;  // G must be realisable
         const long waves = ((long)N_ * G + slots - 1) / slots;
-        const long span = waves * kpg;
+        const long span = waves * (kpg + 1);
         if (best < 0 || span < best) {
           best = span;
           bestG = G;
@@ -270,6 +271,8 @@ class Engine final : public EngineBase {
     part_.alloc(sizeof(C) * (size_t)N_ * G_ * NB);
     sums_.alloc(sizeof(double) * (size_t)N_ * G_ * kSums);
     conv_.alloc(sizeof(int) * N_);
+    cnt_.alloc(sizeof(unsigned) * N_);
+    CK(cudaMemset(cnt_.p, 0, cnt_.bytes));
     img_.alloc(sizeof(ImageAdmm) * N_);
     dual_.alloc(sizeof(double) * N_);
     infeas_.alloc(sizeof(double) * N_);
@@ -373,12 +376,22 @@ class Engine final : public EngineBase {
     a.rho = R(cfg_.rho);
     a.beta = R(cfg_.beta);
     a.tw = dtw_.as<C>();
+    a.cnt = cnt_.as<unsigned>() + n_off;
+    a.conv_w = conv_.as<int>() + n_off;
+    a.xhat = xhat_.as<C>() + (size_t)n_off * NB;
+    a.sigma = sigma_.as<R>();
+    a.lamhat_w = lamhat_.as<C>() + (size_t)n_off * NB;
+    a.img = img_.as<ImageAdmm>() + n_off;
+    a.iter = 0;
+    a.is_last = 0;
     return a;
   }
 
   template <int MODE>
-  void coding_launch(const C* dhat, int n0, int cnt) {
+  void coding_launch(const C* dhat, int n0, int cnt, int iter = 0, int is_last = 0) {
     CodingArgs<R> a = cargs(dhat, n0);
+    a.iter = iter;
+    a.is_last = is_last;
     launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] {
       coding_pass<P, MODE><<<dim3(G_, cnt), T, Smem<P>::coding, st_>>>(a);
     });
@@ -557,7 +570,7 @@ class Engine final : public EngineBase {
     if (all_zero)
       CK(cudaMemsetAsync(part_.as<C>() + (size_t)n0 * G_ * NB, 0, sizeof(C) * (size_t)cnt * G_ * NB, st_));
     else
-      coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);
+      coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);  // lambda_hat from the fused epilogue
     std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
     auto lam_update = [&](int iter, int last, int prologue) {
       launch(kFamLambda, [&] {
@@ -569,14 +582,13 @@ class Engine final : public EngineBase {
                                                  prologue);
       });
     };
-    lam_update(0, 0, 1);
+    if (all_zero) lam_update(0, 0, 1);
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     int pending = -1;  // iteration whose conv flags are in flight
     for (int it = 1; it <= cfg_.max_admm; ++it) {
-      coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt);
-      lam_update(it, it == cfg_.max_admm, 0);
+      coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
       if (pending >= 0) {
         // one-iteration look-ahead: iteration `it` is queued before we wait on it-1
         CK(cudaEventSynchronize(ev[pending & 1]));
@@ -1098,7 +1110,7 @@ class Engine final : public EngineBase {
   cudaStream_t st_ = nullptr;
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
-      infeas_, resc_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
+      infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
       partial_, partial2_, l0_, zhat_;
   std::vector<double> dict_, mu_, xnorm2_, xs_host_;
   std::vector<int> live_h_;

@@ -236,6 +236,21 @@ template <int NSTAGES> struct Parity { static constexpr bool odd = NSTAGES & 1; 
 template <class L> struct CountStages;
 template <int... Rs> struct CountStages<RadixList<Rs...>> { static constexpr int value = sizeof...(Rs); };
 
+template <int R, class L> struct Prepend;
+template <int R, int... Rs> struct Prepend<R, RadixList<Rs...>> { using type = RadixList<R, Rs...>; };
+template <class L> struct Split;
+template <int R> struct Split<RadixList<R>> {
+  static constexpr int first = R, last = R;
+  using tail = RadixList<>;
+  using init = RadixList<>;
+};
+template <int R, int R2, int... Rs> struct Split<RadixList<R, R2, Rs...>> {
+  using rest = Split<RadixList<R2, Rs...>>;
+  static constexpr int first = R, last = rest::last;
+  using tail = RadixList<R2, Rs...>;
+  using init = typename Prepend<R, typename rest::init>::type;
+};
+
 // ---------------------------------------------------------------- 2-D plane
 template <class Rt, int H_, int W_, int T_>
 struct Plane {
@@ -341,10 +356,77 @@ struct Plane {
     return rows<true>(o, c, tw);
   }
 
+  // ---- fused column stages (coding hot loop) ----
+  // Inverse column pass whose first Stockham stage generates its input on the
+  // fly: gen(r, c) returns natural bin (r, c); column 0 packs (r,0)+(r,W/2).
+  // Writes the first stage into `a`, runs the rest ping-pong; returns result.
+  template <class GEN>
+  __device__ static __forceinline__ C* cols_inv_generated(C* a, C* b, const C* tw, GEN&& gen) {
+    using S = Split<ColPlan>;
+    constexpr int R = S::first, J = H / R, LINES = W / 2, ITEMS = LINES * J;
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += T) {
+      const int col = it % LINES, j = it / LINES;
+      C x[R];
+      if (col == 0) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = pack_col0(gen(j + q * J, 0), gen(j + q * J, W / 2));
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = gen(j + q * J, col);
+      }
+      dft<R, true>(x);
+#pragma unroll
+      for (int s = 0; s < R; ++s) a[(j * R + s) * Wh + col] = x[s];
+    }
+    __syncthreads();
+    return run_stages<C, H, true, W / 2, Wh, 1, T, R>(a, b, tw_col(tw), typename S::tail{});
+  }
+
+  // Forward column pass whose last Stockham stage hands each output to
+  // cons(r, col, value, pre) instead of storing it; pre = prefetch(r, col) is
+  // issued before the stage's smem reads. Column 0 outputs (the packed pair
+  // spectrum Y) go to col0[r]; the caller unpacks them after a sync.
+  template <class PRE, class CONS>
+  __device__ static __forceinline__ void cols_fwd_consumed(C* a, C* b, const C* tw, C* col0, PRE&& pre,
+                                                          CONS&& cons) {
+    using S = Split<ColPlan>;
+    constexpr int R = S::last, NS = H / R, J = H / R, LINES = W / 2, ITEMS = LINES * J;
+    C* in = run_stages<C, H, false, W / 2, Wh, 1, T, 1>(a, b, tw_col(tw), typename S::init{});
+    const C* twc = tw_col(tw);
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += T) {
+      const int col = it % LINES, j = it / LINES;  // j < NS: outputs rows j + s*NS
+      using PT = decltype(pre(0, 1));
+      PT pv[R];
+      if (col != 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) pv[s] = pre(j + s * NS, col);
+      }
+      C x[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[q] = in[(j + q * J) * Wh + col];
+      if constexpr (NS > 1) {
+#pragma unroll
+        for (int q = 1; q < R; ++q) x[q] = cmul(x[q], twc[q * j * (H / (NS * R))]);
+      }
+      dft<R, false>(x);
+      if (col == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) col0[j + s * NS] = x[s];
+      } else {
+#pragma unroll
+        for (int s = 0; s < R; ++s) cons(j + s * NS, col, x[s], pv[s]);
+      }
+    }
+    __syncthreads();
+  }
+
   // Natural bins (r,0) and (r,W/2) from a forward PCL column 0.
+  template <int STRIDE = Wh>
   __device__ static __forceinline__ void unpack_col0(const C* pcl, int r, C& x0, C& xn) {
-    const C y = pcl[r * Wh];
-    const C ym = pcl[((H - r) % H) * Wh];
+    const C y = pcl[r * STRIDE];
+    const C ym = pcl[((H - r) % H) * STRIDE];
     x0 = mk<C>(R(0.5) * (y.x + ym.x), R(0.5) * (y.y - ym.y));
     xn = mk<C>(R(0.5) * (y.y + ym.y), R(0.5) * (ym.x - y.x));
   }

@@ -20,6 +20,13 @@ enum PassMode : int {
 // Objective modes: 0 = sum |z|.
 constexpr int kSums = 8;
 
+// Per-image ADMM bookkeeping written by the last CTA of the image (coding_pass epilogue) or lambda_update.
+struct ImageAdmm {
+  int iters;
+  int converged;
+  double primal, zc, thc, tinf;
+};
+
 template <class R>
 struct CodingArgs {
   const cx<R>* dhat;    // K x NB filter spectra
@@ -32,6 +39,14 @@ struct CodingArgs {
   int K, G, kpg;
   R rho, beta;
   const cx<R>* tw;      // twiddle table (global)
+  // fused lambda update (last CTA of each image, see lambda_epilogue)
+  unsigned* cnt;        // N arrival counters, zero between launches
+  int* conv_w;          // conv, writable
+  const cx<R>* xhat;    // N x NB
+  const R* sigma;       // NB
+  cx<R>* lamhat_w;      // N x NB
+  struct ImageAdmm* img;
+  int iter, is_last;
 };
 
 // Bulk prefetch of a contiguous global range into L2 (sm_90+ TMA engine op).
@@ -41,7 +56,7 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) 
 
 template <class P>
 struct Smem {
-  static constexpr size_t tw_bytes = sizeof(typename P::C) * P::TW_LEN;
+  static constexpr size_t tw_bytes = sizeof(typename P::C) * (P::TW_LEN + P::H);  // + COL0
   static constexpr size_t two = 2 * P::buffer_bytes + tw_bytes;
   static constexpr size_t three = 3 * P::buffer_bytes + tw_bytes;
   static constexpr bool acc_in_smem = three <= 220 * 1024;
@@ -65,12 +80,16 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, D = P::D, T = P::T;
   constexpr int W2 = W / 2, RLS = P::RLS;
   constexpr bool ACC_SMEM = Smem<P>::acc_in_smem;
+  // per-thread partial sums: FP32 lanes for the FP32 path (promoted to FP64 once
+  // per filter), FP64 for the FP64 path
+  using Acc = R;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kSums * (T / 32)];
   C* B0 = reinterpret_cast<C*>(smem_raw);
   C* B1 = B0 + NB;
   C* TW = B1 + NB + (ACC_SMEM ? NB : 0);
+  C* COL0 = TW + P::TW_LEN;
   const int n = blockIdx.y, g = blockIdx.x;
   if (MODE == kPassAdmm && a.conv[n]) return;
   C* ACC = ACC_SMEM ? (B1 + NB) : (a.part + ((size_t)n * a.G + g) * NB);
@@ -79,7 +98,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   for (int i = threadIdx.x; i < NB; i += T) ACC[i] = mk<C>(R(0), R(0));
   __syncthreads();
 
-  const R rho = a.rho, beta = a.beta, invD = R(1) / R(D), inv_rho = R(1) / rho;
+  const R rho = a.rho, beta = a.beta, invD = R(1) / R(D);
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
   const int k0 = g * a.kpg;
   const int k1 = min(a.K, k0 + a.kpg);
@@ -90,84 +109,68 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       R* __restrict__ uk = a.u + ((size_t)n * a.K + k) * D;
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if (threadIdx.x == 0) {
-        prefetch_l2_bulk(uk, sizeof(R) * D);  // this filter's state, consumed after the inverse FFT
+        prefetch_l2_bulk(uk, sizeof(R) * D);  // consumed after the inverse FFT
         if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       }
-      constexpr int U = 4;
-      for (int base = 0; base < P::HALF; base += T * U) {
-        C dv[U], lv[U], dn[U], ln[U];
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const int it = base + q * T + threadIdx.x;
-          if (it < P::HALF) {
-            const int r = it / W2, c = it % W2;
-            const int b = r * Wh + c;
-            dv[q] = __ldg(dk + b);
-            lv[q] = __ldg(lam + b);
-            if (c == 0) {
-              dn[q] = __ldg(dk + b + W2);
-              ln[q] = __ldg(lam + b + W2);
-            }
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-          const int it = base + q * T + threadIdx.x;
-          if (it < P::HALF) {
-            const int r = it / W2, c = it % W2;
-            const int b = r * Wh + c;
-            const C t0 = cmulc(dv[q], lv[q]);
-            B0[b] = (c == 0) ? P::pack_col0(t0, cmulc(dn[q], ln[q])) : t0;
-          }
-        }
-      }
-      __syncthreads();
-      C* sp = P::inverse(B0, B1, TW);
+      // t_hat = conj(d_hat_k) lambda_hat generated inside the first inverse column stage
+      C* cs = P::cols_inv_generated(B0, B1, TW, [&](int r, int c) {
+        const int b = r * Wh + c;
+        return cmulc(__ldg(dk + b), __ldg(lam + b));
+      });
+      C* o = (cs == B0) ? B1 : B0;
+      P::cols_to_rows(cs, o);
+      C* sp = P::template rows<true>(o, cs, TW);
+      // prox on u (closed form of coding.cpp:237-246), coalesced over columns
       constexpr int UP = 4;
-      for (int base = 0; base < (H / 2) * W; base += T * UP) {
-       R ua[UP], ub[UP];
+      constexpr int ITEMS = (H / 2) * W;
+      Acc f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
+      for (int base = 0; base < ITEMS; base += T * UP) {
+        R ua[UP], ub[UP];
 #pragma unroll
-       for (int q = 0; q < UP; ++q) {
-         const int it = base + q * T + threadIdx.x;
-         if (it < (H / 2) * W) {
-           const int pa = it / W, c = it % W;
-           ua[q] = uk[(2 * pa) * W + c];
-           ub[q] = uk[(2 * pa + 1) * W + c];
-         }
-       }
-#pragma unroll
-       for (int q = 0; q < UP; ++q) {
-        const int it = base + q * T + threadIdx.x;
-        if (it >= (H / 2) * W) continue;
-        const int pa = it / W, c = it % W;
-        const C v = sp[pa * RLS + c];
-        R* up = uk + (2 * pa) * W + c;
-        const R tv[2] = {v.x * invD, v.y * invD};
-        const R uo[2] = {ua[q], ub[q]};
-        R wv[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const R t = tv[e];
-          const R th_o = fmin(fmax(uo[e], -beta), beta);
-          const R un = t - (th_o - uo[e]);           // u' = t - z/rho
-          const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
-          const R zn = rho * (th - un);              // z' = rho (theta' - u')
-          const R d_tt = th - t;
-          const R dz = rho * d_tt;                   // z' - z = rho (theta' - t)
-          const R dth = th - th_o;
-          s0 += (double)d_tt * (double)d_tt;
-          s1 += (double)th * (double)th;
-          s2 += (double)t * (double)t;
-          s3 += (double)dz * (double)dz;
-          s4 += (double)zn * (double)zn;
-          s5 += (double)dth * (double)dth;
-          s6 = fmax(s6, (double)fabs(t));
-          wv[e] = R(2) * th - un;
-          if (e == 0) up[0] = un; else up[W] = un;
+        for (int q = 0; q < UP; ++q) {
+          const int it = base + q * T + threadIdx.x;
+          if (it < ITEMS) {
+            const int pa = it / W, c = it % W;
+            ua[q] = uk[(2 * pa) * W + c];
+            ub[q] = uk[(2 * pa + 1) * W + c];
+          }
         }
-        sp[pa * RLS + c] = mk<C>(wv[0], wv[1]);
-       }
+#pragma unroll
+        for (int q = 0; q < UP; ++q) {
+          const int it = base + q * T + threadIdx.x;
+          if (it >= ITEMS) continue;
+          const int pa = it / W, c = it % W;
+          const C v = sp[pa * RLS + c];
+          const R tv[2] = {v.x * invD, v.y * invD};
+          const R uo[2] = {ua[q], ub[q]};
+          R wv[2], un2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const R t = tv[e];
+            const R th_o = fmin(fmax(uo[e], -beta), beta);
+            const R un = t - (th_o - uo[e]);           // u' = t - z/rho
+            const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
+            const R zn = rho * (th - un);              // z' = rho (theta' - u')
+            const R d_tt = th - t;
+            const R dz = rho * d_tt;                   // z' - z = rho (theta' - t)
+            const R dth = th - th_o;
+            f0 += d_tt * d_tt;
+            f1 += th * th;
+            f2 += t * t;
+            f3 += dz * dz;
+            f4 += zn * zn;
+            f5 += dth * dth;
+            f6 = fmax(f6, fabs(t));
+            wv[e] = R(2) * th - un;
+            un2[e] = un;
+          }
+          uk[(2 * pa) * W + c] = un2[0];
+          uk[(2 * pa + 1) * W + c] = un2[1];
+          sp[pa * RLS + c] = mk<C>(wv[0], wv[1]);
+        }
       }
+      s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
+      s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
       __syncthreads();
       work = sp;
     } else {
@@ -194,40 +197,27 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       __syncthreads();
       work = B0;
     }
+    // forward r2c of w with acc += d_hat_k w_hat_k fused into the last column stage
     C* other = (work == B0) ? B1 : B0;
-    C* spec = P::forward(work, other, TW);
-    constexpr int UA = 4;
-    for (int base = 0; base < P::HALF; base += T * UA) {
-      C dv[UA], dn[UA];
-#pragma unroll
-      for (int q = 0; q < UA; ++q) {
-        const int it = base + q * T + threadIdx.x;
-        if (it < P::HALF) {
-          const int r = it / W2, c = it % W2;
-          const int b = r * Wh + c;
-          dv[q] = __ldg(dk + b);
-          if (c == 0) dn[q] = __ldg(dk + b + W2);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < UA; ++q) {
-        const int it = base + q * T + threadIdx.x;
-        if (it >= P::HALF) continue;
-        const int r = it / W2, c = it % W2;
-        const int b = r * Wh + c;
-        if (c == 0) {
-          C x0, xn;
-          P::unpack_col0(spec, r, x0, xn);
-          ACC[b] = cadd(ACC[b], cmul(dv[q], x0));
-          ACC[b + W2] = cadd(ACC[b + W2], cmul(dn[q], xn));
-        } else {
-          ACC[b] = cadd(ACC[b], cmul(dv[q], spec[b]));
-        }
-      }
+    C* rs = P::template rows<false>(work, other, TW);
+    C* pc = (rs == work) ? other : work;
+    P::rows_to_cols(rs, pc);
+    P::cols_fwd_consumed(pc, rs, TW, COL0,
+                         [&](int r, int c) { return __ldg(dk + r * Wh + c); },
+                         [&](int r, int c, C v, C d) {
+                           C& acc = ACC[r * Wh + c];
+                           acc = cadd(acc, cmul(d, v));
+                         });
+    for (int r = threadIdx.x; r < H; r += T) {
+      C x0, xn;
+      P::template unpack_col0<1>(COL0, r, x0, xn);  // COL0 is a contiguous column
+      C& a0 = ACC[r * Wh];
+      C& an = ACC[r * Wh + W2];
+      a0 = cadd(a0, cmul(__ldg(dk + r * Wh), x0));
+      an = cadd(an, cmul(__ldg(dk + r * Wh + W2), xn));
     }
-    __syncthreads();
   }
-  (void)inv_rho;
+  __syncthreads();
   if constexpr (ACC_SMEM) {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
     for (int i = threadIdx.x; i < NB; i += T) dst[i] = ACC[i];
@@ -242,14 +232,59 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     o[6] = mx;
     o[7] = 0.0;
   }
+  if constexpr (MODE == kPassAdmm || MODE == kPassPrologue) {
+    // Last CTA of image n to finish reduces the G partials: stop test
+    // (coding.cpp:264-283) and lambda_hat = (sum - x_hat/rho)/sigma (:25-37).
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned prev = atomicAdd(a.cnt + n, 1u);
+      last = prev == (unsigned)(a.G - 1);
+      if (last) a.cnt[n] = 0;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    bool stop = false;
+    if (MODE == kPassAdmm) {
+      double tt = 0, th = 0, t2 = 0, dz2 = 0, z2 = 0, dth = 0, tinf = 0;
+      for (int gg = 0; gg < a.G; ++gg) {
+        const double* s = a.sums + ((size_t)n * a.G + gg) * kSums;
+        tt += __ldcg(s + 0); th += __ldcg(s + 1); t2 += __ldcg(s + 2); dz2 += __ldcg(s + 3);
+        z2 += __ldcg(s + 4); dth += __ldcg(s + 5);
+        tinf = fmax(tinf, __ldcg(s + 6));
+      }
+      const double denom = fmax(fmax(sqrt(th), sqrt(t2)), 1.0);
+      const double primal = sqrt(tt) / denom;
+      const double zc = sqrt(dz2) / fmax(sqrt(z2), 1.0);
+      const double thc = sqrt(dth) / fmax(sqrt(th), 1.0);
+      stop = primal <= kAdmmRelTol && zc <= kAdmmRelTol && thc <= kAdmmRelTol;
+      if (threadIdx.x == 0) {
+        ImageAdmm& m = a.img[n];
+        m.iters = a.iter;
+        m.primal = primal;
+        m.zc = zc;
+        m.thc = thc;
+        m.tinf = tinf;
+        if (stop) {
+          m.converged = 1;
+          a.conv_w[n] = 1;
+        }
+      }
+    }
+    if (stop || (MODE == kPassAdmm && a.is_last)) return;
+    const R inv_rho = R(1) / rho;
+    const C* pn = a.part + (size_t)n * a.G * NB;
+    for (int b = threadIdx.x; b < NB; b += T) {
+      C acc = __ldcg(pn + b);  // L2 view of the other CTAs' partials
+      for (int gg = 1; gg < a.G; ++gg) acc = cadd(acc, __ldcg(pn + (size_t)gg * NB + b));
+      const C xv = a.xhat[(size_t)n * NB + b];
+      const R s = a.sigma[b];
+      a.lamhat_w[(size_t)n * NB + b] = mk<C>((acc.x - xv.x * inv_rho) / s, (acc.y - xv.y * inv_rho) / s);
+    }
+  }
 }
-
-// Per-image ADMM bookkeeping written by lambda_update (CTA 0 of the image).
-struct ImageAdmm {
-  int iters;
-  int converged;
-  double primal, zc, thc, tinf;
-};
 
 // ----------------------------------------------------------------------------
 // lambda_hat = (sum_g part_g - x_hat / rho) / sigma    (coding.cpp:25-37)
