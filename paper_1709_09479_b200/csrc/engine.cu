@@ -247,14 +247,7 @@ class Engine final : public EngineBase {
     }
     // twiddles (forward roots) in long double, rounded once
     std::vector<C> tw(P::TW_LEN);
-    auto fill = [&](int off, int L) {
-      for (int j = 0; j < L; ++j) {
-        const long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
-        tw[off + j] = mk<C>(R(std::cos(a)), R(std::sin(a)));
-      }
-    };
-    fill(0, W);
-    if (!P::SAME_TW) fill(W, H);
+    fill_twiddles<P>(tw.data());
     dtw_.alloc(sizeof(C) * P::TW_LEN);
     CK(cudaMemcpy(dtw_.p, tw.data(), sizeof(C) * P::TW_LEN, cudaMemcpyHostToDevice));
 
@@ -1169,14 +1162,7 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
     attr = true;
   }
   std::vector<C> tw(P::TW_LEN);
-  auto fill = [&](int off, int L) {
-    for (int j = 0; j < L; ++j) {
-      const long double a = -2.0L * 3.141592653589793238462643383279502884L * j / L;
-      tw[off + j] = mk<C>(R(std::cos(a)), R(std::sin(a)));
-    }
-  };
-  fill(0, W);
-  if (!P::SAME_TW) fill(W, H);
+  fill_twiddles<P>(tw.data());
   DevMem dtw, din, dout, spec;
   dtw.alloc(sizeof(C) * P::TW_LEN);
   CK(cudaMemcpy(dtw.p, tw.data(), dtw.bytes, cudaMemcpyHostToDevice));

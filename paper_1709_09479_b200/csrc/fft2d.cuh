@@ -23,6 +23,7 @@
 // column 0 on read (pcl_bin). Every 1-D pass is a Stockham autosort radix
 // sequence executed out of place between two smem buffers (one sync/stage).
 #pragma once
+#include <cmath>
 #include <type_traits>
 #include <utility>
 
@@ -181,61 +182,20 @@ template <int... Rs> struct RadixList {};
 
 template <int L> struct PlanFor;
 template <> struct PlanFor<8> { using type = RadixList<8>; };
+template <> struct PlanFor<10> { using type = RadixList<10>; };
 template <> struct PlanFor<12> { using type = RadixList<4, 3>; };
 template <> struct PlanFor<16> { using type = RadixList<16>; };
 template <> struct PlanFor<20> { using type = RadixList<4, 5>; };
 template <> struct PlanFor<24> { using type = RadixList<8, 3>; };
 template <> struct PlanFor<32> { using type = RadixList<8, 4>; };
+template <> struct PlanFor<50> { using type = RadixList<10, 5>; };
 template <> struct PlanFor<64> { using type = RadixList<8, 8>; };
 template <> struct PlanFor<100> { using type = RadixList<10, 10>; };
 template <> struct PlanFor<128> { using type = RadixList<16, 8>; };
 template <> struct PlanFor<256> { using type = RadixList<16, 16>; };
 
-// One Stockham stage over LINES lines of length L (elements at
-// line*LS + idx*ES), radix R, NS = product of the radices already applied.
-template <class C, int L, int R, int NS, bool INV, int LINES, int ES, int LS, int T>
-__device__ __forceinline__ void stockham_stage(const C* __restrict__ in, C* __restrict__ out,
-                                               const C* __restrict__ tw) {
-  constexpr int J = L / R;
-  constexpr int ITEMS = LINES * J;
-  for (int it = threadIdx.x; it < ITEMS; it += T) {
-    const int b = it % LINES;
-    const int j = it / LINES;
-    const int k = j % NS;
-    C x[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) x[q] = in[b * LS + (j + q * J) * ES];
-    if constexpr (NS > 1) {
-#pragma unroll
-      for (int q = 1; q < R; ++q) {
-        const C w = tw[q * k * (L / (NS * R))];
-        x[q] = INV ? cmulc(w, x[q]) : cmul(x[q], w);
-      }
-    }
-    dft<R, INV>(x);
-    const int o = (j / NS) * NS * R + k;
-#pragma unroll
-    for (int s = 0; s < R; ++s) out[b * LS + (o + s * NS) * ES] = x[s];
-  }
-}
-
-// Runs every stage of RadixList; data starts in a, result pointer returned
-// (a or b by stage parity). Ends with __syncthreads().
-template <class C, int L, bool INV, int LINES, int ES, int LS, int T, int NS>
-__device__ __forceinline__ C* run_stages(C* a, C*, const C*, RadixList<>) {
-  return a;
-}
-template <class C, int L, bool INV, int LINES, int ES, int LS, int T, int NS, int R, int... Rest>
-__device__ __forceinline__ C* run_stages(C* a, C* b, const C* tw, RadixList<R, Rest...>) {
-  stockham_stage<C, L, R, NS, INV, LINES, ES, LS, T>(a, b, tw);
-  __syncthreads();
-  return run_stages<C, L, INV, LINES, ES, LS, T, NS * R>(b, a, tw, RadixList<Rest...>{});
-}
-
-template <int NSTAGES> struct Parity { static constexpr bool odd = NSTAGES & 1; };
 template <class L> struct CountStages;
 template <int... Rs> struct CountStages<RadixList<Rs...>> { static constexpr int value = sizeof...(Rs); };
-
 template <int R, class L> struct Prepend;
 template <int R, int... Rs> struct Prepend<R, RadixList<Rs...>> { using type = RadixList<R, Rs...>; };
 template <class L> struct Split;
@@ -251,178 +211,220 @@ template <int R, int R2, int... Rs> struct Split<RadixList<R, R2, Rs...>> {
   using init = typename Prepend<R, typename rest::init>::type;
 };
 
+// One Stockham stage over LINES lines of length L, radix R, NS = product of
+// the radices already applied. load(line, idx) / store(line, idx, v) address
+// the data (plain smem or fused producers/consumers). Lanes run over lines.
+template <class C, int L, int R, int NS, bool INV, int LINES, int T, class LOAD, class STORE>
+__device__ __forceinline__ void stockham(const C* __restrict__ tw, LOAD&& load, STORE&& store) {
+  constexpr int J = L / R;
+  constexpr int ITEMS = LINES * J;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < ITEMS; it += T) {
+    const int b = it % LINES;
+    const int j = it / LINES;
+    const int k = j % NS;
+    C x[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[q] = load(b, j + q * J);
+    if constexpr (NS > 1) {
+#pragma unroll
+      for (int q = 1; q < R; ++q) {
+        const C w = tw[q * k * (L / (NS * R))];
+        x[q] = INV ? cmulc(w, x[q]) : cmul(x[q], w);
+      }
+    }
+    dft<R, INV>(x);
+    const int o = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int s = 0; s < R; ++s) store(b, o + s * NS, x[s]);
+  }
+}
+
+// Plain smem stages for every radix in the list (ping-pong, one sync each);
+// returns the buffer holding the result.
+template <class C, int L, bool INV, int LINES, int ES, int LS, int T, int NS>
+__device__ __forceinline__ C* run_stages(C* a, C*, const C*, RadixList<>) {
+  return a;
+}
+template <class C, int L, bool INV, int LINES, int ES, int LS, int T, int NS, int R, int... Rest>
+__device__ __forceinline__ C* run_stages(C* a, C* b, const C* tw, RadixList<R, Rest...>) {
+  stockham<C, L, R, NS, INV, LINES, T>(
+      tw, [&](int l, int i) { return a[l * LS + i * ES]; }, [&](int l, int i, C v) { b[l * LS + i * ES] = v; });
+  __syncthreads();
+  return run_stages<C, L, INV, LINES, ES, LS, T, NS * R>(b, a, tw, RadixList<Rest...>{});
+}
+
+template <int A, int B> struct Prod;
+template <class L> struct ListProd;
+template <> struct ListProd<RadixList<>> { static constexpr int value = 1; };
+template <int R, int... Rs> struct ListProd<RadixList<R, Rs...>> {
+  static constexpr int value = R * ListProd<RadixList<Rs...>>::value;
+};
+
 // ---------------------------------------------------------------- 2-D plane
+// Layout (one buffer = NB complex): [H][Wh], Wh = W/2 + 1 (odd line stride
+// for W = 0 mod 4, so lane-per-line accesses are bank-conflict free).
+//  * spectral: natural half spectrum X[r][c], c in [0, W/2]; during the
+//    column passes column 0 holds the packed pair P = X[.][0] + i X[.][W/2]
+//    (both are spectra of real columns) and only columns [0, W/2) transform.
+//  * spatial: element [r][m], m < W/2, holds (x[r][2m], x[r][2m+1]).
+// Row transforms are W/2-point complex FFTs of those pairs with the r2c/c2r
+// pre/post-processing X[k] <-> (Z[k], Z[W/2-k]) fused into the adjacent
+// column stage (forward) or the first row stage (inverse).
 template <class Rt, int H_, int W_, int T_>
 struct Plane {
   using R = Rt;
   using C = cx<Rt>;
   static constexpr int H = H_, W = W_, T = T_;
-  static constexpr int Wh = W / 2 + 1;
-  static constexpr int NB = H * Wh;      // complex elements in NSL / PCL (and smem buffer)
-  static constexpr int RLS = W + 1;      // RPL line stride
+  static constexpr int M = W / 2;     // row FFT length
+  static constexpr int Wh = M + 1;
+  static constexpr int NB = H * Wh;  // complex elements per plane buffer
   static constexpr int D = H * W;
-  static constexpr int HALF = H * (W / 2);  // PCL items (columns [0, W/2))
-  static_assert(H % 2 == 0 && W % 2 == 0, "even grid sizes only");
-  static_assert((H / 2) * RLS <= NB, "RPL must fit in a plane buffer");
-  using RowPlan = typename PlanFor<W>::type;
+  static constexpr int HALF = H * M;  // column-pass items (columns [0, W/2))
+  static_assert(W % 2 == 0, "even grid width only");
+  using RowPlan = typename PlanFor<M>::type;
   using ColPlan = typename PlanFor<H>::type;
-  static constexpr int ROW_STAGES = CountStages<RowPlan>::value;
-  static constexpr int COL_STAGES = CountStages<ColPlan>::value;
-  static constexpr bool SAME_TW = (H == W);
-  static constexpr int TW_LEN = SAME_TW ? W : (W + H);
+  // twiddles: [0,M) row roots W_M^j, [M, M+H) column roots W_H^j,
+  // [M+H, 2M+H+1) pre/post-processing roots W_W^k, k = 0..M
+  static constexpr int TW_ROW = 0, TW_COL = M, TW_PP = M + H;
+  static constexpr int TW_LEN = 2 * M + H + 1;
   static constexpr size_t buffer_bytes = sizeof(C) * NB;
-
-  // twiddle tables (forward roots): tw_row[0..W), tw_col[0..H)
-  __device__ static __forceinline__ const C* tw_row(const C* tw) { return tw; }
-  __device__ static __forceinline__ const C* tw_col(const C* tw) { return SAME_TW ? tw : tw + W; }
 
   __device__ static __forceinline__ void load_twiddles(C* tw_s, const C* __restrict__ tw_g) {
     for (int i = threadIdx.x; i < TW_LEN; i += T) tw_s[i] = tw_g[i];
   }
 
-  template <bool INV>
-  __device__ static __forceinline__ C* rows(C* a, C* b, const C* tw) {
-    return run_stages<C, W, INV, H / 2, 1, RLS, T, 1>(a, b, tw_row(tw), RowPlan{});
-  }
-  template <bool INV>
-  __device__ static __forceinline__ C* cols(C* a, C* b, const C* tw) {
-    return run_stages<C, H, INV, W / 2, Wh, 1, T, 1>(a, b, tw_col(tw), ColPlan{});
+  // --- spatial element (r, m) <-> real pixels (r, 2m), (r, 2m+1)
+  __device__ static __forceinline__ int sidx(int r, int m) { return r * Wh + m; }
+
+  // --- forward ---------------------------------------------------------
+  // Row FFTs (length M) of the spatial pairs in `a`; returns the buffer with Z.
+  __device__ static __forceinline__ C* rows_fwd(C* a, C* b, const C* tw) {
+    return run_stages<C, M, false, H, 1, Wh, T, 1>(a, b, tw + TW_ROW, RowPlan{});
   }
 
-  // RPL(spectral) in `src` -> PCL in `dst` (forward row unpack), then sync.
-  __device__ static __forceinline__ void rows_to_cols(const C* __restrict__ src, C* __restrict__ dst) {
-    constexpr int W2 = W / 2;
-    for (int it = threadIdx.x; it < (H / 2) * W2; it += T) {
-      const int a = it / W2, k = it % W2;
-      const C* row = src + a * RLS;
-      C* o0 = dst + (2 * a) * Wh;
-      C* o1 = o0 + Wh;
-      if (k == 0) {
-        const C c0 = row[0], cn = row[W2];
-        o0[0] = mk<C>(c0.x, cn.x);  // (X_{2a}[0], X_{2a}[W/2]) both real
-        o1[0] = mk<C>(c0.y, cn.y);  // (X_{2a+1}[0], X_{2a+1}[W/2])
-      } else {
-        const C c = row[k], cm = row[W - k];
-        // Xa = (C + conj(Cm))/2 ; Xb = -i/2 (C - conj(Cm))
-        o0[k] = mk<C>(R(0.5) * (c.x + cm.x), R(0.5) * (c.y - cm.y));
-        o1[k] = mk<C>(R(0.5) * (c.y + cm.y), R(0.5) * (cm.x - c.x));
-      }
-    }
-    __syncthreads();
+  // r2c post-processing of row r at column c (natural bin) from the row FFT Z:
+  // X[c] = E + W_W^c O, E = (Z[c] + conj Z[M-c])/2, O = -i/2 (Z[c] - conj Z[M-c]).
+  // Column 0 returns the packed pair (X[0], X[M]) = (Re Z0 + Im Z0, Re Z0 - Im Z0).
+  __device__ static __forceinline__ C post(const C* z, const C* tw, int r, int c) {
+    const C z1 = z[r * Wh + c];
+    if (c == 0) return mk<C>(z1.x + z1.y, z1.x - z1.y);
+    const C z2 = z[r * Wh + (M - c)];
+    // z2c = conj(z2); E = (z1 + z2c)/2 ; O = -i/2 (z1 - z2c)
+    const C e = mk<C>(R(0.5) * (z1.x + z2.x), R(0.5) * (z1.y - z2.y));
+    const C o = mk<C>(R(0.5) * (z1.y + z2.y), R(0.5) * (z2.x - z1.x));
+    return cadd(e, cmul(tw[TW_PP + c], o));
   }
 
-  // PCL(spatial columns) in `src` -> RPL(spectral) in `dst` (inverse row pack), then sync.
-  __device__ static __forceinline__ void cols_to_rows(const C* __restrict__ src, C* __restrict__ dst) {
-    constexpr int W2 = W / 2;
-    for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
-      const int a = it / W, k = it % W;
-      const C* r0 = src + (2 * a) * Wh;
-      const C* r1 = r0 + Wh;
-      C xa, xb;
-      if (k == 0) {
-        xa = mk<C>(r0[0].x, R(0));
-        xb = mk<C>(r1[0].x, R(0));
-      } else if (k == W2) {
-        xa = mk<C>(r0[0].y, R(0));
-        xb = mk<C>(r1[0].y, R(0));
-      } else if (k < W2) {
-        xa = r0[k];
-        xb = r1[k];
-      } else {
-        xa = cconj(r0[W - k]);
-        xb = cconj(r1[W - k]);
-      }
-      // C = Xa + i Xb
-      dst[a * RLS + k] = mk<C>(xa.x - xb.y, xa.y + xb.x);
-    }
-    __syncthreads();
-  }
-
-  // Forward r2c. Input: real plane in RPL in buffer a. Output: PCL spectrum
-  // (returned pointer, a or b). Column 0 holds FFT_col(X0 + i XN).
-  __device__ static __forceinline__ C* forward(C* a, C* b, const C* tw) {
-    C* r = rows<false>(a, b, tw);
-    C* o = (r == a) ? b : a;
-    rows_to_cols(r, o);
-    return cols<false>(o, r, tw);
-  }
-
-  // Inverse c2r (unscaled). Input: PCL spectrum in buffer a (column 0 packed).
-  // Output: RPL real plane times D (returned pointer).
-  __device__ static __forceinline__ C* inverse(C* a, C* b, const C* tw) {
-    C* c = cols<true>(a, b, tw);
-    C* o = (c == a) ? b : a;
-    cols_to_rows(c, o);
-    return rows<true>(o, c, tw);
-  }
-
-  // ---- fused column stages (coding hot loop) ----
-  // Inverse column pass whose first Stockham stage generates its input on the
-  // fly: gen(r, c) returns natural bin (r, c); column 0 packs (r,0)+(r,W/2).
-  // Writes the first stage into `a`, runs the rest ping-pong; returns result.
-  template <class GEN>
-  __device__ static __forceinline__ C* cols_inv_generated(C* a, C* b, const C* tw, GEN&& gen) {
-    using S = Split<ColPlan>;
-    constexpr int R = S::first, J = H / R, LINES = W / 2, ITEMS = LINES * J;
-#pragma unroll 1
-    for (int it = threadIdx.x; it < ITEMS; it += T) {
-      const int col = it % LINES, j = it / LINES;
-      C x[R];
-      if (col == 0) {
-#pragma unroll
-        for (int q = 0; q < R; ++q) x[q] = pack_col0(gen(j + q * J, 0), gen(j + q * J, W / 2));
-      } else {
-#pragma unroll
-        for (int q = 0; q < R; ++q) x[q] = gen(j + q * J, col);
-      }
-      dft<R, true>(x);
-#pragma unroll
-      for (int s = 0; s < R; ++s) a[(j * R + s) * Wh + col] = x[s];
-    }
-    __syncthreads();
-    return run_stages<C, H, true, W / 2, Wh, 1, T, R>(a, b, tw_col(tw), typename S::tail{});
-  }
-
-  // Forward column pass whose last Stockham stage hands each output to
-  // cons(r, col, value, pre) instead of storing it; pre = prefetch(r, col) is
-  // issued before the stage's smem reads. Column 0 outputs (the packed pair
-  // spectrum Y) go to col0[r]; the caller unpacks them after a sync.
+  // Forward column pass over Z (row-FFT output in `z`): the first stage applies
+  // the r2c post-processing on load; the last stage hands every output to
+  // cons(r, c, v, pre(r, c)) (c in [1, M)), column 0 (packed Y) goes to col0[r].
+  // `z` and `b` are both clobbered. Ends with __syncthreads().
   template <class PRE, class CONS>
-  __device__ static __forceinline__ void cols_fwd_consumed(C* a, C* b, const C* tw, C* col0, PRE&& pre,
-                                                          CONS&& cons) {
+  __device__ static __forceinline__ void cols_fwd(C* z, C* b, const C* tw, C* col0, PRE&& pre, CONS&& cons) {
     using S = Split<ColPlan>;
-    constexpr int R = S::last, NS = H / R, J = H / R, LINES = W / 2, ITEMS = LINES * J;
-    C* in = run_stages<C, H, false, W / 2, Wh, 1, T, 1>(a, b, tw_col(tw), typename S::init{});
-    const C* twc = tw_col(tw);
+    constexpr int NST = CountStages<ColPlan>::value;
+    const C* twc = tw + TW_COL;
+    auto consume_store = [&](auto&& load, auto nsc, auto rc) {
+      constexpr int NS = decltype(nsc)::value, R = decltype(rc)::value;
+      constexpr int J = H / R;
+      constexpr int ITEMS = M * J;
 #pragma unroll 1
-    for (int it = threadIdx.x; it < ITEMS; it += T) {
-      const int col = it % LINES, j = it / LINES;  // j < NS: outputs rows j + s*NS
-      using PT = decltype(pre(0, 1));
-      PT pv[R];
-      if (col != 0) {
+      for (int it = threadIdx.x; it < ITEMS; it += T) {
+        const int col = it % M, j = it / M;  // outputs rows j + s*NS (j < NS)
+        using PT = decltype(pre(0, 1));
+        PT pv[R];
+        if (col != 0) {
 #pragma unroll
-        for (int s = 0; s < R; ++s) pv[s] = pre(j + s * NS, col);
+          for (int s = 0; s < R; ++s) pv[s] = pre(j + s * NS, col);
+        }
+        C x[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = load(col, j + q * J);
+        if constexpr (NS > 1) {
+#pragma unroll
+          for (int q = 1; q < R; ++q) x[q] = cmul(x[q], twc[q * j * (H / (NS * R))]);
+        }
+        dft<R, false>(x);
+        if (col == 0) {
+#pragma unroll
+          for (int s = 0; s < R; ++s) col0[j + s * NS] = x[s];
+        } else {
+#pragma unroll
+          for (int s = 0; s < R; ++s) cons(j + s * NS, col, x[s], pv[s]);
+        }
       }
-      C x[R];
-#pragma unroll
-      for (int q = 0; q < R; ++q) x[q] = in[(j + q * J) * Wh + col];
-      if constexpr (NS > 1) {
-#pragma unroll
-        for (int q = 1; q < R; ++q) x[q] = cmul(x[q], twc[q * j * (H / (NS * R))]);
-      }
-      dft<R, false>(x);
-      if (col == 0) {
-#pragma unroll
-        for (int s = 0; s < R; ++s) col0[j + s * NS] = x[s];
-      } else {
-#pragma unroll
-        for (int s = 0; s < R; ++s) cons(j + s * NS, col, x[s], pv[s]);
-      }
+      __syncthreads();
+    };
+    auto post_load = [&](int col, int r) { return post(z, tw, r, col); };
+    if constexpr (NST == 1) {
+      consume_store(post_load, std::integral_constant<int, 1>{}, std::integral_constant<int, S::first>{});
+    } else {
+      constexpr int R1 = S::first;
+      stockham<C, H, R1, 1, false, M, T>(twc, post_load, [&](int l, int i, C v) { b[i * Wh + l] = v; });
+      __syncthreads();
+      using Mid = typename Split<typename S::tail>::init;  // stages between first and last
+      C* in = run_stages<C, H, false, M, Wh, 1, T, R1>(b, z, twc, Mid{});
+      constexpr int NSL = H / S::last;
+      consume_store([&](int l, int i) { return in[i * Wh + l]; }, std::integral_constant<int, NSL>{},
+                    std::integral_constant<int, S::last>{});
     }
-    __syncthreads();
   }
 
-  // Natural bins (r,0) and (r,W/2) from a forward PCL column 0.
+  // --- inverse ---------------------------------------------------------
+  // Inverse column pass with the first stage generating its input:
+  // gen(r, c) returns natural bin (r, c), c in [0, M]; column 0 packs (r,0)+(r,M).
+  // Returns the buffer holding the column-inverse result (PCL).
+  template <class GEN>
+  __device__ static __forceinline__ C* cols_inv(C* a, C* b, const C* tw, GEN&& gen) {
+    using S = Split<ColPlan>;
+    constexpr int R1 = S::first;
+    const C* twc = tw + TW_COL;
+    stockham<C, H, R1, 1, true, M, T>(
+        twc,
+        [&](int col, int r) { return col == 0 ? pack_col0(gen(r, 0), gen(r, M)) : gen(r, col); },
+        [&](int l, int i, C v) { a[i * Wh + l] = v; });
+    __syncthreads();
+    return run_stages<C, H, true, M, Wh, 1, T, R1>(a, b, twc, typename S::tail{});
+  }
+
+  // c2r pre-processing of row r at index k from the column-inverse result p:
+  // Z'[k] = (A + Bc) + i W_W^-k (A - Bc), A = X[k], Bc = conj X[M-k];
+  // X[0] = Re P, X[M] = Im P (packed column 0).
+  __device__ static __forceinline__ C pre(const C* p, const C* tw, int r, int k) {
+    if (k == 0) {
+      const C q = p[r * Wh];
+      return mk<C>(q.x + q.y, q.x - q.y);
+    }
+    const C a = p[r * Wh + k];
+    const C bb = p[r * Wh + (M - k)];
+    const C s = mk<C>(a.x + bb.x, a.y - bb.y);  // A + conj(B)
+    const C d = mk<C>(a.x - bb.x, a.y + bb.y);  // A - conj(B)
+    const C wd = cmulc(tw[TW_PP + k], d);       // W_W^-k (A - conj B)
+    return mk<C>(s.x - wd.y, s.y + wd.x);       // s + i wd
+  }
+
+  // Inverse row pass (first stage applies the c2r pre-processing on load).
+  // Input: column-inverse result in `p`; output: spatial pairs times D in the
+  // returned buffer (p or b).
+  __device__ static __forceinline__ C* rows_inv(C* p, C* b, const C* tw) {
+    using S = Split<RowPlan>;
+    constexpr int R1 = S::first;
+    const C* twr = tw + TW_ROW;
+    stockham<C, M, R1, 1, true, H, T>(
+        twr, [&](int r, int k) { return pre(p, tw, r, k); }, [&](int l, int i, C v) { b[l * Wh + i] = v; });
+    __syncthreads();
+    return run_stages<C, M, true, H, 1, Wh, T, R1>(b, p, twr, typename S::tail{});
+  }
+
+  // Full inverse from a generator (used by c2r and the coding pass).
+  template <class GEN>
+  __device__ static __forceinline__ C* inverse(C* a, C* b, const C* tw, GEN&& gen) {
+    C* c = cols_inv(a, b, tw, gen);
+    return rows_inv(c, c == a ? b : a, tw);
+  }
+
+  // Natural bins (r,0) and (r,W/2) from a packed column-0 spectrum Y (stride STRIDE).
   template <int STRIDE = Wh>
   __device__ static __forceinline__ void unpack_col0(const C* pcl, int r, C& x0, C& xn) {
     const C y = pcl[r * STRIDE];
@@ -430,10 +432,22 @@ struct Plane {
     x0 = mk<C>(R(0.5) * (y.x + ym.x), R(0.5) * (y.y - ym.y));
     xn = mk<C>(R(0.5) * (y.y + ym.y), R(0.5) * (ym.x - y.x));
   }
-  // PCL column-0 entry packing natural bins x0 (col 0) and xn (col W/2).
-  __device__ static __forceinline__ C pack_col0(C x0, C xn) {
-    return mk<C>(x0.x - xn.y, x0.y + xn.x);
-  }
+  // Packed column-0 entry from natural bins x0 (col 0) and xn (col W/2).
+  __device__ static __forceinline__ C pack_col0(C x0, C xn) { return mk<C>(x0.x - xn.y, x0.y + xn.x); }
 };
+
+// Host-side twiddle table for Plane (forward roots, long double).
+template <class P>
+void fill_twiddles(typename P::C* tw) {
+  using C = typename P::C;
+  using R = typename P::R;
+  auto root = [](long double num, long double den) {
+    const long double a = -2.0L * 3.141592653589793238462643383279502884L * num / den;
+    return mk<C>(R(std::cos(a)), R(std::sin(a)));
+  };
+  for (int j = 0; j < P::M; ++j) tw[P::TW_ROW + j] = root(j, P::M);
+  for (int j = 0; j < P::H; ++j) tw[P::TW_COL + j] = root(j, P::H);
+  for (int k = 0; k <= P::M; ++k) tw[P::TW_PP + k] = root(k, P::W);
+}
 
 }  // namespace dcsc_cuda

@@ -66,23 +66,22 @@ struct Smem {
 // ----------------------------------------------------------------------------
 // The fused coding kernel. One CTA = (image n, filter group g); for each filter:
 //   t_hat = conj(d_hat_k) lambda_hat           (coding.cpp:77-86, correlate)
+//     generated inside the first inverse column stage (no smem pass)
 //   t = iDFT(t_hat)                            (coding.cpp:234)
 //   theta' = clamp(t - z/rho), z' = z + rho(theta'-t)   (coding.cpp:237-246)
 //     in closed form on u: u' = t - z/rho, theta' = clamp(u'), z' = rho(theta'-u')
 //   w = theta' + z'/rho = 2 theta' - u'  ->  w_hat = DFT(w)
 //     (one forward FFT replaces DFT(theta) and DFT(z), coding.cpp:260-261,224-227)
-//   acc += d_hat_k w_hat_k                     (lambda_from_w numerator, coding.cpp:25-37)
+//   acc += d_hat_k w_hat_k  inside the last forward column stage
+//                                              (lambda_from_w numerator, coding.cpp:25-37)
+// The last CTA of each image runs the stop test and the lambda_hat update.
 // ----------------------------------------------------------------------------
 template <class P, int MODE>
 __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a) {
   using R = typename P::R;
   using C = typename P::C;
-  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, D = P::D, T = P::T;
-  constexpr int W2 = W / 2, RLS = P::RLS;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, D = P::D, T = P::T, M = P::M;
   constexpr bool ACC_SMEM = Smem<P>::acc_in_smem;
-  // per-thread partial sums: FP32 lanes for the FP32 path (promoted to FP64 once
-  // per filter), FP64 for the FP64 path
-  using Acc = R;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kSums * (T / 32)];
@@ -106,43 +105,35 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     const C* __restrict__ dk = a.dhat + (size_t)k * NB;
     C* work;
     if constexpr (MODE == kPassAdmm) {
-      R* __restrict__ uk = a.u + ((size_t)n * a.K + k) * D;
+      C* __restrict__ uk = reinterpret_cast<C*>(a.u + ((size_t)n * a.K + k) * D);  // pixel pairs
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if (threadIdx.x == 0) {
         prefetch_l2_bulk(uk, sizeof(R) * D);  // consumed after the inverse FFT
         if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       }
-      // t_hat = conj(d_hat_k) lambda_hat generated inside the first inverse column stage
-      C* cs = P::cols_inv_generated(B0, B1, TW, [&](int r, int c) {
+      C* sp = P::inverse(B0, B1, TW, [&](int r, int c) {
         const int b = r * Wh + c;
         return cmulc(__ldg(dk + b), __ldg(lam + b));
       });
-      C* o = (cs == B0) ? B1 : B0;
-      P::cols_to_rows(cs, o);
-      C* sp = P::template rows<true>(o, cs, TW);
-      // prox on u (closed form of coding.cpp:237-246), coalesced over columns
+      // prox on u (closed form of coding.cpp:237-246), pixel pairs, coalesced
       constexpr int UP = 4;
-      constexpr int ITEMS = (H / 2) * W;
-      Acc f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
+      constexpr int ITEMS = H * M;
+      R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
       for (int base = 0; base < ITEMS; base += T * UP) {
-        R ua[UP], ub[UP];
+        C uv[UP];
 #pragma unroll
         for (int q = 0; q < UP; ++q) {
           const int it = base + q * T + threadIdx.x;
-          if (it < ITEMS) {
-            const int pa = it / W, c = it % W;
-            ua[q] = uk[(2 * pa) * W + c];
-            ub[q] = uk[(2 * pa + 1) * W + c];
-          }
+          if (it < ITEMS) uv[q] = uk[it];
         }
 #pragma unroll
         for (int q = 0; q < UP; ++q) {
           const int it = base + q * T + threadIdx.x;
           if (it >= ITEMS) continue;
-          const int pa = it / W, c = it % W;
-          const C v = sp[pa * RLS + c];
+          const int r = it / M, m = it % M;
+          const C v = sp[r * Wh + m];
           const R tv[2] = {v.x * invD, v.y * invD};
-          const R uo[2] = {ua[q], ub[q]};
+          const R uo[2] = {uv[q].x, uv[q].y};
           R wv[2], un2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -164,9 +155,8 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
             wv[e] = R(2) * th - un;
             un2[e] = un;
           }
-          uk[(2 * pa) * W + c] = un2[0];
-          uk[(2 * pa + 1) * W + c] = un2[1];
-          sp[pa * RLS + c] = mk<C>(wv[0], wv[1]);
+          uk[it] = mk<C>(un2[0], un2[1]);
+          sp[r * Wh + m] = mk<C>(wv[0], wv[1]);
         }
       }
       s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
@@ -174,47 +164,45 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       __syncthreads();
       work = sp;
     } else {
-      const R* __restrict__ src = (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D
-                                                      : a.u + ((size_t)n * a.K + k) * D;
-      for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
-        const int pa = it / W, c = it % W;
-        const R v0 = src[(2 * pa) * W + c], v1 = src[(2 * pa + 1) * W + c];
+      const C* __restrict__ src = reinterpret_cast<const C*>(
+          (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D);
+      for (int it = threadIdx.x; it < H * M; it += T) {
+        const int r = it / M, m = it % M;
+        const C v = src[it];
         R w0, w1;
         if constexpr (MODE == kPassPrologue) {
-          w0 = R(2) * fmin(fmax(v0, -beta), beta) - v0;
-          w1 = R(2) * fmin(fmax(v1, -beta), beta) - v1;
+          w0 = R(2) * fmin(fmax(v.x, -beta), beta) - v.x;
+          w1 = R(2) * fmin(fmax(v.y, -beta), beta) - v.y;
         } else if constexpr (MODE == kPassObjective) {
-          w0 = rho * (fmin(fmax(v0, -beta), beta) - v0);
-          w1 = rho * (fmin(fmax(v1, -beta), beta) - v1);
+          w0 = rho * (fmin(fmax(v.x, -beta), beta) - v.x);
+          w1 = rho * (fmin(fmax(v.y, -beta), beta) - v.y);
           s0 += (double)fabs(w0) + (double)fabs(w1);
         } else {
-          w0 = v0;
-          w1 = v1;
+          w0 = v.x;
+          w1 = v.y;
           s0 += (double)fabs(w0) + (double)fabs(w1);
         }
-        B0[pa * RLS + c] = mk<C>(w0, w1);
+        B0[r * Wh + m] = mk<C>(w0, w1);
       }
       __syncthreads();
       work = B0;
     }
     // forward r2c of w with acc += d_hat_k w_hat_k fused into the last column stage
     C* other = (work == B0) ? B1 : B0;
-    C* rs = P::template rows<false>(work, other, TW);
-    C* pc = (rs == work) ? other : work;
-    P::rows_to_cols(rs, pc);
-    P::cols_fwd_consumed(pc, rs, TW, COL0,
-                         [&](int r, int c) { return __ldg(dk + r * Wh + c); },
-                         [&](int r, int c, C v, C d) {
-                           C& acc = ACC[r * Wh + c];
-                           acc = cadd(acc, cmul(d, v));
-                         });
+    C* z = P::rows_fwd(work, other, TW);
+    P::cols_fwd(z, z == work ? other : work, TW, COL0,
+                [&](int r, int c) { return __ldg(dk + r * Wh + c); },
+                [&](int r, int c, C v, C d) {
+                  C& acc = ACC[r * Wh + c];
+                  acc = cadd(acc, cmul(d, v));
+                });
     for (int r = threadIdx.x; r < H; r += T) {
       C x0, xn;
-      P::template unpack_col0<1>(COL0, r, x0, xn);  // COL0 is a contiguous column
+      P::template unpack_col0<1>(COL0, r, x0, xn);
       C& a0 = ACC[r * Wh];
-      C& an = ACC[r * Wh + W2];
+      C& an = ACC[r * Wh + M];
       a0 = cadd(a0, cmul(__ldg(dk + r * Wh), x0));
-      an = cadd(an, cmul(__ldg(dk + r * Wh + W2), xn));
+      an = cadd(an, cmul(__ldg(dk + r * Wh + M), xn));
     }
   }
   __syncthreads();
@@ -339,46 +327,51 @@ __global__ void lambda_update(const cx<R>* __restrict__ part, const double* __re
 // ----------------------------------------------------------------------------
 // Batched r2c of real planes (x_hat, z_hat, padded filters) and c2r.
 // ----------------------------------------------------------------------------
+// Shared tail: forward FFT of the spatial pairs in B0, NSL spectrum to `d`.
+template <class P>
+__device__ __forceinline__ void forward_to_global(typename P::C* B0, typename P::C* B1, const typename P::C* TW,
+                                                  typename P::C* COL0, typename P::C* __restrict__ d) {
+  using C = typename P::C;
+  constexpr int Wh = P::Wh, M = P::M, H = P::H, T = P::T;
+  C* z = P::rows_fwd(B0, B1, TW);
+  P::cols_fwd(z, z == B0 ? B1 : B0, TW, COL0, [](int, int) { return 0; },
+              [&](int r, int c, C v, int) { d[r * Wh + c] = v; });
+  for (int r = threadIdx.x; r < H; r += T) {
+    C x0, xn;
+    P::template unpack_col0<1>(COL0, r, x0, xn);
+    d[r * Wh] = x0;
+    d[r * Wh + M] = xn;
+  }
+}
+
 template <class P, class SRC>
 __global__ void __launch_bounds__(P::T)
 r2c_planes(const SRC* __restrict__ src, size_t src_stride, cx<typename P::R>* __restrict__ dst,
            size_t dst_stride, const cx<typename P::R>* tw, int* live_flags, int live_mod) {
   using R = typename P::R;
   using C = typename P::C;
-  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, M = P::M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* B0 = reinterpret_cast<C*>(smem_raw);
   C* B1 = B0 + NB;
   C* TW = B1 + NB;
+  C* COL0 = TW + P::TW_LEN;
   const int p = blockIdx.x;
   P::load_twiddles(TW, tw);
   const SRC* s = src + (size_t)p * src_stride;
   int any = 0;
-  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
-    const int pa = it / W, c = it % W;
-    const R v0 = R(s[(2 * pa) * W + c]), v1 = R(s[(2 * pa + 1) * W + c]);
+  for (int it = threadIdx.x; it < H * M; it += T) {
+    const int r = it / M, m = it % M;
+    const R v0 = R(s[r * W + 2 * m]), v1 = R(s[r * W + 2 * m + 1]);
     any |= (v0 != R(0)) | (v1 != R(0));
-    B0[pa * P::RLS + c] = mk<C>(v0, v1);
+    B0[r * Wh + m] = mk<C>(v0, v1);
   }
   __syncthreads();
   if (live_flags) {
     any = __syncthreads_or(any);
     if (threadIdx.x == 0 && any) atomicOr(live_flags + (p % live_mod), 1);
   }
-  C* spec = P::forward(B0, B1, TW);
-  C* d = dst + (size_t)p * dst_stride;
-  for (int it = threadIdx.x; it < P::HALF; it += T) {
-    const int r = it / W2, c = it % W2;
-    const int b = r * Wh + c;
-    if (c == 0) {
-      C x0, xn;
-      P::unpack_col0(spec, r, x0, xn);
-      d[b] = x0;
-      d[b + W2] = xn;
-    } else {
-      d[b] = spec[b];
-    }
-  }
+  forward_to_global<P>(B0, B1, TW, COL0, dst + (size_t)p * dst_stride);
 }
 
 // Zero-padded filters (corner placement, spectral.cpp:106-122) -> spectra.
@@ -388,36 +381,24 @@ r2c_filters(const double* __restrict__ d, int mh, int mw, cx<typename P::R>* __r
             const cx<typename P::R>* tw) {
   using R = typename P::R;
   using C = typename P::C;
-  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2;
+  constexpr int H = P::H, Wh = P::Wh, NB = P::NB, T = P::T, M = P::M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* B0 = reinterpret_cast<C*>(smem_raw);
   C* B1 = B0 + NB;
   C* TW = B1 + NB;
+  C* COL0 = TW + P::TW_LEN;
   const int k = blockIdx.x;
   P::load_twiddles(TW, tw);
   const double* f = d + (size_t)k * mh * mw;
-  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
-    const int pa = it / W, c = it % W;
-    const int r0 = 2 * pa, r1 = r0 + 1;
-    const R v0 = (r0 < mh && c < mw) ? R(f[r0 * mw + c]) : R(0);
-    const R v1 = (r1 < mh && c < mw) ? R(f[r1 * mw + c]) : R(0);
-    B0[pa * P::RLS + c] = mk<C>(v0, v1);
+  for (int it = threadIdx.x; it < H * M; it += T) {
+    const int r = it / M, m = it % M;
+    const int c0 = 2 * m, c1 = c0 + 1;
+    const R v0 = (r < mh && c0 < mw) ? R(f[r * mw + c0]) : R(0);
+    const R v1 = (r < mh && c1 < mw) ? R(f[r * mw + c1]) : R(0);
+    B0[r * Wh + m] = mk<C>(v0, v1);
   }
   __syncthreads();
-  C* spec = P::forward(B0, B1, TW);
-  C* o = dst + (size_t)k * NB;
-  for (int it = threadIdx.x; it < P::HALF; it += T) {
-    const int r = it / W2, c = it % W2;
-    const int b = r * Wh + c;
-    if (c == 0) {
-      C x0, xn;
-      P::unpack_col0(spec, r, x0, xn);
-      o[b] = x0;
-      o[b + W2] = xn;
-    } else {
-      o[b] = spec[b];
-    }
-  }
+  forward_to_global<P>(B0, B1, TW, COL0, dst + (size_t)k * NB);
 }
 
 // Batched c2r of NSL spectra (scaled by `scale`/D) into real planes.
@@ -427,28 +408,23 @@ c2r_planes(const cx<typename P::R>* __restrict__ src, size_t src_stride, DST* __
            size_t dst_stride, const cx<typename P::R>* tw, const double* scale) {
   using R = typename P::R;
   using C = typename P::C;
-  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2, D = P::D;
+  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, D = P::D, M = P::M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* B0 = reinterpret_cast<C*>(smem_raw);
   C* B1 = B0 + NB;
   C* TW = B1 + NB;
   const int p = blockIdx.x;
   P::load_twiddles(TW, tw);
-  const C* s = src + (size_t)p * src_stride;
-  for (int it = threadIdx.x; it < P::HALF; it += T) {
-    const int r = it / W2, c = it % W2;
-    const int b = r * Wh + c;
-    B0[b] = (c == 0) ? P::pack_col0(s[b], s[b + W2]) : s[b];
-  }
   __syncthreads();
-  C* sp = P::inverse(B0, B1, TW);
+  const C* s = src + (size_t)p * src_stride;
+  C* sp = P::inverse(B0, B1, TW, [&](int r, int c) { return s[r * Wh + c]; });
   const R sc = R((scale ? scale[p] : 1.0) / (double)D);
   DST* o = dst + (size_t)p * dst_stride;
-  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
-    const int pa = it / W, c = it % W;
-    const C v = sp[pa * P::RLS + c];
-    o[(2 * pa) * W + c] = DST(v.x * sc);
-    o[(2 * pa + 1) * W + c] = DST(v.y * sc);
+  for (int it = threadIdx.x; it < H * M; it += T) {
+    const int r = it / M, m = it % M;
+    const C v = sp[r * Wh + m];
+    o[r * W + 2 * m] = DST(v.x * sc);
+    o[r * W + 2 * m + 1] = DST(v.y * sc);
   }
 }
 
@@ -465,12 +441,12 @@ mask_step(const cx<typename P::R>* __restrict__ c, cx<typename P::R>* __restrict
           const cx<typename P::R>* tw) {
   using R = typename P::R;
   using C = typename P::C;
-  constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, T = P::T, W2 = W / 2, D = P::D;
-  constexpr int RLS = P::RLS;
+  constexpr int H = P::H, Wh = P::Wh, NB = P::NB, T = P::T, D = P::D, M = P::M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* B0 = reinterpret_cast<C*>(smem_raw);
   C* B1 = B0 + NB;
   C* TW = B1 + NB;
+  C* COL0 = TW + P::TW_LEN;
   const int k = blockIdx.x;
   if (!live[k]) {  // dead filter: skipped by the operator (learning.cpp:96)
     if (mode == 0) {
@@ -481,49 +457,31 @@ mask_step(const cx<typename P::R>* __restrict__ c, cx<typename P::R>* __restrict
     return;
   }
   P::load_twiddles(TW, tw);
-  const C* s = c + (size_t)k * NB;
-  for (int it = threadIdx.x; it < P::HALF; it += T) {
-    const int r = it / W2, cc = it % W2;
-    const int b = r * Wh + cc;
-    B0[b] = (cc == 0) ? P::pack_col0(s[b], s[b + W2]) : s[b];
-  }
   __syncthreads();
-  C* sp = P::inverse(B0, B1, TW);
+  const C* s = c + (size_t)k * NB;
+  C* sp = P::inverse(B0, B1, TW, [&](int r, int cc) { return s[r * Wh + cc]; });
   const R invD = R(1) / R(D);
   if (mode == 1) {
     const double scale = -0.5 / fmax(mu[k], 1e-300);
     for (int i = threadIdx.x; i < mh * mw; i += T) {
       const int r = i / mw, cc = i % mw;
-      const C v = sp[(r / 2) * RLS + cc];
-      const R val = ((r & 1) ? v.y : v.x) * invD;
+      const C v = sp[r * Wh + cc / 2];
+      const R val = ((cc & 1) ? v.y : v.x) * invD;
       d_out[(size_t)k * mh * mw + i] = scale * (double)val;
     }
     return;
   }
-  for (int it = threadIdx.x; it < (H / 2) * W; it += T) {
-    const int pa = it / W, cc = it % W;
-    const C v = sp[pa * RLS + cc];
-    const bool in_c = cc < mw;
-    const R v0 = (in_c && 2 * pa < mh) ? v.x * invD : R(0);
-    const R v1 = (in_c && 2 * pa + 1 < mh) ? v.y * invD : R(0);
-    sp[pa * RLS + cc] = mk<C>(v0, v1);
+  for (int it = threadIdx.x; it < H * M; it += T) {
+    const int r = it / M, m = it % M;
+    const C v = sp[r * Wh + m];
+    const bool rin = r < mh;
+    const R v0 = (rin && 2 * m < mw) ? v.x * invD : R(0);
+    const R v1 = (rin && 2 * m + 1 < mw) ? v.y * invD : R(0);
+    sp[r * Wh + m] = mk<C>(v0, v1);
   }
   __syncthreads();
   C* other = (sp == B0) ? B1 : B0;
-  C* spec = P::forward(sp, other, TW);
-  C* o = phat + (size_t)k * NB;
-  for (int it = threadIdx.x; it < P::HALF; it += T) {
-    const int r = it / W2, cc = it % W2;
-    const int b = r * Wh + cc;
-    if (cc == 0) {
-      C x0, xn;
-      P::unpack_col0(spec, r, x0, xn);
-      o[b] = x0;
-      o[b + W2] = xn;
-    } else {
-      o[b] = spec[b];
-    }
-  }
+  forward_to_global<P>(sp, other, TW, COL0, phat + (size_t)k * NB);
 }
 
 // Parseval weight of a half-spectrum bin: columns 0 and W/2 are their own
