@@ -198,6 +198,13 @@ template <class L> struct CountStages;
 template <int... Rs> struct CountStages<RadixList<Rs...>> { static constexpr int value = sizeof...(Rs); };
 template <int R, class L> struct Prepend;
 template <int R, int... Rs> struct Prepend<R, RadixList<Rs...>> { using type = RadixList<R, Rs...>; };
+template <class L, int R> struct Append;
+template <int R, int... Rs> struct Append<RadixList<Rs...>, R> { using type = RadixList<Rs..., R>; };
+template <class L> struct Reverse;
+template <> struct Reverse<RadixList<>> { using type = RadixList<>; };
+template <int R, int... Rs> struct Reverse<RadixList<R, Rs...>> {
+  using type = typename Append<typename Reverse<RadixList<Rs...>>::type, R>::type;
+};
 template <class L> struct Split;
 template <int R> struct Split<RadixList<R>> {
   static constexpr int first = R, last = R;
@@ -210,6 +217,24 @@ template <int R, int R2, int... Rs> struct Split<RadixList<R, R2, Rs...>> {
   using tail = RadixList<R2, Rs...>;
   using init = typename Prepend<R, typename rest::init>::type;
 };
+
+// Stage twiddles x[q] *= W_L^(q k STEP): powers of two come from the table,
+// the rest are composed (depth <= log2 R multiplies), cutting table loads from
+// R-1 to log2(R) per butterfly.
+template <class C, int R, int STEP, bool INV>
+__device__ __forceinline__ void stage_twiddle(C* x, const C* __restrict__ tw, int k) {
+  C w[R];
+  sfor<1, R>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    if constexpr ((q & (q - 1)) == 0) {
+      w[q] = tw[q * k * STEP];
+    } else {
+      constexpr int hb = 1 << (31 - __builtin_clz(q));
+      w[q] = cmul(w[hb], w[q - hb]);
+    }
+    x[q] = INV ? cmulc(w[q], x[q]) : cmul(x[q], w[q]);
+  });
+}
 
 // One Stockham stage over LINES lines of length L, radix R, NS = product of
 // the radices already applied. load(line, idx) / store(line, idx, v) address
@@ -226,13 +251,7 @@ __device__ __forceinline__ void stockham(const C* __restrict__ tw, LOAD&& load, 
     C x[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) x[q] = load(b, j + q * J);
-    if constexpr (NS > 1) {
-#pragma unroll
-      for (int q = 1; q < R; ++q) {
-        const C w = tw[q * k * (L / (NS * R))];
-        x[q] = INV ? cmulc(w, x[q]) : cmul(x[q], w);
-      }
-    }
+    if constexpr (NS > 1) stage_twiddle<C, R, L / (NS * R), INV>(x, tw, k);
     dft<R, INV>(x);
     const int o = (j / NS) * NS * R + k;
 #pragma unroll
@@ -341,10 +360,7 @@ struct Plane {
         C x[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) x[q] = load(col, j + q * J);
-        if constexpr (NS > 1) {
-#pragma unroll
-          for (int q = 1; q < R; ++q) x[q] = cmul(x[q], twc[q * j * (H / (NS * R))]);
-        }
+        if constexpr (NS > 1) stage_twiddle<C, R, H / (NS * R), false>(x, twc, j);
         dft<R, false>(x);
         if (col == 0) {
 #pragma unroll
@@ -369,6 +385,94 @@ struct Plane {
       consume_store([&](int l, int i) { return in[i * Wh + l]; }, std::integral_constant<int, NSL>{},
                     std::integral_constant<int, S::last>{});
     }
+  }
+
+  // Accumulating variant of cols_fwd for the coding pass: the last stage adds
+  // d_hat(r,c) * X(r,c) into per-thread registers acc[i][s] (item i = tid + i*T,
+  // output row j + s*NS). Bin ownership is fixed across calls, so acc lives in
+  // registers for a whole filter group. Column 0 goes to col0 as in cols_fwd.
+  static constexpr int LAST_R = Split<ColPlan>::last;
+  static constexpr int LAST_NS = H / LAST_R;
+  static constexpr int LAST_ITEMS = M * (H / LAST_R);
+  static constexpr int LAST_IPT = (LAST_ITEMS + T - 1) / T;
+  __device__ static __forceinline__ void acc_bin(int i, int s, int& r, int& c) {
+    const int it = threadIdx.x + i * T;
+    c = it % M;
+    r = it / M + s * LAST_NS;
+  }
+  __device__ static __forceinline__ void cols_fwd_acc(C* z, C* b, const C* tw, C* col0, const C* __restrict__ dk,
+                                                      C (&acc)[LAST_IPT][LAST_R]) {
+    using S = Split<ColPlan>;
+    constexpr int NST = CountStages<ColPlan>::value;
+    constexpr int R = LAST_R, NS = LAST_NS, J = H / R;
+    const C* twc = tw + TW_COL;
+    auto last = [&](auto&& load) {
+#pragma unroll
+      for (int i = 0; i < LAST_IPT; ++i) {
+        const int it = threadIdx.x + i * T;
+        if (LAST_IPT * T != LAST_ITEMS && it >= LAST_ITEMS) continue;
+        const int col = it % M, j = it / M;
+        C pv[R];
+        if (col != 0) {
+#pragma unroll
+          for (int s = 0; s < R; ++s) pv[s] = __ldg(dk + (j + s * NS) * Wh + col);
+        }
+        C x[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = load(col, j + q * J);
+        if constexpr (NS > 1) stage_twiddle<C, R, H / (NS * R), false>(x, twc, j);
+        dft<R, false>(x);
+        if (col == 0) {
+#pragma unroll
+          for (int s = 0; s < R; ++s) col0[j + s * NS] = x[s];
+        } else {
+#pragma unroll
+          for (int s = 0; s < R; ++s) acc[i][s] = cadd(acc[i][s], cmul(pv[s], x[s]));
+        }
+      }
+      __syncthreads();
+    };
+    auto post_load = [&](int col, int r) { return post(z, tw, r, col); };
+    if constexpr (NST == 1) {
+      last(post_load);
+    } else {
+      constexpr int R1 = S::first;
+      stockham<C, H, R1, 1, false, M, T>(twc, post_load, [&](int l, int i, C v) { b[i * Wh + l] = v; });
+      __syncthreads();
+      using Mid = typename Split<typename S::tail>::init;
+      C* in = run_stages<C, H, false, M, Wh, 1, T, R1>(b, z, twc, Mid{});
+      last([&](int l, int i) { return in[i * Wh + l]; });
+    }
+  }
+
+  // --- fused row boundary (coding pass) ---------------------------------
+  // The inverse row pass runs the forward plan reversed, so its last stage
+  // (radix RX, outputs m = j + s*M/RX) lines up with the forward pass's first
+  // stage (inputs m = j + q*M/RX): the prox can sit between them in registers.
+  using RowPlanI = typename Reverse<RowPlan>::type;
+  static constexpr int RI_N = CountStages<RowPlanI>::value;
+  static constexpr int RX = Split<RowPlan>::first;
+  static_assert(Split<RowPlanI>::last == RX, "plan reversal");
+  // All inverse row stages but the last (the first applies the c2r
+  // pre-processing); returns the last stage's input buffer (p itself if the
+  // plan has a single stage, whose load then applies the pre-processing).
+  __device__ static __forceinline__ C* rows_inv_head(C* p, C* b, const C* tw) {
+    if constexpr (RI_N == 1) {
+      return p;
+    } else {
+      using S = Split<RowPlanI>;
+      constexpr int R1 = S::first;
+      const C* twr = tw + TW_ROW;
+      stockham<C, M, R1, 1, true, H, T>(
+          twr, [&](int r, int k) { return pre(p, tw, r, k); }, [&](int l, int i, C v) { b[l * Wh + i] = v; });
+      __syncthreads();
+      using Mid = typename Split<typename S::tail>::init;
+      return run_stages<C, M, true, H, 1, Wh, T, R1>(b, p, twr, Mid{});
+    }
+  }
+  // Forward row stages after the first (the first is fused by the caller).
+  __device__ static __forceinline__ C* rows_fwd_tail(C* a, C* b, const C* tw) {
+    return run_stages<C, M, false, H, 1, Wh, T, RX>(a, b, tw + TW_ROW, typename Split<RowPlan>::tail{});
   }
 
   // --- inverse ---------------------------------------------------------

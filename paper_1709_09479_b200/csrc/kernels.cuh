@@ -54,13 +54,55 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// ---- TMA bulk copies (cp.async.bulk) with mbarrier completion (sm_90+/sm_100a)
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <class P>
 struct Smem {
   static constexpr size_t tw_bytes = sizeof(typename P::C) * (P::TW_LEN + P::H);  // + COL0
   static constexpr size_t two = 2 * P::buffer_bytes + tw_bytes;
   static constexpr size_t three = 3 * P::buffer_bytes + tw_bytes;
-  static constexpr bool acc_in_smem = three <= 220 * 1024;
-  static constexpr size_t coding = acc_in_smem ? three : two;
+  // per-filter ADMM state staged in smem by one TMA bulk copy (dense H x M pairs)
+  static constexpr int US = P::M;
+  static constexpr size_t u_bytes = sizeof(typename P::C) * P::H * US;
+  static constexpr size_t u_off = (two + 127) / 128 * 128;
+  static constexpr bool stage_u = u_off + u_bytes <= 220 * 1024;
+  static constexpr size_t coding = stage_u ? u_off + u_bytes : two;
 };
 
 // ----------------------------------------------------------------------------
@@ -81,21 +123,34 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   using R = typename P::R;
   using C = typename P::C;
   constexpr int H = P::H, W = P::W, Wh = P::Wh, NB = P::NB, D = P::D, T = P::T, M = P::M;
-  constexpr bool ACC_SMEM = Smem<P>::acc_in_smem;
-
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kSums * (T / 32)];
   C* B0 = reinterpret_cast<C*>(smem_raw);
   C* B1 = B0 + NB;
-  C* TW = B1 + NB + (ACC_SMEM ? NB : 0);
+  C* TW = B1 + NB;
   C* COL0 = TW + P::TW_LEN;
+  constexpr bool STAGE = (MODE == kPassAdmm) && Smem<P>::stage_u;
+  constexpr int US = Smem<P>::US;
+  C* U = reinterpret_cast<C*>(smem_raw + Smem<P>::u_off);
+  __shared__ __align__(8) unsigned long long ubar_s;
+  unsigned long long* ubar = &ubar_s;
+  unsigned uphase = 0;
   const int n = blockIdx.y, g = blockIdx.x;
   if (MODE == kPassAdmm && a.conv[n]) return;
-  C* ACC = ACC_SMEM ? (B1 + NB) : (a.part + ((size_t)n * a.G + g) * NB);
 
   P::load_twiddles(TW, a.tw);
-  for (int i = threadIdx.x; i < NB; i += T) ACC[i] = mk<C>(R(0), R(0));
+  if (STAGE && threadIdx.x == 0) {
+    mbar_init(ubar, 1);
+    fence_async_smem();
+  }
   __syncthreads();
+  // sum_k d_hat_k w_hat_k for this group, in registers of the bins' owners
+  C acc[P::LAST_IPT][P::LAST_R];
+#pragma unroll
+  for (int i = 0; i < P::LAST_IPT; ++i)
+#pragma unroll
+    for (int s = 0; s < P::LAST_R; ++s) acc[i][s] = mk<C>(R(0), R(0));
+  C acc0 = mk<C>(R(0), R(0)), accN = mk<C>(R(0), R(0));  // bins (tid, 0), (tid, W/2)
 
   const R rho = a.rho, beta = a.beta, invD = R(1) / R(D);
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
@@ -107,33 +162,46 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     if constexpr (MODE == kPassAdmm) {
       C* __restrict__ uk = reinterpret_cast<C*>(a.u + ((size_t)n * a.K + k) * D);  // pixel pairs
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
-      if (threadIdx.x == 0) {
-        prefetch_l2_bulk(uk, sizeof(R) * D);  // consumed after the inverse FFT
-        if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
+      if constexpr (STAGE) {
+        // TMA: this filter's u rows -> U (padded rows); lands during the inverse FFT
+        if (threadIdx.x == 0) {
+          bulk_wait_read0();  // the previous filter's U store has drained
+          mbar_expect_tx(ubar, (unsigned)(sizeof(C) * H * M));
+          bulk_g2s(U, uk, sizeof(C) * H * M, ubar);
+        }
+      } else if (threadIdx.x == 0) {
+        prefetch_l2_bulk(uk, sizeof(R) * D);
       }
-      C* sp = P::inverse(B0, B1, TW, [&](int r, int c) {
+      if (threadIdx.x == 0 && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
+      C* cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
         const int b = r * Wh + c;
         return cmulc(__ldg(dk + b), __ldg(lam + b));
       });
-      // prox on u (closed form of coding.cpp:237-246), pixel pairs, coalesced
-      constexpr int UP = 4;
-      constexpr int ITEMS = H * M;
-      R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
-      for (int base = 0; base < ITEMS; base += T * UP) {
-        C uv[UP];
-#pragma unroll
-        for (int q = 0; q < UP; ++q) {
-          const int it = base + q * T + threadIdx.x;
-          if (it < ITEMS) uv[q] = uk[it];
-        }
-#pragma unroll
-        for (int q = 0; q < UP; ++q) {
-          const int it = base + q * T + threadIdx.x;
-          if (it >= ITEMS) continue;
+      C* hin = P::rows_inv_head(cs, cs == B0 ? B1 : B0, TW);
+      C* fout = (hin == B0) ? B1 : B0;
+      // last inverse row stage (plain), then the prox pass over the staged u
+      {
+        constexpr int RX = P::RX, J = M / RX;
+        const C* twr = TW + P::TW_ROW;
+        stockham<C, M, RX, J, true, H, T>(
+            twr,
+            [&](int r, int kk) { return (P::RI_N == 1) ? P::pre(hin, TW, r, kk) : hin[r * Wh + kk]; },
+            [&](int l, int i, C v) { fout[l * Wh + i] = v; });
+        __syncthreads();
+      }
+      if constexpr (STAGE) mbar_wait(ubar, uphase);
+      uphase ^= 1u;
+      {
+        R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
+        constexpr int ITEMS = H * M;
+#pragma unroll 4
+        for (int it = threadIdx.x; it < ITEMS; it += T) {
           const int r = it / M, m = it % M;
-          const C v = sp[r * Wh + m];
+          C* up = STAGE ? (U + it) : (uk + it);
+          const C uv = *up;
+          const C v = fout[r * Wh + m];
           const R tv[2] = {v.x * invD, v.y * invD};
-          const R uo[2] = {uv[q].x, uv[q].y};
+          const R uo[2] = {uv.x, uv.y};
           R wv[2], un2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -155,14 +223,30 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
             wv[e] = R(2) * th - un;
             un2[e] = un;
           }
-          uk[it] = mk<C>(un2[0], un2[1]);
-          sp[r * Wh + m] = mk<C>(wv[0], wv[1]);
+          *up = mk<C>(un2[0], un2[1]);
+          fout[r * Wh + m] = mk<C>(wv[0], wv[1]);
+        }
+        s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
+        s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
+      }
+      if constexpr (STAGE) fence_async_smem();
+      __syncthreads();
+      if constexpr (STAGE) {
+        if (threadIdx.x == 0) {
+          bulk_s2g(uk, U, sizeof(C) * H * M);
+          bulk_commit();
         }
       }
-      s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
-      s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
-      __syncthreads();
-      work = sp;
+      C* z = P::rows_fwd(fout, hin, TW);
+      P::cols_fwd_acc(z, z == B0 ? B1 : B0, TW, COL0, dk, acc);
+      if (threadIdx.x < H) {
+        const int r = threadIdx.x;
+        C x0, xn;
+        P::template unpack_col0<1>(COL0, r, x0, xn);
+        acc0 = cadd(acc0, cmul(__ldg(dk + r * Wh), x0));
+        accN = cadd(accN, cmul(__ldg(dk + r * Wh + M), xn));
+      }
+      continue;
     } else {
       const C* __restrict__ src = reinterpret_cast<const C*>(
           (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D);
@@ -190,25 +274,34 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     // forward r2c of w with acc += d_hat_k w_hat_k fused into the last column stage
     C* other = (work == B0) ? B1 : B0;
     C* z = P::rows_fwd(work, other, TW);
-    P::cols_fwd(z, z == work ? other : work, TW, COL0,
-                [&](int r, int c) { return __ldg(dk + r * Wh + c); },
-                [&](int r, int c, C v, C d) {
-                  C& acc = ACC[r * Wh + c];
-                  acc = cadd(acc, cmul(d, v));
-                });
-    for (int r = threadIdx.x; r < H; r += T) {
+    P::cols_fwd_acc(z, z == work ? other : work, TW, COL0, dk, acc);
+    static_assert(H <= T, "column-0 owners: one thread per row");
+    if (threadIdx.x < H) {
+      const int r = threadIdx.x;
       C x0, xn;
       P::template unpack_col0<1>(COL0, r, x0, xn);
-      C& a0 = ACC[r * Wh];
-      C& an = ACC[r * Wh + M];
-      a0 = cadd(a0, cmul(__ldg(dk + r * Wh), x0));
-      an = cadd(an, cmul(__ldg(dk + r * Wh + M), xn));
+      acc0 = cadd(acc0, cmul(__ldg(dk + r * Wh), x0));
+      accN = cadd(accN, cmul(__ldg(dk + r * Wh + M), xn));
     }
   }
-  __syncthreads();
-  if constexpr (ACC_SMEM) {
+  if (STAGE && threadIdx.x == 0) bulk_wait0();  // u stores complete before the CTA retires
+  {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
-    for (int i = threadIdx.x; i < NB; i += T) dst[i] = ACC[i];
+#pragma unroll
+    for (int i = 0; i < P::LAST_IPT; ++i) {
+      const int it = threadIdx.x + i * T;
+      if (it >= P::LAST_ITEMS || it % M == 0) continue;
+#pragma unroll
+      for (int s = 0; s < P::LAST_R; ++s) {
+        int r, c;
+        P::acc_bin(i, s, r, c);
+        dst[r * Wh + c] = acc[i][s];
+      }
+    }
+    if (threadIdx.x < H) {
+      dst[threadIdx.x * Wh] = acc0;
+      dst[threadIdx.x * Wh + M] = accN;
+    }
   }
   // reductions of the partial sums (FP64)
   double v[7] = {s0, s1, s2, s3, s4, s5, 0.0};
