@@ -278,6 +278,8 @@ class Engine final : public EngineBase {
     p_.alloc(sizeof(C) * nNB);
     ap_.alloc(sizeof(C) * nNB);
     cvec_.alloc(sizeof(C) * (size_t)K_ * NB);
+    csplit_ = std::max(1, std::min(64, (N_ + 31) / 32));  // images per contract_c chunk <= 32
+    cpart_.alloc(sizeof(double2) * (size_t)csplit_ * K_ * NB);
     phat_.alloc(sizeof(C) * (size_t)K_ * NB);
     live_.alloc(sizeof(int) * K_);
     dmu_.alloc(sizeof(double) * K_);
@@ -688,20 +690,32 @@ class Engine final : public EngineBase {
     zhat_valid_ = true;
   }
 
-  // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
-  void apply_hat(const C* v, C* out) {
-    const dim3 g1((NB + TBV - 1) / TBV, K_);
+  // c_k = sum_n conj(z_hat_nk) v_n (split over image chunks, fixed-order reduce)
+  void correlate_hat(const C* v, const int* done) {
+    constexpr int KC = 8;
+    const dim3 g1((NB + TBV - 1) / TBV, (K_ + KC - 1) / KC, csplit_);
     launch(kFamContract, [&] {
-      contract_c<R><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), v, cvec_.as<C>(), live_.as<int>(), N_, K_, NB);
+      contract_c<R, KC><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), v, cpart_.as<double2>(), live_.as<int>(), N_, K_, NB,
+                                             done);
     });
+    const size_t knb = (size_t)K_ * NB;
+    launch(kFamContract, [&] {
+      contract_c_reduce<R><<<(unsigned)((knb + 255) / 256), 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(),
+                                                                           csplit_, knb, done);
+    });
+  }
+
+  // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
+  void apply_hat(const C* v, C* out, const int* done = nullptr) {
+    correlate_hat(v, done);
     launch(kFamMask, [&] {
       mask_step<P><<<K_, T, Smem<P>::two, st_>>>(cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(),
-                                                 dmu_.as<double>(), mh_, mw_, 0, dtw_.as<C>());
+                                                 dmu_.as<double>(), mh_, mw_, 0, dtw_.as<C>(), done);
     });
     const dim3 g3(tiles_, N_);
     launch(kFamContract, [&] {
       contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(), live_.as<int>(),
-                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0);
+                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0, done);
     });
   }
 
@@ -719,7 +733,9 @@ class Engine final : public EngineBase {
     return *h;
   }
 
-  // gamma_solve (learning.cpp:136-185), warm-started, on half spectra
+  // gamma_solve (learning.cpp:136-185), warm-started, on half spectra. The
+  // iteration loop terminates on the device (CgState::done); the host issues
+  // iterations in chunks and reads the state once per chunk.
   void gamma_solve(double bnorm, int& iters, bool& converged) {
     iters = 0;
     converged = false;
@@ -732,6 +748,8 @@ class Engine final : public EngineBase {
     }
     CgState init{};
     init.bnorm = bnorm;
+    init.tol = cfg_.cg_tol;
+    init.max_iters = cfg_.cg_max;
     CK(cudaMemcpyAsync(cg_.p, &init, sizeof(CgState), cudaMemcpyHostToDevice, st_));
     apply_hat(gam_.as<C>(), ap_.as<C>());
     launch(kFamOther, [&] {
@@ -740,46 +758,42 @@ class Engine final : public EngineBase {
     });
     const double invD = 1.0 / D;
     launch(kFamOther, [&] { cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 0); });
+    const int* done = &cg_.as<CgState>()->done;
     CgState s = read_cg();
-    if (s.rel <= cfg_.cg_tol) {
-      converged = true;
-      return;
-    }
-    for (int it = 1; it <= cfg_.cg_max; ++it) {
-      apply_hat(p_.as<C>(), ap_.as<C>());
-      launch(kFamOther, [&] {
-        cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), N_ * tiles_, invD, cg_.as<CgState>(), 1);
-      });
-      launch(kFamOther, [&] {
-        cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_.as<C>(), r_.as<C>(), p_.as<C>(), ap_.as<C>(),
-                                                cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh);
-      });
-      launch(kFamOther, [&] {
-        cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 2);
-      });
-      launch(kFamOther, [&] {
-        cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(r_.as<C>(), p_.as<C>(), cg_.as<CgState>(), total);
-      });
-      s = read_cg();
-      if (s.bad) break;  // pAp <= 0 guard (learning.cpp:166): gamma unchanged this step
-      iters = it;
-      if (s.rel <= cfg_.cg_tol) {
-        converged = true;
-        break;
+    int issued = 0, chunk = 2;
+    while (!s.done && issued < cfg_.cg_max) {
+      const int n = std::min(chunk, cfg_.cg_max - issued);
+      for (int c = 0; c < n; ++c) {
+        apply_hat(p_.as<C>(), ap_.as<C>(), done);
+        launch(kFamOther, [&] {
+          cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), N_ * tiles_, invD, cg_.as<CgState>(), 1);
+        });
+        launch(kFamOther, [&] {
+          cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_.as<C>(), r_.as<C>(), p_.as<C>(), ap_.as<C>(),
+                                                  cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh);
+        });
+        launch(kFamOther, [&] {
+          cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 2);
+        });
+        launch(kFamOther, [&] {
+          cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(r_.as<C>(), p_.as<C>(), cg_.as<CgState>(), total);
+        });
       }
+      issued += n;
+      chunk = std::min(chunk * 2, 8);
+      s = read_cg();
     }
+    iters = s.iters;
+    converged = s.converged != 0;
   }
 
   // d_recover (learning.cpp:187-216): d_k = -0.5/max(mu_k,1e-300) crop(iDFT(sum_n conj(z_nk) gamma_n))
   void d_recover(std::vector<double>& d) {
-    const dim3 g1((NB + TBV - 1) / TBV, K_);
-    launch(kFamContract, [&] {
-      contract_c<R><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), gam_.as<C>(), cvec_.as<C>(), live_.as<int>(), N_, K_, NB);
-    });
+    correlate_hat(gam_.as<C>(), nullptr);
     // d_recover does not skip dead filters; their correlation is exactly zero anyway
     launch(kFamMask, [&] {
       mask_step<P><<<K_, T, Smem<P>::two, st_>>>(cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(),
-                                                 dmu_.as<double>(), mh_, mw_, 1, dtw_.as<C>());
+                                                 dmu_.as<double>(), mh_, mw_, 1, dtw_.as<C>(), nullptr);
     });
     d.resize((size_t)K_ * M_);
     CK(cudaMemcpyAsync(d.data(), dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
@@ -881,7 +895,8 @@ class Engine final : public EngineBase {
     const dim3 g3(tiles_, N_);
     launch(kFamContract, [&] {
       contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), dcand_.as<C>(), dwk_.as<double>(), live_.as<int>(),
-                                                 xhat_.as<C>(), nullptr, partial_.as<double>(), N_, K_, NB, Wh, 1);
+                                                 xhat_.as<C>(), nullptr, partial_.as<double>(), N_, K_, NB, Wh, 1,
+                                                 nullptr);
     });
     launch(kFamOther, [&] {
       per_image_reduce<<<N_, 256, 0, st_>>>(partial_.as<double>(), tiles_, 0.5 / D, odata_.as<double>());
@@ -1099,12 +1114,12 @@ class Engine final : public EngineBase {
   };
   dcsc_cuda_opts o_;
   dcsc_solver_config cfg_;
-  int N_, K_, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_;
+  int N_, K_, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1;
   cudaStream_t st_ = nullptr;
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_;
+      partial_, partial2_, l0_, zhat_, cpart_;
   std::vector<double> dict_, mu_, xnorm2_, xs_host_;
   std::vector<int> live_h_;
   std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero

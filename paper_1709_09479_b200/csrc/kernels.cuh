@@ -531,7 +531,8 @@ template <class P>
 __global__ void __launch_bounds__(P::T)
 mask_step(const cx<typename P::R>* __restrict__ c, cx<typename P::R>* __restrict__ phat,
           double* __restrict__ d_out, const int* live, const double* mu, int mh, int mw, int mode,
-          const cx<typename P::R>* tw) {
+          const cx<typename P::R>* tw, const int* done) {
+  if (done && *done) return;
   using R = typename P::R;
   using C = typename P::C;
   constexpr int H = P::H, Wh = P::Wh, NB = P::NB, T = P::T, D = P::D, M = P::M;
@@ -585,27 +586,75 @@ __device__ __forceinline__ double bin_weight(int b, int Wh) {
 }
 
 // c_k(w) = sum_n conj(z_hat_nk(w)) v_hat_n(w)   (learning.cpp:97-102, 204-209)
-template <class R>
-__global__ void contract_c(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ v,
-                           cx<R>* __restrict__ c, const int* __restrict__ live, int N, int K,
-                           int NB) {
+// The image sum is split over gridDim.z chunks (FP64 partials, fixed-order
+// second pass in contract_c_reduce) so that N >> 1 still fills the machine.
+template <class R, int KC>
+__global__ void __launch_bounds__(256)
+contract_c(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ v, double2* __restrict__ cpart,
+           const int* __restrict__ live, int N, int K, int NB, const int* done) {
+  if (done && *done) return;
   using C = cx<R>;
-  const int k = blockIdx.y;
+  // CTA = (bin tile, chunk of KC filters, image chunk); v_hat_n(b) is loaded
+  // once per image and reused for the KC filters.
+  const int k0 = blockIdx.y * KC;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= NB) return;
-  double ar = 0.0, ai = 0.0;
-  if (live[k]) {
-    const C* zp = zhat + (size_t)k * NB + b;
-    const size_t zs = (size_t)K * NB;
-#pragma unroll 4
-    for (int n = 0; n < N; ++n) {
-      const C z = zp[(size_t)n * zs];
-      const C x = v[(size_t)n * NB + b];
-      ar += (double)z.x * (double)x.x + (double)z.y * (double)x.y;
-      ai += (double)z.x * (double)x.y - (double)z.y * (double)x.x;
+  const int per = (N + gridDim.z - 1) / gridDim.z;
+  const int n0 = blockIdx.z * per, n1 = min(N, n0 + per);
+  double ar[KC], ai[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) ar[q] = ai[q] = 0.0;
+  const size_t zs = (size_t)K * NB;
+  const C* zp = zhat + (size_t)k0 * NB + b;
+  const int kn = min(KC, K - k0);
+  if (kn == KC) {
+#pragma unroll 2
+    for (int n = n0; n < n1; ++n) {
+      const C x = __ldg(v + (size_t)n * NB + b);
+      C z[KC];
+#pragma unroll
+      for (int q = 0; q < KC; ++q) z[q] = __ldg(zp + (size_t)n * zs + (size_t)q * NB);
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        ar[q] += (double)z[q].x * (double)x.x + (double)z[q].y * (double)x.y;
+        ai[q] += (double)z[q].x * (double)x.y - (double)z[q].y * (double)x.x;
+      }
+    }
+  } else {
+    for (int n = n0; n < n1; ++n) {
+      const C x = __ldg(v + (size_t)n * NB + b);
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        if (q < kn) {
+          const C z = __ldg(zp + (size_t)n * zs + (size_t)q * NB);
+          ar[q] += (double)z.x * (double)x.x + (double)z.y * (double)x.y;
+          ai[q] += (double)z.x * (double)x.y - (double)z.y * (double)x.x;
+        }
+      }
     }
   }
-  c[(size_t)k * NB + b] = mk<C>(R(ar), R(ai));
+#pragma unroll
+  for (int q = 0; q < KC; ++q) {
+    if (q >= kn) break;
+    // dead filters: exactly zero (the operator skips them, learning.cpp:96)
+    const bool lv = live[k0 + q] != 0;
+    cpart[((size_t)blockIdx.z * K + k0 + q) * NB + b] = make_double2(lv ? ar[q] : 0.0, lv ? ai[q] : 0.0);
+  }
+}
+
+template <class R>
+__global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __restrict__ c, int splits,
+                                  size_t KNB, const int* done) {
+  if (done && *done) return;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= KNB) return;
+  double ar = 0.0, ai = 0.0;
+  for (int s = 0; s < splits; ++s) {
+    const double2 p = cpart[(size_t)s * KNB + i];
+    ar += p.x;
+    ai += p.y;
+  }
+  c[i] = mk<cx<R>>(R(ar), R(ai));
 }
 
 // out_n = v_n + sum_k (0.5/mu_k) z_hat_nk p_hat_k (learning.cpp:109-121, in the
@@ -616,23 +665,43 @@ template <class R, int TB>
 __global__ void __launch_bounds__(TB)
 contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const double* __restrict__ wk,
              const int* __restrict__ live, const cx<R>* __restrict__ v, cx<R>* __restrict__ out,
-             double* __restrict__ partial, int N, int K, int NB, int Wh, int mode) {
+             double* __restrict__ partial, int N, int K, int NB, int Wh, int mode, const int* done) {
   using C = cx<R>;
   __shared__ double red[TB / 32];
+  if (done && *done) return;
   const int n = blockIdx.y;
   const int b = blockIdx.x * TB + threadIdx.x;
   double dot = 0.0;
   if (b < NB) {
+    // Dead filters have identically zero z_hat (and p_hat), so summing them
+    // adds exact zeros: no per-filter branch, loads batched 8 deep.
     double ar = 0.0, ai = 0.0;
     const C* zp = zhat + (size_t)n * K * NB + b;
-    for (int k = 0; k < K; ++k) {
-      if (!live[k]) continue;
-      const C z = zp[(size_t)k * NB];
-      const C q = p[(size_t)k * NB + b];
+    const C* pp = p + b;
+    constexpr int U = 8;
+    int k = 0;
+    for (; k + U <= K; k += U) {
+      C z[U], q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        z[u] = __ldg(zp + (size_t)(k + u) * NB);
+        q[u] = __ldg(pp + (size_t)(k + u) * NB);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double w = mode == 0 ? wk[k + u] : 1.0;
+        ar += w * ((double)z[u].x * (double)q[u].x - (double)z[u].y * (double)q[u].y);
+        ai += w * ((double)z[u].x * (double)q[u].y + (double)z[u].y * (double)q[u].x);
+      }
+    }
+    for (; k < K; ++k) {
+      const C z = __ldg(zp + (size_t)k * NB);
+      const C q = __ldg(pp + (size_t)k * NB);
       const double w = mode == 0 ? wk[k] : 1.0;
       ar += w * ((double)z.x * (double)q.x - (double)z.y * (double)q.y);
       ai += w * ((double)z.x * (double)q.y + (double)z.y * (double)q.x);
     }
+    (void)live;
     const C vv = v[(size_t)n * NB + b];
     if (mode == 0) {
       const C o = mk<C>(R((double)vv.x + ar), R((double)vv.y + ai));
@@ -690,10 +759,12 @@ cg_init(const cx<R>* __restrict__ xhat, const cx<R>* __restrict__ ap, cx<R>* __r
   block_partial<TB>(v, partial + blockIdx.x);
 }
 
+// Device-resident CG scalars. `done` stops every CG kernel (device-side loop
+// termination): set when the relative residual reaches tol, when pAp <= 0
+// (learning.cpp:166) or when the budget is spent.
 struct CgState {
-  double rr, pap, alpha, beta, rel, bnorm;
-  int bad;
-  int pad;
+  double rr, pap, alpha, beta, rel, bnorm, tol;
+  int bad, done, iters, max_iters, converged, pad;
 };
 
 // gamma += alpha p ; r -= alpha ap ; partial of rr_new
@@ -703,9 +774,10 @@ cg_update(cx<R>* __restrict__ gam, cx<R>* __restrict__ r, const cx<R>* __restric
           const cx<R>* __restrict__ ap, const CgState* st, double* partial, size_t total, int NB,
           int Wh) {
   using C = cx<R>;
+  if (st->done) return;
   const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
   double v = 0.0;
-  if (i < total && !st->bad) {
+  if (i < total) {
     const double al = st->alpha;
     const C pv = p[i], av = ap[i], gv = gam[i], rv0 = r[i];
     gam[i] = mk<C>(R(gv.x + al * pv.x), R(gv.y + al * pv.y));
@@ -722,16 +794,18 @@ __global__ void __launch_bounds__(TB)
 cg_pupdate(const cx<R>* __restrict__ r, cx<R>* __restrict__ p, const CgState* st, size_t total) {
   using C = cx<R>;
   const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
-  if (i >= total || st->bad) return;
+  if (i >= total || st->done) return;
   const double be = st->beta;
   const C rv = r[i], pv = p[i];
   p[i] = mk<C>(R(rv.x + be * pv.x), R(rv.y + be * pv.y));
 }
 
-// Single-block scalar step of CG. step 0: rr from the init residual; step 1:
-// pap -> alpha (guard pap <= 0, learning.cpp:166); step 2: rr_new -> rel, beta.
+// Single-block scalar step of CG. step 0: rr from the initial residual (done
+// when already below tol); step 1: pap -> alpha (pAp <= 0 stops, gamma
+// untouched, learning.cpp:166); step 2: rr_new -> rel, beta, iteration count.
 __global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step) {
   __shared__ double red[32];
+  if (step != 0 && st->done) return;
   double v = 0.0;
   // fixed-order strided partial sums, then a fixed-order tree: deterministic
   for (int i = threadIdx.x; i < count; i += blockDim.x) v += partial[i];
@@ -747,17 +821,28 @@ __global__ void cg_scalar(const double* partial, int count, double invD, CgState
     st->rr = s;
     st->rel = sqrt(s) / st->bnorm;
     st->bad = 0;
+    st->iters = 0;
+    st->converged = st->rel <= st->tol;
+    st->done = st->converged;
   } else if (step == 1) {
     st->pap = s;
     if (s <= 0.0) {
       st->bad = 1;
+      st->done = 1;
     } else {
       st->alpha = st->rr / s;
     }
   } else {
+    st->iters += 1;
     st->rel = sqrt(s) / st->bnorm;
     st->beta = s / st->rr;
     st->rr = s;
+    if (st->rel <= st->tol) {
+      st->converged = 1;
+      st->done = 1;
+    } else if (st->iters >= st->max_iters) {
+      st->done = 1;
+    }
   }
 }
 
