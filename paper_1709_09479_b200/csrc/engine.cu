@@ -17,6 +17,7 @@
 
 #include "dcsc_cuda.h"
 #include "kernels.cuh"
+#include "kernels_cluster.cuh"
 
 using namespace dcsc_cuda;
 
@@ -202,14 +203,104 @@ class EngineBase {
 
 constexpr int pick_threads(int H, int W) { return H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128); }
 
+// Kernel family per compiled grid: one CTA per plane (Plane), or a 4-CTA
+// cluster per plane (ClusterPlane) when the half spectrum exceeds smem.
+template <class R, int H, int W>
+struct KernelFamily {
+  static constexpr bool cluster = false;
+  static constexpr int CL = 1;
+  using P = Plane<R, H, W, pick_threads(H, W)>;
+};
+template <>
+struct KernelFamily<float, 256, 256> {
+  static constexpr bool cluster = true;
+  static constexpr int CL = 4;
+  using P = ClusterPlane<float, 256, 256, 4, 512>;
+};
+
 template <class R, int H, int W>
 class Engine final : public EngineBase {
  public:
-  static constexpr int T = pick_threads(H, W);
-  using P = Plane<R, H, W, T>;
+  using F = KernelFamily<R, H, W>;
+  using P = typename F::P;
+  static constexpr bool CLU = F::cluster;
+  static constexpr int CLN = F::CL;
+  static constexpr int T = P::T;
   using C = cx<R>;
   static constexpr int NB = P::NB, D = P::D, Wh = P::Wh;
   static constexpr int TBV = 256;  // block size of the streaming kernels
+
+  template <class Q = P>
+  static constexpr size_t smem_coding() {
+    if constexpr (CLU) return SmemCl<Q>::coding; else return Smem<Q>::coding;
+  }
+  template <class Q = P>
+  static constexpr size_t smem_plain() {
+    if constexpr (CLU) return SmemCl<Q>::plain; else return Smem<Q>::two;
+  }
+  template <int MODE>
+  static void launch_coding(int G, int cnt, cudaStream_t st, const CodingArgs<R>& a) {
+    if constexpr (CLU)
+      coding_pass_cl<P, MODE><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
+    else
+      coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+  }
+  template <class SRC>
+  static void launch_r2c(int count, cudaStream_t st, const SRC* src, size_t ss, C* dst, size_t ds, const C* tw,
+                         int* live, int live_mod) {
+    if constexpr (CLU)
+      r2c_planes_cl<P, SRC><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
+    else
+      r2c_planes<P, SRC><<<count, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
+  }
+  template <class DST>
+  static void launch_c2r(int count, cudaStream_t st, const C* src, size_t ss, DST* dst, size_t ds, const C* tw) {
+    if constexpr (CLU)
+      c2r_planes_cl<P, DST><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
+    else
+      c2r_planes<P, DST><<<count, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
+  }
+  static void launch_filters(int K, cudaStream_t st, const double* d, int mh, int mw, C* dst, const C* tw) {
+    if constexpr (CLU)
+      r2c_filters_cl<P><<<K * CLN, T, smem_plain(), st>>>(d, mh, mw, dst, tw);
+    else
+      r2c_filters<P><<<K, T, smem_plain(), st>>>(d, mh, mw, dst, tw);
+  }
+  static void launch_mask(int K, cudaStream_t st, const C* c, C* phat, double* d_out, const int* live,
+                          const double* mu, int mh, int mw, int mode, const C* tw, const int* done) {
+    if constexpr (CLU)
+      mask_step_cl<P><<<K * CLN, T, smem_plain(), st>>>(c, phat, d_out, live, mu, mh, mw, mode, tw, done);
+    else
+      mask_step<P><<<K, T, smem_plain(), st>>>(c, phat, d_out, live, mu, mh, mw, mode, tw, done);
+  }
+  static void set_attributes() {
+    auto big = [](const void* fn, size_t bytes) {
+      if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    };
+    if constexpr (CLU) {
+      big((const void*)coding_pass_cl<P, kPassAdmm>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassPrologue>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassObjective>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassMaps>, smem_coding());
+      big((const void*)r2c_planes_cl<P, R>, smem_plain());
+      big((const void*)r2c_planes_cl<P, double>, smem_plain());
+      big((const void*)c2r_planes_cl<P, R>, smem_plain());
+      big((const void*)c2r_planes_cl<P, double>, smem_plain());
+      big((const void*)r2c_filters_cl<P>, smem_plain());
+      big((const void*)mask_step_cl<P>, smem_plain());
+    } else {
+      big((const void*)coding_pass<P, kPassAdmm>, smem_coding());
+      big((const void*)coding_pass<P, kPassPrologue>, smem_coding());
+      big((const void*)coding_pass<P, kPassObjective>, smem_coding());
+      big((const void*)coding_pass<P, kPassMaps>, smem_coding());
+      big((const void*)r2c_planes<P, R>, smem_plain());
+      big((const void*)r2c_planes<P, double>, smem_plain());
+      big((const void*)c2r_planes<P, R>, smem_plain());
+      big((const void*)c2r_planes<P, double>, smem_plain());
+      big((const void*)r2c_filters<P>, smem_plain());
+      big((const void*)mask_step<P>, smem_plain());
+    }
+  }
 
   explicit Engine(const dcsc_cuda_opts& o) : o_(o), cfg_(o.cfg) {
     N_ = o.n_images;
@@ -228,8 +319,13 @@ class Engine final : public EngineBase {
     {
       int sms = 148, per_sm = 1;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coding_pass<P, kPassAdmm>, T, Smem<P>::coding));
-      const long slots = (long)sms * std::max(per_sm, 1);
+      long slots;
+      if constexpr (CLU) {
+        slots = sms / CLN;  // one CTA per SM (smem-bound), CLN CTAs per plane
+      } else {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coding_pass<P, kPassAdmm>, T, smem_coding()));
+        slots = (long)sms * std::max(per_sm, 1);
+      }
       long best = -1;
       int bestG = 1;
       for (int G = 1; G <= K_; ++G) {
@@ -262,7 +358,7 @@ class Engine final : public EngineBase {
     lamhat_.alloc(sizeof(C) * nNB);
     lam_.alloc(sizeof(R) * nD);
     part_.alloc(sizeof(C) * (size_t)N_ * G_ * NB);
-    sums_.alloc(sizeof(double) * (size_t)N_ * G_ * kSums);
+    sums_.alloc(sizeof(double) * (size_t)N_ * G_ * CLN * kSums);
     conv_.alloc(sizeof(int) * N_);
     cnt_.alloc(sizeof(unsigned) * N_);
     CK(cudaMemset(cnt_.p, 0, cnt_.bytes));
@@ -339,21 +435,7 @@ class Engine final : public EngineBase {
     ++launches;
   }
 
-  void setup_attributes() {
-    auto big = [](const void* fn, size_t bytes) {
-      if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    };
-    big((const void*)coding_pass<P, kPassAdmm>, Smem<P>::coding);
-    big((const void*)coding_pass<P, kPassPrologue>, Smem<P>::coding);
-    big((const void*)coding_pass<P, kPassObjective>, Smem<P>::coding);
-    big((const void*)coding_pass<P, kPassMaps>, Smem<P>::coding);
-    big((const void*)r2c_planes<P, R>, Smem<P>::two);
-    big((const void*)r2c_planes<P, double>, Smem<P>::two);
-    big((const void*)c2r_planes<P, R>, Smem<P>::two);
-    big((const void*)c2r_planes<P, double>, Smem<P>::two);
-    big((const void*)r2c_filters<P>, Smem<P>::two);
-    big((const void*)mask_step<P>, Smem<P>::two);
-  }
+  void setup_attributes() { set_attributes(); }
 
   CodingArgs<R> cargs(const C* dhat, int n_off) {
     CodingArgs<R> a;
@@ -362,7 +444,7 @@ class Engine final : public EngineBase {
     a.u = u_.as<R>() + (size_t)n_off * K_ * D;
     a.maps = maps_.as<R>() + (size_t)n_off * K_ * D;
     a.part = part_.as<C>() + (size_t)n_off * G_ * NB;
-    a.sums = sums_.as<double>() + (size_t)n_off * G_ * kSums;
+    a.sums = sums_.as<double>() + (size_t)n_off * G_ * CLN * kSums;
     a.conv = conv_.as<int>() + n_off;
     a.lamhat = lamhat_.as<C>() + (size_t)n_off * NB;
     a.K = K_;
@@ -387,9 +469,7 @@ class Engine final : public EngineBase {
     CodingArgs<R> a = cargs(dhat, n0);
     a.iter = iter;
     a.is_last = is_last;
-    launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] {
-      coding_pass<P, MODE><<<dim3(G_, cnt), T, Smem<P>::coding, st_>>>(a);
-    });
+    launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] { launch_coding<MODE>(G_, cnt, st_, a); });
   }
 
   void r2c(const void* src, bool src_double, size_t src_stride, C* dst, size_t dst_stride, int count,
@@ -397,27 +477,23 @@ class Engine final : public EngineBase {
     if (count <= 0) return;
     launch(kFamOther, [&] {
       if (src_double)
-        r2c_planes<P, double><<<count, T, Smem<P>::two, st_>>>(static_cast<const double*>(src), src_stride,
-                                                                dst, dst_stride, dtw_.as<C>(), live, live_mod);
+        launch_r2c<double>(count, st_, static_cast<const double*>(src), src_stride, dst, dst_stride, dtw_.as<C>(),
+                           live, live_mod);
       else
-        r2c_planes<P, R><<<count, T, Smem<P>::two, st_>>>(static_cast<const R*>(src), src_stride, dst,
-                                                           dst_stride, dtw_.as<C>(), live, live_mod);
+        launch_r2c<R>(count, st_, static_cast<const R*>(src), src_stride, dst, dst_stride, dtw_.as<C>(), live,
+                      live_mod);
     });
   }
 
   template <class DST>
   void c2r(const C* src, size_t src_stride, DST* dst, size_t dst_stride, int count) {
     if (count <= 0) return;
-    launch(kFamOther, [&] {
-      c2r_planes<P, DST><<<count, T, Smem<P>::two, st_>>>(src, src_stride, dst, dst_stride, dtw_.as<C>(), nullptr);
-    });
+    launch(kFamOther, [&] { launch_c2r<DST>(count, st_, src, src_stride, dst, dst_stride, dtw_.as<C>()); });
   }
 
   void upload_dict_spectra(const double* d, C* dst) {
     CK(cudaMemcpyAsync(ddict_.p, d, sizeof(double) * K_ * M_, cudaMemcpyHostToDevice, st_));
-    launch(kFamOther, [&] {
-      r2c_filters<P><<<K_, T, Smem<P>::two, st_>>>(ddict_.as<double>(), mh_, mw_, dst, dtw_.as<C>());
-    });
+    launch(kFamOther, [&] { launch_filters(K_, st_, ddict_.as<double>(), mh_, mw_, dst, dtw_.as<C>()); });
   }
 
   // ------------------------------------------------------------ API
@@ -709,8 +785,8 @@ class Engine final : public EngineBase {
   void apply_hat(const C* v, C* out, const int* done = nullptr) {
     correlate_hat(v, done);
     launch(kFamMask, [&] {
-      mask_step<P><<<K_, T, Smem<P>::two, st_>>>(cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(),
-                                                 dmu_.as<double>(), mh_, mw_, 0, dtw_.as<C>(), done);
+      launch_mask(K_, st_, cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(), dmu_.as<double>(), mh_, mw_, 0,
+                  dtw_.as<C>(), done);
     });
     const dim3 g3(tiles_, N_);
     launch(kFamContract, [&] {
@@ -792,8 +868,8 @@ class Engine final : public EngineBase {
     correlate_hat(gam_.as<C>(), nullptr);
     // d_recover does not skip dead filters; their correlation is exactly zero anyway
     launch(kFamMask, [&] {
-      mask_step<P><<<K_, T, Smem<P>::two, st_>>>(cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(),
-                                                 dmu_.as<double>(), mh_, mw_, 1, dtw_.as<C>(), nullptr);
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
+                  dtw_.as<C>(), nullptr);
     });
     d.resize((size_t)K_ * M_);
     CK(cudaMemcpyAsync(d.data(), dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
@@ -919,8 +995,8 @@ class Engine final : public EngineBase {
   void objective_pass(const C* dhat, std::vector<double>& data, std::vector<double>& l1) {
     coding_launch<MODE>(dhat, 0, N_);
     launch(kFamOther, [&] {
-      objective_reduce<R><<<N_, 256, 0, st_>>>(part_.as<C>(), sums_.as<double>(), xhat_.as<C>(), G_, NB, Wh, 1.0 / D,
-                                               cfg_.beta, odata_.as<double>(), ol1_.as<double>());
+      objective_reduce<R><<<N_, 256, 0, st_>>>(part_.as<C>(), sums_.as<double>(), xhat_.as<C>(), G_, G_ * CLN, NB,
+                                               Wh, 1.0 / D, cfg_.beta, odata_.as<double>(), ol1_.as<double>());
     });
     data.resize(N_);
     l1.resize(N_);
@@ -1140,7 +1216,8 @@ class Engine final : public EngineBase {
   X(float, 20, 20)    \
   X(float, 64, 64)    \
   X(float, 100, 100)  \
-  X(float, 128, 128)
+  X(float, 128, 128)  \
+  X(float, 256, 256)
 
 int prec_of(const char* t) { return std::strcmp(t, "double") == 0 ? 64 : 32; }
 
@@ -1167,13 +1244,10 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
   using E = Engine<R, H, W>;
   using P = typename E::P;
   using C = cx<R>;
-  constexpr int NB = P::NB, D = P::D, T = E::T;
+  constexpr int NB = P::NB, D = P::D;
   static bool attr = false;
   if (!attr) {
-    if (Smem<P>::two > 48 * 1024) {
-      CK(cudaFuncSetAttribute((const void*)r2c_planes<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<P>::two));
-      CK(cudaFuncSetAttribute((const void*)c2r_planes<P, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<P>::two));
-    }
+    E::set_attributes();
     attr = true;
   }
   std::vector<C> tw(P::TW_LEN);
@@ -1185,7 +1259,7 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
   if (!inverse) {
     din.alloc(sizeof(double) * (size_t)batch * D);
     CK(cudaMemcpy(din.p, in, din.bytes, cudaMemcpyHostToDevice));
-    r2c_planes<P, double><<<batch, T, Smem<P>::two>>>(din.as<double>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+    E::template launch_r2c<double>(batch, 0, din.as<double>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
     CK(cudaGetLastError());
     std::vector<C> h((size_t)batch * NB);
     CK(cudaMemcpy(h.data(), spec.p, spec.bytes, cudaMemcpyDeviceToHost));
@@ -1198,7 +1272,7 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
     for (size_t i = 0; i < h.size(); ++i) h[i] = mk<C>(R(in[2 * i]), R(in[2 * i + 1]));
     CK(cudaMemcpy(spec.p, h.data(), spec.bytes, cudaMemcpyHostToDevice));
     dout.alloc(sizeof(double) * (size_t)batch * D);
-    c2r_planes<P, double><<<batch, T, Smem<P>::two>>>(spec.as<C>(), NB, dout.as<double>(), D, dtw.as<C>(), nullptr);
+    E::template launch_c2r<double>(batch, 0, spec.as<C>(), NB, dout.as<double>(), D, dtw.as<C>());
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, dout.p, dout.bytes, cudaMemcpyDeviceToHost));
   }

@@ -1,0 +1,196 @@
+// 2-D real FFT of one H x W plane split over a CL-CTA thread-block cluster
+// (sm_90+/sm_100a distributed shared memory), for planes whose half spectrum
+// does not fit one CTA's shared memory (C3: 256 x 256 FP32 = 258 KB).
+//
+// Ownership inside the cluster (rank c):
+//   column passes: columns [c*COLS, (c+1)*COLS) of the W/2 transformed columns,
+//                  all H rows, local layout [H][CS] (CS = COLS + 1, odd stride);
+//                  column 0 (in rank 0) carries the packed pair X[.][0] + i X[.][W/2]
+//   row passes:    rows [c*ROWS, (c+1)*ROWS), local layout [ROWS][Wh]
+// The transposes between the passes are fused into the first stage of the
+// following pass: its loads read the owning CTA's shared memory through
+// mapa + ld.shared::cluster, together with the r2c/c2r pre/post-processing
+// pairs (k, W/2-k). Cluster barriers order producer stores, remote reads and
+// buffer reuse. Conventions are those of fft2d.cuh (Plane).
+#pragma once
+#include "fft2d.cuh"
+
+namespace dcsc_cuda {
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float2 dsmem_ld(const float2* p, unsigned rank) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(r) : "memory");
+  return v;
+}
+__device__ __forceinline__ double2 dsmem_ld(const double2* p, unsigned rank) {
+  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(r) : "memory");
+  return v;
+}
+
+template <class Rt, int H_, int W_, int CL_, int T_>
+struct ClusterPlane {
+  using R = Rt;
+  using C = cx<Rt>;
+  static constexpr int H = H_, W = W_, T = T_, CL = CL_;
+  static constexpr int M = W / 2, Wh = M + 1, NB = H * Wh, D = H * W;
+  static constexpr int ROWS = H / CL, COLS = M / CL, CS = COLS + 1;
+  static_assert(H % CL == 0 && M % CL == 0, "cluster split");
+  static constexpr int BUF = (H * CS > ROWS * Wh) ? H * CS : ROWS * Wh;  // complex per buffer
+  static constexpr size_t buffer_bytes = sizeof(C) * BUF;
+  using RowPlan = typename PlanFor<M>::type;
+  using RowPlanI = typename Reverse<RowPlan>::type;
+  using ColPlan = typename PlanFor<H>::type;
+  static constexpr int TW_ROW = 0, TW_COL = M, TW_PP = M + H;
+  static constexpr int TW_LEN = 2 * M + H + 1;
+  static_assert(CountStages<ColPlan>::value >= 2, "column plan needs a transposing and a last stage");
+
+  __device__ static __forceinline__ void load_twiddles(C* tw_s, const C* __restrict__ tw_g) {
+    for (int i = threadIdx.x; i < TW_LEN; i += T) tw_s[i] = tw_g[i];
+  }
+  __device__ static __forceinline__ C pack_col0(C x0, C xn) { return mk<C>(x0.x - xn.y, x0.y + xn.x); }
+
+  // ---- inverse: column pass (local columns), input generated from global ----
+  // gen(r, col) returns natural bin (r, col), col in [0, M]. Returns the
+  // column-pass result buffer (a or b), layout [H][CS].
+  template <class GEN>
+  __device__ static __forceinline__ C* cols_inv(C* a, C* b, const C* tw, unsigned rank, GEN&& gen) {
+    using S = Split<ColPlan>;
+    constexpr int R1 = S::first;
+    const C* twc = tw + TW_COL;
+    const int c0 = rank * COLS;
+    stockham<C, H, R1, 1, true, COLS, T>(
+        twc,
+        [&](int cl, int r) {
+          const int col = c0 + cl;
+          return col == 0 ? pack_col0(gen(r, 0), gen(r, M)) : gen(r, col);
+        },
+        [&](int l, int i, C v) { a[i * CS + l] = v; });
+    __syncthreads();
+    return run_stages<C, H, true, COLS, CS, 1, T, R1>(a, b, twc, typename S::tail{});
+  }
+
+  // c2r pre-processing of global row rg at index k, reading the column-pass
+  // result `cb` (same offset in every CTA) of the owning ranks.
+  __device__ static __forceinline__ C pre_remote(const C* cb, const C* tw, int rg, int k) {
+    if (k == 0) {
+      const C q = dsmem_ld(cb + rg * CS, 0);
+      return mk<C>(q.x + q.y, q.x - q.y);
+    }
+    const C a = dsmem_ld(cb + rg * CS + (k % COLS), k / COLS);
+    const int km = M - k;
+    const C bb = dsmem_ld(cb + rg * CS + (km % COLS), km / COLS);
+    const C s = mk<C>(a.x + bb.x, a.y - bb.y);
+    const C d = mk<C>(a.x - bb.x, a.y + bb.y);
+    const C wd = cmulc(tw[TW_PP + k], d);
+    return mk<C>(s.x - wd.y, s.y + wd.x);
+  }
+
+  // ---- inverse row pass: first (transposing) stage reads the whole cluster's
+  // column results; the caller must cluster_sync before (producers done) and
+  // after (readers done) this stage. Writes `out` [ROWS][Wh]; returns nothing.
+  __device__ static __forceinline__ void rows_inv_first(const C* cb, C* out, const C* tw, unsigned rank) {
+    using S = Split<RowPlanI>;
+    constexpr int R1 = S::first;
+    const int r0 = rank * ROWS;
+    stockham<C, M, R1, 1, true, ROWS, T>(
+        tw + TW_ROW, [&](int rl, int k) { return pre_remote(cb, tw, r0 + rl, k); },
+        [&](int l, int i, C v) { out[l * Wh + i] = v; });
+  }
+  // remaining inverse row stages (local), input in a; returns result buffer
+  __device__ static __forceinline__ C* rows_inv_rest(C* a, C* b, const C* tw) {
+    using S = Split<RowPlanI>;
+    return run_stages<C, M, true, ROWS, 1, Wh, T, S::first>(a, b, tw + TW_ROW, typename S::tail{});
+  }
+
+  // ---- forward row pass (local rows) ----
+  __device__ static __forceinline__ C* rows_fwd(C* a, C* b, const C* tw) {
+    return run_stages<C, M, false, ROWS, 1, Wh, T, 1>(a, b, tw + TW_ROW, RowPlan{});
+  }
+
+  // r2c post-processing of global row r at column col from the row results
+  // `zb` (same offset in every CTA) of the owning ranks.
+  __device__ static __forceinline__ C post_remote(const C* zb, const C* tw, int r, int col) {
+    const unsigned own = r / ROWS;
+    const C* rowp = zb + (r % ROWS) * Wh;
+    const C z1 = dsmem_ld(rowp + col, own);
+    if (col == 0) return mk<C>(z1.x + z1.y, z1.x - z1.y);
+    const C z2 = dsmem_ld(rowp + (M - col), own);
+    const C e = mk<C>(R(0.5) * (z1.x + z2.x), R(0.5) * (z1.y - z2.y));
+    const C o = mk<C>(R(0.5) * (z1.y + z2.y), R(0.5) * (z2.x - z1.x));
+    return cadd(e, cmul(tw[TW_PP + col], o));
+  }
+
+  // ---- forward column pass: first (transposing) stage, reads every CTA's row
+  // results; the caller cluster_syncs before and after it. Writes `out` [H][CS].
+  __device__ static __forceinline__ void cols_fwd_first(const C* zb, C* out, const C* tw, unsigned rank) {
+    using S = Split<ColPlan>;
+    constexpr int R1 = S::first;
+    const int c0 = rank * COLS;
+    stockham<C, H, R1, 1, false, COLS, T>(
+        tw + TW_COL, [&](int cl, int r) { return post_remote(zb, tw, r, c0 + cl); },
+        [&](int l, int i, C v) { out[i * CS + l] = v; });
+  }
+
+  // Middle column stages + the last one handed to cons(r, col, v, pre(r, col))
+  // (col != 0); the packed column 0 (rank 0, local column 0) goes to col0[r].
+  // Input (first-stage output) in a. Ends with __syncthreads().
+  template <class PRE, class CONS>
+  __device__ static __forceinline__ void cols_fwd_rest(C* a, C* b, const C* tw, unsigned rank, C* col0, PRE&& pre,
+                                                      CONS&& cons) {
+    using S = Split<ColPlan>;
+    constexpr int R1 = S::first, RL = S::last, NSL = H / RL, J = H / RL, ITEMS = COLS * J;
+    using Mid = typename Split<typename S::tail>::init;
+    const C* twc = tw + TW_COL;
+    C* in = run_stages<C, H, false, COLS, CS, 1, T, R1>(a, b, twc, Mid{});
+    const int c0 = rank * COLS;
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += T) {
+      const int cl = it % COLS, j = it / COLS;
+      const int col = c0 + cl;
+      using PT = decltype(pre(0, 1));
+      PT pv[RL];
+      if (col != 0) {
+#pragma unroll
+        for (int s = 0; s < RL; ++s) pv[s] = pre(j + s * NSL, col);
+      }
+      C x[RL];
+#pragma unroll
+      for (int q = 0; q < RL; ++q) x[q] = in[(j + q * J) * CS + cl];
+      if constexpr (NSL > 1) stage_twiddle<C, RL, H / (NSL * RL), false>(x, twc, j);
+      dft<RL, false>(x);
+      if (col == 0) {
+#pragma unroll
+        for (int s = 0; s < RL; ++s) col0[j + s * NSL] = x[s];
+      } else {
+#pragma unroll
+        for (int s = 0; s < RL; ++s) cons(j + s * NSL, col, x[s], pv[s]);
+      }
+    }
+    __syncthreads();
+  }
+
+  template <int STRIDE = 1>
+  __device__ static __forceinline__ void unpack_col0(const C* pcl, int r, C& x0, C& xn) {
+    const C y = pcl[r * STRIDE];
+    const C ym = pcl[((H - r) % H) * STRIDE];
+    x0 = mk<C>(R(0.5) * (y.x + ym.x), R(0.5) * (y.y - ym.y));
+    xn = mk<C>(R(0.5) * (y.y + ym.y), R(0.5) * (ym.x - y.x));
+  }
+};
+
+}  // namespace dcsc_cuda

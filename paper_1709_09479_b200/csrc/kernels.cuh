@@ -867,7 +867,7 @@ __global__ void per_image_reduce(const double* partial, int tiles, double scale,
 // reduced partial spectra; l1_n = beta * sum |z| (objective.cpp:59-81).
 template <class R>
 __global__ void objective_reduce(const cx<R>* __restrict__ part, const double* __restrict__ sums,
-                                 const cx<R>* __restrict__ xhat, int G, int NB, int Wh, double invD,
+                                 const cx<R>* __restrict__ xhat, int G, int slots, int NB, int Wh, double invD,
                                  double beta, double* data, double* l1) {
   using C = cx<R>;
   __shared__ double red[32];
@@ -889,7 +889,7 @@ __global__ void objective_reduce(const cx<R>* __restrict__ part, const double* _
     for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
     data[n] = 0.5 * invD * s;
     double a = 0.0;
-    for (int g = 0; g < G; ++g) a += sums[((size_t)n * G + g) * kSums];
+    for (int g = 0; g < slots; ++g) a += sums[((size_t)n * slots + g) * kSums];
     l1[n] = beta * a;
   }
 }

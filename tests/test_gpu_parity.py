@@ -40,7 +40,7 @@ def test_dft_fp64_matches_reference(H, W):
     assert rel(back, x) <= 1e-13
 
 
-@pytest.mark.parametrize("H,W", [(16, 16), (16, 20), (20, 20), (64, 64), (100, 100), (128, 128)])
+@pytest.mark.parametrize("H,W", [(16, 16), (16, 20), (20, 20), (64, 64), (100, 100), (128, 128), (256, 256)])
 def test_dft_fp32_matches_reference(H, W):
     rng = np.random.default_rng(H * 7 + W)
     x = rng.standard_normal((4, H, W)).astype(np.float32).astype(np.float64)
@@ -192,3 +192,48 @@ def test_run_fp64_small_matches_reference():
         assert a["admm_iters"] == b["admm_iters"]
         assert a["mu_iters"] == b["mu_iters"]
     assert rel(g["dict"], r["dict"]) <= 1e-7
+
+
+# ---------------------------------------------------------------- 256 x 256 (C3 planes: 4-CTA cluster FFT)
+def test_cluster_plane_coding_fp32_matches_reference():
+    x, d = problem(1, (256, 256), 4, 11, p=0.01, fp32=True)
+    cfg = ref.Cfg(beta=0.5, max_admm=25, normalize=0)
+    z_r, st_r, s_r = ref.solve_coding(x[0], d, cfg)
+    z_g, st_g, s_g = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=0.5, max_admm=25, normalize=0), precision=32)
+    assert abs(s_g["admm_iters"] - s_r["admm_iters"]) <= 1
+    assert rel(z_g, z_r) <= 1e-3
+    og = dcsc.evaluate_objective(x[0], d, z_g, 0.5, precision=32)
+    orf = ref.objective(x[0], d, z_r, 0.5)
+    assert abs(og[2] - orf[2]) <= FP32_TOL * abs(orf[2])
+    assert abs(s_g["dual_objective"] - s_r["dual_objective"]) <= FP32_TOL * abs(s_r["dual_objective"])
+
+
+def test_cluster_plane_learning_apply_fp32_matches_reference():
+    rng = np.random.default_rng(21)
+    maps = rng.standard_normal((2, 3, 256, 256)) * (rng.random((2, 3, 256, 256)) < 0.01)
+    mu = np.array([1.0, 0.4, 2.0])
+    v = rng.standard_normal((2, 256, 256))
+    out_r = ref.learning_apply(maps, (11, 11), mu, 1e-6, v)
+    with dcsc.Context(2, (256, 256), 3, (11, 11), dcsc.SolverConfig(normalize=0), 32) as ctx:
+        ctx.set_signals(np.zeros((2, 256, 256)))
+        ctx.set_maps(maps.astype(np.float32).astype(np.float64))
+        out_g = ctx.learning_apply(mu, v)
+    assert rel(out_g, out_r) <= 1e-5
+
+
+def test_cluster_plane_learning_fp32_matches_reference():
+    x, d = problem(2, (256, 256), 3, 11, p=0.01, fp32=True)
+    maps = np.stack([ref.solve_coding(xi, d, ref.Cfg(beta=0.5, max_admm=10, normalize=0))[0] for xi in x])
+    maps = maps.astype(np.float32).astype(np.float64)
+    cfg = ref.Cfg(beta=0.5, normalize=0, max_mu_iters=2, cg_max=12)
+    d_r, _, s_r = ref.solve_learning(x, maps, (11, 11), cfg)
+    d_g, _, s_g = dcsc.solve_learning(x, maps, (11, 11), dcsc.SolverConfig(beta=0.5, normalize=0, max_mu_iters=2,
+                                                                           cg_max=12), precision=32)
+    assert s_g["mu_iters"] == s_r["mu_iters"]
+    assert rel(d_g, d_r) <= 1e-3
+    # the learning data term of both dictionaries agrees to the FP32 bar
+    with dcsc.Context(2, (256, 256), 3, (11, 11), dcsc.SolverConfig(normalize=0), 64 if False else 32) as ctx:
+        ctx.set_signals(x)
+        ctx.set_maps(maps)
+        a, b = ctx.learning_data_term(d_g), ctx.learning_data_term(d_r)
+    assert abs(a - b) <= FP32_TOL * abs(b)
