@@ -47,6 +47,9 @@ CONFIGS = {
                max_admm=500, outer=20),
     "c3": dict(N=512, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=False,
                max_admm=500, outer=10),
+    # C3-shaped slice for profiling only (not a BASELINE config)
+    "c3s": dict(N=16, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
+                max_admm=10, outer=1),
     "c4": dict(N=2048, H=64, W=64, K=32, m=7, prec=32, beta=0.5, p=0.005, sigma=0.05, coding_only=False,
                max_admm=500, outer=10),
 }

@@ -102,14 +102,42 @@ struct ClusterPlane {
 
   // ---- inverse row pass: first (transposing) stage reads the whole cluster's
   // column results; the caller must cluster_sync before (producers done) and
-  // after (readers done) this stage. Writes `out` [ROWS][Wh]; returns nothing.
+  // after (readers done) this stage. Writes `out` [ROWS][Wh]. All 2R remote
+  // loads of a butterfly are issued before any is consumed.
   __device__ static __forceinline__ void rows_inv_first(const C* cb, C* out, const C* tw, unsigned rank) {
     using S = Split<RowPlanI>;
-    constexpr int R1 = S::first;
+    constexpr int R = S::first, J = M / R, ITEMS = ROWS * J;
     const int r0 = rank * ROWS;
-    stockham<C, M, R1, 1, true, ROWS, T>(
-        tw + TW_ROW, [&](int rl, int k) { return pre_remote(cb, tw, r0 + rl, k); },
-        [&](int l, int i, C v) { out[l * Wh + i] = v; });
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += T) {
+      const int rl = it % ROWS, j = it / ROWS;
+      const C* row = cb + (r0 + rl) * CS;
+      C av[R], bv[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int k = j + q * J;
+        const int km = (k == 0) ? 0 : M - k;
+        av[q] = dsmem_ld(row + (k % COLS), k / COLS);
+        bv[q] = dsmem_ld(row + (km % COLS), km / COLS);
+      }
+      C x[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int k = j + q * J;
+        if (k == 0) {
+          x[q] = mk<C>(av[q].x + av[q].y, av[q].x - av[q].y);
+        } else {
+          const C a = av[q], bb = bv[q];
+          const C s = mk<C>(a.x + bb.x, a.y - bb.y);
+          const C d = mk<C>(a.x - bb.x, a.y + bb.y);
+          const C wd = cmulc(tw[TW_PP + k], d);
+          x[q] = mk<C>(s.x - wd.y, s.y + wd.x);
+        }
+      }
+      dft<R, true>(x);
+#pragma unroll
+      for (int s2 = 0; s2 < R; ++s2) out[rl * Wh + j * R + s2] = x[s2];
+    }
   }
   // remaining inverse row stages (local), input in a; returns result buffer
   __device__ static __forceinline__ C* rows_inv_rest(C* a, C* b, const C* tw) {
@@ -137,14 +165,42 @@ struct ClusterPlane {
 
   // ---- forward column pass: first (transposing) stage, reads every CTA's row
   // results; the caller cluster_syncs before and after it. Writes `out` [H][CS].
+  // All 2R remote loads of a butterfly are issued before any is consumed.
   __device__ static __forceinline__ void cols_fwd_first(const C* zb, C* out, const C* tw, unsigned rank) {
     using S = Split<ColPlan>;
-    constexpr int R1 = S::first;
+    constexpr int R = S::first, J = H / R, ITEMS = COLS * J;
     const int c0 = rank * COLS;
-    stockham<C, H, R1, 1, false, COLS, T>(
-        tw + TW_COL, [&](int cl, int r) { return post_remote(zb, tw, r, c0 + cl); },
-        [&](int l, int i, C v) { out[i * CS + l] = v; });
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += T) {
+      const int cl = it % COLS, j = it / COLS;
+      const int col = c0 + cl;
+      const int colm = (col == 0) ? 0 : M - col;
+      C z1[R], z2[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int r = j + q * J;
+        const C* rowp = zb + (r % ROWS) * Wh;
+        z1[q] = dsmem_ld(rowp + col, r / ROWS);
+        z2[q] = dsmem_ld(rowp + colm, r / ROWS);
+      }
+      C x[R];
+      const C wpp = tw[TW_PP + col];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (col == 0) {
+          x[q] = mk<C>(z1[q].x + z1[q].y, z1[q].x - z1[q].y);
+        } else {
+          const C e = mk<C>(R_(0.5) * (z1[q].x + z2[q].x), R_(0.5) * (z1[q].y - z2[q].y));
+          const C o = mk<C>(R_(0.5) * (z1[q].y + z2[q].y), R_(0.5) * (z2[q].x - z1[q].x));
+          x[q] = cadd(e, cmul(wpp, o));
+        }
+      }
+      dft<R, false>(x);
+#pragma unroll
+      for (int s2 = 0; s2 < R; ++s2) out[(j * R + s2) * CS + cl] = x[s2];
+    }
   }
+  using R_ = Rt;
 
   // Middle column stages + the last one handed to cons(r, col, v, pre(r, col))
   // (col != 0); the packed column 0 (rank 0, local column 0) goes to col0[r].
