@@ -223,13 +223,20 @@ def run_ours(args, cfg):
         dist = tdist
     from paper_1709_09479_b200 import dcsc
     N = cfg["N"]
-    per = (N + world - 1) // world
-    n0, n1 = rank * per, min(N, (rank + 1) * per)
+    n0, n1 = dcsc.shard_range(N, world, rank)
     x, d_true = make_data(cfg, n0, n1)
     nl = n1 - n0
     sc = dcsc.SolverConfig(beta=cfg["beta"], max_admm=cfg["max_admm"], normalize=0, seed=SEED, tol=1e-300)
     ctx = dcsc.Context(nl, (cfg["H"], cfg["W"]), cfg["K"], (cfg["m"], cfg["m"]), sc, cfg["prec"],
                        device=local if world > 1 else 0)
+    if world > 1 and not cfg["coding_only"]:
+        # learning sums its K x NB correlations and CG scalars over ranks (NCCL)
+        import torch
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.tensor(list(dcsc.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx.set_comm_nccl(world, rank, bytes(uid.cpu().tolist()))
     ctx.set_signals(x)
     ctx.set_dictionary(d_true)
 

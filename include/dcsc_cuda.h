@@ -165,6 +165,17 @@ int dcsc_cuda_event_elapsed(dcsc_cuda_ctx* ctx, int a, int b, double* ms);
 /* bytes of device memory held by the context */
 int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes);
 
+/* multi-rank: one context per GPU holds its shard of images; learning sums
+ * its K x NB correlations and the CG / trace scalars over ranks.
+ * dcsc_cuda_nccl_unique_id: rank 0 creates the id (>= 128 bytes) and ships it
+ * to the other ranks (e.g. torch.distributed broadcast); each rank then calls
+ * dcsc_cuda_set_comm_nccl. dcsc_cuda_set_comm_callback installs a host-side
+ * in-place sum (for testing ranks that share one GPU, e.g. over gloo). */
+typedef int (*dcsc_allreduce_fn)(double* buf, size_t n, void* user);
+int dcsc_cuda_nccl_unique_id(unsigned char* out, size_t len);
+int dcsc_cuda_set_comm_nccl(dcsc_cuda_ctx* ctx, int world, int rank, const unsigned char* id, size_t len);
+int dcsc_cuda_set_comm_callback(dcsc_cuda_ctx* ctx, int world, int rank, dcsc_allreduce_fn fn, void* user);
+
 /* synthetic BASELINE data (host only, no GPU): x N*H*W, d_true K*m*m */
 int dcsc_synth_generate(int n_images, int height, int width, int filters, int m, double p,
                         double sigma, uint64_t seed, int round_fp32, double* x, double* d_true);

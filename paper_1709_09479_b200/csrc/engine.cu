@@ -4,6 +4,8 @@
 // decisions the reference makes on scalars (stop tests, acceptance, the mu
 // settle test) from FP64 reductions read back per iteration.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -171,6 +173,88 @@ void normalize_image(int mode, int H, int W, const double* in, double* out) {
   for (size_t i = 0; i < D; ++i) out[i] = (in[i] - lm[i]) / std::max(lsd[i], fl);
 }
 
+// ---------------------------------------------------------------- multi-rank reduction
+// Learning is image-sharded like coding (no z_hat all-to-all): the K x NB
+// correlation partials, the CG scalars and the trace sums are all-reduced.
+// NCCL is dlopen'ed (libnccl.so.2) so a process that already loaded torch's
+// NCCL shares it; the host-callback reducer lets ranks that share one GPU be
+// tested with host-side (gloo) reductions.
+struct Reducer {
+  int world = 1, rank = 0;
+  virtual ~Reducer() = default;
+  virtual void allreduce(double* dev, size_t n, cudaStream_t st) = 0;  // in-place sum
+};
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  if (!api.h) {
+    api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!api.h) throw CudaErr(std::string("NCCL: dlopen(libnccl.so.2) failed: ") + dlerror());
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(api.h, "ncclCommInitRank"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(api.h, "ncclAllReduce"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+    api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+    if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
+      throw CudaErr("NCCL: missing symbols in libnccl.so.2");
+  }
+  return api;
+}
+
+#define NCK(x)                                                                                        \
+  do {                                                                                                \
+    ncclResult_t r_ = (x);                                                                            \
+    if (r_ != ncclSuccess)                                                                            \
+      throw CudaErr(std::string("NCCL ") + #x + ": " +                                               \
+                    (nccl_api().getErrorString ? nccl_api().getErrorString(r_) : std::to_string(r_))); \
+  } while (0)
+
+struct NcclReducer final : Reducer {
+  ncclComm_t comm = nullptr;
+  NcclReducer(int w, int r, const unsigned char* id, size_t len) {
+    if (len < sizeof(ncclUniqueId)) throw InvErr("NCCL unique id too short");
+    world = w;
+    rank = r;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    NCK(nccl_api().commInitRank(&comm, w, uid, r));
+  }
+  ~NcclReducer() override {
+    if (comm) nccl_api().commDestroy(comm);
+  }
+  void allreduce(double* dev, size_t n, cudaStream_t st) override {
+    NCK(nccl_api().allReduce(dev, dev, n, ncclDouble, ncclSum, comm, st));
+  }
+};
+
+struct HostReducer final : Reducer {
+  dcsc_allreduce_fn fn;
+  void* user;
+  std::vector<double> host;
+  HostReducer(int w, int r, dcsc_allreduce_fn f, void* u) : fn(f), user(u) {
+    world = w;
+    rank = r;
+  }
+  void allreduce(double* dev, size_t n, cudaStream_t st) override {
+    host.resize(n);
+    CK(cudaMemcpyAsync(host.data(), dev, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (fn(host.data(), n, user) != 0) throw CudaErr("host all-reduce callback failed");
+    CK(cudaMemcpyAsync(dev, host.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+};
+
 // ---------------------------------------------------------------- interface
 class EngineBase {
  public:
@@ -197,7 +281,12 @@ class EngineBase {
   virtual void kernel_time(int fam, double* ms, long long* n) = 0;
   virtual void event_mark(int slot) = 0;
   virtual double event_elapsed(int a, int b) = 0;
+  void set_reducer(std::unique_ptr<Reducer> r) { red_ = std::move(r); }
+  bool multi() const { return red_ && red_->world > 1; }
   long long launches = 0;
+ protected:
+  std::unique_ptr<Reducer> red_;
+ public:
   size_t device_bytes = 0;
 };
 
@@ -383,6 +472,8 @@ class Engine final : public EngineBase {
     dd_.alloc(sizeof(double) * (size_t)K_ * M_);
     ddict_.alloc(sizeof(double) * (size_t)K_ * M_);
     cg_.alloc(sizeof(CgState));
+    hred_.alloc(sizeof(double) * std::max(64, K_ + 8));
+    cglob_.alloc(sizeof(double2) * (size_t)K_ * NB);
     tiles_ = (NB + TBV - 1) / TBV;
     const size_t vec_blocks = (nNB + TBV - 1) / TBV;
     accept_chunks_ = std::max(1, std::min(64, (int)((size_t)K_ * D / (TBV * 8))));
@@ -559,6 +650,15 @@ class Engine final : public EngineBase {
     u_zero_.assign(N_, 1);
     mu_.assign(K_, 1.0);
     zhat_valid_ = false;
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // sum v[0..n) over ranks (host values; no-op on one rank)
+  void reduce_host(double* v, int n) {
+    if (!multi()) return;
+    CK(cudaMemcpyAsync(hred_.p, v, sizeof(double) * n, cudaMemcpyHostToDevice, st_));
+    red_->allreduce(hred_.as<double>(), n, st_);
+    CK(cudaMemcpyAsync(v, hred_.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -763,6 +863,14 @@ class Engine final : public EngineBase {
     live_h_.assign(K_, 0);
     CK(cudaMemcpyAsync(live_h_.data(), live_.p, sizeof(int) * K_, cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
+    if (multi()) {  // a filter is dead only if its maps vanish on every rank
+      std::vector<double> lv(K_);
+      for (int k = 0; k < K_; ++k) lv[k] = live_h_[k];
+      reduce_host(lv.data(), K_);
+      for (int k = 0; k < K_; ++k) live_h_[k] = lv[k] > 0.0 ? 1 : 0;
+      CK(cudaMemcpyAsync(live_.p, live_h_.data(), sizeof(int) * K_, cudaMemcpyHostToDevice, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
     zhat_valid_ = true;
   }
 
@@ -775,10 +883,19 @@ class Engine final : public EngineBase {
                                              done);
     });
     const size_t knb = (size_t)K_ * NB;
-    launch(kFamContract, [&] {
-      contract_c_reduce<R><<<(unsigned)((knb + 255) / 256), 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(),
-                                                                           csplit_, knb, done);
-    });
+    const unsigned rb = (unsigned)((knb + 255) / 256);
+    if (!multi()) {
+      launch(kFamContract, [&] {
+        contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(), nullptr, csplit_, knb, done);
+      });
+    } else {  // FP64 partials summed over ranks, then rounded once
+      launch(kFamContract, [&] {
+        contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), nullptr, cglob_.as<double2>(), csplit_, knb,
+                                                  done);
+      });
+      red_->allreduce(reinterpret_cast<double*>(cglob_.p), 2 * knb, st_);
+      launch(kFamContract, [&] { to_cx<R><<<rb, 256, 0, st_>>>(cglob_.as<double2>(), cvec_.as<C>(), knb, done); });
+    }
   }
 
   // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
@@ -809,6 +926,20 @@ class Engine final : public EngineBase {
     return *h;
   }
 
+  // One CG scalar step; across ranks the block partials are first summed
+  // locally, all-reduced, then applied (identical state on every rank).
+  void cg_step(const double* partial, int count, double invD, int step) {
+    if (!multi()) {
+      launch(kFamOther, [&] { cg_scalar<<<1, 1024, 0, st_>>>(partial, count, invD, cg_.as<CgState>(), step, nullptr); });
+      return;
+    }
+    launch(kFamOther, [&] { sum_partials<<<1, 1024, 0, st_>>>(partial, count, hred_.as<double>()); });
+    red_->allreduce(hred_.as<double>(), 1, st_);
+    launch(kFamOther, [&] {
+      cg_scalar<<<1, 1024, 0, st_>>>(partial, count, invD, cg_.as<CgState>(), step, hred_.as<double>());
+    });
+  }
+
   // gamma_solve (learning.cpp:136-185), warm-started, on half spectra. The
   // iteration loop terminates on the device (CgState::done); the host issues
   // iterations in chunks and reads the state once per chunk.
@@ -833,7 +964,7 @@ class Engine final : public EngineBase {
                                             partial_.as<double>(), total, NB, Wh);
     });
     const double invD = 1.0 / D;
-    launch(kFamOther, [&] { cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 0); });
+    cg_step(partial_.as<double>(), (int)vb, invD, 0);
     const int* done = &cg_.as<CgState>()->done;
     CgState s = read_cg();
     int issued = 0, chunk = 2;
@@ -841,16 +972,12 @@ class Engine final : public EngineBase {
       const int n = std::min(chunk, cfg_.cg_max - issued);
       for (int c = 0; c < n; ++c) {
         apply_hat(p_.as<C>(), ap_.as<C>(), done);
-        launch(kFamOther, [&] {
-          cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), N_ * tiles_, invD, cg_.as<CgState>(), 1);
-        });
+        cg_step(partial_.as<double>(), N_ * tiles_, invD, 1);
         launch(kFamOther, [&] {
           cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_.as<C>(), r_.as<C>(), p_.as<C>(), ap_.as<C>(),
                                                   cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh);
         });
-        launch(kFamOther, [&] {
-          cg_scalar<<<1, 1024, 0, st_>>>(partial_.as<double>(), (int)vb, invD, cg_.as<CgState>(), 2);
-        });
+        cg_step(partial_.as<double>(), (int)vb, invD, 2);
         launch(kFamOther, [&] {
           cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(r_.as<C>(), p_.as<C>(), cg_.as<CgState>(), total);
         });
@@ -894,6 +1021,7 @@ class Engine final : public EngineBase {
     }
     double bn = 0.0;
     for (int n = 0; n < N_; ++n) bn += xnorm2_[n];
+    reduce_host(&bn, 1);
     const double bnorm = std::sqrt(bn);
     std::vector<double> d;
     std::vector<double> norms(K_, 0.0);
@@ -987,6 +1115,7 @@ class Engine final : public EngineBase {
     data_terms(d ? d : dict_.data(), data);
     double s = 0.0;
     for (double v : data) s += v;
+    reduce_host(&s, 1);
     *out = s;
   }
 
@@ -1039,6 +1168,7 @@ class Engine final : public EngineBase {
         img[n].residual_norm = std::sqrt(xnorm2_[n]);
         dsum += img[n].data_term;
       }
+      reduce_host(&dsum, 1);
       prev_total = dsum;
     }
     std::vector<dcsc_coding_stats> cs(N_);
@@ -1069,6 +1199,19 @@ class Engine final : public EngineBase {
         after.l1_term += img[n].l1_term;
         after.residual_norm += img[n].residual_norm * img[n].residual_norm;
       }
+      {
+        double s[6] = {after.data_term, after.l1_term, after.residual_norm, (double)admm_total, zc2, zn2};
+        double l0d = (double)l0;
+        reduce_host(s, 6);
+        reduce_host(&l0d, 1);
+        after.data_term = s[0];
+        after.l1_term = s[1];
+        after.residual_norm = s[2];
+        admm_total = (long)s[3];
+        zc2 = s[4];
+        zn2 = s[5];
+        l0 = (long)l0d;
+      }
       after.total = after.data_term + after.l1_term;
       after.residual_norm = std::sqrt(after.residual_norm);
       const double w1 = now_ms();
@@ -1083,6 +1226,7 @@ class Engine final : public EngineBase {
       data_terms(dc.data(), data);
       double cand = 0.0;
       for (double v : data) cand += v;
+      reduce_host(&cand, 1);
       if (!std::isfinite(cand + after.l1_term))
         throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", learning phase");
       dcsc_objective afterl = after;
@@ -1195,7 +1339,7 @@ class Engine final : public EngineBase {
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_, cpart_;
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_;
   std::vector<double> dict_, mu_, xnorm2_, xs_host_;
   std::vector<int> live_h_;
   std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero
@@ -1439,6 +1583,28 @@ int dcsc_cuda_event_mark(dcsc_cuda_ctx* ctx, int slot) {
 int dcsc_cuda_event_elapsed(dcsc_cuda_ctx* ctx, int a, int b, double* ms) {
   CTX_CHECK
   return guarded([&] { *ms = ctx->eng->event_elapsed(a, b); });
+}
+int dcsc_cuda_nccl_unique_id(unsigned char* out, size_t len) {
+  return guarded([&] {
+    if (len < sizeof(ncclUniqueId)) throw InvErr("buffer shorter than ncclUniqueId");
+    ncclUniqueId id;
+    NCK(nccl_api().getUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+int dcsc_cuda_set_comm_nccl(dcsc_cuda_ctx* ctx, int world, int rank, const unsigned char* id, size_t len) {
+  CTX_CHECK
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world) throw InvErr("bad world/rank");
+    ctx->eng->set_reducer(world == 1 ? nullptr : std::make_unique<NcclReducer>(world, rank, id, len));
+  });
+}
+int dcsc_cuda_set_comm_callback(dcsc_cuda_ctx* ctx, int world, int rank, dcsc_allreduce_fn fn, void* user) {
+  CTX_CHECK
+  return guarded([&] {
+    if (world < 1 || rank < 0 || rank >= world || !fn) throw InvErr("bad world/rank/callback");
+    ctx->eng->set_reducer(std::make_unique<HostReducer>(world, rank, fn, user));
+  });
 }
 int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes) {
   CTX_CHECK

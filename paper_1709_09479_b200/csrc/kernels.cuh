@@ -643,8 +643,8 @@ contract_c(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ v, double2*
 }
 
 template <class R>
-__global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __restrict__ c, int splits,
-                                  size_t KNB, const int* done) {
+__global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __restrict__ c,
+                                  double2* __restrict__ c64, int splits, size_t KNB, const int* done) {
   if (done && *done) return;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= KNB) return;
@@ -654,7 +654,33 @@ __global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __re
     ar += p.x;
     ai += p.y;
   }
-  c[i] = mk<cx<R>>(R(ar), R(ai));
+  if (c64)
+    c64[i] = make_double2(ar, ai);  // summed over ranks before rounding
+  else
+    c[i] = mk<cx<R>>(R(ar), R(ai));
+}
+
+template <class R>
+__global__ void to_cx(const double2* __restrict__ src, cx<R>* __restrict__ dst, size_t n, const int* done) {
+  if (done && *done) return;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = mk<cx<R>>(R(src[i].x), R(src[i].y));
+}
+
+// single-block fixed-order sum of block partials into out[0]
+__global__ void sum_partials(const double* partial, int count, double* out) {
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) v += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
+    out[0] = s;
+  }
 }
 
 // out_n = v_n + sum_k (0.5/mu_k) z_hat_nk p_hat_k (learning.cpp:109-121, in the
@@ -803,9 +829,11 @@ cg_pupdate(const cx<R>* __restrict__ r, cx<R>* __restrict__ p, const CgState* st
 // Single-block scalar step of CG. step 0: rr from the initial residual (done
 // when already below tol); step 1: pap -> alpha (pAp <= 0 stops, gamma
 // untouched, learning.cpp:166); step 2: rr_new -> rel, beta, iteration count.
-__global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step) {
+__global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step,
+                          const double* presum) {
   __shared__ double red[32];
   if (step != 0 && st->done) return;
+  if (presum) count = 0;  // already summed (over ranks)
   double v = 0.0;
   // fixed-order strided partial sums, then a fixed-order tree: deterministic
   for (int i = threadIdx.x; i < count; i += blockDim.x) v += partial[i];
@@ -816,6 +844,7 @@ __global__ void cg_scalar(const double* partial, int count, double invD, CgState
   if (threadIdx.x != 0) return;
   double s = 0.0;
   for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
+  if (presum) s = presum[0];
   s *= invD;
   if (step == 0) {
     st->rr = s;

@@ -129,7 +129,40 @@ EXPORTS = [
     "dcsc_cuda_dft2_forward", "dcsc_cuda_dft2_inverse", "dcsc_cuda_kernel_launches",
     "dcsc_cuda_set_profiling", "dcsc_cuda_kernel_time", "dcsc_cuda_event_mark",
     "dcsc_cuda_event_elapsed", "dcsc_cuda_device_bytes", "dcsc_synth_generate",
+    "dcsc_cuda_nccl_unique_id", "dcsc_cuda_set_comm_nccl", "dcsc_cuda_set_comm_callback",
 ]
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
+
+
+def shard_range(n_images: int, world: int, rank: int) -> tuple[int, int]:
+    """Images [n0, n1) owned by `rank` (contiguous, sizes differ by at most one)."""
+    base, extra = divmod(n_images, world)
+    n0 = rank * base + min(rank, extra)
+    return n0, n0 + base + (1 if rank < extra else 0)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _err(lib().dcsc_cuda_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def gloo_allreduce_fn(group=None):
+    """Host all-reduce callback over torch.distributed (gloo): in-place sum."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(ptr, n, _user):
+        try:
+            arr = np.ctypeslib.as_array(ptr, shape=(n,))
+            t = torch.from_numpy(arr)  # shares memory with the C buffer
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            return 0
+        except Exception:  # never raise through the C frame
+            return 1
+
+    return fn
 
 
 def lib():
@@ -299,6 +332,15 @@ class Context:
         conv = C.c_int()
         _err(lib().dcsc_cuda_run(self._h, max_outer, rows, C.byref(n), C.byref(conv)))
         return [rows[i].asdict() for i in range(n.value)], bool(conv.value)
+
+    # -- multi-rank
+    def set_comm_nccl(self, world: int, rank: int, uid: bytes):
+        buf = (C.c_ubyte * len(uid)).from_buffer_copy(uid)
+        _err(lib().dcsc_cuda_set_comm_nccl(self._h, world, rank, buf, len(uid)))
+
+    def set_comm_callback(self, world: int, rank: int, fn):
+        self._cb = ALLREDUCE_FN(fn)  # keep the trampoline alive
+        _err(lib().dcsc_cuda_set_comm_callback(self._h, world, rank, self._cb, None))
 
     # -- measurement
     def synchronize(self):

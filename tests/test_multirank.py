@@ -1,0 +1,81 @@
+"""Multi-rank paths with world_size 2 over gloo (127.0.0.1).
+
+CPU: the host all-reduce callback and the image sharding.
+GPU: two ranks sharing one GPU (host-side gloo reductions only, no kernel
+waits on another rank) reproduce a single-rank run_csc: the sharded learning
+(correlation partials + CG scalars summed over ranks) gives the same trace.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1709_09479_b200 import dcsc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "mr", "worker.py")
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch(world, mode, tmp_path):
+    port = free_port()
+    procs, outs = [], []
+    for r in range(world):
+        out = str(tmp_path / f"rank{r}.npz")
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), MR_OUT=out, MR_MODE=mode)
+        procs.append(subprocess.Popen([sys.executable, WORKER], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+        outs.append(out)
+    for p in procs:
+        o, _ = p.communicate(timeout=600)
+        assert p.returncode == 0, o[-3000:]
+    return [np.load(o) for o in outs]
+
+
+def test_shard_ranges_cover_all_images():
+    for n in (1, 7, 10, 256, 2048):
+        for w in (1, 2, 3, 8):
+            rs = [dcsc.shard_range(n, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_gloo_allreduce_callback_two_ranks(tmp_path):
+    res = launch(2, "cpu", tmp_path)
+    expect = (np.arange(5) + 1.0) * 3.0
+    for r in res:
+        assert int(r["rc"]) == 0
+        assert np.array_equal(r["buf"], expect)
+    assert list(res[0]["shard"]) == [0, 5] and list(res[1]["shard"]) == [5, 10]
+
+
+@pytest.mark.gpu
+def test_two_ranks_match_single_rank(tmp_path):
+    res = launch(2, "gpu", tmp_path)
+    N, grid, K, m = 4, (20, 20), 6, 5
+    x, _ = dcsc.synth_generate(N, grid, K, m, 0.05, 0.01, 7, False)
+    cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
+    one = dcsc.run_csc(x, K, (m, m), cfg, precision=64)
+    keys = ["total", "data_term", "l1_term", "admm_iters", "cg_iters", "mu_iters", "l0"]
+    single = np.array([[r[k] for k in keys] for r in one["trace"]], dtype=np.float64)
+    for r in res:
+        t = r["trace"]
+        assert t.shape == single.shape
+        assert np.all(np.abs(t[:, :3] - single[:, :3]) <= 1e-9 * np.abs(single[:, :3]))
+        assert np.array_equal(t[:, 3], single[:, 3]) and np.array_equal(t[:, 5], single[:, 5])
+        assert np.all(np.abs(t[:, 4] - single[:, 4]) <= 2)
+        assert np.abs(r["dict"] - one["dict"]).max() <= 1e-8 * np.abs(one["dict"]).max()
+    maps = np.concatenate([res[0]["maps"], res[1]["maps"]])
+    assert np.abs(maps - one["maps"]).max() <= 1e-8 * np.abs(one["maps"]).max()
