@@ -662,6 +662,19 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
   }
 
+  // Internal u layout: the single-CTA family stores each plane's pixel pairs
+  // column-major ((c/2)*H + r), the cluster family row-major; i is a
+  // reference-layout index (plane-major, row-major pixels).
+  static size_t u_index(size_t i) {
+    if constexpr (CLU) {
+      return i;
+    } else {
+      const size_t p = i / D, q = i % D;
+      const size_t r = q / W, c = q % W;
+      return p * D + ((c >> 1) * H + r) * 2 + (c & 1);
+    }
+  }
+
   void check_range(int n0, int n1) const {
     if (n0 < 0 || n1 > N_ || n0 >= n1) throw DimErr("image range out of bounds");
   }
@@ -678,7 +691,7 @@ class Engine final : public EngineBase {
     std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
     std::vector<R> u(cnt);
     const double inv_rho = 1.0 / cfg_.rho;
-    for (size_t i = 0; i < cnt; ++i) u[i] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
+    for (size_t i = 0; i < cnt; ++i) u[u_index(i)] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
     CK(cudaMemcpyAsync(u_.as<R>() + (size_t)n0 * K_ * D, u.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
     CK(cudaStreamSynchronize(st_));
   }
@@ -693,9 +706,10 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
     const R beta = R(cfg_.beta), rho = R(cfg_.rho);
     for (size_t i = 0; i < cnt; ++i) {
-      const R th = std::min(std::max(u[i], -beta), beta);
+      const R uv = u[u_index(i)];
+      const R th = std::min(std::max(uv, -beta), beta);
       if (theta) theta[i] = th;
-      if (z) z[i] = rho * (th - u[i]);
+      if (z) z[i] = rho * (th - uv);
     }
     if (lambda)
       for (size_t i = 0; i < l.size(); ++i) lambda[i] = l[i];
@@ -1264,9 +1278,9 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(accept_.p, acc.data(), sizeof(int) * N_, cudaMemcpyHostToDevice, st_));
     const dim3 g(accept_chunks_, N_);
     launch(kFamOther, [&] {
-      accept_maps<R, TBV><<<g, TBV, 0, st_>>>(u_.as<R>(), maps_.as<R>(), accept_.as<int>(), (size_t)K_ * D, cfg_.rho,
-                                               cfg_.beta, partial_.as<double>(), partial2_.as<double>(),
-                                               l0_.as<unsigned long long>());
+      accept_maps<R, TBV, !CLU><<<g, TBV, 0, st_>>>(u_.as<R>(), maps_.as<R>(), accept_.as<int>(), (size_t)K_ * D,
+                                                     cfg_.rho, cfg_.beta, partial_.as<double>(),
+                                                     partial2_.as<double>(), l0_.as<unsigned long long>(), P::H, P::W);
     });
     const size_t cnt = (size_t)N_ * accept_chunks_;
     std::vector<double> a(cnt), b(cnt);

@@ -179,52 +179,57 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       });
       C* hin = P::rows_inv_head(cs, cs == B0 ? B1 : B0, TW);
       C* fout = (hin == B0) ? B1 : B0;
-      // last inverse row stage (plain), then the prox pass over the staged u
-      {
-        constexpr int RX = P::RX, J = M / RX;
-        const C* twr = TW + P::TW_ROW;
-        stockham<C, M, RX, J, true, H, T>(
-            twr,
-            [&](int r, int kk) { return (P::RI_N == 1) ? P::pre(hin, TW, r, kk) : hin[r * Wh + kk]; },
-            [&](int l, int i, C v) { fout[l * Wh + i] = v; });
-        __syncthreads();
-      }
+      // fused: last inverse row stage -> prox on u -> first forward row stage,
+      // in registers. u is stored column-major per plane (pair m, row r at
+      // m*H + r) so lanes over rows read U / u conflict-free and coalesced.
       if constexpr (STAGE) mbar_wait(ubar, uphase);
       uphase ^= 1u;
       {
+        constexpr int RX = P::RX, J = M / RX;
+        const C* twr = TW + P::TW_ROW;
         R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
-        constexpr int ITEMS = H * M;
-#pragma unroll 4
-        for (int it = threadIdx.x; it < ITEMS; it += T) {
-          const int r = it / M, m = it % M;
-          C* up = STAGE ? (U + it) : (uk + it);
-          const C uv = *up;
-          const C v = fout[r * Wh + m];
-          const R tv[2] = {v.x * invD, v.y * invD};
-          const R uo[2] = {uv.x, uv.y};
-          R wv[2], un2[2];
+#pragma unroll 1
+        for (int it = threadIdx.x; it < H * J; it += T) {
+          const int r = it % H, j = it / H;
+          C x[RX];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const R t = tv[e];
-            const R th_o = fmin(fmax(uo[e], -beta), beta);
-            const R un = t - (th_o - uo[e]);           // u' = t - z/rho
-            const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
-            const R zn = rho * (th - un);              // z' = rho (theta' - u')
-            const R d_tt = th - t;
-            const R dz = rho * d_tt;                   // z' - z = rho (theta' - t)
-            const R dth = th - th_o;
-            f0 += d_tt * d_tt;
-            f1 += th * th;
-            f2 += t * t;
-            f3 += dz * dz;
-            f4 += zn * zn;
-            f5 += dth * dth;
-            f6 = fmax(f6, fabs(t));
-            wv[e] = R(2) * th - un;
-            un2[e] = un;
+          for (int q = 0; q < RX; ++q)
+            x[q] = (P::RI_N == 1) ? P::pre(hin, TW, r, j + q * J) : hin[r * Wh + j + q * J];
+          if constexpr (P::RI_N > 1) stage_twiddle<C, RX, 1, true>(x, twr, j);
+          dft<RX, true>(x);
+#pragma unroll
+          for (int s = 0; s < RX; ++s) {
+            C* up = (STAGE ? U : uk) + (j + s * J) * H + r;
+            const C uv = *up;
+            const R tv[2] = {x[s].x * invD, x[s].y * invD};
+            const R uo[2] = {uv.x, uv.y};
+            R wv[2], un2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const R t = tv[e];
+              const R th_o = fmin(fmax(uo[e], -beta), beta);
+              const R un = t - (th_o - uo[e]);           // u' = t - z/rho
+              const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
+              const R zn = rho * (th - un);              // z' = rho (theta' - u')
+              const R d_tt = th - t;
+              const R dz = rho * d_tt;                   // z' - z = rho (theta' - t)
+              const R dth = th - th_o;
+              f0 += d_tt * d_tt;
+              f1 += th * th;
+              f2 += t * t;
+              f3 += dz * dz;
+              f4 += zn * zn;
+              f5 += dth * dth;
+              f6 = fmax(f6, fabs(t));
+              wv[e] = R(2) * th - un;
+              un2[e] = un;
+            }
+            *up = mk<C>(un2[0], un2[1]);
+            x[s] = mk<C>(wv[0], wv[1]);
           }
-          *up = mk<C>(un2[0], un2[1]);
-          fout[r * Wh + m] = mk<C>(wv[0], wv[1]);
+          dft<RX, false>(x);  // first forward row stage (NS = 1)
+#pragma unroll
+          for (int s = 0; s < RX; ++s) fout[r * Wh + j * RX + s] = x[s];
         }
         s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
         s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
           bulk_commit();
         }
       }
-      C* z = P::rows_fwd(fout, hin, TW);
+      C* z = P::rows_fwd_tail(fout, hin, TW);
       P::cols_fwd_acc(z, z == B0 ? B1 : B0, TW, COL0, dk, acc);
       if (threadIdx.x < H) {
         const int r = threadIdx.x;
@@ -252,7 +257,8 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
           (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D);
       for (int it = threadIdx.x; it < H * M; it += T) {
         const int r = it / M, m = it % M;
-        const C v = src[it];
+        // maps are row-major [r][c]; u is column-major pairs [m][r]
+        const C v = (MODE == kPassMaps) ? src[it] : src[m * H + r];
         R w0, w1;
         if constexpr (MODE == kPassPrologue) {
           w0 = R(2) * fmin(fmax(v.x, -beta), beta) - v.x;
@@ -984,11 +990,11 @@ __global__ void sigma_kernel(const cx<R>* __restrict__ dhat, R* __restrict__ sig
 // Accept coded maps (pipeline.cpp:236-246): for accepted images maps = z_cand
 // (closed form from u); block partials of sum (cand-old)^2 over accepted images,
 // sum maps^2 and the l0 count over all images. grid (chunks, N).
-template <class R, int TB>
+template <class R, int TB, bool UT>
 __global__ void __launch_bounds__(TB)
 accept_maps(const R* __restrict__ u, R* __restrict__ maps, const int* __restrict__ accept,
             size_t per_image, double rho, double beta, double* part_dz, double* part_zz,
-            unsigned long long* l0) {
+            unsigned long long* l0, int H, int W) {
   const int n = blockIdx.y;
   const bool acc = accept[n] != 0;
   double dz = 0.0, zz = 0.0;
@@ -999,7 +1005,13 @@ accept_maps(const R* __restrict__ u, R* __restrict__ maps, const int* __restrict
   for (size_t i = (size_t)blockIdx.x * TB + threadIdx.x; i < per_image; i += (size_t)gridDim.x * TB) {
     R m = mp[i];
     if (acc) {
-      const R uv = up[i];
+      size_t ui = i;
+      if (UT) {  // u planes are column-major pixel pairs: (r, c) -> ((c/2) H + r) * 2 + (c & 1)
+        const size_t D = (size_t)H * W, p = i / D, q = i % D;
+        const int r = (int)(q / W), c = (int)(q % W);
+        ui = p * D + ((size_t)(c >> 1) * H + r) * 2 + (c & 1);
+      }
+      const R uv = up[ui];
       const R zc = rr * (fmin(fmax(uv, -bb), bb) - uv);
       const double d = (double)zc - (double)m;
       dz += d * d;
