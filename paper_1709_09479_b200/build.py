@@ -22,7 +22,7 @@ LIB = os.path.join(LIBDIR, "libdcsc_cuda.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + INC, "-I" + CSRC,
+    "-Xcompiler", "-fPIC,-fopenmp", "-Xptxas", "-v", "-I" + INC, "-I" + CSRC,
 ]
 HOST_CXX = shutil.which("g++", path="/usr/bin") or "g++"
 

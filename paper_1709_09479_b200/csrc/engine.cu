@@ -505,6 +505,7 @@ class Engine final : public EngineBase {
     for (auto& e : marks_)
       if (e) cudaEventDestroy(e);
     if (pin_) cudaFreeHost(pin_);
+    if (xstage_) cudaFreeHost(xstage_);
     if (st_) cudaStreamDestroy(st_);
   }
 
@@ -590,20 +591,34 @@ class Engine final : public EngineBase {
   // ------------------------------------------------------------ API
   void set_signals(const double* x) override {
     const size_t nD = (size_t)N_ * D;
-    require_finite(x, nD, "signal");
-    std::vector<double> xn(nD);
-    for (int n = 0; n < N_; ++n) normalize_image(cfg_.normalize, H, W, x + (size_t)n * D, xn.data() + (size_t)n * D);
-    // the device stores R; norms use the stored (rounded) values, as the oracle sees them
-    std::vector<R> xr(nD);
-    for (size_t i = 0; i < nD; ++i) xr[i] = R(xn[i]);
-    xs_host_.assign(nD, 0.0);
-    for (size_t i = 0; i < nD; ++i) xs_host_[i] = double(xr[i]);
+    // host side parallel over images: validate, normalise (pipeline.cpp:78-121),
+    // round to the storage precision into pinned staging, per-image norms of the
+    // stored values (what the oracle sees)
+    int bad = 0;
+#pragma omp parallel for reduction(| : bad)
+    for (long i = 0; i < (long)nD; ++i) bad |= !std::isfinite(x[i]);
+    if (bad) throw NumErr("signal contains a non-finite value");
+    if (!xstage_ || xstage_bytes_ < sizeof(R) * nD) {
+      if (xstage_) cudaFreeHost(xstage_);
+      CK(cudaMallocHost(&xstage_, sizeof(R) * nD));
+      xstage_bytes_ = sizeof(R) * nD;
+    }
+    R* xr = static_cast<R*>(xstage_);
+    xs_host_.resize(nD);
+#pragma omp parallel for schedule(static)
     for (int n = 0; n < N_; ++n) {
+      double* xn = xs_host_.data() + (size_t)n * D;
+      normalize_image(cfg_.normalize, H, W, x + (size_t)n * D, xn);
       double s = 0.0;
-      for (size_t i = 0; i < (size_t)D; ++i) s += xs_host_[(size_t)n * D + i] * xs_host_[(size_t)n * D + i];
+      for (size_t i = 0; i < (size_t)D; ++i) {
+        const R v = R(xn[i]);
+        xr[(size_t)n * D + i] = v;
+        xn[i] = double(v);
+        s += xn[i] * xn[i];
+      }
       xnorm2_[n] = s;
     }
-    CK(cudaMemcpyAsync(x_.p, xr.data(), sizeof(R) * nD, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(x_.p, xr, sizeof(R) * nD, cudaMemcpyHostToDevice, st_));
     r2c(x_.p, false, D, xhat_.as<C>(), NB, N_);
     CK(cudaStreamSynchronize(st_));
   }
@@ -1357,6 +1372,8 @@ class Engine final : public EngineBase {
   std::vector<double> dict_, mu_, xnorm2_, xs_host_;
   std::vector<int> live_h_;
   std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero
+  void* xstage_ = nullptr;    // pinned staging of the signals (host -> device)
+  size_t xstage_bytes_ = 0;
   bool dict_zero_ = false, zhat_valid_ = false, profiling_ = false;
   std::vector<Prof> prof_;
   std::vector<cudaEvent_t> marks_;
