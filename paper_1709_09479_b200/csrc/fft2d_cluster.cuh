@@ -3,9 +3,12 @@
 // does not fit one CTA's shared memory (C3: 256 x 256 FP32 = 258 KB).
 //
 // Ownership inside the cluster (rank c):
-//   column passes: columns [c*COLS, (c+1)*COLS) of the W/2 transformed columns,
-//                  all H rows, local layout [H][CS] (CS = COLS + 1, odd stride);
-//                  column 0 (in rank 0) carries the packed pair X[.][0] + i X[.][W/2]
+//   column passes: COLS = W/(2 CL) of the W/2 transformed columns, all H rows,
+//                  local layout [H][CS] (CS = COLS + 1, odd stride). Columns are
+//                  owned in mirror pairs (c, W/2 - c) so that the r2c/c2r pre/post
+//                  processing of a bin and of its mirror happen in one rank and
+//                  every remote element is fetched once (col_of / owner_of).
+//                  Column 0 (rank 0) carries the packed pair X[.][0] + i X[.][W/2].
 //   row passes:    rows [c*ROWS, (c+1)*ROWS), local layout [ROWS][Wh]
 // The transposes between the passes are fused into the first stage of the
 // following pass: its loads read the owning CTA's shared memory through
@@ -64,6 +67,33 @@ struct ClusterPlane {
   }
   __device__ static __forceinline__ C pack_col0(C x0, C xn) { return mk<C>(x0.x - xn.y, x0.y + xn.x); }
 
+  // ---- pair ownership of the transformed columns [0, M) ----
+  // pair p = min(k, M-k) in [0, M/2]; rank c owns pairs [c*HP, (c+1)*HP),
+  // rank 0 also the self-mirror column M/2. Local index cl < HP is the pair's
+  // low column, cl >= HP its mirror (rank 0: cl = 0 -> column 0 (packed),
+  // cl = HP -> column M/2).
+  static constexpr int HP = COLS / 2;
+  static_assert(CL * HP * 2 == M, "pairs per rank");
+  __device__ static __forceinline__ int col_of(unsigned c, int cl) {
+    if (c == 0) {
+      if (cl == 0) return 0;
+      if (cl == HP) return M / 2;
+      return cl < HP ? cl : M - (cl - HP);
+    }
+    const int p = (int)c * HP + (cl % HP);
+    return cl < HP ? p : M - p;
+  }
+  __device__ static __forceinline__ void owner_of(int k, unsigned& c, int& cl) {
+    const int p = k <= M / 2 ? k : M - k;
+    if (p == M / 2) {
+      c = 0;
+      cl = HP;
+    } else {
+      c = (unsigned)(p / HP);
+      cl = (p % HP) + (k <= M / 2 ? 0 : HP);
+    }
+  }
+
   // ---- inverse: column pass (local columns), input generated from global ----
   // gen(r, col) returns natural bin (r, col), col in [0, M]. Returns the
   // column-pass result buffer (a or b), layout [H][CS].
@@ -72,11 +102,10 @@ struct ClusterPlane {
     using S = Split<ColPlan>;
     constexpr int R1 = S::first;
     const C* twc = tw + TW_COL;
-    const int c0 = rank * COLS;
     stockham<C, H, R1, 1, true, COLS, T>(
         twc,
         [&](int cl, int r) {
-          const int col = c0 + cl;
+          const int col = col_of(rank, cl);
           return col == 0 ? pack_col0(gen(r, 0), gen(r, M)) : gen(r, col);
         },
         [&](int l, int i, C v) { a[i * CS + l] = v; });
@@ -102,41 +131,57 @@ struct ClusterPlane {
 
   // ---- inverse row pass: first (transposing) stage reads the whole cluster's
   // column results; the caller must cluster_sync before (producers done) and
-  // after (readers done) this stage. Writes `out` [ROWS][Wh]. All 2R remote
-  // loads of a butterfly are issued before any is consumed.
+  // after (readers done) this stage. Writes `out` [ROWS][Wh]. Butterflies are
+  // processed in mirror pairs (j, J-j) — and (0, J/2), both self-mirrored — so
+  // each remote element is loaded once and all loads of a task are in flight
+  // together.
+  __device__ static __forceinline__ C pre_pair(C xk, C xm, C w) {  // w = W_W^k
+    const C s = mk<C>(xk.x + xm.x, xk.y - xm.y);                  // X[k] + conj X[M-k]
+    const C d = mk<C>(xk.x - xm.x, xk.y + xm.y);                  // X[k] - conj X[M-k]
+    const C wd = cmulc(w, d);
+    return mk<C>(s.x - wd.y, s.y + wd.x);
+  }
   __device__ static __forceinline__ void rows_inv_first(const C* cb, C* out, const C* tw, unsigned rank) {
     using S = Split<RowPlanI>;
-    constexpr int R = S::first, J = M / R, ITEMS = ROWS * J;
+    constexpr int R = S::first, J = M / R, TASKS = ROWS * (J / 2);
+    static_assert(J % 2 == 0, "paired butterflies");
     const int r0 = rank * ROWS;
 #pragma unroll 1
-    for (int it = threadIdx.x; it < ITEMS; it += T) {
-      const int rl = it % ROWS, j = it / ROWS;
+    for (int task = threadIdx.x; task < TASKS; task += T) {
+      const int rl = task % ROWS, t = task / ROWS;
+      const int ja = t == 0 ? 0 : t, jb = t == 0 ? J / 2 : J - t;
       const C* row = cb + (r0 + rl) * CS;
-      C av[R], bv[R];
+      C a[R], b[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const int k = j + q * J;
-        const int km = (k == 0) ? 0 : M - k;
-        av[q] = dsmem_ld(row + (k % COLS), k / COLS);
-        bv[q] = dsmem_ld(row + (km % COLS), km / COLS);
+        unsigned c;
+        int cl;
+        owner_of(ja + J * q, c, cl);
+        a[q] = dsmem_ld(row + cl, c);
+        owner_of(jb + J * q, c, cl);
+        b[q] = dsmem_ld(row + cl, c);
       }
-      C x[R];
+      C xa[R], xb[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const int k = j + q * J;
-        if (k == 0) {
-          x[q] = mk<C>(av[q].x + av[q].y, av[q].x - av[q].y);
+        const int ka = ja + J * q, kb = jb + J * q;
+        if (t == 0) {
+          // item 0: mirror of 16q is item 0 at R-q (q = 0: packed column 0)
+          xa[q] = (q == 0) ? mk<C>(a[0].x + a[0].y, a[0].x - a[0].y) : pre_pair(a[q], a[R - q], tw[TW_PP + ka]);
+          // item J/2: self-mirrored at R-1-q
+          xb[q] = pre_pair(b[q], b[R - 1 - q], tw[TW_PP + kb]);
         } else {
-          const C a = av[q], bb = bv[q];
-          const C s = mk<C>(a.x + bb.x, a.y - bb.y);
-          const C d = mk<C>(a.x - bb.x, a.y + bb.y);
-          const C wd = cmulc(tw[TW_PP + k], d);
-          x[q] = mk<C>(s.x - wd.y, s.y + wd.x);
+          xa[q] = pre_pair(a[q], b[R - 1 - q], tw[TW_PP + ka]);
+          xb[q] = pre_pair(b[q], a[R - 1 - q], tw[TW_PP + kb]);
         }
       }
-      dft<R, true>(x);
+      dft<R, true>(xa);
+      dft<R, true>(xb);
 #pragma unroll
-      for (int s2 = 0; s2 < R; ++s2) out[rl * Wh + j * R + s2] = x[s2];
+      for (int s2 = 0; s2 < R; ++s2) {
+        out[rl * Wh + ja * R + s2] = xa[s2];
+        out[rl * Wh + jb * R + s2] = xb[s2];
+      }
     }
   }
   // remaining inverse row stages (local), input in a; returns result buffer
@@ -165,39 +210,55 @@ struct ClusterPlane {
 
   // ---- forward column pass: first (transposing) stage, reads every CTA's row
   // results; the caller cluster_syncs before and after it. Writes `out` [H][CS].
-  // All 2R remote loads of a butterfly are issued before any is consumed.
+  // The two columns of a mirror pair are produced together from one load of
+  // Z[c] and Z[M-c]: X[c] = E + w O, X[M-c] = conj(E - w O).
   __device__ static __forceinline__ void cols_fwd_first(const C* zb, C* out, const C* tw, unsigned rank) {
     using S = Split<ColPlan>;
-    constexpr int R = S::first, J = H / R, ITEMS = COLS * J;
-    const int c0 = rank * COLS;
+    constexpr int R = S::first, J = H / R, TASKS = HP * J;
 #pragma unroll 1
-    for (int it = threadIdx.x; it < ITEMS; it += T) {
-      const int cl = it % COLS, j = it / COLS;
-      const int col = c0 + cl;
-      const int colm = (col == 0) ? 0 : M - col;
+    for (int task = threadIdx.x; task < TASKS; task += T) {
+      const int pl = task % HP, j = task / HP;
+      // rank 0 / pl 0: column 0 (packed) and column M/2; otherwise pair (pl, pl + HP)
+      const bool special = rank == 0 && pl == 0;
+      const int cla = pl, clb = pl + HP;
+      const int cola = col_of(rank, cla);        // low column (0 for the special task)
+      const int colb = special ? M / 2 : M - cola;
       C z1[R], z2[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int r = j + q * J;
         const C* rowp = zb + (r % ROWS) * Wh;
-        z1[q] = dsmem_ld(rowp + col, r / ROWS);
-        z2[q] = dsmem_ld(rowp + colm, r / ROWS);
+        z1[q] = dsmem_ld(rowp + cola, r / ROWS);
+        z2[q] = dsmem_ld(rowp + colb, r / ROWS);
       }
-      C x[R];
-      const C wpp = tw[TW_PP + col];
+      C xa[R], xb[R];
+      if (special) {
+        const C wm = tw[TW_PP + M / 2];
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        if (col == 0) {
-          x[q] = mk<C>(z1[q].x + z1[q].y, z1[q].x - z1[q].y);
-        } else {
+        for (int q = 0; q < R; ++q) {
+          xa[q] = mk<C>(z1[q].x + z1[q].y, z1[q].x - z1[q].y);
+          const C e = mk<C>(z2[q].x, R_(0));           // (Z + conj Z)/2
+          const C o = mk<C>(z2[q].y, R_(0));           // -i/2 (Z - conj Z)
+          xb[q] = cadd(e, cmul(wm, o));
+        }
+      } else {
+        const C w = tw[TW_PP + cola];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
           const C e = mk<C>(R_(0.5) * (z1[q].x + z2[q].x), R_(0.5) * (z1[q].y - z2[q].y));
           const C o = mk<C>(R_(0.5) * (z1[q].y + z2[q].y), R_(0.5) * (z2[q].x - z1[q].x));
-          x[q] = cadd(e, cmul(wpp, o));
+          const C wo = cmul(w, o);
+          xa[q] = cadd(e, wo);
+          xb[q] = cconj(csub(e, wo));
         }
       }
-      dft<R, false>(x);
+      dft<R, false>(xa);
+      dft<R, false>(xb);
 #pragma unroll
-      for (int s2 = 0; s2 < R; ++s2) out[(j * R + s2) * CS + cl] = x[s2];
+      for (int s2 = 0; s2 < R; ++s2) {
+        out[(j * R + s2) * CS + cla] = xa[s2];
+        out[(j * R + s2) * CS + clb] = xb[s2];
+      }
     }
   }
   using R_ = Rt;
@@ -213,11 +274,10 @@ struct ClusterPlane {
     using Mid = typename Split<typename S::tail>::init;
     const C* twc = tw + TW_COL;
     C* in = run_stages<C, H, false, COLS, CS, 1, T, R1>(a, b, twc, Mid{});
-    const int c0 = rank * COLS;
 #pragma unroll 1
     for (int it = threadIdx.x; it < ITEMS; it += T) {
       const int cl = it % COLS, j = it / COLS;
-      const int col = c0 + cl;
+      const int col = col_of(rank, cl);
       using PT = decltype(pre(0, 1));
       PT pv[RL];
       if (col != 0) {

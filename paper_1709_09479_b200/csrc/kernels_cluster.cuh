@@ -45,7 +45,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   unsigned uphase = 0;
   const unsigned rank = cluster_rank();
   const int g = blockIdx.x / CL, n = blockIdx.y;
-  const int r0 = rank * ROWS, c0 = rank * COLS;
+  const int r0 = rank * ROWS;
   if (ADMM && a.conv[n]) return;  // the whole cluster sees the same flag
 
   CP::load_twiddles(TW, a.tw);
@@ -172,7 +172,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       const int it = threadIdx.x;
       if (it < ITEMS_L) {
         const int cl = it % COLS, j = it / COLS;
-        const int col = c0 + cl;
+        const int col = CP::col_of(rank, cl);
         C pv[RL];
         if (col != 0) {
 #pragma unroll
@@ -207,7 +207,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     const int it = threadIdx.x;
     if (it < ITEMS_L) {
       const int cl = it % COLS, j = it / COLS;
-      const int col = c0 + cl;
+      const int col = CP::col_of(rank, cl);
       if (col != 0) {
 #pragma unroll
         for (int s = 0; s < RL; ++s) dst[(j + s * JL) * Wh + col] = acc[s];
