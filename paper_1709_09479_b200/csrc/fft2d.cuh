@@ -218,21 +218,16 @@ template <int R, int R2, int... Rs> struct Split<RadixList<R, R2, Rs...>> {
   using init = typename Prepend<R, typename rest::init>::type;
 };
 
-// Stage twiddles x[q] *= W_L^(q k STEP): powers of two come from the table,
-// the rest are composed (depth <= log2 R multiplies), cutting table loads from
-// R-1 to log2(R) per butterfly.
+// Stage twiddles x[q] *= W_L^(q k STEP), read straight from the smem table:
+// lanes of a warp share k, so every load is a single-wavefront broadcast and
+// costs one issue slot (cheaper than composing powers with complex multiplies
+// once the kernel is issue-bound).
 template <class C, int R, int STEP, bool INV>
 __device__ __forceinline__ void stage_twiddle(C* x, const C* __restrict__ tw, int k) {
-  C w[R];
   sfor<1, R>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
-    if constexpr ((q & (q - 1)) == 0) {
-      w[q] = tw[q * k * STEP];
-    } else {
-      constexpr int hb = 1 << (31 - __builtin_clz(q));
-      w[q] = cmul(w[hb], w[q - hb]);
-    }
-    x[q] = INV ? cmulc(w[q], x[q]) : cmul(x[q], w[q]);
+    const C w = tw[q * k * STEP];
+    x[q] = INV ? cmulc(w, x[q]) : cmul(x[q], w);
   });
 }
 

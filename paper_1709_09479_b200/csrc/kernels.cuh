@@ -210,18 +210,16 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
               const R th_o = fmin(fmax(uo[e], -beta), beta);
               const R un = t - (th_o - uo[e]);           // u' = t - z/rho
               const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
-              const R zn = rho * (th - un);              // z' = rho (theta' - u')
-              const R d_tt = th - t;
-              const R dz = rho * d_tt;                   // z' - z = rho (theta' - t)
+              const R ez = th - un;                      // z' / rho
+              const R d_tt = th - t;                     // (z' - z) / rho
               const R dth = th - th_o;
-              f0 += d_tt * d_tt;
+              f0 += d_tt * d_tt;                         // sum dz^2 = rho^2 f0 (slot 3)
               f1 += th * th;
               f2 += t * t;
-              f3 += dz * dz;
-              f4 += zn * zn;
+              f4 += ez * ez;                             // sum z'^2 = rho^2 f4
               f5 += dth * dth;
               f6 = fmax(f6, fabs(t));
-              wv[e] = R(2) * th - un;
+              wv[e] = th + ez;                           // w = theta' + z'/rho
               un2[e] = un;
             }
             *up = mk<C>(un2[0], un2[1]);
@@ -231,8 +229,9 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
 #pragma unroll
           for (int s = 0; s < RX; ++s) fout[r * Wh + j * RX + s] = x[s];
         }
-        s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
-        s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
+        const double rr = (double)rho * (double)rho;
+        s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += rr * (double)f0;
+        s4 += rr * (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
       }
       if constexpr (STAGE) fence_async_smem();
       __syncthreads();
