@@ -46,6 +46,7 @@ extern "C" {
 #define DCSC_ERR_NUMERIC 2   /* dcsc::NumericError */
 #define DCSC_ERR_CUDA 3      /* CUDA / NCCL failure */
 #define DCSC_ERR_INVALID 4   /* std::invalid_argument from validate() */
+#define DCSC_ERR_IO 5        /* dcsc::IoError */
 
 typedef struct dcsc_cuda_ctx dcsc_cuda_ctx;
 
@@ -175,6 +176,17 @@ typedef int (*dcsc_allreduce_fn)(double* buf, size_t n, void* user);
 int dcsc_cuda_nccl_unique_id(unsigned char* out, size_t len);
 int dcsc_cuda_set_comm_nccl(dcsc_cuda_ctx* ctx, int world, int rank, const unsigned char* id, size_t len);
 int dcsc_cuda_set_comm_callback(dcsc_cuda_ctx* ctx, int world, int rank, dcsc_allreduce_fn fn, void* user);
+
+/* On-disk formats, byte-compatible with the reference (host only):
+ * CSCT tensors (tensor_io.hpp:1-30; tensor_io.cpp:45-90) and the
+ * convergence-trace CSV (trace_io.hpp; trace_io.cpp:11-76). Errors return
+ * DCSC_ERR_IO with the message in dcsc_io_last_error. */
+int dcsc_io_last_error(char* buf, size_t len);
+int dcsc_io_write_tensor(const char* path, int ndim, const uint64_t* dims, const double* values);
+int dcsc_io_read_tensor_header(const char* path, int* ndim, uint64_t* dims /* 255 */, uint64_t* count);
+int dcsc_io_read_tensor(const char* path, double* values, uint64_t count);
+int dcsc_io_write_trace_csv(const char* path, const dcsc_trace_row* rows, int n);
+int dcsc_io_read_trace_csv(const char* path, dcsc_trace_row* rows, int max_rows, int* n_rows);
 
 /* synthetic BASELINE data (host only, no GPU): x N*H*W, d_true K*m*m */
 int dcsc_synth_generate(int n_images, int height, int width, int filters, int m, double p,

@@ -236,3 +236,25 @@ def coding_batch(xs, d, cfg: Cfg, want_maps=False):
                                   _p(maps) if want_maps else None,
                                   iters.ctypes.data_as(C.POINTER(C.c_int))))
     return iters, maps
+
+
+def write_tensor(path, values):
+    """The reference's CSCT writer (tensor_io.cpp:45-60)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    dims = (C.c_uint64 * v.ndim)(*v.shape)
+    _check(lib().ref_write_tensor(path.encode(), v.ndim, dims, _p(v)))
+
+
+def read_tensor(path, shape):
+    out = np.zeros(shape)
+    _check(lib().ref_read_tensor(path.encode(), _p(out), C.c_uint64(out.size)))
+    return out
+
+
+def write_trace_csv(path, trace):
+    """The reference's trace CSV writer (trace_io.cpp:15-30)."""
+    rows = (RefTraceRow * max(len(trace), 1))()
+    for i, t in enumerate(trace):
+        for f, _ in RefTraceRow._fields_:
+            setattr(rows[i], f, t.get(f, 0))
+    _check(lib().ref_write_trace_csv(path.encode(), rows, len(trace)))

@@ -29,6 +29,8 @@
 #include "dcsc/parallel.hpp"
 #include "dcsc/pipeline.hpp"
 #include "dcsc/spectral.hpp"
+#include "dcsc/tensor_io.hpp"
+#include "dcsc/trace_io.hpp"
 #include "dcsc/types.hpp"
 
 using namespace dcsc;
@@ -83,6 +85,9 @@ int guarded(F&& f) {
   } catch (const NumericError& e) {
     g_err = e.what();
     return 2;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 5;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 4;
@@ -431,6 +436,46 @@ int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int 
     if (maps_out)
       for (int n = 0; n < N; ++n) std::copy(maps[n].values.begin(), maps[n].values.end(), maps_out + n * K * D);
     if (dict_out) std::copy(dict.values.begin(), dict.values.end(), dict_out);
+  });
+}
+
+// The reference's CSCT writer/reader (tensor_io.cpp:45-90) and trace CSV
+// writer (trace_io.cpp:15-30), for byte-compatibility tests of the product's.
+int ref_write_tensor(const char* path, int ndim, const std::uint64_t* dims, const double* values) {
+  return guarded([&] {
+    TensorData t;
+    t.dims.assign(dims, dims + ndim);
+    std::uint64_t n = 1;
+    for (auto d : t.dims) n *= d;
+    t.values.assign(values, values + n);
+    write_tensor(path, t);
+  });
+}
+
+int ref_read_tensor(const char* path, double* values, std::uint64_t count) {
+  return guarded([&] {
+    TensorData t = read_tensor(path);
+    if (t.values.size() != count) throw IoError("count mismatch");
+    std::copy(t.values.begin(), t.values.end(), values);
+  });
+}
+
+int ref_write_trace_csv(const char* path, const ref_trace_row* rows, int n) {
+  return guarded([&] {
+    ConvergenceTrace tr;
+    for (int i = 0; i < n; ++i) {
+      TraceRow r;
+      r.outer_iter = rows[i].outer_iter;
+      r.phase = rows[i].phase == 0 ? Phase::Coding : Phase::Learning;
+      r.objective.total = rows[i].total;
+      r.objective.data_term = rows[i].data_term;
+      r.objective.l1_term = rows[i].l1_term;
+      r.admm_iters = rows[i].admm_iters;
+      r.cg_iters = rows[i].cg_iters;
+      r.elapsed_ms = rows[i].elapsed_ms;
+      tr.rows.push_back(r);
+    }
+    write_trace_csv(std::string(path), tr);
   });
 }
 

@@ -21,6 +21,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libdcsc_cuda.so")
 
 
+class IoError(RuntimeError):
+    pass
+
+
 class DimensionError(RuntimeError):
     pass
 
@@ -37,7 +41,7 @@ class InvalidArgument(ValueError):
     pass
 
 
-_ERRS = {1: DimensionError, 2: NumericError, 3: CudaError, 4: InvalidArgument}
+_ERRS = {1: DimensionError, 2: NumericError, 3: CudaError, 4: InvalidArgument, 5: IoError}
 
 
 class _SolverConfig(C.Structure):
@@ -130,6 +134,8 @@ EXPORTS = [
     "dcsc_cuda_set_profiling", "dcsc_cuda_kernel_time", "dcsc_cuda_event_mark",
     "dcsc_cuda_event_elapsed", "dcsc_cuda_device_bytes", "dcsc_synth_generate",
     "dcsc_cuda_nccl_unique_id", "dcsc_cuda_set_comm_nccl", "dcsc_cuda_set_comm_callback",
+    "dcsc_io_last_error", "dcsc_io_write_tensor", "dcsc_io_read_tensor_header", "dcsc_io_read_tensor",
+    "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -486,3 +492,47 @@ def synth_generate(n_images, grid, filters, m, p, sigma, seed, round_fp32):
     _err(lib().dcsc_synth_generate(n_images, H, W, filters, m, C.c_double(p), C.c_double(sigma),
                                    C.c_uint64(seed), int(round_fp32), _dp(x), _dp(d)))
     return x, d
+
+
+# ---------------------------------------------------------------- on-disk formats
+def _io(rc: int):
+    if rc == 0:
+        return
+    buf = C.create_string_buffer(2048)
+    lib().dcsc_io_last_error(buf, 2048)
+    raise IoError(buf.value.decode())
+
+
+def write_tensor(path: str, values) -> None:
+    """CSCT tensor writer (tensor_io.cpp:45-60): dims = values.shape."""
+    v = _f64(values)
+    dims = (C.c_uint64 * v.ndim)(*v.shape)
+    _io(lib().dcsc_io_write_tensor(path.encode(), v.ndim, dims, _dp(v)))
+
+
+def read_tensor(path: str) -> np.ndarray:
+    """CSCT tensor reader (tensor_io.cpp:62-90)."""
+    nd = C.c_int()
+    dims = (C.c_uint64 * 255)()
+    cnt = C.c_uint64()
+    _io(lib().dcsc_io_read_tensor_header(path.encode(), C.byref(nd), dims, C.byref(cnt)))
+    out = np.zeros(tuple(dims[i] for i in range(nd.value)))
+    _io(lib().dcsc_io_read_tensor(path.encode(), _dp(out), cnt))
+    return out
+
+
+def write_trace_csv(path: str, trace) -> None:
+    """Trace CSV writer (trace_io.cpp:15-30); trace = list of row dicts."""
+    rows = (TraceRow * max(len(trace), 1))()
+    for i, r in enumerate(trace):
+        for f, _ in TraceRow._fields_:
+            setattr(rows[i], f, r.get(f, 0))
+    _io(lib().dcsc_io_write_trace_csv(path.encode(), rows, len(trace)))
+
+
+def read_trace_csv(path: str, max_rows: int = 100000):
+    """Trace CSV reader (trace_io.cpp:32-76)."""
+    rows = (TraceRow * max_rows)()
+    n = C.c_int()
+    _io(lib().dcsc_io_read_trace_csv(path.encode(), rows, max_rows, C.byref(n)))
+    return [rows[i].asdict() for i in range(n.value)]
