@@ -237,3 +237,16 @@ def test_cluster_plane_learning_fp32_matches_reference():
         ctx.set_maps(maps)
         a, b = ctx.learning_data_term(d_g), ctx.learning_data_term(d_r)
     assert abs(a - b) <= FP32_TOL * abs(b)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_run_with_normalisation_matches_reference(mode):
+    """normalize Global (1) / Local (2) (pipeline.cpp:78-121) inside run_csc."""
+    rng = np.random.default_rng(40 + mode)
+    x = rng.random((2, 20, 20)) * 3.0 + 1.0  # raw, un-normalised signals
+    cfg = ref.Cfg(beta=0.3, max_outer=2, normalize=mode, seed=5, tol=1e-300, max_admm=120)
+    r = ref.run(x, 4, (5, 5), cfg)
+    g = dcsc.run_csc(x, 4, (5, 5), dcsc.SolverConfig(beta=0.3, max_outer=2, normalize=mode, seed=5, tol=1e-300,
+                                                     max_admm=120), precision=64)
+    compare_runs(g, r, 1e-9)
+    assert rel(g["dict"], r["dict"]) <= 1e-7
