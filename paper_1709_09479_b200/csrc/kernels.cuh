@@ -101,8 +101,15 @@ struct Smem {
   static constexpr int US = P::M;
   static constexpr size_t u_bytes = sizeof(typename P::C) * P::H * US;
   static constexpr size_t u_off = (two + 127) / 128 * 128;
-  static constexpr bool stage_u = u_off + u_bytes <= 220 * 1024;
-  static constexpr size_t coding = stage_u ? u_off + u_bytes : two;
+  // Preferred: lambda_hat of the CTA's image resident in smem for the whole
+  // filter group (one TMA load per CTA; the generated t_hat stage then reads
+  // only d_hat from L2) and u read straight from L2/HBM in the fused row stage
+  // (column-major pairs: coalesced). Fallback when that does not fit: stage
+  // each filter's u plane by TMA.
+  static constexpr size_t lam_bytes = sizeof(typename P::C) * P::NB;
+  static constexpr bool lam_smem = u_off + lam_bytes <= 220 * 1024;
+  static constexpr bool stage_u = !lam_smem && u_off + u_bytes <= 220 * 1024;
+  static constexpr size_t coding = lam_smem ? u_off + lam_bytes : (stage_u ? u_off + u_bytes : two);
 };
 
 // ----------------------------------------------------------------------------
@@ -138,12 +145,21 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   const int n = blockIdx.y, g = blockIdx.x;
   if (MODE == kPassAdmm && a.conv[n]) return;
 
+  constexpr bool LAMS = (MODE == kPassAdmm) && Smem<P>::lam_smem;
+  C* LAM = reinterpret_cast<C*>(smem_raw + Smem<P>::u_off);
   P::load_twiddles(TW, a.tw);
-  if (STAGE && threadIdx.x == 0) {
+  if ((STAGE || LAMS) && threadIdx.x == 0) {
     mbar_init(ubar, 1);
     fence_async_smem();
   }
   __syncthreads();
+  if constexpr (LAMS) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(ubar, (unsigned)(sizeof(C) * NB));
+      bulk_g2s(LAM, a.lamhat + (size_t)n * NB, (unsigned)(sizeof(C) * NB), ubar);
+    }
+    mbar_wait(ubar, 0);
+  }
   // sum_k d_hat_k w_hat_k for this group, in registers of the bins' owners
   C acc[P::LAST_IPT][P::LAST_R];
 #pragma unroll
@@ -175,7 +191,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       if (threadIdx.x == 0 && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       C* cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
         const int b = r * Wh + c;
-        return cmulc(__ldg(dk + b), __ldg(lam + b));
+        return cmulc(__ldg(dk + b), LAMS ? LAM[b] : __ldg(lam + b));
       });
       C* hin = P::rows_inv_head(cs, cs == B0 ? B1 : B0, TW);
       C* fout = (hin == B0) ? B1 : B0;
