@@ -154,6 +154,11 @@ int dcsc_cuda_dft2_forward(int height, int width, int precision, int batch, cons
 int dcsc_cuda_dft2_inverse(int height, int width, int precision, int batch, const double* in,
                            double* out);
 
+/* device-timed batched r2c / c2r of random planes (mean ms per batch call),
+ * the comparator hook against cuFFT (scripts/fft_comparator.py) */
+int dcsc_cuda_fft_timing(int height, int width, int precision, int batch, int iters, double* ms_r2c,
+                         double* ms_c2r);
+
 /* measurement: kernels launched by this context so far; per-kernel-family
  * CUDA-event timing (family: 0 coding_pass ADMM, 1 lambda_update,
  * 2 learning contractions, 3 learning mask step, 4 other) */

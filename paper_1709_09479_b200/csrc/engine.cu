@@ -1454,6 +1454,59 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
   CK(cudaDeviceSynchronize());
 }
 
+// Device-timed batched r2c and c2r of `batch` planes (random data), for the
+// cuFFT comparator (scripts/fft_comparator.py). Returns the mean ms per call.
+template <class R, int H, int W>
+void fft_timing(int batch, int iters, double* ms_r2c, double* ms_c2r) {
+  using E = Engine<R, H, W>;
+  using P = typename E::P;
+  using C = cx<R>;
+  constexpr int NB = P::NB, D = P::D;
+  E::set_attributes();
+  std::vector<C> tw(P::TW_LEN);
+  fill_twiddles<P>(tw.data());
+  DevMem dtw, real, spec;
+  dtw.alloc(sizeof(C) * P::TW_LEN);
+  CK(cudaMemcpy(dtw.p, tw.data(), dtw.bytes, cudaMemcpyHostToDevice));
+  real.alloc(sizeof(R) * (size_t)batch * D);
+  spec.alloc(sizeof(C) * (size_t)batch * NB);
+  std::vector<R> h((size_t)batch * D);
+  std::mt19937_64 rng(1);
+  for (auto& v : h) v = R(static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5);
+  CK(cudaMemcpy(real.p, h.data(), real.bytes, cudaMemcpyHostToDevice));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  auto time_it = [&](auto&& f) {
+    for (int i = 0; i < 3; ++i) f();
+    CK(cudaEventRecord(a));
+    for (int i = 0; i < iters; ++i) f();
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return (double)ms / iters;
+  };
+  *ms_r2c = time_it([&] {
+    E::template launch_r2c<R>(batch, 0, real.as<R>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+  });
+  *ms_c2r = time_it([&] { E::template launch_c2r<R>(batch, 0, spec.as<C>(), NB, real.as<R>(), D, dtw.as<C>()); });
+  CK(cudaGetLastError());
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
+void fft_timing_dispatch(int H, int W, int prec, int batch, int iters, double* r2c, double* c2r) {
+#define DCSC_FT(Rt, Hh, Ww)                                 \
+  if (prec == prec_of(#Rt) && H == Hh && W == Ww) {        \
+    fft_timing<Rt, Hh, Ww>(batch, iters, r2c, c2r);        \
+    return;                                                 \
+  }
+  DCSC_SIZES(DCSC_FT)
+#undef DCSC_FT
+  throw DimErr("no compiled FFT for this grid/precision");
+}
+
 void dft_dispatch(int H, int W, int prec, bool inverse, int batch, const double* in, double* out) {
 #define DCSC_DFT(Rt, Hh, Ww)                           \
   if (prec == prec_of(#Rt) && H == Hh && W == Ww) {    \
@@ -1593,6 +1646,10 @@ int dcsc_cuda_dft2_forward(int height, int width, int precision, int batch, cons
 }
 int dcsc_cuda_dft2_inverse(int height, int width, int precision, int batch, const double* in, double* out) {
   return guarded([&] { dft_dispatch(height, width, precision, true, batch, in, out); });
+}
+int dcsc_cuda_fft_timing(int height, int width, int precision, int batch, int iters, double* ms_r2c,
+                         double* ms_c2r) {
+  return guarded([&] { fft_timing_dispatch(height, width, precision, batch, iters, ms_r2c, ms_c2r); });
 }
 int dcsc_cuda_kernel_launches(dcsc_cuda_ctx* ctx, long long* count) {
   CTX_CHECK

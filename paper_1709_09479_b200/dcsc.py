@@ -135,7 +135,7 @@ EXPORTS = [
     "dcsc_cuda_event_elapsed", "dcsc_cuda_device_bytes", "dcsc_synth_generate",
     "dcsc_cuda_nccl_unique_id", "dcsc_cuda_set_comm_nccl", "dcsc_cuda_set_comm_callback",
     "dcsc_io_last_error", "dcsc_io_write_tensor", "dcsc_io_read_tensor_header", "dcsc_io_read_tensor",
-    "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv",
+    "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -482,6 +482,13 @@ def inverse_dft2(s, width: int, precision: int = 64):
     out = np.zeros((B, H, width))
     _err(lib().dcsc_cuda_dft2_inverse(H, width, precision, B, s.ctypes.data_as(C.POINTER(C.c_double)), _dp(out)))
     return out
+
+
+def fft_timing(grid, precision: int, batch: int, iters: int = 20):
+    """Device-timed batched r2c / c2r of our FFT engine (ms per batch call)."""
+    a, b = C.c_double(), C.c_double()
+    _err(lib().dcsc_cuda_fft_timing(grid[0], grid[1], precision, batch, iters, C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def synth_generate(n_images, grid, filters, m, p, sigma, seed, round_fp32):
