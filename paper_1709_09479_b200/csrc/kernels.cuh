@@ -476,7 +476,15 @@ r2c_planes(const SRC* __restrict__ src, size_t src_stride, cx<typename P::R>* __
   int any = 0;
   for (int it = threadIdx.x; it < H * M; it += T) {
     const int r = it / M, m = it % M;
-    const R v0 = R(s[r * W + 2 * m]), v1 = R(s[r * W + 2 * m + 1]);
+    R v0, v1;
+    if constexpr (std::is_same<SRC, R>::value) {  // pixel pair as one vector load
+      const C v = reinterpret_cast<const C*>(s)[it];
+      v0 = v.x;
+      v1 = v.y;
+    } else {
+      v0 = R(s[r * W + 2 * m]);
+      v1 = R(s[r * W + 2 * m + 1]);
+    }
     any |= (v0 != R(0)) | (v1 != R(0));
     B0[r * Wh + m] = mk<C>(v0, v1);
   }
@@ -537,8 +545,12 @@ c2r_planes(const cx<typename P::R>* __restrict__ src, size_t src_stride, DST* __
   for (int it = threadIdx.x; it < H * M; it += T) {
     const int r = it / M, m = it % M;
     const C v = sp[r * Wh + m];
-    o[r * W + 2 * m] = DST(v.x * sc);
-    o[r * W + 2 * m + 1] = DST(v.y * sc);
+    if constexpr (std::is_same<DST, R>::value) {
+      reinterpret_cast<C*>(o)[it] = mk<C>(v.x * sc, v.y * sc);
+    } else {
+      o[r * W + 2 * m] = DST(v.x * sc);
+      o[r * W + 2 * m + 1] = DST(v.y * sc);
+    }
   }
 }
 
