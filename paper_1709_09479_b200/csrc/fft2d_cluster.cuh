@@ -6,15 +6,20 @@
 //   column passes: COLS = W/(2 CL) of the W/2 transformed columns, all H rows,
 //                  local layout [H][CS] (CS = COLS + 1, odd stride). Columns are
 //                  owned in mirror pairs (c, W/2 - c) so that the r2c/c2r pre/post
-//                  processing of a bin and of its mirror happen in one rank and
-//                  every remote element is fetched once (col_of / owner_of).
-//                  Column 0 (rank 0) carries the packed pair X[.][0] + i X[.][W/2].
-//   row passes:    rows [c*ROWS, (c+1)*ROWS), local layout [ROWS][Wh]
-// The transposes between the passes are fused into the first stage of the
-// following pass: its loads read the owning CTA's shared memory through
-// mapa + ld.shared::cluster, together with the r2c/c2r pre/post-processing
-// pairs (k, W/2-k). Cluster barriers order producer stores, remote reads and
-// buffer reuse. Conventions are those of fft2d.cuh (Plane).
+//                  processing of a bin and of its mirror happen in one rank
+//                  (col_of / owner_of). Column 0 (rank 0) carries the packed pair
+//                  X[.][0] + i X[.][W/2].
+//   row passes:    rows [c*ROWS, (c+1)*ROWS), local layout [ROWS][Wh].
+// Transposes are block exchanges: a column buffer [H][CS] is CL contiguous
+// blocks [ROWS][CS] (block q = rank q's rows), and each block travels to its
+// rank with one TMA bulk copy into the peer's staging buffer
+// (cp.async.bulk.shared::cluster.shared::cta, completion counted on the
+// receiver's mbarrier; kernels_cluster.cuh). The staging buffer then reads as
+// [CL src][ROWS][CS] — i.e. exactly the [H][CS] column layout after the
+// forward exchange — and the first stage of the next pass loads from it with
+// the r2c/c2r pre/post-processing pairs (k, W/2-k) fused; the forward row pass
+// stores its last stage straight into the send layout. No remote loads go
+// through the LSU. Conventions are those of fft2d.cuh (Plane).
 #pragma once
 #include "fft2d.cuh"
 
@@ -30,21 +35,6 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ float2 dsmem_ld(const float2* p, unsigned rank) {
-  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p)), r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  float2 v;
-  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(r) : "memory");
-  return v;
-}
-__device__ __forceinline__ double2 dsmem_ld(const double2* p, unsigned rank) {
-  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p)), r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-  double2 v;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(r) : "memory");
-  return v;
-}
-
 template <class Rt, int H_, int W_, int CL_, int T_>
 struct ClusterPlane {
   using R = Rt;
@@ -52,15 +42,19 @@ struct ClusterPlane {
   static constexpr int H = H_, W = W_, T = T_, CL = CL_;
   static constexpr int M = W / 2, Wh = M + 1, NB = H * Wh, D = H * W;
   static constexpr int ROWS = H / CL, COLS = M / CL, CS = COLS + 1;
+  static constexpr int BLOCK = ROWS * CS;  // complex per exchanged block
   static_assert(H % CL == 0 && M % CL == 0, "cluster split");
+  static_assert((BLOCK * sizeof(C)) % 16 == 0, "bulk copies move multiples of 16 bytes");
   static constexpr int BUF = (H * CS > ROWS * Wh) ? H * CS : ROWS * Wh;  // complex per buffer
-  static constexpr size_t buffer_bytes = sizeof(C) * BUF;
+  static constexpr size_t buffer_bytes = (sizeof(C) * BUF + 127) / 128 * 128;
+  static constexpr unsigned block_bytes = sizeof(C) * BLOCK;
   using RowPlan = typename PlanFor<M>::type;
   using RowPlanI = typename Reverse<RowPlan>::type;
   using ColPlan = typename PlanFor<H>::type;
   static constexpr int TW_ROW = 0, TW_COL = M, TW_PP = M + H;
   static constexpr int TW_LEN = 2 * M + H + 1;
-  static_assert(CountStages<ColPlan>::value >= 2, "column plan needs a transposing and a last stage");
+  static_assert(CountStages<ColPlan>::value >= 2, "column plan needs a first and a last stage");
+  static_assert(CountStages<RowPlan>::value >= 2, "row plan needs a first and a last stage");
 
   __device__ static __forceinline__ void load_twiddles(C* tw_s, const C* __restrict__ tw_g) {
     for (int i = threadIdx.x; i < TW_LEN; i += T) tw_s[i] = tw_g[i];
@@ -93,6 +87,13 @@ struct ClusterPlane {
       cl = (p % HP) + (k <= M / 2 ? 0 : HP);
     }
   }
+  // offset of (row-local rl, column k) in a staging buffer [CL][ROWS][CS]
+  __device__ static __forceinline__ int stage_off(int rl, int k) {
+    unsigned c;
+    int cl;
+    owner_of(k, c, cl);
+    return (int)c * BLOCK + rl * CS + cl;
+  }
 
   // ---- inverse: column pass (local columns), input generated from global ----
   // gen(r, col) returns natural bin (r, col), col in [0, M]. Returns the
@@ -113,60 +114,36 @@ struct ClusterPlane {
     return run_stages<C, H, true, COLS, CS, 1, T, R1>(a, b, twc, typename S::tail{});
   }
 
-  // c2r pre-processing of global row rg at index k, reading the column-pass
-  // result `cb` (same offset in every CTA) of the owning ranks.
-  __device__ static __forceinline__ C pre_remote(const C* cb, const C* tw, int rg, int k) {
-    if (k == 0) {
-      const C q = dsmem_ld(cb + rg * CS, 0);
-      return mk<C>(q.x + q.y, q.x - q.y);
-    }
-    const C a = dsmem_ld(cb + rg * CS + (k % COLS), k / COLS);
-    const int km = M - k;
-    const C bb = dsmem_ld(cb + rg * CS + (km % COLS), km / COLS);
-    const C s = mk<C>(a.x + bb.x, a.y - bb.y);
-    const C d = mk<C>(a.x - bb.x, a.y + bb.y);
-    const C wd = cmulc(tw[TW_PP + k], d);
-    return mk<C>(s.x - wd.y, s.y + wd.x);
-  }
-
-  // ---- inverse row pass: first (transposing) stage reads the whole cluster's
-  // column results; the caller must cluster_sync before (producers done) and
-  // after (readers done) this stage. Writes `out` [ROWS][Wh]. Butterflies are
-  // processed in mirror pairs (j, J-j) — and (0, J/2), both self-mirrored — so
-  // each remote element is loaded once and all loads of a task are in flight
-  // together.
   __device__ static __forceinline__ C pre_pair(C xk, C xm, C w) {  // w = W_W^k
     const C s = mk<C>(xk.x + xm.x, xk.y - xm.y);                  // X[k] + conj X[M-k]
     const C d = mk<C>(xk.x - xm.x, xk.y + xm.y);                  // X[k] - conj X[M-k]
     const C wd = cmulc(w, d);
     return mk<C>(s.x - wd.y, s.y + wd.x);
   }
-  __device__ static __forceinline__ void rows_inv_first(const C* cb, C* out, const C* tw, unsigned rank) {
+  // ---- inverse row pass, first stage: reads the received column blocks
+  // `stg` [CL][ROWS][CS] with the c2r pre-processing fused; writes `out`
+  // [ROWS][Wh]. Butterflies go in mirror pairs (j, J-j) — and (0, J/2), both
+  // self-mirrored — so every staged element is loaded once.
+  __device__ static __forceinline__ void rows_inv_first(const C* stg, C* out, const C* tw) {
     using S = Split<RowPlanI>;
     constexpr int R = S::first, J = M / R, TASKS = ROWS * (J / 2);
     static_assert(J % 2 == 0, "paired butterflies");
-    const int r0 = rank * ROWS;
 #pragma unroll 1
     for (int task = threadIdx.x; task < TASKS; task += T) {
       const int rl = task % ROWS, t = task / ROWS;
       const int ja = t == 0 ? 0 : t, jb = t == 0 ? J / 2 : J - t;
-      const C* row = cb + (r0 + rl) * CS;
       C a[R], b[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        unsigned c;
-        int cl;
-        owner_of(ja + J * q, c, cl);
-        a[q] = dsmem_ld(row + cl, c);
-        owner_of(jb + J * q, c, cl);
-        b[q] = dsmem_ld(row + cl, c);
+        a[q] = stg[stage_off(rl, ja + J * q)];
+        b[q] = stg[stage_off(rl, jb + J * q)];
       }
       C xa[R], xb[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int ka = ja + J * q, kb = jb + J * q;
         if (t == 0) {
-          // item 0: mirror of 16q is item 0 at R-q (q = 0: packed column 0)
+          // item 0: mirror of J q is item 0 at R-q (q = 0: packed column 0)
           xa[q] = (q == 0) ? mk<C>(a[0].x + a[0].y, a[0].x - a[0].y) : pre_pair(a[q], a[R - q], tw[TW_PP + ka]);
           // item J/2: self-mirrored at R-1-q
           xb[q] = pre_pair(b[q], b[R - 1 - q], tw[TW_PP + kb]);
@@ -190,29 +167,29 @@ struct ClusterPlane {
     return run_stages<C, M, true, ROWS, 1, Wh, T, S::first>(a, b, tw + TW_ROW, typename S::tail{});
   }
 
-  // ---- forward row pass (local rows) ----
-  __device__ static __forceinline__ C* rows_fwd(C* a, C* b, const C* tw) {
-    return run_stages<C, M, false, ROWS, 1, Wh, T, 1>(a, b, tw + TW_ROW, RowPlan{});
+  // ---- forward row pass (local rows): spatial pairs in `a`, scratch `b`;
+  // the last stage stores into the send layout snd [CL dst][ROWS][CS]
+  // (column k of row rl -> its owner's block). snd may alias `a`.
+  __device__ static __forceinline__ void rows_fwd_to_send(C* a, C* b, C* snd, const C* tw) {
+    using S = Split<RowPlan>;
+    static_assert(CountStages<RowPlan>::value == 2, "two-stage row plan: a -> b -> snd");
+    constexpr int RL = S::last;
+    constexpr int NSL = M / RL;
+    stockham<C, M, S::first, 1, false, ROWS, T>(
+        tw + TW_ROW, [&](int l, int i) { return a[l * Wh + i]; }, [&](int l, int i, C v) { b[l * Wh + i] = v; });
+    __syncthreads();
+    stockham<C, M, RL, NSL, false, ROWS, T>(
+        tw + TW_ROW, [&](int l, int i) { return b[l * Wh + i]; },
+        [&](int l, int i, C v) { snd[stage_off(l, i)] = v; });
+    __syncthreads();
   }
 
-  // r2c post-processing of global row r at column col from the row results
-  // `zb` (same offset in every CTA) of the owning ranks.
-  __device__ static __forceinline__ C post_remote(const C* zb, const C* tw, int r, int col) {
-    const unsigned own = r / ROWS;
-    const C* rowp = zb + (r % ROWS) * Wh;
-    const C z1 = dsmem_ld(rowp + col, own);
-    if (col == 0) return mk<C>(z1.x + z1.y, z1.x - z1.y);
-    const C z2 = dsmem_ld(rowp + (M - col), own);
-    const C e = mk<C>(R(0.5) * (z1.x + z2.x), R(0.5) * (z1.y - z2.y));
-    const C o = mk<C>(R(0.5) * (z1.y + z2.y), R(0.5) * (z2.x - z1.x));
-    return cadd(e, cmul(tw[TW_PP + col], o));
-  }
-
-  // ---- forward column pass: first (transposing) stage, reads every CTA's row
-  // results; the caller cluster_syncs before and after it. Writes `out` [H][CS].
-  // The two columns of a mirror pair are produced together from one load of
-  // Z[c] and Z[M-c]: X[c] = E + w O, X[M-c] = conj(E - w O).
-  __device__ static __forceinline__ void cols_fwd_first(const C* zb, C* out, const C* tw, unsigned rank) {
+  // ---- forward column pass, first stage: reads the received column buffer
+  // zc [H][CS] (rows of every rank, this rank's columns) with the r2c
+  // post-processing fused. The two columns of a mirror pair are produced
+  // together from one load of Z[c] and Z[M-c]: X[c] = E + w O,
+  // X[M-c] = conj(E - w O). Writes `out` [H][CS].
+  __device__ static __forceinline__ void cols_fwd_first(const C* zc, C* out, const C* tw, unsigned rank) {
     using S = Split<ColPlan>;
     constexpr int R = S::first, J = H / R, TASKS = HP * J;
 #pragma unroll 1
@@ -221,15 +198,13 @@ struct ClusterPlane {
       // rank 0 / pl 0: column 0 (packed) and column M/2; otherwise pair (pl, pl + HP)
       const bool special = rank == 0 && pl == 0;
       const int cla = pl, clb = pl + HP;
-      const int cola = col_of(rank, cla);        // low column (0 for the special task)
-      const int colb = special ? M / 2 : M - cola;
+      const int cola = col_of(rank, cla);  // low column (0 for the special task)
       C z1[R], z2[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int r = j + q * J;
-        const C* rowp = zb + (r % ROWS) * Wh;
-        z1[q] = dsmem_ld(rowp + cola, r / ROWS);
-        z2[q] = dsmem_ld(rowp + colb, r / ROWS);
+        z1[q] = zc[r * CS + cla];
+        z2[q] = zc[r * CS + clb];
       }
       C xa[R], xb[R];
       if (special) {
@@ -237,8 +212,8 @@ struct ClusterPlane {
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           xa[q] = mk<C>(z1[q].x + z1[q].y, z1[q].x - z1[q].y);
-          const C e = mk<C>(z2[q].x, R_(0));           // (Z + conj Z)/2
-          const C o = mk<C>(z2[q].y, R_(0));           // -i/2 (Z - conj Z)
+          const C e = mk<C>(z2[q].x, R_(0));  // (Z + conj Z)/2
+          const C o = mk<C>(z2[q].y, R_(0));  // -i/2 (Z - conj Z)
           xb[q] = cadd(e, cmul(wm, o));
         }
       } else {

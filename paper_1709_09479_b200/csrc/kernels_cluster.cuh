@@ -1,7 +1,18 @@
 // Cluster (multi-CTA per plane) variants of the hot-path kernels for planes
 // whose half spectrum exceeds one CTA's shared memory (C3: 256 x 256 FP32).
 // Same algorithms and reference anchors as kernels.cuh; the FFT work of one
-// plane is split over a CP::CL-CTA cluster (fft2d_cluster.cuh).
+// plane is split over a CP::CL-CTA cluster (fft2d_cluster.cuh), the two
+// transposes per plane are TMA bulk block exchanges between the CTAs' shared
+// memories (cl_issue_exchange).
+//
+// Buffers (3 x [BUF] complex per CTA): X, Y, Z. One plane round trip:
+//   cols_inv      gen -> X -> Y            (Y = send blocks of exchange I)
+//   exchange I    Y -> peers' Z            (Z = [CL src][ROWS][CS])
+//   rows_inv      Z -> X -> Z              (Z = spatial rows)
+//   prox / load   Z in place
+//   rows_fwd      Z -> X -> Z (send layout; exchange F)
+//   exchange F    Z -> peers' Y            (Y = [H][CS] column buffer)
+//   cols_fwd      Y -> X -> consumer
 #pragma once
 #include "fft2d_cluster.cuh"
 #include "kernels.cuh"
@@ -11,18 +22,77 @@ namespace dcsc_cuda {
 template <class CP>
 struct SmemCl {
   using C = typename CP::C;
-  static constexpr size_t bufs = 2 * CP::buffer_bytes;
+  static constexpr size_t bufs = 3 * CP::buffer_bytes;
   static constexpr size_t tw_off = bufs;
   static constexpr size_t col0_off = tw_off + sizeof(C) * CP::TW_LEN;
-  static constexpr size_t u_off = (col0_off + sizeof(C) * CP::H + 127) / 128 * 128;
-  static constexpr size_t u_bytes = sizeof(C) * CP::ROWS * CP::M;  // this CTA's rows of u (pixel pairs)
-  static constexpr size_t plain = u_off;
-  static constexpr size_t coding = u_off + u_bytes;
+  static constexpr size_t plain = col0_off + sizeof(C) * CP::H;
+  static constexpr size_t coding = plain;
 };
+
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init_cluster() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Bulk copy of `bytes` from this CTA's smem to the same-offset address `dst`
+// in peer CTA `peer`; completion is counted on the peer's mbarrier `bar`.
+__device__ __forceinline__ void bulk_s2peer(void* dst, unsigned peer, const void* src, unsigned bytes,
+                                            unsigned long long* bar) {
+  unsigned d, b;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(smem_addr(dst)), "r"(peer));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(b) : "r"(smem_addr(bar)), "r"(peer));
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   d),
+               "r"(smem_addr(src)), "r"(bytes), "r"(b)
+               : "memory");
+}
+
+// Block q of snd -> slot `rank` of peer q's stg (one bulk copy per peer,
+// itself included). The caller has made snd visible to the async proxy
+// (fence_async_smem + __syncthreads) and knows every peer's stg is free.
+template <class CP>
+__device__ __forceinline__ void cl_issue_exchange(const typename CP::C* snd, typename CP::C* stg, unsigned rank,
+                                                  unsigned long long* bar) {
+  if (threadIdx.x == 0) mbar_expect_tx(bar, CP::CL * CP::block_bytes);
+  if (threadIdx.x < CP::CL) {
+    const unsigned q = threadIdx.x;
+    bulk_s2peer(stg + rank * CP::BLOCK, q, snd + q * CP::BLOCK, CP::block_bytes, bar);
+  }
+}
+
+// Fully synchronised exchange (single-plane helper kernels).
+template <class CP>
+__device__ __forceinline__ void cl_exchange_sync(const typename CP::C* snd, typename CP::C* stg, unsigned rank,
+                                                 unsigned long long* bar, unsigned& phase) {
+  fence_async_smem();
+  __syncthreads();
+  cluster_sync_all();  // every rank: send blocks written, staging free
+  cl_issue_exchange<CP>(snd, stg, rank, bar);
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+  cluster_sync_all();  // every block delivered: send buffers reusable
+}
+
+template <class CP>
+__device__ __forceinline__ void cl_init_exchange(unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init_cluster();
+  }
+  __syncthreads();
+}
 
 // The fused coding kernel (see coding_pass in kernels.cuh) with each plane's
 // FFTs split over a cluster: rank c owns rows [c*ROWS, ...) of u / w and
-// columns [c*COLS, ...) of the spectra. blockIdx.x = group * CL + rank.
+// columns col_of(c, .) of the spectra. blockIdx.x = group * CL + rank.
+// Cluster barrier phases are split (arrive early, wait late): B_I (after the
+// staged blocks of exchange I are consumed) is awaited before exchange F is
+// issued, B_F (after exchange F's blocks are consumed) before the next
+// filter's exchange I / plane load — two barriers per filter, each with a
+// pass of slack.
 template <class CP, int MODE>
 __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     coding_pass_cl(CodingArgs<typename CP::R> a) {
@@ -30,32 +100,32 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   using C = typename CP::C;
   using SM = SmemCl<CP>;
   constexpr int H = CP::H, M = CP::M, Wh = CP::Wh, NB = CP::NB, D = CP::D, T = CP::T, CL = CP::CL;
-  constexpr int ROWS = CP::ROWS, COLS = CP::COLS;
+  constexpr int ROWS = CP::ROWS, COLS = CP::COLS, CS = CP::CS;
+  constexpr int BS = CP::buffer_bytes / sizeof(C);
   constexpr bool ADMM = MODE == kPassAdmm;
+  using S = Split<typename CP::ColPlan>;
+  static_assert(CountStages<typename CP::ColPlan>::value == 2, "two-stage column plan (X -> Y)");
+  static_assert(CountStages<typename CP::RowPlan>::value == 2, "two-stage row plan (Z -> X -> Z)");
 
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double red[kSums * (T / 32)];
-  __shared__ __align__(8) unsigned long long ubar_s;
-  C* B0 = reinterpret_cast<C*>(smem_raw);
-  C* B1 = B0 + CP::BUF;
+  __shared__ __align__(8) unsigned long long xbar_s;
+  C* X = reinterpret_cast<C*>(smem_raw);
+  C* Y = X + BS;
+  C* Z = Y + BS;
   C* TW = reinterpret_cast<C*>(smem_raw + SM::tw_off);
   C* COL0 = reinterpret_cast<C*>(smem_raw + SM::col0_off);
-  C* U = reinterpret_cast<C*>(smem_raw + SM::u_off);
-  unsigned long long* ubar = &ubar_s;
-  unsigned uphase = 0;
+  unsigned long long* xbar = &xbar_s;
+  unsigned xphase = 0;
   const unsigned rank = cluster_rank();
   const int g = blockIdx.x / CL, n = blockIdx.y;
   const int r0 = rank * ROWS;
   if (ADMM && a.conv[n]) return;  // the whole cluster sees the same flag
 
   CP::load_twiddles(TW, a.tw);
-  if (ADMM && threadIdx.x == 0) {
-    mbar_init(ubar, 1);
-    fence_async_smem();
-  }
-  __syncthreads();
+  cl_init_exchange<CP>(xbar);
+  cluster_arrive();  // matched by the wait before the first filter's exchange
 
-  using S = Split<typename CP::ColPlan>;
   constexpr int RL = S::last, JL = H / RL, ITEMS_L = COLS * JL;
   static_assert(ITEMS_L <= T, "one last-stage item per thread");
   C acc[RL];
@@ -69,34 +139,33 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   const int k1 = min(a.K, k0 + a.kpg);
   for (int k = k0; k < k1; ++k) {
     const C* __restrict__ dk = a.dhat + (size_t)k * NB;
-    C* w;  // buffer holding this CTA's rows of w (spatial pairs)
     if constexpr (ADMM) {
       C* __restrict__ uk = reinterpret_cast<C*>(a.u + ((size_t)n * a.K + k) * D) + (size_t)r0 * M;
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if (threadIdx.x == 0) {
-        bulk_wait_read0();
-        mbar_expect_tx(ubar, (unsigned)SM::u_bytes);
-        bulk_g2s(U, uk, (unsigned)SM::u_bytes, ubar);
+        prefetch_l2_bulk(uk, sizeof(C) * ROWS * M);
         if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       }
-      C* cs = CP::cols_inv(B0, B1, TW, rank, [&](int r, int c) {
+      CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
         const int b = r * Wh + c;
         return cmulc(__ldg(dk + b), __ldg(lam + b));
       });
-      C* ob = (cs == B0) ? B1 : B0;
-      cluster_sync_all();  // every rank's column results are in place
-      CP::rows_inv_first(cs, ob, TW, rank);
+      fence_async_smem();
       __syncthreads();
-      cluster_sync_all();  // every rank is done reading cs
-      C* sp = CP::rows_inv_rest(ob, cs, TW);
-      mbar_wait(ubar, uphase);
-      uphase ^= 1u;
+      cluster_wait();  // B_F (previous filter): peers' Z free
+      cl_issue_exchange<CP>(Y, Z, rank, xbar);
+      mbar_wait(xbar, xphase);
+      xphase ^= 1u;
+      CP::rows_inv_first(Z, X, TW);
+      __syncthreads();
+      cluster_arrive();  // B_I: my Z consumed, my incoming blocks complete
+      CP::rows_inv_rest(X, Z, TW);
       R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
 #pragma unroll 4
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
         const int rl = it / M, m = it % M;
-        const C uv = U[it];
-        const C v = sp[rl * Wh + m];
+        const C uv = uk[it];
+        const C v = Z[rl * Wh + m];
         const R tv[2] = {v.x * invD, v.y * invD};
         const R uo[2] = {uv.x, uv.y};
         R wv[2], un2[2];
@@ -120,22 +189,17 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
           wv[e] = R(2) * th - un;
           un2[e] = un;
         }
-        U[it] = mk<C>(un2[0], un2[1]);
-        sp[rl * Wh + m] = mk<C>(wv[0], wv[1]);
+        uk[it] = mk<C>(un2[0], un2[1]);
+        Z[rl * Wh + m] = mk<C>(wv[0], wv[1]);
       }
       s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
       s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
-      fence_async_smem();
       __syncthreads();
-      if (threadIdx.x == 0) {
-        bulk_s2g(uk, U, (unsigned)SM::u_bytes);
-        bulk_commit();
-      }
-      w = sp;
     } else {
       const C* __restrict__ src = reinterpret_cast<const C*>(
           (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D) +
           (size_t)r0 * M;
+      cluster_wait();  // B_F (previous filter): my Z no longer read by peers' copies
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
         const int rl = it / M, m = it % M;
         const C v = src[it];
@@ -152,23 +216,23 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
           w1 = v.y;
           s0 += (double)fabs(w0) + (double)fabs(w1);
         }
-        B0[rl * Wh + m] = mk<C>(w0, w1);
+        Z[rl * Wh + m] = mk<C>(w0, w1);
       }
       __syncthreads();
-      w = B0;
     }
-    // forward: local rows, transposing first column stage, accumulating last stage
-    C* z = CP::rows_fwd(w, w == B0 ? B1 : B0, TW);
-    C* zo = (z == B0) ? B1 : B0;
-    cluster_sync_all();  // every rank's row results are in place
-    CP::cols_fwd_first(z, zo, TW, rank);
+    // forward: local rows into the send layout, exchange F, column pass
+    CP::rows_fwd_to_send(Z, X, Z, TW);
+    fence_async_smem();
     __syncthreads();
-    cluster_sync_all();  // every rank is done reading z
+    if constexpr (ADMM) cluster_wait();  // B_I: peers' Y free (else covered by the wait at the filter start)
+    cl_issue_exchange<CP>(Z, Y, rank, xbar);
+    mbar_wait(xbar, xphase);
+    xphase ^= 1u;
+    CP::cols_fwd_first(Y, X, TW, rank);
+    __syncthreads();
+    cluster_arrive();  // B_F: my Y consumed, my incoming blocks complete
     {
-      // middle stages (none for a two-stage plan) then the accumulating last stage
-      using Mid = typename Split<typename S::tail>::init;
       const C* twc = TW + CP::TW_COL;
-      C* in = run_stages<C, H, false, COLS, CP::CS, 1, T, S::first>(zo, z, twc, Mid{});
       const int it = threadIdx.x;
       if (it < ITEMS_L) {
         const int cl = it % COLS, j = it / COLS;
@@ -180,7 +244,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         }
         C x[RL];
 #pragma unroll
-        for (int q = 0; q < RL; ++q) x[q] = in[(j + q * JL) * CP::CS + cl];
+        for (int q = 0; q < RL; ++q) x[q] = X[(j + q * JL) * CS + cl];
         if constexpr (JL > 1) stage_twiddle<C, RL, H / (JL * RL), false>(x, twc, j);
         dft<RL, false>(x);
         if (col == 0) {
@@ -201,7 +265,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       accN = cadd(accN, cmul(__ldg(dk + r * Wh + M), xn));
     }
   }
-  if (ADMM && threadIdx.x == 0) bulk_wait0();
+  cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
   {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
     const int it = threadIdx.x;
@@ -218,7 +282,6 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       dst[threadIdx.x * Wh + M] = accN;
     }
   }
-  cluster_sync_all();  // no rank exits while a peer may still address its smem
   double v[7] = {s0, s1, s2, s3, s4, s5, 0.0};
   block_sum<T, 7>(v, red);
   const double mx = block_max(s6, red, T);
@@ -281,44 +344,53 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   }
 }
 
-// Forward of this CTA's rows (spatial pairs already in B0) to a global NSL
-// spectrum d; every rank stores its own columns, rank 0 the packed pair.
+// Single-plane helpers. Buffers as above; every exchange fully synchronised.
 template <class CP>
-__device__ __forceinline__ void cl_forward_to_global(typename CP::C* B0, typename CP::C* B1,
-                                                     const typename CP::C* TW, typename CP::C* COL0,
-                                                     unsigned rank, typename CP::C* __restrict__ d) {
+struct ClBufs {
+  using C = typename CP::C;
+  C *X, *Y, *Z, *TW, *COL0;
+  unsigned long long* bar;
+  unsigned phase;
+  __device__ ClBufs(unsigned char* raw, unsigned long long* b) : bar(b), phase(0) {
+    constexpr int BS = CP::buffer_bytes / sizeof(C);
+    X = reinterpret_cast<C*>(raw);
+    Y = X + BS;
+    Z = Y + BS;
+    TW = reinterpret_cast<C*>(raw + SmemCl<CP>::tw_off);
+    COL0 = reinterpret_cast<C*>(raw + SmemCl<CP>::col0_off);
+  }
+};
+
+// Forward of this CTA's rows (spatial pairs in Z) to a global NSL spectrum d;
+// every rank stores its own columns, rank 0 the packed pair.
+template <class CP>
+__device__ __forceinline__ void cl_forward_to_global(ClBufs<CP>& b, unsigned rank, typename CP::C* __restrict__ d) {
   using C = typename CP::C;
   constexpr int Wh = CP::Wh, M = CP::M, H = CP::H, T = CP::T;
-  C* z = CP::rows_fwd(B0, B1, TW);
-  C* zo = (z == B0) ? B1 : B0;
-  cluster_sync_all();
-  CP::cols_fwd_first(z, zo, TW, rank);
+  CP::rows_fwd_to_send(b.Z, b.X, b.Z, b.TW);
+  cl_exchange_sync<CP>(b.Z, b.Y, rank, b.bar, b.phase);
+  CP::cols_fwd_first(b.Y, b.X, b.TW, rank);
   __syncthreads();
-  cluster_sync_all();
-  CP::cols_fwd_rest(zo, z, TW, rank, COL0, [](int, int) { return 0; },
+  CP::cols_fwd_rest(b.X, b.Y, b.TW, rank, b.COL0, [](int, int) { return 0; },
                     [&](int r, int c, C v, int) { d[r * Wh + c] = v; });
   if (rank == 0)
     for (int r = threadIdx.x; r < H; r += T) {
       C x0, xn;
-      CP::unpack_col0(COL0, r, x0, xn);
+      CP::unpack_col0(b.COL0, r, x0, xn);
       d[r * Wh] = x0;
       d[r * Wh + M] = xn;
     }
 }
 
-// Inverse of a global NSL spectrum (gen) into this CTA's rows; returns the
-// buffer with the spatial pairs (times D).
+// Inverse of a global NSL spectrum (gen) into this CTA's rows; the spatial
+// pairs (times D) end in Z.
 template <class CP, class GEN>
-__device__ __forceinline__ typename CP::C* cl_inverse(typename CP::C* B0, typename CP::C* B1,
-                                                      const typename CP::C* TW, unsigned rank, GEN&& gen) {
-  using C = typename CP::C;
-  C* cs = CP::cols_inv(B0, B1, TW, rank, gen);
-  C* ob = (cs == B0) ? B1 : B0;
-  cluster_sync_all();
-  CP::rows_inv_first(cs, ob, TW, rank);
+__device__ __forceinline__ void cl_inverse(ClBufs<CP>& b, unsigned rank, GEN&& gen) {
+  CP::cols_inv(b.X, b.Y, b.TW, rank, gen);
+  cl_exchange_sync<CP>(b.Y, b.Z, rank, b.bar, b.phase);
+  CP::rows_inv_first(b.Z, b.X, b.TW);
   __syncthreads();
-  cluster_sync_all();
-  return CP::rows_inv_rest(ob, cs, TW);
+  CP::rows_inv_rest(b.X, b.Z, b.TW);
 }
 
 template <class CP, class SRC>
@@ -327,28 +399,25 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
                   size_t dst_stride, const cx<typename CP::R>* tw, int* live_flags, int live_mod) {
   using R = typename CP::R;
   using C = typename CP::C;
-  using SM = SmemCl<CP>;
   constexpr int W = CP::W, Wh = CP::Wh, T = CP::T, M = CP::M, ROWS = CP::ROWS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* B0 = reinterpret_cast<C*>(smem_raw);
-  C* B1 = B0 + CP::BUF;
-  C* TW = reinterpret_cast<C*>(smem_raw + SM::tw_off);
-  C* COL0 = reinterpret_cast<C*>(smem_raw + SM::col0_off);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar_s;
+  ClBufs<CP> b(smem_raw, &bar_s);
   const unsigned rank = cluster_rank();
   const int p = blockIdx.x / CP::CL, r0 = rank * ROWS;
-  CP::load_twiddles(TW, tw);
+  CP::load_twiddles(b.TW, tw);
+  cl_init_exchange<CP>(b.bar);
   const SRC* s = src + (size_t)p * src_stride;
   int any = 0;
   for (int it = threadIdx.x; it < ROWS * M; it += T) {
     const int rl = it / M, m = it % M;
     const R v0 = R(s[(r0 + rl) * W + 2 * m]), v1 = R(s[(r0 + rl) * W + 2 * m + 1]);
     any |= (v0 != R(0)) | (v1 != R(0));
-    B0[rl * Wh + m] = mk<C>(v0, v1);
+    b.Z[rl * Wh + m] = mk<C>(v0, v1);
   }
   any = __syncthreads_or(any);
   if (live_flags && threadIdx.x == 0 && any) atomicOr(live_flags + (p % live_mod), 1);
-  cl_forward_to_global<CP>(B0, B1, TW, COL0, rank, dst + (size_t)p * dst_stride);
-  cluster_sync_all();
+  cl_forward_to_global<CP>(b, rank, dst + (size_t)p * dst_stride);
 }
 
 template <class CP>
@@ -357,27 +426,24 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
                    const cx<typename CP::R>* tw) {
   using R = typename CP::R;
   using C = typename CP::C;
-  using SM = SmemCl<CP>;
   constexpr int Wh = CP::Wh, T = CP::T, M = CP::M, ROWS = CP::ROWS, NB = CP::NB;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* B0 = reinterpret_cast<C*>(smem_raw);
-  C* B1 = B0 + CP::BUF;
-  C* TW = reinterpret_cast<C*>(smem_raw + SM::tw_off);
-  C* COL0 = reinterpret_cast<C*>(smem_raw + SM::col0_off);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar_s;
+  ClBufs<CP> b(smem_raw, &bar_s);
   const unsigned rank = cluster_rank();
   const int k = blockIdx.x / CP::CL, r0 = rank * ROWS;
-  CP::load_twiddles(TW, tw);
+  CP::load_twiddles(b.TW, tw);
+  cl_init_exchange<CP>(b.bar);
   const double* f = d + (size_t)k * mh * mw;
   for (int it = threadIdx.x; it < ROWS * M; it += T) {
     const int rl = it / M, m = it % M, r = r0 + rl;
     const int c0 = 2 * m, c1 = c0 + 1;
     const R v0 = (r < mh && c0 < mw) ? R(f[r * mw + c0]) : R(0);
     const R v1 = (r < mh && c1 < mw) ? R(f[r * mw + c1]) : R(0);
-    B0[rl * Wh + m] = mk<C>(v0, v1);
+    b.Z[rl * Wh + m] = mk<C>(v0, v1);
   }
   __syncthreads();
-  cl_forward_to_global<CP>(B0, B1, TW, COL0, rank, dst + (size_t)k * NB);
-  cluster_sync_all();
+  cl_forward_to_global<CP>(b, rank, dst + (size_t)k * NB);
 }
 
 template <class CP, class DST>
@@ -386,27 +452,24 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
                   size_t dst_stride, const cx<typename CP::R>* tw, const double* scale) {
   using R = typename CP::R;
   using C = typename CP::C;
-  using SM = SmemCl<CP>;
   constexpr int W = CP::W, Wh = CP::Wh, T = CP::T, M = CP::M, ROWS = CP::ROWS, D = CP::D;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* B0 = reinterpret_cast<C*>(smem_raw);
-  C* B1 = B0 + CP::BUF;
-  C* TW = reinterpret_cast<C*>(smem_raw + SM::tw_off);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar_s;
+  ClBufs<CP> b(smem_raw, &bar_s);
   const unsigned rank = cluster_rank();
   const int p = blockIdx.x / CP::CL, r0 = rank * ROWS;
-  CP::load_twiddles(TW, tw);
-  __syncthreads();
+  CP::load_twiddles(b.TW, tw);
+  cl_init_exchange<CP>(b.bar);
   const C* s = src + (size_t)p * src_stride;
-  C* sp = cl_inverse<CP>(B0, B1, TW, rank, [&](int r, int c) { return s[r * Wh + c]; });
+  cl_inverse<CP>(b, rank, [&](int r, int c) { return s[r * Wh + c]; });
   const R sc = R((scale ? scale[p] : 1.0) / (double)D);
   DST* o = dst + (size_t)p * dst_stride;
   for (int it = threadIdx.x; it < ROWS * M; it += T) {
     const int rl = it / M, m = it % M;
-    const C v = sp[rl * Wh + m];
+    const C v = b.Z[rl * Wh + m];
     o[(r0 + rl) * W + 2 * m] = DST(v.x * sc);
     o[(r0 + rl) * W + 2 * m + 1] = DST(v.y * sc);
   }
-  cluster_sync_all();
 }
 
 template <class CP>
@@ -416,14 +479,10 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
                  const cx<typename CP::R>* tw, const int* done) {
   using R = typename CP::R;
   using C = typename CP::C;
-  using SM = SmemCl<CP>;
   constexpr int Wh = CP::Wh, T = CP::T, M = CP::M, ROWS = CP::ROWS, D = CP::D, NB = CP::NB;
   if (done && *done) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* B0 = reinterpret_cast<C*>(smem_raw);
-  C* B1 = B0 + CP::BUF;
-  C* TW = reinterpret_cast<C*>(smem_raw + SM::tw_off);
-  C* COL0 = reinterpret_cast<C*>(smem_raw + SM::col0_off);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar_s;
   const unsigned rank = cluster_rank();
   const int k = blockIdx.x / CP::CL, r0 = rank * ROWS;
   if (!live[k]) {
@@ -434,36 +493,34 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     }
     return;
   }
-  CP::load_twiddles(TW, tw);
-  __syncthreads();
+  ClBufs<CP> b(smem_raw, &bar_s);
+  CP::load_twiddles(b.TW, tw);
+  cl_init_exchange<CP>(b.bar);
   const C* s = c + (size_t)k * NB;
-  C* sp = cl_inverse<CP>(B0, B1, TW, rank, [&](int r, int cc) { return s[r * Wh + cc]; });
+  cl_inverse<CP>(b, rank, [&](int r, int cc) { return s[r * Wh + cc]; });
   const R invD = R(1) / R(D);
   if (mode == 1) {
     if (rank == 0) {  // the support rows (mh <= ROWS) live in rank 0
       const double scale = -0.5 / fmax(mu[k], 1e-300);
       for (int i = threadIdx.x; i < mh * mw; i += T) {
         const int r = i / mw, cc = i % mw;
-        const C v = sp[r * Wh + cc / 2];
+        const C v = b.Z[r * Wh + cc / 2];
         const R val = ((cc & 1) ? v.y : v.x) * invD;
         d_out[(size_t)k * mh * mw + i] = scale * (double)val;
       }
     }
-    cluster_sync_all();
     return;
   }
   for (int it = threadIdx.x; it < ROWS * M; it += T) {
     const int rl = it / M, m = it % M;
-    const C v = sp[rl * Wh + m];
+    const C v = b.Z[rl * Wh + m];
     const bool rin = r0 + rl < mh;
     const R v0 = (rin && 2 * m < mw) ? v.x * invD : R(0);
     const R v1 = (rin && 2 * m + 1 < mw) ? v.y * invD : R(0);
-    sp[rl * Wh + m] = mk<C>(v0, v1);
+    b.Z[rl * Wh + m] = mk<C>(v0, v1);
   }
   __syncthreads();
-  C* other = (sp == B0) ? B1 : B0;
-  cl_forward_to_global<CP>(sp, other, TW, COL0, rank, phat + (size_t)k * NB);
-  cluster_sync_all();
+  cl_forward_to_global<CP>(b, rank, phat + (size_t)k * NB);
 }
 
 }  // namespace dcsc_cuda
