@@ -94,6 +94,13 @@ struct ClusterPlane {
     owner_of(k, c, cl);
     return (int)c * BLOCK + rl * CS + cl;
   }
+  // element (rl, k) of the staged blocks; block `rank` stays in `self`
+  __device__ static __forceinline__ C staged(const C* stg, const C* self, unsigned rank, int rl, int k) {
+    unsigned c;
+    int cl;
+    owner_of(k, c, cl);
+    return (c == rank ? self : stg)[(int)c * BLOCK + rl * CS + cl];
+  }
 
   // ---- inverse: column pass (local columns), input generated from global ----
   // gen(r, col) returns natural bin (r, col), col in [0, M]. Returns the
@@ -124,7 +131,10 @@ struct ClusterPlane {
   // `stg` [CL][ROWS][CS] with the c2r pre-processing fused; writes `out`
   // [ROWS][Wh]. Butterflies go in mirror pairs (j, J-j) — and (0, J/2), both
   // self-mirrored — so every staged element is loaded once.
-  __device__ static __forceinline__ void rows_inv_first(const C* stg, C* out, const C* tw) {
+  // The block of this rank itself is read from its own send buffer `self`
+  // (it is not copied).
+  __device__ static __forceinline__ void rows_inv_first(const C* stg, const C* self, unsigned rank, C* out,
+                                                        const C* tw) {
     using S = Split<RowPlanI>;
     constexpr int R = S::first, J = M / R, TASKS = ROWS * (J / 2);
     static_assert(J % 2 == 0, "paired butterflies");
@@ -135,8 +145,8 @@ struct ClusterPlane {
       C a[R], b[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        a[q] = stg[stage_off(rl, ja + J * q)];
-        b[q] = stg[stage_off(rl, jb + J * q)];
+        a[q] = staged(stg, self, rank, rl, ja + J * q);
+        b[q] = staged(stg, self, rank, rl, jb + J * q);
       }
       C xa[R], xb[R];
 #pragma unroll
@@ -189,7 +199,9 @@ struct ClusterPlane {
   // post-processing fused. The two columns of a mirror pair are produced
   // together from one load of Z[c] and Z[M-c]: X[c] = E + w O,
   // X[M-c] = conj(E - w O). Writes `out` [H][CS].
-  __device__ static __forceinline__ void cols_fwd_first(const C* zc, C* out, const C* tw, unsigned rank) {
+  // Rows of this rank itself are read from its own send buffer `self`.
+  __device__ static __forceinline__ void cols_fwd_first(const C* zc, const C* self, C* out, const C* tw,
+                                                        unsigned rank) {
     using S = Split<ColPlan>;
     constexpr int R = S::first, J = H / R, TASKS = HP * J;
 #pragma unroll 1
@@ -203,8 +215,9 @@ struct ClusterPlane {
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int r = j + q * J;
-        z1[q] = zc[r * CS + cla];
-        z2[q] = zc[r * CS + clb];
+        const C* base = (r / ROWS == (int)rank) ? self : zc;
+        z1[q] = base[r * CS + cla];
+        z2[q] = base[r * CS + clb];
       }
       C xa[R], xb[R];
       if (special) {

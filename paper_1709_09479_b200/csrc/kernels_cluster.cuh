@@ -50,14 +50,14 @@ __device__ __forceinline__ void bulk_s2peer(void* dst, unsigned peer, const void
                : "memory");
 }
 
-// Block q of snd -> slot `rank` of peer q's stg (one bulk copy per peer,
-// itself included). The caller has made snd visible to the async proxy
+// Block q of snd -> slot `rank` of peer q's stg (one bulk copy per peer; the
+// rank's own block is not copied, consumers read it from snd). The caller has made snd visible to the async proxy
 // (fence_async_smem + __syncthreads) and knows every peer's stg is free.
 template <class CP>
 __device__ __forceinline__ void cl_issue_exchange(const typename CP::C* snd, typename CP::C* stg, unsigned rank,
                                                   unsigned long long* bar) {
-  if (threadIdx.x == 0) mbar_expect_tx(bar, CP::CL * CP::block_bytes);
-  if (threadIdx.x < CP::CL) {
+  if (threadIdx.x == 0) mbar_expect_tx(bar, (CP::CL - 1) * CP::block_bytes);
+  if (threadIdx.x < CP::CL && threadIdx.x != rank) {
     const unsigned q = threadIdx.x;
     bulk_s2peer(stg + rank * CP::BLOCK, q, snd + q * CP::BLOCK, CP::block_bytes, bar);
   }
@@ -156,7 +156,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       cl_issue_exchange<CP>(Y, Z, rank, xbar);
       mbar_wait(xbar, xphase);
       xphase ^= 1u;
-      CP::rows_inv_first(Z, X, TW);
+      CP::rows_inv_first(Z, Y, rank, X, TW);
       __syncthreads();
       cluster_arrive();  // B_I: my Z consumed, my incoming blocks complete
       CP::rows_inv_rest(X, Z, TW);
@@ -228,7 +228,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     cl_issue_exchange<CP>(Z, Y, rank, xbar);
     mbar_wait(xbar, xphase);
     xphase ^= 1u;
-    CP::cols_fwd_first(Y, X, TW, rank);
+    CP::cols_fwd_first(Y, Z, X, TW, rank);
     __syncthreads();
     cluster_arrive();  // B_F: my Y consumed, my incoming blocks complete
     {
@@ -369,7 +369,7 @@ __device__ __forceinline__ void cl_forward_to_global(ClBufs<CP>& b, unsigned ran
   constexpr int Wh = CP::Wh, M = CP::M, H = CP::H, T = CP::T;
   CP::rows_fwd_to_send(b.Z, b.X, b.Z, b.TW);
   cl_exchange_sync<CP>(b.Z, b.Y, rank, b.bar, b.phase);
-  CP::cols_fwd_first(b.Y, b.X, b.TW, rank);
+  CP::cols_fwd_first(b.Y, b.Z, b.X, b.TW, rank);
   __syncthreads();
   CP::cols_fwd_rest(b.X, b.Y, b.TW, rank, b.COL0, [](int, int) { return 0; },
                     [&](int r, int c, C v, int) { d[r * Wh + c] = v; });
@@ -388,7 +388,7 @@ template <class CP, class GEN>
 __device__ __forceinline__ void cl_inverse(ClBufs<CP>& b, unsigned rank, GEN&& gen) {
   CP::cols_inv(b.X, b.Y, b.TW, rank, gen);
   cl_exchange_sync<CP>(b.Y, b.Z, rank, b.bar, b.phase);
-  CP::rows_inv_first(b.Z, b.X, b.TW);
+  CP::rows_inv_first(b.Z, b.Y, rank, b.X, b.TW);
   __syncthreads();
   CP::rows_inv_rest(b.X, b.Z, b.TW);
 }
