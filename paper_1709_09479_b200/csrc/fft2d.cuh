@@ -395,13 +395,17 @@ struct Plane {
     c = it % M;
     r = it / M + s * LAST_NS;
   }
+  // `hook(free)` runs at the start of the last stage with the buffer that
+  // stage does not read (the coding pass stages its next filter there).
+  template <class HOOK>
   __device__ static __forceinline__ void cols_fwd_acc(C* z, C* b, const C* tw, C* col0, const C* __restrict__ dk,
-                                                      C (&acc)[LAST_IPT][LAST_R]) {
+                                                      C (&acc)[LAST_IPT][LAST_R], HOOK&& hook) {
     using S = Split<ColPlan>;
     constexpr int NST = CountStages<ColPlan>::value;
     constexpr int R = LAST_R, NS = LAST_NS, J = H / R;
     const C* twc = tw + TW_COL;
-    auto last = [&](auto&& load) {
+    auto last = [&](auto&& load, C* freebuf) {
+      hook(freebuf);
 #pragma unroll
       for (int i = 0; i < LAST_IPT; ++i) {
         const int it = threadIdx.x + i * T;
@@ -429,14 +433,14 @@ struct Plane {
     };
     auto post_load = [&](int col, int r) { return post(z, tw, r, col); };
     if constexpr (NST == 1) {
-      last(post_load);
+      last(post_load, b);
     } else {
       constexpr int R1 = S::first;
       stockham<C, H, R1, 1, false, M, T>(twc, post_load, [&](int l, int i, C v) { b[i * Wh + l] = v; });
       __syncthreads();
       using Mid = typename Split<typename S::tail>::init;
       C* in = run_stages<C, H, false, M, Wh, 1, T, R1>(b, z, twc, Mid{});
-      last([&](int l, int i) { return in[i * Wh + l]; });
+      last([&](int l, int i) { return in[i * Wh + l]; }, in == b ? z : b);
     }
   }
 

@@ -147,9 +147,22 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
 
   constexpr bool LAMS = (MODE == kPassAdmm) && Smem<P>::lam_smem;
   C* LAM = reinterpret_cast<C*>(smem_raw + Smem<P>::u_off);
+  // With lambda_hat in smem, the t_hat stage's only global operand is d_hat:
+  // each filter's d_hat plane is staged into the free plane buffer by one TMA
+  // bulk copy issued at the start of the previous filter's last forward column
+  // stage (which reads only the other buffer), so its L2 latency overlaps
+  // that stage. The column-0 epilogue's d_hat(r, 0), d_hat(r, W/2) are
+  // fetched into registers at the same point (d0, dM).
+  constexpr bool PREF = LAMS;
+  __shared__ __align__(8) unsigned long long dbar_s;
+  unsigned long long* dbar = &dbar_s;
+  unsigned dphase = 0;
+  C* stg = B1;  // buffer holding the staged d_hat of the current filter
+  C d0 = mk<C>(R(0), R(0)), dMv = mk<C>(R(0), R(0));
   P::load_twiddles(TW, a.tw);
   if ((STAGE || LAMS) && threadIdx.x == 0) {
     mbar_init(ubar, 1);
+    if (PREF) mbar_init(dbar, 1);
     fence_async_smem();
   }
   __syncthreads();
@@ -157,6 +170,10 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     if (threadIdx.x == 0) {
       mbar_expect_tx(ubar, (unsigned)(sizeof(C) * NB));
       bulk_g2s(LAM, a.lamhat + (size_t)n * NB, (unsigned)(sizeof(C) * NB), ubar);
+      if (PREF && g * a.kpg < a.K) {
+        mbar_expect_tx(dbar, (unsigned)(sizeof(C) * NB));
+        bulk_g2s(stg, a.dhat + (size_t)g * a.kpg * NB, (unsigned)(sizeof(C) * NB), dbar);
+      }
     }
     mbar_wait(ubar, 0);
   }
@@ -189,10 +206,21 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
         prefetch_l2_bulk(uk, sizeof(R) * D);
       }
       if (threadIdx.x == 0 && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
-      C* cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
-        const int b = r * Wh + c;
-        return cmulc(__ldg(dk + b), LAMS ? LAM[b] : __ldg(lam + b));
-      });
+      C* cs;
+      if constexpr (PREF) {
+        mbar_wait(dbar, dphase);
+        dphase ^= 1u;
+        const C* sd = stg;
+        cs = P::cols_inv(stg == B0 ? B1 : B0, stg, TW, [&](int r, int c) {
+          const int b = r * Wh + c;
+          return cmulc(sd[b], LAM[b]);
+        });
+      } else {
+        cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
+          const int b = r * Wh + c;
+          return cmulc(__ldg(dk + b), LAMS ? LAM[b] : __ldg(lam + b));
+        });
+      }
       C* hin = P::rows_inv_head(cs, cs == B0 ? B1 : B0, TW);
       C* fout = (hin == B0) ? B1 : B0;
       // fused: last inverse row stage -> prox on u -> first forward row stage,
@@ -258,13 +286,31 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
         }
       }
       C* z = P::rows_fwd_tail(fout, hin, TW);
-      P::cols_fwd_acc(z, z == B0 ? B1 : B0, TW, COL0, dk, acc);
+      P::cols_fwd_acc(z, z == B0 ? B1 : B0, TW, COL0, dk, acc, [&](C* freebuf) {
+        if constexpr (PREF) {
+          if (threadIdx.x < H) {
+            d0 = __ldg(dk + threadIdx.x * Wh);
+            dMv = __ldg(dk + threadIdx.x * Wh + M);
+          }
+          stg = freebuf;
+          if (threadIdx.x == 0 && k + 1 < k1) {
+            fence_async_smem();
+            mbar_expect_tx(dbar, (unsigned)(sizeof(C) * NB));
+            bulk_g2s(freebuf, dk + NB, (unsigned)(sizeof(C) * NB), dbar);
+          }
+        }
+      });
       if (threadIdx.x < H) {
         const int r = threadIdx.x;
         C x0, xn;
         P::template unpack_col0<1>(COL0, r, x0, xn);
-        acc0 = cadd(acc0, cmul(__ldg(dk + r * Wh), x0));
-        accN = cadd(accN, cmul(__ldg(dk + r * Wh + M), xn));
+        if constexpr (PREF) {
+          acc0 = cadd(acc0, cmul(d0, x0));
+          accN = cadd(accN, cmul(dMv, xn));
+        } else {
+          acc0 = cadd(acc0, cmul(__ldg(dk + r * Wh), x0));
+          accN = cadd(accN, cmul(__ldg(dk + r * Wh + M), xn));
+        }
       }
       continue;
     } else {
@@ -295,7 +341,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     // forward r2c of w with acc += d_hat_k w_hat_k fused into the last column stage
     C* other = (work == B0) ? B1 : B0;
     C* z = P::rows_fwd(work, other, TW);
-    P::cols_fwd_acc(z, z == work ? other : work, TW, COL0, dk, acc);
+    P::cols_fwd_acc(z, z == work ? other : work, TW, COL0, dk, acc, [](C*) {});
     static_assert(H <= T, "column-0 owners: one thread per row");
     if (threadIdx.x < H) {
       const int r = threadIdx.x;
