@@ -78,6 +78,60 @@ def solve_coding(x, d, beta, rho, max_admm, theta=None, z=None):
     return z, theta, lam, stats
 
 
+def solve_coding_tcsc(x, d, beta, rho, max_admm, theta=None, z=None):
+    """solve_coding_tcsc (tcsc.cpp:211-230): admm_coding (coding.cpp:166-329)
+    with the BlockKernel of tcsc.cpp:121-171 for a J-channel signal x (J,H,W)
+    and dictionary d (K,J,mh,mw). lambda_hat(w) solves the per-bin J x J
+    system (D D^H + I/rho) lambda_hat = sum_k d_hat_jk w_hat_k - x_hat/rho
+    (tcsc.cpp:31-88; Woodbury is the same solution); t_hat_k =
+    sum_j conj(d_hat_jk) lambda_hat_j (tcsc.cpp:90-102)."""
+    K, J = d.shape[:2]
+    grid = x.shape[1:]
+    dh = fwd(pad(d, grid))                              # (K, J, H, W), tcsc.cpp:195-209
+    Dw = np.moveaxis(dh, (0, 1), (-1, -2))              # (H, W, J, K): block(bin)
+    G = Dw @ np.conj(np.swapaxes(Dw, -1, -2)) + np.eye(J) / rho   # tcsc.cpp:44-47
+    xh = fwd(x)                                         # (J, H, W)
+    theta = np.zeros((K,) + grid) if theta is None else theta.copy()
+    z = np.zeros((K,) + grid) if z is None else z.copy()
+    stats = dict(admm_iters=0, converged=False, degenerate_dictionary=False, dual_rescaled=False)
+    if not np.any(d):                                   # coding.cpp:181-191
+        stats.update(converged=True, degenerate_dictionary=True)
+        lam = -x
+        stats["dual_objective"] = -0.5 * (lam * lam).sum() - (lam * x).sum()
+        return np.zeros_like(z), np.zeros_like(theta), lam, stats
+    th_h, z_h = fwd(theta), fwd(z)
+    inv_rho = 1.0 / rho
+    t_inf = 0.0
+    for it in range(1, max_admm + 1):
+        w_h = th_h + z_h * inv_rho
+        r = np.einsum("kjhw,khw->hwj", dh, w_h) - np.moveaxis(xh, 0, -1) * inv_rho   # tcsc.cpp:75-80
+        lam_h = np.moveaxis(np.linalg.solve(G, r[..., None])[..., 0], -1, 0)         # (J, H, W)
+        t = inv(np.einsum("kjhw,jhw->khw", np.conj(dh), lam_h))                     # tcsc.cpp:90-102
+        th_new = np.clip(t - z * inv_rho, -beta, beta)
+        dth = th_new - theta
+        dz = rho * (th_new - t)
+        theta = th_new
+        z = z + dz
+        tt = ((th_new - t) ** 2).sum(); th2 = (th_new ** 2).sum(); t2 = (t ** 2).sum()
+        dz2 = (dz ** 2).sum(); z2 = (z ** 2).sum(); dth2 = (dth ** 2).sum()
+        t_inf = np.abs(t).max()
+        th_h, z_h = fwd(theta), fwd(z)
+        primal = np.sqrt(tt) / max(np.sqrt(th2), np.sqrt(t2), 1.0)
+        zc = np.sqrt(dz2) / max(np.sqrt(z2), 1.0)
+        thc = np.sqrt(dth2) / max(np.sqrt(th2), 1.0)
+        stats.update(admm_iters=it, primal_residual=primal, z_change=zc, theta_change=thc)
+        if primal <= ADMM_REL_TOL and zc <= ADMM_REL_TOL and thc <= ADMM_REL_TOL:
+            stats["converged"] = True
+            break
+    lam = inv(lam_h)
+    stats["dual_infeasibility"] = max(0.0, t_inf - beta)
+    if t_inf > beta:
+        lam = lam * (beta / t_inf)
+        stats["dual_rescaled"] = True
+    stats["dual_objective"] = -0.5 * (lam * lam).sum() - (lam * x).sum()
+    return z, theta, lam, stats
+
+
 class LearningOperator:
     """LearningOperator (learning.cpp:24-134)."""
 

@@ -1,8 +1,10 @@
 """ctypes binding of oracle/_ref/libdcsc_ref.so (TEST INFRASTRUCTURE ONLY).
 
 The library is the UNMODIFIED reference solver (proj/src/{types,parallel,
-spectral,objective,coding,learning,pipeline}.cpp) built by oracle/Makefile
-against the FFTW3-API shim. Only tests/, __graft_entry__.smoke() and bench.py's
+spectral,objective,coding,learning,pipeline,tensor_io,trace_io,tcsc}.cpp) built
+by oracle/Makefile against the FFTW3-API shim and (tcsc.cpp) the Eigen-API shim.
+Multi-channel (J > 1) entry points take signals as (N, J, H, W), dictionaries
+as (K, J, mh, mw) and run the reference's TCSC path (Joint channel mode). Only tests/, __graft_entry__.smoke() and bench.py's
 cpu_baseline / --impl reference leg may import this module; it is the checker,
 never the thing measured as the product.
 """
@@ -258,3 +260,98 @@ def write_trace_csv(path, trace):
         for f, _ in RefTraceRow._fields_:
             setattr(rows[i], f, t.get(f, 0))
     _check(lib().ref_write_trace_csv(path.encode(), rows, len(trace)))
+
+
+# ---------------------------------------------------------------- J channels
+def init_dictionary_j(K: int, J: int, m: tuple[int, int], grid: tuple[int, int], seed: int) -> np.ndarray:
+    out = np.zeros((K, J, m[0], m[1]))
+    _check(lib().ref_init_dictionary_j(K, J, m[0], m[1], grid[0], grid[1], C.c_uint64(seed), _p(out)))
+    return out
+
+
+def solve_coding_tcsc(x, d, cfg: Cfg, state=None, method: int = 0):
+    """solve_coding_tcsc (proj/src/tcsc.cpp:211-230). x (J,H,W), d (K,J,mh,mw);
+    state = (theta K*D, z K*D, lambda J*D) or None. method 0 Auto, 1 Direct, 2 Woodbury."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    J, H, W = x.shape
+    K, Jd, mh, mw = d.shape
+    assert Jd == J
+    if state is None:
+        theta = np.zeros((K, H, W)); z = np.zeros((K, H, W)); lam = np.zeros((J, H, W)); warm = 0
+    else:
+        theta, z, lam = (np.array(a, dtype=np.float64, copy=True) for a in state); warm = 1
+    st = RefCodingStats()
+    c = cfg.c()
+    _check(lib().ref_solve_coding_tcsc(H, W, J, _p(x), K, mh, mw, _p(d), C.byref(c), warm,
+                                       _p(theta), _p(z), _p(lam), int(method), C.byref(st)))
+    stats = {f: getattr(st, f) for f, _ in RefCodingStats._fields_}
+    return z.copy(), (theta, z, lam), stats
+
+
+def solve_learning_j(xs, maps, support, cfg: Cfg, state=None):
+    """solve_learning / solve_learning_tcsc over J-channel images xs (N,J,H,W);
+    state = (gamma (J,N,H,W), mu K) or None. Returns d (K,J,mh,mw)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    N, J, H, W = xs.shape
+    K = maps.shape[1]
+    if state is None:
+        gamma = np.zeros((J, N, H, W)); mu = np.ones(K); warm = 0
+    else:
+        gamma = np.array(state[0], dtype=np.float64, copy=True).reshape(J, N, H, W)
+        mu = np.array(state[1], dtype=np.float64, copy=True); warm = 1
+    d = np.zeros((K, J, support[0], support[1]))
+    st = RefLearningStats()
+    c = cfg.c()
+    _check(lib().ref_solve_learning_j(N, H, W, J, _p(xs), K, _p(maps), support[0], support[1],
+                                      C.byref(c), warm, _p(gamma), _p(mu), _p(d), C.byref(st)))
+    stats = {f: getattr(st, f) for f, _ in RefLearningStats._fields_}
+    return d, (gamma, mu), stats
+
+
+def objective_j(x, d, z, beta):
+    """evaluate_objective of a J-channel image x (J,H,W) with d (K,J,mh,mw)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.zeros(4)
+    J, H, W = x.shape
+    K, _, mh, mw = d.shape
+    _check(lib().ref_objective_j(H, W, J, _p(x), K, mh, mw, _p(d), _p(z), C.c_double(beta), _p(out)))
+    return tuple(out)
+
+
+def run_j(xs, K, support, cfg: Cfg, dump_dicts=True):
+    """Instrumented run_csc replica on J-channel signals xs (N,J,H,W), Joint mode for J > 1."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    N, J, H, W = xs.shape
+    mh, mw = support
+    rows = (RefTraceRow * (2 * max(cfg.max_outer, 1)))()
+    n_outer = C.c_int(0)
+    dict_iter = np.zeros((cfg.max_outer + 1, K, J, mh, mw)) if dump_dicts else None
+    maps = np.zeros((N, K, H, W))
+    dfin = np.zeros((K, J, mh, mw))
+    c = cfg.c()
+    _check(lib().ref_run_j(C.byref(c), N, H, W, J, _p(xs), K, mh, mw, rows, C.byref(n_outer),
+                           _p(dict_iter) if dump_dicts else None, _p(maps), _p(dfin)))
+    trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(2 * n_outer.value)]
+    return {"trace": trace, "n_outer": n_outer.value,
+            "dicts": dict_iter[: n_outer.value + 1] if dump_dicts else None,
+            "maps": maps, "dict": dfin}
+
+
+def run_csc_j(xs, K, support, cfg: Cfg):
+    """The reference's own run_csc on J-channel signals (Joint mode for J > 1)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    N, J, H, W = xs.shape
+    mh, mw = support
+    rows = (RefTraceRow * (2 * max(cfg.max_outer, 1)))()
+    n_rows = C.c_int(0)
+    dfin = np.zeros((K, J, mh, mw))
+    maps = np.zeros((N, K, H, W))
+    c = cfg.c()
+    _check(lib().ref_run_csc_j(C.byref(c), N, H, W, J, _p(xs), K, mh, mw, rows, C.byref(n_rows),
+                               _p(dfin), _p(maps)))
+    trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(n_rows.value)]
+    return {"trace": trace, "dict": dfin, "maps": maps}

@@ -3,9 +3,12 @@
 // bench.py's cpu_baseline / --impl reference leg; never by the product).
 //
 // oracle/Makefile compiles /root/reference/proj/src/{types,parallel,spectral,
-// objective,coding,learning,pipeline}.cpp in place (no sources are copied)
-// against oracle/fftw3.h + oracle/fftw_shim.c, links this file and
-// oracle/tcsc_stub.cpp, and writes oracle/_ref/libdcsc_ref.so.
+// objective,coding,learning,pipeline,tensor_io,trace_io,tcsc}.cpp in place (no
+// sources are copied) against oracle/fftw3.h + oracle/fftw_shim.c and (tcsc.cpp)
+// the Eigen-API shim oracle/eigen_shim/, links this file, and writes
+// oracle/_ref/libdcsc_ref.so. The *_j entry points take J channels (signals
+// N x J x D, dictionary K x J x M, lambda J x D, gamma J x N x D); J > 1 runs
+// the reference's TCSC path (Joint channel mode, pipeline.cpp:168).
 //
 // ref_run() is an instrumented replica of dcsc::run_csc
 // (proj/src/pipeline.cpp:158-301) assembled ONLY from the reference's public
@@ -29,6 +32,7 @@
 #include "dcsc/parallel.hpp"
 #include "dcsc/pipeline.hpp"
 #include "dcsc/spectral.hpp"
+#include "dcsc/tcsc.hpp"
 #include "dcsc/tensor_io.hpp"
 #include "dcsc/trace_io.hpp"
 #include "dcsc/types.hpp"
@@ -117,16 +121,42 @@ double now_ms() {
   return std::chrono::duration<double, std::milli>(clock::now().time_since_epoch()).count();
 }
 
-Dictionary make_dict(int K, int mh, int mw, const double* d) {
-  Dictionary dict(K, {mh, mw}, 1);
+Dictionary make_dict(int K, int mh, int mw, const double* d, int J = 1) {
+  Dictionary dict(K, {mh, mw}, J);
   std::copy(d, d + dict.values.size(), dict.values.begin());
   return dict;
 }
 
-SignalTensor make_signal(int H, int W, const double* x) {
-  SignalTensor s({H, W}, 1);
+SignalTensor make_signal(int H, int W, const double* x, int J = 1) {
+  SignalTensor s({H, W}, J);
   std::copy(x, x + s.values.size(), s.values.begin());
   return s;
+}
+
+void put_coding_stats(const CodingStats& s, ref_coding_stats* st) {
+  if (!st) return;
+  st->admm_iters = s.admm_iters;
+  st->converged = s.converged;
+  st->degenerate_dictionary = s.degenerate_dictionary;
+  st->dual_rescaled = s.dual_rescaled;
+  st->primal_residual = s.primal_residual;
+  st->theta_change = s.theta_change;
+  st->z_change = s.z_change;
+  st->dual_objective = s.dual_objective;
+  st->dual_infeasibility = s.dual_infeasibility;
+}
+
+void put_learning_stats(const LearningStats& s, ref_learning_stats* st) {
+  if (!st) return;
+  st->mu_iters = s.mu_iters;
+  st->cg_iters = s.cg_iters;
+  st->cg_iters_first = s.cg_iters_first;
+  st->converged = s.converged;
+  st->degenerate = s.degenerate;
+  st->mu_clamped = s.mu_clamped;
+  st->cg_budget_hit = s.cg_budget_hit;
+  st->rescaled_filters = s.rescaled_filters;
+  st->n_dead = static_cast<int>(s.dead_filters.size());
 }
 
 long count_l0(const std::vector<SparseMaps>& maps) {
@@ -178,15 +208,20 @@ int ref_inverse_dft(int rank, const int* dims, const double* in, double* out) {
   });
 }
 
-int ref_init_dictionary(int K, int mh, int mw, int H, int W, std::uint64_t seed, double* out) {
+int ref_init_dictionary_j(int K, int J, int mh, int mw, int H, int W, std::uint64_t seed, double* out) {
   return guarded([&] {
     RunConfig rc;
     rc.solver.seed = seed;
     rc.filters = K;
     rc.support = {mh, mw};
-    InitVariables v = init_variables(rc, {H, W}, 1, 1);
+    rc.channel_mode = J > 1 ? ChannelMode::Joint : ChannelMode::Separate;
+    InitVariables v = init_variables(rc, {H, W}, J, 1);
     std::copy(v.dict.values.begin(), v.dict.values.end(), out);
   });
+}
+
+int ref_init_dictionary(int K, int mh, int mw, int H, int W, std::uint64_t seed, double* out) {
+  return ref_init_dictionary_j(K, 1, mh, mw, H, W, seed, out);
 }
 
 // One solve_coding call. theta/z/lambda are in/out warm state (K*D, K*D, D);
@@ -209,17 +244,34 @@ int ref_solve_coding(int H, int W, const double* x, int K, int mh, int mw, const
     std::copy(state.theta.begin(), state.theta.end(), theta);
     std::copy(state.z.begin(), state.z.end(), z);
     std::copy(state.lambda.begin(), state.lambda.end(), lambda);
-    if (st) {
-      st->admm_iters = s.admm_iters;
-      st->converged = s.converged;
-      st->degenerate_dictionary = s.degenerate_dictionary;
-      st->dual_rescaled = s.dual_rescaled;
-      st->primal_residual = s.primal_residual;
-      st->theta_change = s.theta_change;
-      st->z_change = s.z_change;
-      st->dual_objective = s.dual_objective;
-      st->dual_infeasibility = s.dual_infeasibility;
+    put_coding_stats(s, st);
+  });
+}
+
+// solve_coding_tcsc (tcsc.cpp) on a J-channel signal x (J*D); d is K*J*M;
+// lambda is J*D. method: 0 Auto, 1 Direct, 2 Woodbury.
+int ref_solve_coding_tcsc(int H, int W, int J, const double* x, int K, int mh, int mw, const double* d,
+                          const ref_cfg* cfg, int warm, double* theta, double* z, double* lambda,
+                          int method, ref_coding_stats* st) {
+  return guarded([&] {
+    const SignalTensor xs = make_signal(H, W, x, J);
+    const Dictionary dict = make_dict(K, mh, mw, d, J);
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    CodingDualState state;
+    if (warm) {
+      state.theta.assign(theta, theta + K * D);
+      state.z.assign(z, z + K * D);
+      state.lambda.assign(lambda, lambda + J * D);
     }
+    CodingStats s;
+    const BlockSolveMethod m = method == 1   ? BlockSolveMethod::Direct
+                               : method == 2 ? BlockSolveMethod::Woodbury
+                                             : BlockSolveMethod::Auto;
+    solve_coding_tcsc(xs, dict, to_cfg(cfg), state, &s, m);
+    std::copy(state.theta.begin(), state.theta.end(), theta);
+    std::copy(state.z.begin(), state.z.end(), z);
+    std::copy(state.lambda.begin(), state.lambda.end(), lambda);
+    put_coding_stats(s, st);
   });
 }
 
@@ -245,58 +297,64 @@ int ref_coding_batch(int N, int H, int W, const double* xs, int K, int mh, int m
   });
 }
 
-// One solve_learning call over N images. gamma (N*D) / mu (K) are in/out warm
-// state; warm = 0 starts from the empty state. d_out receives K*M values.
-int ref_solve_learning(int N, int H, int W, const double* xs, int K, const double* maps, int mh,
-                       int mw, const ref_cfg* cfg, int warm, double* gamma, double* mu,
-                       double* d_out, ref_learning_stats* st) {
+// One solve_learning call over N J-channel images (xs N*J*D). gamma (J*N*D,
+// channel-major) / mu (K) are in/out warm state; warm = 0 starts from the
+// empty state. d_out receives K*J*M values.
+int ref_solve_learning_j(int N, int H, int W, int J, const double* xs, int K, const double* maps, int mh,
+                         int mw, const ref_cfg* cfg, int warm, double* gamma, double* mu, double* d_out,
+                         ref_learning_stats* st) {
   return guarded([&] {
     const std::size_t D = static_cast<std::size_t>(H) * W;
     std::vector<SignalTensor> sig;
     std::vector<SparseMaps> zs;
     for (int n = 0; n < N; ++n) {
-      sig.push_back(make_signal(H, W, xs + n * D));
+      sig.push_back(make_signal(H, W, xs + n * J * D, J));
       SparseMaps m(K, {H, W});
       std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
       zs.push_back(std::move(m));
     }
     LearningDualState state;
     if (warm) {
-      state.gamma.assign(1, std::vector<double>(gamma, gamma + N * D));
+      state.gamma.clear();
+      for (int j = 0; j < J; ++j)
+        state.gamma.emplace_back(gamma + j * N * D, gamma + (j + 1) * N * D);
       state.mu.assign(mu, mu + K);
     }
     LearningStats s;
-    Dictionary dict = solve_learning(sig, zs, {mh, mw}, to_cfg(cfg), state, &s);
+    Dictionary dict = J > 1 ? solve_learning_tcsc(sig, zs, {mh, mw}, to_cfg(cfg), state, &s)
+                            : solve_learning(sig, zs, {mh, mw}, to_cfg(cfg), state, &s);
     std::copy(dict.values.begin(), dict.values.end(), d_out);
-    if (!state.gamma.empty()) std::copy(state.gamma[0].begin(), state.gamma[0].end(), gamma);
+    for (int j = 0; j < (int)state.gamma.size() && j < J; ++j)
+      std::copy(state.gamma[j].begin(), state.gamma[j].end(), gamma + j * N * D);
     std::copy(state.mu.begin(), state.mu.end(), mu);
-    if (st) {
-      st->mu_iters = s.mu_iters;
-      st->cg_iters = s.cg_iters;
-      st->cg_iters_first = s.cg_iters_first;
-      st->converged = s.converged;
-      st->degenerate = s.degenerate;
-      st->mu_clamped = s.mu_clamped;
-      st->cg_budget_hit = s.cg_budget_hit;
-      st->rescaled_filters = s.rescaled_filters;
-      st->n_dead = static_cast<int>(s.dead_filters.size());
-    }
+    put_learning_stats(s, st);
   });
 }
 
-// evaluate_objective for one image: out = {data_term, l1_term, total, residual_norm}
-int ref_objective(int H, int W, const double* x, int K, int mh, int mw, const double* d,
-                  const double* z, double beta, double* out) {
+int ref_solve_learning(int N, int H, int W, const double* xs, int K, const double* maps, int mh,
+                       int mw, const ref_cfg* cfg, int warm, double* gamma, double* mu,
+                       double* d_out, ref_learning_stats* st) {
+  return ref_solve_learning_j(N, H, W, 1, xs, K, maps, mh, mw, cfg, warm, gamma, mu, d_out, st);
+}
+
+// evaluate_objective for one J-channel image: out = {data_term, l1_term, total, residual_norm}
+int ref_objective_j(int H, int W, int J, const double* x, int K, int mh, int mw, const double* d,
+                    const double* z, double beta, double* out) {
   return guarded([&] {
     SparseMaps m(K, {H, W});
     std::copy(z, z + m.values.size(), m.values.begin());
     const ObjectiveBreakdown b =
-        evaluate_objective(make_signal(H, W, x), make_dict(K, mh, mw, d), m, beta);
+        evaluate_objective(make_signal(H, W, x, J), make_dict(K, mh, mw, d, J), m, beta);
     out[0] = b.data_term;
     out[1] = b.l1_term;
     out[2] = b.total;
     out[3] = b.residual_norm;
   });
+}
+
+int ref_objective(int H, int W, const double* x, int K, int mh, int mw, const double* d,
+                  const double* z, double beta, double* out) {
+  return ref_objective_j(H, W, 1, x, K, mh, mw, d, z, beta, out);
 }
 
 // LearningOperator::apply (proj/src/learning.cpp:83-122) on stacked N*D vectors.
@@ -322,21 +380,25 @@ int ref_learning_apply(int N, int H, int W, int K, const double* maps, int mh, i
 // the initial dictionary then the accepted dictionary after each outer
 // iteration. maps_out (optional) receives the final N*K*D maps, dict_out the
 // final K*M dictionary. Returns the number of outer iterations run in *n_outer.
-int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
-            int mw, ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out,
-            double* dict_out) {
+// J > 1: Joint channel mode (solve_coding_tcsc), signals N*J*D, dictionary K*J*M.
+int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_raw, int K, int mh,
+              int mw, ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out,
+              double* dict_out) {
   return guarded([&] {
     RunConfig cfg;
     cfg.solver = to_cfg(cfgp);
     cfg.filters = K;
     cfg.support = {mh, mw};
+    cfg.channel_mode = J > 1 ? ChannelMode::Joint : ChannelMode::Separate;
+    const bool tcsc = J > 1;
     const std::size_t D = static_cast<std::size_t>(H) * W;
     const double beta = cfg.solver.beta;
     const double tau = cfg.solver.tol;
     std::vector<SignalTensor> xs(N);
-    for (int n = 0; n < N; ++n) xs[n] = normalize(make_signal(H, W, xs_raw + n * D), cfg.solver.normalize);
+    for (int n = 0; n < N; ++n)
+      xs[n] = normalize(make_signal(H, W, xs_raw + n * J * D, J), cfg.solver.normalize);
 
-    InitVariables vars = init_variables(cfg, {H, W}, 1, N);
+    InitVariables vars = init_variables(cfg, {H, W}, J, N);
     Dictionary dict = vars.dict;
     std::vector<SparseMaps> maps = vars.maps;
     const std::size_t KM = dict.values.size();
@@ -366,7 +428,8 @@ int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int 
       std::vector<CodingStats> cs(N);
       const double c0 = now_ms();
       par::parallel_for(N, [&](std::int64_t n) {
-        cand[n] = solve_coding(xs[n], dict, cfg.solver, vars.coding[n], &cs[n]);
+        cand[n] = tcsc ? solve_coding_tcsc(xs[n], dict, cfg.solver, vars.coding[n], &cs[n])
+                       : solve_coding(xs[n], dict, cfg.solver, vars.coding[n], &cs[n]);
       });
       const double coding_ms = now_ms() - c0;
       long admm_total = 0;
@@ -400,7 +463,8 @@ int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int 
 
       LearningStats ls;
       const double l0 = now_ms();
-      Dictionary dc = solve_learning(xs, maps, cfg.support, cfg.solver, vars.learning, &ls);
+      Dictionary dc = tcsc ? solve_learning_tcsc(xs, maps, cfg.support, cfg.solver, vars.learning, &ls)
+                           : solve_learning(xs, maps, cfg.support, cfg.solver, vars.learning, &ls);
       const double learning_ms = now_ms() - l0;
       double d_change_sq = 0.0, d_norm_sq = 0.0;
       ObjectiveBreakdown after_learning = after_coding;
@@ -437,6 +501,12 @@ int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int 
       for (int n = 0; n < N; ++n) std::copy(maps[n].values.begin(), maps[n].values.end(), maps_out + n * K * D);
     if (dict_out) std::copy(dict.values.begin(), dict.values.end(), dict_out);
   });
+}
+
+int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
+            int mw, ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out,
+            double* dict_out) {
+  return ref_run_j(cfgp, N, H, W, 1, xs_raw, K, mh, mw, rows, n_outer, dict_iter, maps_out, dict_out);
 }
 
 // The reference's CSCT writer/reader (tensor_io.cpp:45-90) and trace CSV
@@ -480,16 +550,17 @@ int ref_write_trace_csv(const char* path, const ref_trace_row* rows, int n) {
 }
 
 // The reference's own run_csc, for checking the replica (trace rows only).
-int ref_run_csc(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
-                int mw, ref_trace_row* rows, int* n_rows, double* dict_out, double* maps_out) {
+int ref_run_csc_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_raw, int K, int mh,
+                  int mw, ref_trace_row* rows, int* n_rows, double* dict_out, double* maps_out) {
   return guarded([&] {
     RunConfig cfg;
     cfg.solver = to_cfg(cfgp);
     cfg.filters = K;
     cfg.support = {mh, mw};
+    cfg.channel_mode = J > 1 ? ChannelMode::Joint : ChannelMode::Separate;
     const std::size_t D = static_cast<std::size_t>(H) * W;
     Dataset data;
-    for (int n = 0; n < N; ++n) data.signals.push_back(make_signal(H, W, xs_raw + n * D));
+    for (int n = 0; n < N; ++n) data.signals.push_back(make_signal(H, W, xs_raw + n * J * D, J));
     RunResult r = run_csc(cfg, data);
     *n_rows = static_cast<int>(r.trace.rows.size());
     for (std::size_t i = 0; i < r.trace.rows.size(); ++i) {
@@ -502,6 +573,11 @@ int ref_run_csc(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, 
     if (maps_out)
       for (int n = 0; n < N; ++n) std::copy(r.maps[n].values.begin(), r.maps[n].values.end(), maps_out + n * K * D);
   });
+}
+
+int ref_run_csc(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
+                int mw, ref_trace_row* rows, int* n_rows, double* dict_out, double* maps_out) {
+  return ref_run_csc_j(cfgp, N, H, W, 1, xs_raw, K, mh, mw, rows, n_rows, dict_out, maps_out);
 }
 
 }  // extern "C"
