@@ -18,10 +18,13 @@
  *   dcsc_cuda_set/get_coding_state  dcsc::CodingDualState (coding.hpp:15-25)
  *   dcsc_cuda_coding                dcsc::solve_coding (coding.hpp:74-77),
  *                                   batched over images: replaces the OpenMP
- *                                   loop at pipeline.cpp:221-227
+ *                                   loop at pipeline.cpp:221-227; with
+ *                                   channels > 1 dcsc::solve_coding_tcsc
+ *                                   (tcsc.hpp:53-60, pipeline.cpp:222-224)
  *   dcsc_cuda_set/get_maps          dcsc::SparseMaps (types.hpp:81-94)
  *   dcsc_cuda_set/get_learning_state dcsc::LearningDualState (learning.hpp:15-23)
- *   dcsc_cuda_learning              dcsc::solve_learning (learning.hpp:99-104)
+ *   dcsc_cuda_learning              dcsc::solve_learning (learning.hpp:99-104);
+ *                                   channels > 1: solve_learning_tcsc (tcsc.hpp:62-68)
  *   dcsc_cuda_objective             dcsc::evaluate_objective (objective.hpp:14-15)
  *   dcsc_cuda_learning_data_term    dcsc::learning_data_term (objective.hpp:18-19)
  *   dcsc_cuda_learning_apply        dcsc::LearningOperator::apply (learning.hpp:57)
@@ -69,6 +72,10 @@ typedef struct {
   int precision;           /* 32 or 64: storage/FFT precision; reductions are FP64 */
   int device;              /* CUDA device ordinal */
   dcsc_solver_config cfg;
+  int channels;            /* J (0 or 1 = single channel). J > 1 runs the
+                              reference's Joint channel mode: TCSC coding
+                              (tcsc.hpp: per-bin J x J block solves) and
+                              per-channel learning (solve_learning_tcsc) */
 } dcsc_cuda_opts;
 
 /* dcsc::CodingStats (coding.hpp:27-37) */
@@ -108,16 +115,18 @@ int dcsc_cuda_create(const dcsc_cuda_opts* opts, dcsc_cuda_ctx** out);
 int dcsc_cuda_destroy(dcsc_cuda_ctx* ctx);
 int dcsc_cuda_synchronize(dcsc_cuda_ctx* ctx);
 
-/* signals x: N*H*W doubles; normalised per cfg.normalize (pipeline.cpp:78-121) */
+/* signals x: N*J*H*W doubles (image-major, then channel); normalised per
+ * cfg.normalize (pipeline.cpp:78-121) */
 int dcsc_cuda_set_signals(dcsc_cuda_ctx* ctx, const double* x);
 int dcsc_cuda_get_signals(dcsc_cuda_ctx* ctx, double* x);
-/* dictionary: K*mh*mw doubles */
+/* dictionary: K*J*mh*mw doubles (filter-major, Dictionary::filter(k, j)) */
 int dcsc_cuda_set_dictionary(dcsc_cuda_ctx* ctx, const double* d);
 int dcsc_cuda_get_dictionary(dcsc_cuda_ctx* ctx, double* d);
 /* init_variables: seeded dictionary, zero maps / coding state, gamma = 0, mu = 1 */
 int dcsc_cuda_init_variables(dcsc_cuda_ctx* ctx);
 
-/* warm coding state for images [n0, n1): theta, z (K*D each per image), NULL = zeros */
+/* warm coding state for images [n0, n1): theta, z (K*D each per image), NULL = zeros;
+ * get also returns lambda (J*D per image) */
 int dcsc_cuda_set_coding_state(dcsc_cuda_ctx* ctx, int n0, int n1, const double* theta,
                                const double* z);
 int dcsc_cuda_get_coding_state(dcsc_cuda_ctx* ctx, int n0, int n1, double* theta, double* z,
@@ -129,7 +138,7 @@ int dcsc_cuda_coding(dcsc_cuda_ctx* ctx, int n0, int n1, dcsc_coding_stats* stat
 int dcsc_cuda_set_maps(dcsc_cuda_ctx* ctx, int n0, int n1, const double* z);
 int dcsc_cuda_get_maps(dcsc_cuda_ctx* ctx, int n0, int n1, double* z);
 
-/* learning warm state: gamma N*D (NULL = zeros), mu K (NULL = ones) */
+/* learning warm state: gamma J*N*D (channel-major; NULL = zeros), mu K (NULL = ones) */
 int dcsc_cuda_set_learning_state(dcsc_cuda_ctx* ctx, const double* gamma, const double* mu);
 int dcsc_cuda_get_learning_state(dcsc_cuda_ctx* ctx, double* gamma, double* mu);
 /* solve_learning over all images' maps; writes the candidate dictionary

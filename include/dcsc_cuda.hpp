@@ -6,9 +6,13 @@
 //   dcsc::solve_coding   -> dcsc::cuda::solve_coding     (coding.hpp:74-77)
 //   dcsc::solve_learning -> dcsc::cuda::solve_learning   (learning.hpp:99-104)
 //   dcsc::run_csc        -> dcsc::cuda::run_csc          (pipeline.hpp:58)
+//   dcsc::solve_coding_tcsc / solve_learning_tcsc
+//                        -> dcsc::cuda::solve_coding_tcsc / solve_learning_tcsc
+//                                                        (tcsc.hpp:53-68)
 // Precision defaults to FP64 (the reference's arithmetic); FP32 is opt-in.
-// Grid support: 2-D, single channel (J = 1), sizes compiled into the library
-// (dcsc_cuda_supported_grid); anything else throws dcsc::DimensionError.
+// Grid support: 2-D, J <= 8 channels (J > 1 = Joint channel mode), sizes
+// compiled into the library (dcsc_cuda_supported_grid); anything else throws
+// dcsc::DimensionError.
 #pragma once
 
 #include <cmath>
@@ -20,6 +24,7 @@
 #include "dcsc/coding.hpp"
 #include "dcsc/learning.hpp"
 #include "dcsc/pipeline.hpp"
+#include "dcsc/tcsc.hpp"
 #include "dcsc/types.hpp"
 #include "dcsc_cuda.h"
 
@@ -61,7 +66,7 @@ struct Options {
 class Context {
  public:
   Context(int n_images, const GridDims& dims, int filters, const GridDims& support,
-          const SolverConfig& cfg, Options opt = {}) {
+          const SolverConfig& cfg, Options opt = {}, int channels = 1) {
     if (dims.size() != 2 || support.size() != 2)
       throw DimensionError("dcsc::cuda supports 2-D grids only");
     dcsc_cuda_opts o{};
@@ -74,6 +79,7 @@ class Context {
     o.precision = opt.precision;
     o.device = opt.device;
     o.cfg = to_c(cfg);
+    o.channels = channels;
     dcsc_cuda_ctx* c = nullptr;
     check(dcsc_cuda_create(&o, &c));
     ctx_.reset(c);
@@ -101,6 +107,32 @@ inline CodingStats to_stats(const dcsc_coding_stats& s) {
   return o;
 }
 
+namespace detail {
+// one J-channel signal, warm state in/out (J = 1: solve_coding, J > 1: TCSC)
+inline SparseMaps code_one(const SignalTensor& x, const Dictionary& d, const SolverConfig& cfg,
+                           CodingDualState& state, CodingStats* stats, Options opt) {
+  SolverConfig c = cfg;
+  c.normalize = NormalizeMode::None;  // solve_coding never normalises
+  Context ctx(1, x.dims, d.filters, d.support, c, opt, x.channels);
+  check(dcsc_cuda_set_signals(ctx.get(), x.values.data()));
+  check(dcsc_cuda_set_dictionary(ctx.get(), d.values.data()));
+  const std::size_t kd = static_cast<std::size_t>(d.filters) * x.grid_count();
+  if (state.z.size() == kd && state.theta.size() == kd)
+    check(dcsc_cuda_set_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data()));
+  dcsc_coding_stats s{};
+  check(dcsc_cuda_coding(ctx.get(), 0, 1, &s));
+  state.theta.assign(kd, 0.0);
+  state.z.assign(kd, 0.0);
+  state.lambda.assign(static_cast<std::size_t>(x.channels) * x.grid_count(), 0.0);
+  check(dcsc_cuda_get_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data(),
+                                   state.lambda.data()));
+  if (stats) *stats = to_stats(s);
+  SparseMaps maps(d.filters, x.dims);
+  maps.values = state.z;
+  return maps;
+}
+}  // namespace detail
+
 // solve_coding (coding.hpp:74-77): one single-channel signal, warm state in/out.
 inline SparseMaps solve_coding(const SignalTensor& x, const Dictionary& d, const SolverConfig& cfg,
                                CodingDualState& state, CodingStats* stats = nullptr,
@@ -111,28 +143,26 @@ inline SparseMaps solve_coding(const SignalTensor& x, const Dictionary& d, const
   if (x.channels != 1)
     throw DimensionError("solve_coding expects a single-channel signal; use the TCSC path");
   if (d.channels != 1) throw DimensionError("solve_coding expects a single-channel dictionary");
-  SolverConfig c = cfg;
-  c.normalize = NormalizeMode::None;  // solve_coding never normalises
-  Context ctx(1, x.dims, d.filters, d.support, c, opt);
-  check(dcsc_cuda_set_signals(ctx.get(), x.values.data()));
-  check(dcsc_cuda_set_dictionary(ctx.get(), d.values.data()));
-  const std::size_t kd = static_cast<std::size_t>(d.filters) * x.grid_count();
-  if (state.z.size() == kd && state.theta.size() == kd)
-    check(dcsc_cuda_set_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data()));
-  dcsc_coding_stats s{};
-  check(dcsc_cuda_coding(ctx.get(), 0, 1, &s));
-  state.theta.assign(kd, 0.0);
-  state.z.assign(kd, 0.0);
-  state.lambda.assign(x.grid_count(), 0.0);
-  check(dcsc_cuda_get_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data(),
-                                   state.lambda.data()));
-  if (stats) *stats = to_stats(s);
-  SparseMaps maps(d.filters, x.dims);
-  maps.values = state.z;
-  return maps;
+  return detail::code_one(x, d, cfg, state, stats, opt);
 }
 
-// solve_learning (learning.hpp:99-104), J = 1.
+// solve_coding_tcsc (tcsc.hpp:53-60): J-channel signal, maps shared across
+// channels; the per-bin block solve replaces both the Direct and the Woodbury
+// route (same solution), so `method` is accepted for signature parity only.
+inline SparseMaps solve_coding_tcsc(const SignalTensor& x, const Dictionary& d, const SolverConfig& cfg,
+                                    CodingDualState& state, CodingStats* stats = nullptr,
+                                    BlockSolveMethod method = BlockSolveMethod::Auto, Options opt = {}) {
+  (void)method;
+  cfg.validate();
+  x.validate();
+  d.validate();
+  if (x.channels != d.channels)
+    throw DimensionError("solve_coding_tcsc: signal and dictionary channel counts differ");
+  return detail::code_one(x, d, cfg, state, stats, opt);
+}
+
+// solve_learning (learning.hpp:99-104); J > 1 = solve_learning_tcsc (per-channel
+// gamma systems under one mu ascent).
 inline Dictionary solve_learning(std::span<const SignalTensor> xs, std::span<const SparseMaps> zs,
                                  const GridDims& support, const SolverConfig& cfg,
                                  LearningDualState& state, LearningStats* stats = nullptr,
@@ -146,25 +176,36 @@ inline Dictionary solve_learning(std::span<const SignalTensor> xs, std::span<con
   const std::size_t D = grid_count(dims);
   SolverConfig c = cfg;
   c.normalize = NormalizeMode::None;
-  Context ctx(N, dims, K, support, c, opt);
-  std::vector<double> x(N * D), z(static_cast<std::size_t>(N) * K * D);
+  const int J = xs.front().channels;
+  Context ctx(N, dims, K, support, c, opt, J);
+  const std::size_t JD = static_cast<std::size_t>(J) * D;
+  std::vector<double> x(N * JD), z(static_cast<std::size_t>(N) * K * D);
   for (int n = 0; n < N; ++n) {
-    if (xs[n].channels != 1) throw DimensionError("dcsc::cuda::solve_learning supports J = 1");
-    std::copy(xs[n].values.begin(), xs[n].values.end(), x.begin() + n * D);
+    if (xs[n].channels != J || xs[n].dims != dims)
+      throw DimensionError("solve_learning: images must share dims and channels");
+    std::copy(xs[n].values.begin(), xs[n].values.end(), x.begin() + n * JD);
     std::copy(zs[n].values.begin(), zs[n].values.end(), z.begin() + static_cast<std::size_t>(n) * K * D);
   }
   check(dcsc_cuda_set_signals(ctx.get(), x.data()));
   check(dcsc_cuda_set_maps(ctx.get(), 0, N, z.data()));
-  const bool warm_g = state.gamma.size() == 1 && state.gamma[0].size() == N * D;
+  bool warm_g = state.gamma.size() == static_cast<std::size_t>(J);
+  for (const auto& g : state.gamma) warm_g = warm_g && g.size() == N * D;
   const bool warm_m = state.mu.size() == static_cast<std::size_t>(K);
-  check(dcsc_cuda_set_learning_state(ctx.get(), warm_g ? state.gamma[0].data() : nullptr,
-                                     warm_m ? state.mu.data() : nullptr));
-  Dictionary dict(K, support, 1);
+  std::vector<double> g0;
+  if (warm_g) {
+    g0.resize(static_cast<std::size_t>(J) * N * D);
+    for (int j = 0; j < J; ++j) std::copy(state.gamma[j].begin(), state.gamma[j].end(), g0.begin() + j * N * D);
+  }
+  check(dcsc_cuda_set_learning_state(ctx.get(), warm_g ? g0.data() : nullptr, warm_m ? state.mu.data() : nullptr));
+  Dictionary dict(K, support, J);
   dcsc_learning_stats s{};
   check(dcsc_cuda_learning(ctx.get(), dict.values.data(), &s));
-  state.gamma.assign(1, std::vector<double>(N * D));
+  std::vector<double> g1(static_cast<std::size_t>(J) * N * D);
   state.mu.assign(K, 1.0);
-  check(dcsc_cuda_get_learning_state(ctx.get(), state.gamma[0].data(), state.mu.data()));
+  check(dcsc_cuda_get_learning_state(ctx.get(), g1.data(), state.mu.data()));
+  state.gamma.assign(J, std::vector<double>(N * D));
+  for (int j = 0; j < J; ++j)
+    std::copy(g1.begin() + j * N * D, g1.begin() + (j + 1) * N * D, state.gamma[j].begin());
   state.mu_iters_total += s.mu_iters;
   state.cg_iters_total += s.cg_iters;
   if (stats) {
@@ -182,21 +223,29 @@ inline Dictionary solve_learning(std::span<const SignalTensor> xs, std::span<con
   return dict;
 }
 
+inline Dictionary solve_learning_tcsc(std::span<const SignalTensor> xs, std::span<const SparseMaps> zs,
+                                      const GridDims& support, const SolverConfig& cfg, LearningDualState& state,
+                                      LearningStats* stats = nullptr, Options opt = {}) {
+  return solve_learning(xs, zs, support, cfg, state, stats, opt);  // tcsc.cpp:263-270
+}
+
 // run_csc (pipeline.hpp:58): the whole alternating loop device-resident.
+// J > 1 signals require ChannelMode::Joint (RunConfig::validate, pipeline.cpp:66-76).
 inline RunResult run_csc(const RunConfig& cfg, const Dataset& data, Options opt = {}) {
   if (data.signals.empty()) throw std::invalid_argument("dataset is empty");
   const GridDims dims = data.signals.front().dims;
+  const int J = data.signals.front().channels;
   for (const SignalTensor& s : data.signals) {
     s.validate();
-    if (s.dims != dims || s.channels != 1)
-      throw DimensionError("all dataset signals must share dims (J = 1 on the CUDA path)");
+    if (s.dims != dims || s.channels != J) throw DimensionError("all dataset signals must share dims and channels");
   }
-  cfg.validate(dims, 1);
+  cfg.validate(dims, J);
   const int N = static_cast<int>(data.signals.size());
   const std::size_t D = grid_count(dims);
-  Context ctx(N, dims, cfg.filters, cfg.support, cfg.solver, opt);
-  std::vector<double> x(N * D);
-  for (int n = 0; n < N; ++n) std::copy(data.signals[n].values.begin(), data.signals[n].values.end(), x.begin() + n * D);
+  const std::size_t JD = static_cast<std::size_t>(J) * D;
+  Context ctx(N, dims, cfg.filters, cfg.support, cfg.solver, opt, J);
+  std::vector<double> x(N * JD);
+  for (int n = 0; n < N; ++n) std::copy(data.signals[n].values.begin(), data.signals[n].values.end(), x.begin() + n * JD);
   check(dcsc_cuda_set_signals(ctx.get(), x.data()));
   RunResult r;
   std::vector<dcsc_trace_row> rows(2 * std::max(cfg.solver.max_outer, 1));
@@ -214,7 +263,7 @@ inline RunResult run_csc(const RunConfig& cfg, const Dataset& data, Options opt 
   }
   r.converged = conv != 0;
   r.outer_iters = n_rows / 2;
-  r.dict = Dictionary(cfg.filters, cfg.support, 1);
+  r.dict = Dictionary(cfg.filters, cfg.support, J);
   check(dcsc_cuda_get_dictionary(ctx.get(), r.dict.values.data()));
   r.maps.assign(N, SparseMaps(cfg.filters, dims));
   std::vector<double> z(static_cast<std::size_t>(N) * cfg.filters * D);

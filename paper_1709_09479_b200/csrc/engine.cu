@@ -20,6 +20,7 @@
 #include "dcsc_cuda.h"
 #include "kernels.cuh"
 #include "kernels_cluster.cuh"
+#include "tcsc_kernels.cuh"
 
 using namespace dcsc_cuda;
 
@@ -134,9 +135,15 @@ std::vector<double> gaussian_blur(int H, int W, const double* v, double sigma) {
   return cur;
 }
 
-// dcsc::normalize (pipeline.cpp:78-121) for one single-channel image.
-void normalize_image(int mode, int H, int W, const double* in, double* out) {
-  const size_t D = (size_t)H * W;
+// dcsc::normalize (pipeline.cpp:78-121) for one J-channel image: Global uses
+// the mean / std of all J*D values, Local runs per channel.
+void normalize_image(int mode, int H, int W, const double* in, double* out, int J = 1) {
+  if (mode == 2 && J > 1) {
+    for (int j = 0; j < J; ++j)
+      normalize_image(mode, H, W, in + (size_t)j * H * W, out + (size_t)j * H * W, 1);
+    return;
+  }
+  const size_t D = (size_t)H * W * J;  // None / Global act on all J*D values
   if (mode == 0) {
     std::copy(in, in + D, out);
     return;
@@ -329,10 +336,14 @@ class Engine final : public EngineBase {
   }
   template <int MODE>
   static void launch_coding(int G, int cnt, cudaStream_t st, const CodingArgs<R>& a) {
-    if constexpr (CLU)
+    if constexpr (CLU) {
       coding_pass_cl<P, MODE><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
-    else
-      coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+    } else {
+      if (a.J > 1)
+        coding_pass<P, MODE, true><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else
+        coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+    }
   }
   template <class SRC>
   static void launch_r2c(int count, cudaStream_t st, const SRC* src, size_t ss, C* dst, size_t ds, const C* tw,
@@ -382,6 +393,10 @@ class Engine final : public EngineBase {
       big((const void*)coding_pass<P, kPassPrologue>, smem_coding());
       big((const void*)coding_pass<P, kPassObjective>, smem_coding());
       big((const void*)coding_pass<P, kPassMaps>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassPrologue, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassObjective, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassMaps, true>, smem_coding());
       big((const void*)r2c_planes<P, R>, smem_plain());
       big((const void*)r2c_planes<P, double>, smem_plain());
       big((const void*)c2r_planes<P, R>, smem_plain());
@@ -394,6 +409,9 @@ class Engine final : public EngineBase {
   explicit Engine(const dcsc_cuda_opts& o) : o_(o), cfg_(o.cfg) {
     N_ = o.n_images;
     K_ = o.filters;
+    J_ = std::max(1, o.channels);
+    if (J_ > kMaxChannels) throw DimErr("at most " + std::to_string(kMaxChannels) + " channels are supported");
+    if (J_ > 1 && CLU) throw DimErr("multi-channel (TCSC) coding is not compiled for the cluster grid family");
     mh_ = o.support_h;
     mw_ = o.support_w;
     M_ = mh_ * mw_;
@@ -437,15 +455,19 @@ class Engine final : public EngineBase {
     CK(cudaMemcpy(dtw_.p, tw.data(), sizeof(C) * P::TW_LEN, cudaMemcpyHostToDevice));
 
     const size_t nD = (size_t)N_ * D, nNB = (size_t)N_ * NB;
-    x_.alloc(sizeof(R) * nD);
-    xhat_.alloc(sizeof(C) * nNB);
-    dhat_.alloc(sizeof(C) * (size_t)K_ * NB);
-    dcand_.alloc(sizeof(C) * (size_t)K_ * NB);
+    x_.alloc(sizeof(R) * nD * J_);                    // N x J x D
+    xhat_.alloc(sizeof(C) * nNB * J_);                // J x N x NB (channel-major)
+    dhat_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);    // J x K x NB (channel-major)
+    dcand_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);
     sigma_.alloc(sizeof(R) * NB);
     u_.alloc(sizeof(R) * nD * K_);
     maps_.alloc(sizeof(R) * nD * K_);
-    lamhat_.alloc(sizeof(C) * nNB);
-    lam_.alloc(sizeof(R) * nD);
+    lamhat_.alloc(sizeof(C) * nNB * J_);              // N x J x NB
+    lam_.alloc(sizeof(R) * nD * J_);                  // N x J x D
+    if (J_ > 1) {
+      ginv_.alloc(sizeof(C) * (size_t)NB * J_ * J_);
+      what_.alloc(sizeof(C) * nNB * K_);
+    }
     part_.alloc(sizeof(C) * (size_t)N_ * G_ * NB);
     sums_.alloc(sizeof(double) * (size_t)N_ * G_ * CLN * kSums);
     conv_.alloc(sizeof(int) * N_);
@@ -458,7 +480,7 @@ class Engine final : public EngineBase {
     odata_.alloc(sizeof(double) * N_);
     ol1_.alloc(sizeof(double) * N_);
     accept_.alloc(sizeof(int) * N_);
-    gam_.alloc(sizeof(C) * nNB);
+    gam_.alloc(sizeof(C) * nNB * J_);                 // J x N x NB
     r_.alloc(sizeof(C) * nNB);
     p_.alloc(sizeof(C) * nNB);
     ap_.alloc(sizeof(C) * nNB);
@@ -470,7 +492,7 @@ class Engine final : public EngineBase {
     dmu_.alloc(sizeof(double) * K_);
     dwk_.alloc(sizeof(double) * K_);
     dd_.alloc(sizeof(double) * (size_t)K_ * M_);
-    ddict_.alloc(sizeof(double) * (size_t)K_ * M_);
+    ddict_.alloc(sizeof(double) * (size_t)J_ * K_ * M_);
     cg_.alloc(sizeof(CgState));
     hred_.alloc(sizeof(double) * std::max(64, K_ + 8));
     cglob_.alloc(sizeof(double2) * (size_t)K_ * NB);
@@ -482,18 +504,21 @@ class Engine final : public EngineBase {
     partial2_.alloc(sizeof(double) * (size_t)N_ * accept_chunks_);
     l0_.alloc(sizeof(unsigned long long) * (size_t)N_ * accept_chunks_);
     device_bytes = x_.bytes + xhat_.bytes + dhat_.bytes + dcand_.bytes + sigma_.bytes + u_.bytes +
-                   maps_.bytes + lamhat_.bytes + lam_.bytes + part_.bytes + sums_.bytes +
-                   4 * gam_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes;
+                   maps_.bytes + lamhat_.bytes + lam_.bytes + part_.bytes + sums_.bytes + gam_.bytes +
+                   3 * r_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes + ginv_.bytes + what_.bytes;
     CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
     CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
     CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
     CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
     CK(cudaMemsetAsync(x_.p, 0, x_.bytes, st_));
     CK(cudaMemsetAsync(xhat_.p, 0, xhat_.bytes, st_));
-    dict_.assign((size_t)K_ * M_, 0.0);
+    dict_.assign((size_t)K_ * J_ * M_, 0.0);
     u_zero_.assign(N_, 1);
     mu_.assign(K_, 1.0);
     xnorm2_.assign(N_, 0.0);
+    xnorm2c_.assign((size_t)N_ * J_, 0.0);
+    xh_ch_ = xhat_.as<C>();
+    gam_ch_ = gam_.as<C>();
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -532,13 +557,14 @@ class Engine final : public EngineBase {
   CodingArgs<R> cargs(const C* dhat, int n_off) {
     CodingArgs<R> a;
     a.dhat = dhat;
-    a.lamhat = lamhat_.as<C>();
+    a.J = J_;
+    a.what = what_.as<C>() ? what_.as<C>() + (size_t)n_off * K_ * NB : nullptr;
     a.u = u_.as<R>() + (size_t)n_off * K_ * D;
     a.maps = maps_.as<R>() + (size_t)n_off * K_ * D;
     a.part = part_.as<C>() + (size_t)n_off * G_ * NB;
     a.sums = sums_.as<double>() + (size_t)n_off * G_ * CLN * kSums;
     a.conv = conv_.as<int>() + n_off;
-    a.lamhat = lamhat_.as<C>() + (size_t)n_off * NB;
+    a.lamhat = lamhat_.as<C>() + (size_t)n_off * J_ * NB;
     a.K = K_;
     a.G = G_;
     a.kpg = kpg_;
@@ -549,7 +575,7 @@ class Engine final : public EngineBase {
     a.conv_w = conv_.as<int>() + n_off;
     a.xhat = xhat_.as<C>() + (size_t)n_off * NB;
     a.sigma = sigma_.as<R>();
-    a.lamhat_w = lamhat_.as<C>() + (size_t)n_off * NB;
+    a.lamhat_w = lamhat_.as<C>() + (size_t)n_off * J_ * NB;
     a.img = img_.as<ImageAdmm>() + n_off;
     a.iter = 0;
     a.is_last = 0;
@@ -583,17 +609,29 @@ class Engine final : public EngineBase {
     launch(kFamOther, [&] { launch_c2r<DST>(count, st_, src, src_stride, dst, dst_stride, dtw_.as<C>()); });
   }
 
+  // host dictionary K x J x M (Dictionary::filter(k, j), types.cpp:60-68) ->
+  // device spectra J x K x NB (channel-major: channel j's K planes contiguous)
   void upload_dict_spectra(const double* d, C* dst) {
-    CK(cudaMemcpyAsync(ddict_.p, d, sizeof(double) * K_ * M_, cudaMemcpyHostToDevice, st_));
-    launch(kFamOther, [&] { launch_filters(K_, st_, ddict_.as<double>(), mh_, mw_, dst, dtw_.as<C>()); });
+    const double* src = d;
+    if (J_ > 1) {
+      dstage_.resize((size_t)J_ * K_ * M_);
+      for (int k = 0; k < K_; ++k)
+        for (int j = 0; j < J_; ++j)
+          std::copy(d + ((size_t)k * J_ + j) * M_, d + ((size_t)k * J_ + j + 1) * M_,
+                    dstage_.data() + ((size_t)j * K_ + k) * M_);
+      src = dstage_.data();
+    }
+    CK(cudaMemcpyAsync(ddict_.p, src, sizeof(double) * J_ * K_ * M_, cudaMemcpyHostToDevice, st_));
+    launch(kFamOther, [&] { launch_filters(J_ * K_, st_, ddict_.as<double>(), mh_, mw_, dst, dtw_.as<C>()); });
+    CK(cudaStreamSynchronize(st_));  // dstage_ is reused
   }
 
   // ------------------------------------------------------------ API
   void set_signals(const double* x) override {
-    const size_t nD = (size_t)N_ * D;
+    const size_t nD = (size_t)N_ * J_ * D;
     // host side parallel over images: validate, normalise (pipeline.cpp:78-121),
-    // round to the storage precision into pinned staging, per-image norms of the
-    // stored values (what the oracle sees)
+    // round to the storage precision into pinned staging, per-image (and
+    // per-channel) norms of the stored values (what the oracle sees)
     int bad = 0;
 #pragma omp parallel for reduction(| : bad)
     for (long i = 0; i < (long)nD; ++i) bad |= !std::isfinite(x[i]);
@@ -605,34 +643,48 @@ class Engine final : public EngineBase {
     }
     R* xr = static_cast<R*>(xstage_);
     xs_host_.resize(nD);
+    const size_t JD = (size_t)J_ * D;
 #pragma omp parallel for schedule(static)
     for (int n = 0; n < N_; ++n) {
-      double* xn = xs_host_.data() + (size_t)n * D;
-      normalize_image(cfg_.normalize, H, W, x + (size_t)n * D, xn);
+      double* xn = xs_host_.data() + (size_t)n * JD;
+      normalize_image(cfg_.normalize, H, W, x + (size_t)n * JD, xn, J_);
       double s = 0.0;
-      for (size_t i = 0; i < (size_t)D; ++i) {
-        const R v = R(xn[i]);
-        xr[(size_t)n * D + i] = v;
-        xn[i] = double(v);
-        s += xn[i] * xn[i];
+      for (int j = 0; j < J_; ++j) {
+        double sj = 0.0;
+        for (size_t i = (size_t)j * D; i < (size_t)(j + 1) * D; ++i) {
+          const R v = R(xn[i]);
+          xr[(size_t)n * JD + i] = v;
+          xn[i] = double(v);
+          sj += xn[i] * xn[i];
+        }
+        xnorm2c_[(size_t)n * J_ + j] = sj;
+        s += sj;
       }
       xnorm2_[n] = s;
     }
     CK(cudaMemcpyAsync(x_.p, xr, sizeof(R) * nD, cudaMemcpyHostToDevice, st_));
-    r2c(x_.p, false, D, xhat_.as<C>(), NB, N_);
+    for (int j = 0; j < J_; ++j)  // x_hat channel-major: J x N x NB
+      r2c(x_.as<R>() + (size_t)j * D, false, JD, xhat_.as<C>() + (size_t)j * N_ * NB, NB, N_);
     CK(cudaStreamSynchronize(st_));
   }
 
   void get_signals(double* x) override { std::copy(xs_host_.begin(), xs_host_.end(), x); }
 
   void set_dictionary(const double* d) override {
-    require_finite(d, (size_t)K_ * M_, "dictionary");
-    dict_.assign(d, d + (size_t)K_ * M_);
+    const size_t cnt = (size_t)K_ * J_ * M_;
+    require_finite(d, cnt, "dictionary");
+    dict_.assign(d, d + cnt);
     dict_zero_ = std::all_of(dict_.begin(), dict_.end(), [](double v) { return v == 0.0; });
     upload_dict_spectra(dict_.data(), dhat_.as<C>());
-    launch(kFamOther, [&] {
-      sigma_kernel<R><<<(NB + 255) / 256, 256, 0, st_>>>(dhat_.as<C>(), sigma_.as<R>(), K_, NB, cfg_.rho);
-    });
+    if (J_ == 1) {
+      launch(kFamOther, [&] {
+        sigma_kernel<R><<<(NB + 255) / 256, 256, 0, st_>>>(dhat_.as<C>(), sigma_.as<R>(), K_, NB, cfg_.rho);
+      });
+    } else {  // per-bin block factorisation, once per dictionary (tcsc.cpp:31-55)
+      launch(kFamOther, [&] {
+        tc_factor<R><<<(NB + 127) / 128, 128, 0, st_>>>(dhat_.as<C>(), ginv_.as<C>(), K_, J_, NB, cfg_.rho);
+      });
+    }
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -640,22 +692,23 @@ class Engine final : public EngineBase {
 
   // init_variables (pipeline.cpp:123-156)
   void init_variables() override {
-    std::vector<double> d((size_t)K_ * M_);
+    const int JM = J_ * M_;  // filter k spans its J channel slices (k-major)
+    std::vector<double> d((size_t)K_ * JM);
     std::mt19937_64 rng(cfg_.seed);
     auto uniform = [&rng]() { return static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5; };
     for (int k = 0; k < K_; ++k) {
       double sq = 0.0;
-      for (int i = 0; i < M_; ++i) {
+      for (int i = 0; i < JM; ++i) {
         const double v = uniform();
-        d[(size_t)k * M_ + i] = v;
+        d[(size_t)k * JM + i] = v;
         sq += v * v;
       }
       double nrm = std::sqrt(sq);
       if (nrm == 0.0) {
-        d[(size_t)k * M_] = 1.0;
+        d[(size_t)k * JM] = 1.0;
         nrm = 1.0;
       }
-      for (int i = 0; i < M_; ++i) d[(size_t)k * M_ + i] /= nrm;
+      for (int i = 0; i < JM; ++i) d[(size_t)k * JM + i] /= nrm;
     }
     set_dictionary(d.data());
     CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
@@ -700,7 +753,7 @@ class Engine final : public EngineBase {
     if (!theta && !z) {  // the reference's empty state (coding.cpp:175-179): device-side reset
       std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
       CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * cnt, st_));
-      CK(cudaMemsetAsync(lam_.as<R>() + (size_t)n0 * D, 0, sizeof(R) * (size_t)(n1 - n0) * D, st_));
+      CK(cudaMemsetAsync(lam_.as<R>() + (size_t)n0 * J_ * D, 0, sizeof(R) * (size_t)(n1 - n0) * J_ * D, st_));
       return;
     }
     std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
@@ -716,8 +769,9 @@ class Engine final : public EngineBase {
     const size_t cnt = (size_t)(n1 - n0) * K_ * D;
     std::vector<R> u(cnt);
     CK(cudaMemcpyAsync(u.data(), u_.as<R>() + (size_t)n0 * K_ * D, sizeof(R) * cnt, cudaMemcpyDeviceToHost, st_));
-    std::vector<R> l((size_t)(n1 - n0) * D);
-    CK(cudaMemcpyAsync(l.data(), lam_.as<R>() + (size_t)n0 * D, sizeof(R) * l.size(), cudaMemcpyDeviceToHost, st_));
+    std::vector<R> l((size_t)(n1 - n0) * J_ * D);
+    CK(cudaMemcpyAsync(l.data(), lam_.as<R>() + (size_t)n0 * J_ * D, sizeof(R) * l.size(), cudaMemcpyDeviceToHost,
+                       st_));
     CK(cudaStreamSynchronize(st_));
     const R beta = R(cfg_.beta), rho = R(cfg_.rho);
     for (size_t i = 0; i < cnt; ++i) {
@@ -739,18 +793,19 @@ class Engine final : public EngineBase {
       // degenerate dictionary: z = theta = 0, lambda = -x (coding.cpp:181-191)
       std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
       CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * (size_t)cnt * K_ * D, st_));
-      const size_t tot = (size_t)cnt * D;
+      const size_t JD = (size_t)J_ * D;
+      const size_t tot = (size_t)cnt * JD;
       launch(kFamOther, [&] {
-        neg_copy<R><<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(x_.as<R>() + (size_t)n0 * D,
-                                                                   lam_.as<R>() + (size_t)n0 * D, tot);
+        neg_copy<R><<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(x_.as<R>() + (size_t)n0 * JD,
+                                                                   lam_.as<R>() + (size_t)n0 * JD, tot);
       });
       CK(cudaStreamSynchronize(st_));
       for (int i = 0; i < cnt; ++i) {
         double ls = 0.0, lx = 0.0;
-        for (size_t j = 0; j < (size_t)D; ++j) {
-          const double lv = -xs_host_[(size_t)(n0 + i) * D + j];
+        for (size_t j = 0; j < JD; ++j) {
+          const double lv = -xs_host_[(size_t)(n0 + i) * JD + j];
           ls += lv * lv;
-          lx += lv * xs_host_[(size_t)(n0 + i) * D + j];
+          lx += lv * xs_host_[(size_t)(n0 + i) * JD + j];
         }
         out[i] = dcsc_coding_stats{};
         out[i].converged = 1;
@@ -767,10 +822,23 @@ class Engine final : public EngineBase {
     // initial lambda_hat from the warm state (the first assemble_w, coding.cpp:216-229);
     // a zero state has w_hat = 0, so the FFT pass is skipped and part is zeroed
     const bool all_zero = std::all_of(u_zero_.begin() + n0, u_zero_.begin() + n1, [](char v) { return v != 0; });
-    if (all_zero)
+    // multi-channel: lambda_hat from the per-bin J x J solves (tcsc.cpp:68-88)
+    auto tc_lam = [&](int kw, bool skip_conv) {
+      launch(kFamLambda, [&] {
+        tc_lambda<R><<<dim3((NB + 127) / 128, cnt), 128, 0, st_>>>(
+            what_.as<C>() + (size_t)n0 * K_ * NB, dhat_.as<C>(), ginv_.as<C>(), xhat_.as<C>() + (size_t)n0 * NB,
+            (size_t)N_ * NB, lamhat_.as<C>() + (size_t)n0 * J_ * NB, skip_conv ? conv_.as<int>() + n0 : nullptr, K_,
+            kw, J_, NB, R(1.0 / cfg_.rho));
+      });
+    };
+    if (J_ > 1) {
+      if (!all_zero) coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);  // w_hat of the warm state
+      tc_lam(all_zero ? 0 : K_, false);
+    } else if (all_zero) {
       CK(cudaMemsetAsync(part_.as<C>() + (size_t)n0 * G_ * NB, 0, sizeof(C) * (size_t)cnt * G_ * NB, st_));
-    else
+    } else {
       coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);  // lambda_hat from the fused epilogue
+    }
     std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
     auto lam_update = [&](int iter, int last, int prologue) {
       launch(kFamLambda, [&] {
@@ -782,13 +850,14 @@ class Engine final : public EngineBase {
                                                  prologue);
       });
     };
-    if (all_zero) lam_update(0, 0, 1);
+    if (all_zero && J_ == 1) lam_update(0, 0, 1);
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     int pending = -1;  // iteration whose conv flags are in flight
     for (int it = 1; it <= cfg_.max_admm; ++it) {
       coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
+      if (J_ > 1 && it < cfg_.max_admm) tc_lam(K_, true);
       if (pending >= 0) {
         // one-iteration look-ahead: iteration `it` is queued before we wait on it-1
         CK(cudaEventSynchronize(ev[pending & 1]));
@@ -806,10 +875,10 @@ class Engine final : public EngineBase {
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
     // exit: lambda = iDFT(lambda_hat), rescale, dual objective (coding.cpp:287-309)
-    c2r<R>(lamhat_.as<C>() + (size_t)n0 * NB, NB, lam_.as<R>() + (size_t)n0 * D, D, cnt);
+    c2r<R>(lamhat_.as<C>() + (size_t)n0 * J_ * NB, NB, lam_.as<R>() + (size_t)n0 * J_ * D, D, cnt * J_);
     launch(kFamOther, [&] {
-      admm_exit<R><<<cnt, 256, 0, st_>>>(lam_.as<R>() + (size_t)n0 * D, x_.as<R>() + (size_t)n0 * D,
-                                         img_.as<ImageAdmm>() + n0, D, cfg_.beta, dual_.as<double>() + n0,
+      admm_exit<R><<<cnt, 256, 0, st_>>>(lam_.as<R>() + (size_t)n0 * J_ * D, x_.as<R>() + (size_t)n0 * J_ * D,
+                                         img_.as<ImageAdmm>() + n0, J_ * D, cfg_.beta, dual_.as<double>() + n0,
                                          infeas_.as<double>() + n0, resc_.as<int>() + n0);
     });
     std::vector<ImageAdmm> im(cnt);
@@ -855,11 +924,11 @@ class Engine final : public EngineBase {
   }
 
   void set_learning_state(const double* gamma, const double* mu) override {
-    if (gamma) {
+    if (gamma) {  // J x N x D (LearningDualState::gamma[j], learning.hpp:15-23)
       DevMem tmp;
-      tmp.alloc(sizeof(double) * (size_t)N_ * D);
+      tmp.alloc(sizeof(double) * (size_t)J_ * N_ * D);
       CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
-      r2c(tmp.p, true, D, gam_.as<C>(), NB, N_);
+      r2c(tmp.p, true, D, gam_.as<C>(), NB, J_ * N_);
       CK(cudaStreamSynchronize(st_));
     } else {
       CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
@@ -872,8 +941,8 @@ class Engine final : public EngineBase {
   void get_learning_state(double* gamma, double* mu) override {
     if (gamma) {
       DevMem tmp;
-      tmp.alloc(sizeof(double) * (size_t)N_ * D);
-      c2r<double>(gam_.as<C>(), NB, tmp.as<double>(), D, N_);
+      tmp.alloc(sizeof(double) * (size_t)J_ * N_ * D);
+      c2r<double>(gam_.as<C>(), NB, tmp.as<double>(), D, J_ * N_);
       CK(cudaMemcpyAsync(gamma, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
       CK(cudaStreamSynchronize(st_));
     }
@@ -978,7 +1047,7 @@ class Engine final : public EngineBase {
     const size_t total = (size_t)N_ * NB;
     const unsigned vb = (unsigned)((total + TBV - 1) / TBV);
     if (bnorm == 0.0) {
-      CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+      CK(cudaMemsetAsync(gam_ch_, 0, sizeof(C) * total, st_));
       converged = true;
       return;
     }
@@ -987,9 +1056,9 @@ class Engine final : public EngineBase {
     init.tol = cfg_.cg_tol;
     init.max_iters = cfg_.cg_max;
     CK(cudaMemcpyAsync(cg_.p, &init, sizeof(CgState), cudaMemcpyHostToDevice, st_));
-    apply_hat(gam_.as<C>(), ap_.as<C>());
+    apply_hat(gam_ch_, ap_.as<C>());
     launch(kFamOther, [&] {
-      cg_init<R, TBV><<<vb, TBV, 0, st_>>>(xhat_.as<C>(), ap_.as<C>(), r_.as<C>(), p_.as<C>(),
+      cg_init<R, TBV><<<vb, TBV, 0, st_>>>(xh_ch_, ap_.as<C>(), r_.as<C>(), p_.as<C>(),
                                             partial_.as<double>(), total, NB, Wh);
     });
     const double invD = 1.0 / D;
@@ -1003,7 +1072,7 @@ class Engine final : public EngineBase {
         apply_hat(p_.as<C>(), ap_.as<C>(), done);
         cg_step(partial_.as<double>(), N_ * tiles_, invD, 1);
         launch(kFamOther, [&] {
-          cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_.as<C>(), r_.as<C>(), p_.as<C>(), ap_.as<C>(),
+          cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_ch_, r_.as<C>(), p_.as<C>(), ap_.as<C>(),
                                                   cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh);
         });
         cg_step(partial_.as<double>(), (int)vb, invD, 2);
@@ -1021,7 +1090,7 @@ class Engine final : public EngineBase {
 
   // d_recover (learning.cpp:187-216): d_k = -0.5/max(mu_k,1e-300) crop(iDFT(sum_n conj(z_nk) gamma_n))
   void d_recover(std::vector<double>& d) {
-    correlate_hat(gam_.as<C>(), nullptr);
+    correlate_hat(gam_ch_, nullptr);
     // d_recover does not skip dead filters; their correlation is exactly zero anyway
     launch(kFamMask, [&] {
       launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
@@ -1032,7 +1101,9 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
   }
 
-  // solve_learning (learning.cpp:227-355) over all images
+  // solve_learning (learning.cpp:227-355) over all images; J > 1 runs the J
+  // per-channel gamma systems under one mu ascent with joint filter norms
+  // (solve_learning_tcsc, tcsc.cpp:263-270 -> learning.cpp:276-345)
   void learning(double* d_out, dcsc_learning_stats* st) override {
     dcsc_learning_stats ls{};
     if ((int)mu_.size() != K_) mu_.assign(K_, 1.0);
@@ -1040,19 +1111,21 @@ class Engine final : public EngineBase {
     int n_live = 0;
     for (int k = 0; k < K_; ++k) n_live += live_h_[k] ? 1 : 0;
     ls.n_dead = K_ - n_live;
+    const size_t JM = (size_t)J_ * M_;
     if (n_live == 0) {  // every map zero: zero dictionary, gamma = 0 (learning.cpp:258-270)
       ls.degenerate = 1;
       CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
       CK(cudaStreamSynchronize(st_));
-      std::fill(d_out, d_out + (size_t)K_ * M_, 0.0);
+      std::fill(d_out, d_out + (size_t)K_ * JM, 0.0);
       if (st) *st = ls;
       return;
     }
-    double bn = 0.0;
-    for (int n = 0; n < N_; ++n) bn += xnorm2_[n];
-    reduce_host(&bn, 1);
-    const double bnorm = std::sqrt(bn);
-    std::vector<double> d;
+    std::vector<double> bnorm(J_, 0.0);
+    for (int n = 0; n < N_; ++n)
+      for (int j = 0; j < J_; ++j) bnorm[j] += xnorm2c_[(size_t)n * J_ + j];
+    reduce_host(bnorm.data(), J_);
+    for (double& b : bnorm) b = std::sqrt(b);
+    std::vector<std::vector<double>> parts(J_);
     std::vector<double> norms(K_, 0.0);
     bool clamped = false;
     for (int iter = 1; iter <= cfg_.max_mu_iters; ++iter) {
@@ -1063,16 +1136,26 @@ class Engine final : public EngineBase {
           clamped = true;
         }
       upload_mu();
-      int cg_iters = 0;
-      bool cg_conv = false;
-      gamma_solve(bnorm, cg_iters, cg_conv);
-      ls.cg_iters += cg_iters;
-      if (!cg_conv) ls.cg_budget_hit = 1;
-      if (iter == 1) ls.cg_iters_first = cg_iters;
-      d_recover(d);
+      long iter_cg = 0;
+      for (int j = 0; j < J_; ++j) {
+        select_channel(j);
+        int cg_iters = 0;
+        bool cg_conv = false;
+        gamma_solve(bnorm[j], cg_iters, cg_conv);
+        iter_cg += cg_iters;
+        if (!cg_conv) ls.cg_budget_hit = 1;
+      }
+      ls.cg_iters += iter_cg;
+      if (iter == 1) ls.cg_iters_first = iter_cg;
+      for (int j = 0; j < J_; ++j) {
+        select_channel(j);
+        d_recover(parts[j]);
+      }
+      select_channel(0);
       for (int k = 0; k < K_; ++k) {
         double sq = 0.0;
-        for (int i = 0; i < M_; ++i) sq += d[(size_t)k * M_ + i] * d[(size_t)k * M_ + i];
+        for (int j = 0; j < J_; ++j)
+          for (int i = 0; i < M_; ++i) sq += parts[j][(size_t)k * M_ + i] * parts[j][(size_t)k * M_ + i];
         norms[k] = std::sqrt(sq);
       }
       ls.mu_iters = iter;
@@ -1099,9 +1182,16 @@ class Engine final : public EngineBase {
         scale = 1.0 / norms[k];
         ++ls.rescaled_filters;
       }
-      for (int i = 0; i < M_; ++i) d_out[(size_t)k * M_ + i] = scale * d[(size_t)k * M_ + i];
+      for (int j = 0; j < J_; ++j)
+        for (int i = 0; i < M_; ++i) d_out[(size_t)k * JM + (size_t)j * M_ + i] = scale * parts[j][(size_t)k * M_ + i];
     }
     if (st) *st = ls;
+  }
+
+  // learning views of channel j: x_hat_j and gamma_j (both N x NB)
+  void select_channel(int j) {
+    xh_ch_ = xhat_.as<C>() + (size_t)j * N_ * NB;
+    gam_ch_ = gam_.as<C>() + (size_t)j * N_ * NB;
   }
 
   void learning_apply(const double* mu, const double* v, double* out) override {
@@ -1121,22 +1211,28 @@ class Engine final : public EngineBase {
     mu_ = keep;
   }
 
-  // per-image data terms of `d` against the accepted maps (Parseval on z_hat)
+  // per-image data terms of `d` against the accepted maps (Parseval on z_hat),
+  // summed over channels
   void data_terms(const double* d, std::vector<double>& data) {
     build_zhat();
     upload_dict_spectra(d, dcand_.as<C>());
     const dim3 g3(tiles_, N_);
-    launch(kFamContract, [&] {
-      contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), dcand_.as<C>(), dwk_.as<double>(), live_.as<int>(),
-                                                 xhat_.as<C>(), nullptr, partial_.as<double>(), N_, K_, NB, Wh, 1,
-                                                 nullptr);
-    });
-    launch(kFamOther, [&] {
-      per_image_reduce<<<N_, 256, 0, st_>>>(partial_.as<double>(), tiles_, 0.5 / D, odata_.as<double>());
-    });
-    data.resize(N_);
-    CK(cudaMemcpyAsync(data.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
-    CK(cudaStreamSynchronize(st_));
+    data.assign(N_, 0.0);
+    std::vector<double> part(N_);
+    for (int j = 0; j < J_; ++j) {
+      launch(kFamContract, [&] {
+        contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), dcand_.as<C>() + (size_t)j * K_ * NB,
+                                                   dwk_.as<double>(), live_.as<int>(),
+                                                   xhat_.as<C>() + (size_t)j * N_ * NB, nullptr,
+                                                   partial_.as<double>(), N_, K_, NB, Wh, 1, nullptr);
+      });
+      launch(kFamOther, [&] {
+        per_image_reduce<<<N_, 256, 0, st_>>>(partial_.as<double>(), tiles_, 0.5 / D, odata_.as<double>());
+      });
+      CK(cudaMemcpyAsync(part.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      for (int n = 0; n < N_; ++n) data[n] += part[n];
+    }
   }
 
   void learning_data_term(const double* d, double* out) override {
@@ -1152,10 +1248,18 @@ class Engine final : public EngineBase {
   template <int MODE>
   void objective_pass(const C* dhat, std::vector<double>& data, std::vector<double>& l1) {
     coding_launch<MODE>(dhat, 0, N_);
-    launch(kFamOther, [&] {
-      objective_reduce<R><<<N_, 256, 0, st_>>>(part_.as<C>(), sums_.as<double>(), xhat_.as<C>(), G_, G_ * CLN, NB,
-                                               Wh, 1.0 / D, cfg_.beta, odata_.as<double>(), ol1_.as<double>());
-    });
+    if (J_ > 1) {
+      launch(kFamOther, [&] {
+        tc_objective<R><<<N_, 256, 0, st_>>>(what_.as<C>(), dhat, xhat_.as<C>(), (size_t)N_ * NB, sums_.as<double>(),
+                                             G_ * CLN, K_, J_, NB, Wh, 1.0 / D, cfg_.beta, odata_.as<double>(),
+                                             ol1_.as<double>());
+      });
+    } else {
+      launch(kFamOther, [&] {
+        objective_reduce<R><<<N_, 256, 0, st_>>>(part_.as<C>(), sums_.as<double>(), xhat_.as<C>(), G_, G_ * CLN,
+                                                 NB, Wh, 1.0 / D, cfg_.beta, odata_.as<double>(), ol1_.as<double>());
+      });
+    }
     data.resize(N_);
     l1.resize(N_);
     CK(cudaMemcpyAsync(data.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
@@ -1248,7 +1352,7 @@ class Engine final : public EngineBase {
                      admm_total, 0, 0, coding_ms, w1 - w0, l0};
 
       dcsc_learning_stats ls{};
-      std::vector<double> dc((size_t)K_ * M_);
+      std::vector<double> dc((size_t)K_ * J_ * M_);
       learning(dc.data(), &ls);
       const double learning_ms = now_ms() - w1;
       std::vector<double> data;
@@ -1363,13 +1467,15 @@ class Engine final : public EngineBase {
   };
   dcsc_cuda_opts o_;
   dcsc_solver_config cfg_;
-  int N_, K_, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1;
+  int N_, K_, J_ = 1, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1;
   cudaStream_t st_ = nullptr;
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_;
-  std::vector<double> dict_, mu_, xnorm2_, xs_host_;
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_, ginv_, what_;
+  std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
+  C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
+  C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel
   std::vector<int> live_h_;
   std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero
   void* xstage_ = nullptr;    // pinned staging of the signals (host -> device)
@@ -1553,6 +1659,7 @@ int dcsc_cuda_create(const dcsc_cuda_opts* opts, dcsc_cuda_ctx** out) {
       throw DimErr("filter support must fit inside the grid");
     if (opts->precision != 32 && opts->precision != 64) throw InvErr("precision must be 32 or 64");
     if (opts->cfg.normalize < 0 || opts->cfg.normalize > 2) throw InvErr("normalize must be 0, 1 or 2");
+    if (opts->channels < 0) throw InvErr("channel count must be >= 0");
     auto* c = new dcsc_cuda_ctx;
     try {
       c->eng = make_engine(*opts);

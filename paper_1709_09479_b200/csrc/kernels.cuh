@@ -47,6 +47,11 @@ struct CodingArgs {
   cx<R>* lamhat_w;      // N x NB
   struct ImageAdmm* img;
   int iter, is_last;
+  // multi-channel (TCSC, J > 1) passes: dhat is J x K x NB (channel-major),
+  // lamhat N x J x NB; the pass stores w_hat_k to what (N x K x NB) instead of
+  // accumulating, and the per-bin J x J solve runs in tc_lambda.
+  int J;
+  cx<R>* what;
 };
 
 // Bulk prefetch of a contiguous global range into L2 (sm_90+ TMA engine op).
@@ -125,7 +130,11 @@ struct Smem {
 //                                              (lambda_from_w numerator, coding.cpp:25-37)
 // The last CTA of each image runs the stop test and the lambda_hat update.
 // ----------------------------------------------------------------------------
-template <class P, int MODE>
+// TC (multi-channel, J > 1, tcsc.cpp:121-171): t_hat_k = sum_j conj(d_hat_jk)
+// lambda_hat_j in the generator, w_hat_k stored to a.what by the last forward
+// column stage, and the epilogue only runs the stop test (tc_lambda solves
+// the per-bin J x J systems).
+template <class P, int MODE, bool TC = false>
 __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a) {
   using R = typename P::R;
   using C = typename P::C;
@@ -136,7 +145,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   C* B1 = B0 + NB;
   C* TW = B1 + NB;
   C* COL0 = TW + P::TW_LEN;
-  constexpr bool STAGE = (MODE == kPassAdmm) && Smem<P>::stage_u;
+  constexpr bool STAGE = (MODE == kPassAdmm) && !TC && Smem<P>::stage_u;
   constexpr int US = Smem<P>::US;
   C* U = reinterpret_cast<C*>(smem_raw + Smem<P>::u_off);
   __shared__ __align__(8) unsigned long long ubar_s;
@@ -145,7 +154,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   const int n = blockIdx.y, g = blockIdx.x;
   if (MODE == kPassAdmm && a.conv[n]) return;
 
-  constexpr bool LAMS = (MODE == kPassAdmm) && Smem<P>::lam_smem;
+  constexpr bool LAMS = (MODE == kPassAdmm) && !TC && Smem<P>::lam_smem;
   C* LAM = reinterpret_cast<C*>(smem_raw + Smem<P>::u_off);
   // With lambda_hat in smem, the t_hat stage's only global operand is d_hat:
   // each filter's d_hat plane is staged into the free plane buffer by one TMA
@@ -189,6 +198,17 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
   const int k0 = g * a.kpg;
   const int k1 = min(a.K, k0 + a.kpg);
+  // TC: forward column pass of the row FFTs in z, natural bins of w_hat_k -> a.what
+  auto store_what = [&](C* z, C* other, int k) {
+    C* wk = a.what + ((size_t)n * a.K + k) * NB;
+    P::cols_fwd(z, other, TW, COL0, [](int, int) { return 0; }, [&](int r, int c, C v, int) { wk[r * Wh + c] = v; });
+    if (threadIdx.x < H) {
+      C x0, xn;
+      P::template unpack_col0<1>(COL0, threadIdx.x, x0, xn);
+      wk[threadIdx.x * Wh] = x0;
+      wk[threadIdx.x * Wh + M] = xn;
+    }
+  };
   for (int k = k0; k < k1; ++k) {
     const C* __restrict__ dk = a.dhat + (size_t)k * NB;
     C* work;
@@ -207,7 +227,16 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       }
       if (threadIdx.x == 0 && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       C* cs;
-      if constexpr (PREF) {
+      if constexpr (TC) {
+        const int J = a.J;
+        cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
+          const int b = r * Wh + c;
+          C t = mk<C>(R(0), R(0));
+          for (int j = 0; j < J; ++j)
+            t = cadd(t, cmulc(__ldg(a.dhat + ((size_t)j * a.K + k) * NB + b), __ldg(a.lamhat + ((size_t)n * J + j) * NB + b)));
+          return t;
+        });
+      } else if constexpr (PREF) {
         mbar_wait(dbar, dphase);
         dphase ^= 1u;
         const C* sd = stg;
@@ -286,6 +315,10 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
         }
       }
       C* z = P::rows_fwd_tail(fout, hin, TW);
+      if constexpr (TC) {
+        store_what(z, z == B0 ? B1 : B0, k);
+        continue;
+      }
       P::cols_fwd_acc(z, z == B0 ? B1 : B0, TW, COL0, dk, acc, [&](C* freebuf) {
         if constexpr (PREF) {
           if (threadIdx.x < H) {
@@ -341,6 +374,10 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     // forward r2c of w with acc += d_hat_k w_hat_k fused into the last column stage
     C* other = (work == B0) ? B1 : B0;
     C* z = P::rows_fwd(work, other, TW);
+    if constexpr (TC) {
+      store_what(z, z == work ? other : work, k);
+      continue;
+    }
     P::cols_fwd_acc(z, z == work ? other : work, TW, COL0, dk, acc, [](C*) {});
     static_assert(H <= T, "column-0 owners: one thread per row");
     if (threadIdx.x < H) {
@@ -352,7 +389,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     }
   }
   if (STAGE && threadIdx.x == 0) bulk_wait0();  // u stores complete before the CTA retires
-  {
+  if constexpr (!TC) {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
 #pragma unroll
     for (int i = 0; i < P::LAST_IPT; ++i) {
@@ -421,7 +458,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
         }
       }
     }
-    if (stop || (MODE == kPassAdmm && a.is_last)) return;
+    if (TC || stop || (MODE == kPassAdmm && a.is_last)) return;
     const R inv_rho = R(1) / rho;
     const C* pn = a.part + (size_t)n * a.G * NB;
     for (int b = threadIdx.x; b < NB; b += T) {

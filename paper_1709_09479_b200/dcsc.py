@@ -57,7 +57,7 @@ class _Opts(C.Structure):
     _fields_ = [
         ("n_images", C.c_int), ("height", C.c_int), ("width", C.c_int), ("filters", C.c_int),
         ("support_h", C.c_int), ("support_w", C.c_int), ("precision", C.c_int), ("device", C.c_int),
-        ("cfg", _SolverConfig),
+        ("cfg", _SolverConfig), ("channels", C.c_int),
     ]
 
 
@@ -211,15 +211,16 @@ class Context:
     """Device-resident CSC state (the opaque dcsc_cuda_ctx)."""
 
     def __init__(self, n_images: int, grid: tuple[int, int], filters: int, support: tuple[int, int],
-                 cfg: SolverConfig | None = None, precision: int = 64, device: int = 0):
+                 cfg: SolverConfig | None = None, precision: int = 64, device: int = 0, channels: int = 1):
         self.cfg = cfg or SolverConfig()
         self.N, (self.H, self.W), self.K = n_images, grid, filters
+        self.J = max(1, int(channels))
         self.mh, self.mw = support
         self.D = self.H * self.W
         self.M = self.mh * self.mw
         self.precision = precision
         o = _Opts(n_images, grid[0], grid[1], filters, support[0], support[1], precision, device,
-                  self.cfg.c())
+                  self.cfg.c(), self.J)
         h = C.c_void_p()
         _err(lib().dcsc_cuda_create(C.byref(o), C.byref(h)))
         self._h = h
@@ -244,21 +245,27 @@ class Context:
     # -- data
     def set_signals(self, xs):
         xs = _f64(xs)
-        assert xs.size == self.N * self.D
+        assert xs.size == self.N * self.J * self.D
         _err(lib().dcsc_cuda_set_signals(self._h, _dp(xs)))
 
+    def _sig_shape(self, lead):
+        return lead + ((self.J,) if self.J > 1 else ()) + (self.H, self.W)
+
     def get_signals(self):
-        out = np.zeros((self.N, self.H, self.W))
+        out = np.zeros(self._sig_shape((self.N,)))
         _err(lib().dcsc_cuda_get_signals(self._h, _dp(out)))
         return out
 
     def set_dictionary(self, d):
         d = _f64(d)
-        assert d.size == self.K * self.M
+        assert d.size == self.K * self.J * self.M
         _err(lib().dcsc_cuda_set_dictionary(self._h, _dp(d)))
 
+    def _dict_shape(self):
+        return (self.K,) + ((self.J,) if self.J > 1 else ()) + (self.mh, self.mw)
+
     def get_dictionary(self):
-        out = np.zeros((self.K, self.mh, self.mw))
+        out = np.zeros(self._dict_shape())
         _err(lib().dcsc_cuda_get_dictionary(self._h, _dp(out)))
         return out
 
@@ -276,7 +283,7 @@ class Context:
         cnt = n1 - n0
         th = np.zeros((cnt, self.K, self.H, self.W))
         z = np.zeros_like(th)
-        lam = np.zeros((cnt, self.H, self.W))
+        lam = np.zeros(self._sig_shape((cnt,)))
         _err(lib().dcsc_cuda_get_coding_state(self._h, n0, n1, _dp(th), _dp(z), _dp(lam)))
         return th, z, lam
 
@@ -302,13 +309,13 @@ class Context:
         _err(lib().dcsc_cuda_set_learning_state(self._h, _dp(g), _dp(m)))
 
     def get_learning_state(self):
-        g = np.zeros((self.N, self.H, self.W))
+        g = np.zeros(((self.J,) if self.J > 1 else ()) + (self.N, self.H, self.W))
         m = np.zeros(self.K)
         _err(lib().dcsc_cuda_get_learning_state(self._h, _dp(g), _dp(m)))
         return g, m
 
     def learning(self):
-        d = np.zeros((self.K, self.mh, self.mw))
+        d = np.zeros(self._dict_shape())
         st = LearningStats()
         _err(lib().dcsc_cuda_learning(self._h, _dp(d), C.byref(st)))
         return d, st.asdict()
@@ -406,7 +413,7 @@ def solve_coding(x, d, cfg: SolverConfig, state: CodingDualState | None = None, 
     x = _f64(x)
     d = _f64(d)
     if x.ndim != 2:
-        raise DimensionError("solve_coding expects a single-channel 2-D signal; use the TCSC path")
+        raise DimensionError("solve_coding expects a single-channel 2-D signal; use solve_coding_tcsc")
     K, mh, mw = d.shape
     H, W = x.shape
     if mh > H or mw > W:
@@ -423,15 +430,40 @@ def solve_coding(x, d, cfg: SolverConfig, state: CodingDualState | None = None, 
     return z[0].copy(), CodingDualState(th[0], z[0], lam[0]), stats
 
 
+def solve_coding_tcsc(x, d, cfg: SolverConfig, state: CodingDualState | None = None, precision: int = 64):
+    """solve_coding_tcsc (tcsc.cpp:211-230) for one J-channel image x (J,H,W)
+    with d (K,J,mh,mw); returns (maps, state, stats). lambda is (J,H,W)."""
+    x = _f64(x)
+    d = _f64(d)
+    if x.ndim != 3 or d.ndim != 4 or d.shape[1] != x.shape[0]:
+        raise DimensionError("solve_coding_tcsc: signal and dictionary channel counts differ")
+    J, H, W = x.shape
+    K, _, mh, mw = d.shape
+    if mh > H or mw > W:
+        raise DimensionError("filter support larger than the signal grid")
+    c = SolverConfig(**{**cfg.__dict__, "normalize": 0})
+    with Context(1, (H, W), K, (mh, mw), c, precision, channels=J) as ctx:
+        ctx.set_signals(x[None])
+        ctx.set_dictionary(d)
+        state = state or CodingDualState()
+        if state.initialized():
+            ctx.set_coding_state(state.theta[None], state.z[None])
+        stats = ctx.coding()[0]
+        th, z, lam = ctx.get_coding_state()
+    lam = lam[0].reshape(J, H, W)
+    return z[0].copy(), CodingDualState(th[0], z[0], lam), stats
+
+
 def solve_learning(xs, maps, support, cfg: SolverConfig, state: LearningDualState | None = None,
                    precision: int = 64):
     """solve_learning (learning.cpp:227-355); returns (dictionary, state, stats)."""
     xs = _f64(xs)
     maps = _f64(maps)
-    N, H, W = xs.shape
+    J = xs.shape[1] if xs.ndim == 4 else 1
+    N, H, W = xs.shape[0], xs.shape[-2], xs.shape[-1]
     K = maps.shape[1]
     c = SolverConfig(**{**cfg.__dict__, "normalize": 0})
-    with Context(N, (H, W), K, tuple(support), c, precision) as ctx:
+    with Context(N, (H, W), K, tuple(support), c, precision, channels=J) as ctx:
         ctx.set_signals(xs)
         ctx.set_maps(maps)
         state = state or LearningDualState()
@@ -444,22 +476,26 @@ def solve_learning(xs, maps, support, cfg: SolverConfig, state: LearningDualStat
 
 
 def evaluate_objective(x, d, z, beta, precision: int = 64):
-    """evaluate_objective (objective.cpp:59-81) -> (data, l1, total, residual_norm)."""
+    """evaluate_objective (objective.cpp:59-81) -> (data, l1, total, residual_norm).
+    J-channel: x (J,H,W), d (K,J,mh,mw)."""
     x = _f64(x)
     d = _f64(d)
-    K, mh, mw = d.shape
-    H, W = x.shape
-    with Context(1, (H, W), K, (mh, mw), SolverConfig(beta=beta, normalize=0), precision) as ctx:
+    J = x.shape[0] if x.ndim == 3 else 1
+    K, mh, mw = d.shape[0], d.shape[-2], d.shape[-1]
+    H, W = x.shape[-2], x.shape[-1]
+    with Context(1, (H, W), K, (mh, mw), SolverConfig(beta=beta, normalize=0), precision, channels=J) as ctx:
         ctx.set_signals(x[None])
         ctx.set_maps(_f64(z)[None])
         return ctx.objective(d)[0]
 
 
 def run_csc(xs, filters: int, support, cfg: SolverConfig, precision: int = 64):
-    """run_csc (pipeline.cpp:158-301): returns dict(trace, dict, maps, converged)."""
+    """run_csc (pipeline.cpp:158-301): returns dict(trace, dict, maps, converged).
+    xs (N,H,W) or (N,J,H,W); J > 1 is the Joint channel mode (TCSC)."""
     xs = _f64(xs)
-    N, H, W = xs.shape
-    with Context(N, (H, W), filters, tuple(support), cfg, precision) as ctx:
+    J = xs.shape[1] if xs.ndim == 4 else 1
+    N, H, W = xs.shape[0], xs.shape[-2], xs.shape[-1]
+    with Context(N, (H, W), filters, tuple(support), cfg, precision, channels=J) as ctx:
         ctx.set_signals(xs)
         trace, conv = ctx.run(cfg.max_outer)
         return {"trace": trace, "dict": ctx.get_dictionary(), "maps": ctx.get_maps(),

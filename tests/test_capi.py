@@ -68,3 +68,9 @@ def test_synth_images_independent_of_batch():
     xa, _ = dcsc.synth_generate(4, (16, 16), 2, 3, 0.1, 0.01, 5, False)
     xb, _ = dcsc.synth_generate(2, (16, 16), 2, 3, 0.1, 0.01, 5, False)
     assert np.array_equal(xa[:2], xb)
+
+
+def test_channel_count_is_validated_before_touching_the_device():
+    # J > 8 is rejected by the engine constructor (DimensionError) on any host
+    with pytest.raises(dcsc.DimensionError):
+        dcsc.Context(2, (20, 20), 4, (5, 5), dcsc.SolverConfig(normalize=0), 64, channels=9)
