@@ -47,6 +47,9 @@ CONFIGS = {
                max_admm=500, outer=20),
     "c3": dict(N=512, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=False,
                max_admm=500, outer=10),
+    # C1 with J = 3 channels (Joint mode / TCSC; not a BASELINE config)
+    "c1j3": dict(N=256, H=128, W=128, K=64, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
+                 max_admm=50, outer=1, J=3),
     # C3-shaped slice for profiling only (not a BASELINE config)
     "c3s": dict(N=16, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
                 max_admm=10, outer=1),
@@ -128,19 +131,33 @@ def dist_env():
 
 
 def make_data(cfg, n0, n1):
+    """Seeded synthetic signals of the config's shape. J > 1: channel j is the
+    generator's output for seed SEED + j; the dictionary is the channel stack of
+    the per-channel ground truths, jointly renormalised to unit filters."""
     from paper_1709_09479_b200 import dcsc
-    x, d_true = dcsc.synth_generate(cfg["N"], (cfg["H"], cfg["W"]), cfg["K"], cfg["m"], cfg["p"], cfg["sigma"],
-                                    SEED, cfg["prec"] == 32)
-    return x[n0:n1].copy(), d_true
+    J = cfg.get("J", 1)
+    xs, ds = [], []
+    for j in range(J):
+        x, d_true = dcsc.synth_generate(cfg["N"], (cfg["H"], cfg["W"]), cfg["K"], cfg["m"], cfg["p"],
+                                        cfg["sigma"], SEED + j, cfg["prec"] == 32)
+        xs.append(x[n0:n1])
+        ds.append(d_true)
+    if J == 1:
+        return xs[0].copy(), ds[0]
+    d = np.stack(ds, axis=1)
+    d /= np.sqrt((d ** 2).sum(axis=(1, 2, 3), keepdims=True))
+    return np.ascontiguousarray(np.stack(xs, axis=1)), d
 
 
 def coding_bytes(cfg, n_img):
-    """per ADMM iteration B = n*(4 K D s + Dh 2s) + K Dh 2s."""
+    """per ADMM iteration B = n*(4 K D s + J Dh 2s) + J K Dh 2s
+    (J = 1 at the BASELINE configs)."""
     s = 4 if cfg["prec"] == 32 else 8
     D = cfg["H"] * cfg["W"]
     Dh = cfg["H"] * (cfg["W"] // 2 + 1)
     K = cfg["K"]
-    return n_img * (4 * K * D * s + Dh * 2 * s) + K * Dh * 2 * s
+    J = cfg.get("J", 1)
+    return n_img * (4 * K * D * s + J * Dh * 2 * s) + J * K * Dh * 2 * s
 
 
 def traffic_from_profiles(name):
@@ -159,7 +176,10 @@ def ref_sample_coding(cfg, x, d, threads, admm_cap):
     n_img = min(len(x), max(threads, 1))
     c = ref.Cfg(beta=cfg["beta"], max_admm=admm_cap, normalize=0)
     t0 = time.perf_counter()
-    iters, _ = ref.coding_batch(x[:n_img], d, c)
+    if cfg.get("J", 1) > 1:
+        iters, _ = ref.coding_batch_j(x[:n_img], d, c)
+    else:
+        iters, _ = ref.coding_batch(x[:n_img], d, c)
     dt = time.perf_counter() - t0
     # per-image ADMM iterations cost the same from a cold start; scale to N images x max_admm
     full = dt * (cfg["N"] * cfg["max_admm"]) / max(int(iters.sum()), 1)
@@ -246,11 +266,13 @@ def config_block(cfg, args):
     name = args.config
     wl = (f"{name.upper()}: N={cfg['N']} images {cfg['H']}x{cfg['W']} FP{cfg['prec']}, K={cfg['K']} filters "
           f"{cfg['m']}x{cfg['m']}, beta={cfg['beta']}, rho=0.1, ")
+    if cfg.get("J", 1) > 1:
+        wl += f"J={cfg['J']} channels (Joint mode, TCSC), "
     if cfg["coding_only"]:
         wl += f"coding only, fixed ground-truth dictionary, {cfg['max_admm']} ADMM iters, cold start"
     else:
         wl += "coding+learning outer iteration of run_csc from init_variables"
-    return {"workload": wl, "images": cfg["N"], "filters": cfg["K"], "grid": [cfg["H"], cfg["W"]],
+    return {"workload": wl, "images": cfg["N"], "channels": cfg.get("J", 1), "filters": cfg["K"], "grid": [cfg["H"], cfg["W"]],
             "support": [cfg["m"], cfg["m"]], "precision": f"fp{cfg['prec']}", "parallelism": f"images sharded x{args.gpus}",
             "l2": "inputs larger than L2 (ADMM state u = N*K*D*s)", "seed": SEED}
 
@@ -272,7 +294,7 @@ def run_ours(args, cfg):
     nl = n1 - n0
     sc = dcsc.SolverConfig(beta=cfg["beta"], max_admm=cfg["max_admm"], normalize=0, seed=SEED, tol=1e-300)
     ctx = dcsc.Context(nl, (cfg["H"], cfg["W"]), cfg["K"], (cfg["m"], cfg["m"]), sc, cfg["prec"],
-                       device=local if world > 1 else 0)
+                       device=local if world > 1 else 0, channels=cfg.get("J", 1))
     if world > 1 and not cfg["coding_only"]:
         # learning sums its K x NB correlations and CG scalars over ranks (NCCL)
         import torch
@@ -337,7 +359,7 @@ def run_ours(args, cfg):
         e2e_s = float(t.item())
     e2e = e2e_steps / e2e_s
     s = 4 if cfg["prec"] == 32 else 8
-    h2d = nl * cfg["H"] * cfg["W"] * s
+    h2d = nl * cfg.get("J", 1) * cfg["H"] * cfg["W"] * s
     admm_max = max(st["admm_iters"] for st in stats) if cfg["coding_only"] else 0
     d2h = nl * (56 + 40) + nl * 4 * max(admm_max, 1)
 

@@ -355,3 +355,18 @@ def run_csc_j(xs, K, support, cfg: Cfg):
                                _p(dfin), _p(maps)))
     trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(n_rows.value)]
     return {"trace": trace, "dict": dfin, "maps": maps}
+
+
+def coding_batch_j(xs, d, cfg: Cfg, want_maps=False):
+    """solve_coding_tcsc over J-channel images xs (N,J,H,W), d (K,J,mh,mw), OpenMP over images."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    N, J, H, W = xs.shape
+    K, _, mh, mw = d.shape
+    iters = np.zeros(N, dtype=np.int32)
+    maps = np.zeros((N, K, H, W)) if want_maps else None
+    c = cfg.c()
+    _check(lib().ref_coding_batch_j(N, H, W, J, _p(xs), K, mh, mw, _p(d), C.byref(c),
+                                    _p(maps) if want_maps else None,
+                                    iters.ctypes.data_as(C.POINTER(C.c_int))))
+    return iters, maps

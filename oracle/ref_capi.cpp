@@ -297,6 +297,30 @@ int ref_coding_batch(int N, int H, int W, const double* xs, int K, int mh, int m
   });
 }
 
+// solve_coding_tcsc over N J-channel images (xs N*J*D, d K*J*M) from the empty
+// state, OpenMP-parallel over images (pipeline.cpp:221-227, Joint mode).
+int ref_coding_batch_j(int N, int H, int W, int J, const double* xs, int K, int mh, int mw,
+                       const double* d, const ref_cfg* cfg, double* maps_out, int* iters_out) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    const Dictionary dict = make_dict(K, mh, mw, d, J);
+    const SolverConfig sc = to_cfg(cfg);
+    std::vector<SignalTensor> sig;
+    for (int n = 0; n < N; ++n) sig.push_back(make_signal(H, W, xs + n * J * D, J));
+    std::vector<SparseMaps> out(N);
+    std::vector<CodingStats> st(N);
+    std::vector<CodingDualState> state(N);
+    par::parallel_for(N, [&](std::int64_t n) {
+      out[n] = J > 1 ? solve_coding_tcsc(sig[n], dict, sc, state[n], &st[n])
+                     : solve_coding(sig[n], dict, sc, state[n], &st[n]);
+    });
+    for (int n = 0; n < N; ++n) {
+      if (iters_out) iters_out[n] = st[n].admm_iters;
+      if (maps_out) std::copy(out[n].values.begin(), out[n].values.end(), maps_out + n * K * D);
+    }
+  });
+}
+
 // One solve_learning call over N J-channel images (xs N*J*D). gamma (J*N*D,
 // channel-major) / mu (K) are in/out warm state; warm = 0 starts from the
 // empty state. d_out receives K*J*M values.
