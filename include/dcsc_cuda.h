@@ -27,6 +27,7 @@
  *                                   channels > 1: solve_learning_tcsc (tcsc.hpp:62-68)
  *   dcsc_cuda_objective             dcsc::evaluate_objective (objective.hpp:14-15)
  *   dcsc_cuda_learning_data_term    dcsc::learning_data_term (objective.hpp:18-19)
+ *   dcsc_cuda_reconstruct           dcsc::reconstruct (objective.hpp:11)
  *   dcsc_cuda_learning_apply        dcsc::LearningOperator::apply (learning.hpp:57)
  *   dcsc_cuda_run                   dcsc::run_csc (pipeline.hpp:58) + trace rows
  *                                   (types.hpp:122-136, trace_io.hpp)
@@ -144,6 +145,10 @@ int dcsc_cuda_get_learning_state(dcsc_cuda_ctx* ctx, double* gamma, double* mu);
 /* solve_learning over all images' maps; writes the candidate dictionary
  * (K*mh*mw) to d_out without installing it */
 int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* stats);
+/* reconstruct (objective.cpp:39-57) of the accepted maps of images [n0, n1)
+ * with dictionary d (K*J*M; NULL = the context dictionary): out (n1-n0)*J*D.
+ * GPU side of the reference CLI's `reconstruct` / `encode` (csc_main.cpp:147-202) */
+int dcsc_cuda_reconstruct(dcsc_cuda_ctx* ctx, const double* d, int n0, int n1, double* out);
 /* LearningOperator::apply with the given mu on N*D vectors */
 int dcsc_cuda_learning_apply(dcsc_cuda_ctx* ctx, const double* mu, const double* v, double* out);
 
@@ -205,6 +210,9 @@ int dcsc_io_read_trace_csv(const char* path, dcsc_trace_row* rows, int max_rows,
 /* synthetic BASELINE data (host only, no GPU): x N*H*W, d_true K*m*m */
 int dcsc_synth_generate(int n_images, int height, int width, int filters, int m, double p,
                         double sigma, uint64_t seed, int round_fp32, double* x, double* d_true);
+/* the reference bench harness's dataset (bench.cpp:9-21): uniform [0,1) values
+ * from one mt19937_64(seed), N*J*H*W doubles */
+int dcsc_synth_dataset(int n_images, int channels, int height, int width, uint64_t seed, double* x);
 
 #ifdef __cplusplus
 }

@@ -370,3 +370,15 @@ def coding_batch_j(xs, d, cfg: Cfg, want_maps=False):
                                     _p(maps) if want_maps else None,
                                     iters.ctypes.data_as(C.POINTER(C.c_int))))
     return iters, maps
+
+
+def reconstruct(d, z):
+    """reconstruct (objective.cpp:39-57): d (K,mh,mw) or (K,J,mh,mw), z (K,H,W)."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    J = d.shape[1] if d.ndim == 4 else 1
+    K, mh, mw = d.shape[0], d.shape[-2], d.shape[-1]
+    _, H, W = z.shape
+    out = np.zeros((J, H, W))
+    _check(lib().ref_reconstruct_j(H, W, J, K, mh, mw, _p(d), _p(z), _p(out)))
+    return out if d.ndim == 4 else out[0]

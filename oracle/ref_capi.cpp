@@ -376,6 +376,17 @@ int ref_objective_j(int H, int W, int J, const double* x, int K, int mh, int mw,
   });
 }
 
+// reconstruct (objective.cpp:39-57): out J*D from d (K*J*M) and maps z (K*D)
+int ref_reconstruct_j(int H, int W, int J, int K, int mh, int mw, const double* d, const double* z,
+                      double* out) {
+  return guarded([&] {
+    SparseMaps m(K, {H, W});
+    std::copy(z, z + m.values.size(), m.values.begin());
+    const SignalTensor r = reconstruct(make_dict(K, mh, mw, d, J), m);
+    std::copy(r.values.begin(), r.values.end(), out);
+  });
+}
+
 int ref_objective(int H, int W, const double* x, int K, int mh, int mw, const double* d,
                   const double* z, double beta, double* out) {
   return ref_objective_j(H, W, 1, x, K, mh, mw, d, z, beta, out);

@@ -282,6 +282,7 @@ class EngineBase {
   virtual void learning_apply(const double* mu, const double* v, double* out) = 0;
   virtual void objective(const double* d, dcsc_objective* per_image) = 0;
   virtual void learning_data_term(const double* d, double* data) = 0;
+  virtual void reconstruct(const double* d, int n0, int n1, double* out) = 0;
   virtual void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) = 0;
   virtual void synchronize() = 0;
   virtual void set_profiling(int on) = 0;
@@ -1284,6 +1285,31 @@ class Engine final : public EngineBase {
     }
   }
 
+  // reconstruct (objective.cpp:39-57) of the accepted maps of images [n0, n1)
+  // with `d` (NULL = the context dictionary): out is (n1-n0) x J x D
+  void reconstruct(const double* d, int n0, int n1, double* out) override {
+    check_range(n0, n1);
+    const int cnt = n1 - n0;
+    const C* dh = dhat_.as<C>();
+    if (d) {
+      require_finite(d, (size_t)K_ * J_ * M_, "dictionary");
+      upload_dict_spectra(d, dcand_.as<C>());
+      dh = dcand_.as<C>();
+    }
+    coding_launch<kPassMaps>(dh, n0, cnt);
+    DevMem spec, sp;
+    spec.alloc(sizeof(C) * (size_t)cnt * J_ * NB);
+    sp.alloc(sizeof(double) * (size_t)cnt * J_ * D);
+    launch(kFamOther, [&] {
+      recon_spectrum<R><<<dim3((NB + 255) / 256, cnt), 256, 0, st_>>>(
+          part_.as<C>() + (size_t)n0 * G_ * NB, what_.as<C>() ? what_.as<C>() + (size_t)n0 * K_ * NB : nullptr, dh,
+          spec.as<C>(), J_, K_, G_, NB);
+    });
+    c2r<double>(spec.as<C>(), NB, sp.as<double>(), D, cnt * J_);
+    CK(cudaMemcpyAsync(out, sp.p, sp.bytes, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
   // run_csc (pipeline.cpp:158-301) from init_variables
   void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) override {
     *n_rows = 0;
@@ -1744,6 +1770,13 @@ int dcsc_cuda_learning_data_term(dcsc_cuda_ctx* ctx, const double* d, double* da
   CTX_CHECK
   return guarded([&] { ctx->eng->learning_data_term(d, data); });
 }
+int dcsc_cuda_reconstruct(dcsc_cuda_ctx* ctx, const double* d, int n0, int n1, double* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw InvErr("null argument");
+    ctx->eng->reconstruct(d, n0, n1, out);
+  });
+}
+
 int dcsc_cuda_run(dcsc_cuda_ctx* ctx, int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) {
   CTX_CHECK
   return guarded([&] { ctx->eng->run(max_outer, rows, n_rows, converged); });

@@ -95,3 +95,14 @@ extern "C" int dcsc_synth_generate(int N, int H, int W, int K, int m, double p, 
   }
   return DCSC_OK;
 }
+
+// The reference bench harness's dataset (bench.cpp:9-21): one mt19937_64
+// seeded with `seed`, values u = (rng() >> 11) * 2^-53 in [0, 1), drawn image
+// by image in row-major order. x: N*J*H*W.
+extern "C" int dcsc_synth_dataset(int N, int J, int H, int W, std::uint64_t seed, double* x) {
+  if (N < 1 || J < 1 || H < 1 || W < 1 || !x) return DCSC_ERR_DIMENSION;
+  std::mt19937_64 rng(seed);
+  const std::size_t total = (std::size_t)N * J * H * W;
+  for (std::size_t i = 0; i < total; ++i) x[i] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+  return DCSC_OK;
+}

@@ -141,4 +141,28 @@ __global__ void tc_objective(const cx<R>* __restrict__ what, const cx<R>* __rest
   }
 }
 
+// Reconstruction spectrum y_n,j = sum_k d_hat_jk z_hat_nk (objective.cpp:39-57 in
+// the Fourier basis): J = 1 sums the coding pass's G group partials (fixed
+// order), J > 1 contracts the stored z_hat planes. out: N x J x NB.
+template <class R>
+__global__ void recon_spectrum(const cx<R>* __restrict__ part, const cx<R>* __restrict__ what,
+                               const cx<R>* __restrict__ dhat, cx<R>* __restrict__ out, int J, int K, int G, int NB) {
+  using C = cx<R>;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = blockIdx.y;
+  if (b >= NB) return;
+  if (J == 1) {
+    C acc = part[((size_t)n * G) * NB + b];
+    for (int g = 1; g < G; ++g) acc = cadd(acc, part[((size_t)n * G + g) * NB + b]);
+    out[(size_t)n * NB + b] = acc;
+    return;
+  }
+  for (int j = 0; j < J; ++j) {
+    C acc = mk<C>(R(0), R(0));
+    for (int k = 0; k < K; ++k)
+      acc = cadd(acc, cmul(dhat[((size_t)j * K + k) * NB + b], what[((size_t)n * K + k) * NB + b]));
+    out[((size_t)n * J + j) * NB + b] = acc;
+  }
+}
+
 }  // namespace dcsc_cuda

@@ -135,7 +135,8 @@ EXPORTS = [
     "dcsc_cuda_event_elapsed", "dcsc_cuda_device_bytes", "dcsc_synth_generate",
     "dcsc_cuda_nccl_unique_id", "dcsc_cuda_set_comm_nccl", "dcsc_cuda_set_comm_callback",
     "dcsc_io_last_error", "dcsc_io_write_tensor", "dcsc_io_read_tensor_header", "dcsc_io_read_tensor",
-    "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing",
+    "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing", "dcsc_cuda_reconstruct",
+    "dcsc_synth_dataset",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -339,6 +340,14 @@ class Context:
         _err(lib().dcsc_cuda_learning_data_term(self._h, _dp(dd), C.byref(v)))
         return v.value
 
+    def reconstruct(self, d=None, n0=0, n1=None):
+        """dcsc::reconstruct (objective.cpp:39-57) of the accepted maps of images [n0, n1)."""
+        n1 = self.N if n1 is None else n1
+        out = np.zeros(self._sig_shape((n1 - n0,)))
+        dd = None if d is None else _f64(d)
+        _err(lib().dcsc_cuda_reconstruct(self._h, _dp(dd), n0, n1, _dp(out)))
+        return out
+
     def run(self, max_outer: int):
         rows = (TraceRow * (2 * max(max_outer, 1)))()
         n = C.c_int()
@@ -489,6 +498,40 @@ def evaluate_objective(x, d, z, beta, precision: int = 64):
         return ctx.objective(d)[0]
 
 
+def reconstruct(d, z, precision: int = 64):
+    """reconstruct (objective.cpp:39-57): one image from maps z (K,H,W) and a
+    dictionary d (K,mh,mw) or (K,J,mh,mw); returns (H,W) or (J,H,W)."""
+    d = _f64(d)
+    z = _f64(z)
+    J = d.shape[1] if d.ndim == 4 else 1
+    K, mh, mw = d.shape[0], d.shape[-2], d.shape[-1]
+    if z.shape[0] != K:
+        raise DimensionError("dictionary and maps disagree on the filter count")
+    H, W = z.shape[-2], z.shape[-1]
+    with Context(1, (H, W), K, (mh, mw), SolverConfig(normalize=0), precision, channels=J) as ctx:
+        ctx.set_maps(z[None])
+        return ctx.reconstruct(d)[0]
+
+
+def encode(x, d, cfg: SolverConfig, precision: int = 64):
+    """The reference CLI's `encode` (csc_main.cpp:147-172) on the GPU: normalise
+    x per cfg.normalize, code it (TCSC when d has J > 1 channels), evaluate the
+    objective. Returns (maps, objective (data, l1, total, residual), stats)."""
+    x = _f64(x)
+    d = _f64(d)
+    J = d.shape[1] if d.ndim == 4 else 1
+    K, mh, mw = d.shape[0], d.shape[-2], d.shape[-1]
+    H, W = x.shape[-2], x.shape[-1]
+    with Context(1, (H, W), K, (mh, mw), cfg, precision, channels=J) as ctx:
+        ctx.set_signals(x[None])
+        ctx.set_dictionary(d)
+        stats = ctx.coding()[0]
+        _, z, _ = ctx.get_coding_state()
+        ctx.set_maps(z)
+        obj = ctx.objective()[0]
+    return z[0], obj, stats
+
+
 def run_csc(xs, filters: int, support, cfg: SolverConfig, precision: int = 64):
     """run_csc (pipeline.cpp:158-301): returns dict(trace, dict, maps, converged).
     xs (N,H,W) or (N,J,H,W); J > 1 is the Joint channel mode (TCSC)."""
@@ -538,6 +581,13 @@ def synth_generate(n_images, grid, filters, m, p, sigma, seed, round_fp32):
 
 
 # ---------------------------------------------------------------- on-disk formats
+def synth_dataset(n_images: int, channels: int, grid, seed: int) -> np.ndarray:
+    """synthetic_dataset (bench.cpp:9-21): (N, H, W) or (N, J, H, W) uniform [0, 1)."""
+    out = np.zeros((n_images, channels, grid[0], grid[1]))
+    _err(lib().dcsc_synth_dataset(n_images, channels, grid[0], grid[1], C.c_uint64(seed), _dp(out)))
+    return out if channels > 1 else out[:, 0]
+
+
 def _io(rc: int):
     if rc == 0:
         return

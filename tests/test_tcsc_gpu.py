@@ -132,3 +132,28 @@ def test_tcsc_run_fp64_matches_reference():
         for key in ("total", "data_term", "l1_term"):
             assert abs(a[key] - b[key]) <= 1e-8 * abs(b[key]), (a, b, key)
     assert rel(g["dict"], r["dict"]) <= 1e-7
+
+
+# ---------------------------------------------------------------- reconstruct / encode
+@pytest.mark.parametrize("J,prec,tol", [(1, 64, 1e-12), (3, 64, 1e-12), (1, 32, 2e-5), (3, 32, 2e-5)])
+def test_reconstruct_matches_reference(J, prec, tol):
+    rng = np.random.default_rng(J + prec)
+    K, m, grid = 5, 5, (20, 20)
+    d = rng.standard_normal((K, J, m, m)) if J > 1 else rng.standard_normal((K, m, m))
+    z = rng.standard_normal((K,) + grid) * (rng.random((K,) + grid) < 0.1)
+    assert rel(dcsc.reconstruct(d, z, precision=prec), ref.reconstruct(d, z)) <= tol
+
+
+def test_encode_matches_reference_cli_path():
+    x, d = problem(1, 3, (20, 20), 4, 5, seed=12)
+    cfg = dcsc.SolverConfig(beta=0.1, max_admm=200, normalize=1)
+    z, obj, st = dcsc.encode(x[0], d, cfg)
+    xn = dcsc.Context(1, (20, 20), 4, (5, 5), cfg, 64, channels=3)
+    xn.set_signals(x[0][None])
+    xnorm = xn.get_signals()[0]
+    xn.close()
+    z_r, _, s_r = ref.solve_coding_tcsc(xnorm, d, ref.Cfg(beta=0.1, max_admm=200, normalize=0))
+    assert st["admm_iters"] == s_r["admm_iters"]
+    assert rel(z, z_r) <= FP64_TOL
+    o_r = ref.objective_j(xnorm, d, z_r, 0.1)
+    assert abs(obj[2] - o_r[2]) <= FP64_TOL * abs(o_r[2])
