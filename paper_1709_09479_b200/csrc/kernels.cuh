@@ -195,7 +195,10 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
   C acc0 = mk<C>(R(0), R(0)), accN = mk<C>(R(0), R(0));  // bins (tid, 0), (tid, W/2)
 
   const R rho = a.rho, beta = a.beta, invD = R(1) / R(D);
-  double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
+  // per-thread stop-test sums over the CTA's filters, in the storage precision
+  // (FP32: <= 32 terms per filter x kpg filters per thread before the FP64 block
+  // reduction); Σdz² = ρ²·Σ(θ'−t)² and Σz'² = ρ²·Σ(z'/ρ)² are formed at the end
+  R s0 = 0, s1 = 0, s2 = 0, s4 = 0, s5 = 0, s6 = 0;
   const int k0 = g * a.kpg;
   const int k1 = min(a.K, k0 + a.kpg);
   // TC: forward column pass of the row FFTs in z, natural bins of w_hat_k -> a.what
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       {
         constexpr int RX = P::RX, J = M / RX;
         const C* twr = TW + P::TW_ROW;
-        R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
+        R& f0 = s0; R& f1 = s1; R& f2 = s2; R& f4 = s4; R& f5 = s5; R& f6 = s6;
 #pragma unroll 1
         for (int it = threadIdx.x; it < H * J; it += T) {
           const int r = it % H, j = it / H;
@@ -302,9 +305,6 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
 #pragma unroll
           for (int s = 0; s < RX; ++s) fout[r * Wh + j * RX + s] = x[s];
         }
-        const double rr = (double)rho * (double)rho;
-        s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += rr * (double)f0;
-        s4 += rr * (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
       }
       if constexpr (STAGE) fence_async_smem();
       __syncthreads();
@@ -360,11 +360,11 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
         } else if constexpr (MODE == kPassObjective) {
           w0 = rho * (fmin(fmax(v.x, -beta), beta) - v.x);
           w1 = rho * (fmin(fmax(v.y, -beta), beta) - v.y);
-          s0 += (double)fabs(w0) + (double)fabs(w1);
+          s0 += fabs(w0) + fabs(w1);
         } else {
           w0 = v.x;
           w1 = v.y;
-          s0 += (double)fabs(w0) + (double)fabs(w1);
+          s0 += fabs(w0) + fabs(w1);
         }
         B0[r * Wh + m] = mk<C>(w0, w1);
       }
@@ -408,9 +408,11 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     }
   }
   // reductions of the partial sums (FP64)
-  double v[7] = {s0, s1, s2, s3, s4, s5, 0.0};
+  const double rr2 = (double)rho * (double)rho;
+  double v[7] = {(double)s0, (double)s1, (double)s2, MODE == kPassAdmm ? rr2 * (double)s0 : 0.0,
+                 rr2 * (double)s4, (double)s5, 0.0};
   block_sum<T, 7>(v, red);
-  const double mx = block_max(s6, red, T);
+  const double mx = block_max((double)s6, red, T);
   if (threadIdx.x == 0) {
     double* o = a.sums + ((size_t)n * a.G + g) * kSums;
     for (int i = 0; i < 6; ++i) o[i] = v[i];
