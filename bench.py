@@ -11,8 +11,11 @@ full coding+learning outer iteration (run_csc) instead.
 value  = outer iterations/s with inputs resident in HBM (device events).
 e2e    = the same metric through the C-ABI with host buffers each step
          (signals h2d + coding + per-image stats d2h), host wall clock.
-Multi-GPU: one process per GPU; images are sharded across ranks (no data-path
-collective: the coding half-step has no exchange); max-over-ranks timing.
+Multi-GPU: one process per GPU, max-over-ranks device timing. Coding-only
+configs (C1 default) scale weakly: each rank codes its own N-image C1 workload
+(images are independent units; no data-path collective), value = world x
+steps / time. Full configs (--config c0/c2/c3/c4) split their N images over
+the ranks (strong scaling; learning all-reduces its correlations).
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libdcsc_ref.so, the unmodified reference solver TUs) on the
@@ -208,7 +211,8 @@ def run_reference(args, cfg):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if cfg["coding_only"] else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": config_block(cfg, args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -253,7 +257,8 @@ def run_reference_full(args, cfg, x, threads):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if cfg["coding_only"] else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": config_block(cfg, args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -273,7 +278,8 @@ def config_block(cfg, args):
     else:
         wl += "coding+learning outer iteration of run_csc from init_variables"
     return {"workload": wl, "images": cfg["N"], "channels": cfg.get("J", 1), "filters": cfg["K"], "grid": [cfg["H"], cfg["W"]],
-            "support": [cfg["m"], cfg["m"]], "precision": f"fp{cfg['prec']}", "parallelism": f"images sharded x{args.gpus}",
+            "support": [cfg["m"], cfg["m"]], "precision": f"fp{cfg['prec']}", "parallelism": (f"dp{args.gpus}: {cfg['N']} images per GPU (weak)" if cfg["coding_only"]
+                            else f"images sharded x{args.gpus} (strong)"),
             "l2": "inputs larger than L2 (ADMM state u = N*K*D*s)", "seed": SEED}
 
 
@@ -289,9 +295,20 @@ def run_ours(args, cfg):
         dist = tdist
     from paper_1709_09479_b200 import dcsc
     N = cfg["N"]
-    n0, n1 = dcsc.shard_range(N, world, rank)
-    x, d_true = make_data(cfg, n0, n1)
+    # Coding-only configs shard the independent units (images) with no
+    # collective: weak scaling, every rank codes its own N-image C1 workload
+    # (rank r takes images [r N, (r+1) N) of one seeded N*world-image dataset),
+    # so one step = `world` C1 outer iterations. Full configs (learning couples
+    # the images through all-reduces) keep the N images and split them.
+    weak = cfg["coding_only"]
+    if weak:
+        n0, n1 = rank * N, (rank + 1) * N
+        x, d_true = make_data(dict(cfg, N=N * world), n0, n1)
+    else:
+        n0, n1 = dcsc.shard_range(N, world, rank)
+        x, d_true = make_data(cfg, n0, n1)
     nl = n1 - n0
+    units = world if weak else 1  # C1-workload outer iterations per step, all ranks
     sc = dcsc.SolverConfig(beta=cfg["beta"], max_admm=cfg["max_admm"], normalize=0, seed=SEED, tol=1e-300)
     ctx = dcsc.Context(nl, (cfg["H"], cfg["W"]), cfg["K"], (cfg["m"], cfg["m"]), sc, cfg["prec"],
                        device=local if world > 1 else 0, channels=cfg.get("J", 1))
@@ -340,7 +357,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ctx.set_profiling(False)
-    value = args.steps / (ms / 1000.0)
+    value = units * args.steps / (ms / 1000.0)
 
     # e2e through the C-ABI with host buffers: signals h2d + solve + stats d2h each step
     e2e_steps = max(1, min(args.steps, 5))
@@ -357,7 +374,7 @@ def run_ours(args, cfg):
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = e2e_steps / e2e_s
+    e2e = units * e2e_steps / e2e_s
     s = 4 if cfg["prec"] == 32 else 8
     h2d = nl * cfg.get("J", 1) * cfg["H"] * cfg["W"] * s
     admm_max = max(st["admm_iters"] for st in stats) if cfg["coding_only"] else 0
@@ -368,7 +385,8 @@ def run_ours(args, cfg):
     peak, peak_kind = load_peaks()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak" if weak else "strong",
+        "vs_baseline": None,
         "dtype": "f32" if cfg["prec"] == 32 else "f64", "data": "synthetic (seeded BASELINE.json generator)",
         "config": config_block(cfg, args),
         "e2e": {"value": e2e * 1.0, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
