@@ -6,7 +6,7 @@ translation units + FFTW3 shim, built by oracle/Makefile) is run on the seeded
 BASELINE.json generator inputs. The GPU tests compare against these files, so
 they need neither the reference sources nor its build on the GPU box.
 
-usage: python tests/golden/make_golden.py [small|c1slice|c0|all]
+usage: python tests/golden/make_golden.py [small|c1slice|tcsc|c0|all]
 """
 import os
 import sys
@@ -62,6 +62,24 @@ def coding_case(name, N, grid, K, m, p, sigma, seed, fp32, beta, max_admm):
     print(f"{name}: {N} images")
 
 
+def tcsc_case(name, N, J, grid, K, m, p, sigma, seed, cfg):
+    """Joint channel mode (J > 1, the reference's TCSC path): channel j of the
+    signals is the generator's output for seed + j (as bench.py's J-channel data)."""
+    x = np.stack([dcsc.synth_generate(N, grid, K, m, p, sigma, seed + j, False)[0] for j in range(J)], axis=1)
+    ref.set_threads(0)
+    t0 = time.time()
+    r = ref.run_j(x, K, (m, m), cfg)
+    dt = time.time() - t0
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), x=x, trace=trace_array(r["trace"]),
+                        trace_keys=np.array(TRACE_KEYS), dicts=r["dicts"],
+                        maps_l0=np.array([(np.abs(r["maps"]) > 1e-12 * np.abs(r["maps"]).max()).sum()]),
+                        cfg=np.array([cfg.beta, cfg.rho, cfg.tol, cfg.max_outer, cfg.max_admm, cfg.max_mu_iters,
+                                      cfg.cg_tol, cfg.cg_max, cfg.mu_floor, cfg.seed, cfg.normalize]),
+                        shape=np.array([N, grid[0], grid[1], K, m, J]), gen=np.array([p, sigma, seed, 0]),
+                        seconds=np.array([dt]))
+    print(f"{name}: {len(r['trace'])} rows in {dt:.1f}s")
+
+
 def main(which):
     if which in ("small", "all"):
         run_case("run_small_fp64", 3, (20, 20), 6, 5, 0.05, 0.01, 7, False,
@@ -70,6 +88,9 @@ def main(which):
                  ref.Cfg(beta=0.5, max_outer=2, max_admm=200, normalize=0, seed=2, tol=1e-300))
     if which in ("c1slice", "all"):
         coding_case("coding_c1slice_fp32", 2, (128, 128), 64, 11, 0.01, 0.01, 20250917, True, 0.5, 50)
+    if which in ("tcsc", "all"):
+        tcsc_case("run_tcsc_j3_fp64", 3, 3, (20, 20), 6, 5, 0.05, 0.01, 7,
+                  ref.Cfg(beta=0.2, max_outer=3, max_admm=200, normalize=1, seed=11, tol=1e-300))
     if which in ("c0", "all"):
         # BASELINE.json configs[0]: N=10 100x100 FP64, K=100 11x11, beta=1.0, 10 outer iterations
         run_case("run_c0_fp64", 10, (100, 100), 100, 11, 0.01, 0.01, 20250917, False,

@@ -95,3 +95,17 @@ def test_golden_c0_fp64():
     check_trace(trace, g, 1e-9, exact_iters=True)
     dref = g["dicts"][-1]
     assert np.abs(d - dref).max() <= 1e-8 * np.abs(dref).max()
+
+
+def test_golden_tcsc_j3_fp64():
+    """Joint channel mode (J = 3) against the reference TCSC run: <= 1e-8, same iteration counts."""
+    g = load("run_tcsc_j3_fp64")
+    N, H, W, K, m, J = (int(v) for v in g["shape"])
+    x = g["x"]
+    with dcsc.Context(N, (H, W), K, (m, m), cfg_of(g), 64, channels=J) as ctx:
+        ctx.set_signals(x)
+        trace, _ = ctx.run(cfg_of(g).max_outer)
+        d = ctx.get_dictionary()
+    check_trace(trace, g, 1e-8, exact_iters=True)
+    dref = g["dicts"][-1]
+    assert np.abs(d - dref).max() <= 1e-7 * np.abs(dref).max()

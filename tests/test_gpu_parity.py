@@ -250,3 +250,46 @@ def test_run_with_normalisation_matches_reference(mode):
                                                      max_admm=120), precision=64)
     compare_runs(g, r, 1e-9)
     assert rel(g["dict"], r["dict"]) <= 1e-7
+
+
+# ---------------------------------------------------------------- edge cases
+def test_single_filter_and_full_support_fp64():
+    # K = 1 and a filter support equal to the grid (types.cpp:106-114 allows support == dims)
+    x, _ = problem(1, (16, 16), 1, 16)
+    d = ref.init_dictionary(1, (16, 16), (16, 16), seed=4)
+    cfg = ref.Cfg(beta=0.05, max_admm=200, normalize=0)
+    z_r, st_r, s_r = ref.solve_coding(x[0], d, cfg)
+    z_g, st_g, s_g = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=0.05, max_admm=200, normalize=0))
+    assert s_g["admm_iters"] == s_r["admm_iters"]
+    assert rel(z_g, z_r) <= FP64_TOL and rel(st_g.lam, st_r[2]) <= FP64_TOL
+
+
+def test_support_larger_than_grid_is_a_dimension_error():
+    with pytest.raises(dcsc.DimensionError):
+        dcsc.Context(1, (16, 16), 2, (17, 3), dcsc.SolverConfig(normalize=0), 64)
+
+
+def test_coding_image_subranges_are_independent():
+    # batched coding over [n0, n1) equals coding each image alone (pipeline.cpp:221-227)
+    x, d = problem(4, (20, 20), 4, 5)
+    sc = dcsc.SolverConfig(beta=0.1, max_admm=150, normalize=0)
+    with dcsc.Context(4, (20, 20), 4, (5, 5), sc, 64) as ctx:
+        ctx.set_signals(x)
+        ctx.set_dictionary(d)
+        s_a = ctx.coding(1, 3)
+        _, z_a, lam_a = ctx.get_coding_state(1, 3)
+        s_b = ctx.coding(0, 4)
+        _, z_b, _ = ctx.get_coding_state(0, 4)
+    for i, n in enumerate((1, 2)):
+        z1, st1, s1 = dcsc.solve_coding(x[n], d, sc)
+        assert s_a[i]["admm_iters"] == s1["admm_iters"]
+        assert rel(z_a[i], z1) <= 1e-12 and rel(lam_a[i], st1.lam) <= 1e-12
+    # the second call warm-starts images 1, 2 from their state and cold-starts 0, 3
+    assert s_b[1]["admm_iters"] <= s_a[0]["admm_iters"]
+
+
+def test_huge_beta_gives_zero_maps_and_lambda_minus_x():
+    x, d = problem(1, (20, 20), 4, 5)
+    z, st, s = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=1e6, rho=1.0, max_admm=500, normalize=0))
+    assert np.all(z == 0)
+    assert rel(st.lam, -x[0]) <= 1e-3

@@ -102,3 +102,22 @@ def test_joint_replica_equals_run_csc():
     for ra, rb in zip(a["trace"], b["trace"]):
         assert ra["total"] == rb["total"] and ra["admm_iters"] == rb["admm_iters"]
     assert np.array_equal(a["dict"], b["dict"]) and np.array_equal(a["maps"], b["maps"])
+
+
+def test_reference_reproduces_golden_tcsc():
+    import os
+    from paper_1709_09479_b200 import dcsc
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "run_tcsc_j3_fp64.npz"))
+    c = g["cfg"]
+    cfg = ref.Cfg(beta=c[0], rho=c[1], tol=c[2], max_outer=int(c[3]), max_admm=int(c[4]), max_mu_iters=int(c[5]),
+                  cg_tol=c[6], cg_max=int(c[7]), mu_floor=c[8], seed=int(c[9]), normalize=int(c[10]))
+    N, H, W, K, m, J = (int(v) for v in g["shape"])
+    p, sigma, seed = float(g["gen"][0]), float(g["gen"][1]), int(g["gen"][2])
+    x = np.stack([dcsc.synth_generate(N, (H, W), K, m, p, sigma, seed + j, False)[0] for j in range(J)], axis=1)
+    assert np.array_equal(x, g["x"])
+    r = ref.run_j(x, K, (m, m), cfg)
+    keys = list(g["trace_keys"])
+    for row, grow in zip(r["trace"], g["trace"]):
+        for k in ("total", "data_term", "l1_term"):
+            assert abs(row[k] - grow[keys.index(k)]) <= 1e-12 * abs(grow[keys.index(k)])
+        assert row["admm_iters"] == grow[keys.index("admm_iters")]
