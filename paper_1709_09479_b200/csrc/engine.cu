@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -429,7 +431,18 @@ class Engine final : public EngineBase {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
       long slots;
       if constexpr (CLU) {
-        slots = sms / CLN;  // one CTA per SM (smem-bound), CLN CTAs per plane
+        // clusters must sit inside one GPC: ask the runtime how many fit at
+        // once (4-CTA clusters strand SMs on GPCs whose SM count is not a
+        // multiple of 4) instead of assuming sms / CLN
+        slots = sms / CLN;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(CLN, 1, 1);
+        lc.blockDim = dim3(T, 1, 1);
+        lc.dynamicSmemBytes = smem_coding();
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)coding_pass_cl<P, kPassAdmm>, &lc) == cudaSuccess && ncl > 0)
+          slots = ncl;
+        cudaGetLastError();
       } else {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coding_pass<P, kPassAdmm>, T, smem_coding()));
         slots = (long)sms * std::max(per_sm, 1);
@@ -446,8 +459,14 @@ class Engine final : public EngineBase {
           bestG = G;
         }
       }
+      if (const char* e = std::getenv("DCSC_GROUPS")) {  // experiment override
+        const int g = std::atoi(e);
+        if (g >= 1 && g <= K_) bestG = g;
+      }
       kpg_ = (K_ + bestG - 1) / bestG;
-      G_ = bestG;
+      G_ = (K_ + kpg_ - 1) / kpg_;
+      if (std::getenv("DCSC_VERBOSE"))
+        std::fprintf(stderr, "dcsc: N=%d K=%d slots=%ld groups G=%d (%d filters per CTA)\n", N_, K_, slots, G_, kpg_);
     }
     // twiddles (forward roots) in long double, rounded once
     std::vector<C> tw(P::TW_LEN);
