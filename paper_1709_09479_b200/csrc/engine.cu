@@ -505,7 +505,18 @@ class Engine final : public EngineBase {
     p_.alloc(sizeof(C) * nNB);
     ap_.alloc(sizeof(C) * nNB);
     cvec_.alloc(sizeof(C) * (size_t)K_ * NB);
-    csplit_ = std::max(1, std::min(64, (N_ + 31) / 32));  // images per contract_c chunk <= 32
+    // contract_c splits the image sum only as far as needed to fill the GPU
+    // (~4 CTAs of 256 threads per SM): every split adds a K x NB FP64 partial
+    // plane written and re-read per CG apply (C3: 1 GB at 16 splits)
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      const long base = (long)((NB + TBV - 1) / TBV) * ((K_ + 7) / 8);
+      const double want = std::max(1.0, 4.0 * sms / (double)base);
+      const long p2 = 1L << (int)std::lround(std::log2(want));  // nearest power of two (measured: C4 16 > 17)
+      csplit_ = (int)std::max(1L, std::min({p2, 64L, (long)N_}));
+    }
+    if (const char* e = std::getenv("DCSC_CSPLIT")) csplit_ = std::max(1, std::min(N_, std::atoi(e)));
     cpart_.alloc(sizeof(double2) * (size_t)csplit_ * K_ * NB);
     phat_.alloc(sizeof(C) * (size_t)K_ * NB);
     live_.alloc(sizeof(int) * K_);
