@@ -313,8 +313,11 @@ struct KernelFamily {
 template <>
 struct KernelFamily<float, 256, 256> {
   static constexpr bool cluster = true;
-  static constexpr int CL = 4;
-  using P = ClusterPlane<float, 256, 256, 4, 512>;
+#ifndef DCSC_CL256
+#define DCSC_CL256 4
+#endif
+  static constexpr int CL = DCSC_CL256;
+  using P = ClusterPlane<float, 256, 256, CL, (CL == 8 ? 256 : 512)>;
 };
 
 template <class R, int H, int W>
