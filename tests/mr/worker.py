@@ -1,5 +1,5 @@
 """One rank of a multi-rank run_csc (tests/test_multirank.py). Env: RANK,
-WORLD_SIZE, MASTER_ADDR, MASTER_PORT, MR_OUT (npz path), MR_MODE (gpu|cpu)."""
+WORLD_SIZE, MASTER_ADDR, MASTER_PORT, MR_OUT (npz path), MR_MODE (gpu|gpu_j|cpu)."""
 import os
 import sys
 
@@ -7,6 +7,12 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
+
+
+def mr_signals(dcsc, N, grid, K, m, J):
+    """J = 1: the seeded generator; J > 1: channel j from seed 7 + j."""
+    xs = [dcsc.synth_generate(N, grid, K, m, 0.05, 0.01, 7 + j, False)[0] for j in range(J)]
+    return xs[0] if J == 1 else np.ascontiguousarray(np.stack(xs, axis=1))
 
 
 def main():
@@ -26,10 +32,11 @@ def main():
         dist.destroy_process_group()
         return
     N, grid, K, m = 4, (20, 20), 6, 5
-    x, _ = dcsc.synth_generate(N, grid, K, m, 0.05, 0.01, 7, False)
+    J = 2 if os.environ.get("MR_MODE") == "gpu_j" else 1
+    x = mr_signals(dcsc, N, grid, K, m, J)
     n0, n1 = dcsc.shard_range(N, world, rank)
     cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
-    with dcsc.Context(n1 - n0, grid, K, (m, m), cfg, 64) as ctx:
+    with dcsc.Context(n1 - n0, grid, K, (m, m), cfg, 64, channels=J) as ctx:
         ctx.set_comm_callback(world, rank, dcsc.gloo_allreduce_fn())
         ctx.set_signals(x[n0:n1])
         trace, _ = ctx.run(cfg.max_outer)

@@ -79,3 +79,23 @@ def test_two_ranks_match_single_rank(tmp_path):
         assert np.abs(r["dict"] - one["dict"]).max() <= 1e-8 * np.abs(one["dict"]).max()
     maps = np.concatenate([res[0]["maps"], res[1]["maps"]])
     assert np.abs(maps - one["maps"]).max() <= 1e-8 * np.abs(one["maps"]).max()
+
+
+@pytest.mark.gpu
+def test_two_ranks_match_single_rank_joint_channels(tmp_path):
+    """Joint mode (J = 2): per-channel CG under the shared mu ascent, sharded over ranks."""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "mr"))
+    import worker  # noqa: E402
+    res = launch(2, "gpu_j", tmp_path)
+    N, grid, K, m = 4, (20, 20), 6, 5
+    x = worker.mr_signals(dcsc, N, grid, K, m, 2)
+    cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
+    one = dcsc.run_csc(x, K, (m, m), cfg, precision=64)
+    keys = ["total", "data_term", "l1_term", "admm_iters", "cg_iters", "mu_iters", "l0"]
+    single = np.array([[r[k] for k in keys] for r in one["trace"]], dtype=np.float64)
+    for r in res:
+        t = r["trace"]
+        assert t.shape == single.shape
+        assert np.all(np.abs(t[:, :3] - single[:, :3]) <= 1e-9 * np.abs(single[:, :3]))
+        assert np.array_equal(t[:, 3], single[:, 3]) and np.array_equal(t[:, 5], single[:, 5])
+        assert np.abs(r["dict"] - one["dict"]).max() <= 1e-8 * np.abs(one["dict"]).max()
