@@ -557,10 +557,7 @@ class Engine final : public EngineBase {
   }
 
   ~Engine() override {
-    for (auto& e : prof_) {
-      cudaEventDestroy(e.a);
-      cudaEventDestroy(e.b);
-    }
+    for (auto& e : evpool_) cudaEventDestroy(e);
     for (auto& e : marks_)
       if (e) cudaEventDestroy(e);
     if (pin_) cudaFreeHost(pin_);
@@ -569,12 +566,23 @@ class Engine final : public EngineBase {
   }
 
   // ------------------------------------------------------------ launches
+  // per-launch profiling events come from a pool reused across profiling
+  // windows (creating two events per launch costs microseconds of host time,
+  // which shows up in wall-clock traces of launch-dense phases)
+  cudaEvent_t pooled_event() {
+    if (evused_ == evpool_.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      evpool_.push_back(e);
+    }
+    return evpool_[evused_++];
+  }
   template <class F>
   void launch(int fam, F&& f) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (profiling_) {
-      CK(cudaEventCreate(&a));
-      CK(cudaEventCreate(&b));
+      a = pooled_event();
+      b = pooled_event();
       CK(cudaEventRecord(a, st_));
     }
     f();
@@ -1480,11 +1488,8 @@ class Engine final : public EngineBase {
 
   void set_profiling(int on) override {
     CK(cudaStreamSynchronize(st_));
-    for (auto& e : prof_) {
-      cudaEventDestroy(e.a);
-      cudaEventDestroy(e.b);
-    }
     prof_.clear();
+    evused_ = 0;
     profiling_ = on != 0;
   }
 
@@ -1541,6 +1546,8 @@ class Engine final : public EngineBase {
   size_t xstage_bytes_ = 0;
   bool dict_zero_ = false, zhat_valid_ = false, profiling_ = false;
   std::vector<Prof> prof_;
+  std::vector<cudaEvent_t> evpool_;
+  size_t evused_ = 0;
   std::vector<cudaEvent_t> marks_;
 };
 
