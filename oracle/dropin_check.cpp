@@ -11,18 +11,21 @@
 #include "dcsc/pipeline.hpp"
 #include "dcsc_cuda.hpp"
 
+// usage: dropin_check [outer] [channels]   (channels > 1: Joint mode, TCSC)
 int main(int argc, char** argv) {
   const int N = 3, H = 20, W = 20, K = 6, m = 5, outer = argc > 1 ? std::atoi(argv[1]) : 3;
+  const int J = argc > 2 ? std::atoi(argv[2]) : 1;
   dcsc::Dataset data;
   std::mt19937_64 rng(123);
   for (int n = 0; n < N; ++n) {
-    dcsc::SignalTensor x({H, W}, 1);
+    dcsc::SignalTensor x({H, W}, J);
     for (double& v : x.values) v = static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5;
     data.signals.push_back(x);
   }
   dcsc::RunConfig cfg;
   cfg.filters = K;
   cfg.support = {m, m};
+  cfg.channel_mode = J > 1 ? dcsc::ChannelMode::Joint : dcsc::ChannelMode::Separate;
   cfg.solver.beta = 0.2;
   cfg.solver.max_outer = outer;
   cfg.solver.tol = 1e-300;
@@ -49,7 +52,7 @@ int main(int argc, char** argv) {
     dref = std::max(dref, std::abs(a.dict.values[i]));
   }
   const bool ok = worst <= 1e-9 && dmax <= 1e-8 * dref;
-  std::printf("{\"ok\": %s, \"rows\": %zu, \"max_rel_objective\": %.3e, \"max_rel_dict\": %.3e}\n",
-              ok ? "true" : "false", a.trace.rows.size(), worst, dmax / dref);
+  std::printf("{\"ok\": %s, \"channels\": %d, \"rows\": %zu, \"max_rel_objective\": %.3e, \"max_rel_dict\": %.3e}\n",
+              ok ? "true" : "false", J, a.trace.rows.size(), worst, dmax / dref);
   return ok ? 0 : 1;
 }

@@ -11,9 +11,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
 
 
-def test_reference_program_drop_in():
+@pytest.mark.parametrize("channels", [1, 3])
+def test_reference_program_drop_in(channels):
     if not os.path.exists(BIN):
         pytest.fail("oracle/_ref/dropin_check not built (make -C oracle dropin)")
-    r = subprocess.run([BIN, "3"], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([BIN, "3", str(channels)], capture_output=True, text=True, timeout=300)
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert r.returncode == 0 and out["ok"], out
