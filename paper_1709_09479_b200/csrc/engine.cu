@@ -528,6 +528,14 @@ class Engine final : public EngineBase {
     dd_.alloc(sizeof(double) * (size_t)K_ * M_);
     ddict_.alloc(sizeof(double) * (size_t)J_ * K_ * M_);
     cg_.alloc(sizeof(CgState));
+    cgcnt_.alloc(sizeof(unsigned) * 2);
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      fused_rows_ = 8 * sms;  // blocks of a fused CG launch: ~8 resident x 256 threads per SM
+    }
+    no_cg_fuse_ = std::getenv("DCSC_NO_CG_FUSE") != nullptr;
+    CK(cudaMemsetAsync(cgcnt_.p, 0, cgcnt_.bytes, st_));
     hred_.alloc(sizeof(double) * std::max(64, K_ + 8));
     cglob_.alloc(sizeof(double2) * (size_t)K_ * NB);
     tiles_ = (NB + TBV - 1) / TBV;
@@ -1039,16 +1047,23 @@ class Engine final : public EngineBase {
   }
 
   // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
-  void apply_hat(const C* v, C* out, const int* done = nullptr) {
+  // fuse_alpha (single rank, inside the CG loop): contract_out's last block
+  // also runs the alpha step (no separate cg_scalar launch)
+  void apply_hat(const C* v, C* out, const int* done = nullptr, bool fuse_alpha = false) {
     correlate_hat(v, done);
     launch(kFamMask, [&] {
       launch_mask(K_, st_, cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(), dmu_.as<double>(), mh_, mw_, 0,
                   dtw_.as<C>(), done);
     });
-    const dim3 g3(tiles_, N_);
+    // fused: fewer image rows per launch (each block loops over images) so the
+    // last-block alpha step sums few partials and the arrival counter sees
+    // few atomics
+    const dim3 g3(tiles_, fuse_alpha ? std::min(N_, std::max(1, fused_rows_ / tiles_)) : N_);
     launch(kFamContract, [&] {
       contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(), live_.as<int>(),
-                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0, done);
+                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0, done,
+                                                 fuse_alpha ? cg_.as<CgState>() : nullptr, cgcnt_.as<unsigned>(),
+                                                 1.0 / D);
     });
   }
 
@@ -1110,14 +1125,17 @@ class Engine final : public EngineBase {
     int issued = 0, chunk = 2;
     while (!s.done && issued < cfg_.cg_max) {
       const int n = std::min(chunk, cfg_.cg_max - issued);
+      const bool fuse = !multi() && !no_cg_fuse_;  // single rank: scalar steps in the producers' last blocks
       for (int c = 0; c < n; ++c) {
-        apply_hat(p_.as<C>(), ap_.as<C>(), done);
-        cg_step(partial_.as<double>(), N_ * tiles_, invD, 1);
+        apply_hat(p_.as<C>(), ap_.as<C>(), done, fuse);
+        if (!fuse) cg_step(partial_.as<double>(), N_ * tiles_, invD, 1);
         launch(kFamOther, [&] {
-          cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gam_ch_, r_.as<C>(), p_.as<C>(), ap_.as<C>(),
-                                                  cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh);
+          cg_update<R, TBV><<<fuse ? std::min<unsigned>(vb, (unsigned)fused_rows_) : vb, TBV, 0, st_>>>(
+                                                  gam_ch_, r_.as<C>(), p_.as<C>(), ap_.as<C>(),
+                                                  cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh,
+                                                  fuse ? cgcnt_.as<unsigned>() + 1 : nullptr, invD);
         });
-        cg_step(partial_.as<double>(), (int)vb, invD, 2);
+        if (!fuse) cg_step(partial_.as<double>(), (int)vb, invD, 2);
         launch(kFamOther, [&] {
           cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(r_.as<C>(), p_.as<C>(), cg_.as<CgState>(), total);
         });
@@ -1531,12 +1549,13 @@ class Engine final : public EngineBase {
   };
   dcsc_cuda_opts o_;
   dcsc_solver_config cfg_;
-  int N_, K_, J_ = 1, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1;
+  int N_, K_, J_ = 1, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1, fused_rows_ = 1184;
+  bool no_cg_fuse_ = false;
   cudaStream_t st_ = nullptr;
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_, ginv_, what_;
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_, ginv_, what_, cgcnt_;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
   C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel

@@ -801,6 +801,78 @@ __global__ void sum_partials(const double* partial, int count, double* out) {
   }
 }
 
+struct CgState {
+  double rr, pap, alpha, beta, rel, bnorm, tol;
+  int bad, done, iters, max_iters, converged, pad;
+};
+
+// Single-block scalar step of CG. step 0: rr from the initial residual (done
+// when already below tol); step 1: pap -> alpha (pAp <= 0 stops, gamma
+// untouched, learning.cpp:166); step 2: rr_new -> rel, beta, iteration count.
+// Run by one whole block (the cg_scalar kernel, or the last block of the
+// kernel that produced the partials).
+__device__ __forceinline__ void cg_scalar_block(const double* partial, int count, double invD, CgState* st, int step,
+                                                const double* presum) {
+  __shared__ double red[32];
+  if (step != 0 && st->done) return;
+  if (presum) count = 0;  // already summed (over ranks)
+  double v = 0.0;
+  // fixed-order strided partial sums, then a fixed-order tree: deterministic
+  for (int i = threadIdx.x; i < count; i += blockDim.x) v += __ldcg(partial + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
+  if (presum) s = presum[0];
+  s *= invD;
+  if (step == 0) {
+    st->rr = s;
+    st->rel = sqrt(s) / st->bnorm;
+    st->bad = 0;
+    st->iters = 0;
+    st->converged = st->rel <= st->tol;
+    st->done = st->converged;
+  } else if (step == 1) {
+    st->pap = s;
+    if (s <= 0.0) {
+      st->bad = 1;
+      st->done = 1;
+    } else {
+      st->alpha = st->rr / s;
+    }
+  } else {
+    st->iters += 1;
+    st->rel = sqrt(s) / st->bnorm;
+    st->beta = s / st->rr;
+    st->rr = s;
+    if (st->rel <= st->tol) {
+      st->converged = 1;
+      st->done = 1;
+    } else if (st->iters >= st->max_iters) {
+      st->done = 1;
+    }
+  }
+}
+
+// After a block has written its partial: true in the block that arrives last
+// (its partial reads then see every block's write). The counter is reset.
+__device__ __forceinline__ bool last_block_arrive(unsigned* counter, unsigned total) {
+  __shared__ int am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counter, 1u);
+    am_last = prev == total - 1;
+    if (am_last) *counter = 0;
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last != 0;
+}
+
 // out_n = v_n + sum_k (0.5/mu_k) z_hat_nk p_hat_k (learning.cpp:109-121, in the
 // frequency domain), with the block partial of <v, out> (Parseval, FP64).
 // mode 1 (learning data term): y_n = sum_k d_hat_k z_hat_nk, partial of
@@ -809,13 +881,16 @@ template <class R, int TB>
 __global__ void __launch_bounds__(TB)
 contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const double* __restrict__ wk,
              const int* __restrict__ live, const cx<R>* __restrict__ v, cx<R>* __restrict__ out,
-             double* __restrict__ partial, int N, int K, int NB, int Wh, int mode, const int* done) {
+             double* __restrict__ partial, int N, int K, int NB, int Wh, int mode, const int* done,
+             CgState* cgst = nullptr, unsigned* cnt = nullptr, double invD = 0.0) {
   using C = cx<R>;
   __shared__ double red[TB / 32];
   if (done && *done) return;
-  const int n = blockIdx.y;
   const int b = blockIdx.x * TB + threadIdx.x;
   double dot = 0.0;
+  // images n = blockIdx.y, + gridDim.y, ...: one image per block unless the
+  // caller (fused CG apply) launches fewer rows to keep the partial count small
+  for (int n = blockIdx.y; n < N; n += gridDim.y) {
   if (b < NB) {
     // Dead filters have identically zero z_hat (and p_hat), so summing them
     // adds exact zeros: no per-filter branch, loads batched 8 deep.
@@ -850,11 +925,12 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
     if (mode == 0) {
       const C o = mk<C>(R((double)vv.x + ar), R((double)vv.y + ai));
       out[(size_t)n * NB + b] = o;
-      dot = bin_weight(b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
+      dot += bin_weight(b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
     } else {
       const double rr = ar - (double)vv.x, ri = ai - (double)vv.y;
-      dot = bin_weight(b, Wh) * (rr * rr + ri * ri);
+      dot += bin_weight(b, Wh) * (rr * rr + ri * ri);
     }
+  }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
@@ -863,8 +939,11 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < TB / 32; ++w) s += red[w];
-    partial[(size_t)n * gridDim.x + blockIdx.x] = s;
+    partial[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
   }
+  // single-rank CG: the last block turns the <p, Ap> partials into alpha
+  if (cgst && last_block_arrive(cnt, gridDim.x * gridDim.y))
+    cg_scalar_block(partial, gridDim.x * gridDim.y, invD, cgst, 1, nullptr);
 }
 
 // ----------------------------------------------------------------------------
@@ -906,30 +985,27 @@ cg_init(const cx<R>* __restrict__ xhat, const cx<R>* __restrict__ ap, cx<R>* __r
 // Device-resident CG scalars. `done` stops every CG kernel (device-side loop
 // termination): set when the relative residual reaches tol, when pAp <= 0
 // (learning.cpp:166) or when the budget is spent.
-struct CgState {
-  double rr, pap, alpha, beta, rel, bnorm, tol;
-  int bad, done, iters, max_iters, converged, pad;
-};
 
 // gamma += alpha p ; r -= alpha ap ; partial of rr_new
 template <class R, int TB>
 __global__ void __launch_bounds__(TB)
 cg_update(cx<R>* __restrict__ gam, cx<R>* __restrict__ r, const cx<R>* __restrict__ p,
-          const cx<R>* __restrict__ ap, const CgState* st, double* partial, size_t total, int NB,
-          int Wh) {
+          const cx<R>* __restrict__ ap, CgState* st, double* partial, size_t total, int NB,
+          int Wh, unsigned* cnt = nullptr, double invD = 0.0) {
   using C = cx<R>;
   if (st->done) return;
-  const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
   double v = 0.0;
-  if (i < total) {
-    const double al = st->alpha;
+  const double al = st->alpha;
+  for (size_t i = (size_t)blockIdx.x * TB + threadIdx.x; i < total; i += (size_t)gridDim.x * TB) {
     const C pv = p[i], av = ap[i], gv = gam[i], rv0 = r[i];
     gam[i] = mk<C>(R(gv.x + al * pv.x), R(gv.y + al * pv.y));
     const C rv = mk<C>(R(rv0.x - al * av.x), R(rv0.y - al * av.y));
     r[i] = rv;
-    v = bin_weight((int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
+    v += bin_weight((int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
   }
   block_partial<TB>(v, partial + blockIdx.x);
+  // single-rank CG: the last block turns the rr partials into beta / stop
+  if (cnt && last_block_arrive(cnt, gridDim.x)) cg_scalar_block(partial, gridDim.x, invD, st, 2, nullptr);
 }
 
 // p = r + beta p
@@ -944,53 +1020,9 @@ cg_pupdate(const cx<R>* __restrict__ r, cx<R>* __restrict__ p, const CgState* st
   p[i] = mk<C>(R(rv.x + be * pv.x), R(rv.y + be * pv.y));
 }
 
-// Single-block scalar step of CG. step 0: rr from the initial residual (done
-// when already below tol); step 1: pap -> alpha (pAp <= 0 stops, gamma
-// untouched, learning.cpp:166); step 2: rr_new -> rel, beta, iteration count.
 __global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step,
                           const double* presum) {
-  __shared__ double red[32];
-  if (step != 0 && st->done) return;
-  if (presum) count = 0;  // already summed (over ranks)
-  double v = 0.0;
-  // fixed-order strided partial sums, then a fixed-order tree: deterministic
-  for (int i = threadIdx.x; i < count; i += blockDim.x) v += partial[i];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  double s = 0.0;
-  for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += red[w];
-  if (presum) s = presum[0];
-  s *= invD;
-  if (step == 0) {
-    st->rr = s;
-    st->rel = sqrt(s) / st->bnorm;
-    st->bad = 0;
-    st->iters = 0;
-    st->converged = st->rel <= st->tol;
-    st->done = st->converged;
-  } else if (step == 1) {
-    st->pap = s;
-    if (s <= 0.0) {
-      st->bad = 1;
-      st->done = 1;
-    } else {
-      st->alpha = st->rr / s;
-    }
-  } else {
-    st->iters += 1;
-    st->rel = sqrt(s) / st->bnorm;
-    st->beta = s / st->rr;
-    st->rr = s;
-    if (st->rel <= st->tol) {
-      st->converged = 1;
-      st->done = 1;
-    } else if (st->iters >= st->max_iters) {
-      st->done = 1;
-    }
-  }
+  cg_scalar_block(partial, count, invD, st, step, presum);
 }
 
 // Per-image sum of block partials (learning data term / objective), out[n] = 0.5*invD*sum.
