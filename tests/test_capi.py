@@ -74,3 +74,9 @@ def test_channel_count_is_validated_before_touching_the_device():
     # J > 8 is rejected by the engine constructor (DimensionError) on any host
     with pytest.raises(dcsc.DimensionError):
         dcsc.Context(2, (20, 20), 4, (5, 5), dcsc.SolverConfig(normalize=0), 64, channels=9)
+
+
+def test_joint_mode_on_the_cluster_grid_is_a_dimension_error():
+    # the 256^2 (4-CTA cluster) family is single-channel in this round
+    with pytest.raises(dcsc.DimensionError):
+        dcsc.Context(1, (256, 256), 4, (11, 11), dcsc.SolverConfig(normalize=0), 32, channels=3)
