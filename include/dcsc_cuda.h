@@ -177,6 +177,8 @@ int dcsc_cuda_fft_timing(int height, int width, int precision, int batch, int it
  * CUDA-event timing (family: 0 coding_pass ADMM, 1 lambda_update,
  * 2 learning contractions, 3 learning mask step, 4 other) */
 int dcsc_cuda_kernel_launches(dcsc_cuda_ctx* ctx, long long* count);
+/* per-launch CUDA-event timing on the library stream: 0 off, 1 every launch,
+ * 2 coding-pass launches only (cheap enough to leave on in a timed region) */
 int dcsc_cuda_set_profiling(dcsc_cuda_ctx* ctx, int enable);
 int dcsc_cuda_kernel_time(dcsc_cuda_ctx* ctx, int family, double* total_ms, long long* launches);
 /* device-event timer on the context stream: mark(slot), elapsed(slot a, slot b) */

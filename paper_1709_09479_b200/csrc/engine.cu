@@ -588,14 +588,15 @@ class Engine final : public EngineBase {
   template <class F>
   void launch(int fam, F&& f) {
     cudaEvent_t a = nullptr, b = nullptr;
-    if (profiling_) {
+    const bool prof = profiling_ == 1 || (profiling_ == 2 && fam == kFamCoding);
+    if (prof) {
       a = pooled_event();
       b = pooled_event();
       CK(cudaEventRecord(a, st_));
     }
     f();
     CK(cudaGetLastError());
-    if (profiling_) {
+    if (prof) {
       CK(cudaEventRecord(b, st_));
       prof_.push_back({fam, a, b});
     }
@@ -1508,7 +1509,7 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
     prof_.clear();
     evused_ = 0;
-    profiling_ = on != 0;
+    profiling_ = on;  // 1: every launch, 2: coding-pass launches only
   }
 
   void kernel_time(int fam, double* ms, long long* n) override {
@@ -1563,7 +1564,8 @@ class Engine final : public EngineBase {
   std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero
   void* xstage_ = nullptr;    // pinned staging of the signals (host -> device)
   size_t xstage_bytes_ = 0;
-  bool dict_zero_ = false, zhat_valid_ = false, profiling_ = false;
+  bool dict_zero_ = false, zhat_valid_ = false;
+  int profiling_ = 0;
   std::vector<Prof> prof_;
   std::vector<cudaEvent_t> evpool_;
   size_t evused_ = 0;

@@ -373,7 +373,8 @@ class Context:
         _err(lib().dcsc_cuda_kernel_launches(self._h, C.byref(v)))
         return v.value
 
-    def set_profiling(self, on: bool):
+    def set_profiling(self, on: int):
+        """0 off, 1 every launch, 2 coding-pass launches only."""
         _err(lib().dcsc_cuda_set_profiling(self._h, int(on)))
 
     def kernel_time(self, family: int):
