@@ -345,7 +345,13 @@ class Engine final : public EngineBase {
     if constexpr (CLU) {
       coding_pass_cl<P, MODE><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
     } else {
-      if (a.J > 1)
+      if (MODE == kPassAdmm && a.J == 2)  // common channel counts: compile-time loops
+        coding_pass<P, MODE, true, 2><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else if (MODE == kPassAdmm && a.J == 3)
+        coding_pass<P, MODE, true, 3><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else if (MODE == kPassAdmm && a.J == 4)
+        coding_pass<P, MODE, true, 4><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else if (a.J > 1)
         coding_pass<P, MODE, true><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
       else
         coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
@@ -400,6 +406,9 @@ class Engine final : public EngineBase {
       big((const void*)coding_pass<P, kPassObjective>, smem_coding());
       big((const void*)coding_pass<P, kPassMaps>, smem_coding());
       big((const void*)coding_pass<P, kPassAdmm, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true, 2>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true, 3>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true, 4>, smem_coding());
       big((const void*)coding_pass<P, kPassPrologue, true>, smem_coding());
       big((const void*)coding_pass<P, kPassObjective, true>, smem_coding());
       big((const void*)coding_pass<P, kPassMaps, true>, smem_coding());
@@ -876,10 +885,18 @@ class Engine final : public EngineBase {
     // multi-channel: lambda_hat from the per-bin J x J solves (tcsc.cpp:68-88)
     auto tc_lam = [&](int kw, bool skip_conv) {
       launch(kFamLambda, [&] {
-        tc_lambda<R><<<dim3((NB + 127) / 128, cnt), 128, 0, st_>>>(
-            what_.as<C>() + (size_t)n0 * K_ * NB, dhat_.as<C>(), ginv_.as<C>(), xhat_.as<C>() + (size_t)n0 * NB,
-            (size_t)N_ * NB, lamhat_.as<C>() + (size_t)n0 * J_ * NB, skip_conv ? conv_.as<int>() + n0 : nullptr, K_,
-            kw, J_, NB, R(1.0 / cfg_.rho));
+        const dim3 grid((NB + 127) / 128, cnt);
+        const C* wp = what_.as<C>() + (size_t)n0 * K_ * NB;
+        const C* xp = xhat_.as<C>() + (size_t)n0 * NB;
+        C* lp = lamhat_.as<C>() + (size_t)n0 * J_ * NB;
+        const int* cv = skip_conv ? conv_.as<int>() + n0 : nullptr;
+        const R ir = R(1.0 / cfg_.rho);
+        if (J_ == 3)
+          tc_lambda<R, 3><<<grid, 128, 0, st_>>>(wp, dhat_.as<C>(), ginv_.as<C>(), xp, (size_t)N_ * NB, lp, cv, K_,
+                                                 kw, J_, NB, ir);
+        else
+          tc_lambda<R><<<grid, 128, 0, st_>>>(wp, dhat_.as<C>(), ginv_.as<C>(), xp, (size_t)N_ * NB, lp, cv, K_, kw,
+                                              J_, NB, ir);
       });
     };
     if (J_ > 1) {

@@ -134,7 +134,9 @@ struct Smem {
 // lambda_hat_j in the generator, w_hat_k stored to a.what by the last forward
 // column stage, and the epilogue only runs the stop test (tc_lambda solves
 // the per-bin J x J systems).
-template <class P, int MODE, bool TC = false>
+// JT > 0: the channel count as a compile-time constant (the t_hat generator's
+// channel loop is then unrolled and its 2J loads per bin issued together).
+template <class P, int MODE, bool TC = false, int JT = 0>
 __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a) {
   using R = typename P::R;
   using C = typename P::C;
@@ -231,10 +233,11 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       if (threadIdx.x == 0 && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       C* cs;
       if constexpr (TC) {
-        const int J = a.J;
+        const int J = JT > 0 ? JT : a.J;
         cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
           const int b = r * Wh + c;
           C t = mk<C>(R(0), R(0));
+#pragma unroll
           for (int j = 0; j < J; ++j)
             t = cadd(t, cmulc(__ldg(a.dhat + ((size_t)j * a.K + k) * NB + b), __ldg(a.lamhat + ((size_t)n * J + j) * NB + b)));
           return t;

@@ -72,34 +72,39 @@ __global__ void tc_factor(const cx<R>* __restrict__ dhat, cx<R>* __restrict__ gi
 // lambda_hat_j(w) = sum_i Ginv_ji(w) r_i(w), r_j = sum_k d_hat_jk w_hat_k - x_hat_j / rho
 // (tcsc.cpp:68-88). One thread per (bin, image); images whose ADMM stopped keep
 // the lambda_hat of their last iteration (coding.cpp:287-291). kw = 0: w_hat = 0.
-template <class R>
+template <class R, int JT = 0>
 __global__ void tc_lambda(const cx<R>* __restrict__ what, const cx<R>* __restrict__ dhat,
                           const cx<R>* __restrict__ ginv, const cx<R>* __restrict__ xhat, size_t xstride,
-                          cx<R>* __restrict__ lamhat, const int* conv, int K, int kw, int J, int NB, R inv_rho) {
+                          cx<R>* __restrict__ lamhat, const int* conv, int K, int kw, int Jr, int NB, R inv_rho) {
   using C = cx<R>;
+  constexpr int JM = JT > 0 ? JT : kMaxChannels;  // register arrays sized for the compile-time count
+  const int J = JT > 0 ? JT : Jr;
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = blockIdx.y;
   if (b >= NB || (conv && conv[n])) return;
-  C r[kMaxChannels];
+  C r[JM];
 #pragma unroll
-  for (int j = 0; j < kMaxChannels; ++j) r[j] = mk<C>(R(0), R(0));
+  for (int j = 0; j < JM; ++j) r[j] = mk<C>(R(0), R(0));
+#pragma unroll 4
   for (int k = 0; k < kw; ++k) {
     const C w = what[((size_t)n * K + k) * NB + b];
 #pragma unroll
-    for (int j = 0; j < kMaxChannels; ++j)
+    for (int j = 0; j < JM; ++j)
       if (j < J) r[j] = cadd(r[j], cmul(dhat[((size_t)j * K + k) * NB + b], w));
   }
 #pragma unroll
-  for (int j = 0; j < kMaxChannels; ++j)
+  for (int j = 0; j < JM; ++j)
     if (j < J) {
       const C xv = xhat[(size_t)j * xstride + (size_t)n * NB + b];
       r[j] = mk<C>(r[j].x - xv.x * inv_rho, r[j].y - xv.y * inv_rho);
     }
   const C* g = ginv + (size_t)b * J * J;
-  for (int j = 0; j < J; ++j) {
+#pragma unroll
+  for (int j = 0; j < JM; ++j) {
+    if (j >= J) break;
     C l = mk<C>(R(0), R(0));
 #pragma unroll
-    for (int i = 0; i < kMaxChannels; ++i)
+    for (int i = 0; i < JM; ++i)
       if (i < J) l = cadd(l, cmul(g[j * J + i], r[i]));
     lamhat[((size_t)n * J + j) * NB + b] = l;
   }
