@@ -6,12 +6,12 @@
  * (FFTW_FORWARD) or +1 (FFTW_BACKWARD). FFTW itself is not in this image and
  * its version is unpinned by the reference (proj/CMakeLists.txt:16-17).
  *
- * Algorithm: per axis, a recursive mixed-radix decimation-in-time
- * Cooley-Tukey transform (radix 4, 2, 3, 5, then any remaining prime by a
- * direct O(p^2) butterfly). Twiddles are tabulated once per plan from
- * sin/cos evaluated directly in double (no recurrences), so the transform is
- * accurate to a few ulps * log(n). Multi-dimensional transforms apply the 1-D
- * transform along each axis in turn. Executing a plan is thread-safe (all
+ * Algorithm: per axis, an iterative mixed-radix Stockham autosort transform
+ * (radix 4, 2, 3, 5 butterflies, any remaining odd prime by a direct O(p^2)
+ * butterfly) run over all the sequences of the axis at once, the innermost
+ * loop over contiguous memory. Per-stage twiddles are tabulated once per plan
+ * from sin/cos evaluated directly in double (exact at the quarter points, no
+ * recurrences), so the transform is accurate to a few ulps * log(n). Executing a plan is thread-safe (all
  * scratch is per call), matching FFTW's "execute on fresh arrays" contract that
  * the reference relies on under OpenMP (spectral.cpp:16-18).
  *
@@ -29,11 +29,16 @@ typedef struct {
   double re, im;
 } cplx;
 
+/* One Stockham stage: radix r, ns = product of the radices already applied. */
 typedef struct {
-  int n;
-  int nfac;
-  int fac[64];
-  cplx* w; /* w[j] = exp(sign * 2 pi i j / n) */
+  int r, ns;
+  cplx* tw; /* tw[k * r + q] = exp(sign 2 pi i q k / (ns r)), k < ns, q < r */
+} stage;
+
+typedef struct {
+  int n, nst;
+  stage st[64];
+  cplx* root; /* root[q] = exp(sign 2 pi i q / r) for the generic odd-prime radix (largest r) */
 } axis_plan;
 
 struct fftw_plan_s {
@@ -52,101 +57,166 @@ fftw_complex* fftw_alloc_complex(size_t n) {
 
 void fftw_free(void* p) { free(p); }
 
-static void factorize(axis_plan* a) {
-  int n = a->n;
-  a->nfac = 0;
-  while (n % 4 == 0) { a->fac[a->nfac++] = 4; n /= 4; }
-  while (n % 2 == 0) { a->fac[a->nfac++] = 2; n /= 2; }
-  for (int p = 3; n > 1; p += 2) {
-    while (n % p == 0) { a->fac[a->nfac++] = p; n /= p; }
-  }
-  if (a->nfac == 0) a->fac[a->nfac++] = 1;
+static const double kTwoPi = 6.283185307179586476925286766559;
+
+/* exp(sign 2 pi i m / d), exact at the quarter points */
+static cplx unit_root(long m, long d, int sign) {
+  m %= d;
+  if (m < 0) m += d;
+  cplx w;
+  if (m == 0) { w.re = 1; w.im = 0; return w; }
+  if (4 * m == d) { w.re = 0; w.im = (double)sign; return w; }
+  if (2 * m == d) { w.re = -1; w.im = 0; return w; }
+  if (4 * m == 3 * d) { w.re = 0; w.im = -(double)sign; return w; }
+  const double ang = kTwoPi * (double)m / (double)d;
+  w.re = cos(ang);
+  w.im = (double)sign * sin(ang);
+  return w;
 }
 
-static void init_axis(axis_plan* a, int n, int sign) {
+static int init_axis(axis_plan* a, int n, int sign) {
   a->n = n;
-  factorize(a);
-  a->w = (cplx*)malloc((size_t)n * sizeof(cplx));
-  const double two_pi = 6.283185307179586476925286766559;
-  for (int j = 0; j < n; ++j) {
-    /* reduce the angle to the first octant-friendly form for accuracy */
-    const double ang = two_pi * (double)j / (double)n;
-    a->w[j].re = cos(ang);
-    a->w[j].im = (double)sign * sin(ang);
+  a->nst = 0;
+  a->root = NULL;
+  int fac[64], nf = 0, m = n;
+  while (m % 4 == 0) { fac[nf++] = 4; m /= 4; }
+  while (m % 2 == 0) { fac[nf++] = 2; m /= 2; }
+  for (int p = 3; m > 1; p += 2)
+    while (m % p == 0) { fac[nf++] = p; m /= p; }
+  int ns = 1, rmax = 1;
+  for (int f = 0; f < nf; ++f) {
+    const int r = fac[f];
+    if (r > 64) return 0; /* primes above 64 are not needed by the reference sizes */
+    stage* st = &a->st[a->nst++];
+    st->r = r;
+    st->ns = ns;
+    st->tw = (cplx*)malloc((size_t)ns * r * sizeof(cplx));
+    for (int k = 0; k < ns; ++k)
+      for (int q = 0; q < r; ++q) st->tw[k * r + q] = unit_root((long)q * k, (long)ns * r, sign);
+    ns *= r;
+    if (r > rmax && r > 5) rmax = r;
   }
-  /* exact values at the quarter points */
-  if (n % 4 == 0) {
-    a->w[0].re = 1; a->w[0].im = 0;
-    a->w[n / 4].re = 0; a->w[n / 4].im = (double)sign;
-    a->w[n / 2].re = -1; a->w[n / 2].im = 0;
-    a->w[3 * n / 4].re = 0; a->w[3 * n / 4].im = -(double)sign;
-  } else if (n % 2 == 0) {
-    a->w[n / 2].re = -1; a->w[n / 2].im = 0;
+  if (rmax > 5) {
+    a->root = (cplx*)malloc((size_t)rmax * sizeof(cplx));
+    for (int q = 0; q < rmax; ++q) a->root[q] = unit_root(q, rmax, sign);
   }
+  return 1;
+}
+
+static void free_axis(axis_plan* a) {
+  for (int s = 0; s < a->nst; ++s) free(a->st[s].tw);
+  free(a->root);
 }
 
 static inline cplx cmul(cplx a, cplx b) {
   cplx r = {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
   return r;
 }
+static inline cplx cadd(cplx a, cplx b) {
+  cplx r = {a.re + b.re, a.im + b.im};
+  return r;
+}
+static inline cplx csub(cplx a, cplx b) {
+  cplx r = {a.re - b.re, a.im - b.im};
+  return r;
+}
+/* multiply by sign * i */
+static inline cplx mul_si(cplx a, double s) {
+  cplx r = {-s * a.im, s * a.re};
+  return r;
+}
 
-/* out[0..n) = DFT_n(in[0], in[is], ...), wst = N/n indexes the axis table. */
-static void fft_rec(const cplx* in, size_t is, cplx* out, int n, const int* fac,
-                    const axis_plan* ap, int wst, int sign) {
-  if (n == 1) {
-    out[0] = in[0];
-    return;
-  }
-  const int r = fac[0];
-  const int m = n / r;
-  const int N = ap->n;
-  const cplx* w = ap->w;
-  for (int q = 0; q < r; ++q) fft_rec(in + (size_t)q * is, is * (size_t)r, out + (size_t)q * m, m, fac + 1, ap, wst * r, sign);
-
-  if (r == 2) {
-    for (int k = 0; k < m; ++k) {
-      const cplx a = out[k];
-      const cplx b = cmul(out[m + k], w[(size_t)k * wst % N]);
-      out[k].re = a.re + b.re; out[k].im = a.im + b.im;
-      out[m + k].re = a.re - b.re; out[m + k].im = a.im - b.im;
-    }
-    return;
-  }
-  if (r == 4) {
-    const double s = (double)sign; /* W_4 = s*i */
-    for (int k = 0; k < m; ++k) {
-      const cplx x0 = out[k];
-      const cplx x1 = cmul(out[m + k], w[(size_t)k * wst % N]);
-      const cplx x2 = cmul(out[2 * m + k], w[(size_t)2 * k * wst % N]);
-      const cplx x3 = cmul(out[3 * m + k], w[(size_t)3 * k * wst % N]);
-      const cplx t0 = {x0.re + x2.re, x0.im + x2.im};
-      const cplx t1 = {x0.re - x2.re, x0.im - x2.im};
-      const cplx t2 = {x1.re + x3.re, x1.im + x3.im};
-      const cplx t3 = {x1.re - x3.re, x1.im - x3.im};
-      /* s*i*t3 */
-      const cplx it3 = {-s * t3.im, s * t3.re};
-      out[k].re = t0.re + t2.re; out[k].im = t0.im + t2.im;
-      out[m + k].re = t1.re + it3.re; out[m + k].im = t1.im + it3.im;
-      out[2 * m + k].re = t0.re - t2.re; out[2 * m + k].im = t0.im - t2.im;
-      out[3 * m + k].re = t1.re - it3.re; out[3 * m + k].im = t1.im - it3.im;
-    }
-    return;
-  }
-  /* generic radix r: y_q = out[q m + k] W_n^{qk}; out[k + s m] = sum_q y_q W_r^{qs} */
-  cplx y[64];
-  cplx acc[64];
-  for (int k = 0; k < m; ++k) {
-    for (int q = 0; q < r; ++q) y[q] = q == 0 ? out[k] : cmul(out[(size_t)q * m + k], w[(size_t)q * k * wst % N]);
-    for (int s2 = 0; s2 < r; ++s2) {
-      cplx a = y[0];
-      for (int q = 1; q < r; ++q) {
-        const cplx t = cmul(y[q], w[((size_t)q * s2 % r) * (size_t)m * wst % N]);
-        a.re += t.re; a.im += t.im;
+/* One Stockham stage over a batch of `bat` transforms: element (index j,
+ * transform c) at x[j * es + c * bs]. Output index o = (j / ns) ns r + k + s ns. */
+static void run_stage(const stage* st, int n, size_t bat, size_t es, size_t bs, const cplx* x, cplx* y, int sign,
+                      const cplx* root) {
+  const int r = st->r, ns = st->ns, J = n / r;
+  const double sg = (double)sign;
+  for (int j = 0; j < J; ++j) {
+    const int k = j % ns;
+    const size_t o = (size_t)(j / ns) * ns * r + k;
+    const cplx* w = st->tw + (size_t)k * r;
+    const cplx* xj = x + (size_t)j * es;
+    cplx* yo = y + o * es;
+    const size_t xs = (size_t)J * es, ys = (size_t)ns * es;
+    if (r == 2) {
+      for (size_t c = 0, cb = 0; c < bat; ++c, cb += bs) {
+        const cplx a = xj[cb], b = k ? cmul(xj[xs + cb], w[1]) : xj[xs + cb];
+        yo[cb] = cadd(a, b);
+        yo[ys + cb] = csub(a, b);
       }
-      acc[s2] = a;
+    } else if (r == 4) {
+      for (size_t c = 0, cb = 0; c < bat; ++c, cb += bs) {
+        const cplx x0 = xj[cb];
+        const cplx x1 = k ? cmul(xj[xs + cb], w[1]) : xj[xs + cb];
+        const cplx x2 = k ? cmul(xj[2 * xs + cb], w[2]) : xj[2 * xs + cb];
+        const cplx x3 = k ? cmul(xj[3 * xs + cb], w[3]) : xj[3 * xs + cb];
+        const cplx t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_si(csub(x1, x3), sg);
+        yo[cb] = cadd(t0, t2);
+        yo[ys + cb] = cadd(t1, t3);
+        yo[2 * ys + cb] = csub(t0, t2);
+        yo[3 * ys + cb] = csub(t1, t3);
+      }
+    } else if (r == 3) {
+      const double c1 = -0.5, s1 = sg * 0.86602540378443864676372317075294;
+      for (size_t c = 0, cb = 0; c < bat; ++c, cb += bs) {
+        const cplx x0 = xj[cb];
+        const cplx x1 = k ? cmul(xj[xs + cb], w[1]) : xj[xs + cb];
+        const cplx x2 = k ? cmul(xj[2 * xs + cb], w[2]) : xj[2 * xs + cb];
+        const cplx t = cadd(x1, x2), d = csub(x1, x2);
+        const cplx m = {x0.re + c1 * t.re, x0.im + c1 * t.im};
+        const cplx e = {-s1 * d.im, s1 * d.re}; /* i s1 d */
+        yo[cb] = cadd(x0, t);
+        yo[ys + cb] = cadd(m, e);
+        yo[2 * ys + cb] = csub(m, e);
+      }
+    } else if (r == 5) {
+      const double c1 = 0.30901699437494742410229341718282, c2 = -0.80901699437494742410229341718282;
+      const double s1 = sg * 0.95105651629515357211643933337938, s2 = sg * 0.58778525229247312916870595463907;
+      for (size_t c = 0, cb = 0; c < bat; ++c, cb += bs) {
+        const cplx x0 = xj[cb];
+        const cplx x1 = k ? cmul(xj[xs + cb], w[1]) : xj[xs + cb];
+        const cplx x2 = k ? cmul(xj[2 * xs + cb], w[2]) : xj[2 * xs + cb];
+        const cplx x3 = k ? cmul(xj[3 * xs + cb], w[3]) : xj[3 * xs + cb];
+        const cplx x4 = k ? cmul(xj[4 * xs + cb], w[4]) : xj[4 * xs + cb];
+        const cplx a1 = cadd(x1, x4), a2 = cadd(x2, x3), b1 = csub(x1, x4), b2 = csub(x2, x3);
+        const cplx m1 = {x0.re + c1 * a1.re + c2 * a2.re, x0.im + c1 * a1.im + c2 * a2.im};
+        const cplx m2 = {x0.re + c2 * a1.re + c1 * a2.re, x0.im + c2 * a1.im + c1 * a2.im};
+        /* i (s1 b1 + s2 b2), i (s2 b1 - s1 b2) */
+        const cplx n1 = {-(s1 * b1.im + s2 * b2.im), s1 * b1.re + s2 * b2.re};
+        const cplx n2 = {-(s2 * b1.im - s1 * b2.im), s2 * b1.re - s1 * b2.re};
+        yo[cb] = cadd(x0, cadd(a1, a2));
+        yo[ys + cb] = cadd(m1, n1);
+        yo[4 * ys + cb] = csub(m1, n1);
+        yo[2 * ys + cb] = cadd(m2, n2);
+        yo[3 * ys + cb] = csub(m2, n2);
+      }
+    } else { /* generic odd prime: direct DFT_r of the twiddled inputs */
+      cplx t[64];
+      for (size_t c = 0, cb = 0; c < bat; ++c, cb += bs) {
+        for (int q = 0; q < r; ++q) t[q] = (q && k) ? cmul(xj[q * xs + cb], w[q]) : xj[q * xs + cb];
+        for (int s2 = 0; s2 < r; ++s2) {
+          cplx acc = t[0];
+          for (int q = 1; q < r; ++q) acc = cadd(acc, cmul(t[q], root[((long)q * s2) % r]));
+          yo[s2 * ys + cb] = acc;
+        }
+      }
     }
-    for (int s2 = 0; s2 < r; ++s2) out[k + (size_t)s2 * m] = acc[s2];
   }
+}
+
+/* In-place transform of `bat` length-n sequences at x (element j of sequence c
+ * at x[j * es + c * bs], the n * bat elements dense); scratch holds n * bat values. */
+static void fft_batch(const axis_plan* ap, cplx* x, cplx* scratch, size_t bat, size_t es, size_t bs, int sign) {
+  cplx* a = x;
+  cplx* b = scratch;
+  for (int s = 0; s < ap->nst; ++s) {
+    run_stage(&ap->st[s], ap->n, bat, es, bs, a, b, sign, ap->root);
+    cplx* t = a;
+    a = b;
+    b = t;
+  }
+  if (a != x) memcpy(x, a, (size_t)ap->n * bat * sizeof(cplx));
 }
 
 fftw_plan fftw_plan_dft(int rank, const int* n, fftw_complex* in, fftw_complex* out, int sign,
@@ -158,52 +228,49 @@ fftw_plan fftw_plan_dft(int rank, const int* n, fftw_complex* in, fftw_complex* 
   p->sign = sign;
   p->total = 1;
   for (int a = 0; a < rank; ++a) {
-    if (n[a] < 1) { free(p); return NULL; }
+    if (n[a] < 1 || !init_axis(&p->axes[a], n[a], sign)) {
+      for (int b = 0; b < a; ++b) free_axis(&p->axes[b]);
+      free(p);
+      return NULL;
+    }
     p->dims[a] = n[a];
     p->total *= (size_t)n[a];
-    init_axis(&p->axes[a], n[a], sign);
-    for (int f = 0; f < p->axes[a].nfac; ++f)
-      if (p->axes[a].fac[f] > 64) { /* primes above 64 are not needed by the reference sizes */
-        free(p); return NULL;
-      }
   }
   return p;
 }
 
 void fftw_destroy_plan(fftw_plan p) {
   if (!p) return;
-  for (int a = 0; a < p->rank; ++a) free(p->axes[a].w);
+  for (int a = 0; a < p->rank; ++a) free_axis(&p->axes[a]);
   free(p);
 }
 
+/* Per axis: the leading dims index independent blocks; within a block the
+ * axis has stride `inner` (product of the later dims), so the block is `inner`
+ * interleaved sequences of length n — transformed together, the innermost
+ * loop running over contiguous memory. */
 void fftw_execute_dft(const fftw_plan p, fftw_complex* in_, fftw_complex* out_) {
   const size_t total = p->total;
   cplx* out = (cplx*)out_;
   if ((void*)in_ != (void*)out_) memcpy(out, in_, total * sizeof(cplx));
-  size_t maxn = 1;
-  for (int a = 0; a < p->rank; ++a) if ((size_t)p->dims[a] > maxn) maxn = (size_t)p->dims[a];
-  cplx* line = (cplx*)malloc(2 * maxn * sizeof(cplx));
-  cplx* res = line + maxn;
-  size_t inner = total; /* product of dims after axis a */
+  /* per-thread scratch, grown on demand (plans execute concurrently under OpenMP) */
+  static _Thread_local cplx* scratch = NULL;
+  static _Thread_local size_t scratch_n = 0;
+  if (scratch_n < total) {
+    free(scratch);
+    scratch = (cplx*)malloc(total * sizeof(cplx));
+    scratch_n = total;
+  }
+  size_t inner = total;
   for (int a = 0; a < p->rank; ++a) {
     const int n = p->dims[a];
     inner /= (size_t)n;
-    const size_t outer = total / ((size_t)n * inner);
-    const axis_plan* ap = &p->axes[a];
     if (n == 1) continue;
-    for (size_t o = 0; o < outer; ++o) {
-      for (size_t i = 0; i < inner; ++i) {
-        cplx* base = out + o * (size_t)n * inner + i;
-        if (inner == 1) {
-          fft_rec(base, 1, res, n, ap->fac, ap, 1, p->sign);
-          memcpy(base, res, (size_t)n * sizeof(cplx));
-        } else {
-          for (int j = 0; j < n; ++j) line[j] = base[(size_t)j * inner];
-          fft_rec(line, 1, res, n, ap->fac, ap, 1, p->sign);
-          for (int j = 0; j < n; ++j) base[(size_t)j * inner] = res[j];
-        }
-      }
-    }
+    const size_t outer = total / ((size_t)n * inner);
+    if (inner == 1) /* last axis: all rows at once, the batch loop running over rows */
+      fft_batch(&p->axes[a], out, scratch, outer, 1, (size_t)n, p->sign);
+    else
+      for (size_t o = 0; o < outer; ++o)
+        fft_batch(&p->axes[a], out + o * (size_t)n * inner, scratch, inner, inner, 1, p->sign);
   }
-  free(line);
 }
