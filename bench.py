@@ -140,10 +140,10 @@ def make_data(cfg, n0, n1):
     from paper_1709_09479_b200 import dcsc
     J = cfg.get("J", 1)
     xs, ds = [], []
-    for j in range(J):
-        x, d_true = dcsc.synth_generate(cfg["N"], (cfg["H"], cfg["W"]), cfg["K"], cfg["m"], cfg["p"],
-                                        cfg["sigma"], SEED + j, cfg["prec"] == 32)
-        xs.append(x[n0:n1])
+    for j in range(J):  # only this rank's images are generated (per-image streams)
+        x, d_true = dcsc.synth_generate(n1 - n0, (cfg["H"], cfg["W"]), cfg["K"], cfg["m"], cfg["p"],
+                                        cfg["sigma"], SEED + j, cfg["prec"] == 32, first=n0)
+        xs.append(x)
         ds.append(d_true)
     if J == 1:
         return xs[0].copy(), ds[0]
@@ -303,7 +303,7 @@ def run_ours(args, cfg):
     weak = cfg["coding_only"]
     if weak:
         n0, n1 = rank * N, (rank + 1) * N
-        x, d_true = make_data(dict(cfg, N=N * world), n0, n1)
+        x, d_true = make_data(cfg, n0, n1)
     else:
         n0, n1 = dcsc.shard_range(N, world, rank)
         x, d_true = make_data(cfg, n0, n1)

@@ -212,6 +212,9 @@ int dcsc_io_read_trace_csv(const char* path, dcsc_trace_row* rows, int max_rows,
 /* synthetic BASELINE data (host only, no GPU): x N*H*W, d_true K*m*m */
 int dcsc_synth_generate(int n_images, int height, int width, int filters, int m, double p,
                         double sigma, uint64_t seed, int round_fp32, double* x, double* d_true);
+/* images [n0, n0 + n_images) of the same seeded dataset (per-image streams) */
+int dcsc_synth_generate_range(int n0, int n_images, int height, int width, int filters, int m, double p,
+                              double sigma, uint64_t seed, int round_fp32, double* x, double* d_true);
 /* the reference bench harness's dataset (bench.cpp:9-21): uniform [0,1) values
  * from one mt19937_64(seed), N*J*H*W doubles */
 int dcsc_synth_dataset(int n_images, int channels, int height, int width, uint64_t seed, double* x);

@@ -43,9 +43,11 @@ inline std::uint64_t mix(std::uint64_t seed, std::uint64_t stream, std::uint64_t
 
 }  // namespace
 
-extern "C" int dcsc_synth_generate(int N, int H, int W, int K, int m, double p, double sigma,
-                                   std::uint64_t seed, int round_fp32, double* x, double* d_true) {
-  if (N < 1 || H < 1 || W < 1 || K < 1 || m < 1 || m > H || m > W) return DCSC_ERR_DIMENSION;
+// Images [n0, n0 + N) of the seeded dataset (each image has its own streams,
+// so any range is generated independently of the others).
+extern "C" int dcsc_synth_generate_range(int n0, int N, int H, int W, int K, int m, double p, double sigma,
+                                         std::uint64_t seed, int round_fp32, double* x, double* d_true) {
+  if (n0 < 0 || N < 1 || H < 1 || W < 1 || K < 1 || m < 1 || m > H || m > W) return DCSC_ERR_DIMENSION;
   const int M = m * m;
   std::vector<double> d(static_cast<size_t>(K) * M);
   {
@@ -65,10 +67,11 @@ extern "C" int dcsc_synth_generate(int N, int H, int W, int K, int m, double p, 
     for (size_t i = 0; i < d.size(); ++i) d_true[i] = d[i];
   const size_t D = static_cast<size_t>(H) * W;
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int n = 0; n < N; ++n) {
-    std::mt19937_64 rm(mix(seed, 2, static_cast<std::uint64_t>(n)));
-    std::mt19937_64 re(mix(seed, 3, static_cast<std::uint64_t>(n)));
-    double* xn = x + static_cast<size_t>(n) * D;
+  for (int img = 0; img < N; ++img) {
+    const std::uint64_t n = static_cast<std::uint64_t>(n0) + static_cast<std::uint64_t>(img);
+    std::mt19937_64 rm(mix(seed, 2, n));
+    std::mt19937_64 re(mix(seed, 3, n));
+    double* xn = x + static_cast<size_t>(img) * D;
     for (size_t i = 0; i < D; ++i) xn[i] = 0.0;
     for (int k = 0; k < K; ++k) {
       const double* dk = d.data() + static_cast<size_t>(k) * M;
@@ -105,4 +108,9 @@ extern "C" int dcsc_synth_dataset(int N, int J, int H, int W, std::uint64_t seed
   const std::size_t total = (std::size_t)N * J * H * W;
   for (std::size_t i = 0; i < total; ++i) x[i] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
   return DCSC_OK;
+}
+
+extern "C" int dcsc_synth_generate(int N, int H, int W, int K, int m, double p, double sigma,
+                                   std::uint64_t seed, int round_fp32, double* x, double* d_true) {
+  return dcsc_synth_generate_range(0, N, H, W, K, m, p, sigma, seed, round_fp32, x, d_true);
 }

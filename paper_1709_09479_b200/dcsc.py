@@ -136,7 +136,7 @@ EXPORTS = [
     "dcsc_cuda_nccl_unique_id", "dcsc_cuda_set_comm_nccl", "dcsc_cuda_set_comm_callback",
     "dcsc_io_last_error", "dcsc_io_write_tensor", "dcsc_io_read_tensor_header", "dcsc_io_read_tensor",
     "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing", "dcsc_cuda_reconstruct",
-    "dcsc_synth_dataset",
+    "dcsc_synth_dataset", "dcsc_synth_generate_range",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -571,13 +571,14 @@ def fft_timing(grid, precision: int, batch: int, iters: int = 20):
     return a.value, b.value
 
 
-def synth_generate(n_images, grid, filters, m, p, sigma, seed, round_fp32):
-    """Synthetic BASELINE data; host-only, no GPU needed."""
+def synth_generate(n_images, grid, filters, m, p, sigma, seed, round_fp32, first=0):
+    """Synthetic BASELINE data; host-only, no GPU needed.
+    Images [first, first + n_images) of the seeded dataset."""
     H, W = grid
     x = np.zeros((n_images, H, W))
     d = np.zeros((filters, m, m))
-    _err(lib().dcsc_synth_generate(n_images, H, W, filters, m, C.c_double(p), C.c_double(sigma),
-                                   C.c_uint64(seed), int(round_fp32), _dp(x), _dp(d)))
+    _err(lib().dcsc_synth_generate_range(first, n_images, H, W, filters, m, C.c_double(p), C.c_double(sigma),
+                                         C.c_uint64(seed), int(round_fp32), _dp(x), _dp(d)))
     return x, d
 
 
