@@ -29,6 +29,7 @@
  *   dcsc_cuda_learning_data_term    dcsc::learning_data_term (objective.hpp:18-19)
  *   dcsc_cuda_reconstruct           dcsc::reconstruct (objective.hpp:11)
  *   dcsc_cuda_learning_apply        dcsc::LearningOperator::apply (learning.hpp:57)
+ *   dcsc_cuda_learning_correlation  dcsc::LearningOperator::correlation (learning.hpp:59-60)
  *   dcsc_cuda_run                   dcsc::run_csc (pipeline.hpp:58) + trace rows
  *                                   (types.hpp:122-136, trace_io.hpp)
  *   dcsc_cuda_dft2_forward/_inverse dcsc::forward_dft / inverse_dft
@@ -149,6 +150,10 @@ int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* s
  * with dictionary d (K*J*M; NULL = the context dictionary): out (n1-n0)*J*D.
  * GPU side of the reference CLI's `reconstruct` / `encode` (csc_main.cpp:147-202) */
 int dcsc_cuda_reconstruct(dcsc_cuda_ctx* ctx, const double* d, int n0, int n1, double* out);
+/* LearningOperator::correlation (learning.cpp:124-134) for every filter k:
+ * sum_n S_k Z_nk^T v_n over the accepted maps, v N*D (this rank's images; summed
+ * over ranks), out K*mh*mw */
+int dcsc_cuda_learning_correlation(dcsc_cuda_ctx* ctx, const double* v, double* out);
 /* LearningOperator::apply with the given mu on N*D vectors */
 int dcsc_cuda_learning_apply(dcsc_cuda_ctx* ctx, const double* mu, const double* v, double* out);
 

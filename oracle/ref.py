@@ -382,3 +382,13 @@ def reconstruct(d, z):
     out = np.zeros((J, H, W))
     _check(lib().ref_reconstruct_j(H, W, J, K, mh, mw, _p(d), _p(z), _p(out)))
     return out if d.ndim == 4 else out[0]
+
+
+def learning_correlation(maps, support, v):
+    """LearningOperator::correlation (learning.cpp:124-134) for every filter: (K, mh, mw)."""
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    N, K, H, W = maps.shape
+    out = np.zeros((K, support[0], support[1]))
+    _check(lib().ref_learning_correlation(N, H, W, K, _p(maps), support[0], support[1], _p(v), _p(out)))
+    return out

@@ -409,6 +409,26 @@ int ref_learning_apply(int N, int H, int W, int K, const double* maps, int mh, i
   });
 }
 
+// LearningOperator::correlation (learning.cpp:124-134) for every filter: out K*M.
+int ref_learning_correlation(int N, int H, int W, int K, const double* maps, int mh, int mw, const double* v,
+                             double* out) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    std::vector<SparseMaps> zs;
+    for (int n = 0; n < N; ++n) {
+      SparseMaps m(K, {H, W});
+      std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
+      zs.push_back(std::move(m));
+    }
+    LearningOperator op(zs, {mh, mw}, 1e-6);
+    const std::size_t M = static_cast<std::size_t>(mh) * mw;
+    for (int k = 0; k < K; ++k) {
+      const std::vector<double> c = op.correlation(k, std::span<const double>(v, N * D));
+      std::copy(c.begin(), c.end(), out + k * M);
+    }
+  });
+}
+
 // Instrumented replica of run_csc (see header comment). xs are the RAW signals;
 // normalisation follows cfg->normalize exactly as run_csc does. rows must hold
 // 2*max_outer entries. dict_iter (optional) receives (max_outer+1)*K*M values:

@@ -285,6 +285,7 @@ class EngineBase {
   virtual void objective(const double* d, dcsc_objective* per_image) = 0;
   virtual void learning_data_term(const double* d, double* data) = 0;
   virtual void reconstruct(const double* d, int n0, int n1, double* out) = 0;
+  virtual void learning_correlation(const double* v, double* out) = 0;
   virtual void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) = 0;
   virtual void synchronize() = 0;
   virtual void set_profiling(int on) = 0;
@@ -427,6 +428,10 @@ class Engine final : public EngineBase {
     J_ = std::max(1, o.channels);
     if (J_ > kMaxChannels) throw DimErr("at most " + std::to_string(kMaxChannels) + " channels are supported");
     if (J_ > 1 && CLU) throw DimErr("multi-channel (TCSC) coding is not compiled for the cluster grid family");
+    if constexpr (CLU) {  // the cropped support must sit in the first rank's row block
+      if (o.support_h > P::ROWS)
+        throw DimErr("filter support taller than " + std::to_string(P::ROWS) + " rows on the cluster grid family");
+    }
     mh_ = o.support_h;
     mw_ = o.support_w;
     M_ = mh_ * mw_;
@@ -1272,6 +1277,23 @@ class Engine final : public EngineBase {
     gam_ch_ = gam_.as<C>() + (size_t)j * N_ * NB;
   }
 
+  // LearningOperator::correlation (learning.cpp:124-134) for every filter:
+  // out[k] = crop(iDFT(sum_n conj(z_hat_nk) DFT(v_n))), K x M (channel-free)
+  void learning_correlation(const double* v, double* out) override {
+    build_zhat();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, v, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
+    correlate_hat(r_.as<C>(), nullptr);
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 2,
+                  dtw_.as<C>(), nullptr);
+    });
+    CK(cudaMemcpyAsync(out, dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
   void learning_apply(const double* mu, const double* v, double* out) override {
     build_zhat();
     std::vector<double> keep = mu_;
@@ -1836,6 +1858,13 @@ int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* s
   CTX_CHECK
   return guarded([&] { ctx->eng->learning(d_out, stats); });
 }
+int dcsc_cuda_learning_correlation(dcsc_cuda_ctx* ctx, const double* v, double* out) {
+  return guarded([&] {
+    if (!ctx || !v || !out) throw InvErr("null argument");
+    ctx->eng->learning_correlation(v, out);
+  });
+}
+
 int dcsc_cuda_learning_apply(dcsc_cuda_ctx* ctx, const double* mu, const double* v, double* out) {
   CTX_CHECK
   return guarded([&] { ctx->eng->learning_apply(mu, v, out); });

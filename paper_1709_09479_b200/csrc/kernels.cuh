@@ -676,8 +676,8 @@ mask_step(const cx<typename P::R>* __restrict__ c, cx<typename P::R>* __restrict
   const C* s = c + (size_t)k * NB;
   C* sp = P::inverse(B0, B1, TW, [&](int r, int cc) { return s[r * Wh + cc]; });
   const R invD = R(1) / R(D);
-  if (mode == 1) {
-    const double scale = -0.5 / fmax(mu[k], 1e-300);
+  if (mode != 0) {  // 1: d_recover (-0.5/mu scaling), 2: plain cropped correlation
+    const double scale = mode == 2 ? 1.0 : -0.5 / fmax(mu[k], 1e-300);
     for (int i = threadIdx.x; i < mh * mw; i += T) {
       const int r = i / mw, cc = i % mw;
       const C v = sp[r * Wh + cc / 2];

@@ -499,9 +499,9 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   const C* s = c + (size_t)k * NB;
   cl_inverse<CP>(b, rank, [&](int r, int cc) { return s[r * Wh + cc]; });
   const R invD = R(1) / R(D);
-  if (mode == 1) {
+  if (mode != 0) {  // 1: d_recover (-0.5/mu scaling), 2: plain cropped correlation
     if (rank == 0) {  // the support rows (mh <= ROWS) live in rank 0
-      const double scale = -0.5 / fmax(mu[k], 1e-300);
+      const double scale = mode == 2 ? 1.0 : -0.5 / fmax(mu[k], 1e-300);
       for (int i = threadIdx.x; i < mh * mw; i += T) {
         const int r = i / mw, cc = i % mw;
         const C v = b.Z[r * Wh + cc / 2];

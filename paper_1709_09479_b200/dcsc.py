@@ -136,7 +136,7 @@ EXPORTS = [
     "dcsc_cuda_nccl_unique_id", "dcsc_cuda_set_comm_nccl", "dcsc_cuda_set_comm_callback",
     "dcsc_io_last_error", "dcsc_io_write_tensor", "dcsc_io_read_tensor_header", "dcsc_io_read_tensor",
     "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing", "dcsc_cuda_reconstruct",
-    "dcsc_synth_dataset", "dcsc_synth_generate_range",
+    "dcsc_synth_dataset", "dcsc_synth_generate_range", "dcsc_cuda_learning_correlation",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -326,6 +326,13 @@ class Context:
         v = _f64(v)
         out = np.zeros_like(v)
         _err(lib().dcsc_cuda_learning_apply(self._h, _dp(mu), _dp(v), _dp(out)))
+        return out
+
+    def learning_correlation(self, v):
+        """LearningOperator::correlation (learning.cpp:124-134) for all filters: (K, mh, mw)."""
+        v = _f64(v)
+        out = np.zeros((self.K, self.mh, self.mw))
+        _err(lib().dcsc_cuda_learning_correlation(self._h, _dp(v), _dp(out)))
         return out
 
     def objective(self, d=None):

@@ -293,3 +293,17 @@ def test_huge_beta_gives_zero_maps_and_lambda_minus_x():
     z, st, s = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=1e6, rho=1.0, max_admm=500, normalize=0))
     assert np.all(z == 0)
     assert rel(st.lam, -x[0]) <= 1e-3
+
+
+def test_learning_correlation_fp64_matches_reference():
+    # LearningOperator::correlation (learning.cpp:124-134), a13 of SURVEY.md 8(a)
+    x, d = problem(3, (16, 20), 4, 5)
+    maps = coded_maps(x, d, 0.1)
+    rng = np.random.default_rng(4)
+    v = rng.standard_normal(x.shape)
+    out_r = ref.learning_correlation(maps, (5, 5), v)
+    with dcsc.Context(3, (16, 20), 4, (5, 5), dcsc.SolverConfig(normalize=0), 64) as ctx:
+        ctx.set_signals(x)
+        ctx.set_maps(maps)
+        out_g = ctx.learning_correlation(v)
+    assert rel(out_g, out_r) <= 1e-12
