@@ -150,6 +150,21 @@ int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* s
  * with dictionary d (K*J*M; NULL = the context dictionary): out (n1-n0)*J*D.
  * GPU side of the reference CLI's `reconstruct` / `encode` (csc_main.cpp:147-202) */
 int dcsc_cuda_reconstruct(dcsc_cuda_ctx* ctx, const double* d, int n0, int n1, double* out);
+/* Stateless ops (coding.hpp:45-66, learning.hpp:81-95, tcsc.hpp:38-51), for
+ * replaying iterations; they leave the context's coding / learning state as is.
+ * apply_dictionary_adjoint / block_dictionary_adjoint: lambda (n1-n0)*J*D ->
+ * D^T lambda (n1-n0)*K*D against the context dictionary */
+int dcsc_cuda_dictionary_adjoint(dcsc_cuda_ctx* ctx, int n0, int n1, const double* lambda, double* out);
+/* lambda_update / lambda_update_blocked: theta, z (n1-n0)*K*D -> lambda (n1-n0)*J*D
+ * against the context's signals and dictionary */
+int dcsc_cuda_lambda_update(dcsc_cuda_ctx* ctx, int n0, int n1, const double* theta, const double* z,
+                            double* out);
+/* gamma_solve on one channel with the given mu (K): gamma N*D warm start in /
+ * solution out over the accepted maps */
+int dcsc_cuda_gamma_solve(dcsc_cuda_ctx* ctx, int channel, const double* mu, double* gamma, int* iters,
+                          int* converged);
+/* d_recover: gamma N*D (one channel), mu K -> K*mh*mw */
+int dcsc_cuda_d_recover(dcsc_cuda_ctx* ctx, int channel, const double* gamma, const double* mu, double* out);
 /* LearningOperator::correlation (learning.cpp:124-134) for every filter k:
  * sum_n S_k Z_nk^T v_n over the accepted maps, v N*D (this rank's images; summed
  * over ranks), out K*mh*mw */

@@ -392,3 +392,51 @@ def learning_correlation(maps, support, v):
     out = np.zeros((K, support[0], support[1]))
     _check(lib().ref_learning_correlation(N, H, W, K, _p(maps), support[0], support[1], _p(v), _p(out)))
     return out
+
+
+# ---------------------------------------------------------------- stateless ops (J = 1)
+def lambda_update(x, d, theta, z, rho):
+    """lambda_update (coding.cpp:103-124) for one image."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    H, W = x.shape
+    K, mh, mw = d.shape
+    out = np.zeros((H, W))
+    _check(lib().ref_lambda_update(H, W, _p(x), K, mh, mw, _p(d), _p(np.ascontiguousarray(theta, dtype=np.float64)),
+                                   _p(np.ascontiguousarray(z, dtype=np.float64)), C.c_double(rho), _p(out)))
+    return out
+
+
+def dictionary_adjoint(d, lam):
+    """apply_dictionary_adjoint (coding.cpp:126-135): (K, H, W)."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    K, mh, mw = d.shape
+    H, W = lam.shape
+    out = np.zeros((K, H, W))
+    _check(lib().ref_dictionary_adjoint(H, W, K, mh, mw, _p(d), _p(lam), _p(out)))
+    return out
+
+
+def gamma_solve(maps, support, mu, mu_floor, x, cg_tol, cg_max, gamma):
+    """gamma_solve (learning.cpp:136-185) on the stacked system; gamma is the warm start."""
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    N, K, H, W = maps.shape
+    g = np.array(gamma, dtype=np.float64, copy=True).reshape(N, H, W)
+    it, conv = C.c_int(), C.c_int()
+    _check(lib().ref_gamma_solve(N, H, W, K, _p(maps), support[0], support[1],
+                                 _p(np.ascontiguousarray(mu, dtype=np.float64)), C.c_double(mu_floor),
+                                 _p(np.ascontiguousarray(x, dtype=np.float64)), C.c_double(cg_tol), int(cg_max),
+                                 _p(g), C.byref(it), C.byref(conv)))
+    return g, it.value, bool(conv.value)
+
+
+def d_recover(maps, support, gamma, mu):
+    """d_recover (learning.cpp:187-216): (K, mh, mw)."""
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    N, K, H, W = maps.shape
+    out = np.zeros((K, support[0], support[1]))
+    _check(lib().ref_d_recover(N, H, W, K, _p(maps), support[0], support[1],
+                               _p(np.ascontiguousarray(gamma, dtype=np.float64)),
+                               _p(np.ascontiguousarray(mu, dtype=np.float64)), _p(out)))
+    return out

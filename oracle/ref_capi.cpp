@@ -409,6 +409,75 @@ int ref_learning_apply(int N, int H, int W, int K, const double* maps, int mh, i
   });
 }
 
+// Stateless ops (coding.hpp:45-66, learning.hpp:81-95) for one J = 1 image /
+// the stacked learning system, for the GPU stateless-op parity tests.
+int ref_lambda_update(int H, int W, const double* x, int K, int mh, int mw, const double* d, const double* theta,
+                      const double* z, double rho, double* out) {
+  return guarded([&] {
+    const GridDims g{H, W};
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    const Dictionary dict = make_dict(K, mh, mw, d);
+    std::vector<Spectrum> dh, th, zh;
+    for (int k = 0; k < K; ++k) {
+      dh.push_back(filter_spectrum(dict, k, 0, g));
+      th.push_back(forward_dft(g, std::span<const double>(theta + k * D, D)));
+      zh.push_back(forward_dft(g, std::span<const double>(z + k * D, D)));
+    }
+    const Spectrum xh = forward_dft(g, std::span<const double>(x, D));
+    const std::vector<double> lam = lambda_update(dh, th, zh, xh, rho);
+    std::copy(lam.begin(), lam.end(), out);
+  });
+}
+
+int ref_dictionary_adjoint(int H, int W, int K, int mh, int mw, const double* d, const double* lambda, double* out) {
+  return guarded([&] {
+    const GridDims g{H, W};
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    const Dictionary dict = make_dict(K, mh, mw, d);
+    std::vector<Spectrum> dh;
+    for (int k = 0; k < K; ++k) dh.push_back(filter_spectrum(dict, k, 0, g));
+    const std::vector<double> t = apply_dictionary_adjoint(dh, forward_dft(g, std::span<const double>(lambda, D)));
+    std::copy(t.begin(), t.end(), out);
+  });
+}
+
+int ref_gamma_solve(int N, int H, int W, int K, const double* maps, int mh, int mw, const double* mu,
+                    double mu_floor, const double* x, double cg_tol, int cg_max, double* gamma, int* iters,
+                    int* converged) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    std::vector<SparseMaps> zs;
+    for (int n = 0; n < N; ++n) {
+      SparseMaps m(K, {H, W});
+      std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
+      zs.push_back(std::move(m));
+    }
+    LearningOperator op(zs, {mh, mw}, mu_floor);
+    op.set_mu(std::span<const double>(mu, K));
+    const CgResult r = gamma_solve(op, std::span<const double>(x, N * D), cg_tol, cg_max,
+                                   std::span<double>(gamma, N * D));
+    *iters = r.iters;
+    *converged = r.converged;
+  });
+}
+
+int ref_d_recover(int N, int H, int W, int K, const double* maps, int mh, int mw, const double* gamma,
+                  const double* mu, double* out) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    std::vector<SparseMaps> zs;
+    for (int n = 0; n < N; ++n) {
+      SparseMaps m(K, {H, W});
+      std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
+      zs.push_back(std::move(m));
+    }
+    LearningOperator op(zs, {mh, mw}, 1e-300);
+    const auto dk = d_recover(op, std::span<const double>(gamma, N * D), std::span<const double>(mu, K));
+    const std::size_t M = static_cast<std::size_t>(mh) * mw;
+    for (int k = 0; k < K; ++k) std::copy(dk[k].begin(), dk[k].end(), out + k * M);
+  });
+}
+
 // LearningOperator::correlation (learning.cpp:124-134) for every filter: out K*M.
 int ref_learning_correlation(int N, int H, int W, int K, const double* maps, int mh, int mw, const double* v,
                              double* out) {

@@ -286,6 +286,10 @@ class EngineBase {
   virtual void learning_data_term(const double* d, double* data) = 0;
   virtual void reconstruct(const double* d, int n0, int n1, double* out) = 0;
   virtual void learning_correlation(const double* v, double* out) = 0;
+  virtual void dictionary_adjoint(int n0, int n1, const double* lam, double* out) = 0;
+  virtual void lambda_update_op(int n0, int n1, const double* theta, const double* z, double* out) = 0;
+  virtual void gamma_solve_op(int channel, const double* mu, double* gamma, int* iters, int* converged) = 0;
+  virtual void d_recover_op(int channel, const double* gamma, const double* mu, double* out) = 0;
   virtual void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) = 0;
   virtual void synchronize() = 0;
   virtual void set_profiling(int on) = 0;
@@ -1294,6 +1298,119 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
   }
 
+  // ---------------------------------------------------------- stateless ops
+  // (coding.hpp:45-66, learning.hpp:81-95), for replaying iterations; they
+  // leave the context's coding and learning state untouched.
+
+  // D^T lambda: apply_dictionary_adjoint (coding.cpp:126-135), J > 1
+  // block_dictionary_adjoint (tcsc.cpp:185-193). lam (n1-n0) x J x D -> out (n1-n0) x K x D.
+  void dictionary_adjoint(int n0, int n1, const double* lam, double* out) override {
+    check_range(n0, n1);
+    const size_t JD = (size_t)J_ * D, KD = (size_t)K_ * D;
+    DevMem lin, lh, th, tout;
+    lin.alloc(sizeof(double) * JD);
+    lh.alloc(sizeof(C) * (size_t)J_ * NB);
+    th.alloc(sizeof(C) * (size_t)K_ * NB);
+    tout.alloc(sizeof(double) * KD);
+    for (int i = 0; i < n1 - n0; ++i) {
+      CK(cudaMemcpyAsync(lin.p, lam + i * JD, sizeof(double) * JD, cudaMemcpyHostToDevice, st_));
+      r2c(lin.p, true, D, lh.as<C>(), NB, J_);
+      launch(kFamOther, [&] {
+        adjoint_spectra<R><<<dim3((NB + 255) / 256, K_), 256, 0, st_>>>(dhat_.as<C>(), lh.as<C>(), th.as<C>(), K_,
+                                                                       J_, NB);
+      });
+      c2r<double>(th.as<C>(), NB, tout.as<double>(), D, K_);
+      CK(cudaMemcpyAsync(out + i * KD, tout.p, sizeof(double) * KD, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+  }
+
+  // lambda_update (coding.cpp:103-124; J > 1 lambda_update_blocked,
+  // tcsc.cpp:162-183) from theta, z ((n1-n0) x K x D each) against the
+  // context's signals and dictionary: out (n1-n0) x J x D.
+  void lambda_update_op(int n0, int n1, const double* theta, const double* z, double* out) override {
+    check_range(n0, n1);
+    const size_t KD = (size_t)K_ * D, JD = (size_t)J_ * D;
+    std::vector<double> w(KD);
+    DevMem win, wh, lh, lout;
+    win.alloc(sizeof(double) * KD);
+    wh.alloc(sizeof(C) * (size_t)K_ * NB);
+    lh.alloc(sizeof(C) * (size_t)J_ * NB);
+    lout.alloc(sizeof(double) * JD);
+    const double inv_rho = 1.0 / cfg_.rho;
+    for (int i = 0; i < n1 - n0; ++i) {
+      for (size_t q = 0; q < KD; ++q) w[q] = theta[i * KD + q] + z[i * KD + q] * inv_rho;  // coding.cpp:224-227
+      CK(cudaMemcpyAsync(win.p, w.data(), sizeof(double) * KD, cudaMemcpyHostToDevice, st_));
+      r2c(win.p, true, D, wh.as<C>(), NB, K_);
+      const int n = n0 + i;
+      launch(kFamOther, [&] {
+        if (J_ == 1)
+          lambda_from_w<R><<<(NB + 255) / 256, 256, 0, st_>>>(wh.as<C>(), dhat_.as<C>(), xhat_.as<C>() + (size_t)n * NB,
+                                                               sigma_.as<R>(), lh.as<C>(), K_, NB, R(inv_rho));
+        else
+          tc_lambda<R><<<dim3((NB + 127) / 128, 1), 128, 0, st_>>>(wh.as<C>(), dhat_.as<C>(), ginv_.as<C>(),
+                                                                 xhat_.as<C>() + (size_t)n * NB, (size_t)N_ * NB,
+                                                                 lh.as<C>(), nullptr, K_, K_, J_, NB, R(inv_rho));
+      });
+      c2r<double>(lh.as<C>(), NB, lout.as<double>(), D, J_);
+      CK(cudaMemcpyAsync(out + i * JD, lout.p, sizeof(double) * JD, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+  }
+
+  // gamma_solve (learning.cpp:136-185) on channel `channel` with the given mu
+  // (clamped at the floor as LearningOperator::set_mu does); gamma (N x D) is
+  // the warm start on entry and the solution on exit.
+  void gamma_solve_op(int channel, const double* mu, double* gamma, int* iters, int* converged) override {
+    if (channel < 0 || channel >= J_) throw DimErr("channel out of range");
+    build_zhat();
+    const std::vector<double> keep_mu = mu_;
+    DevMem keep_g;
+    keep_g.alloc(sizeof(C) * (size_t)N_ * NB);
+    select_channel(channel);
+    CK(cudaMemcpyAsync(keep_g.p, gam_ch_, keep_g.bytes, cudaMemcpyDeviceToDevice, st_));
+    mu_.assign(mu, mu + K_);
+    for (double& m : mu_) m = std::max(m, cfg_.mu_floor);
+    upload_mu();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, gam_ch_, NB, N_);
+    double bn = 0.0;
+    for (int n = 0; n < N_; ++n) bn += xnorm2c_[(size_t)n * J_ + channel];
+    reduce_host(&bn, 1);
+    int it = 0;
+    bool conv = false;
+    gamma_solve(std::sqrt(bn), it, conv);
+    c2r<double>(gam_ch_, NB, tmp.as<double>(), D, N_);
+    CK(cudaMemcpyAsync(gamma, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(gam_ch_, keep_g.p, keep_g.bytes, cudaMemcpyDeviceToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    mu_ = keep_mu;
+    select_channel(0);
+    if (iters) *iters = it;
+    if (converged) *converged = conv ? 1 : 0;
+  }
+
+  // d_recover (learning.cpp:187-216) for one channel's gamma (N x D): out K x M
+  void d_recover_op(int channel, const double* gamma, const double* mu, double* out) override {
+    if (channel < 0 || channel >= J_) throw DimErr("channel out of range");
+    build_zhat();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
+    correlate_hat(r_.as<C>(), nullptr);
+    CK(cudaMemcpyAsync(dmu_.p, mu, sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
+                  dtw_.as<C>(), nullptr);
+    });
+    CK(cudaMemcpyAsync(out, dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+    upload_mu();  // the context's own mu back on the device
+    CK(cudaStreamSynchronize(st_));
+  }
+
   void learning_apply(const double* mu, const double* v, double* out) override {
     build_zhat();
     std::vector<double> keep = mu_;
@@ -1858,6 +1975,35 @@ int dcsc_cuda_learning(dcsc_cuda_ctx* ctx, double* d_out, dcsc_learning_stats* s
   CTX_CHECK
   return guarded([&] { ctx->eng->learning(d_out, stats); });
 }
+int dcsc_cuda_dictionary_adjoint(dcsc_cuda_ctx* ctx, int n0, int n1, const double* lambda, double* out) {
+  return guarded([&] {
+    if (!ctx || !lambda || !out) throw InvErr("null argument");
+    ctx->eng->dictionary_adjoint(n0, n1, lambda, out);
+  });
+}
+
+int dcsc_cuda_lambda_update(dcsc_cuda_ctx* ctx, int n0, int n1, const double* theta, const double* z, double* out) {
+  return guarded([&] {
+    if (!ctx || !theta || !z || !out) throw InvErr("null argument");
+    ctx->eng->lambda_update_op(n0, n1, theta, z, out);
+  });
+}
+
+int dcsc_cuda_gamma_solve(dcsc_cuda_ctx* ctx, int channel, const double* mu, double* gamma, int* iters,
+                          int* converged) {
+  return guarded([&] {
+    if (!ctx || !mu || !gamma) throw InvErr("null argument");
+    ctx->eng->gamma_solve_op(channel, mu, gamma, iters, converged);
+  });
+}
+
+int dcsc_cuda_d_recover(dcsc_cuda_ctx* ctx, int channel, const double* gamma, const double* mu, double* out) {
+  return guarded([&] {
+    if (!ctx || !gamma || !mu || !out) throw InvErr("null argument");
+    ctx->eng->d_recover_op(channel, gamma, mu, out);
+  });
+}
+
 int dcsc_cuda_learning_correlation(dcsc_cuda_ctx* ctx, const double* v, double* out) {
   return guarded([&] {
     if (!ctx || !v || !out) throw InvErr("null argument");

@@ -146,6 +146,37 @@ __global__ void tc_objective(const cx<R>* __restrict__ what, const cx<R>* __rest
   }
 }
 
+// Stateless-op helpers (coding.hpp:45-66). t_hat_k = sum_j conj(d_hat_jk)
+// lambda_hat_j for one image (D^T lambda spectra, K planes).
+template <class R>
+__global__ void adjoint_spectra(const cx<R>* __restrict__ dhat, const cx<R>* __restrict__ lamhat,
+                                cx<R>* __restrict__ out, int K, int J, int NB) {
+  using C = cx<R>;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (b >= NB) return;
+  C t = mk<C>(R(0), R(0));
+  for (int j = 0; j < J; ++j)
+    t = cadd(t, cmulc(dhat[((size_t)j * K + k) * NB + b], lamhat[(size_t)j * NB + b]));
+  out[(size_t)k * NB + b] = t;
+}
+
+// Single-channel lambda_hat = (sum_k d_hat_k w_hat_k - x_hat / rho) / sigma for
+// one image from its w_hat planes (lambda_from_w, coding.cpp:25-37).
+template <class R>
+__global__ void lambda_from_w(const cx<R>* __restrict__ what, const cx<R>* __restrict__ dhat,
+                              const cx<R>* __restrict__ xhat, const R* __restrict__ sigma, cx<R>* __restrict__ lamhat,
+                              int K, int NB, R inv_rho) {
+  using C = cx<R>;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= NB) return;
+  C acc = mk<C>(R(0), R(0));
+  for (int k = 0; k < K; ++k) acc = cadd(acc, cmul(dhat[(size_t)k * NB + b], what[(size_t)k * NB + b]));
+  const C xv = xhat[b];
+  const R s = sigma[b];
+  lamhat[b] = mk<C>((acc.x - xv.x * inv_rho) / s, (acc.y - xv.y * inv_rho) / s);
+}
+
 // Reconstruction spectrum y_n,j = sum_k d_hat_jk z_hat_nk (objective.cpp:39-57 in
 // the Fourier basis): J = 1 sums the coding pass's G group partials (fixed
 // order), J > 1 contracts the stored z_hat planes. out: N x J x NB.

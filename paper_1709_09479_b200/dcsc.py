@@ -137,6 +137,7 @@ EXPORTS = [
     "dcsc_io_last_error", "dcsc_io_write_tensor", "dcsc_io_read_tensor_header", "dcsc_io_read_tensor",
     "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing", "dcsc_cuda_reconstruct",
     "dcsc_synth_dataset", "dcsc_synth_generate_range", "dcsc_cuda_learning_correlation",
+    "dcsc_cuda_dictionary_adjoint", "dcsc_cuda_lambda_update", "dcsc_cuda_gamma_solve", "dcsc_cuda_d_recover",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -326,6 +327,35 @@ class Context:
         v = _f64(v)
         out = np.zeros_like(v)
         _err(lib().dcsc_cuda_learning_apply(self._h, _dp(mu), _dp(v), _dp(out)))
+        return out
+
+    # -- stateless ops (coding.hpp:45-66, learning.hpp:81-95)
+    def dictionary_adjoint(self, lam, n0=0, n1=None):
+        """D^T lambda (apply_dictionary_adjoint): lam (n, [J,] H, W) -> (n, K, H, W)."""
+        n1 = self.N if n1 is None else n1
+        lam = _f64(lam)
+        out = np.zeros((n1 - n0, self.K, self.H, self.W))
+        _err(lib().dcsc_cuda_dictionary_adjoint(self._h, n0, n1, _dp(lam), _dp(out)))
+        return out
+
+    def lambda_update(self, theta, z, n0=0, n1=None):
+        """lambda_update (coding.cpp:103-124): theta, z (n, K, H, W) -> lambda (n, [J,] H, W)."""
+        n1 = self.N if n1 is None else n1
+        out = np.zeros(self._sig_shape((n1 - n0,)))
+        _err(lib().dcsc_cuda_lambda_update(self._h, n0, n1, _dp(_f64(theta)), _dp(_f64(z)), _dp(out)))
+        return out
+
+    def gamma_solve(self, mu, gamma, channel=0):
+        """gamma_solve (learning.cpp:136-185): returns (gamma, iters, converged)."""
+        g = np.array(gamma, dtype=np.float64, copy=True).reshape(self.N, self.H, self.W)
+        it, conv = C.c_int(), C.c_int()
+        _err(lib().dcsc_cuda_gamma_solve(self._h, channel, _dp(_f64(mu)), _dp(g), C.byref(it), C.byref(conv)))
+        return g, it.value, bool(conv.value)
+
+    def d_recover(self, gamma, mu, channel=0):
+        """d_recover (learning.cpp:187-216): (K, mh, mw) for one channel's gamma."""
+        out = np.zeros((self.K, self.mh, self.mw))
+        _err(lib().dcsc_cuda_d_recover(self._h, channel, _dp(_f64(gamma)), _dp(_f64(mu)), _dp(out)))
         return out
 
     def learning_correlation(self, v):

@@ -307,3 +307,36 @@ def test_learning_correlation_fp64_matches_reference():
         ctx.set_maps(maps)
         out_g = ctx.learning_correlation(v)
     assert rel(out_g, out_r) <= 1e-12
+
+
+# ---------------------------------------------------------------- stateless ops (coding.hpp:45-66, learning.hpp:81-95)
+def test_stateless_coding_ops_fp64_match_reference():
+    x, d = problem(2, (20, 20), 4, 5)
+    rng = np.random.default_rng(11)
+    theta = rng.standard_normal((2, 4, 20, 20)) * 0.1
+    z = rng.standard_normal((2, 4, 20, 20)) * 0.1
+    lam = rng.standard_normal((2, 20, 20))
+    with dcsc.Context(2, (20, 20), 4, (5, 5), dcsc.SolverConfig(rho=0.3, normalize=0), 64) as ctx:
+        ctx.set_signals(x)
+        ctx.set_dictionary(d)
+        lg = ctx.lambda_update(theta, z)
+        tg = ctx.dictionary_adjoint(lam)
+    for n in range(2):
+        assert rel(lg[n], ref.lambda_update(x[n], d, theta[n], z[n], 0.3)) <= 1e-12
+        assert rel(tg[n], ref.dictionary_adjoint(d, lam[n])) <= 1e-12
+
+
+def test_stateless_learning_ops_fp64_match_reference():
+    x, d = problem(3, (16, 20), 4, 5)
+    maps = coded_maps(x, d, 0.1)
+    mu = np.array([1.0, 0.3, 2.0, 0.7])
+    g0 = np.zeros_like(x)
+    with dcsc.Context(3, (16, 20), 4, (5, 5), dcsc.SolverConfig(normalize=0), 64) as ctx:
+        ctx.set_signals(x)
+        ctx.set_maps(maps)
+        g_g, it_g, cv_g = ctx.gamma_solve(mu, g0)
+        g_r, it_r, cv_r = ref.gamma_solve(maps, (5, 5), mu, 1e-6, x, 1e-6, 300, g0)
+        d_g = ctx.d_recover(g_r, mu)  # same gamma on both sides
+    assert cv_g == cv_r and abs(it_g - it_r) <= 2
+    assert rel(g_g, g_r) <= 1e-7  # CG stops at rel. residual 1e-6 (learning.cpp:156)
+    assert rel(d_g, ref.d_recover(maps, (5, 5), g_r, mu)) <= 1e-12
