@@ -734,7 +734,7 @@ contract_c(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ v, double2*
       const C x = __ldg(v + (size_t)n * NB + b);
       C z[KC];
 #pragma unroll
-      for (int q = 0; q < KC; ++q) z[q] = __ldg(zp + (size_t)n * zs + (size_t)q * NB);
+      for (int q = 0; q < KC; ++q) z[q] = __ldcs(zp + (size_t)n * zs + (size_t)q * NB);
 #pragma unroll
       for (int q = 0; q < KC; ++q) {
         ar[q] += (double)z[q].x * (double)x.x + (double)z[q].y * (double)x.y;
@@ -906,7 +906,7 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
       C z[U], q[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        z[u] = __ldg(zp + (size_t)(k + u) * NB);
+        z[u] = __ldcs(zp + (size_t)(k + u) * NB);  // streaming: keep p_hat resident in L2
         q[u] = __ldg(pp + (size_t)(k + u) * NB);
       }
 #pragma unroll
@@ -917,7 +917,7 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
       }
     }
     for (; k < K; ++k) {
-      const C z = __ldg(zp + (size_t)k * NB);
+      const C z = __ldcs(zp + (size_t)k * NB);
       const C q = __ldg(pp + (size_t)k * NB);
       const double w = mode == 0 ? wk[k] : 1.0;
       ar += w * ((double)z.x * (double)q.x - (double)z.y * (double)q.y);
