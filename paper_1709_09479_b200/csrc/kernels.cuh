@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
 #pragma unroll
           for (int s = 0; s < RX; ++s) {
             C* up = (STAGE ? U : uk) + (j + s * J) * H + r;
-            const C uv = *up;
+            const C uv = STAGE ? *up : __ldcs(up);  // u streams through once: evict-first
             const R tv[2] = {x[s].x * invD, x[s].y * invD};
             const R uo[2] = {uv.x, uv.y};
             R wv[2], un2[2];
@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
               wv[e] = th + ez;                           // w = theta' + z'/rho
               un2[e] = un;
             }
-            *up = mk<C>(un2[0], un2[1]);
+            if constexpr (STAGE) *up = mk<C>(un2[0], un2[1]);
+            else __stcs(up, mk<C>(un2[0], un2[1]));
             x[s] = mk<C>(wv[0], wv[1]);
           }
           dft<RX, false>(x);  // first forward row stage (NS = 1)

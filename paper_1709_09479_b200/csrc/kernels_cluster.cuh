@@ -164,7 +164,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
 #pragma unroll 4
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
         const int rl = it / M, m = it % M;
-        const C uv = uk[it];
+        const C uv = __ldcs(uk + it);  // u streams through once: evict-first (keeps d_hat, lambda_hat in L2)
         const C v = Z[rl * Wh + m];
         const R tv[2] = {v.x * invD, v.y * invD};
         const R uo[2] = {uv.x, uv.y};
@@ -189,7 +189,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
           wv[e] = R(2) * th - un;
           un2[e] = un;
         }
-        uk[it] = mk<C>(un2[0], un2[1]);
+        __stcs(uk + it, mk<C>(un2[0], un2[1]));
         Z[rl * Wh + m] = mk<C>(wv[0], wv[1]);
       }
       s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
