@@ -10,6 +10,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -52,26 +53,34 @@ def build(verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     nvcc = _nvcc()
     hdrs = _headers()
-    objs = []
+    objs, jobs = [], []
     for src in sorted(os.listdir(CSRC)):
         path = os.path.join(CSRC, src)
+        if not src.endswith((".cu", ".cpp")):
+            continue
+        obj = os.path.join(OBJDIR, src + ".o")
+        objs.append(obj)
+        if not _stale(obj, [path] + hdrs):
+            continue
         if src.endswith(".cu"):
-            obj = os.path.join(OBJDIR, src + ".o")
-            if _stale(obj, [path] + hdrs):
-                cmd = [nvcc, "-c", path, "-o", obj] + NVCC_FLAGS + ["-ccbin", HOST_CXX]
-                log = os.path.join(OBJDIR, src + ".ptxas.log")
-                with open(log, "w") as f:
-                    r = subprocess.run(cmd, stdout=f, stderr=subprocess.STDOUT)
-                if r.returncode != 0:
-                    sys.stderr.write(open(log).read()[-20000:])
-                    raise RuntimeError(f"nvcc failed on {src}")
-            objs.append(obj)
-        elif src.endswith(".cpp"):
-            obj = os.path.join(OBJDIR, src + ".o")
-            if _stale(obj, [path] + hdrs):
-                cmd = [HOST_CXX, "-c", path, "-o", obj, "-O3", "-fPIC", "-fopenmp", "-std=c++17", "-I" + INC, "-I" + CSRC]
-                subprocess.run(cmd, check=True)
-            objs.append(obj)
+            cmd = [nvcc, "-c", path, "-o", obj] + NVCC_FLAGS + ["-ccbin", HOST_CXX]
+        else:
+            cmd = [HOST_CXX, "-c", path, "-o", obj, "-O3", "-fPIC", "-fopenmp", "-std=c++17", "-I" + INC, "-I" + CSRC]
+        jobs.append((src, cmd))
+
+    def run(job):
+        src, cmd = job
+        log = os.path.join(OBJDIR, src + ".build.log")
+        with open(log, "w") as f:
+            r = subprocess.run(cmd, stdout=f, stderr=subprocess.STDOUT)
+        return src, r.returncode, log
+
+    # the per-grid engine units (inst_*.cu) are independent: compile in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for src, rc, log in ex.map(run, jobs):
+            if rc != 0:
+                sys.stderr.write(open(log).read()[-20000:])
+                raise RuntimeError(f"compile failed on {src}")
     if _stale(LIB, objs):
         cmd = [nvcc, "-shared", "-o", LIB] + objs + ARCH + ["-ccbin", HOST_CXX, "-Xcompiler", "-fopenmp", "-lgomp"]
         subprocess.run(cmd, check=True)

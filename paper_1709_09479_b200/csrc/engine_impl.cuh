@@ -1,0 +1,1677 @@
+// Engine<R, H, W>: host orchestration of the B200 dual-domain CSC path for one
+// compiled grid/precision. Included by the per-grid instantiation units
+// (inst_*.cu) so the kernel families compile in parallel; the C-ABI lives in
+// engine.cu. One Engine keeps every hot-path buffer device-resident; the host
+// only makes the discrete decisions the reference makes on scalars (stop tests,
+// acceptance, the mu settle test) from FP64 reductions read back per iteration.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dcsc_cuda.h"
+#include "kernels.cuh"
+#include "kernels_cluster.cuh"
+#include "tcsc_kernels.cuh"
+
+using namespace dcsc_cuda;
+#include "engine_shared.h"
+
+using namespace dcsc_engine;
+
+namespace {
+
+double now_ms() {
+  using clock = std::chrono::steady_clock;
+  return std::chrono::duration<double, std::milli>(clock::now().time_since_epoch()).count();
+}
+
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b) {
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    bytes = b;
+    if (b) CK(cudaMalloc(&p, b));
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+void validate_cfg(const dcsc_solver_config& c) {  // types.cpp:106-114
+  if (!(c.beta > 0)) throw InvErr("beta must be > 0");
+  if (!(c.rho > 0)) throw InvErr("rho must be > 0");
+  if (!(c.tol > 0)) throw InvErr("tol must be > 0");
+  if (!(c.mu_floor > 0)) throw InvErr("mu_floor must be > 0");
+  if (c.max_outer < 0 || c.max_admm < 1 || c.max_mu_iters < 1 || c.cg_max < 1)
+    throw InvErr("iteration caps must be positive");
+  if (!(c.cg_tol > 0)) throw InvErr("cg_tol must be > 0");
+}
+
+void require_finite(const double* v, size_t n, const char* what) {  // types.cpp:26-29
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) throw NumErr(std::string(what) + " contains a non-finite value");
+}
+
+constexpr double kFilterNormTol = 1e-3;  // learning.cpp:14
+
+// Kernel families for the per-launch CUDA-event profiler.
+enum Family { kFamCoding = 0, kFamLambda = 1, kFamContract = 2, kFamMask = 3, kFamOther = 4, kFamCount = 5 };
+
+// Circular Gaussian blur (sigma in samples, truncated at 4 sigma) along both
+// axes, as pipeline.cpp:26-57 does for local contrast normalisation.
+std::vector<double> gaussian_blur(int H, int W, const double* v, double sigma) {
+  const int radius = static_cast<int>(std::ceil(4.0 * sigma));
+  std::vector<double> ker(2 * radius + 1);
+  double ks = 0.0;
+  for (int i = -radius; i <= radius; ++i) {
+    ker[i + radius] = std::exp(-0.5 * (i * i) / (sigma * sigma));
+    ks += ker[i + radius];
+  }
+  for (double& k : ker) k /= ks;
+  std::vector<double> cur(v, v + (size_t)H * W), next(cur.size());
+  const int dims[2] = {H, W};
+  for (int axis = 0; axis < 2; ++axis) {
+    const int n = dims[axis];
+    for (int r = 0; r < H; ++r)
+      for (int c = 0; c < W; ++c) {
+        double acc = 0.0;
+        const int c0 = axis == 0 ? r : c;
+        for (int i = -radius; i <= radius; ++i) {
+          int cc = (c0 + i) % n;
+          if (cc < 0) cc += n;
+          acc += ker[i + radius] * (axis == 0 ? cur[(size_t)cc * W + c] : cur[(size_t)r * W + cc]);
+        }
+        next[(size_t)r * W + c] = acc;
+      }
+    cur.swap(next);
+  }
+  return cur;
+}
+
+// dcsc::normalize (pipeline.cpp:78-121) for one J-channel image: Global uses
+// the mean / std of all J*D values, Local runs per channel.
+void normalize_image(int mode, int H, int W, const double* in, double* out, int J = 1) {
+  if (mode == 2 && J > 1) {
+    for (int j = 0; j < J; ++j)
+      normalize_image(mode, H, W, in + (size_t)j * H * W, out + (size_t)j * H * W, 1);
+    return;
+  }
+  const size_t D = (size_t)H * W * J;  // None / Global act on all J*D values
+  if (mode == 0) {
+    std::copy(in, in + D, out);
+    return;
+  }
+  if (mode == 1) {
+    double m = 0.0;
+    for (size_t i = 0; i < D; ++i) m += in[i];
+    m /= (double)D;
+    double var = 0.0;
+    for (size_t i = 0; i < D; ++i) var += (in[i] - m) * (in[i] - m);
+    const double sd = std::sqrt(var / (double)D);
+    if (sd < 1e-8) {
+      std::fill(out, out + D, 0.0);
+      return;
+    }
+    for (size_t i = 0; i < D; ++i) out[i] = (in[i] - m) / sd;
+    return;
+  }
+  const std::vector<double> lm = gaussian_blur(H, W, in, 3.0);
+  std::vector<double> sq(D);
+  for (size_t i = 0; i < D; ++i) sq[i] = in[i] * in[i];
+  const std::vector<double> ls = gaussian_blur(H, W, sq.data(), 3.0);
+  std::vector<double> lsd(D);
+  double fl = 0.0;
+  for (size_t i = 0; i < D; ++i) {
+    lsd[i] = std::sqrt(std::max(ls[i] - lm[i] * lm[i], 0.0));
+    fl += lsd[i];
+  }
+  fl /= (double)D;
+  if (fl < 1e-8) {
+    for (size_t i = 0; i < D; ++i) out[i] = in[i] - lm[i];
+    return;
+  }
+  for (size_t i = 0; i < D; ++i) out[i] = (in[i] - lm[i]) / std::max(lsd[i], fl);
+}
+
+
+constexpr int pick_threads(int H, int W) { return H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128); }
+
+// Kernel family per compiled grid: one CTA per plane (Plane), or a 4-CTA
+// cluster per plane (ClusterPlane) when the half spectrum exceeds smem.
+template <class R, int H, int W>
+struct KernelFamily {
+  static constexpr bool cluster = false;
+  static constexpr int CL = 1;
+  using P = Plane<R, H, W, pick_threads(H, W)>;
+};
+template <>
+struct KernelFamily<float, 256, 256> {
+  static constexpr bool cluster = true;
+#ifndef DCSC_CL256
+#define DCSC_CL256 4
+#endif
+  static constexpr int CL = DCSC_CL256;
+  using P = ClusterPlane<float, 256, 256, CL, (CL == 8 ? 256 : 512)>;
+};
+
+template <class R, int H, int W>
+class Engine final : public EngineBase {
+ public:
+  using F = KernelFamily<R, H, W>;
+  using P = typename F::P;
+  static constexpr bool CLU = F::cluster;
+  static constexpr int CLN = F::CL;
+  static constexpr int T = P::T;
+  using C = cx<R>;
+  static constexpr int NB = P::NB, D = P::D, Wh = P::Wh;
+  static constexpr int TBV = 256;  // block size of the streaming kernels
+
+  template <class Q = P>
+  static constexpr size_t smem_coding() {
+    if constexpr (CLU) return SmemCl<Q>::coding; else return Smem<Q>::coding;
+  }
+  template <class Q = P>
+  static constexpr size_t smem_plain() {
+    if constexpr (CLU) return SmemCl<Q>::plain; else return Smem<Q>::two;
+  }
+  template <int MODE>
+  static void launch_coding(int G, int cnt, cudaStream_t st, const CodingArgs<R>& a) {
+    if constexpr (CLU) {
+      coding_pass_cl<P, MODE><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
+    } else {
+      if (MODE == kPassAdmm && a.J == 2)  // common channel counts: compile-time loops
+        coding_pass<P, MODE, true, 2><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else if (MODE == kPassAdmm && a.J == 3)
+        coding_pass<P, MODE, true, 3><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else if (MODE == kPassAdmm && a.J == 4)
+        coding_pass<P, MODE, true, 4><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else if (a.J > 1)
+        coding_pass<P, MODE, true><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+      else
+        coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
+    }
+  }
+  template <class SRC>
+  static void launch_r2c(int count, cudaStream_t st, const SRC* src, size_t ss, C* dst, size_t ds, const C* tw,
+                         int* live, int live_mod) {
+    if constexpr (CLU)
+      r2c_planes_cl<P, SRC><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
+    else
+      r2c_planes<P, SRC><<<count, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
+  }
+  template <class DST>
+  static void launch_c2r(int count, cudaStream_t st, const C* src, size_t ss, DST* dst, size_t ds, const C* tw) {
+    if constexpr (CLU)
+      c2r_planes_cl<P, DST><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
+    else
+      c2r_planes<P, DST><<<count, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
+  }
+  static void launch_filters(int K, cudaStream_t st, const double* d, int mh, int mw, C* dst, const C* tw) {
+    if constexpr (CLU)
+      r2c_filters_cl<P><<<K * CLN, T, smem_plain(), st>>>(d, mh, mw, dst, tw);
+    else
+      r2c_filters<P><<<K, T, smem_plain(), st>>>(d, mh, mw, dst, tw);
+  }
+  static void launch_mask(int K, cudaStream_t st, const C* c, C* phat, double* d_out, const int* live,
+                          const double* mu, int mh, int mw, int mode, const C* tw, const int* done) {
+    if constexpr (CLU)
+      mask_step_cl<P><<<K * CLN, T, smem_plain(), st>>>(c, phat, d_out, live, mu, mh, mw, mode, tw, done);
+    else
+      mask_step<P><<<K, T, smem_plain(), st>>>(c, phat, d_out, live, mu, mh, mw, mode, tw, done);
+  }
+  static void set_attributes() {
+    auto big = [](const void* fn, size_t bytes) {
+      if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    };
+    if constexpr (CLU) {
+      big((const void*)coding_pass_cl<P, kPassAdmm>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassPrologue>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassObjective>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassMaps>, smem_coding());
+      big((const void*)r2c_planes_cl<P, R>, smem_plain());
+      big((const void*)r2c_planes_cl<P, double>, smem_plain());
+      big((const void*)c2r_planes_cl<P, R>, smem_plain());
+      big((const void*)c2r_planes_cl<P, double>, smem_plain());
+      big((const void*)r2c_filters_cl<P>, smem_plain());
+      big((const void*)mask_step_cl<P>, smem_plain());
+    } else {
+      big((const void*)coding_pass<P, kPassAdmm>, smem_coding());
+      big((const void*)coding_pass<P, kPassPrologue>, smem_coding());
+      big((const void*)coding_pass<P, kPassObjective>, smem_coding());
+      big((const void*)coding_pass<P, kPassMaps>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true, 2>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true, 3>, smem_coding());
+      big((const void*)coding_pass<P, kPassAdmm, true, 4>, smem_coding());
+      big((const void*)coding_pass<P, kPassPrologue, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassObjective, true>, smem_coding());
+      big((const void*)coding_pass<P, kPassMaps, true>, smem_coding());
+      big((const void*)r2c_planes<P, R>, smem_plain());
+      big((const void*)r2c_planes<P, double>, smem_plain());
+      big((const void*)c2r_planes<P, R>, smem_plain());
+      big((const void*)c2r_planes<P, double>, smem_plain());
+      big((const void*)r2c_filters<P>, smem_plain());
+      big((const void*)mask_step<P>, smem_plain());
+    }
+  }
+
+  explicit Engine(const dcsc_cuda_opts& o) : o_(o), cfg_(o.cfg) {
+    N_ = o.n_images;
+    K_ = o.filters;
+    J_ = std::max(1, o.channels);
+    if (J_ > kMaxChannels) throw DimErr("at most " + std::to_string(kMaxChannels) + " channels are supported");
+    if (J_ > 1 && CLU) throw DimErr("multi-channel (TCSC) coding is not compiled for the cluster grid family");
+    if constexpr (CLU) {  // the cropped support must sit in the first rank's row block
+      if (o.support_h > P::ROWS)
+        throw DimErr("filter support taller than " + std::to_string(P::ROWS) + " rows on the cluster grid family");
+    }
+    mh_ = o.support_h;
+    mw_ = o.support_w;
+    M_ = mh_ * mw_;
+    CK(cudaSetDevice(o.device));
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&pin_, 1 << 20));
+    setup_attributes();
+    // Filter groups per image: a CTA runs kpg filters; pick G minimising the
+    // makespan ceil(N*G / slots) * (ceil(K/G) + 1): wave quantisation plus a
+    // per-CTA overhead of about one filter's worth (partial spectrum write and
+    // re-read, twiddles, the epilogue). Ties -> fewer groups.
+    {
+      int sms = 148, per_sm = 1;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      long slots;
+      if constexpr (CLU) {
+        // clusters must sit inside one GPC: ask the runtime how many fit at
+        // once (4-CTA clusters strand SMs on GPCs whose SM count is not a
+        // multiple of 4) instead of assuming sms / CLN
+        slots = sms / CLN;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(CLN, 1, 1);
+        lc.blockDim = dim3(T, 1, 1);
+        lc.dynamicSmemBytes = smem_coding();
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)coding_pass_cl<P, kPassAdmm>, &lc) == cudaSuccess && ncl > 0)
+          slots = ncl;
+        cudaGetLastError();
+      } else {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coding_pass<P, kPassAdmm>, T, smem_coding()));
+        slots = (long)sms * std::max(per_sm, 1);
+      }
+      long best = -1;
+      int bestG = 1;
+      for (int G = 1; G <= K_; ++G) {
+        const int kpg = (K_ + G - 1) / G;
+        if ((K_ + kpg - 1) / kpg != G) continue;  // G must be realisable
+        const long waves = ((long)N_ * G + slots - 1) / slots;
+        const long span = waves * (kpg + 1);
+        if (best < 0 || span < best) {
+          best = span;
+          bestG = G;
+        }
+      }
+      if (const char* e = std::getenv("DCSC_GROUPS")) {  // experiment override
+        const int g = std::atoi(e);
+        if (g >= 1 && g <= K_) bestG = g;
+      }
+      kpg_ = (K_ + bestG - 1) / bestG;
+      G_ = (K_ + kpg_ - 1) / kpg_;
+      if (std::getenv("DCSC_VERBOSE"))
+        std::fprintf(stderr, "dcsc: N=%d K=%d slots=%ld groups G=%d (%d filters per CTA)\n", N_, K_, slots, G_, kpg_);
+    }
+    // twiddles (forward roots) in long double, rounded once
+    std::vector<C> tw(P::TW_LEN);
+    fill_twiddles<P>(tw.data());
+    dtw_.alloc(sizeof(C) * P::TW_LEN);
+    CK(cudaMemcpy(dtw_.p, tw.data(), sizeof(C) * P::TW_LEN, cudaMemcpyHostToDevice));
+
+    const size_t nD = (size_t)N_ * D, nNB = (size_t)N_ * NB;
+    x_.alloc(sizeof(R) * nD * J_);                    // N x J x D
+    xhat_.alloc(sizeof(C) * nNB * J_);                // J x N x NB (channel-major)
+    dhat_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);    // J x K x NB (channel-major)
+    dcand_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);
+    sigma_.alloc(sizeof(R) * NB);
+    u_.alloc(sizeof(R) * nD * K_);
+    maps_.alloc(sizeof(R) * nD * K_);
+    lamhat_.alloc(sizeof(C) * nNB * J_);              // N x J x NB
+    lam_.alloc(sizeof(R) * nD * J_);                  // N x J x D
+    if (J_ > 1) {
+      ginv_.alloc(sizeof(C) * (size_t)NB * J_ * J_);
+      what_.alloc(sizeof(C) * nNB * K_);
+    }
+    part_.alloc(sizeof(C) * (size_t)N_ * G_ * NB);
+    sums_.alloc(sizeof(double) * (size_t)N_ * G_ * CLN * kSums);
+    conv_.alloc(sizeof(int) * N_);
+    cnt_.alloc(sizeof(unsigned) * N_);
+    CK(cudaMemset(cnt_.p, 0, cnt_.bytes));
+    img_.alloc(sizeof(ImageAdmm) * N_);
+    dual_.alloc(sizeof(double) * N_);
+    infeas_.alloc(sizeof(double) * N_);
+    resc_.alloc(sizeof(int) * N_);
+    odata_.alloc(sizeof(double) * N_);
+    ol1_.alloc(sizeof(double) * N_);
+    accept_.alloc(sizeof(int) * N_);
+    gam_.alloc(sizeof(C) * nNB * J_);                 // J x N x NB
+    r_.alloc(sizeof(C) * nNB);
+    p_.alloc(sizeof(C) * nNB);
+    ap_.alloc(sizeof(C) * nNB);
+    cvec_.alloc(sizeof(C) * (size_t)K_ * NB);
+    // contract_c splits the image sum only as far as needed to fill the GPU
+    // (~4 CTAs of 256 threads per SM): every split adds a K x NB FP64 partial
+    // plane written and re-read per CG apply (C3: 1 GB at 16 splits)
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      const long base = (long)((NB + TBV - 1) / TBV) * ((K_ + 7) / 8);
+      const double want = std::max(1.0, 4.0 * sms / (double)base);
+      const long p2 = 1L << (int)std::lround(std::log2(want));  // nearest power of two (measured: C4 16 > 17)
+      csplit_ = (int)std::max(1L, std::min({p2, 64L, (long)N_}));
+    }
+    if (const char* e = std::getenv("DCSC_CSPLIT")) csplit_ = std::max(1, std::min(N_, std::atoi(e)));
+    cpart_.alloc(sizeof(double2) * (size_t)csplit_ * K_ * NB);
+    phat_.alloc(sizeof(C) * (size_t)K_ * NB);
+    live_.alloc(sizeof(int) * K_);
+    dmu_.alloc(sizeof(double) * K_);
+    dwk_.alloc(sizeof(double) * K_);
+    dd_.alloc(sizeof(double) * (size_t)K_ * M_);
+    ddict_.alloc(sizeof(double) * (size_t)J_ * K_ * M_);
+    cg_.alloc(sizeof(CgState));
+    cgcnt_.alloc(sizeof(unsigned) * 2);
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+      fused_rows_ = 8 * sms;  // blocks of a fused CG launch: ~8 resident x 256 threads per SM
+    }
+    no_cg_fuse_ = std::getenv("DCSC_NO_CG_FUSE") != nullptr;
+    CK(cudaMemsetAsync(cgcnt_.p, 0, cgcnt_.bytes, st_));
+    hred_.alloc(sizeof(double) * std::max(64, K_ + 8));
+    cglob_.alloc(sizeof(double2) * (size_t)K_ * NB);
+    tiles_ = (NB + TBV - 1) / TBV;
+    const size_t vec_blocks = (nNB + TBV - 1) / TBV;
+    accept_chunks_ = std::max(1, std::min(64, (int)((size_t)K_ * D / (TBV * 8))));
+    const size_t np = std::max({(size_t)N_ * tiles_, vec_blocks, (size_t)N_ * accept_chunks_});
+    partial_.alloc(sizeof(double) * np);
+    partial2_.alloc(sizeof(double) * (size_t)N_ * accept_chunks_);
+    l0_.alloc(sizeof(unsigned long long) * (size_t)N_ * accept_chunks_);
+    device_bytes = x_.bytes + xhat_.bytes + dhat_.bytes + dcand_.bytes + sigma_.bytes + u_.bytes +
+                   maps_.bytes + lamhat_.bytes + lam_.bytes + part_.bytes + sums_.bytes + gam_.bytes +
+                   3 * r_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes + ginv_.bytes + what_.bytes;
+    CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
+    CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
+    CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
+    CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    CK(cudaMemsetAsync(x_.p, 0, x_.bytes, st_));
+    CK(cudaMemsetAsync(xhat_.p, 0, xhat_.bytes, st_));
+    dict_.assign((size_t)K_ * J_ * M_, 0.0);
+    u_zero_.assign(N_, 1);
+    mu_.assign(K_, 1.0);
+    xnorm2_.assign(N_, 0.0);
+    xnorm2c_.assign((size_t)N_ * J_, 0.0);
+    xh_ch_ = xhat_.as<C>();
+    gam_ch_ = gam_.as<C>();
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  ~Engine() override {
+    for (auto& e : evpool_) cudaEventDestroy(e);
+    for (auto& e : marks_)
+      if (e) cudaEventDestroy(e);
+    if (pin_) cudaFreeHost(pin_);
+    if (xstage_) cudaFreeHost(xstage_);
+    if (st_) cudaStreamDestroy(st_);
+  }
+
+  // ------------------------------------------------------------ launches
+  // per-launch profiling events come from a pool reused across profiling
+  // windows (creating two events per launch costs microseconds of host time,
+  // which shows up in wall-clock traces of launch-dense phases)
+  cudaEvent_t pooled_event() {
+    if (evused_ == evpool_.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      evpool_.push_back(e);
+    }
+    return evpool_[evused_++];
+  }
+  template <class F>
+  void launch(int fam, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    const bool prof = profiling_ == 1 || (profiling_ == 2 && fam == kFamCoding);
+    if (prof) {
+      a = pooled_event();
+      b = pooled_event();
+      CK(cudaEventRecord(a, st_));
+    }
+    f();
+    CK(cudaGetLastError());
+    if (prof) {
+      CK(cudaEventRecord(b, st_));
+      prof_.push_back({fam, a, b});
+    }
+    ++launches;
+  }
+
+  void setup_attributes() { set_attributes(); }
+
+  CodingArgs<R> cargs(const C* dhat, int n_off) {
+    CodingArgs<R> a;
+    a.dhat = dhat;
+    a.J = J_;
+    a.what = what_.as<C>() ? what_.as<C>() + (size_t)n_off * K_ * NB : nullptr;
+    a.u = u_.as<R>() + (size_t)n_off * K_ * D;
+    a.maps = maps_.as<R>() + (size_t)n_off * K_ * D;
+    a.part = part_.as<C>() + (size_t)n_off * G_ * NB;
+    a.sums = sums_.as<double>() + (size_t)n_off * G_ * CLN * kSums;
+    a.conv = conv_.as<int>() + n_off;
+    a.lamhat = lamhat_.as<C>() + (size_t)n_off * J_ * NB;
+    a.K = K_;
+    a.G = G_;
+    a.kpg = kpg_;
+    a.rho = R(cfg_.rho);
+    a.beta = R(cfg_.beta);
+    a.tw = dtw_.as<C>();
+    a.cnt = cnt_.as<unsigned>() + n_off;
+    a.conv_w = conv_.as<int>() + n_off;
+    a.xhat = xhat_.as<C>() + (size_t)n_off * NB;
+    a.sigma = sigma_.as<R>();
+    a.lamhat_w = lamhat_.as<C>() + (size_t)n_off * J_ * NB;
+    a.img = img_.as<ImageAdmm>() + n_off;
+    a.iter = 0;
+    a.is_last = 0;
+    return a;
+  }
+
+  template <int MODE>
+  void coding_launch(const C* dhat, int n0, int cnt, int iter = 0, int is_last = 0) {
+    CodingArgs<R> a = cargs(dhat, n0);
+    a.iter = iter;
+    a.is_last = is_last;
+    launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] { launch_coding<MODE>(G_, cnt, st_, a); });
+  }
+
+  void r2c(const void* src, bool src_double, size_t src_stride, C* dst, size_t dst_stride, int count,
+           int* live = nullptr, int live_mod = 1) {
+    if (count <= 0) return;
+    launch(kFamOther, [&] {
+      if (src_double)
+        launch_r2c<double>(count, st_, static_cast<const double*>(src), src_stride, dst, dst_stride, dtw_.as<C>(),
+                           live, live_mod);
+      else
+        launch_r2c<R>(count, st_, static_cast<const R*>(src), src_stride, dst, dst_stride, dtw_.as<C>(), live,
+                      live_mod);
+    });
+  }
+
+  template <class DST>
+  void c2r(const C* src, size_t src_stride, DST* dst, size_t dst_stride, int count) {
+    if (count <= 0) return;
+    launch(kFamOther, [&] { launch_c2r<DST>(count, st_, src, src_stride, dst, dst_stride, dtw_.as<C>()); });
+  }
+
+  // host dictionary K x J x M (Dictionary::filter(k, j), types.cpp:60-68) ->
+  // device spectra J x K x NB (channel-major: channel j's K planes contiguous)
+  void upload_dict_spectra(const double* d, C* dst) {
+    const double* src = d;
+    if (J_ > 1) {
+      dstage_.resize((size_t)J_ * K_ * M_);
+      for (int k = 0; k < K_; ++k)
+        for (int j = 0; j < J_; ++j)
+          std::copy(d + ((size_t)k * J_ + j) * M_, d + ((size_t)k * J_ + j + 1) * M_,
+                    dstage_.data() + ((size_t)j * K_ + k) * M_);
+      src = dstage_.data();
+    }
+    CK(cudaMemcpyAsync(ddict_.p, src, sizeof(double) * J_ * K_ * M_, cudaMemcpyHostToDevice, st_));
+    launch(kFamOther, [&] { launch_filters(J_ * K_, st_, ddict_.as<double>(), mh_, mw_, dst, dtw_.as<C>()); });
+    CK(cudaStreamSynchronize(st_));  // dstage_ is reused
+  }
+
+  // ------------------------------------------------------------ API
+  void set_signals(const double* x) override {
+    const size_t nD = (size_t)N_ * J_ * D;
+    // host side parallel over images: validate, normalise (pipeline.cpp:78-121),
+    // round to the storage precision into pinned staging, per-image (and
+    // per-channel) norms of the stored values (what the oracle sees)
+    int bad = 0;
+#pragma omp parallel for reduction(| : bad)
+    for (long i = 0; i < (long)nD; ++i) bad |= !std::isfinite(x[i]);
+    if (bad) throw NumErr("signal contains a non-finite value");
+    if (!xstage_ || xstage_bytes_ < sizeof(R) * nD) {
+      if (xstage_) cudaFreeHost(xstage_);
+      CK(cudaMallocHost(&xstage_, sizeof(R) * nD));
+      xstage_bytes_ = sizeof(R) * nD;
+    }
+    R* xr = static_cast<R*>(xstage_);
+    xs_host_.resize(nD);
+    const size_t JD = (size_t)J_ * D;
+#pragma omp parallel for schedule(static)
+    for (int n = 0; n < N_; ++n) {
+      double* xn = xs_host_.data() + (size_t)n * JD;
+      normalize_image(cfg_.normalize, H, W, x + (size_t)n * JD, xn, J_);
+      double s = 0.0;
+      for (int j = 0; j < J_; ++j) {
+        double sj = 0.0;
+        for (size_t i = (size_t)j * D; i < (size_t)(j + 1) * D; ++i) {
+          const R v = R(xn[i]);
+          xr[(size_t)n * JD + i] = v;
+          xn[i] = double(v);
+          sj += xn[i] * xn[i];
+        }
+        xnorm2c_[(size_t)n * J_ + j] = sj;
+        s += sj;
+      }
+      xnorm2_[n] = s;
+    }
+    CK(cudaMemcpyAsync(x_.p, xr, sizeof(R) * nD, cudaMemcpyHostToDevice, st_));
+    for (int j = 0; j < J_; ++j)  // x_hat channel-major: J x N x NB
+      r2c(x_.as<R>() + (size_t)j * D, false, JD, xhat_.as<C>() + (size_t)j * N_ * NB, NB, N_);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_signals(double* x) override { std::copy(xs_host_.begin(), xs_host_.end(), x); }
+
+  void set_dictionary(const double* d) override {
+    const size_t cnt = (size_t)K_ * J_ * M_;
+    require_finite(d, cnt, "dictionary");
+    dict_.assign(d, d + cnt);
+    dict_zero_ = std::all_of(dict_.begin(), dict_.end(), [](double v) { return v == 0.0; });
+    upload_dict_spectra(dict_.data(), dhat_.as<C>());
+    if (J_ == 1) {
+      launch(kFamOther, [&] {
+        sigma_kernel<R><<<(NB + 255) / 256, 256, 0, st_>>>(dhat_.as<C>(), sigma_.as<R>(), K_, NB, cfg_.rho);
+      });
+    } else {  // per-bin block factorisation, once per dictionary (tcsc.cpp:31-55)
+      launch(kFamOther, [&] {
+        tc_factor<R><<<(NB + 127) / 128, 128, 0, st_>>>(dhat_.as<C>(), ginv_.as<C>(), K_, J_, NB, cfg_.rho);
+      });
+    }
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_dictionary(double* d) override { std::copy(dict_.begin(), dict_.end(), d); }
+
+  // init_variables (pipeline.cpp:123-156)
+  void init_variables() override {
+    const int JM = J_ * M_;  // filter k spans its J channel slices (k-major)
+    std::vector<double> d((size_t)K_ * JM);
+    std::mt19937_64 rng(cfg_.seed);
+    auto uniform = [&rng]() { return static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5; };
+    for (int k = 0; k < K_; ++k) {
+      double sq = 0.0;
+      for (int i = 0; i < JM; ++i) {
+        const double v = uniform();
+        d[(size_t)k * JM + i] = v;
+        sq += v * v;
+      }
+      double nrm = std::sqrt(sq);
+      if (nrm == 0.0) {
+        d[(size_t)k * JM] = 1.0;
+        nrm = 1.0;
+      }
+      for (int i = 0; i < JM; ++i) d[(size_t)k * JM + i] /= nrm;
+    }
+    set_dictionary(d.data());
+    CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
+    CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
+    CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
+    CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    u_zero_.assign(N_, 1);
+    mu_.assign(K_, 1.0);
+    zhat_valid_ = false;
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // sum v[0..n) over ranks (host values; no-op on one rank)
+  void reduce_host(double* v, int n) {
+    if (!multi()) return;
+    CK(cudaMemcpyAsync(hred_.p, v, sizeof(double) * n, cudaMemcpyHostToDevice, st_));
+    red_->allreduce(hred_.as<double>(), n, st_);
+    CK(cudaMemcpyAsync(v, hred_.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // Internal u layout: the single-CTA family stores each plane's pixel pairs
+  // column-major ((c/2)*H + r), the cluster family row-major; i is a
+  // reference-layout index (plane-major, row-major pixels).
+  static size_t u_index(size_t i) {
+    if constexpr (CLU) {
+      return i;
+    } else {
+      const size_t p = i / D, q = i % D;
+      const size_t r = q / W, c = q % W;
+      return p * D + ((c >> 1) * H + r) * 2 + (c & 1);
+    }
+  }
+
+  void check_range(int n0, int n1) const {
+    if (n0 < 0 || n1 > N_ || n0 >= n1) throw DimErr("image range out of bounds");
+  }
+
+  void set_coding_state(int n0, int n1, const double* theta, const double* z) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    if (!theta && !z) {  // the reference's empty state (coding.cpp:175-179): device-side reset
+      std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
+      CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * cnt, st_));
+      CK(cudaMemsetAsync(lam_.as<R>() + (size_t)n0 * J_ * D, 0, sizeof(R) * (size_t)(n1 - n0) * J_ * D, st_));
+      return;
+    }
+    std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
+    std::vector<R> u(cnt);
+    const double inv_rho = 1.0 / cfg_.rho;
+    for (size_t i = 0; i < cnt; ++i) u[u_index(i)] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
+    CK(cudaMemcpyAsync(u_.as<R>() + (size_t)n0 * K_ * D, u.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_coding_state(int n0, int n1, double* theta, double* z, double* lambda) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> u(cnt);
+    CK(cudaMemcpyAsync(u.data(), u_.as<R>() + (size_t)n0 * K_ * D, sizeof(R) * cnt, cudaMemcpyDeviceToHost, st_));
+    std::vector<R> l((size_t)(n1 - n0) * J_ * D);
+    CK(cudaMemcpyAsync(l.data(), lam_.as<R>() + (size_t)n0 * J_ * D, sizeof(R) * l.size(), cudaMemcpyDeviceToHost,
+                       st_));
+    CK(cudaStreamSynchronize(st_));
+    const R beta = R(cfg_.beta), rho = R(cfg_.rho);
+    for (size_t i = 0; i < cnt; ++i) {
+      const R uv = u[u_index(i)];
+      const R th = std::min(std::max(uv, -beta), beta);
+      if (theta) theta[i] = th;
+      if (z) z[i] = rho * (th - uv);
+    }
+    if (lambda)
+      for (size_t i = 0; i < l.size(); ++i) lambda[i] = l[i];
+  }
+
+  // solve_coding for images [n0, n1) (coding.cpp:166-329, 333-356)
+  void coding(int n0, int n1, dcsc_coding_stats* stats) override {
+    check_range(n0, n1);
+    const int cnt = n1 - n0;
+    std::vector<dcsc_coding_stats> out(cnt);
+    if (dict_zero_) {
+      // degenerate dictionary: z = theta = 0, lambda = -x (coding.cpp:181-191)
+      std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
+      CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * (size_t)cnt * K_ * D, st_));
+      const size_t JD = (size_t)J_ * D;
+      const size_t tot = (size_t)cnt * JD;
+      launch(kFamOther, [&] {
+        neg_copy<R><<<(unsigned)((tot + 255) / 256), 256, 0, st_>>>(x_.as<R>() + (size_t)n0 * JD,
+                                                                   lam_.as<R>() + (size_t)n0 * JD, tot);
+      });
+      CK(cudaStreamSynchronize(st_));
+      for (int i = 0; i < cnt; ++i) {
+        double ls = 0.0, lx = 0.0;
+        for (size_t j = 0; j < JD; ++j) {
+          const double lv = -xs_host_[(size_t)(n0 + i) * JD + j];
+          ls += lv * lv;
+          lx += lv * xs_host_[(size_t)(n0 + i) * JD + j];
+        }
+        out[i] = dcsc_coding_stats{};
+        out[i].converged = 1;
+        out[i].degenerate_dictionary = 1;
+        out[i].dual_objective = -0.5 * ls - lx;
+      }
+      if (stats) std::copy(out.begin(), out.end(), stats);
+      return;
+    }
+    int* conv_h = static_cast<int*>(pin_);
+    CK(cudaMemsetAsync(conv_.as<int>() + n0, 0, sizeof(int) * cnt, st_));
+    CK(cudaMemsetAsync(img_.as<ImageAdmm>() + n0, 0, sizeof(ImageAdmm) * cnt, st_));
+    const dim3 lgrid((NB + 255) / 256, cnt);
+    // initial lambda_hat from the warm state (the first assemble_w, coding.cpp:216-229);
+    // a zero state has w_hat = 0, so the FFT pass is skipped and part is zeroed
+    const bool all_zero = std::all_of(u_zero_.begin() + n0, u_zero_.begin() + n1, [](char v) { return v != 0; });
+    // multi-channel: lambda_hat from the per-bin J x J solves (tcsc.cpp:68-88)
+    auto tc_lam = [&](int kw, bool skip_conv) {
+      launch(kFamLambda, [&] {
+        const dim3 grid((NB + 127) / 128, cnt);
+        const C* wp = what_.as<C>() + (size_t)n0 * K_ * NB;
+        const C* xp = xhat_.as<C>() + (size_t)n0 * NB;
+        C* lp = lamhat_.as<C>() + (size_t)n0 * J_ * NB;
+        const int* cv = skip_conv ? conv_.as<int>() + n0 : nullptr;
+        const R ir = R(1.0 / cfg_.rho);
+        if (J_ == 3)
+          tc_lambda<R, 3><<<grid, 128, 0, st_>>>(wp, dhat_.as<C>(), ginv_.as<C>(), xp, (size_t)N_ * NB, lp, cv, K_,
+                                                 kw, J_, NB, ir);
+        else
+          tc_lambda<R><<<grid, 128, 0, st_>>>(wp, dhat_.as<C>(), ginv_.as<C>(), xp, (size_t)N_ * NB, lp, cv, K_, kw,
+                                              J_, NB, ir);
+      });
+    };
+    if (J_ > 1) {
+      if (!all_zero) coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);  // w_hat of the warm state
+      tc_lam(all_zero ? 0 : K_, false);
+    } else if (all_zero) {
+      CK(cudaMemsetAsync(part_.as<C>() + (size_t)n0 * G_ * NB, 0, sizeof(C) * (size_t)cnt * G_ * NB, st_));
+    } else {
+      coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);  // lambda_hat from the fused epilogue
+    }
+    std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
+    auto lam_update = [&](int iter, int last, int prologue) {
+      launch(kFamLambda, [&] {
+        lambda_update<R><<<lgrid, 256, 0, st_>>>(part_.as<C>() + (size_t)n0 * G_ * NB,
+                                                 sums_.as<double>() + (size_t)n0 * G_ * kSums,
+                                                 xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(),
+                                                 lamhat_.as<C>() + (size_t)n0 * NB, conv_.as<int>() + n0,
+                                                 img_.as<ImageAdmm>() + n0, G_, NB, R(cfg_.rho), iter, last,
+                                                 prologue);
+      });
+    };
+    if (all_zero && J_ == 1) lam_update(0, 0, 1);
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    int pending = -1;  // iteration whose conv flags are in flight
+    for (int it = 1; it <= cfg_.max_admm; ++it) {
+      coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
+      if (J_ > 1 && it < cfg_.max_admm) tc_lam(K_, true);
+      if (pending >= 0) {
+        // one-iteration look-ahead: iteration `it` is queued before we wait on it-1
+        CK(cudaEventSynchronize(ev[pending & 1]));
+        bool all = true;
+        for (int i = 0; i < cnt; ++i) all = all && conv_h[(pending & 1) * 65536 + i];
+        if (all) break;
+      }
+      if (cnt <= 65536) {
+        CK(cudaMemcpyAsync(conv_h + (it & 1) * 65536, conv_.as<int>() + n0, sizeof(int) * cnt,
+                           cudaMemcpyDeviceToHost, st_));
+        CK(cudaEventRecord(ev[it & 1], st_));
+        pending = it;
+      }
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    // exit: lambda = iDFT(lambda_hat), rescale, dual objective (coding.cpp:287-309)
+    c2r<R>(lamhat_.as<C>() + (size_t)n0 * J_ * NB, NB, lam_.as<R>() + (size_t)n0 * J_ * D, D, cnt * J_);
+    launch(kFamOther, [&] {
+      admm_exit<R><<<cnt, 256, 0, st_>>>(lam_.as<R>() + (size_t)n0 * J_ * D, x_.as<R>() + (size_t)n0 * J_ * D,
+                                         img_.as<ImageAdmm>() + n0, J_ * D, cfg_.beta, dual_.as<double>() + n0,
+                                         infeas_.as<double>() + n0, resc_.as<int>() + n0);
+    });
+    std::vector<ImageAdmm> im(cnt);
+    std::vector<double> du(cnt), inf(cnt);
+    std::vector<int> rs(cnt);
+    CK(cudaMemcpyAsync(im.data(), img_.as<ImageAdmm>() + n0, sizeof(ImageAdmm) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(du.data(), dual_.as<double>() + n0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(inf.data(), infeas_.as<double>() + n0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(rs.data(), resc_.as<int>() + n0, sizeof(int) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (int i = 0; i < cnt; ++i) {
+      dcsc_coding_stats& s = out[i];
+      s.admm_iters = im[i].iters;
+      s.converged = im[i].converged;
+      s.degenerate_dictionary = 0;
+      s.dual_rescaled = rs[i];
+      s.primal_residual = im[i].primal;
+      s.theta_change = im[i].thc;
+      s.z_change = im[i].zc;
+      s.dual_objective = du[i];
+      s.dual_infeasibility = inf[i];
+    }
+    if (stats) std::copy(out.begin(), out.end(), stats);
+  }
+
+  void set_maps(int n0, int n1, const double* z) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> v(cnt);
+    for (size_t i = 0; i < cnt; ++i) v[i] = R(z[i]);
+    CK(cudaMemcpyAsync(maps_.as<R>() + (size_t)n0 * K_ * D, v.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    zhat_valid_ = false;
+  }
+
+  void get_maps(int n0, int n1, double* z) override {
+    check_range(n0, n1);
+    const size_t cnt = (size_t)(n1 - n0) * K_ * D;
+    std::vector<R> v(cnt);
+    CK(cudaMemcpyAsync(v.data(), maps_.as<R>() + (size_t)n0 * K_ * D, sizeof(R) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    for (size_t i = 0; i < cnt; ++i) z[i] = v[i];
+  }
+
+  void set_learning_state(const double* gamma, const double* mu) override {
+    if (gamma) {  // J x N x D (LearningDualState::gamma[j], learning.hpp:15-23)
+      DevMem tmp;
+      tmp.alloc(sizeof(double) * (size_t)J_ * N_ * D);
+      CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
+      r2c(tmp.p, true, D, gam_.as<C>(), NB, J_ * N_);
+      CK(cudaStreamSynchronize(st_));
+    } else {
+      CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+    }
+    if (mu) mu_.assign(mu, mu + K_);
+    else mu_.assign(K_, 1.0);
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void get_learning_state(double* gamma, double* mu) override {
+    if (gamma) {
+      DevMem tmp;
+      tmp.alloc(sizeof(double) * (size_t)J_ * N_ * D);
+      c2r<double>(gam_.as<C>(), NB, tmp.as<double>(), D, J_ * N_);
+      CK(cudaMemcpyAsync(gamma, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+    if (mu) std::copy(mu_.begin(), mu_.end(), mu);
+  }
+
+  // z_hat of the accepted maps and the dead-filter flags (learning.cpp:41-64)
+  void build_zhat() {
+    if (zhat_valid_) return;
+    if (!zhat_.p) {
+      zhat_.alloc(sizeof(C) * (size_t)N_ * K_ * NB);
+      device_bytes += zhat_.bytes;
+    }
+    CK(cudaMemsetAsync(live_.p, 0, sizeof(int) * K_, st_));
+    r2c(maps_.p, false, D, zhat_.as<C>(), NB, N_ * K_, live_.as<int>(), K_);
+    live_h_.assign(K_, 0);
+    CK(cudaMemcpyAsync(live_h_.data(), live_.p, sizeof(int) * K_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    if (multi()) {  // a filter is dead only if its maps vanish on every rank
+      std::vector<double> lv(K_);
+      for (int k = 0; k < K_; ++k) lv[k] = live_h_[k];
+      reduce_host(lv.data(), K_);
+      for (int k = 0; k < K_; ++k) live_h_[k] = lv[k] > 0.0 ? 1 : 0;
+      CK(cudaMemcpyAsync(live_.p, live_h_.data(), sizeof(int) * K_, cudaMemcpyHostToDevice, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+    zhat_valid_ = true;
+  }
+
+  // c_k = sum_n conj(z_hat_nk) v_n (split over image chunks, fixed-order reduce)
+  void correlate_hat(const C* v, const int* done) {
+    constexpr int KC = 8;
+    const dim3 g1((NB + TBV - 1) / TBV, (K_ + KC - 1) / KC, csplit_);
+    launch(kFamContract, [&] {
+      contract_c<R, KC><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), v, cpart_.as<double2>(), live_.as<int>(), N_, K_, NB,
+                                             done);
+    });
+    const size_t knb = (size_t)K_ * NB;
+    const unsigned rb = (unsigned)((knb + 255) / 256);
+    if (!multi()) {
+      launch(kFamContract, [&] {
+        contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(), nullptr, csplit_, knb, done);
+      });
+    } else {  // FP64 partials summed over ranks, then rounded once
+      launch(kFamContract, [&] {
+        contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), nullptr, cglob_.as<double2>(), csplit_, knb,
+                                                  done);
+      });
+      red_->allreduce(reinterpret_cast<double*>(cglob_.p), 2 * knb, st_);
+      launch(kFamContract, [&] { to_cx<R><<<rb, 256, 0, st_>>>(cglob_.as<double2>(), cvec_.as<C>(), knb, done); });
+    }
+  }
+
+  // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
+  // fuse_alpha (single rank, inside the CG loop): contract_out's last block
+  // also runs the alpha step (no separate cg_scalar launch)
+  void apply_hat(const C* v, C* out, const int* done = nullptr, bool fuse_alpha = false) {
+    correlate_hat(v, done);
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(), dmu_.as<double>(), mh_, mw_, 0,
+                  dtw_.as<C>(), done);
+    });
+    // fused: fewer image rows per launch (each block loops over images) so the
+    // last-block alpha step sums few partials and the arrival counter sees
+    // few atomics
+    const dim3 g3(tiles_, fuse_alpha ? std::min(N_, std::max(1, fused_rows_ / tiles_)) : N_);
+    launch(kFamContract, [&] {
+      contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(), live_.as<int>(),
+                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0, done,
+                                                 fuse_alpha ? cg_.as<CgState>() : nullptr, cgcnt_.as<unsigned>(),
+                                                 1.0 / D);
+    });
+  }
+
+  void upload_mu() {
+    std::vector<double> wk(K_);
+    for (int k = 0; k < K_; ++k) wk[k] = 0.5 / mu_[k];
+    CK(cudaMemcpyAsync(dmu_.p, mu_.data(), sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(dwk_.p, wk.data(), sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
+  }
+
+  CgState read_cg() {
+    CgState* h = reinterpret_cast<CgState*>(static_cast<char*>(pin_) + 600000);
+    CK(cudaMemcpyAsync(h, cg_.p, sizeof(CgState), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    return *h;
+  }
+
+  // One CG scalar step; across ranks the block partials are first summed
+  // locally, all-reduced, then applied (identical state on every rank).
+  void cg_step(const double* partial, int count, double invD, int step) {
+    if (!multi()) {
+      launch(kFamOther, [&] { cg_scalar<<<1, 1024, 0, st_>>>(partial, count, invD, cg_.as<CgState>(), step, nullptr); });
+      return;
+    }
+    launch(kFamOther, [&] { sum_partials<<<1, 1024, 0, st_>>>(partial, count, hred_.as<double>()); });
+    red_->allreduce(hred_.as<double>(), 1, st_);
+    launch(kFamOther, [&] {
+      cg_scalar<<<1, 1024, 0, st_>>>(partial, count, invD, cg_.as<CgState>(), step, hred_.as<double>());
+    });
+  }
+
+  // gamma_solve (learning.cpp:136-185), warm-started, on half spectra. The
+  // iteration loop terminates on the device (CgState::done); the host issues
+  // iterations in chunks and reads the state once per chunk.
+  void gamma_solve(double bnorm, int& iters, bool& converged) {
+    iters = 0;
+    converged = false;
+    const size_t total = (size_t)N_ * NB;
+    const unsigned vb = (unsigned)((total + TBV - 1) / TBV);
+    if (bnorm == 0.0) {
+      CK(cudaMemsetAsync(gam_ch_, 0, sizeof(C) * total, st_));
+      converged = true;
+      return;
+    }
+    CgState init{};
+    init.bnorm = bnorm;
+    init.tol = cfg_.cg_tol;
+    init.max_iters = cfg_.cg_max;
+    CK(cudaMemcpyAsync(cg_.p, &init, sizeof(CgState), cudaMemcpyHostToDevice, st_));
+    apply_hat(gam_ch_, ap_.as<C>());
+    launch(kFamOther, [&] {
+      cg_init<R, TBV><<<vb, TBV, 0, st_>>>(xh_ch_, ap_.as<C>(), r_.as<C>(), p_.as<C>(),
+                                            partial_.as<double>(), total, NB, Wh);
+    });
+    const double invD = 1.0 / D;
+    cg_step(partial_.as<double>(), (int)vb, invD, 0);
+    const int* done = &cg_.as<CgState>()->done;
+    CgState s = read_cg();
+    int issued = 0, chunk = 2;
+    while (!s.done && issued < cfg_.cg_max) {
+      const int n = std::min(chunk, cfg_.cg_max - issued);
+      const bool fuse = !multi() && !no_cg_fuse_;  // single rank: scalar steps in the producers' last blocks
+      for (int c = 0; c < n; ++c) {
+        apply_hat(p_.as<C>(), ap_.as<C>(), done, fuse);
+        if (!fuse) cg_step(partial_.as<double>(), N_ * tiles_, invD, 1);
+        launch(kFamOther, [&] {
+          cg_update<R, TBV><<<fuse ? std::min<unsigned>(vb, (unsigned)fused_rows_) : vb, TBV, 0, st_>>>(
+                                                  gam_ch_, r_.as<C>(), p_.as<C>(), ap_.as<C>(),
+                                                  cg_.as<CgState>(), partial_.as<double>(), total, NB, Wh,
+                                                  fuse ? cgcnt_.as<unsigned>() + 1 : nullptr, invD);
+        });
+        if (!fuse) cg_step(partial_.as<double>(), (int)vb, invD, 2);
+        launch(kFamOther, [&] {
+          cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(r_.as<C>(), p_.as<C>(), cg_.as<CgState>(), total);
+        });
+      }
+      issued += n;
+      chunk = std::min(chunk * 2, 8);
+      s = read_cg();
+    }
+    iters = s.iters;
+    converged = s.converged != 0;
+  }
+
+  // d_recover (learning.cpp:187-216): d_k = -0.5/max(mu_k,1e-300) crop(iDFT(sum_n conj(z_nk) gamma_n))
+  void d_recover(std::vector<double>& d) {
+    correlate_hat(gam_ch_, nullptr);
+    // d_recover does not skip dead filters; their correlation is exactly zero anyway
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
+                  dtw_.as<C>(), nullptr);
+    });
+    d.resize((size_t)K_ * M_);
+    CK(cudaMemcpyAsync(d.data(), dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // solve_learning (learning.cpp:227-355) over all images; J > 1 runs the J
+  // per-channel gamma systems under one mu ascent with joint filter norms
+  // (solve_learning_tcsc, tcsc.cpp:263-270 -> learning.cpp:276-345)
+  void learning(double* d_out, dcsc_learning_stats* st) override {
+    dcsc_learning_stats ls{};
+    if ((int)mu_.size() != K_) mu_.assign(K_, 1.0);
+    build_zhat();
+    int n_live = 0;
+    for (int k = 0; k < K_; ++k) n_live += live_h_[k] ? 1 : 0;
+    ls.n_dead = K_ - n_live;
+    const size_t JM = (size_t)J_ * M_;
+    if (n_live == 0) {  // every map zero: zero dictionary, gamma = 0 (learning.cpp:258-270)
+      ls.degenerate = 1;
+      CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
+      CK(cudaStreamSynchronize(st_));
+      std::fill(d_out, d_out + (size_t)K_ * JM, 0.0);
+      if (st) *st = ls;
+      return;
+    }
+    std::vector<double> bnorm(J_, 0.0);
+    for (int n = 0; n < N_; ++n)
+      for (int j = 0; j < J_; ++j) bnorm[j] += xnorm2c_[(size_t)n * J_ + j];
+    reduce_host(bnorm.data(), J_);
+    for (double& b : bnorm) b = std::sqrt(b);
+    std::vector<std::vector<double>> parts(J_);
+    std::vector<double> norms(K_, 0.0);
+    bool clamped = false;
+    for (int iter = 1; iter <= cfg_.max_mu_iters; ++iter) {
+      clamped = false;
+      for (int k = 0; k < K_; ++k)
+        if (mu_[k] < cfg_.mu_floor) {
+          mu_[k] = cfg_.mu_floor;
+          clamped = true;
+        }
+      upload_mu();
+      long iter_cg = 0;
+      for (int j = 0; j < J_; ++j) {
+        select_channel(j);
+        int cg_iters = 0;
+        bool cg_conv = false;
+        gamma_solve(bnorm[j], cg_iters, cg_conv);
+        iter_cg += cg_iters;
+        if (!cg_conv) ls.cg_budget_hit = 1;
+      }
+      ls.cg_iters += iter_cg;
+      if (iter == 1) ls.cg_iters_first = iter_cg;
+      for (int j = 0; j < J_; ++j) {
+        select_channel(j);
+        d_recover(parts[j]);
+      }
+      select_channel(0);
+      for (int k = 0; k < K_; ++k) {
+        double sq = 0.0;
+        for (int j = 0; j < J_; ++j)
+          for (int i = 0; i < M_; ++i) sq += parts[j][(size_t)k * M_ + i] * parts[j][(size_t)k * M_ + i];
+        norms[k] = std::sqrt(sq);
+      }
+      ls.mu_iters = iter;
+      bool settled = true;
+      for (int k = 0; k < K_; ++k) {
+        const bool at_boundary = std::abs(norms[k] - 1.0) <= kFilterNormTol;
+        const bool inactive = mu_[k] <= cfg_.mu_floor * (1.0 + 1e-9) && norms[k] < 1.0;
+        if (!at_boundary && !inactive) {
+          settled = false;
+          break;
+        }
+      }
+      if (settled) {
+        ls.converged = 1;
+        break;
+      }
+      if (iter < cfg_.max_mu_iters)
+        for (int k = 0; k < K_; ++k) mu_[k] = std::max(mu_[k] * norms[k], cfg_.mu_floor);
+    }
+    ls.mu_clamped = clamped ? 1 : 0;
+    for (int k = 0; k < K_; ++k) {
+      double scale = 1.0;
+      if (norms[k] > 1.0) {
+        scale = 1.0 / norms[k];
+        ++ls.rescaled_filters;
+      }
+      for (int j = 0; j < J_; ++j)
+        for (int i = 0; i < M_; ++i) d_out[(size_t)k * JM + (size_t)j * M_ + i] = scale * parts[j][(size_t)k * M_ + i];
+    }
+    if (st) *st = ls;
+  }
+
+  // learning views of channel j: x_hat_j and gamma_j (both N x NB)
+  void select_channel(int j) {
+    xh_ch_ = xhat_.as<C>() + (size_t)j * N_ * NB;
+    gam_ch_ = gam_.as<C>() + (size_t)j * N_ * NB;
+  }
+
+  // LearningOperator::correlation (learning.cpp:124-134) for every filter:
+  // out[k] = crop(iDFT(sum_n conj(z_hat_nk) DFT(v_n))), K x M (channel-free)
+  void learning_correlation(const double* v, double* out) override {
+    build_zhat();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, v, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
+    correlate_hat(r_.as<C>(), nullptr);
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 2,
+                  dtw_.as<C>(), nullptr);
+    });
+    CK(cudaMemcpyAsync(out, dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // ---------------------------------------------------------- stateless ops
+  // (coding.hpp:45-66, learning.hpp:81-95), for replaying iterations; they
+  // leave the context's coding and learning state untouched.
+
+  // D^T lambda: apply_dictionary_adjoint (coding.cpp:126-135), J > 1
+  // block_dictionary_adjoint (tcsc.cpp:185-193). lam (n1-n0) x J x D -> out (n1-n0) x K x D.
+  void dictionary_adjoint(int n0, int n1, const double* lam, double* out) override {
+    check_range(n0, n1);
+    const size_t JD = (size_t)J_ * D, KD = (size_t)K_ * D;
+    DevMem lin, lh, th, tout;
+    lin.alloc(sizeof(double) * JD);
+    lh.alloc(sizeof(C) * (size_t)J_ * NB);
+    th.alloc(sizeof(C) * (size_t)K_ * NB);
+    tout.alloc(sizeof(double) * KD);
+    for (int i = 0; i < n1 - n0; ++i) {
+      CK(cudaMemcpyAsync(lin.p, lam + i * JD, sizeof(double) * JD, cudaMemcpyHostToDevice, st_));
+      r2c(lin.p, true, D, lh.as<C>(), NB, J_);
+      launch(kFamOther, [&] {
+        adjoint_spectra<R><<<dim3((NB + 255) / 256, K_), 256, 0, st_>>>(dhat_.as<C>(), lh.as<C>(), th.as<C>(), K_,
+                                                                       J_, NB);
+      });
+      c2r<double>(th.as<C>(), NB, tout.as<double>(), D, K_);
+      CK(cudaMemcpyAsync(out + i * KD, tout.p, sizeof(double) * KD, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+  }
+
+  // lambda_update (coding.cpp:103-124; J > 1 lambda_update_blocked,
+  // tcsc.cpp:162-183) from theta, z ((n1-n0) x K x D each) against the
+  // context's signals and dictionary: out (n1-n0) x J x D.
+  void lambda_update_op(int n0, int n1, const double* theta, const double* z, double* out) override {
+    check_range(n0, n1);
+    const size_t KD = (size_t)K_ * D, JD = (size_t)J_ * D;
+    std::vector<double> w(KD);
+    DevMem win, wh, lh, lout;
+    win.alloc(sizeof(double) * KD);
+    wh.alloc(sizeof(C) * (size_t)K_ * NB);
+    lh.alloc(sizeof(C) * (size_t)J_ * NB);
+    lout.alloc(sizeof(double) * JD);
+    const double inv_rho = 1.0 / cfg_.rho;
+    for (int i = 0; i < n1 - n0; ++i) {
+      for (size_t q = 0; q < KD; ++q) w[q] = theta[i * KD + q] + z[i * KD + q] * inv_rho;  // coding.cpp:224-227
+      CK(cudaMemcpyAsync(win.p, w.data(), sizeof(double) * KD, cudaMemcpyHostToDevice, st_));
+      r2c(win.p, true, D, wh.as<C>(), NB, K_);
+      const int n = n0 + i;
+      launch(kFamOther, [&] {
+        if (J_ == 1)
+          lambda_from_w<R><<<(NB + 255) / 256, 256, 0, st_>>>(wh.as<C>(), dhat_.as<C>(), xhat_.as<C>() + (size_t)n * NB,
+                                                               sigma_.as<R>(), lh.as<C>(), K_, NB, R(inv_rho));
+        else
+          tc_lambda<R><<<dim3((NB + 127) / 128, 1), 128, 0, st_>>>(wh.as<C>(), dhat_.as<C>(), ginv_.as<C>(),
+                                                                 xhat_.as<C>() + (size_t)n * NB, (size_t)N_ * NB,
+                                                                 lh.as<C>(), nullptr, K_, K_, J_, NB, R(inv_rho));
+      });
+      c2r<double>(lh.as<C>(), NB, lout.as<double>(), D, J_);
+      CK(cudaMemcpyAsync(out + i * JD, lout.p, sizeof(double) * JD, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+  }
+
+  // gamma_solve (learning.cpp:136-185) on channel `channel` with the given mu
+  // (clamped at the floor as LearningOperator::set_mu does); gamma (N x D) is
+  // the warm start on entry and the solution on exit.
+  void gamma_solve_op(int channel, const double* mu, double* gamma, int* iters, int* converged) override {
+    if (channel < 0 || channel >= J_) throw DimErr("channel out of range");
+    build_zhat();
+    const std::vector<double> keep_mu = mu_;
+    DevMem keep_g;
+    keep_g.alloc(sizeof(C) * (size_t)N_ * NB);
+    select_channel(channel);
+    CK(cudaMemcpyAsync(keep_g.p, gam_ch_, keep_g.bytes, cudaMemcpyDeviceToDevice, st_));
+    mu_.assign(mu, mu + K_);
+    for (double& m : mu_) m = std::max(m, cfg_.mu_floor);
+    upload_mu();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, gam_ch_, NB, N_);
+    double bn = 0.0;
+    for (int n = 0; n < N_; ++n) bn += xnorm2c_[(size_t)n * J_ + channel];
+    reduce_host(&bn, 1);
+    int it = 0;
+    bool conv = false;
+    gamma_solve(std::sqrt(bn), it, conv);
+    c2r<double>(gam_ch_, NB, tmp.as<double>(), D, N_);
+    CK(cudaMemcpyAsync(gamma, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(gam_ch_, keep_g.p, keep_g.bytes, cudaMemcpyDeviceToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+    mu_ = keep_mu;
+    select_channel(0);
+    if (iters) *iters = it;
+    if (converged) *converged = conv ? 1 : 0;
+  }
+
+  // d_recover (learning.cpp:187-216) for one channel's gamma (N x D): out K x M
+  void d_recover_op(int channel, const double* gamma, const double* mu, double* out) override {
+    if (channel < 0 || channel >= J_) throw DimErr("channel out of range");
+    build_zhat();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, gamma, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
+    correlate_hat(r_.as<C>(), nullptr);
+    CK(cudaMemcpyAsync(dmu_.p, mu, sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
+                  dtw_.as<C>(), nullptr);
+    });
+    CK(cudaMemcpyAsync(out, dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+    upload_mu();  // the context's own mu back on the device
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void learning_apply(const double* mu, const double* v, double* out) override {
+    build_zhat();
+    std::vector<double> keep = mu_;
+    mu_.assign(mu, mu + K_);
+    for (int k = 0; k < K_; ++k) mu_[k] = std::max(mu_[k], cfg_.mu_floor);  // set_mu clamps (learning.cpp:66-81)
+    upload_mu();
+    DevMem tmp;
+    tmp.alloc(sizeof(double) * (size_t)N_ * D);
+    CK(cudaMemcpyAsync(tmp.p, v, tmp.bytes, cudaMemcpyHostToDevice, st_));
+    r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
+    apply_hat(r_.as<C>(), ap_.as<C>());
+    c2r<double>(ap_.as<C>(), NB, tmp.as<double>(), D, N_);
+    CK(cudaMemcpyAsync(out, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    mu_ = keep;
+  }
+
+  // per-image data terms of `d` against the accepted maps (Parseval on z_hat),
+  // summed over channels
+  void data_terms(const double* d, std::vector<double>& data) {
+    build_zhat();
+    upload_dict_spectra(d, dcand_.as<C>());
+    const dim3 g3(tiles_, N_);
+    data.assign(N_, 0.0);
+    std::vector<double> part(N_);
+    for (int j = 0; j < J_; ++j) {
+      launch(kFamContract, [&] {
+        contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), dcand_.as<C>() + (size_t)j * K_ * NB,
+                                                   dwk_.as<double>(), live_.as<int>(),
+                                                   xhat_.as<C>() + (size_t)j * N_ * NB, nullptr,
+                                                   partial_.as<double>(), N_, K_, NB, Wh, 1, nullptr);
+      });
+      launch(kFamOther, [&] {
+        per_image_reduce<<<N_, 256, 0, st_>>>(partial_.as<double>(), tiles_, 0.5 / D, odata_.as<double>());
+      });
+      CK(cudaMemcpyAsync(part.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      for (int n = 0; n < N_; ++n) data[n] += part[n];
+    }
+  }
+
+  void learning_data_term(const double* d, double* out) override {
+    std::vector<double> data;
+    data_terms(d ? d : dict_.data(), data);
+    double s = 0.0;
+    for (double v : data) s += v;
+    reduce_host(&s, 1);
+    *out = s;
+  }
+
+  // per-image objective of a map source (coding candidates in u, or the accepted maps)
+  template <int MODE>
+  void objective_pass(const C* dhat, std::vector<double>& data, std::vector<double>& l1) {
+    coding_launch<MODE>(dhat, 0, N_);
+    if (J_ > 1) {
+      launch(kFamOther, [&] {
+        tc_objective<R><<<N_, 256, 0, st_>>>(what_.as<C>(), dhat, xhat_.as<C>(), (size_t)N_ * NB, sums_.as<double>(),
+                                             G_ * CLN, K_, J_, NB, Wh, 1.0 / D, cfg_.beta, odata_.as<double>(),
+                                             ol1_.as<double>());
+      });
+    } else {
+      launch(kFamOther, [&] {
+        objective_reduce<R><<<N_, 256, 0, st_>>>(part_.as<C>(), sums_.as<double>(), xhat_.as<C>(), G_, G_ * CLN,
+                                                 NB, Wh, 1.0 / D, cfg_.beta, odata_.as<double>(), ol1_.as<double>());
+      });
+    }
+    data.resize(N_);
+    l1.resize(N_);
+    CK(cudaMemcpyAsync(data.data(), odata_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(l1.data(), ol1_.p, sizeof(double) * N_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  void objective(const double* d, dcsc_objective* per_image) override {
+    const C* dh = dhat_.as<C>();
+    if (d) {
+      upload_dict_spectra(d, dcand_.as<C>());
+      dh = dcand_.as<C>();
+    }
+    std::vector<double> data, l1;
+    objective_pass<kPassMaps>(dh, data, l1);
+    for (int n = 0; n < N_; ++n) {
+      per_image[n].data_term = data[n];
+      per_image[n].l1_term = l1[n];
+      per_image[n].total = data[n] + l1[n];
+      per_image[n].residual_norm = std::sqrt(2.0 * data[n]);
+      if (!std::isfinite(per_image[n].total)) throw NumErr("objective is not finite");
+    }
+  }
+
+  // reconstruct (objective.cpp:39-57) of the accepted maps of images [n0, n1)
+  // with `d` (NULL = the context dictionary): out is (n1-n0) x J x D
+  void reconstruct(const double* d, int n0, int n1, double* out) override {
+    check_range(n0, n1);
+    const int cnt = n1 - n0;
+    const C* dh = dhat_.as<C>();
+    if (d) {
+      require_finite(d, (size_t)K_ * J_ * M_, "dictionary");
+      upload_dict_spectra(d, dcand_.as<C>());
+      dh = dcand_.as<C>();
+    }
+    coding_launch<kPassMaps>(dh, n0, cnt);
+    DevMem spec, sp;
+    spec.alloc(sizeof(C) * (size_t)cnt * J_ * NB);
+    sp.alloc(sizeof(double) * (size_t)cnt * J_ * D);
+    launch(kFamOther, [&] {
+      recon_spectrum<R><<<dim3((NB + 255) / 256, cnt), 256, 0, st_>>>(
+          part_.as<C>() + (size_t)n0 * G_ * NB, what_.as<C>() ? what_.as<C>() + (size_t)n0 * K_ * NB : nullptr, dh,
+          spec.as<C>(), J_, K_, G_, NB);
+    });
+    c2r<double>(spec.as<C>(), NB, sp.as<double>(), D, cnt * J_);
+    CK(cudaMemcpyAsync(out, sp.p, sp.bytes, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+
+  // run_csc (pipeline.cpp:158-301) from init_variables
+  void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) override {
+    *n_rows = 0;
+    *converged = 0;
+    init_variables();
+    if (max_outer == 0) return;
+    std::vector<dcsc_objective> img(N_);
+    double prev_total = 0.0;
+    {
+      double dsum = 0.0;
+      for (int n = 0; n < N_; ++n) {
+        img[n].data_term = 0.5 * xnorm2_[n];  // maps are zero: reconstruct = 0
+        img[n].l1_term = 0.0;
+        img[n].total = img[n].data_term;
+        img[n].residual_norm = std::sqrt(xnorm2_[n]);
+        dsum += img[n].data_term;
+      }
+      reduce_host(&dsum, 1);
+      prev_total = dsum;
+    }
+    std::vector<dcsc_coding_stats> cs(N_);
+    std::vector<int> acc(N_);
+    int row = 0;
+    for (int outer = 1; outer <= max_outer; ++outer) {
+      const double w0 = now_ms();
+      coding(0, N_, cs.data());
+      const double coding_ms = now_ms() - w0;
+      std::vector<double> cdata, cl1;
+      objective_pass<kPassObjective>(dhat_.as<C>(), cdata, cl1);
+      long admm_total = 0;
+      for (int n = 0; n < N_; ++n) {
+        admm_total += cs[n].admm_iters;
+        const double tot = cdata[n] + cl1[n];
+        if (!std::isfinite(tot))
+          throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", coding phase");
+        acc[n] = tot <= img[n].total ? 1 : 0;
+        if (acc[n]) img[n] = {cdata[n], cl1[n], tot, std::sqrt(2.0 * cdata[n])};
+      }
+      double zc2 = 0.0, zn2 = 0.0;
+      long l0 = 0;
+      accept(acc, zc2, zn2, l0);
+      zhat_valid_ = false;
+      dcsc_objective after{};
+      for (int n = 0; n < N_; ++n) {
+        after.data_term += img[n].data_term;
+        after.l1_term += img[n].l1_term;
+        after.residual_norm += img[n].residual_norm * img[n].residual_norm;
+      }
+      {
+        double s[6] = {after.data_term, after.l1_term, after.residual_norm, (double)admm_total, zc2, zn2};
+        double l0d = (double)l0;
+        reduce_host(s, 6);
+        reduce_host(&l0d, 1);
+        after.data_term = s[0];
+        after.l1_term = s[1];
+        after.residual_norm = s[2];
+        admm_total = (long)s[3];
+        zc2 = s[4];
+        zn2 = s[5];
+        l0 = (long)l0d;
+      }
+      after.total = after.data_term + after.l1_term;
+      after.residual_norm = std::sqrt(after.residual_norm);
+      const double w1 = now_ms();
+      rows[row++] = {outer, 0, after.total, after.data_term, after.l1_term, after.residual_norm,
+                     admm_total, 0, 0, coding_ms, w1 - w0, l0};
+
+      dcsc_learning_stats ls{};
+      std::vector<double> dc((size_t)K_ * J_ * M_);
+      learning(dc.data(), &ls);
+      const double learning_ms = now_ms() - w1;
+      std::vector<double> data;
+      data_terms(dc.data(), data);
+      double cand = 0.0;
+      for (double v : data) cand += v;
+      reduce_host(&cand, 1);
+      if (!std::isfinite(cand + after.l1_term))
+        throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", learning phase");
+      dcsc_objective afterl = after;
+      double dc2 = 0.0, dn2 = 0.0;
+      if (cand <= after.data_term) {
+        for (size_t i = 0; i < dc.size(); ++i) {
+          const double dl = dc[i] - dict_[i];
+          dc2 += dl * dl;
+        }
+        set_dictionary(dc.data());
+        afterl.data_term = cand;
+        afterl.total = cand + after.l1_term;
+        afterl.residual_norm = std::sqrt(2.0 * cand);
+        for (int n = 0; n < N_; ++n)
+          img[n] = {data[n], img[n].l1_term, data[n] + img[n].l1_term, std::sqrt(2.0 * data[n])};
+      }
+      for (double v : dict_) dn2 += v * v;
+      const double w2 = now_ms();
+      rows[row++] = {outer, 1, afterl.total, afterl.data_term, afterl.l1_term, afterl.residual_norm,
+                     0, ls.cg_iters, ls.mu_iters, learning_ms, w2 - w1, l0};
+      *n_rows = row;
+      const double obj_change = std::abs(prev_total - afterl.total) / std::max(std::abs(prev_total), 1e-30);
+      const double z_change = std::sqrt(zc2) / std::max(std::sqrt(zn2), 1.0);
+      const double d_change = std::sqrt(dc2) / std::max(std::sqrt(dn2), 1.0);
+      prev_total = afterl.total;
+      if (obj_change <= cfg_.tol && z_change <= cfg_.tol && d_change <= cfg_.tol) {
+        *converged = 1;
+        break;
+      }
+    }
+  }
+
+  // accept-only-descent for the coding half-step (pipeline.cpp:231-247)
+  void accept(const std::vector<int>& acc, double& zc2, double& zn2, long& l0) {
+    CK(cudaMemcpyAsync(accept_.p, acc.data(), sizeof(int) * N_, cudaMemcpyHostToDevice, st_));
+    const dim3 g(accept_chunks_, N_);
+    launch(kFamOther, [&] {
+      accept_maps<R, TBV, !CLU><<<g, TBV, 0, st_>>>(u_.as<R>(), maps_.as<R>(), accept_.as<int>(), (size_t)K_ * D,
+                                                     cfg_.rho, cfg_.beta, partial_.as<double>(),
+                                                     partial2_.as<double>(), l0_.as<unsigned long long>(), P::H, P::W);
+    });
+    const size_t cnt = (size_t)N_ * accept_chunks_;
+    std::vector<double> a(cnt), b(cnt);
+    std::vector<unsigned long long> c(cnt);
+    CK(cudaMemcpyAsync(a.data(), partial_.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(b.data(), partial2_.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(c.data(), l0_.p, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    zc2 = zn2 = 0.0;
+    l0 = 0;
+    for (size_t i = 0; i < cnt; ++i) {
+      zc2 += a[i];
+      zn2 += b[i];
+      l0 += (long)c[i];
+    }
+  }
+
+  void synchronize() override { CK(cudaStreamSynchronize(st_)); }
+
+  void set_profiling(int on) override {
+    CK(cudaStreamSynchronize(st_));
+    prof_.clear();
+    evused_ = 0;
+    profiling_ = on;  // 1: every launch, 2: coding-pass launches only
+  }
+
+  void kernel_time(int fam, double* ms, long long* n) override {
+    CK(cudaStreamSynchronize(st_));
+    double t = 0.0;
+    long long c = 0;
+    for (auto& e : prof_)
+      if (e.fam == fam) {
+        float x = 0.f;
+        CK(cudaEventElapsedTime(&x, e.a, e.b));
+        t += x;
+        ++c;
+      }
+    *ms = t;
+    *n = c;
+  }
+
+  void event_mark(int slot) override {
+    if (slot < 0 || slot >= 64) throw InvErr("event slot out of range");
+    if ((int)marks_.size() < 64) marks_.resize(64, nullptr);
+    if (!marks_[slot]) CK(cudaEventCreate(&marks_[slot]));
+    CK(cudaEventRecord(marks_[slot], st_));
+  }
+
+  double event_elapsed(int a, int b) override {
+    if (a < 0 || b < 0 || a >= (int)marks_.size() || b >= (int)marks_.size() || !marks_[a] || !marks_[b])
+      throw InvErr("event slot not marked");
+    CK(cudaEventSynchronize(marks_[b]));
+    float x = 0.f;
+    CK(cudaEventElapsedTime(&x, marks_[a], marks_[b]));
+    return x;
+  }
+
+ private:
+  struct Prof {
+    int fam;
+    cudaEvent_t a, b;
+  };
+  dcsc_cuda_opts o_;
+  dcsc_solver_config cfg_;
+  int N_, K_, J_ = 1, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1, fused_rows_ = 1184;
+  bool no_cg_fuse_ = false;
+  cudaStream_t st_ = nullptr;
+  void* pin_ = nullptr;
+  DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
+      infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_, ginv_, what_, cgcnt_;
+  std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
+  C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
+  C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel
+  std::vector<int> live_h_;
+  std::vector<char> u_zero_;  // per image: ADMM state known to be exactly zero
+  void* xstage_ = nullptr;    // pinned staging of the signals (host -> device)
+  size_t xstage_bytes_ = 0;
+  bool dict_zero_ = false, zhat_valid_ = false;
+  int profiling_ = 0;
+  std::vector<Prof> prof_;
+  std::vector<cudaEvent_t> evpool_;
+  size_t evused_ = 0;
+  std::vector<cudaEvent_t> marks_;
+};
+
+// Standalone half-spectrum DFTs
+template <class R, int H, int W>
+void dft_batch(bool inverse, int batch, const double* in, double* out) {
+  using E = Engine<R, H, W>;
+  using P = typename E::P;
+  using C = cx<R>;
+  constexpr int NB = P::NB, D = P::D;
+  static bool attr = false;
+  if (!attr) {
+    E::set_attributes();
+    attr = true;
+  }
+  std::vector<C> tw(P::TW_LEN);
+  fill_twiddles<P>(tw.data());
+  DevMem dtw, din, dout, spec;
+  dtw.alloc(sizeof(C) * P::TW_LEN);
+  CK(cudaMemcpy(dtw.p, tw.data(), dtw.bytes, cudaMemcpyHostToDevice));
+  spec.alloc(sizeof(C) * (size_t)batch * NB);
+  if (!inverse) {
+    din.alloc(sizeof(double) * (size_t)batch * D);
+    CK(cudaMemcpy(din.p, in, din.bytes, cudaMemcpyHostToDevice));
+    E::template launch_r2c<double>(batch, 0, din.as<double>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+    CK(cudaGetLastError());
+    std::vector<C> h((size_t)batch * NB);
+    CK(cudaMemcpy(h.data(), spec.p, spec.bytes, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h.size(); ++i) {
+      out[2 * i] = h[i].x;
+      out[2 * i + 1] = h[i].y;
+    }
+  } else {
+    std::vector<C> h((size_t)batch * NB);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = mk<C>(R(in[2 * i]), R(in[2 * i + 1]));
+    CK(cudaMemcpy(spec.p, h.data(), spec.bytes, cudaMemcpyHostToDevice));
+    dout.alloc(sizeof(double) * (size_t)batch * D);
+    E::template launch_c2r<double>(batch, 0, spec.as<C>(), NB, dout.as<double>(), D, dtw.as<C>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout.p, dout.bytes, cudaMemcpyDeviceToHost));
+  }
+  CK(cudaDeviceSynchronize());
+}
+
+// Device-timed batched r2c and c2r of `batch` planes (random data), for the
+// cuFFT comparator (scripts/fft_comparator.py). Returns the mean ms per call.
+template <class R, int H, int W>
+void fft_timing(int batch, int iters, double* ms_r2c, double* ms_c2r) {
+  using E = Engine<R, H, W>;
+  using P = typename E::P;
+  using C = cx<R>;
+  constexpr int NB = P::NB, D = P::D;
+  E::set_attributes();
+  std::vector<C> tw(P::TW_LEN);
+  fill_twiddles<P>(tw.data());
+  DevMem dtw, real, spec;
+  dtw.alloc(sizeof(C) * P::TW_LEN);
+  CK(cudaMemcpy(dtw.p, tw.data(), dtw.bytes, cudaMemcpyHostToDevice));
+  real.alloc(sizeof(R) * (size_t)batch * D);
+  spec.alloc(sizeof(C) * (size_t)batch * NB);
+  std::vector<R> h((size_t)batch * D);
+  std::mt19937_64 rng(1);
+  for (auto& v : h) v = R(static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5);
+  CK(cudaMemcpy(real.p, h.data(), real.bytes, cudaMemcpyHostToDevice));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  auto time_it = [&](auto&& f) {
+    for (int i = 0; i < 3; ++i) f();
+    CK(cudaEventRecord(a));
+    for (int i = 0; i < iters; ++i) f();
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return (double)ms / iters;
+  };
+  *ms_r2c = time_it([&] {
+    E::template launch_r2c<R>(batch, 0, real.as<R>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+  });
+  *ms_c2r = time_it([&] { E::template launch_c2r<R>(batch, 0, spec.as<C>(), NB, real.as<R>(), D, dtw.as<C>()); });
+  CK(cudaGetLastError());
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
+}  // namespace
+
+#define DCSC_ENGINE_INSTANTIATE(Rt, Hh, Ww)                                                    \
+  namespace dcsc_engine {                                                                      \
+  std::unique_ptr<EngineBase> make_engine_##Rt##_##Hh##_##Ww(const dcsc_cuda_opts& o) {         \
+    return std::make_unique<Engine<Rt, Hh, Ww>>(o);                                            \
+  }                                                                                            \
+  void dft_batch_##Rt##_##Hh##_##Ww(bool inverse, int batch, const double* in, double* out) {   \
+    dft_batch<Rt, Hh, Ww>(inverse, batch, in, out);                                            \
+  }                                                                                            \
+  void fft_timing_##Rt##_##Hh##_##Ww(int batch, int iters, double* ms_r2c, double* ms_c2r) {   \
+    fft_timing<Rt, Hh, Ww>(batch, iters, ms_r2c, ms_c2r);                                      \
+  }                                                                                            \
+  }

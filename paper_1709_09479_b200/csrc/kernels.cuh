@@ -790,7 +790,7 @@ __global__ void to_cx(const double2* __restrict__ src, cx<R>* __restrict__ dst, 
 }
 
 // single-block fixed-order sum of block partials into out[0]
-__global__ void sum_partials(const double* partial, int count, double* out) {
+static __global__ void sum_partials(const double* partial, int count, double* out) {
   __shared__ double red[32];
   double v = 0.0;
   for (int i = threadIdx.x; i < count; i += blockDim.x) v += partial[i];
@@ -1024,13 +1024,13 @@ cg_pupdate(const cx<R>* __restrict__ r, cx<R>* __restrict__ p, const CgState* st
   p[i] = mk<C>(R(rv.x + be * pv.x), R(rv.y + be * pv.y));
 }
 
-__global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step,
+static __global__ void cg_scalar(const double* partial, int count, double invD, CgState* st, int step,
                           const double* presum) {
   cg_scalar_block(partial, count, invD, st, step, presum);
 }
 
 // Per-image sum of block partials (learning data term / objective), out[n] = 0.5*invD*sum.
-__global__ void per_image_reduce(const double* partial, int tiles, double scale, double* out) {
+static __global__ void per_image_reduce(const double* partial, int tiles, double scale, double* out) {
   __shared__ double red[32];
   const int n = blockIdx.x;
   double v = 0.0;
