@@ -48,9 +48,17 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose: bool = False, defines=(), tag=None, only=None) -> str:
+    """Build the library. Experiment variants: `tag` builds build/var_<tag>/libdcsc_cuda.so
+    with extra -D `defines`, recompiling only the units named in `only` (the
+    rest are the default objects); load it with DCSC_LIB=<path>."""
+    lib, objdir = LIB, OBJDIR
+    if tag:
+        lib = os.path.join(ROOT, "build", "var_" + tag, "libdcsc_cuda.so")
+        objdir = os.path.join(ROOT, "build", "obj_" + tag)
+        build()
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     nvcc = _nvcc()
     hdrs = _headers()
     objs, jobs = [], []
@@ -58,19 +66,22 @@ def build(verbose: bool = False) -> str:
         path = os.path.join(CSRC, src)
         if not src.endswith((".cu", ".cpp")):
             continue
-        obj = os.path.join(OBJDIR, src + ".o")
+        if tag and src not in (only or ()):
+            objs.append(os.path.join(OBJDIR, src + ".o"))
+            continue
+        obj = os.path.join(objdir, src + ".o")
         objs.append(obj)
-        if not _stale(obj, [path] + hdrs):
+        if not _stale(obj, [path] + hdrs) and not tag:
             continue
         if src.endswith(".cu"):
-            cmd = [nvcc, "-c", path, "-o", obj] + NVCC_FLAGS + ["-ccbin", HOST_CXX]
+            cmd = [nvcc, "-c", path, "-o", obj] + NVCC_FLAGS + ["-D" + d for d in defines] + ["-ccbin", HOST_CXX]
         else:
             cmd = [HOST_CXX, "-c", path, "-o", obj, "-O3", "-fPIC", "-fopenmp", "-std=c++17", "-I" + INC, "-I" + CSRC]
         jobs.append((src, cmd))
 
     def run(job):
         src, cmd = job
-        log = os.path.join(OBJDIR, src + ".build.log")
+        log = os.path.join(objdir, src + ".build.log")
         with open(log, "w") as f:
             r = subprocess.run(cmd, stdout=f, stderr=subprocess.STDOUT)
         return src, r.returncode, log
@@ -81,10 +92,10 @@ def build(verbose: bool = False) -> str:
             if rc != 0:
                 sys.stderr.write(open(log).read()[-20000:])
                 raise RuntimeError(f"compile failed on {src}")
-    if _stale(LIB, objs):
-        cmd = [nvcc, "-shared", "-o", LIB] + objs + ARCH + ["-ccbin", HOST_CXX, "-Xcompiler", "-fopenmp", "-lgomp"]
+    if _stale(lib, objs) or tag:
+        cmd = [nvcc, "-shared", "-o", lib] + objs + ARCH + ["-ccbin", HOST_CXX, "-Xcompiler", "-fopenmp", "-lgomp"]
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libdcsc_cuda.so")
+# DCSC_LIB selects an experiment build (build.py tag=...); default: the in-tree library
+LIB_PATH = os.environ.get("DCSC_LIB") or os.path.join(PKG, "lib", "libdcsc_cuda.so")
 
 
 class IoError(RuntimeError):
