@@ -9,7 +9,6 @@ compiles 16x16 and up, so the same properties are checked on 16x16 / 20x20.
 import numpy as np
 import pytest
 
-from oracle import ref
 from paper_1709_09479_b200 import dcsc
 
 pytestmark = pytest.mark.gpu
@@ -81,19 +80,26 @@ def test_lambda_matches_dense_solve():
 
 
 def test_dual_feasibility_support_stationarity_and_duality_gap():
-    # test_coding.cpp:203-235
-    rng = np.random.default_rng(37)
+    # test_coding.cpp:203-235 on a 16x16 instance (the reference's 8x8 grid is
+    # not compiled here). Support stationarity is checked at 2e-4 instead of
+    # 1e-4: on 16x16 instances the reference itself stops (ADMM tol 1e-4) with
+    # |D^T lambda| up to 1.1e-4 below beta on the support (this seed, oracle).
+    from oracle import ref
+
+    rng = np.random.default_rng(59)
     d = rng_dictionary(rng, 3, 3)
     x = rng.standard_normal((16, 16))
     cfg = dcsc.SolverConfig(beta=0.1, rho=0.1, max_admm=8000, normalize=0)
     z, st, stats = dcsc.solve_coding(x, d, cfg)
+    _, _, rstats = ref.solve_coding(x, d, ref.Cfg(beta=0.1, rho=0.1, max_admm=8000, normalize=0))
+    assert stats["converged"] and stats["admm_iters"] == rstats["admm_iters"]
     assert np.abs(st.theta).max() <= cfg.beta
     with ctx_for(x[None], d, cfg) as ctx:
         dt = ctx.dictionary_adjoint(st.lam[None])[0]
     assert np.abs(dt).max() <= cfg.beta + 1e-6
     on = np.abs(z) > 1e-6
     assert on.any()
-    assert (np.abs(dt[on]) >= cfg.beta - 1e-4).all()
+    assert (np.abs(dt[on]) >= cfg.beta - 2e-4).all()
     primal = dcsc.evaluate_objective(x, d, z, cfg.beta)[2]
     assert (primal - stats["dual_objective"]) / primal < 1e-3
     assert primal - stats["dual_objective"] > -1e-9
@@ -112,13 +118,21 @@ def test_shift_equivariance():
 
 
 def test_warm_restart_resumes_near_the_solution():
-    # test_coding.cpp:275-290
-    rng = np.random.default_rng(40)
+    # test_coding.cpp:275-290, on a 16x16 instance whose cold start converges
+    # (the reference's own counts, from the oracle, must match exactly)
+    from oracle import ref
+
+    rng = np.random.default_rng(59)
     d = rng_dictionary(rng, 2, 3)
     x = rng.standard_normal((16, 16))
     cfg = dcsc.SolverConfig(beta=0.1, rho=0.1, max_admm=8000, normalize=0)
     _, st, cold = dcsc.solve_coding(x, d, cfg)
     _, _, warm = dcsc.solve_coding(x, d, cfg, st)
+    rcfg = ref.Cfg(beta=0.1, rho=0.1, max_admm=8000, normalize=0)
+    _, rst, rcold = ref.solve_coding(x, d, rcfg)
+    _, _, rwarm = ref.solve_coding(x, d, rcfg, rst)
+    assert (cold["admm_iters"], warm["admm_iters"]) == (rcold["admm_iters"], rwarm["admm_iters"])
+    assert cold["converged"]
     assert warm["admm_iters"] <= cold["admm_iters"]
     assert warm["admm_iters"] < 50
 
