@@ -110,12 +110,8 @@ struct ClusterPlane {
     using S = Split<ColPlan>;
     constexpr int R1 = S::first;
     const C* twc = tw + TW_COL;
-    stockham<C, H, R1, 1, true, COLS, T>(
-        twc,
-        [&](int cl, int r) {
-          const int col = col_of(rank, cl);
-          return col == 0 ? pack_col0(gen(r, 0), gen(r, M)) : gen(r, col);
-        },
+    gen_first_stage_inv<C, H, R1, COLS, T>(
+        M, [&](int cl) { return col_of(rank, cl); }, gen, [](C x0, C xn) { return pack_col0(x0, xn); },
         [&](int l, int i, C v) { a[i * CS + l] = v; });
     __syncthreads();
     return run_stages<C, H, true, COLS, CS, 1, T, R1>(a, b, twc, typename S::tail{});

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
         mbar_wait(dbar, dphase);
         dphase ^= 1u;
         const C* sd = stg;
-        cs = P::cols_inv(stg == B0 ? B1 : B0, stg, TW, [&](int r, int c) {
+        cs = P::template cols_inv<false>(stg == B0 ? B1 : B0, stg, TW, [&](int r, int c) {
           const int b = r * Wh + c;
           return cmulc(sd[b], LAM[b]);
         });

@@ -93,6 +93,11 @@ __device__ __forceinline__ void cl_init_exchange(unsigned long long* bar) {
 // issued, B_F (after exchange F's blocks are consumed) before the next
 // filter's exchange I / plane load — two barriers per filter, each with a
 // pass of slack.
+#ifndef DCSC_CL_PROX_UNROLL
+#define DCSC_CL_PROX_UNROLL 16
+#endif
+constexpr int kClProxUnroll = DCSC_CL_PROX_UNROLL;  // u loads in flight per thread in the prox loop
+
 template <class CP, int MODE>
 __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     coding_pass_cl(CodingArgs<typename CP::R> a) {
@@ -161,7 +166,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       cluster_arrive();  // B_I: my Z consumed, my incoming blocks complete
       CP::rows_inv_rest(X, Z, TW);
       R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
-#pragma unroll 4
+#pragma unroll kClProxUnroll
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
         const int rl = it / M, m = it % M;
         const C uv = __ldcs(uk + it);  // u streams through once: evict-first (keeps d_hat, lambda_hat in L2)
@@ -231,6 +236,13 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     CP::cols_fwd_first(Y, Z, X, TW, rank);
     __syncthreads();
     cluster_arrive();  // B_F: my Y consumed, my incoming blocks complete
+    // column-0 epilogue operands (rank 0) fetched with the last stage's loads,
+    // so rank 0 does not trail its peers by an L2 round trip every filter
+    C d0 = mk<C>(R(0), R(0)), dMv = mk<C>(R(0), R(0));
+    if (rank == 0 && threadIdx.x < H) {
+      d0 = __ldg(dk + threadIdx.x * Wh);
+      dMv = __ldg(dk + threadIdx.x * Wh + M);
+    }
     {
       const C* twc = TW + CP::TW_COL;
       const int it = threadIdx.x;
@@ -261,8 +273,8 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       const int r = threadIdx.x;
       C x0, xn;
       CP::unpack_col0(COL0, r, x0, xn);
-      acc0 = cadd(acc0, cmul(__ldg(dk + r * Wh), x0));
-      accN = cadd(accN, cmul(__ldg(dk + r * Wh + M), xn));
+      acc0 = cadd(acc0, cmul(d0, x0));
+      accN = cadd(accN, cmul(dMv, xn));
     }
   }
   cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
