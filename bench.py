@@ -287,11 +287,22 @@ def config_block(cfg, args):
 def run_ours(args, cfg):
     world, rank, local = dist_env()
     dist = None
+    # DCSC_BENCH_DIST_BACKEND=gloo: host-side collectives (and the learning
+    # all-reduce through the gloo host callback), so the multi-rank path can be
+    # exercised with several ranks sharing one GPU; timings are then not scaling data.
+    backend = os.environ.get("DCSC_BENCH_DIST_BACKEND", "nccl")
+    dev = 0
+    tdev = "cpu"
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(local)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev = local % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            tdev = "cuda"
+        else:
+            tdist.init_process_group("gloo")
         dist = tdist
     from paper_1709_09479_b200 import dcsc
     N = cfg["N"]
@@ -311,15 +322,18 @@ def run_ours(args, cfg):
     units = world if weak else 1  # C1-workload outer iterations per step, all ranks
     sc = dcsc.SolverConfig(beta=cfg["beta"], max_admm=cfg["max_admm"], normalize=0, seed=SEED, tol=1e-300)
     ctx = dcsc.Context(nl, (cfg["H"], cfg["W"]), cfg["K"], (cfg["m"], cfg["m"]), sc, cfg["prec"],
-                       device=local if world > 1 else 0, channels=cfg.get("J", 1))
+                       device=dev, channels=cfg.get("J", 1))
     if world > 1 and not cfg["coding_only"]:
         # learning sums its K x NB correlations and CG scalars over ranks (NCCL)
         import torch
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.tensor(list(dcsc.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        ctx.set_comm_nccl(world, rank, bytes(uid.cpu().tolist()))
+        if backend == "nccl":
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.tensor(list(dcsc.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            ctx.set_comm_nccl(world, rank, bytes(uid.cpu().tolist()))
+        else:
+            ctx.set_comm_callback(world, rank, dcsc.gloo_allreduce_fn())
     ctx.set_signals(x)
     ctx.set_dictionary(d_true)
 
@@ -339,7 +353,7 @@ def run_ours(args, cfg):
     barrier()
     ctx.set_profiling(2)  # per-launch events on the roofline kernel only (coding pass)
     l0 = ctx.kernel_launches()
-    with ClockSampler(local if world > 1 else 0) as clk:
+    with ClockSampler(dev) as clk:
         ctx.event_mark(0)
         stats = None
         for _ in range(args.steps):
@@ -357,7 +371,7 @@ def run_ours(args, cfg):
     fam_ms = {fam_names[f]: round(ctx.kernel_time(f)[0], 3) for f in range(5)}
     if dist:
         import torch
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ctx.set_profiling(False)
@@ -375,7 +389,7 @@ def run_ours(args, cfg):
     e2e_s = time.perf_counter() - t0
     if dist:
         import torch
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = units * e2e_steps / e2e_s

@@ -17,6 +17,9 @@
 // the final state; the replica additionally dumps the per-outer-iteration
 // dictionary, the l0 count of the maps and mu_iters. tests/ assert that its
 // trace equals run_csc's (ref_run_csc) bit for bit at one thread.
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -184,6 +187,12 @@ int ref_last_error(char* buf, std::size_t len) {
 }
 
 int ref_set_threads(int n) {
+  // par::max_threads() is capped by omp_get_max_threads(), which a launcher's
+  // OMP_NUM_THREADS=1 (torchrun's default) would pin to 1: raise the OpenMP
+  // thread budget of this (calling) thread too.
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#endif
   par::set_max_threads(n);
   return par::max_threads();
 }
