@@ -405,7 +405,6 @@ class Engine final : public EngineBase {
     no_cg_fuse_ = std::getenv("DCSC_NO_CG_FUSE") != nullptr;
     CK(cudaMemsetAsync(cgcnt_.p, 0, cgcnt_.bytes, st_));
     hred_.alloc(sizeof(double) * std::max(64, K_ + 8));
-    cglob_.alloc(sizeof(double2) * (size_t)K_ * NB);
     tiles_ = (NB + TBV - 1) / TBV;
     const size_t vec_blocks = (nNB + TBV - 1) / TBV;
     accept_chunks_ = std::max(1, std::min(64, (int)((size_t)K_ * D / (TBV * 8))));
@@ -909,18 +908,23 @@ class Engine final : public EngineBase {
     });
     const size_t knb = (size_t)K_ * NB;
     const unsigned rb = (unsigned)((knb + 255) / 256);
-    if (!multi()) {
-      launch(kFamContract, [&] {
-        contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(), nullptr, csplit_, knb, done);
-      });
-    } else {  // FP64 partials summed over ranks, then rounded once
-      launch(kFamContract, [&] {
-        contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), nullptr, cglob_.as<double2>(), csplit_, knb,
-                                                  done);
-      });
-      red_->allreduce(reinterpret_cast<double*>(cglob_.p), 2 * knb, st_);
-      launch(kFamContract, [&] { to_cx<R><<<rb, 256, 0, st_>>>(cglob_.as<double2>(), cvec_.as<C>(), knb, done); });
-    }
+    // multi-rank: this is the rank's partial correlation; the ranks' sum is
+    // taken after the mask's crop (mask_crop / apply_hat), K x M values instead of K x NB
+    launch(kFamContract, [&] {
+      contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(), csplit_, knb, done);
+    });
+  }
+
+  // Cropped correlation of cvec_ (mask_step mode 1: d_recover scaling, mode 2:
+  // plain) into dd_ (K x M), summed over ranks: the crop of the inverse DFT is
+  // linear, so crop(iDFT(sum_r c_r)) = sum_r crop(iDFT(c_r)) and the ranks
+  // exchange K x M values (C3: 124 KB) instead of the K x NB spectra (67 MB).
+  void mask_crop(int mode, const int* done) {
+    launch(kFamMask, [&] {
+      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_,
+                  mode, dtw_.as<C>(), done);
+    });
+    if (multi()) red_->allreduce(dd_.as<double>(), (size_t)K_ * M_, st_);
   }
 
   // A v for half-spectrum stacks (LearningOperator::apply, learning.cpp:83-122)
@@ -928,10 +932,15 @@ class Engine final : public EngineBase {
   // also runs the alpha step (no separate cg_scalar launch)
   void apply_hat(const C* v, C* out, const int* done = nullptr, bool fuse_alpha = false) {
     correlate_hat(v, done);
-    launch(kFamMask, [&] {
-      launch_mask(K_, st_, cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(), dmu_.as<double>(), mh_, mw_, 0,
-                  dtw_.as<C>(), done);
-    });
+    if (!multi()) {
+      launch(kFamMask, [&] {
+        launch_mask(K_, st_, cvec_.as<C>(), phat_.as<C>(), nullptr, live_.as<int>(), dmu_.as<double>(), mh_, mw_, 0,
+                    dtw_.as<C>(), done);
+      });
+    } else {  // crop per rank, sum the K x M crops, then p_hat = DFT(pad(crop))
+      mask_crop(2, done);
+      launch(kFamMask, [&] { launch_filters(K_, st_, dd_.as<double>(), mh_, mw_, phat_.as<C>(), dtw_.as<C>()); });
+    }
     // fused: fewer image rows per launch (each block loops over images) so the
     // last-block alpha step sums few partials and the arrival counter sees
     // few atomics
@@ -1029,10 +1038,7 @@ class Engine final : public EngineBase {
   void d_recover(std::vector<double>& d) {
     correlate_hat(gam_ch_, nullptr);
     // d_recover does not skip dead filters; their correlation is exactly zero anyway
-    launch(kFamMask, [&] {
-      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
-                  dtw_.as<C>(), nullptr);
-    });
+    mask_crop(1, nullptr);
     d.resize((size_t)K_ * M_);
     CK(cudaMemcpyAsync(d.data(), dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
@@ -1140,10 +1146,7 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(tmp.p, v, tmp.bytes, cudaMemcpyHostToDevice, st_));
     r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
     correlate_hat(r_.as<C>(), nullptr);
-    launch(kFamMask, [&] {
-      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 2,
-                  dtw_.as<C>(), nullptr);
-    });
+    mask_crop(2, nullptr);
     CK(cudaMemcpyAsync(out, dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
   }
@@ -1252,10 +1255,7 @@ class Engine final : public EngineBase {
     r2c(tmp.p, true, D, r_.as<C>(), NB, N_);
     correlate_hat(r_.as<C>(), nullptr);
     CK(cudaMemcpyAsync(dmu_.p, mu, sizeof(double) * K_, cudaMemcpyHostToDevice, st_));
-    launch(kFamMask, [&] {
-      launch_mask(K_, st_, cvec_.as<C>(), nullptr, dd_.as<double>(), live_.as<int>(), dmu_.as<double>(), mh_, mw_, 1,
-                  dtw_.as<C>(), nullptr);
-    });
+    mask_crop(1, nullptr);
     CK(cudaMemcpyAsync(out, dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
     upload_mu();  // the context's own mu back on the device
     CK(cudaStreamSynchronize(st_));
@@ -1562,7 +1562,7 @@ class Engine final : public EngineBase {
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_, cpart_, hred_, cglob_, ginv_, what_, cgcnt_;
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, ginv_, what_, cgcnt_;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
   C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel

@@ -765,8 +765,8 @@ contract_c(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ v, double2*
 }
 
 template <class R>
-__global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __restrict__ c,
-                                  double2* __restrict__ c64, int splits, size_t KNB, const int* done) {
+__global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __restrict__ c, int splits, size_t KNB,
+                                  const int* done) {
   if (done && *done) return;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= KNB) return;
@@ -776,17 +776,7 @@ __global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __re
     ar += p.x;
     ai += p.y;
   }
-  if (c64)
-    c64[i] = make_double2(ar, ai);  // summed over ranks before rounding
-  else
-    c[i] = mk<cx<R>>(R(ar), R(ai));
-}
-
-template <class R>
-__global__ void to_cx(const double2* __restrict__ src, cx<R>* __restrict__ dst, size_t n, const int* done) {
-  if (done && *done) return;
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = mk<cx<R>>(R(src[i].x), R(src[i].y));
+  c[i] = mk<cx<R>>(R(ar), R(ai));
 }
 
 // single-block fixed-order sum of block partials into out[0]
