@@ -350,6 +350,9 @@ class Engine final : public EngineBase {
     xhat_.alloc(sizeof(C) * nNB * J_);                // J x N x NB (channel-major)
     dhat_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);    // J x K x NB (channel-major)
     dcand_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);
+    if constexpr (CLU) {
+      if (J_ == 1) dhat_rb_.alloc(sizeof(C) * (size_t)K_ * CLN * P::BUF);  // rank-blocked d_hat (cl_rank_block)
+    }
     sigma_.alloc(sizeof(R) * NB);
     u_.alloc(sizeof(R) * nD * K_);
     maps_.alloc(sizeof(R) * nD * K_);
@@ -414,7 +417,8 @@ class Engine final : public EngineBase {
     l0_.alloc(sizeof(unsigned long long) * (size_t)N_ * accept_chunks_);
     device_bytes = x_.bytes + xhat_.bytes + dhat_.bytes + dcand_.bytes + sigma_.bytes + u_.bytes +
                    maps_.bytes + lamhat_.bytes + lam_.bytes + part_.bytes + sums_.bytes + gam_.bytes +
-                   3 * r_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes + ginv_.bytes + what_.bytes;
+                   3 * r_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes + ginv_.bytes + what_.bytes +
+                   dhat_rb_.bytes;
     CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
     CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
     CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
@@ -495,6 +499,7 @@ class Engine final : public EngineBase {
     a.sigma = sigma_.as<R>();
     a.lamhat_w = lamhat_.as<C>() + (size_t)n_off * J_ * NB;
     a.img = img_.as<ImageAdmm>() + n_off;
+    a.dhat_rb = (dhat == dhat_.as<C>() && dhat_rb_.p) ? dhat_rb_.as<C>() : nullptr;
     a.iter = 0;
     a.is_last = 0;
     return a;
@@ -594,6 +599,12 @@ class Engine final : public EngineBase {
     dict_.assign(d, d + cnt);
     dict_zero_ = std::all_of(dict_.begin(), dict_.end(), [](double v) { return v == 0.0; });
     upload_dict_spectra(dict_.data(), dhat_.as<C>());
+    if constexpr (CLU) {
+      if (dhat_rb_.p)
+        launch(kFamOther, [&] {
+          cl_rank_block<P><<<592, 256, 0, st_>>>(dhat_.as<C>(), dhat_rb_.as<C>(), K_);
+        });
+    }
     if (J_ == 1) {
       launch(kFamOther, [&] {
         sigma_kernel<R><<<(NB + 255) / 256, 256, 0, st_>>>(dhat_.as<C>(), sigma_.as<R>(), K_, NB, cfg_.rho);
@@ -1562,7 +1573,7 @@ class Engine final : public EngineBase {
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_, cpart_, hred_, ginv_, what_, cgcnt_;
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, ginv_, what_, cgcnt_, dhat_rb_;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
   C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel

@@ -52,6 +52,10 @@ struct CodingArgs {
   // accumulating, and the per-bin J x J solve runs in tc_lambda.
   int J;
   cx<R>* what;
+  // cluster family (J = 1): d_hat in the rank-blocked layout K x CL x [H][CS]
+  // (cl_rank_block), so a rank's generator slice is one contiguous TMA copy;
+  // nullptr: the generator reads d_hat from L2
+  const cx<R>* dhat_rb;
 };
 
 // Bulk prefetch of a contiguous global range into L2 (sm_90+ TMA engine op).

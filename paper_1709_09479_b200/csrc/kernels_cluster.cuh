@@ -105,6 +105,31 @@ __device__ __forceinline__ void cl_init_exchange(unsigned long long* bar) {
 // issued, B_F (after exchange F's blocks are consumed) before the next
 // filter's exchange I / plane load — two barriers per filter, each with a
 // pass of slack.
+// d_hat (K x NB) -> rank-blocked copy K x CL x [H][CS]: slot cl < COLS holds
+// column col_of(c, cl) of rank c, slot COLS column W/2 (rank 0's packed pair
+// partner; zero elsewhere). Built once per dictionary (set_dictionary).
+template <class CP>
+__global__ void cl_rank_block(const cx<typename CP::R>* __restrict__ dhat, cx<typename CP::R>* __restrict__ out,
+                              int K) {
+  using C = typename CP::C;
+  constexpr int H = CP::H, CS = CP::CS, COLS = CP::COLS, CL = CP::CL, Wh = CP::Wh, M = CP::M, NB = CP::NB;
+  constexpr int BUF = CP::BUF;
+  static_assert(BUF == H * CS, "rank block = one column buffer");
+  const size_t total = (size_t)K * CL * BUF;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i % BUF);
+    const int c = (int)((i / BUF) % CL);
+    const size_t k = i / ((size_t)BUF * CL);
+    const int r = e / CS, cl = e % CS;
+    C v = mk<C>(typename CP::R(0), typename CP::R(0));
+    if (cl < COLS)
+      v = dhat[k * NB + r * Wh + CP::col_of((unsigned)c, cl)];
+    else if (c == 0)
+      v = dhat[k * NB + r * Wh + M];
+    out[i] = v;
+  }
+}
+
 #ifndef DCSC_CL_PROX_UNROLL
 #define DCSC_CL_PROX_UNROLL 16
 #endif
@@ -119,6 +144,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   constexpr int H = CP::H, M = CP::M, Wh = CP::Wh, NB = CP::NB, D = CP::D, T = CP::T, CL = CP::CL;
   constexpr int ROWS = CP::ROWS, COLS = CP::COLS, CS = CP::CS;
   constexpr int BS = CP::buffer_bytes / sizeof(C);
+  static_assert(BS == CP::BUF, "rank-blocked d_hat stride (cl_rank_block) = buffer size");
   constexpr bool ADMM = MODE == kPassAdmm;
   using S = Split<typename CP::ColPlan>;
   static_assert(CountStages<typename CP::ColPlan>::value == 2, "two-stage column plan (X -> Y)");
@@ -140,7 +166,21 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   if (ADMM && a.conv[n]) return;  // the whole cluster sees the same flag
 
   CP::load_twiddles(TW, a.tw);
-  cl_init_exchange<CP>(xbar);
+  // The generator's d_hat slice of each filter is staged by one TMA copy into
+  // Y (rank-blocked layout) while the previous filter's last stage runs; Y is
+  // free then (exchange F's blocks consumed) and no peer writes it before this
+  // rank's own next-filter exchange (B_I). Only lambda_hat is read from L2.
+  __shared__ __align__(8) unsigned long long dbar_s;
+  unsigned long long* dbar = &dbar_s;
+  unsigned dphase = 0;
+  const bool DST = ADMM && a.dhat_rb != nullptr;
+  const int k0s = (int)(blockIdx.x / CL) * a.kpg;
+  if (DST && threadIdx.x == 0) mbar_init(dbar, 1);
+  cl_init_exchange<CP>(xbar);  // (fences the mbarrier inits, syncs the CTA)
+  if (DST && threadIdx.x == 0 && k0s < a.K) {
+    mbar_expect_tx(dbar, (unsigned)(sizeof(C) * BS));
+    bulk_g2s(Y, a.dhat_rb + ((size_t)k0s * CL + rank) * BS, (unsigned)(sizeof(C) * BS), dbar);
+  }
   cluster_arrive();  // matched by the wait before the first filter's exchange
 
   constexpr int RL = S::last, JL = H / RL, ITEMS_L = COLS * JL;
@@ -163,10 +203,22 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         prefetch_l2_bulk(uk, sizeof(C) * ROWS * M);
         if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       }
-      CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
-        const int b = r * Wh + c;
-        return cmulc(__ldg(dk + b), __ldg(lam + b));
-      });
+      if (DST) {
+        mbar_wait(dbar, dphase);
+        dphase ^= 1u;
+        CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
+          unsigned cr;
+          int cl;
+          CP::owner_of(c, cr, cl);
+          const int slot = c == M ? COLS : cl;
+          return cmulc(Y[r * CS + slot], __ldg(lam + r * Wh + c));
+        });
+      } else {
+        CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
+          const int b = r * Wh + c;
+          return cmulc(__ldg(dk + b), __ldg(lam + b));
+        });
+      }
       fence_async_smem();
       __syncthreads();
       cluster_wait();  // B_F (previous filter): peers' Z free
@@ -248,6 +300,11 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     CP::cols_fwd_first(Y, Z, X, TW, rank);
     __syncthreads();
     cluster_arrive();  // B_F: my Y consumed, my incoming blocks complete
+    if (DST && threadIdx.x == 0 && k + 1 < k1) {  // next filter's d_hat slice -> Y
+      fence_async_smem();
+      mbar_expect_tx(dbar, (unsigned)(sizeof(C) * BS));
+      bulk_g2s(Y, a.dhat_rb + ((size_t)(k + 1) * CL + rank) * BS, (unsigned)(sizeof(C) * BS), dbar);
+    }
     // column-0 epilogue operands (rank 0) fetched with the last stage's loads,
     // so rank 0 does not trail its peers by an L2 round trip every filter
     C d0 = mk<C>(R(0), R(0)), dMv = mk<C>(R(0), R(0));
