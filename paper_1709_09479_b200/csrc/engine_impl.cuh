@@ -956,11 +956,19 @@ class Engine final : public EngineBase {
     // last-block alpha step sums few partials and the arrival counter sees
     // few atomics
     const dim3 g3(tiles_, fuse_alpha ? std::min(N_, std::max(1, fused_rows_ / tiles_)) : N_);
+    // two images per pass share the p_hat loads once the p_hat stack outgrows ~16 MB (C3)
+    const bool pair = sizeof(C) * (size_t)K_ * NB > (16u << 20);
     launch(kFamContract, [&] {
-      contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(), live_.as<int>(),
-                                                 v, out, partial_.as<double>(), N_, K_, NB, Wh, 0, done,
-                                                 fuse_alpha ? cg_.as<CgState>() : nullptr, cgcnt_.as<unsigned>(),
-                                                 1.0 / D);
+      if (pair)
+        contract_out<R, TBV, 2><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(),
+                                                      live_.as<int>(), v, out, partial_.as<double>(), N_, K_, NB, Wh,
+                                                      0, done, fuse_alpha ? cg_.as<CgState>() : nullptr,
+                                                      cgcnt_.as<unsigned>(), 1.0 / D);
+      else
+        contract_out<R, TBV><<<g3, TBV, 0, st_>>>(zhat_.as<C>(), phat_.as<C>(), dwk_.as<double>(), live_.as<int>(),
+                                                   v, out, partial_.as<double>(), N_, K_, NB, Wh, 0, done,
+                                                   fuse_alpha ? cg_.as<CgState>() : nullptr, cgcnt_.as<unsigned>(),
+                                                   1.0 / D);
     });
   }
 

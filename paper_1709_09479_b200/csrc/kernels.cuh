@@ -875,7 +875,7 @@ __device__ __forceinline__ bool last_block_arrive(unsigned* counter, unsigned to
 // frequency domain), with the block partial of <v, out> (Parseval, FP64).
 // mode 1 (learning data term): y_n = sum_k d_hat_k z_hat_nk, partial of
 // |y_n - x_hat_n|^2 weighted, no identity (objective.cpp:83-95).
-template <class R, int TB>
+template <class R, int TB, int NI = 1>
 __global__ void __launch_bounds__(TB)
 contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const double* __restrict__ wk,
              const int* __restrict__ live, const cx<R>* __restrict__ v, cx<R>* __restrict__ out,
@@ -887,46 +887,69 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
   const int b = blockIdx.x * TB + threadIdx.x;
   double dot = 0.0;
   // images n = blockIdx.y, + gridDim.y, ...: one image per block unless the
-  // caller (fused CG apply) launches fewer rows to keep the partial count small
-  for (int n = blockIdx.y; n < N; n += gridDim.y) {
+  // caller (fused CG apply) launches fewer rows to keep the partial count small.
+  // NI images per pass share each p_hat load (NI = 2 pays when the p_hat
+  // stack is far beyond L1 reuse, C3: 5.89 vs 6.11 s of contractions per outer
+  // iteration; at C2/C4 NI = 1 is 3-5% faster). Same accumulation order.
+  for (int n = blockIdx.y; n < N; n += NI * gridDim.y) {
   if (b < NB) {
     // Dead filters have identically zero z_hat (and p_hat), so summing them
     // adds exact zeros: no per-filter branch, loads batched 8 deep.
-    double ar = 0.0, ai = 0.0;
-    const C* zp = zhat + (size_t)n * K * NB + b;
+    double ar[NI], ai[NI];
+    const C* zp[NI];
+    bool ok[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int ni = n + i * gridDim.y;
+      ok[i] = ni < N;
+      zp[i] = zhat + (size_t)(ok[i] ? ni : n) * K * NB + b;
+      ar[i] = ai[i] = 0.0;
+    }
     const C* pp = p + b;
     constexpr int U = 8;
     int k = 0;
     for (; k + U <= K; k += U) {
-      C z[U], q[U];
+      C z[NI][U], q[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        z[u] = __ldcs(zp + (size_t)(k + u) * NB);  // streaming: keep p_hat resident in L2
+#pragma unroll
+        for (int i = 0; i < NI; ++i) z[i][u] = __ldcs(zp[i] + (size_t)(k + u) * NB);  // streaming: keep p_hat in L2
         q[u] = __ldg(pp + (size_t)(k + u) * NB);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double w = mode == 0 ? wk[k + u] : 1.0;
-        ar += w * ((double)z[u].x * (double)q[u].x - (double)z[u].y * (double)q[u].y);
-        ai += w * ((double)z[u].x * (double)q[u].y + (double)z[u].y * (double)q[u].x);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          ar[i] += w * ((double)z[i][u].x * (double)q[u].x - (double)z[i][u].y * (double)q[u].y);
+          ai[i] += w * ((double)z[i][u].x * (double)q[u].y + (double)z[i][u].y * (double)q[u].x);
+        }
       }
     }
     for (; k < K; ++k) {
-      const C z = __ldcs(zp + (size_t)k * NB);
       const C q = __ldg(pp + (size_t)k * NB);
       const double w = mode == 0 ? wk[k] : 1.0;
-      ar += w * ((double)z.x * (double)q.x - (double)z.y * (double)q.y);
-      ai += w * ((double)z.x * (double)q.y + (double)z.y * (double)q.x);
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const C z = __ldcs(zp[i] + (size_t)k * NB);
+        ar[i] += w * ((double)z.x * (double)q.x - (double)z.y * (double)q.y);
+        ai[i] += w * ((double)z.x * (double)q.y + (double)z.y * (double)q.x);
+      }
     }
     (void)live;
-    const C vv = v[(size_t)n * NB + b];
-    if (mode == 0) {
-      const C o = mk<C>(R((double)vv.x + ar), R((double)vv.y + ai));
-      out[(size_t)n * NB + b] = o;
-      dot += bin_weight(b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
-    } else {
-      const double rr = ar - (double)vv.x, ri = ai - (double)vv.y;
-      dot += bin_weight(b, Wh) * (rr * rr + ri * ri);
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      if (!ok[i]) continue;
+      const size_t o_n = (size_t)(n + i * gridDim.y) * NB + b;
+      const C vv = v[o_n];
+      if (mode == 0) {
+        const C o = mk<C>(R((double)vv.x + ar[i]), R((double)vv.y + ai[i]));
+        out[o_n] = o;
+        dot += bin_weight(b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
+      } else {
+        const double rr = ar[i] - (double)vv.x, ri = ai[i] - (double)vv.y;
+        dot += bin_weight(b, Wh) * (rr * rr + ri * ri);
+      }
     }
   }
   }
