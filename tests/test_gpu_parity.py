@@ -239,6 +239,18 @@ def test_cluster_plane_learning_fp32_matches_reference():
     assert abs(a - b) <= FP32_TOL * abs(b)
 
 
+def test_cluster_plane_run_fp32_matches_reference():
+    """run_csc on the 256x256 cluster family over 2 outer iterations: the
+    learned dictionary re-enters coding through set_dictionary (rank-blocked
+    d_hat copy rebuilt), so a stale copy would show in the second outer step."""
+    x, _ = problem(2, (256, 256), 3, 11, p=0.01, fp32=True)
+    kw = dict(beta=0.5, max_outer=2, normalize=0, seed=9, tol=1e-300, max_admm=20, max_mu_iters=3, cg_max=15)
+    r = ref.run(x, 3, (11, 11), ref.Cfg(**kw))
+    g = dcsc.run_csc(x, 3, (11, 11), dcsc.SolverConfig(**kw), precision=32)
+    compare_runs(g, r, FP32_TOL)
+    assert rel(g["dict"], r["dict"]) <= 1e-3
+
+
 @pytest.mark.parametrize("mode", [1, 2])
 def test_run_with_normalisation_matches_reference(mode):
     """normalize Global (1) / Local (2) (pipeline.cpp:78-121) inside run_csc."""
