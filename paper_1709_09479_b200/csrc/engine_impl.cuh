@@ -389,6 +389,10 @@ class Engine final : public EngineBase {
       const double want = std::max(1.0, 4.0 * sms / (double)base);
       const long p2 = 1L << (int)std::lround(std::log2(want));  // nearest power of two (measured: C4 16 > 17)
       csplit_ = (int)std::max(1L, std::min({p2, 64L, (long)N_}));
+      if (const char* e = std::getenv("DCSC_CSPLIT")) {  // experiment override
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= std::min(64, N_)) csplit_ = v;
+      }
     }
     if (const char* e = std::getenv("DCSC_CSPLIT")) csplit_ = std::max(1, std::min(N_, std::atoi(e)));
     cpart_.alloc(sizeof(double2) * (size_t)csplit_ * K_ * NB);
