@@ -24,8 +24,9 @@ struct InvErr : std::runtime_error { using std::runtime_error::runtime_error; };
     if (e_ != cudaSuccess) throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));     \
   } while (0)
 
-// Learning is image-sharded like coding (no z_hat all-to-all): the K x NB
-// correlation partials, the CG scalars and the trace sums are all-reduced.
+// Learning is image-sharded like coding (no z_hat all-to-all): the K x M
+// cropped correlations (each rank crops its own partial), the CG scalars and
+// the trace sums are all-reduced.
 // NCCL is dlopen'ed (libnccl.so.2) so a process that already loaded torch's
 // NCCL shares it; the host-callback reducer lets ranks that share one GPU be
 // tested with host-side (gloo) reductions.
@@ -34,7 +35,6 @@ struct Reducer {
   virtual ~Reducer() = default;
   virtual void allreduce(double* dev, size_t n, cudaStream_t st) = 0;  // in-place sum
 };
-
 
 // ---------------------------------------------------------------- interface
 class EngineBase {
