@@ -276,3 +276,31 @@ def test_full_size_coding_properties_and_determinism(name, max_admm):
     inner = np.abs(th1) < beta * (1 - 1e-6)
     assert (z1[inner] == 0).all()
     assert np.isfinite(lam1).all() and np.isfinite(z1).all()
+
+
+def test_reference_parameter_setting_monotone_feasible_and_matching():
+    # test_pipeline.cpp:210-226: synthetic_dataset({64,64}, 1, 10, 123), K = 49,
+    # 11x11, beta 0.5, rho 0.1, two outer iterations, max_admm 50, cg_max 30,
+    # seed 6 (default Global normalisation) — and the trace equals the oracle's
+    from oracle import ref
+
+    x = dcsc.synth_dataset(10, 1, (64, 64), 123)
+    kw = dict(beta=0.5, rho=0.1, max_outer=2, max_admm=50, cg_max=30, seed=6, normalize=1)
+    g = dcsc.run_csc(x, 49, (11, 11), dcsc.SolverConfig(**kw), precision=64)
+    tot = [r["total"] for r in g["trace"]]
+    assert len(tot) == 4
+    assert all(b <= a + 1e-9 * abs(a) for a, b in zip(tot, tot[1:])), tot
+    assert (np.linalg.norm(g["dict"].reshape(49, -1), axis=1) <= 1.0 + 1e-6).all()
+    r = ref.run(x, 49, (11, 11), ref.Cfg(**kw), dump_dicts=False)
+    for a, b in zip(g["trace"], r["trace"]):
+        assert a["admm_iters"] == b["admm_iters"] and a["mu_iters"] == b["mu_iters"]
+        assert abs(a["total"] - b["total"]) <= 1e-8 * abs(b["total"])
+    assert np.abs(g["dict"] - r["dict"]).max() <= 1e-7
+
+
+def test_non_finite_signals_are_a_numeric_error():
+    # test_pipeline.cpp:228-240
+    x = np.zeros((1, 16, 16))
+    x[0, 3, 4] = np.nan
+    with pytest.raises(dcsc.NumericError):
+        dcsc.run_csc(x, 2, (3, 3), dcsc.SolverConfig(max_outer=1))
