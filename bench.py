@@ -365,10 +365,11 @@ def run_ours(args, cfg):
     cod_ms, cod_n = ctx.kernel_time(0)
     # per-family breakdown from one extra, untimed step with every launch evented
     ctx.set_profiling(1)
-    step()
+    prof_step = step()
     ctx.synchronize()
     fam_names = ["coding_pass_admm", "lambda_update", "learning_contract", "learning_mask", "other"]
     fam_ms = {fam_names[f]: round(ctx.kernel_time(f)[0], 3) for f in range(5)}
+    learn_ms, learn_n = ctx.kernel_time(2)  # z_hat streams (contract_c / contract_out) of that step
     if dist:
         import torch
         t = torch.tensor([ms], device=tdev)
@@ -426,6 +427,26 @@ def run_ours(args, cfg):
                            "traffic": traffic_from_profiles(args.config), "algorithmic_bytes_per_launch": algo,
                            "avg_launch_ms": avg, "launches": cod_n,
                            "share_of_step": cod_ms / ms}
+    if learn_n and not cfg["coding_only"]:
+        # learning's z_hat streams over the profiled outer iteration: each CG
+        # apply (cg_iters + one warm-start residual apply per mu iteration) is one
+        # contract_c + one contract_out, each d_recover one contract_c; launches
+        # issued past the device-side CG stop exit at once and are not counted
+        rows = [r for r in prof_step[0] if r["phase"] == 1] if isinstance(prof_step, tuple) else []
+        cg_it = sum(r["cg_iters"] for r in rows)
+        mu_it = sum(r["mu_iters"] for r in rows)
+        streams = 2 * (cg_it + mu_it) + mu_it
+        if streams > 0:
+            sc = 8 if cfg["prec"] == 32 else 16
+            nbins = cfg["H"] * (cfg["W"] // 2 + 1)
+            per = (nl * cfg["K"] + 3 * nl + cfg["K"]) * nbins * sc  # z_hat + v/out + p_hat per launch
+            ach = per * streams / (learn_ms / 1000.0) / 1e9
+            out["roofline_learning"] = {
+                "bound": "hbm", "kernel": "contract_c / contract_out (z_hat streams)", "achieved": ach,
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak,
+                "algorithmic_bytes_per_launch": per, "launches_counted": streams, "cg_iters": cg_it,
+                "mu_iters": mu_it, "kernel_ms": learn_ms,
+                "note": "one extra, untimed outer iteration with every launch evented"}
     out["clocks"] = clk.summary()
     if world == 1 and not args.no_cpu_baseline and cfg["coding_only"]:
         try:

@@ -195,7 +195,8 @@ int dcsc_cuda_fft_timing(int height, int width, int precision, int batch, int it
 
 /* measurement: kernels launched by this context so far; per-kernel-family
  * CUDA-event timing (family: 0 coding_pass ADMM, 1 lambda_update,
- * 2 learning contractions, 3 learning mask step, 4 other) */
+ * 2 learning contractions — the z_hat streams contract_c / contract_out, one
+ * z_hat read per launch —, 3 learning mask step, 4 other) */
 int dcsc_cuda_kernel_launches(dcsc_cuda_ctx* ctx, long long* count);
 /* per-launch CUDA-event timing on the library stream: 0 off, 1 every launch,
  * 2 coding-pass launches only (cheap enough to leave on in a timed region) */

@@ -925,7 +925,7 @@ class Engine final : public EngineBase {
     const unsigned rb = (unsigned)((knb + 255) / 256);
     // multi-rank: this is the rank's partial correlation; the ranks' sum is
     // taken after the mask's crop (mask_crop / apply_hat), K x M values instead of K x NB
-    launch(kFamContract, [&] {
+    launch(kFamOther, [&] {  // (kFamContract holds only the z_hat streams: contract_c, contract_out)
       contract_c_reduce<R><<<rb, 256, 0, st_>>>(cpart_.as<double2>(), cvec_.as<C>(), csplit_, knb, done);
     });
   }
