@@ -155,6 +155,10 @@ void normalize_image(int mode, int H, int W, const double* in, double* out, int 
 }
 
 
+#ifndef DCSC_KC
+#define DCSC_KC 8  // filters per contract_c CTA (v_hat reuse)
+#endif
+
 constexpr int pick_threads(int H, int W) { return H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128); }
 
 // Kernel family per compiled grid: one CTA per plane (Plane), or a 4-CTA
@@ -385,7 +389,7 @@ class Engine final : public EngineBase {
     {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
-      const long base = (long)((NB + TBV - 1) / TBV) * ((K_ + 7) / 8);
+      const long base = (long)((NB + TBV - 1) / TBV) * ((K_ + DCSC_KC - 1) / DCSC_KC);
       const double want = std::max(1.0, 4.0 * sms / (double)base);
       const long p2 = 1L << (int)std::lround(std::log2(want));  // nearest power of two (measured: C4 16 > 17)
       csplit_ = (int)std::max(1L, std::min({p2, 64L, (long)N_}));
@@ -915,7 +919,7 @@ class Engine final : public EngineBase {
 
   // c_k = sum_n conj(z_hat_nk) v_n (split over image chunks, fixed-order reduce)
   void correlate_hat(const C* v, const int* done) {
-    constexpr int KC = 8;
+    constexpr int KC = DCSC_KC;
     const dim3 g1((NB + TBV - 1) / TBV, (K_ + KC - 1) / KC, csplit_);
     launch(kFamContract, [&] {
       contract_c<R, KC><<<g1, TBV, 0, st_>>>(zhat_.as<C>(), v, cpart_.as<double2>(), live_.as<int>(), N_, K_, NB,
