@@ -352,3 +352,16 @@ def test_stateless_learning_ops_fp64_match_reference():
     assert cv_g == cv_r and abs(it_g - it_r) <= 2
     assert rel(g_g, g_r) <= 1e-7  # CG stops at rel. residual 1e-6 (learning.cpp:156)
     assert rel(d_g, ref.d_recover(maps, (5, 5), g_r, mu)) <= 1e-12
+
+
+def test_c4_shaped_run_fp32_matches_reference():
+    """A C4-shaped slice (BASELINE configs[4]: 64x64 FP32, K=32 filters 7x7,
+    p=0.005, sigma=0.05) for 2 outer iterations of run_csc against the oracle on
+    the same FP32-rounded inputs: objectives <= 1e-4, dictionary <= 1e-3."""
+    x, _ = dcsc.synth_generate(12, (64, 64), 32, 7, 0.005, 0.05, 20250917, True)
+    kw = dict(beta=0.5, max_outer=2, normalize=0, seed=20250917, tol=1e-300, max_admm=120, max_mu_iters=10,
+              cg_max=60)
+    r = ref.run(x, 32, (7, 7), ref.Cfg(**kw))
+    g = dcsc.run_csc(x, 32, (7, 7), dcsc.SolverConfig(**kw), precision=32)
+    compare_runs(g, r, FP32_TOL)
+    assert rel(g["dict"], r["dict"]) <= 1e-3
