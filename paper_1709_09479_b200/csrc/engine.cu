@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -373,7 +374,15 @@ int dcsc_cuda_set_comm_nccl(dcsc_cuda_ctx* ctx, int world, int rank, const unsig
   CTX_CHECK
   return guarded([&] {
     if (world < 1 || rank < 0 || rank >= world) throw InvErr("bad world/rank");
-    ctx->eng->set_reducer(world == 1 ? nullptr : std::make_unique<NcclReducer>(world, rank, id, len));
+    const char* f = std::getenv("DCSC_FORCE_MULTI");
+    const bool force = f && f[0] == '1';
+    if (world == 1 && !force) {
+      ctx->eng->set_reducer(nullptr);
+      return;
+    }
+    auto r = std::make_unique<NcclReducer>(world, rank, id, len);
+    r->forced = world == 1;
+    ctx->eng->set_reducer(std::move(r));
   });
 }
 int dcsc_cuda_set_comm_callback(dcsc_cuda_ctx* ctx, int world, int rank, dcsc_allreduce_fn fn, void* user) {

@@ -32,6 +32,9 @@ struct InvErr : std::runtime_error { using std::runtime_error::runtime_error; };
 // tested with host-side (gloo) reductions.
 struct Reducer {
   int world = 1, rank = 0;
+  // DCSC_FORCE_MULTI=1 (tests): a 1-rank communicator still takes the
+  // multi-rank code paths, so the NCCL reducer runs end to end on one GPU
+  bool forced = false;
   virtual ~Reducer() = default;
   virtual void allreduce(double* dev, size_t n, cudaStream_t st) = 0;  // in-place sum
 };
@@ -69,7 +72,7 @@ class EngineBase {
   virtual void event_mark(int slot) = 0;
   virtual double event_elapsed(int a, int b) = 0;
   void set_reducer(std::unique_ptr<Reducer> r) { red_ = std::move(r); }
-  bool multi() const { return red_ && red_->world > 1; }
+  bool multi() const { return red_ && (red_->world > 1 || red_->forced); }
   long long launches = 0;
  protected:
   std::unique_ptr<Reducer> red_;

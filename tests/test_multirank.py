@@ -99,3 +99,42 @@ def test_two_ranks_match_single_rank_joint_channels(tmp_path):
         assert np.all(np.abs(t[:, :3] - single[:, :3]) <= 1e-9 * np.abs(single[:, :3]))
         assert np.array_equal(t[:, 3], single[:, 3]) and np.array_equal(t[:, 5], single[:, 5])
         assert np.abs(r["dict"] - one["dict"]).max() <= 1e-8 * np.abs(one["dict"]).max()
+
+
+@pytest.mark.gpu
+def test_nccl_reducer_one_rank_multi_paths_match_single_rank():
+    """The NCCL reducer end to end on one GPU: a 1-rank communicator with
+    DCSC_FORCE_MULTI=1 takes every multi-rank path (crop-then-all-reduce of the
+    correlations, all-reduced CG scalars and trace sums) through ncclAllReduce;
+    the run must equal the plain single-rank run (FP64)."""
+    import subprocess
+    import sys
+
+    code = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.getcwd())
+from paper_1709_09479_b200 import dcsc
+x, _ = dcsc.synth_generate(3, (20, 20), 5, 5, 0.05, 0.01, 17, False)
+cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=4, tol=1e-300)
+out = {}
+for mode in ("plain", "nccl"):
+    with dcsc.Context(3, (20, 20), 5, (5, 5), cfg, 64) as ctx:
+        if mode == "nccl":
+            ctx.set_comm_nccl(1, 0, dcsc.nccl_unique_id())
+        ctx.set_signals(x)
+        ctx.init_variables()
+        rows, _ = ctx.run(3)
+        out[mode] = ([r["total"] for r in rows], [r["cg_iters"] for r in rows], ctx.get_dictionary().tolist())
+print(json.dumps(out))
+'''
+    env = dict(os.environ, DCSC_FORCE_MULTI="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-3000:]
+    import json
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    (tp, cp, dp), (tn, cn, dn) = out["plain"], out["nccl"]
+    assert cp == cn
+    assert max(abs(a - b) / abs(b) for a, b in zip(tn, tp)) <= 1e-10
+    assert np.abs(np.array(dn) - np.array(dp)).max() <= 1e-9
