@@ -5,6 +5,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/m_c1_ref.json
 for c in c0 c2 c4; do python bench.py --config $c --steps 2 --warmup 2 > gpurun_out/m_${c}.json 2> gpurun_out/m_${c}.err; done
 python bench.py --config c1j3 --steps 3 --warmup 3 > gpurun_out/m_c1j3.json 2> gpurun_out/m_c1j3.err
 python bench.py --config c3s --steps 5 --warmup 3 > gpurun_out/m_c3s.json 2> gpurun_out/m_c3s.err
+python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/m_c3.json 2> gpurun_out/m_c3.err
 python scripts/run_trace.py c2 2 > gpurun_out/m_c2_trace.json 2>/dev/null
 python scripts/run_trace.py c4 2 > gpurun_out/m_c4_trace.json 2>/dev/null
 python scripts/run_trace.py c3 1 > gpurun_out/m_c3_trace.json 2>/dev/null
