@@ -7,12 +7,92 @@
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
 
 #include "dcsc/pipeline.hpp"
 #include "dcsc_cuda.hpp"
 
+// Error behaviour: the reference and the drop-in must throw the same exception
+// type for the same bad input (types.hpp:24-38, pipeline.cpp:66-80,159-167).
+template <class F>
+static const char* thrown(F&& f) {
+  try {
+    f();
+  } catch (const dcsc::DimensionError&) {
+    return "DimensionError";
+  } catch (const dcsc::NumericError&) {
+    return "NumericError";
+  } catch (const std::invalid_argument&) {
+    return "invalid_argument";
+  } catch (const std::exception&) {
+    return "other";
+  }
+  return "none";
+}
+
+static int check_errors() {
+  auto signal = [](int h, int w, double fill) {
+    dcsc::SignalTensor x({h, w}, 1);
+    for (std::size_t i = 0; i < x.values.size(); ++i) x.values[i] = fill + 0.001 * static_cast<double>(i % 7);
+    return x;
+  };
+  dcsc::RunConfig cfg;
+  cfg.filters = 2;
+  cfg.support = {3, 3};
+  cfg.solver.max_outer = 1;
+  struct Case {
+    const char* name;
+    dcsc::Dataset data;
+    dcsc::RunConfig cfg;
+  };
+  std::vector<Case> cases;
+  cases.push_back({"empty dataset", dcsc::Dataset{}, cfg});
+  {
+    dcsc::Dataset d;
+    d.signals = {signal(16, 16, 0.1), signal(20, 20, 0.2)};
+    d.names = {"a", "b"};
+    cases.push_back({"ragged dataset", d, cfg});
+  }
+  {
+    dcsc::Dataset d;
+    d.signals = {signal(16, 16, 0.1)};
+    d.signals[0].values[5] = std::nan("");
+    d.names = {"nan"};
+    cases.push_back({"non-finite signal", d, cfg});
+  }
+  {
+    dcsc::Dataset d;
+    d.signals = {signal(16, 16, 0.1)};
+    d.names = {"a"};
+    dcsc::RunConfig big = cfg;
+    big.support = {17, 3};
+    cases.push_back({"support larger than grid", d, big});
+    dcsc::RunConfig nofilt = cfg;
+    nofilt.filters = 0;
+    cases.push_back({"no filters", d, nofilt});
+    dcsc::RunConfig badbeta = cfg;
+    badbeta.solver.beta = -1.0;
+    cases.push_back({"negative beta", d, badbeta});
+  }
+  bool ok = true;
+  std::printf("{\"errors\": [");
+  for (std::size_t i = 0; i < cases.size(); ++i) {
+    const char* a = thrown([&] { dcsc::run_csc(cases[i].cfg, cases[i].data); });
+    const char* b = thrown([&] { dcsc::cuda::run_csc(cases[i].cfg, cases[i].data); });
+    const bool same = std::string(a) == b && std::string(a) != "none";
+    ok = ok && same;
+    std::printf("%s{\"case\": \"%s\", \"reference\": \"%s\", \"cuda\": \"%s\"}", i ? ", " : "", cases[i].name, a, b);
+  }
+  std::printf("], \"ok\": %s}\n", ok ? "true" : "false");
+  return ok ? 0 : 1;
+}
+
 // usage: dropin_check [outer] [channels]   (channels > 1: Joint mode, TCSC)
+//        dropin_check errors               (exception parity on bad inputs)
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "errors") return check_errors();
   const int N = 3, H = 20, W = 20, K = 6, m = 5, outer = argc > 1 ? std::atoi(argv[1]) : 3;
   const int J = argc > 2 ? std::atoi(argv[2]) : 1;
   dcsc::Dataset data;
