@@ -304,3 +304,32 @@ def test_non_finite_signals_are_a_numeric_error():
     x[0, 3, 4] = np.nan
     with pytest.raises(dcsc.NumericError):
         dcsc.run_csc(x, 2, (3, 3), dcsc.SolverConfig(max_outer=1))
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_full_size_run_properties_and_determinism(name):
+    """One run_csc outer iteration (coding + learning) at the full BASELINE
+    size with capped budgets: the learned dictionary stays in the unit ball,
+    learning does not increase the objective (accept rule, pipeline.cpp:272),
+    and a rerun is bit-identical (fixed-order reductions throughout)."""
+    import bench
+
+    c = bench.CONFIGS[name]
+    x, _ = bench.make_data(c, 0, c["N"])
+    cfg = dcsc.SolverConfig(beta=c["beta"], max_admm=4, max_mu_iters=3, cg_max=20, normalize=0, seed=bench.SEED,
+                            tol=1e-300)
+
+    def once():
+        with dcsc.Context(c["N"], (c["H"], c["W"]), c["K"], (c["m"], c["m"]), cfg, c["prec"]) as ctx:
+            ctx.set_signals(x)
+            ctx.init_variables()
+            rows, _ = ctx.run(1)
+            return rows, ctx.get_dictionary()
+
+    r1, d1 = once()
+    r2, d2 = once()
+    assert [r["total"] for r in r1] == [r["total"] for r in r2]
+    assert np.array_equal(d1, d2)
+    assert len(r1) == 2 and r1[1]["total"] <= r1[0]["total"] * (1 + 1e-6)
+    assert (np.linalg.norm(d1.reshape(c["K"], -1), axis=1) <= 1.0 + 1e-5).all()
+    assert np.isfinite(d1).all()
