@@ -275,7 +275,8 @@ __device__ __forceinline__ C* run_stages(C* a, C* b, const C* tw, RadixList<R, R
 // uniform over the item, so it is taken once per item and every generator
 // load of the item is issued before the first use (with a per-element
 // ternary the compiler serialised one global round trip per element).
-template <class C, int L, int R, int LINES, int T, class COLOF, class GEN, class PACK, class STORE>
+template <class C, int L, int R, int LINES, int T, bool SPLIT = false, class COLOF, class GEN, class PACK,
+          class STORE>
 __device__ __forceinline__ void gen_first_stage_inv(int N0, COLOF&& col_of, GEN&& gen, PACK&& pack,
                                                     STORE&& store) {
   constexpr int J = L / R;
@@ -285,18 +286,36 @@ __device__ __forceinline__ void gen_first_stage_inv(int N0, COLOF&& col_of, GEN&
     const int line = it % LINES, j = it / LINES;
     const int col = col_of(line);
     C x[R];
-    if (col == 0) {
-      C g0[R], gn[R];
+    if constexpr (SPLIT) {
+      // one load batch per branch path (heavy multi-channel generators: the
+      // merged form below costs registers there, c1j3 2.38 -> 2.92 ms)
+      if (col == 0) {
+        C g0[R], gn[R];
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        g0[q] = gen(j + q * J, 0);
-        gn[q] = gen(j + q * J, N0);
+        for (int q = 0; q < R; ++q) {
+          g0[q] = gen(j + q * J, 0);
+          gn[q] = gen(j + q * J, N0);
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = pack(g0[q], gn[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = gen(j + q * J, col);
       }
-#pragma unroll
-      for (int q = 0; q < R; ++q) x[q] = pack(g0[q], gn[q]);
     } else {
+      // every lane issues its item's loads; the column-0 lane (one per warp in
+      // some layouts, e.g. rank 0 of a cluster) adds the partner column's
+      // loads on top, so a warp pays one load round trip, not one per branch
+      // path (c3s 1.268 -> 1.247 ms, C0 0.186 -> 0.180 ms)
 #pragma unroll
       for (int q = 0; q < R; ++q) x[q] = gen(j + q * J, col);
+      if (col == 0) {
+        C gn[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) gn[q] = gen(j + q * J, N0);
+#pragma unroll
+        for (int q = 0; q < R; ++q) x[q] = pack(x[q], gn[q]);
+      }
     }
     dft<R, true>(x);
 #pragma unroll
@@ -518,13 +537,13 @@ struct Plane {
   // generators that read global memory; generators that read only shared
   // memory (the staged coding pass) keep the per-element form, which the
   // compiler predicates (1% faster at 128x128).
-  template <bool HOIST = true, class GEN>
+  template <bool HOIST = true, bool SPLIT = false, class GEN>
   __device__ static __forceinline__ C* cols_inv(C* a, C* b, const C* tw, GEN&& gen) {
     using S = Split<ColPlan>;
     constexpr int R1 = S::first;
     const C* twc = tw + TW_COL;
     if constexpr (HOIST) {
-      gen_first_stage_inv<C, H, R1, M, T>(
+      gen_first_stage_inv<C, H, R1, M, T, SPLIT>(
           M, [](int l) { return l; }, gen, [](C x0, C xn) { return pack_col0(x0, xn); },
           [&](int l, int i, C v) { a[i * Wh + l] = v; });
     } else {

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
       C* cs;
       if constexpr (TC) {
         const int J = JT > 0 ? JT : a.J;
-        cs = P::cols_inv(B0, B1, TW, [&](int r, int c) {
+        cs = P::template cols_inv<true, true>(B0, B1, TW, [&](int r, int c) {
           const int b = r * Wh + c;
           C t = mk<C>(R(0), R(0));
 #pragma unroll

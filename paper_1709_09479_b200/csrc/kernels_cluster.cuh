@@ -19,6 +19,18 @@
 
 namespace dcsc_cuda {
 
+#ifdef DCSC_CL_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CLT(slot) \
+  if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < CL && k >= k0 + 2 && k < k0 + 5) tt[k - k0 - 2][slot] = gtimer();
+#else
+#define CLT(slot)
+#endif
+
 template <class CP>
 struct SmemCl {
   using C = typename CP::C;
@@ -194,7 +206,13 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
   const int k0 = g * a.kpg;
   const int k1 = min(a.K, k0 + a.kpg);
+#ifdef DCSC_CL_TRACE
+  unsigned long long tt[3][8] = {};
+#endif
   for (int k = k0; k < k1; ++k) {
+#ifdef DCSC_CL_TRACE
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < CL && k >= k0 + 2 && k < k0 + 5) tt[k - k0 - 2][6] = gtimer();
+#endif
     const C* __restrict__ dk = a.dhat + (size_t)k * NB;
     if constexpr (ADMM) {
       C* __restrict__ uk = reinterpret_cast<C*>(a.u + ((size_t)n * a.K + k) * D) + (size_t)r0 * M;
@@ -221,9 +239,12 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       }
       fence_async_smem();
       __syncthreads();
+      CLT(0)
       cluster_wait();  // B_F (previous filter): peers' Z free
+      CLT(1)
       cl_issue_exchange<CP>(Y, Z, rank, xbar);
       mbar_wait(xbar, xphase);
+      CLT(2)
       xphase ^= 1u;
       CP::rows_inv_first(Z, Y, rank, X, TW);
       __syncthreads();
@@ -293,9 +314,12 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     CP::rows_fwd_to_send(Z, X, Z, TW);
     fence_async_smem();
     __syncthreads();
+    CLT(3)
     if constexpr (ADMM) cluster_wait();  // B_I: peers' Y free (else covered by the wait at the filter start)
+    CLT(4)
     cl_issue_exchange<CP>(Z, Y, rank, xbar);
     mbar_wait(xbar, xphase);
+    CLT(5)
     xphase ^= 1u;
     CP::cols_fwd_first(Y, Z, X, TW, rank);
     __syncthreads();
@@ -346,6 +370,12 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       accN = cadd(accN, cmul(dMv, xn));
     }
   }
+#ifdef DCSC_CL_TRACE
+  if (ADMM && threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < CL)
+    for (int f = 0; f < 3; ++f)
+      printf("CLT f=%d rank=%u start=%llu ready_I=%llu bf_I=%llu recv_I=%llu ready_F=%llu bi_F=%llu recv_F=%llu\n", f,
+             rank, tt[f][6], tt[f][0], tt[f][1], tt[f][2], tt[f][3], tt[f][4], tt[f][5]);
+#endif
   cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
   {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
