@@ -159,7 +159,12 @@ void normalize_image(int mode, int H, int W, const double* in, double* out, int 
 #define DCSC_KC 8  // filters per contract_c CTA (v_hat reuse)
 #endif
 
-constexpr int pick_threads(int H, int W) { return H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128); }
+#ifndef DCSC_T128
+#define DCSC_T128 512  // threads per CTA of the 128x128 family (experiment knob)
+#endif
+constexpr int pick_threads(int H, int W) {
+  return H * W == 128 * 128 ? DCSC_T128 : (H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128));
+}
 
 // Kernel family per compiled grid: one CTA per plane (Plane), or a 4-CTA
 // cluster per plane (ClusterPlane) when the half spectrum exceeds smem.
