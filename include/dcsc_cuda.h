@@ -32,6 +32,8 @@
  *   dcsc_cuda_learning_correlation  dcsc::LearningOperator::correlation (learning.hpp:59-60)
  *   dcsc_cuda_run                   dcsc::run_csc (pipeline.hpp:58) + trace rows
  *                                   (types.hpp:122-136, trace_io.hpp)
+ *   dcsc_cuda_run_begin / _step     the same run_csc outer loop
+ *                                   (pipeline.cpp:216-299), one iteration per call
  *   dcsc_cuda_dft2_forward/_inverse dcsc::forward_dft / inverse_dft
  *                                   (spectral.hpp:27-38), half-spectrum form
  */
@@ -181,6 +183,17 @@ int dcsc_cuda_learning_data_term(dcsc_cuda_ctx* ctx, const double* d, double* da
 int dcsc_cuda_run(dcsc_cuda_ctx* ctx, int max_outer, dcsc_trace_row* rows, int* n_rows,
                   int* converged);
 
+/* run_csc one outer iteration at a time (the same arithmetic as
+ * dcsc_cuda_run): run_begin = init_variables + the initial objectives
+ * (pipeline.cpp:169-213); each run_step is the next outer iteration
+ * (pipeline.cpp:216-299), rows needs 2 entries (coding, learning);
+ * *converged = 1 when the run's stop test (pipeline.cpp:290-298) is met */
+int dcsc_cuda_run_begin(dcsc_cuda_ctx* ctx);
+int dcsc_cuda_run_step(dcsc_cuda_ctx* ctx, dcsc_trace_row* rows, int* converged);
+/* acceptance decisions of the last run_step: image_accept (this rank's N
+ * images, pipeline.cpp:236), dict_accept (pipeline.cpp:272); either may be NULL */
+int dcsc_cuda_run_accepts(dcsc_cuda_ctx* ctx, int* image_accept, int* dict_accept);
+
 /* standalone half-spectrum DFTs of a batch of H x W real planes:
  * forward writes batch * H * (W/2+1) complex (interleaved re,im) */
 int dcsc_cuda_dft2_forward(int height, int width, int precision, int batch, const double* in,
@@ -199,7 +212,8 @@ int dcsc_cuda_fft_timing(int height, int width, int precision, int batch, int it
  * z_hat read per launch —, 3 learning mask step, 4 other) */
 int dcsc_cuda_kernel_launches(dcsc_cuda_ctx* ctx, long long* count);
 /* per-launch CUDA-event timing on the library stream: 0 off, 1 every launch,
- * 2 coding-pass launches only (cheap enough to leave on in a timed region) */
+ * 2 coding-pass launches only (cheap enough to leave on in a timed region),
+ * 3 coding-pass launches + the learning z_hat streams (families 0 and 2) */
 int dcsc_cuda_set_profiling(dcsc_cuda_ctx* ctx, int enable);
 int dcsc_cuda_kernel_time(dcsc_cuda_ctx* ctx, int family, double* total_ms, long long* launches);
 /* device-event timer on the context stream: mark(slot), elapsed(slot a, slot b) */

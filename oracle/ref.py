@@ -190,23 +190,50 @@ def learning_apply(maps, support, mu, mu_floor, v):
     return out
 
 
-def run(xs, K, support, cfg: Cfg, dump_dicts=True):
-    """Instrumented run_csc replica (oracle/ref_capi.cpp:ref_run)."""
+def run(xs, K, support, cfg: Cfg, dump_dicts=True, want_maps=True):
+    """Instrumented run_csc replica (oracle/ref_capi.cpp:ref_run_ext). Besides the
+    trace and the per-outer dictionaries it returns, per outer iteration, the
+    near-tie counts of the accepted maps' soft-threshold argument (bands
+    1e-7, 1e-6, 1e-5, 1e-4 relative to beta) and the acceptance flags (N image
+    flags, then the dictionary flag)."""
     xs = np.ascontiguousarray(xs, dtype=np.float64)
     N, H, W = xs.shape
     mh, mw = support
     rows = (RefTraceRow * (2 * max(cfg.max_outer, 1)))()
     n_outer = C.c_int(0)
     dict_iter = np.zeros((cfg.max_outer + 1, K, mh, mw)) if dump_dicts else None
-    maps = np.zeros((N, K, H, W))
+    maps = np.zeros((N, K, H, W)) if want_maps else None
     dfin = np.zeros((K, mh, mw))
+    ties = np.zeros((max(cfg.max_outer, 1), 4), dtype=np.int64)
+    acc = np.zeros((max(cfg.max_outer, 1), N + 1), dtype=np.int32)
     c = cfg.c()
-    _check(lib().ref_run(C.byref(c), N, H, W, _p(xs), K, mh, mw, rows, C.byref(n_outer),
-                         _p(dict_iter) if dump_dicts else None, _p(maps), _p(dfin)))
+    _check(lib().ref_run_ext(C.byref(c), N, H, W, _p(xs), K, mh, mw, rows, C.byref(n_outer),
+                             _p(dict_iter) if dump_dicts else None, _p(maps) if want_maps else None, _p(dfin),
+                             ties.ctypes.data_as(C.POINTER(C.c_long)), acc.ctypes.data_as(C.POINTER(C.c_int))))
     trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(2 * n_outer.value)]
     return {"trace": trace, "n_outer": n_outer.value,
             "dicts": dict_iter[: n_outer.value + 1] if dump_dicts else None,
-            "maps": maps, "dict": dfin}
+            "maps": maps, "dict": dfin, "ties": ties[: n_outer.value], "accepts": acc[: n_outer.value]}
+
+
+def set_parallel_objective(on: bool) -> None:
+    """Golden generation only: the replica evaluates per-image objectives in
+    parallel (identical values; the reference itself runs them serially)."""
+    lib().ref_set_parallel_objective(int(on))
+
+
+def synth_generate(n_images, grid, filters, m, p, sigma, seed, round_fp32, first=0):
+    """The seeded BASELINE generator (paper_1709_09479_b200/csrc/synth.cpp, host
+    only) compiled into this library, so the reference arm and the golden
+    scripts never load the CUDA library. Same values as dcsc.synth_generate."""
+    H, W = grid
+    x = np.zeros((n_images, H, W))
+    d = np.zeros((filters, m, m))
+    rc = lib().dcsc_synth_generate_range(first, n_images, H, W, filters, m, C.c_double(p), C.c_double(sigma),
+                                         C.c_uint64(seed), int(round_fp32), _p(x), _p(d))
+    if rc != 0:
+        raise ValueError("synth_generate: bad arguments")
+    return x, d
 
 
 def run_csc(xs, K, support, cfg: Cfg):
@@ -334,7 +361,7 @@ def run_j(xs, K, support, cfg: Cfg, dump_dicts=True):
     dfin = np.zeros((K, J, mh, mw))
     c = cfg.c()
     _check(lib().ref_run_j(C.byref(c), N, H, W, J, _p(xs), K, mh, mw, rows, C.byref(n_outer),
-                           _p(dict_iter) if dump_dicts else None, _p(maps), _p(dfin)))
+                           _p(dict_iter) if dump_dicts else None, _p(maps), _p(dfin), None, None))
     trace = [{f: getattr(rows[i], f) for f, _ in RefTraceRow._fields_} for i in range(2 * n_outer.value)]
     return {"trace": trace, "n_outer": n_outer.value,
             "dicts": dict_iter[: n_outer.value + 1] if dump_dicts else None,
@@ -440,3 +467,13 @@ def d_recover(maps, support, gamma, mu):
                                _p(np.ascontiguousarray(gamma, dtype=np.float64)),
                                _p(np.ascontiguousarray(mu, dtype=np.float64)), _p(out)))
     return out
+
+
+def time_learning(maps, support, n_apply=2):
+    """Wall ms of the reference's LearningOperator build and of one apply (bench.py cpu baseline)."""
+    maps = np.ascontiguousarray(maps, dtype=np.float64)
+    N, K, H, W = maps.shape
+    b, a = C.c_double(), C.c_double()
+    _check(lib().ref_time_learning(N, H, W, K, _p(maps), support[0], support[1], int(n_apply), C.byref(b),
+                                   C.byref(a)))
+    return b.value, a.value

@@ -21,6 +21,7 @@
 #include <omp.h>
 #endif
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -487,6 +488,33 @@ int ref_d_recover(int N, int H, int W, int K, const double* maps, int mh, int mw
   });
 }
 
+// CPU-baseline unit costs of the reference learning step (bench.py): wall ms to
+// build the LearningOperator (learning.cpp:24-64: N*K forward FFTs) and the mean
+// wall ms of one LearningOperator::apply (learning.cpp:83-122) over n_apply calls.
+int ref_time_learning(int N, int H, int W, int K, const double* maps, int mh, int mw, int n_apply,
+                      double* build_ms, double* apply_ms) {
+  return guarded([&] {
+    const std::size_t D = static_cast<std::size_t>(H) * W;
+    std::vector<SparseMaps> zs;
+    for (int n = 0; n < N; ++n) {
+      SparseMaps m(K, {H, W});
+      std::copy(maps + n * K * D, maps + (n + 1) * K * D, m.values.begin());
+      zs.push_back(std::move(m));
+    }
+    const double t0 = now_ms();
+    LearningOperator op(zs, {mh, mw}, 1e-6);
+    const double t1 = now_ms();
+    std::vector<double> mu(K, 1.0), v(N * D, 0.0), out(N * D);
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = std::sin(0.37 * static_cast<double>(i));
+    op.set_mu(std::span<const double>(mu.data(), K));
+    for (int a = 0; a < n_apply; ++a)
+      op.apply(std::span<const double>(v.data(), N * D), std::span<double>(out.data(), N * D));
+    const double t2 = now_ms();
+    *build_ms = t1 - t0;
+    *apply_ms = (t2 - t1) / std::max(n_apply, 1);
+  });
+}
+
 // LearningOperator::correlation (learning.cpp:124-134) for every filter: out K*M.
 int ref_learning_correlation(int N, int H, int W, int K, const double* maps, int mh, int mw, const double* v,
                              double* out) {
@@ -514,9 +542,23 @@ int ref_learning_correlation(int N, int H, int W, int K, const double* maps, int
 // iteration. maps_out (optional) receives the final N*K*D maps, dict_out the
 // final K*M dictionary. Returns the number of outer iterations run in *n_outer.
 // J > 1: Joint channel mode (solve_coding_tcsc), signals N*J*D, dictionary K*J*M.
+//
+// Parity instrumentation (optional, NULL = off): ties_out receives 4 counts per
+// outer iteration — entries of the accepted maps' soft-threshold argument
+// u = theta - z/rho (so z = -rho soft(u, beta), coding.cpp:237-246) with
+// ||u| - beta| <= delta * beta for delta = 1e-7, 1e-6, 1e-5, 1e-4 (the support
+// near-ties); accept_out receives N + 1 flags per outer iteration — the
+// per-image coding acceptances (pipeline.cpp:236) then the dictionary
+// acceptance (pipeline.cpp:272).
+static int g_parallel_objective = 0;  // golden generation only: objective passes over images in parallel
+int ref_set_parallel_objective(int on) {
+  g_parallel_objective = on;
+  return 0;
+}
+
 int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_raw, int K, int mh,
               int mw, ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out,
-              double* dict_out) {
+              double* dict_out, long* ties_out, int* accept_out) {
   return guarded([&] {
     RunConfig cfg;
     cfg.solver = to_cfg(cfgp);
@@ -553,6 +595,19 @@ int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_
     double prev_total = total_objective().total;
     std::vector<ObjectiveBreakdown> image_obj(N);
     for (int n = 0; n < N; ++n) image_obj[n] = evaluate_objective(xs[n], dict, maps[n], beta);
+    // near-tie counts of each image's accepted maps (4 bands), see header
+    std::vector<std::array<long, 4>> ties(N, std::array<long, 4>{0, 0, 0, 0});
+    auto count_ties = [&](const CodingDualState& st) {
+      std::array<long, 4> t{0, 0, 0, 0};
+      const double inv_rho = 1.0 / cfg.solver.rho;
+      const double bands[4] = {1e-7, 1e-6, 1e-5, 1e-4};
+      for (std::size_t i = 0; i < st.theta.size(); ++i) {
+        const double u = st.theta[i] - st.z[i] * inv_rho;
+        const double gap = std::abs(std::abs(u) - beta);
+        for (int b = 0; b < 4; ++b) t[b] += gap <= bands[b] * beta ? 1 : 0;
+      }
+      return t;
+    };
 
     int row = 0;
     for (int outer = 1; outer <= cfg.solver.max_outer; ++outer) {
@@ -567,11 +622,16 @@ int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_
       const double coding_ms = now_ms() - c0;
       long admm_total = 0;
       double z_change_sq = 0.0, z_norm_sq = 0.0;
+      std::vector<ObjectiveBreakdown> cobj(N);
+      if (g_parallel_objective)
+        par::parallel_for(N, [&](std::int64_t n) { cobj[n] = evaluate_objective(xs[n], dict, cand[n], beta); });
       for (int n = 0; n < N; ++n) {
         admm_total += cs[n].admm_iters;
-        const ObjectiveBreakdown c = evaluate_objective(xs[n], dict, cand[n], beta);
+        const ObjectiveBreakdown c = g_parallel_objective ? cobj[n] : evaluate_objective(xs[n], dict, cand[n], beta);
         if (!std::isfinite(c.total)) throw NumericError("non-finite objective (coding)");
+        if (accept_out) accept_out[(size_t)(outer - 1) * (N + 1) + n] = c.total <= image_obj[n].total ? 1 : 0;
         if (c.total <= image_obj[n].total) {
+          if (ties_out && !tcsc) ties[n] = count_ties(vars.coding[n]);
           for (std::size_t i = 0; i < cand[n].values.size(); ++i) {
             const double delta = cand[n].values[i] - maps[n].values[i];
             z_change_sq += delta * delta;
@@ -593,6 +653,12 @@ int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_
       rows[row++] = {outer, 0, after_coding.total, after_coding.data_term, after_coding.l1_term,
                      after_coding.residual_norm, admm_total, 0, 0, coding_ms, wall1 - wall0,
                      count_l0(maps)};
+      if (ties_out)
+        for (int b = 0; b < 4; ++b) {
+          long t = 0;
+          for (int n = 0; n < N; ++n) t += ties[n][b];
+          ties_out[(size_t)(outer - 1) * 4 + b] = t;
+        }
 
       LearningStats ls;
       const double l0 = now_ms();
@@ -604,6 +670,7 @@ int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_
       const double cand_data = learning_data_term(xs, dc, maps);
       if (!std::isfinite(cand_data + after_coding.l1_term))
         throw NumericError("non-finite objective (learning)");
+      if (accept_out) accept_out[(size_t)(outer - 1) * (N + 1) + N] = cand_data <= after_coding.data_term ? 1 : 0;
       if (cand_data <= after_coding.data_term) {
         for (std::size_t i = 0; i < dc.values.size(); ++i) {
           const double delta = dc.values[i] - dict.values[i];
@@ -613,7 +680,10 @@ int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_
         after_learning.data_term = cand_data;
         after_learning.total = cand_data + after_coding.l1_term;
         after_learning.residual_norm = std::sqrt(2.0 * cand_data);
-        for (int n = 0; n < N; ++n) image_obj[n] = evaluate_objective(xs[n], dict, maps[n], beta);
+        if (g_parallel_objective)
+          par::parallel_for(N, [&](std::int64_t n) { image_obj[n] = evaluate_objective(xs[n], dict, maps[n], beta); });
+        else
+          for (int n = 0; n < N; ++n) image_obj[n] = evaluate_objective(xs[n], dict, maps[n], beta);
       }
       for (double v : dict.values) d_norm_sq += v * v;
       const double wall2 = now_ms();
@@ -639,7 +709,15 @@ int ref_run_j(const ref_cfg* cfgp, int N, int H, int W, int J, const double* xs_
 int ref_run(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh,
             int mw, ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out,
             double* dict_out) {
-  return ref_run_j(cfgp, N, H, W, 1, xs_raw, K, mh, mw, rows, n_outer, dict_iter, maps_out, dict_out);
+  return ref_run_j(cfgp, N, H, W, 1, xs_raw, K, mh, mw, rows, n_outer, dict_iter, maps_out, dict_out, nullptr,
+                   nullptr);
+}
+
+int ref_run_ext(const ref_cfg* cfgp, int N, int H, int W, const double* xs_raw, int K, int mh, int mw,
+                ref_trace_row* rows, int* n_outer, double* dict_iter, double* maps_out, double* dict_out,
+                long* ties_out, int* accept_out) {
+  return ref_run_j(cfgp, N, H, W, 1, xs_raw, K, mh, mw, rows, n_outer, dict_iter, maps_out, dict_out, ties_out,
+                   accept_out);
 }
 
 // The reference's CSCT writer/reader (tensor_io.cpp:45-90) and trace CSV

@@ -331,6 +331,22 @@ int dcsc_cuda_run(dcsc_cuda_ctx* ctx, int max_outer, dcsc_trace_row* rows, int* 
   CTX_CHECK
   return guarded([&] { ctx->eng->run(max_outer, rows, n_rows, converged); });
 }
+int dcsc_cuda_run_begin(dcsc_cuda_ctx* ctx) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->run_begin(); });
+}
+int dcsc_cuda_run_step(dcsc_cuda_ctx* ctx, dcsc_trace_row* rows, int* converged) {
+  CTX_CHECK
+  return guarded([&] {
+    if (!rows) throw InvErr("null argument");
+    const int c = ctx->eng->run_step(rows);
+    if (converged) *converged = c;
+  });
+}
+int dcsc_cuda_run_accepts(dcsc_cuda_ctx* ctx, int* image_accept, int* dict_accept) {
+  CTX_CHECK
+  return guarded([&] { ctx->eng->run_accepts(image_accept, dict_accept); });
+}
 int dcsc_cuda_dft2_forward(int height, int width, int precision, int batch, const double* in, double* out) {
   return guarded([&] { dft_dispatch(height, width, precision, false, batch, in, out); });
 }

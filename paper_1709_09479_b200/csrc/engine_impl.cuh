@@ -472,7 +472,7 @@ class Engine final : public EngineBase {
   template <class F>
   void launch(int fam, F&& f) {
     cudaEvent_t a = nullptr, b = nullptr;
-    const bool prof = profiling_ == 1 || (profiling_ == 2 && fam == kFamCoding);
+    const bool prof = profiling_ == 1 || (profiling_ >= 2 && fam == kFamCoding) || (profiling_ == 3 && fam == kFamContract);
     if (prof) {
       a = pooled_event();
       b = pooled_event();
@@ -1408,108 +1408,130 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
   }
 
-  // run_csc (pipeline.cpp:158-301) from init_variables
+  // run_csc (pipeline.cpp:158-301) from init_variables, split into a
+  // begin (init_variables + the initial per-image objectives, :169-213) and
+  // one outer iteration per step (:216-299), so a caller can take the outer
+  // loop one iteration at a time (bench, per-outer parity dumps) without
+  // re-initialising
+  void run_begin() override {
+    init_variables();
+    run_img_.assign(N_, dcsc_objective{});
+    double dsum = 0.0;
+    for (int n = 0; n < N_; ++n) {
+      run_img_[n].data_term = 0.5 * xnorm2_[n];  // maps are zero: reconstruct = 0
+      run_img_[n].l1_term = 0.0;
+      run_img_[n].total = run_img_[n].data_term;
+      run_img_[n].residual_norm = std::sqrt(xnorm2_[n]);
+      dsum += run_img_[n].data_term;
+    }
+    reduce_host(&dsum, 1);
+    run_prev_total_ = dsum;
+    run_outer_ = 0;
+    run_ready_ = true;
+  }
+
+  // one outer iteration; rows[0] = coding row, rows[1] = learning row;
+  // returns 1 when the run's stop test (pipeline.cpp:290-298) is met
+  int run_step(dcsc_trace_row* rows) override {
+    if (!run_ready_) throw InvErr("run_step before run_begin");
+    const int outer = ++run_outer_;
+    std::vector<dcsc_objective>& img = run_img_;
+    std::vector<dcsc_coding_stats> cs(N_);
+    std::vector<int> acc(N_);
+    const double w0 = now_ms();
+    coding(0, N_, cs.data());
+    const double coding_ms = now_ms() - w0;
+    std::vector<double> cdata, cl1;
+    objective_pass<kPassObjective>(dhat_.as<C>(), cdata, cl1);
+    long admm_total = 0;
+    for (int n = 0; n < N_; ++n) {
+      admm_total += cs[n].admm_iters;
+      const double tot = cdata[n] + cl1[n];
+      if (!std::isfinite(tot))
+        throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", coding phase");
+      acc[n] = tot <= img[n].total ? 1 : 0;
+      if (acc[n]) img[n] = {cdata[n], cl1[n], tot, std::sqrt(2.0 * cdata[n])};
+    }
+    double zc2 = 0.0, zn2 = 0.0;
+    long l0 = 0;
+    accept(acc, zc2, zn2, l0);
+    run_acc_ = acc;
+    zhat_valid_ = false;
+    dcsc_objective after{};
+    for (int n = 0; n < N_; ++n) {
+      after.data_term += img[n].data_term;
+      after.l1_term += img[n].l1_term;
+      after.residual_norm += img[n].residual_norm * img[n].residual_norm;
+    }
+    {
+      double s[7] = {after.data_term, after.l1_term, after.residual_norm, (double)admm_total, zc2, zn2, (double)l0};
+      reduce_host(s, 7);
+      after.data_term = s[0];
+      after.l1_term = s[1];
+      after.residual_norm = s[2];
+      admm_total = (long)s[3];
+      zc2 = s[4];
+      zn2 = s[5];
+      l0 = (long)s[6];
+    }
+    after.total = after.data_term + after.l1_term;
+    after.residual_norm = std::sqrt(after.residual_norm);
+    const double w1 = now_ms();
+    rows[0] = {outer, 0, after.total, after.data_term, after.l1_term, after.residual_norm,
+               admm_total, 0, 0, coding_ms, w1 - w0, l0};
+
+    dcsc_learning_stats ls{};
+    std::vector<double> dc((size_t)K_ * J_ * M_);
+    learning(dc.data(), &ls);
+    const double learning_ms = now_ms() - w1;
+    std::vector<double> data;
+    data_terms(dc.data(), data);
+    double cand = 0.0;
+    for (double v : data) cand += v;
+    reduce_host(&cand, 1);
+    if (!std::isfinite(cand + after.l1_term))
+      throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", learning phase");
+    dcsc_objective afterl = after;
+    double dc2 = 0.0, dn2 = 0.0;
+    run_dacc_ = cand <= after.data_term ? 1 : 0;
+    if (cand <= after.data_term) {
+      for (size_t i = 0; i < dc.size(); ++i) {
+        const double dl = dc[i] - dict_[i];
+        dc2 += dl * dl;
+      }
+      set_dictionary(dc.data());
+      afterl.data_term = cand;
+      afterl.total = cand + after.l1_term;
+      afterl.residual_norm = std::sqrt(2.0 * cand);
+      for (int n = 0; n < N_; ++n)
+        img[n] = {data[n], img[n].l1_term, data[n] + img[n].l1_term, std::sqrt(2.0 * data[n])};
+    }
+    for (double v : dict_) dn2 += v * v;
+    const double w2 = now_ms();
+    rows[1] = {outer, 1, afterl.total, afterl.data_term, afterl.l1_term, afterl.residual_norm,
+               0, ls.cg_iters, ls.mu_iters, learning_ms, w2 - w1, l0};
+    const double prev = run_prev_total_;
+    const double obj_change = std::abs(prev - afterl.total) / std::max(std::abs(prev), 1e-30);
+    const double z_change = std::sqrt(zc2) / std::max(std::sqrt(zn2), 1.0);
+    const double d_change = std::sqrt(dc2) / std::max(std::sqrt(dn2), 1.0);
+    run_prev_total_ = afterl.total;
+    return (obj_change <= cfg_.tol && z_change <= cfg_.tol && d_change <= cfg_.tol) ? 1 : 0;
+  }
+
+  // acceptance decisions of the last run_step: per image (pipeline.cpp:236), dictionary (:272)
+  void run_accepts(int* image_accept, int* dict_accept) override {
+    if (image_accept) std::copy(run_acc_.begin(), run_acc_.end(), image_accept);
+    if (dict_accept) *dict_accept = run_dacc_;
+  }
+
   void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) override {
     *n_rows = 0;
     *converged = 0;
-    init_variables();
-    if (max_outer == 0) return;
-    std::vector<dcsc_objective> img(N_);
-    double prev_total = 0.0;
-    {
-      double dsum = 0.0;
-      for (int n = 0; n < N_; ++n) {
-        img[n].data_term = 0.5 * xnorm2_[n];  // maps are zero: reconstruct = 0
-        img[n].l1_term = 0.0;
-        img[n].total = img[n].data_term;
-        img[n].residual_norm = std::sqrt(xnorm2_[n]);
-        dsum += img[n].data_term;
-      }
-      reduce_host(&dsum, 1);
-      prev_total = dsum;
-    }
-    std::vector<dcsc_coding_stats> cs(N_);
-    std::vector<int> acc(N_);
-    int row = 0;
+    run_begin();
     for (int outer = 1; outer <= max_outer; ++outer) {
-      const double w0 = now_ms();
-      coding(0, N_, cs.data());
-      const double coding_ms = now_ms() - w0;
-      std::vector<double> cdata, cl1;
-      objective_pass<kPassObjective>(dhat_.as<C>(), cdata, cl1);
-      long admm_total = 0;
-      for (int n = 0; n < N_; ++n) {
-        admm_total += cs[n].admm_iters;
-        const double tot = cdata[n] + cl1[n];
-        if (!std::isfinite(tot))
-          throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", coding phase");
-        acc[n] = tot <= img[n].total ? 1 : 0;
-        if (acc[n]) img[n] = {cdata[n], cl1[n], tot, std::sqrt(2.0 * cdata[n])};
-      }
-      double zc2 = 0.0, zn2 = 0.0;
-      long l0 = 0;
-      accept(acc, zc2, zn2, l0);
-      zhat_valid_ = false;
-      dcsc_objective after{};
-      for (int n = 0; n < N_; ++n) {
-        after.data_term += img[n].data_term;
-        after.l1_term += img[n].l1_term;
-        after.residual_norm += img[n].residual_norm * img[n].residual_norm;
-      }
-      {
-        double s[6] = {after.data_term, after.l1_term, after.residual_norm, (double)admm_total, zc2, zn2};
-        double l0d = (double)l0;
-        reduce_host(s, 6);
-        reduce_host(&l0d, 1);
-        after.data_term = s[0];
-        after.l1_term = s[1];
-        after.residual_norm = s[2];
-        admm_total = (long)s[3];
-        zc2 = s[4];
-        zn2 = s[5];
-        l0 = (long)l0d;
-      }
-      after.total = after.data_term + after.l1_term;
-      after.residual_norm = std::sqrt(after.residual_norm);
-      const double w1 = now_ms();
-      rows[row++] = {outer, 0, after.total, after.data_term, after.l1_term, after.residual_norm,
-                     admm_total, 0, 0, coding_ms, w1 - w0, l0};
-
-      dcsc_learning_stats ls{};
-      std::vector<double> dc((size_t)K_ * J_ * M_);
-      learning(dc.data(), &ls);
-      const double learning_ms = now_ms() - w1;
-      std::vector<double> data;
-      data_terms(dc.data(), data);
-      double cand = 0.0;
-      for (double v : data) cand += v;
-      reduce_host(&cand, 1);
-      if (!std::isfinite(cand + after.l1_term))
-        throw NumErr("non-finite objective at outer iteration " + std::to_string(outer) + ", learning phase");
-      dcsc_objective afterl = after;
-      double dc2 = 0.0, dn2 = 0.0;
-      if (cand <= after.data_term) {
-        for (size_t i = 0; i < dc.size(); ++i) {
-          const double dl = dc[i] - dict_[i];
-          dc2 += dl * dl;
-        }
-        set_dictionary(dc.data());
-        afterl.data_term = cand;
-        afterl.total = cand + after.l1_term;
-        afterl.residual_norm = std::sqrt(2.0 * cand);
-        for (int n = 0; n < N_; ++n)
-          img[n] = {data[n], img[n].l1_term, data[n] + img[n].l1_term, std::sqrt(2.0 * data[n])};
-      }
-      for (double v : dict_) dn2 += v * v;
-      const double w2 = now_ms();
-      rows[row++] = {outer, 1, afterl.total, afterl.data_term, afterl.l1_term, afterl.residual_norm,
-                     0, ls.cg_iters, ls.mu_iters, learning_ms, w2 - w1, l0};
-      *n_rows = row;
-      const double obj_change = std::abs(prev_total - afterl.total) / std::max(std::abs(prev_total), 1e-30);
-      const double z_change = std::sqrt(zc2) / std::max(std::sqrt(zn2), 1.0);
-      const double d_change = std::sqrt(dc2) / std::max(std::sqrt(dn2), 1.0);
-      prev_total = afterl.total;
-      if (obj_change <= cfg_.tol && z_change <= cfg_.tol && d_change <= cfg_.tol) {
+      const int done = run_step(rows + 2 * (outer - 1));
+      *n_rows = 2 * outer;
+      if (done) {
         *converged = 1;
         break;
       }
@@ -1547,7 +1569,7 @@ class Engine final : public EngineBase {
     CK(cudaStreamSynchronize(st_));
     prof_.clear();
     evused_ = 0;
-    profiling_ = on;  // 1: every launch, 2: coding-pass launches only
+    profiling_ = on;  // 1: every launch, 2: coding-pass launches only, 3: coding pass + z_hat streams
   }
 
   void kernel_time(int fam, double* ms, long long* n) override {
@@ -1605,6 +1627,12 @@ class Engine final : public EngineBase {
   bool dict_zero_ = false, zhat_valid_ = false;
   int profiling_ = 0;
   std::vector<Prof> prof_;
+  std::vector<dcsc_objective> run_img_;  // per-image objectives of the run in progress
+  double run_prev_total_ = 0.0;
+  int run_outer_ = 0;
+  bool run_ready_ = false;
+  std::vector<int> run_acc_;
+  int run_dacc_ = 0;
   std::vector<cudaEvent_t> evpool_;
   size_t evused_ = 0;
   std::vector<cudaEvent_t> marks_;

@@ -66,6 +66,9 @@ class EngineBase {
   virtual void gamma_solve_op(int channel, const double* mu, double* gamma, int* iters, int* converged) = 0;
   virtual void d_recover_op(int channel, const double* gamma, const double* mu, double* out) = 0;
   virtual void run(int max_outer, dcsc_trace_row* rows, int* n_rows, int* converged) = 0;
+  virtual void run_begin() = 0;
+  virtual int run_step(dcsc_trace_row* rows) = 0;
+  virtual void run_accepts(int* image_accept, int* dict_accept) = 0;
   virtual void synchronize() = 0;
   virtual void set_profiling(int on) = 0;
   virtual void kernel_time(int fam, double* ms, long long* n) = 0;

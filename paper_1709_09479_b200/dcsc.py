@@ -139,6 +139,7 @@ EXPORTS = [
     "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing", "dcsc_cuda_reconstruct",
     "dcsc_synth_dataset", "dcsc_synth_generate_range", "dcsc_cuda_learning_correlation",
     "dcsc_cuda_dictionary_adjoint", "dcsc_cuda_lambda_update", "dcsc_cuda_gamma_solve", "dcsc_cuda_d_recover",
+    "dcsc_cuda_run_begin", "dcsc_cuda_run_step", "dcsc_cuda_run_accepts",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -392,6 +393,24 @@ class Context:
         conv = C.c_int()
         _err(lib().dcsc_cuda_run(self._h, max_outer, rows, C.byref(n), C.byref(conv)))
         return [rows[i].asdict() for i in range(n.value)], bool(conv.value)
+
+    def run_begin(self):
+        """run_csc's set-up (pipeline.cpp:169-213): init_variables + initial objectives."""
+        _err(lib().dcsc_cuda_run_begin(self._h))
+
+    def run_step(self):
+        """The next run_csc outer iteration (pipeline.cpp:216-299): (coding row, learning row), converged."""
+        rows = (TraceRow * 2)()
+        conv = C.c_int()
+        _err(lib().dcsc_cuda_run_step(self._h, rows, C.byref(conv)))
+        return [rows[0].asdict(), rows[1].asdict()], bool(conv.value)
+
+    def run_accepts(self):
+        """Acceptance flags of the last run_step: (per-image array, dictionary flag)."""
+        img = np.zeros(self.N, dtype=np.int32)
+        dacc = C.c_int()
+        _err(lib().dcsc_cuda_run_accepts(self._h, img.ctypes.data_as(C.POINTER(C.c_int)), C.byref(dacc)))
+        return img, bool(dacc.value)
 
     # -- multi-rank
     def set_comm_nccl(self, world: int, rank: int, uid: bytes):

@@ -6,7 +6,12 @@ translation units + FFTW3 shim, built by oracle/Makefile) is run on the seeded
 BASELINE.json generator inputs. The GPU tests compare against these files, so
 they need neither the reference sources nor its build on the GPU box.
 
-usage: python tests/golden/make_golden.py [small|c1slice|tcsc|c0|all]
+usage: python tests/golden/make_golden.py [small|c1slice|tcsc|c0|c1|c2|c3|c4|all]
+
+The BASELINE-config fixtures (c1, c2, c3, c4) store only checksums of the
+inputs (the GPU tests regenerate them with the same seeded generator and check
+the checksum) plus, per outer iteration, the trace row, the accepted
+dictionary, the acceptance flags and the near-tie counts of the accepted maps.
 """
 import os
 import sys
@@ -80,6 +85,72 @@ def tcsc_case(name, N, J, grid, K, m, p, sigma, seed, cfg):
     print(f"{name}: {len(r['trace'])} rows in {dt:.1f}s")
 
 
+def x_checksum(x):
+    """Order-sensitive checksum of the generated inputs (float64 sums of x and i*x)."""
+    flat = x.reshape(-1)
+    return np.array([flat.sum(), (flat * np.arange(flat.size, dtype=np.float64)).sum(), float(flat.size)])
+
+
+def run_full(name, N, grid, K, m, p, sigma, seed, fp32, cfg):
+    """A BASELINE config through the instrumented run_csc replica (per-outer dictionaries,
+    near-tie counts, acceptance flags); per-image objective passes run in parallel."""
+    x, _ = ref.synth_generate(N, grid, K, m, p, sigma, seed, fp32)
+    ref.set_threads(0)
+    ref.set_parallel_objective(True)
+    t0 = time.time()
+    r = ref.run(x, K, (m, m), cfg, want_maps=False)
+    dt = time.time() - t0
+    ref.set_parallel_objective(False)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), x_sum=x_checksum(x), trace=trace_array(r["trace"]),
+                        trace_keys=np.array(TRACE_KEYS), dicts=r["dicts"], ties=r["ties"], accepts=r["accepts"],
+                        cfg=np.array([cfg.beta, cfg.rho, cfg.tol, cfg.max_outer, cfg.max_admm, cfg.max_mu_iters,
+                                      cfg.cg_tol, cfg.cg_max, cfg.mu_floor, cfg.seed, cfg.normalize]),
+                        shape=np.array([N, grid[0], grid[1], K, m]), gen=np.array([p, sigma, seed, fp32]),
+                        seconds=np.array([dt]), threads=np.array([os.cpu_count()]))
+    print(f"{name}: {len(r['trace'])} rows in {dt:.1f}s", flush=True)
+
+
+def coding_full(name, N, grid, K, m, p, sigma, seed, fp32, beta, max_admm):
+    """C1: solve_coding of every image (cold start, ground-truth dictionary), one
+    image per host thread; per-image stats, objective, l0, checksums and the
+    near-tie counts of the soft-threshold argument u = theta - z/rho."""
+    from concurrent.futures import ThreadPoolExecutor
+    x, d_true = ref.synth_generate(N, grid, K, m, p, sigma, seed, fp32)
+    cfg = ref.Cfg(beta=beta, max_admm=max_admm, normalize=0)
+    ref.set_threads(1)
+    bands = np.array([1e-7, 1e-6, 1e-5, 1e-4])
+
+    def one(n):
+        z, (th, zz, lam), st = ref.solve_coding(x[n], d_true, cfg)
+        ob = ref.objective(x[n], d_true, z, beta)
+        gap = np.abs(np.abs(th - zz / cfg.rho) - beta)
+        ties = [(gap <= b * beta).sum() for b in bands]
+        return [st["admm_iters"], st["converged"], st["dual_objective"], ob[0], ob[1], ob[2],
+                (np.abs(z) > 1e-12 * np.abs(z).max()).sum(), np.abs(z).sum(), (z * z).sum(), (lam * lam).sum()] + ties
+
+    t0 = time.time()
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        rows = list(ex.map(one, range(N)))
+    dt = time.time() - t0
+    ref.set_threads(0)
+    # the reference's own batched coding (OpenMP over images, pipeline.cpp:221) timed at full size
+    t1 = time.time()
+    ref.coding_batch(x, d_true, cfg)
+    dt_batch = time.time() - t1
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), x_sum=x_checksum(x), d=d_true, rows=np.array(rows),
+                        cols=np.array(["admm_iters", "converged", "dual_objective", "data", "l1", "total", "l0",
+                                       "z_abs_sum", "z_sq_sum", "lam_sq_sum", "ties_1e-7", "ties_1e-6",
+                                       "ties_1e-5", "ties_1e-4"]),
+                        gen=np.array([p, sigma, seed, fp32]), beta=np.array([beta]), max_admm=np.array([max_admm]),
+                        shape=np.array([N, grid[0], grid[1], K, m]), seconds=np.array([dt]),
+                        coding_batch_seconds=np.array([dt_batch]), threads=np.array([os.cpu_count()]))
+    print(f"{name}: {N} images in {dt:.1f}s (reference coding_batch at full size {dt_batch:.1f}s on "
+          f"{os.cpu_count()} threads)", flush=True)
+
+
+SEED = 20250917  # bench.py SEED
+
+
 def main(which):
     if which in ("small", "all"):
         run_case("run_small_fp64", 3, (20, 20), 6, 5, 0.05, 0.01, 7, False,
@@ -95,6 +166,20 @@ def main(which):
         # BASELINE.json configs[0]: N=10 100x100 FP64, K=100 11x11, beta=1.0, 10 outer iterations
         run_case("run_c0_fp64", 10, (100, 100), 100, 11, 0.01, 0.01, 20250917, False,
                  ref.Cfg(beta=1.0, max_outer=10, normalize=0, seed=0, tol=1e-300))
+
+
+    # BASELINE.json configs at full (C1, C2) or subset (C3, C4) size, FP32 inputs
+    if which in ("c4", "all"):  # configs[4] on an N/8 subset at full K, 64x64: 2 outer iterations
+        run_full("run_c4sub_fp32", 256, (64, 64), 32, 7, 0.005, 0.05, SEED, True,
+                 ref.Cfg(beta=0.5, max_outer=2, normalize=0, seed=SEED, tol=1e-300))
+    if which in ("c1", "all"):  # configs[1] at full size: 256 images, 50 ADMM iterations
+        coding_full("coding_c1_fp32", 256, (128, 128), 64, 11, 0.01, 0.01, SEED, True, 0.5, 50)
+    if which in ("c2", "all"):  # configs[2] at full size: 2 of its 20 outer iterations
+        run_full("run_c2_fp32", 100, (100, 100), 100, 11, 0.02, 0.01, SEED, True,
+                 ref.Cfg(beta=0.5, max_outer=2, normalize=0, seed=SEED, tol=1e-300))
+    if which in ("c3", "all"):  # configs[3] on an N/16 subset at full K, 256x256, ADMM capped at 50
+        run_full("run_c3sub_fp32", 32, (256, 256), 128, 11, 0.01, 0.01, SEED, True,
+                 ref.Cfg(beta=0.5, max_outer=1, max_admm=50, normalize=0, seed=SEED, tol=1e-300))
 
 
 if __name__ == "__main__":
