@@ -158,12 +158,15 @@ def spawn_ranks(args) -> int | None:
     return subprocess.call(cmd)
 
 
-def make_data(cfg, n0, n1, gen):
+def make_data(cfg, n0, n1, gen=None):
     """Seeded synthetic signals of the config's shape (images [n0, n1)). `gen` is
     the generator function: dcsc.synth_generate on our arm, ref.synth_generate (the
     same source compiled into the oracle library) on the reference arm. J > 1:
     channel j is the generator's output for seed SEED + j; the dictionary is the
     channel stack of the per-channel ground truths, jointly renormalised."""
+    if gen is None:
+        from paper_1709_09479_b200 import dcsc
+        gen = dcsc.synth_generate
     J = cfg.get("J", 1)
     xs, ds = [], []
     for j in range(J):

@@ -58,16 +58,6 @@ struct DevMem {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-void validate_cfg(const dcsc_solver_config& c) {  // types.cpp:106-114
-  if (!(c.beta > 0)) throw InvErr("beta must be > 0");
-  if (!(c.rho > 0)) throw InvErr("rho must be > 0");
-  if (!(c.tol > 0)) throw InvErr("tol must be > 0");
-  if (!(c.mu_floor > 0)) throw InvErr("mu_floor must be > 0");
-  if (c.max_outer < 0 || c.max_admm < 1 || c.max_mu_iters < 1 || c.cg_max < 1)
-    throw InvErr("iteration caps must be positive");
-  if (!(c.cg_tol > 0)) throw InvErr("cg_tol must be > 0");
-}
-
 void require_finite(const double* v, size_t n, const char* what) {  // types.cpp:26-29
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(v[i])) throw NumErr(std::string(what) + " contains a non-finite value");
@@ -403,7 +393,6 @@ class Engine final : public EngineBase {
         if (v >= 1 && v <= std::min(64, N_)) csplit_ = v;
       }
     }
-    if (const char* e = std::getenv("DCSC_CSPLIT")) csplit_ = std::max(1, std::min(N_, std::atoi(e)));
     cpart_.alloc(sizeof(double2) * (size_t)csplit_ * K_ * NB);
     phat_.alloc(sizeof(C) * (size_t)K_ * NB);
     live_.alloc(sizeof(int) * K_);
@@ -515,6 +504,7 @@ class Engine final : public EngineBase {
     a.dhat_rb = (dhat == dhat_.as<C>() && dhat_rb_.p) ? dhat_rb_.as<C>() : nullptr;
     a.iter = 0;
     a.is_last = 0;
+    a.theta0 = use_theta0_ ? theta0_.as<R>() + (size_t)n_off * K_ * D : nullptr;
     return a;
   }
 
@@ -658,6 +648,7 @@ class Engine final : public EngineBase {
     CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
     CK(cudaMemsetAsync(gam_.p, 0, gam_.bytes, st_));
     u_zero_.assign(N_, 1);
+    t0_pending_.assign(N_, 0);
     mu_.assign(K_, 1.0);
     zhat_valid_ = false;
     CK(cudaStreamSynchronize(st_));
@@ -694,16 +685,60 @@ class Engine final : public EngineBase {
     const size_t cnt = (size_t)(n1 - n0) * K_ * D;
     if (!theta && !z) {  // the reference's empty state (coding.cpp:175-179): device-side reset
       std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
+      if (!t0_pending_.empty()) std::fill(t0_pending_.begin() + n0, t0_pending_.begin() + n1, 0);
       CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * cnt, st_));
       CK(cudaMemsetAsync(lam_.as<R>() + (size_t)n0 * J_ * D, 0, sizeof(R) * (size_t)(n1 - n0) * J_ * D, st_));
       return;
     }
     std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
-    std::vector<R> u(cnt);
-    const double inv_rho = 1.0 / cfg_.rho;
-    for (size_t i = 0; i < cnt; ++i) u[u_index(i)] = R((theta ? theta[i] : 0.0) - (z ? z[i] : 0.0) * inv_rho);
+    std::vector<R> u(cnt), th(cnt);
+    const double inv_rho = 1.0 / cfg_.rho, beta = cfg_.beta;
+    // The single state array u = theta - z/rho reproduces the reference's first
+    // iteration (w = theta + z/rho, theta_old) only when theta = clamp(u), which
+    // holds for every state ADMM produces. Other states (theta outside the box,
+    // z given without theta, a state saved under another beta / rho) keep
+    // theta for the prologue and the first iteration (CodingArgs::theta0).
+    bool consistent = true;
+    for (size_t i = 0; i < cnt; ++i) {
+      const double tv = theta ? theta[i] : 0.0;
+      const double uv = tv - (z ? z[i] : 0.0) * inv_rho;
+      u[u_index(i)] = R(uv);
+      th[u_index(i)] = R(tv);
+      const double cl = std::min(std::max(uv, -beta), beta);
+      if (std::abs(cl - tv) > 1e-12 * std::max({beta, std::abs(tv), std::abs(uv)})) consistent = false;
+    }
     CK(cudaMemcpyAsync(u_.as<R>() + (size_t)n0 * K_ * D, u.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
+    if (!consistent) {
+      if (!theta0_.p) {
+        theta0_.alloc(sizeof(R) * (size_t)N_ * K_ * D);
+        device_bytes += theta0_.bytes;
+      }
+      CK(cudaMemcpyAsync(theta0_.as<R>() + (size_t)n0 * K_ * D, th.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice,
+                         st_));
+    }
+    t0_pending_.resize(N_, 0);
+    std::fill(t0_pending_.begin() + n0, t0_pending_.begin() + n1, consistent ? 0 : 1);
     CK(cudaStreamSynchronize(st_));
+  }
+
+  // theta0 of images [n0, n1) that have no pending theta: clamp(u) (their
+  // states are ADMM-consistent), so one theta0 launch serves a mixed range
+  void theta0_fill_consistent(int n0, int n1) {
+    const size_t KD = (size_t)K_ * D;
+    std::vector<R> u(KD);
+    const R beta = R(cfg_.beta);
+    for (int n = n0; n < n1; ++n) {
+      if (t0_pending_[n]) continue;
+      CK(cudaMemcpyAsync(u.data(), u_.as<R>() + (size_t)n * KD, sizeof(R) * KD, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      for (auto& v : u) v = std::min(std::max(v, -beta), beta);
+      CK(cudaMemcpyAsync(theta0_.as<R>() + (size_t)n * KD, u.data(), sizeof(R) * KD, cudaMemcpyHostToDevice, st_));
+      CK(cudaStreamSynchronize(st_));
+    }
+  }
+  bool theta0_pending(int n0, int n1) const {
+    if (t0_pending_.empty()) return false;
+    return std::any_of(t0_pending_.begin() + n0, t0_pending_.begin() + n1, [](char v) { return v != 0; });
   }
 
   void get_coding_state(int n0, int n1, double* theta, double* z, double* lambda) override {
@@ -715,10 +750,19 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(l.data(), lam_.as<R>() + (size_t)n0 * J_ * D, sizeof(R) * l.size(), cudaMemcpyDeviceToHost,
                        st_));
     CK(cudaStreamSynchronize(st_));
+    std::vector<R> t0;
+    if (theta0_pending(n0, n1)) {
+      t0.resize(cnt);
+      CK(cudaMemcpyAsync(t0.data(), theta0_.as<R>() + (size_t)n0 * K_ * D, sizeof(R) * cnt, cudaMemcpyDeviceToHost,
+                         st_));
+      CK(cudaStreamSynchronize(st_));
+    }
     const R beta = R(cfg_.beta), rho = R(cfg_.rho);
+    const size_t KD = (size_t)K_ * D;
     for (size_t i = 0; i < cnt; ++i) {
       const R uv = u[u_index(i)];
-      const R th = std::min(std::max(uv, -beta), beta);
+      const bool pend = !t0.empty() && t0_pending_[n0 + i / KD];
+      const R th = pend ? t0[u_index(i)] : std::min(std::max(uv, -beta), beta);
       if (theta) theta[i] = th;
       if (z) z[i] = rho * (th - uv);
     }
@@ -734,6 +778,7 @@ class Engine final : public EngineBase {
     if (dict_zero_) {
       // degenerate dictionary: z = theta = 0, lambda = -x (coding.cpp:181-191)
       std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 1);
+      if (!t0_pending_.empty()) std::fill(t0_pending_.begin() + n0, t0_pending_.begin() + n1, 0);
       CK(cudaMemsetAsync(u_.as<R>() + (size_t)n0 * K_ * D, 0, sizeof(R) * (size_t)cnt * K_ * D, st_));
       const size_t JD = (size_t)J_ * D;
       const size_t tot = (size_t)cnt * JD;
@@ -764,6 +809,10 @@ class Engine final : public EngineBase {
     // initial lambda_hat from the warm state (the first assemble_w, coding.cpp:216-229);
     // a zero state has w_hat = 0, so the FFT pass is skipped and part is zeroed
     const bool all_zero = std::all_of(u_zero_.begin() + n0, u_zero_.begin() + n1, [](char v) { return v != 0; });
+    // a warm state that is not ADMM-consistent: theta0 feeds the prologue and iteration 1
+    const bool t0_pending = theta0_pending(n0, n1);
+    if (t0_pending) theta0_fill_consistent(n0, n1);
+    use_theta0_ = t0_pending;
     // multi-channel: lambda_hat from the per-bin J x J solves (tcsc.cpp:68-88)
     auto tc_lam = [&](int kw, bool skip_conv) {
       launch(kFamLambda, [&] {
@@ -790,6 +839,8 @@ class Engine final : public EngineBase {
       coding_launch<kPassPrologue>(dhat_.as<C>(), n0, cnt);  // lambda_hat from the fused epilogue
     }
     std::fill(u_zero_.begin() + n0, u_zero_.begin() + n1, 0);
+    use_theta0_ = false;
+    if (t0_pending) std::fill(t0_pending_.begin() + n0, t0_pending_.begin() + n1, 0);
     auto lam_update = [&](int iter, int last, int prologue) {
       launch(kFamLambda, [&] {
         lambda_update<R><<<lgrid, 256, 0, st_>>>(part_.as<C>() + (size_t)n0 * G_ * NB,
@@ -806,7 +857,9 @@ class Engine final : public EngineBase {
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     int pending = -1;  // iteration whose conv flags are in flight
     for (int it = 1; it <= cfg_.max_admm; ++it) {
+      use_theta0_ = t0_pending && it == 1;
       coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
+      use_theta0_ = false;
       if (J_ > 1 && it < cfg_.max_admm) tc_lam(K_, true);
       if (pending >= 0) {
         // one-iteration look-ahead: iteration `it` is queued before we wait on it-1
@@ -1616,7 +1669,9 @@ class Engine final : public EngineBase {
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
-      partial_, partial2_, l0_, zhat_, cpart_, hred_, ginv_, what_, cgcnt_, dhat_rb_;
+      partial_, partial2_, l0_, zhat_, cpart_, hred_, ginv_, what_, cgcnt_, dhat_rb_, theta0_;
+  std::vector<char> t0_pending_;  // per image: theta0_ holds a not ADMM-consistent warm theta
+  bool use_theta0_ = false;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
   C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel

@@ -56,6 +56,10 @@ struct CodingArgs {
   // (cl_rank_block), so a rank's generator slice is one contiguous TMA copy;
   // nullptr: the generator reads d_hat from L2
   const cx<R>* dhat_rb;
+  // warm state whose theta is not clamp(theta - z/rho) (set_coding_state of a
+  // state not produced by ADMM): theta (u layout) for the prologue's
+  // w = theta + z/rho and the first iteration's theta_old; nullptr otherwise
+  const R* theta0;
 };
 
 // Bulk prefetch of a contiguous global range into L2 (sm_90+ TMA engine op).
@@ -223,6 +227,8 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     C* work;
     if constexpr (MODE == kPassAdmm) {
       C* __restrict__ uk = reinterpret_cast<C*>(a.u + ((size_t)n * a.K + k) * D);  // pixel pairs
+      const C* __restrict__ t0k =
+          a.theta0 ? reinterpret_cast<const C*>(a.theta0 + ((size_t)n * a.K + k) * D) : nullptr;
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if constexpr (STAGE) {
         // TMA: this filter's u rows -> U (padded rows); lands during the inverse FFT
@@ -286,11 +292,14 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
             const C uv = STAGE ? *up : __ldcs(up);  // u streams through once: evict-first
             const R tv[2] = {x[s].x * invD, x[s].y * invD};
             const R uo[2] = {uv.x, uv.y};
+            C t0v = mk<C>(R(0), R(0));
+            if (t0k) t0v = __ldg(t0k + (j + s * J) * H + r);
+            const R t0[2] = {t0v.x, t0v.y};
             R wv[2], un2[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const R t = tv[e];
-              const R th_o = fmin(fmax(uo[e], -beta), beta);
+              const R th_o = t0k ? t0[e] : fmin(fmax(uo[e], -beta), beta);
               const R un = t - (th_o - uo[e]);           // u' = t - z/rho
               const R th = fmin(fmax(un, -beta), beta);  // theta' = clamp(u')
               const R ez = th - un;                      // z' / rho
@@ -357,14 +366,19 @@ __global__ void __launch_bounds__(P::T) coding_pass(CodingArgs<typename P::R> a)
     } else {
       const C* __restrict__ src = reinterpret_cast<const C*>(
           (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D);
+      const C* __restrict__ t0k =
+          (MODE == kPassPrologue && a.theta0) ? reinterpret_cast<const C*>(a.theta0 + ((size_t)n * a.K + k) * D)
+                                              : nullptr;
       for (int it = threadIdx.x; it < H * M; it += T) {
         const int r = it / M, m = it % M;
         // maps are row-major [r][c]; u is column-major pairs [m][r]
         const C v = (MODE == kPassMaps) ? src[it] : src[m * H + r];
         R w0, w1;
         if constexpr (MODE == kPassPrologue) {
-          w0 = R(2) * fmin(fmax(v.x, -beta), beta) - v.x;
-          w1 = R(2) * fmin(fmax(v.y, -beta), beta) - v.y;
+          // w = theta + z/rho = 2 theta - u (theta = clamp(u) for an ADMM-produced state)
+          const C th = t0k ? t0k[m * H + r] : mk<C>(fmin(fmax(v.x, -beta), beta), fmin(fmax(v.y, -beta), beta));
+          w0 = R(2) * th.x - v.x;
+          w1 = R(2) * th.y - v.y;
         } else if constexpr (MODE == kPassObjective) {
           w0 = rho * (fmin(fmax(v.x, -beta), beta) - v.x);
           w1 = rho * (fmin(fmax(v.y, -beta), beta) - v.y);

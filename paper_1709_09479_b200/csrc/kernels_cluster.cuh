@@ -216,6 +216,8 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     const C* __restrict__ dk = a.dhat + (size_t)k * NB;
     if constexpr (ADMM) {
       C* __restrict__ uk = reinterpret_cast<C*>(a.u + ((size_t)n * a.K + k) * D) + (size_t)r0 * M;
+      const C* __restrict__ t0k =
+          a.theta0 ? reinterpret_cast<const C*>(a.theta0 + ((size_t)n * a.K + k) * D) + (size_t)r0 * M : nullptr;
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if (threadIdx.x == 0) {
         prefetch_l2_bulk(uk, sizeof(C) * ROWS * M);
@@ -258,11 +260,14 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         const C v = Z[rl * Wh + m];
         const R tv[2] = {v.x * invD, v.y * invD};
         const R uo[2] = {uv.x, uv.y};
+        C t0v = mk<C>(R(0), R(0));
+        if (t0k) t0v = __ldg(t0k + it);
+        const R t0[2] = {t0v.x, t0v.y};
         R wv[2], un2[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const R t = tv[e];
-          const R th_o = fmin(fmax(uo[e], -beta), beta);
+          const R th_o = t0k ? t0[e] : fmin(fmax(uo[e], -beta), beta);
           const R un = t - (th_o - uo[e]);
           const R th = fmin(fmax(un, -beta), beta);
           const R zn = rho * (th - un);
@@ -289,14 +294,19 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       const C* __restrict__ src = reinterpret_cast<const C*>(
           (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D) +
           (size_t)r0 * M;
+      const C* __restrict__ t0k = (MODE == kPassPrologue && a.theta0)
+                                      ? reinterpret_cast<const C*>(a.theta0 + ((size_t)n * a.K + k) * D) + (size_t)r0 * M
+                                      : nullptr;
       cluster_wait();  // B_F (previous filter): my Z no longer read by peers' copies
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
         const int rl = it / M, m = it % M;
         const C v = src[it];
         R w0, w1;
         if constexpr (MODE == kPassPrologue) {
-          w0 = R(2) * fmin(fmax(v.x, -beta), beta) - v.x;
-          w1 = R(2) * fmin(fmax(v.y, -beta), beta) - v.y;
+          // w = theta + z/rho = 2 theta - u (theta = clamp(u) for an ADMM-produced state)
+          const C th = t0k ? t0k[it] : mk<C>(fmin(fmax(v.x, -beta), beta), fmin(fmax(v.y, -beta), beta));
+          w0 = R(2) * th.x - v.x;
+          w1 = R(2) * th.y - v.y;
         } else if constexpr (MODE == kPassObjective) {
           w0 = rho * (fmin(fmax(v.x, -beta), beta) - v.x);
           w1 = rho * (fmin(fmax(v.y, -beta), beta) - v.y);

@@ -1,0 +1,143 @@
+"""The BASELINE.json configs against the reference, per outer iteration.
+
+Fixtures (tests/golden/, written by tests/golden/make_golden.py from the
+reference solver itself, oracle/_ref) at full size (C1, C2) or on an image
+subset at full K and grid (C3: N/16 with ADMM capped at 50; C4: N/8). The
+inputs are regenerated here by the same seeded generator and checked against
+the fixture's checksum.
+
+North-star bar (BASELINE.json), asserted at EVERY outer iteration:
+* objective total, data and l1 terms within FP32_TOL = 1e-4 relative;
+* the accepted dictionary within FP32_TOL, element-wise relative to max |d|;
+* ||z||_0 equal modulo near-ties: |l0_gpu - l0_ref| <= the number of the
+  reference's accepted-map entries whose soft-threshold argument u satisfies
+  ||u| - beta| <= TIE_BAND * beta (the band the FP32 state tolerance allows);
+* the discrete decisions equal: ADMM iteration totals, mu iterations, CG
+  iterations, per-image coding acceptances and the dictionary acceptance
+  (pipeline.cpp:232-247, 272; learning.cpp:304-327; coding.cpp:273-283).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1709_09479_b200 import dcsc
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+FP32_TOL = 1e-4
+TIE_BAND_IDX = 2  # ties_out bands: 1e-7, 1e-6, 1e-5, 1e-4 -> 1e-5
+
+
+def load(name):
+    path = os.path.join(GOLD, name + ".npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {name} not generated")
+    return np.load(path)
+
+
+def x_checksum(x):
+    flat = x.reshape(-1)
+    return np.array([flat.sum(), (flat * np.arange(flat.size, dtype=np.float64)).sum(), float(flat.size)])
+
+
+def cfg_of(g):
+    c = g["cfg"]
+    return dcsc.SolverConfig(beta=float(c[0]), rho=float(c[1]), tol=float(c[2]), max_outer=int(c[3]),
+                             max_admm=int(c[4]), max_mu_iters=int(c[5]), cg_tol=float(c[6]), cg_max=int(c[7]),
+                             mu_floor=float(c[8]), seed=int(c[9]), normalize=int(c[10]))
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+def check_run(name):
+    g = load(name)
+    N, H, W, K, m = (int(v) for v in g["shape"])
+    p, sigma, seed, fp32 = g["gen"]
+    x, _ = dcsc.synth_generate(N, (H, W), K, m, float(p), float(sigma), int(seed), bool(fp32))
+    assert np.array_equal(x_checksum(x), g["x_sum"]), "generator drifted from the fixture"
+    cfg = cfg_of(g)
+    keys = list(g["trace_keys"])
+    col = {k: keys.index(k) for k in keys}
+    report = []
+    with dcsc.Context(N, (H, W), K, (m, m), cfg, 32) as ctx:
+        ctx.set_signals(x)
+        ctx.run_begin()
+        for o in range(cfg.max_outer):
+            rows, _ = ctx.run_step()
+            img_acc, d_acc = ctx.run_accepts()
+            d = ctx.get_dictionary()
+            for phase in (0, 1):
+                gr = g["trace"][2 * o + phase]
+                r = rows[phase]
+                assert r["outer_iter"] == o + 1 and r["phase"] == phase
+                for k in ("total", "data_term", "l1_term"):
+                    err = abs(r[k] - gr[col[k]]) / abs(gr[col[k]])
+                    assert err <= FP32_TOL, (name, o + 1, phase, k, r[k], gr[col[k]])
+                    report.append(err)
+            # discrete decisions
+            assert rows[0]["admm_iters"] == int(g["trace"][2 * o][col["admm_iters"]]), (name, o + 1, "admm")
+            assert rows[1]["mu_iters"] == int(g["trace"][2 * o + 1][col["mu_iters"]]), (name, o + 1, "mu")
+            assert rows[1]["cg_iters"] == int(g["trace"][2 * o + 1][col["cg_iters"]]), (name, o + 1, "cg")
+            acc = g["accepts"][o]
+            assert np.array_equal(img_acc, acc[:N]), (name, o + 1, "image acceptances")
+            assert d_acc == bool(acc[N]), (name, o + 1, "dictionary acceptance")
+            # l0 modulo near-ties of the soft threshold
+            l0_ref = int(g["trace"][2 * o][col["l0"]])
+            ties = int(g["ties"][o][TIE_BAND_IDX])
+            assert abs(rows[0]["l0"] - l0_ref) <= ties, (name, o + 1, rows[0]["l0"], l0_ref, ties)
+            # the accepted dictionary after this outer iteration
+            derr = rel(d, g["dicts"][o + 1])
+            assert derr <= FP32_TOL, (name, o + 1, "dictionary", derr)
+    return max(report)
+
+
+def test_c4_subset_per_outer():
+    """configs[4] on an N/8 subset (256 images 64x64, K=32 7x7), 2 outer iterations."""
+    check_run("run_c4sub_fp32")
+
+
+def test_c2_full_per_outer():
+    """configs[2] at full size (100 images 100x100, K=100 11x11), 2 of its 20 outer iterations."""
+    check_run("run_c2_fp32")
+
+
+def test_c3_subset_per_outer():
+    """configs[3] on an N/16 subset (32 images 256x256, K=128 11x11; ADMM capped at 50): the
+    4-CTA cluster family, 1 outer iteration."""
+    check_run("run_c3sub_fp32")
+
+
+def test_c1_full_coding():
+    """configs[1] at full size: 256 images 128x128, K=64, 50 ADMM iterations from a cold start with the
+    ground-truth dictionary; per image: iteration count, dual objective, objective, l0 modulo ties,
+    map and dual-variable checksums."""
+    g = load("coding_c1_fp32")
+    N, H, W, K, m = (int(v) for v in g["shape"])
+    p, sigma, seed, fp32 = g["gen"]
+    x, d_true = dcsc.synth_generate(N, (H, W), K, m, float(p), float(sigma), int(seed), bool(fp32))
+    assert np.array_equal(x_checksum(x), g["x_sum"])
+    assert np.array_equal(d_true, g["d"])
+    beta, max_admm = float(g["beta"][0]), int(g["max_admm"][0])
+    cols = list(g["cols"])
+    c = {k: cols.index(k) for k in cols}
+    with dcsc.Context(N, (H, W), K, (m, m), dcsc.SolverConfig(beta=beta, max_admm=max_admm, normalize=0), 32) as ctx:
+        ctx.set_signals(x)
+        ctx.set_dictionary(d_true)
+        st = ctx.coding()
+        _, z, lam = ctx.get_coding_state()
+        ctx.set_maps(z)
+        ob = ctx.objective()
+    for n in range(N):
+        row = g["rows"][n]
+        assert st[n]["admm_iters"] == int(row[c["admm_iters"]]), n
+        assert bool(st[n]["converged"]) == bool(row[c["converged"]]), n
+        for key, val in (("dual_objective", st[n]["dual_objective"]), ("total", ob[n][2]), ("data", ob[n][0]),
+                         ("l1", ob[n][1]), ("z_abs_sum", np.abs(z[n]).sum()), ("z_sq_sum", (z[n] ** 2).sum()),
+                         ("lam_sq_sum", (lam[n] ** 2).sum())):
+            ref_v = row[c[key]]
+            assert abs(val - ref_v) <= FP32_TOL * abs(ref_v), (n, key, val, ref_v)
+        l0 = int((z[n] != 0).sum())
+        assert abs(l0 - int(row[c["l0"]])) <= int(row[c["ties_1e-5"]]), (n, l0, row[c["l0"]])
