@@ -203,11 +203,17 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   C acc0 = mk<C>(R(0), R(0)), accN = mk<C>(R(0), R(0));
 
   const R rho = a.rho, beta = a.beta, invD = R(1) / R(D);
+  // non-ADMM passes: the l1 sum in s0; ADMM: the seven stop-test sums are
+  // reduced per filter over each warp (FP32 shuffles over 32 lanes x 32 terms)
+  // and accumulated in FP64 per warp in shared memory, so no FP64 running sums
+  // occupy registers across the filter loop (they spilled)
   double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
+  __shared__ double wsum[T / 32][8];
+  if (ADMM && threadIdx.x < (T / 32) * 8) (&wsum[0][0])[threadIdx.x] = 0.0;
   const int k0 = g * a.kpg;
   const int k1 = min(a.K, k0 + a.kpg);
 #ifdef DCSC_CL_TRACE
-  unsigned long long tt[3][8] = {};
+  unsigned long long tt[3][12] = {};
 #endif
   for (int k = k0; k < k1; ++k) {
 #ifdef DCSC_CL_TRACE
@@ -250,8 +256,10 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       xphase ^= 1u;
       CP::rows_inv_first(Z, Y, rank, X, TW);
       __syncthreads();
+      CLT(7)
       cluster_arrive();  // B_I: my Z consumed, my incoming blocks complete
       CP::rows_inv_rest(X, Z, TW);
+      CLT(8)
       R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
 #pragma unroll kClProxUnroll
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
@@ -287,9 +295,23 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         __stcs(uk + it, mk<C>(un2[0], un2[1]));
         Z[rl * Wh + m] = mk<C>(wv[0], wv[1]);
       }
-      s0 += (double)f0; s1 += (double)f1; s2 += (double)f2; s3 += (double)f3;
-      s4 += (double)f4; s5 += (double)f5; s6 = fmax(s6, (double)f6);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        f0 += __shfl_xor_sync(0xffffffffu, f0, o);
+        f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+        f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+        f3 += __shfl_xor_sync(0xffffffffu, f3, o);
+        f4 += __shfl_xor_sync(0xffffffffu, f4, o);
+        f5 += __shfl_xor_sync(0xffffffffu, f5, o);
+        f6 = fmax(f6, __shfl_xor_sync(0xffffffffu, f6, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        double* ws = wsum[threadIdx.x >> 5];
+        ws[0] += (double)f0; ws[1] += (double)f1; ws[2] += (double)f2; ws[3] += (double)f3;
+        ws[4] += (double)f4; ws[5] += (double)f5; ws[6] = fmax(ws[6], (double)f6);
+      }
       __syncthreads();
+      CLT(9)
     } else {
       const C* __restrict__ src = reinterpret_cast<const C*>(
           (MODE == kPassMaps) ? a.maps + ((size_t)n * a.K + k) * D : a.u + ((size_t)n * a.K + k) * D) +
@@ -333,6 +355,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     xphase ^= 1u;
     CP::cols_fwd_first(Y, Z, X, TW, rank);
     __syncthreads();
+    CLT(10)
     cluster_arrive();  // B_F: my Y consumed, my incoming blocks complete
     if (DST && threadIdx.x == 0 && k + 1 < k1) {  // next filter's d_hat slice -> Y
       fence_async_smem();
@@ -371,6 +394,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         }
       }
       __syncthreads();
+      CLT(11)
     }
     if (rank == 0 && threadIdx.x < H) {
       const int r = threadIdx.x;
@@ -383,8 +407,9 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
 #ifdef DCSC_CL_TRACE
   if (ADMM && threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < CL)
     for (int f = 0; f < 3; ++f)
-      printf("CLT f=%d rank=%u start=%llu ready_I=%llu bf_I=%llu recv_I=%llu ready_F=%llu bi_F=%llu recv_F=%llu\n", f,
-             rank, tt[f][6], tt[f][0], tt[f][1], tt[f][2], tt[f][3], tt[f][4], tt[f][5]);
+      printf("CLT f=%d rank=%u start=%llu ready_I=%llu bf_I=%llu recv_I=%llu rif=%llu rir=%llu prox=%llu "
+             "ready_F=%llu bi_F=%llu recv_F=%llu cff=%llu last=%llu\n", f, rank, tt[f][6], tt[f][0], tt[f][1],
+             tt[f][2], tt[f][7], tt[f][8], tt[f][9], tt[f][3], tt[f][4], tt[f][5], tt[f][10], tt[f][11]);
 #endif
   cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
   {
@@ -401,6 +426,13 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     if (rank == 0 && threadIdx.x < H) {
       dst[threadIdx.x * Wh] = acc0;
       dst[threadIdx.x * Wh + M] = accN;
+    }
+  }
+  if constexpr (ADMM) {
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      const double* ws = wsum[threadIdx.x >> 5];
+      s0 = ws[0]; s1 = ws[1]; s2 = ws[2]; s3 = ws[3]; s4 = ws[4]; s5 = ws[5]; s6 = ws[6];
     }
   }
   double v[7] = {s0, s1, s2, s3, s4, s5, 0.0};
