@@ -279,9 +279,10 @@ def ref_outer_seconds(cfg, uc, n_img, counts):
     work counts: coding (admm_total image-iterations + per-image set-up, packed
     over the OpenMP threads as measured), 3 objective passes per image
     (pipeline.cpp:234, 269-270 learning_data_term, 282), learning (operator
-    build + (cg_iters + mu_iters) applies + mu_iters d_recover at ~half an apply)."""
+    build + (cg_iters + mu_iters) applies + mu_iters d_recover at ~half an apply).
+    Coding-only configs (C1) time solve_coding of every image and nothing else."""
     code = counts["admm_total"] * uc["coding_iter_s"] + n_img * uc["coding_setup_s"]
-    obj = 3 * n_img * uc["objective_s"]
+    obj = 0.0 if cfg["coding_only"] else 3 * n_img * uc["objective_s"]
     learn = 0.0
     if not cfg["coding_only"]:
         apply_s = uc["apply_s_fixed"] + uc["apply_s_per_image"] * n_img
