@@ -106,15 +106,40 @@ struct ClusterPlane {
   // gen(r, col) returns natural bin (r, col), col in [0, M]. Returns the
   // column-pass result buffer (a or b), layout [H][CS].
   template <class GEN>
-  __device__ static __forceinline__ C* cols_inv(C* a, C* b, const C* tw, unsigned rank, GEN&& gen) {
+  __device__ static __forceinline__ void cols_inv_gen(C* a, unsigned rank, GEN&& gen) {
     using S = Split<ColPlan>;
-    constexpr int R1 = S::first;
-    const C* twc = tw + TW_COL;
-    gen_first_stage_inv<C, H, R1, COLS, T>(
+    gen_first_stage_inv<C, H, S::first, COLS, T>(
         M, [&](int cl) { return col_of(rank, cl); }, gen, [](C x0, C xn) { return pack_col0(x0, xn); },
         [&](int l, int i, C v) { a[i * CS + l] = v; });
     __syncthreads();
-    return run_stages<C, H, true, COLS, CS, 1, T, R1>(a, b, twc, typename S::tail{});
+  }
+  // generator whose packed column 0 is produced by gen(r, 0) itself (no
+  // partner column loads): every lane issues the same loads
+  template <class GEN>
+  __device__ static __forceinline__ void cols_inv_gen_prepacked(C* a, unsigned rank, GEN&& gen) {
+    using S = Split<ColPlan>;
+    constexpr int R = S::first, J = H / R, ITEMS = COLS * J;
+#pragma unroll 1
+    for (int it = threadIdx.x; it < ITEMS; it += T) {
+      const int line = it % COLS, j = it / COLS;
+      const int col = col_of(rank, line);
+      C x[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[q] = gen(j + q * J, col);
+      dft<R, true>(x);
+#pragma unroll
+      for (int s = 0; s < R; ++s) a[(j * R + s) * CS + line] = x[s];
+    }
+    __syncthreads();
+  }
+  __device__ static __forceinline__ C* cols_inv_rest(C* a, C* b, const C* tw) {
+    using S = Split<ColPlan>;
+    return run_stages<C, H, true, COLS, CS, 1, T, S::first>(a, b, tw + TW_COL, typename S::tail{});
+  }
+  template <class GEN>
+  __device__ static __forceinline__ C* cols_inv(C* a, C* b, const C* tw, unsigned rank, GEN&& gen) {
+    cols_inv_gen(a, rank, gen);
+    return cols_inv_rest(a, b, tw);
   }
 
   __device__ static __forceinline__ C pre_pair(C xk, C xm, C w) {  // w = W_W^k

@@ -38,7 +38,10 @@ struct SmemCl {
   static constexpr size_t tw_off = bufs;
   static constexpr size_t col0_off = tw_off + sizeof(C) * CP::TW_LEN;
   static constexpr size_t plain = col0_off + sizeof(C) * CP::H;
-  static constexpr size_t coding = plain;
+  // coding pass: lambda_hat columns 0 and W/2 of the CTA's image (rank 0
+  // pre-packs its generator column from them) and a column of ones
+  static constexpr size_t lamc_off = plain;
+  static constexpr size_t coding = lamc_off + 2 * sizeof(C) * CP::H;
 };
 
 // The split cluster barriers only guard buffer reuse (write-after-read): all
@@ -142,6 +145,9 @@ __global__ void cl_rank_block(const cx<typename CP::R>* __restrict__ dhat, cx<ty
   }
 }
 
+#ifndef DCSC_CL_PV_RB
+#define DCSC_CL_PV_RB 0  // last-stage d_hat from the rank-blocked slice (A/B: 1.313 vs 1.219 ms per c3s launch, off)
+#endif
 #ifndef DCSC_CL_PROX_UNROLL
 #define DCSC_CL_PROX_UNROLL 16
 #endif
@@ -187,6 +193,15 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   unsigned dphase = 0;
   const bool DST = ADMM && a.dhat_rb != nullptr;
   const int k0s = (int)(blockIdx.x / CL) * a.kpg;
+  // rank 0's packed generator column P(r) = t(r, 0) + i t(r, W/2), t = conj(d) lambda:
+  // one warp pre-packs conj(P) into the staged d_hat slot 0 per filter, and the
+  // generator multiplies it by a lambda of ones, so no lane issues partner loads
+  C* LAMC = reinterpret_cast<C*>(smem_raw + SM::lamc_off);
+  if (DST && rank == 0 && threadIdx.x < H) {
+    const C* lamn = a.lamhat + (size_t)n * NB;
+    LAMC[threadIdx.x] = lamn[threadIdx.x * Wh];
+    LAMC[H + threadIdx.x] = lamn[threadIdx.x * Wh + M];
+  }
   if (DST && threadIdx.x == 0) mbar_init(dbar, 1);
   cl_init_exchange<CP>(xbar);  // (fences the mbarrier inits, syncs the CTA)
   if (DST && threadIdx.x == 0 && k0s < a.K) {
@@ -213,7 +228,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   const int k0 = g * a.kpg;
   const int k1 = min(a.K, k0 + a.kpg);
 #ifdef DCSC_CL_TRACE
-  unsigned long long tt[3][12] = {};
+  unsigned long long tt[3][14] = {};
 #endif
   for (int k = k0; k < k1; ++k) {
 #ifdef DCSC_CL_TRACE
@@ -227,18 +242,32 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if (threadIdx.x == 0) {
         prefetch_l2_bulk(uk, sizeof(C) * ROWS * M);
-        if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
+        if (!(DST && DCSC_CL_PV_RB) && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       }
       if (DST) {
         mbar_wait(dbar, dphase);
         dphase ^= 1u;
-        CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
+        CLT(12)
+        if (rank == 0) {
+          if (threadIdx.x < 32) {
+            for (int r = threadIdx.x; r < H; r += 32) {
+              const C p0 = cmulc(Y[r * CS], LAMC[r]), pm = cmulc(Y[r * CS + COLS], LAMC[H + r]);
+              Y[r * CS] = cconj(CP::pack_col0(p0, pm));
+            }
+          }
+          __syncthreads();
+        }
+        const C one = mk<C>(R(1), R(0));
+        CP::cols_inv_gen_prepacked(X, rank, [&](int r, int c) {
           unsigned cr;
           int cl;
           CP::owner_of(c, cr, cl);
-          const int slot = c == M ? COLS : cl;
-          return cmulc(Y[r * CS + slot], __ldg(lam + r * Wh + c));
+          // c = 0 (rank 0): slot 0 holds conj(P) and multiplies 1
+          const C lv = c == 0 ? one : __ldg(lam + r * Wh + c);
+          return cmulc(Y[r * CS + cl], lv);
         });
+        CLT(13)
+        CP::cols_inv_rest(X, Y, TW);
       } else {
         CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
           const int b = r * Wh + c;
@@ -364,10 +393,14 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     }
     // column-0 epilogue operands (rank 0) fetched with the last stage's loads,
     // so rank 0 does not trail its peers by an L2 round trip every filter
+    // ADMM: the last stage's d_hat operands come from this rank's contiguous
+    // slice of the rank-blocked copy (L2-hot: TMA'd for this filter's generator)
+    const bool PVRB = DST && DCSC_CL_PV_RB;
+    const C* __restrict__ dsl = PVRB ? a.dhat_rb + ((size_t)k * CL + rank) * BS : nullptr;
     C d0 = mk<C>(R(0), R(0)), dMv = mk<C>(R(0), R(0));
     if (rank == 0 && threadIdx.x < H) {
-      d0 = __ldg(dk + threadIdx.x * Wh);
-      dMv = __ldg(dk + threadIdx.x * Wh + M);
+      d0 = PVRB ? __ldg(dsl + threadIdx.x * CS) : __ldg(dk + threadIdx.x * Wh);
+      dMv = PVRB ? __ldg(dsl + threadIdx.x * CS + COLS) : __ldg(dk + threadIdx.x * Wh + M);
     }
     {
       const C* twc = TW + CP::TW_COL;
@@ -378,7 +411,8 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         C pv[RL];
         if (col != 0) {
 #pragma unroll
-          for (int s = 0; s < RL; ++s) pv[s] = __ldg(dk + (j + s * JL) * Wh + col);
+          for (int s = 0; s < RL; ++s)
+            pv[s] = PVRB ? __ldg(dsl + (j + s * JL) * CS + cl) : __ldg(dk + (j + s * JL) * Wh + col);
         }
         C x[RL];
 #pragma unroll
@@ -408,8 +442,9 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   if (ADMM && threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < CL)
     for (int f = 0; f < 3; ++f)
       printf("CLT f=%d rank=%u start=%llu ready_I=%llu bf_I=%llu recv_I=%llu rif=%llu rir=%llu prox=%llu "
-             "ready_F=%llu bi_F=%llu recv_F=%llu cff=%llu last=%llu\n", f, rank, tt[f][6], tt[f][0], tt[f][1],
-             tt[f][2], tt[f][7], tt[f][8], tt[f][9], tt[f][3], tt[f][4], tt[f][5], tt[f][10], tt[f][11]);
+             "ready_F=%llu bi_F=%llu recv_F=%llu cff=%llu last=%llu dwait=%llu gen1=%llu\n", f, rank, tt[f][6], tt[f][0],
+             tt[f][1], tt[f][2], tt[f][7], tt[f][8], tt[f][9], tt[f][3], tt[f][4], tt[f][5], tt[f][10], tt[f][11],
+             tt[f][12], tt[f][13]);
 #endif
   cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
   {
