@@ -123,6 +123,10 @@ int dcsc_cuda_synchronize(dcsc_cuda_ctx* ctx);
  * cfg.normalize (pipeline.cpp:78-121) */
 int dcsc_cuda_set_signals(dcsc_cuda_ctx* ctx, const double* x);
 int dcsc_cuda_get_signals(dcsc_cuda_ctx* ctx, double* x);
+/* per image (N ints): 1 when the last set_signals' normalisation met a constant
+ * input (dcsc::normalize's degenerate flag, pipeline.cpp:84-121; run_csc turns
+ * it into RunResult::warnings, pipeline.cpp:177-183) */
+int dcsc_cuda_signal_flags(dcsc_cuda_ctx* ctx, int* degenerate);
 /* dictionary: K*J*mh*mw doubles (filter-major, Dictionary::filter(k, j)) */
 int dcsc_cuda_set_dictionary(dcsc_cuda_ctx* ctx, const double* d);
 int dcsc_cuda_get_dictionary(dcsc_cuda_ctx* ctx, double* d);

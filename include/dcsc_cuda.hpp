@@ -108,17 +108,57 @@ inline CodingStats to_stats(const dcsc_coding_stats& s) {
 }
 
 namespace detail {
+// Per-thread context cache for the per-call wrappers: the reference calls
+// solve_coding once per image from OpenMP threads (pipeline.cpp:221-227), so
+// each host thread keeps one device context (buffers, stream, twiddles) for
+// the last shape / config / device it used instead of creating and destroying
+// one per call, and skips the dictionary upload + spectra rebuild when the
+// dictionary is unchanged (the same d for every image of an outer iteration).
+struct CachedContext {
+  std::unique_ptr<Context> ctx;
+  std::vector<int> key;
+  std::vector<double> cfg_key, dict;
+  bool dict_valid = false;
+};
+// slot 0: solve_coding (one image), slot 1: solve_learning (all images)
+inline CachedContext& cached_context(int slot, int n, const GridDims& dims, int filters, const GridDims& support,
+                                     const SolverConfig& cfg, Options opt, int channels) {
+  thread_local CachedContext cache[2];
+  CachedContext& cc = cache[slot];
+  const dcsc_solver_config c = to_c(cfg);
+  std::vector<int> key = {n, dims[0], dims[1], filters, support[0], support[1], opt.precision, opt.device, channels,
+                          c.max_outer, c.max_admm, c.max_mu_iters, c.cg_max, c.normalize};
+  std::vector<double> ck = {c.beta, c.rho, c.tol, c.cg_tol, c.mu_floor, static_cast<double>(c.seed)};
+  if (!cc.ctx || key != cc.key || ck != cc.cfg_key) {
+    cc.ctx.reset();
+    cc.ctx = std::make_unique<Context>(n, dims, filters, support, cfg, opt, channels);
+    cc.key = std::move(key);
+    cc.cfg_key = std::move(ck);
+    cc.dict_valid = false;
+  }
+  return cc;
+}
+
 // one J-channel signal, warm state in/out (J = 1: solve_coding, J > 1: TCSC)
 inline SparseMaps code_one(const SignalTensor& x, const Dictionary& d, const SolverConfig& cfg,
                            CodingDualState& state, CodingStats* stats, Options opt) {
+  if (x.dims.size() != 2 || d.support.size() != 2) throw DimensionError("dcsc::cuda supports 2-D grids only");
   SolverConfig c = cfg;
   c.normalize = NormalizeMode::None;  // solve_coding never normalises
-  Context ctx(1, x.dims, d.filters, d.support, c, opt, x.channels);
+  CachedContext& cc = cached_context(0, 1, x.dims, d.filters, d.support, c, opt, x.channels);
+  Context& ctx = *cc.ctx;
   check(dcsc_cuda_set_signals(ctx.get(), x.values.data()));
-  check(dcsc_cuda_set_dictionary(ctx.get(), d.values.data()));
+  if (!cc.dict_valid || cc.dict != d.values) {
+    cc.dict_valid = false;
+    check(dcsc_cuda_set_dictionary(ctx.get(), d.values.data()));
+    cc.dict = d.values;
+    cc.dict_valid = true;
+  }
   const std::size_t kd = static_cast<std::size_t>(d.filters) * x.grid_count();
   if (state.z.size() == kd && state.theta.size() == kd)
     check(dcsc_cuda_set_coding_state(ctx.get(), 0, 1, state.theta.data(), state.z.data()));
+  else  // the reference's empty state (coding.cpp:175-179)
+    check(dcsc_cuda_set_coding_state(ctx.get(), 0, 1, nullptr, nullptr));
   dcsc_coding_stats s{};
   check(dcsc_cuda_coding(ctx.get(), 0, 1, &s));
   state.theta.assign(kd, 0.0);
@@ -177,7 +217,8 @@ inline Dictionary solve_learning(std::span<const SignalTensor> xs, std::span<con
   SolverConfig c = cfg;
   c.normalize = NormalizeMode::None;
   const int J = xs.front().channels;
-  Context ctx(N, dims, K, support, c, opt, J);
+  if (dims.size() != 2 || support.size() != 2) throw DimensionError("dcsc::cuda supports 2-D grids only");
+  Context& ctx = *detail::cached_context(1, N, dims, K, support, c, opt, J).ctx;
   const std::size_t JD = static_cast<std::size_t>(J) * D;
   std::vector<double> x(N * JD), z(static_cast<std::size_t>(N) * K * D);
   for (int n = 0; n < N; ++n) {
@@ -248,6 +289,15 @@ inline RunResult run_csc(const RunConfig& cfg, const Dataset& data, Options opt 
   for (int n = 0; n < N; ++n) std::copy(data.signals[n].values.begin(), data.signals[n].values.end(), x.begin() + n * JD);
   check(dcsc_cuda_set_signals(ctx.get(), x.data()));
   RunResult r;
+  {  // normalisation warnings (pipeline.cpp:177-183)
+    std::vector<int> degen(N);
+    check(dcsc_cuda_signal_flags(ctx.get(), degen.data()));
+    for (int n = 0; n < N; ++n)
+      if (degen[n]) {
+        const std::string name = static_cast<std::size_t>(n) < data.names.size() ? data.names[n] : std::to_string(n);
+        r.warnings.push_back("normalize: constant input '" + name + "' mapped to zeros");
+      }
+  }
   std::vector<dcsc_trace_row> rows(2 * std::max(cfg.solver.max_outer, 1));
   int n_rows = 0, conv = 0;
   check(dcsc_cuda_run(ctx.get(), cfg.solver.max_outer, rows.data(), &n_rows, &conv));

@@ -89,10 +89,63 @@ static int check_errors() {
   return ok ? 0 : 1;
 }
 
+// The reference's own call pattern (pipeline.cpp:221-227): solve_coding once
+// per image from OpenMP threads, warm states carried over two sweeps, then
+// solve_learning; dcsc::cuda's per-thread cached contexts against the
+// reference's sequential calls (FP64, identical iteration counts, <= 1e-9).
+static int check_threads() {
+  const int N = 12, H = 20, W = 20, K = 4, m = 5;
+  std::mt19937_64 rng(7);
+  std::vector<dcsc::SignalTensor> xs;
+  for (int n = 0; n < N; ++n) {
+    dcsc::SignalTensor x({H, W}, 1);
+    for (double& v : x.values) v = static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5;
+    xs.push_back(x);
+  }
+  dcsc::Dictionary d(K, {m, m}, 1);
+  for (double& v : d.values) v = static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5;
+  dcsc::SolverConfig cfg;
+  cfg.beta = 0.1;
+  cfg.max_admm = 60;
+  std::vector<dcsc::CodingDualState> sa(N), sb(N);
+  std::vector<dcsc::SparseMaps> za(N), zb(N);
+  std::vector<dcsc::CodingStats> ca(N), cb(N);
+  double worst = 0.0;
+  bool iters_ok = true;
+  for (int sweep = 0; sweep < 2; ++sweep) {
+    for (int n = 0; n < N; ++n) za[n] = dcsc::solve_coding(xs[n], d, cfg, sa[n], &ca[n]);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(4)
+    for (int n = 0; n < N; ++n) zb[n] = dcsc::cuda::solve_coding(xs[n], d, cfg, sb[n], &cb[n]);
+    for (int n = 0; n < N; ++n) {
+      iters_ok = iters_ok && ca[n].admm_iters == cb[n].admm_iters;
+      double zm = 0.0, dz = 0.0;
+      for (std::size_t i = 0; i < za[n].values.size(); ++i) {
+        zm = std::max(zm, std::abs(za[n].values[i]));
+        dz = std::max(dz, std::abs(za[n].values[i] - zb[n].values[i]));
+      }
+      worst = std::max(worst, dz / std::max(zm, 1e-300));
+    }
+  }
+  dcsc::LearningDualState la, lb;
+  const dcsc::Dictionary da = dcsc::solve_learning(xs, za, {m, m}, cfg, la);
+  const dcsc::Dictionary db = dcsc::cuda::solve_learning(xs, zb, {m, m}, cfg, lb);
+  double dmax = 0.0, dref = 0.0;
+  for (std::size_t i = 0; i < da.values.size(); ++i) {
+    dmax = std::max(dmax, std::abs(da.values[i] - db.values[i]));
+    dref = std::max(dref, std::abs(da.values[i]));
+  }
+  const bool ok = iters_ok && worst <= 1e-9 && dmax <= 1e-7 * dref;
+  std::printf("{\"threads\": 4, \"ok\": %s, \"iters_equal\": %s, \"max_rel_z\": %.3e, \"max_rel_dict\": %.3e}\n",
+              ok ? "true" : "false", iters_ok ? "true" : "false", worst, dmax / std::max(dref, 1e-300));
+  return ok ? 0 : 1;
+}
+
 // usage: dropin_check [outer] [channels]   (channels > 1: Joint mode, TCSC)
 //        dropin_check errors               (exception parity on bad inputs)
+//        dropin_check threads              (per-image calls from OpenMP threads)
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "errors") return check_errors();
+  if (argc > 1 && std::string(argv[1]) == "threads") return check_threads();
   const int N = 3, H = 20, W = 20, K = 6, m = 5, outer = argc > 1 ? std::atoi(argv[1]) : 3;
   const int J = argc > 2 ? std::atoi(argv[2]) : 1;
   dcsc::Dataset data;

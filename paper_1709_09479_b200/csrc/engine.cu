@@ -331,6 +331,13 @@ int dcsc_cuda_run(dcsc_cuda_ctx* ctx, int max_outer, dcsc_trace_row* rows, int* 
   CTX_CHECK
   return guarded([&] { ctx->eng->run(max_outer, rows, n_rows, converged); });
 }
+int dcsc_cuda_signal_flags(dcsc_cuda_ctx* ctx, int* degenerate) {
+  CTX_CHECK
+  return guarded([&] {
+    if (!degenerate) throw InvErr("null argument");
+    ctx->eng->signal_flags(degenerate);
+  });
+}
 int dcsc_cuda_run_begin(dcsc_cuda_ctx* ctx) {
   CTX_CHECK
   return guarded([&] { ctx->eng->run_begin(); });

@@ -101,10 +101,11 @@ std::vector<double> gaussian_blur(int H, int W, const double* v, double sigma) {
 
 // dcsc::normalize (pipeline.cpp:78-121) for one J-channel image: Global uses
 // the mean / std of all J*D values, Local runs per channel.
-void normalize_image(int mode, int H, int W, const double* in, double* out, int J = 1) {
+// *degen: the reference's degenerate flag (constant input, pipeline.cpp:90-93, 111-115).
+void normalize_image(int mode, int H, int W, const double* in, double* out, int J = 1, bool* degen = nullptr) {
   if (mode == 2 && J > 1) {
     for (int j = 0; j < J; ++j)
-      normalize_image(mode, H, W, in + (size_t)j * H * W, out + (size_t)j * H * W, 1);
+      normalize_image(mode, H, W, in + (size_t)j * H * W, out + (size_t)j * H * W, 1, degen);
     return;
   }
   const size_t D = (size_t)H * W * J;  // None / Global act on all J*D values
@@ -121,6 +122,7 @@ void normalize_image(int mode, int H, int W, const double* in, double* out, int 
     const double sd = std::sqrt(var / (double)D);
     if (sd < 1e-8) {
       std::fill(out, out + D, 0.0);
+      if (degen) *degen = true;
       return;
     }
     for (size_t i = 0; i < D; ++i) out[i] = (in[i] - m) / sd;
@@ -139,6 +141,7 @@ void normalize_image(int mode, int H, int W, const double* in, double* out, int 
   fl /= (double)D;
   if (fl < 1e-8) {
     for (size_t i = 0; i < D; ++i) out[i] = in[i] - lm[i];
+    if (degen) *degen = true;
     return;
   }
   for (size_t i = 0; i < D; ++i) out[i] = (in[i] - lm[i]) / std::max(lsd[i], fl);
@@ -569,11 +572,14 @@ class Engine final : public EngineBase {
     }
     R* xr = static_cast<R*>(xstage_);
     xs_host_.resize(nD);
+    degen_.assign(N_, 0);
     const size_t JD = (size_t)J_ * D;
 #pragma omp parallel for schedule(static)
     for (int n = 0; n < N_; ++n) {
       double* xn = xs_host_.data() + (size_t)n * JD;
-      normalize_image(cfg_.normalize, H, W, x + (size_t)n * JD, xn, J_);
+      bool dg = false;
+      normalize_image(cfg_.normalize, H, W, x + (size_t)n * JD, xn, J_, &dg);
+      degen_[n] = dg ? 1 : 0;
       double s = 0.0;
       for (int j = 0; j < J_; ++j) {
         double sj = 0.0;
@@ -595,6 +601,9 @@ class Engine final : public EngineBase {
   }
 
   void get_signals(double* x) override { std::copy(xs_host_.begin(), xs_host_.end(), x); }
+  void signal_flags(int* degenerate) override {
+    for (int n = 0; n < N_; ++n) degenerate[n] = n < (int)degen_.size() ? degen_[n] : 0;
+  }
 
   void set_dictionary(const double* d) override {
     const size_t cnt = (size_t)K_ * J_ * M_;
@@ -1673,6 +1682,7 @@ class Engine final : public EngineBase {
   std::vector<char> t0_pending_;  // per image: theta0_ holds a not ADMM-consistent warm theta
   bool use_theta0_ = false;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
+  std::vector<int> degen_;  // per image: normalisation met a constant input
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)
   C* gam_ch_ = nullptr;  // learning view: gamma_hat of the current channel
   std::vector<int> live_h_;

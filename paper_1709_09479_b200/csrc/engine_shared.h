@@ -45,6 +45,7 @@ class EngineBase {
   virtual ~EngineBase() = default;
   virtual void set_signals(const double* x) = 0;
   virtual void get_signals(double* x) = 0;
+  virtual void signal_flags(int* degenerate) = 0;
   virtual void set_dictionary(const double* d) = 0;
   virtual void get_dictionary(double* d) = 0;
   virtual void init_variables() = 0;

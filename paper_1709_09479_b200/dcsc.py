@@ -139,7 +139,7 @@ EXPORTS = [
     "dcsc_io_write_trace_csv", "dcsc_io_read_trace_csv", "dcsc_cuda_fft_timing", "dcsc_cuda_reconstruct",
     "dcsc_synth_dataset", "dcsc_synth_generate_range", "dcsc_cuda_learning_correlation",
     "dcsc_cuda_dictionary_adjoint", "dcsc_cuda_lambda_update", "dcsc_cuda_gamma_solve", "dcsc_cuda_d_recover",
-    "dcsc_cuda_run_begin", "dcsc_cuda_run_step", "dcsc_cuda_run_accepts",
+    "dcsc_cuda_run_begin", "dcsc_cuda_run_step", "dcsc_cuda_run_accepts", "dcsc_cuda_signal_flags",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -254,6 +254,12 @@ class Context:
 
     def _sig_shape(self, lead):
         return lead + ((self.J,) if self.J > 1 else ()) + (self.H, self.W)
+
+    def signal_flags(self):
+        """Per image: True when normalisation met a constant input (pipeline.cpp:177-183)."""
+        out = np.zeros(self.N, dtype=np.int32)
+        _err(lib().dcsc_cuda_signal_flags(self._h, out.ctypes.data_as(C.POINTER(C.c_int))))
+        return out.astype(bool)
 
     def get_signals(self):
         out = np.zeros(self._sig_shape((self.N,)))
@@ -590,17 +596,21 @@ def encode(x, d, cfg: SolverConfig, precision: int = 64):
     return z[0], obj, stats
 
 
-def run_csc(xs, filters: int, support, cfg: SolverConfig, precision: int = 64):
-    """run_csc (pipeline.cpp:158-301): returns dict(trace, dict, maps, converged).
-    xs (N,H,W) or (N,J,H,W); J > 1 is the Joint channel mode (TCSC)."""
+def run_csc(xs, filters: int, support, cfg: SolverConfig, precision: int = 64, names=None):
+    """run_csc (pipeline.cpp:158-301): returns dict(trace, dict, maps, converged, warnings).
+    xs (N,H,W) or (N,J,H,W); J > 1 is the Joint channel mode (TCSC). `warnings`
+    follows RunResult::warnings (pipeline.cpp:177-183) for constant inputs."""
     xs = _f64(xs)
     J = xs.shape[1] if xs.ndim == 4 else 1
     N, H, W = xs.shape[0], xs.shape[-2], xs.shape[-1]
     with Context(N, (H, W), filters, tuple(support), cfg, precision, channels=J) as ctx:
         ctx.set_signals(xs)
+        flags = ctx.signal_flags()
+        warnings = [f"normalize: constant input '{names[n] if names is not None and n < len(names) else n}' "
+                    "mapped to zeros" for n in range(N) if flags[n]]
         trace, conv = ctx.run(cfg.max_outer)
         return {"trace": trace, "dict": ctx.get_dictionary(), "maps": ctx.get_maps(),
-                "converged": conv}
+                "converged": conv, "warnings": warnings}
 
 
 def forward_dft2(x, precision: int = 64):

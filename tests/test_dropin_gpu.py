@@ -30,3 +30,30 @@ def test_reference_program_error_parity():
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert r.returncode == 0 and out["ok"], out
     assert len(out["errors"]) == 6
+
+
+def test_reference_program_per_image_calls_from_openmp_threads():
+    """The reference's per-image call pattern (pipeline.cpp:221-227): dcsc::cuda::solve_coding
+    called concurrently from 4 OpenMP threads (each with its cached device context),
+    warm states over two sweeps, then solve_learning; equal to the reference's
+    sequential calls (iteration counts equal, maps <= 1e-9, dictionary <= 1e-7)."""
+    if not os.path.exists(BIN):
+        pytest.fail("oracle/_ref/dropin_check not built (make -C oracle dropin)")
+    r = subprocess.run([BIN, "threads"], capture_output=True, text=True, timeout=300)
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert r.returncode == 0 and out["ok"], out
+
+
+def test_run_csc_warnings_for_constant_inputs():
+    """RunResult::warnings parity (pipeline.cpp:177-183): a constant image under
+    Global normalisation is reported by name and mapped to zeros."""
+    import numpy as np
+
+    from paper_1709_09479_b200 import dcsc
+
+    rng = np.random.default_rng(1)
+    xs = rng.random((3, 16, 16))
+    xs[1] = 0.25
+    r = dcsc.run_csc(xs, 2, (3, 3), dcsc.SolverConfig(beta=0.2, max_outer=1, normalize=1, tol=1e-300), 64,
+                     names=["a", "flat", "c"])
+    assert r["warnings"] == ["normalize: constant input 'flat' mapped to zeros"]
