@@ -168,6 +168,12 @@ struct KernelFamily {
   using P = Plane<R, H, W, pick_threads(H, W)>;
 };
 template <>
+struct KernelFamily<double, 128, 128> {  // FP64 128x128: 133 KB per plane buffer
+  static constexpr bool cluster = true;
+  static constexpr int CL = 4;
+  using P = ClusterPlane<double, 128, 128, 4, 256>;
+};
+template <>
 struct KernelFamily<float, 256, 256> {
   static constexpr bool cluster = true;
 #ifndef DCSC_CL256

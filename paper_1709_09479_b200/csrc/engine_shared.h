@@ -85,16 +85,25 @@ class EngineBase {
 };
 
 // ---------------------------------------------------------------- size table
+// Adding a grid: one X(...) line here, a DCSC_ENGINE_INSTANTIATE in an
+// inst_*.cu unit, and PlanFor<H>, PlanFor<W/2> radix plans (fft2d.cuh) built
+// from radices 2, 3, 4, 5, 6, 8, 10, 16.
 #define DCSC_SIZES(X) \
   X(double, 16, 16)   \
   X(double, 16, 20)   \
   X(double, 20, 20)   \
+  X(double, 32, 32)   \
+  X(double, 48, 48)   \
   X(double, 64, 64)   \
   X(double, 100, 100) \
+  X(double, 128, 128) \
   X(float, 16, 16)    \
   X(float, 16, 20)    \
   X(float, 20, 20)    \
+  X(float, 32, 32)    \
+  X(float, 48, 48)    \
   X(float, 64, 64)    \
+  X(float, 80, 80)    \
   X(float, 100, 100)  \
   X(float, 128, 128)  \
   X(float, 256, 256)

@@ -188,8 +188,11 @@ template <> struct PlanFor<16> { using type = RadixList<16>; };
 template <> struct PlanFor<20> { using type = RadixList<4, 5>; };
 template <> struct PlanFor<24> { using type = RadixList<8, 3>; };
 template <> struct PlanFor<32> { using type = RadixList<8, 4>; };
+template <> struct PlanFor<40> { using type = RadixList<8, 5>; };
+template <> struct PlanFor<48> { using type = RadixList<16, 3>; };
 template <> struct PlanFor<50> { using type = RadixList<10, 5>; };
 template <> struct PlanFor<64> { using type = RadixList<8, 8>; };
+template <> struct PlanFor<80> { using type = RadixList<16, 5>; };
 template <> struct PlanFor<100> { using type = RadixList<10, 10>; };
 template <> struct PlanFor<128> { using type = RadixList<16, 8>; };
 template <> struct PlanFor<256> { using type = RadixList<16, 16>; };
