@@ -402,7 +402,8 @@ def config_block(cfg, args, world):
     return {"workload": wl, "images": cfg["N"], "channels": cfg.get("J", 1), "filters": cfg["K"],
             "grid": [cfg["H"], cfg["W"]], "support": [cfg["m"], cfg["m"]], "precision": f"fp{cfg['prec']}",
             "parallelism": (f"{cfg['N']} images per GPU x {world} GPUs (weak)" if cfg["coding_only"]
-                            else f"{cfg['N']} images sharded over {world} GPU(s) (strong)"),
+                            else f"{cfg['N']} images sharded over {world} GPU(s) (strong), learning "
+                                 f"{getattr(args, 'learning_layout', 'image')}-sharded"),
             "l2": "inputs larger than L2 (ADMM state u = N*K*D*s)", "seed": SEED}
 
 
@@ -478,6 +479,7 @@ def run_ours(args, cfg):
             nccl_ranks = world
         else:
             ctx.set_comm_callback(world, rank, dcsc.gloo_allreduce_fn())
+        ctx.set_learning_layout(args.learning_layout)
     ctx.set_signals(x)
     ctx.set_dictionary(d_true)
 
@@ -687,6 +689,9 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dump-counts", action="store_true")
+    ap.add_argument("--learning-layout", default="image", choices=["image", "freq"],
+                    help="multi-GPU learning: image-sharded (crop all-reduce) or frequency-sharded "
+                         "(z_hat all-to-all per outer iteration)")
     args = ap.parse_args()
     rc = spawn_ranks(args)
     if rc is not None:

@@ -236,6 +236,17 @@ typedef int (*dcsc_allreduce_fn)(double* buf, size_t n, void* user);
 int dcsc_cuda_nccl_unique_id(unsigned char* out, size_t len);
 int dcsc_cuda_set_comm_nccl(dcsc_cuda_ctx* ctx, int world, int rank, const unsigned char* id, size_t len);
 int dcsc_cuda_set_comm_callback(dcsc_cuda_ctx* ctx, int world, int rank, dcsc_allreduce_fn fn, void* user);
+/* learning layout across ranks (call after set_comm_*; J = 1):
+ * 0 image-sharded (default): each rank keeps z_hat of its own images, the
+ *   K x M cropped correlations are all-reduced per operator apply;
+ * 1 frequency-sharded (BASELINE.json north_star): after coding, one
+ *   all-to-all (grouped ncclSend/ncclRecv) moves z_hat (and x_hat) from
+ *   image-major to frequency-major blocks, so each rank runs CG over all N
+ *   images on 1/world of the bins; the cropped correlations are still
+ *   all-reduced (crop(iDFT(sum_r c_r)) = sum_r crop(iDFT(c_r))) and the
+ *   per-image learning data terms are all-reduced. Learning-state get/set is
+ *   not available in this layout. A no-op on one rank. */
+int dcsc_cuda_set_learning_layout(dcsc_cuda_ctx* ctx, int layout);
 
 /* On-disk formats, byte-compatible with the reference (host only):
  * CSCT tensors (tensor_io.hpp:1-30; tensor_io.cpp:45-90) and the

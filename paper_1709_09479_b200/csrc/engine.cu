@@ -62,6 +62,10 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 
 NcclApi& nccl_api() {
@@ -74,6 +78,10 @@ NcclApi& nccl_api() {
     api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(api.h, "ncclAllReduce"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(api.h, "ncclCommDestroy"));
     api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+    api.send = reinterpret_cast<decltype(api.send)>(dlsym(api.h, "ncclSend"));
+    api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(api.h, "ncclRecv"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(api.h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(api.h, "ncclGroupEnd"));
     if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
       throw CudaErr("NCCL: missing symbols in libnccl.so.2");
   }
@@ -104,6 +112,21 @@ struct NcclReducer final : Reducer {
   void allreduce(double* dev, size_t n, cudaStream_t st) override {
     NCK(nccl_api().allReduce(dev, dev, n, ncclDouble, ncclSum, comm, st));
   }
+  // grouped point-to-point all-to-all (NCCL 2.27 has no ncclAllToAll)
+  void alltoall(const void* send, const size_t* sbytes, void* recv, const size_t* rbytes,
+                cudaStream_t st) override {
+    NcclApi& api = nccl_api();
+    if (!api.send || !api.recv || !api.groupStart || !api.groupEnd) throw CudaErr("NCCL: no ncclSend/ncclRecv");
+    size_t so = 0, ro = 0;
+    NCK(api.groupStart());
+    for (int q = 0; q < world; ++q) {
+      if (sbytes[q]) NCK(api.send(static_cast<const char*>(send) + so, sbytes[q], ncclInt8, q, comm, st));
+      if (rbytes[q]) NCK(api.recv(static_cast<char*>(recv) + ro, rbytes[q], ncclInt8, q, comm, st));
+      so += sbytes[q];
+      ro += rbytes[q];
+    }
+    NCK(api.groupEnd());
+  }
 };
 
 struct HostReducer final : Reducer {
@@ -121,6 +144,38 @@ struct HostReducer final : Reducer {
     if (fn(host.data(), n, user) != 0) throw CudaErr("host all-reduce callback failed");
     CK(cudaMemcpyAsync(dev, host.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
+  }
+  // all-to-all through the sum callback (tests with ranks sharing one GPU):
+  // the size matrix first, then per destination one zero-padded buffer of
+  // every source's block, summed over ranks
+  void alltoall(const void* send, const size_t* sbytes, void* recv, const size_t* rbytes,
+                cudaStream_t st) override {
+    std::vector<double> sz((size_t)world * world, 0.0);
+    for (int q = 0; q < world; ++q) sz[(size_t)rank * world + q] = (double)sbytes[q];
+    if (fn(sz.data(), sz.size(), user) != 0) throw CudaErr("host all-reduce callback failed");
+    size_t so = 0;
+    for (int q = 0; q < world; ++q) {
+      size_t tot = 0, mine = 0;
+      for (int r = 0; r < world; ++r) {
+        if (r == rank) mine = tot;
+        tot += (size_t)sz[(size_t)r * world + q];
+      }
+      std::vector<double> buf(tot / 8, 0.0);
+      if (sbytes[q]) {
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(buf.data()) + mine, static_cast<const char*>(send) + so,
+                           sbytes[q], cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      if (fn(buf.data(), buf.size(), user) != 0) throw CudaErr("host all-reduce callback failed");
+      if (q == rank) {
+        size_t want = 0;
+        for (int r = 0; r < world; ++r) want += rbytes[r];
+        if (want != tot) throw CudaErr("all-to-all size mismatch");
+        CK(cudaMemcpyAsync(recv, buf.data(), tot, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      so += sbytes[q];
+    }
   }
 };
 int prec_of(const char* t) { return std::strcmp(t, "double") == 0 ? 64 : 32; }
@@ -348,6 +403,13 @@ int dcsc_cuda_run_step(dcsc_cuda_ctx* ctx, dcsc_trace_row* rows, int* converged)
     if (!rows) throw InvErr("null argument");
     const int c = ctx->eng->run_step(rows);
     if (converged) *converged = c;
+  });
+}
+int dcsc_cuda_set_learning_layout(dcsc_cuda_ctx* ctx, int layout) {
+  CTX_CHECK
+  return guarded([&] {
+    if (layout != 0 && layout != 1) throw InvErr("learning layout: 0 image-sharded, 1 frequency-sharded");
+    ctx->eng->set_learning_layout(layout);
   });
 }
 int dcsc_cuda_run_accepts(dcsc_cuda_ctx* ctx, int* image_accept, int* dict_accept) {

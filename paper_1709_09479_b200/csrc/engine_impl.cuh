@@ -579,6 +579,7 @@ class Engine final : public EngineBase {
     R* xr = static_cast<R*>(xstage_);
     xs_host_.resize(nD);
     degen_.assign(N_, 0);
+    xf_valid_ = false;
     const size_t JD = (size_t)J_ * D;
 #pragma omp parallel for schedule(static)
     for (int n = 0; n < N_; ++n) {
@@ -666,6 +667,7 @@ class Engine final : public EngineBase {
     t0_pending_.assign(N_, 0);
     mu_.assign(K_, 1.0);
     zhat_valid_ = false;
+    zf_valid_ = false;
     CK(cudaStreamSynchronize(st_));
   }
 
@@ -930,6 +932,7 @@ class Engine final : public EngineBase {
     CK(cudaMemcpyAsync(maps_.as<R>() + (size_t)n0 * K_ * D, v.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st_));
     CK(cudaStreamSynchronize(st_));
     zhat_valid_ = false;
+    zf_valid_ = false;
   }
 
   void get_maps(int n0, int n1, double* z) override {
@@ -942,6 +945,7 @@ class Engine final : public EngineBase {
   }
 
   void set_learning_state(const double* gamma, const double* mu) override {
+    if (freq_) throw InvErr("learning state is not available in the frequency-sharded layout");
     if (gamma) {  // J x N x D (LearningDualState::gamma[j], learning.hpp:15-23)
       DevMem tmp;
       tmp.alloc(sizeof(double) * (size_t)J_ * N_ * D);
@@ -957,6 +961,7 @@ class Engine final : public EngineBase {
   }
 
   void get_learning_state(double* gamma, double* mu) override {
+    if (freq_ && gamma) throw InvErr("learning state is not available in the frequency-sharded layout");
     if (gamma) {
       DevMem tmp;
       tmp.alloc(sizeof(double) * (size_t)J_ * N_ * D);
@@ -1148,6 +1153,10 @@ class Engine final : public EngineBase {
   // per-channel gamma systems under one mu ascent with joint filter norms
   // (solve_learning_tcsc, tcsc.cpp:263-270 -> learning.cpp:276-345)
   void learning(double* d_out, dcsc_learning_stats* st) override {
+    if (freq_) {
+      learning_freq(d_out, st);
+      return;
+    }
     dcsc_learning_stats ls{};
     if ((int)mu_.size() != K_) mu_.assign(K_, 1.0);
     build_zhat();
@@ -1381,6 +1390,10 @@ class Engine final : public EngineBase {
   // per-image data terms of `d` against the accepted maps (Parseval on z_hat),
   // summed over channels
   void data_terms(const double* d, std::vector<double>& data) {
+    if (freq_) {
+      data_terms_freq(d, data);
+      return;
+    }
     build_zhat();
     upload_dict_spectra(d, dcand_.as<C>());
     const dim3 g3(tiles_, N_);
@@ -1525,6 +1538,7 @@ class Engine final : public EngineBase {
     accept(acc, zc2, zn2, l0);
     run_acc_ = acc;
     zhat_valid_ = false;
+    zf_valid_ = false;
     dcsc_objective after{};
     for (int n = 0; n < N_; ++n) {
       after.data_term += img[n].data_term;
@@ -1604,6 +1618,262 @@ class Engine final : public EngineBase {
         break;
       }
     }
+  }
+
+  // ---------------------------------------------------- frequency-sharded learning
+  // (BASELINE.json north_star). Rank r owns the half-spectrum
+  // bins [b0_r, b0_r + nbl_r), b0_r = r NB / world, for ALL images: after
+  // coding, one all-to-all (grouped ncclSend/ncclRecv) moves z_hat from
+  // image-major [N_r][K][NB] to frequency-major [N_tot][K][nbl] (x_hat once per
+  // set_signals). The contractions (learning.cpp:97-121) and the CG vector
+  // updates then run on the local bins of every image; the mask step needs all
+  // bins of c_k, and the crop of an inverse DFT is linear, so each rank crops
+  // the inverse DFT of its local bins (zero elsewhere) and the K x M crops are
+  // all-reduced as in the image-sharded layout (d_recover identically); the
+  // CG scalars (Parseval with the bins' global weights) and the per-image
+  // learning data terms (objective.cpp:83-95) are all-reduced.
+  void set_learning_layout(int freq) override {
+    freq_ = false;
+    if (!freq || !multi()) return;
+    if (J_ != 1) throw DimErr("frequency-sharded learning supports single-channel data");
+    const int world = red_->world, rank = red_->rank;
+    std::vector<double> nr(world, 0.0);
+    nr[rank] = N_;
+    reduce_host(nr.data(), world);
+    fn_rank_.assign(world, 0);
+    fntot_ = 0;
+    fnoff_ = 0;
+    for (int q = 0; q < world; ++q) {
+      fn_rank_[q] = (long)nr[q];
+      if (q < rank) fnoff_ += (int)fn_rank_[q];
+      fntot_ += (int)fn_rank_[q];
+    }
+    fb0_ = (int)((long)rank * NB / world);
+    fnbl_ = (int)((long)(rank + 1) * NB / world) - fb0_;
+    ftiles_ = (fnbl_ + TBV - 1) / TBV;
+    const size_t vec = (size_t)fntot_ * fnbl_;
+    zf_.alloc(sizeof(C) * vec * K_);
+    xf_.alloc(sizeof(C) * vec);
+    gf_.alloc(sizeof(C) * vec);
+    rf_.alloc(sizeof(C) * vec);
+    pf_.alloc(sizeof(C) * vec);
+    apf_.alloc(sizeof(C) * vec);
+    fsend_.alloc(sizeof(C) * (size_t)N_ * K_ * NB);
+    fpart_.alloc(sizeof(double) * std::max((size_t)fntot_ * ftiles_, (vec + TBV - 1) / TBV));
+    fodata_.alloc(sizeof(double) * fntot_);
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o_.device);
+      const long base = (long)ftiles_ * ((K_ + DCSC_KC - 1) / DCSC_KC);
+      const double want = std::max(1.0, 4.0 * sms / (double)base);
+      const long p2 = 1L << (int)std::lround(std::log2(want));
+      fcsplit_ = (int)std::max(1L, std::min({p2, 64L, (long)fntot_}));
+    }
+    fcpart_.alloc(sizeof(double2) * (size_t)fcsplit_ * K_ * fnbl_);
+    device_bytes += zf_.bytes + 5 * xf_.bytes + fsend_.bytes + fcpart_.bytes;
+    CK(cudaMemsetAsync(gf_.p, 0, gf_.bytes, st_));
+    CK(cudaStreamSynchronize(st_));
+    zf_valid_ = xf_valid_ = false;
+    freq_ = true;
+  }
+
+  // image-major [planes_r][NB] on every rank -> frequency-major [sum_r planes_r][nbl]
+  // (`per_image` planes per image)
+  void to_freq(const C* src, C* dst, int per_image) {
+    const int world = red_->world;
+    const size_t planes = (size_t)N_ * per_image;
+    launch(kFamOther, [&] {
+      pack_bins<C><<<1184, 256, 0, st_>>>(src, fsend_.as<C>(), planes, NB, world);
+    });
+    std::vector<size_t> sb(world), rb(world);
+    for (int q = 0; q < world; ++q) {
+      const long b0 = (long)q * NB / world, b1 = (long)(q + 1) * NB / world;
+      sb[q] = sizeof(C) * planes * (size_t)(b1 - b0);
+      rb[q] = sizeof(C) * (size_t)fn_rank_[q] * per_image * (size_t)fnbl_;
+    }
+    red_->alltoall(fsend_.p, sb.data(), dst, rb.data(), st_);
+  }
+
+  void freq_operands() {
+    build_zhat();
+    if (!zf_valid_) {
+      to_freq(zhat_.as<C>(), zf_.as<C>(), K_);
+      zf_valid_ = true;
+    }
+    if (!xf_valid_) {
+      to_freq(xhat_.as<C>(), xf_.as<C>(), 1);
+      xf_valid_ = true;
+    }
+  }
+
+  // c_k on the local bins of every image -> full K x NB spectra (zero elsewhere)
+  void correlate_freq(const C* v, const int* done) {
+    constexpr int KC = DCSC_KC;
+    const dim3 g1(ftiles_, (K_ + KC - 1) / KC, fcsplit_);
+    launch(kFamContract, [&] {
+      contract_c<R, KC><<<g1, TBV, 0, st_>>>(zf_.as<C>(), v, fcpart_.as<double2>(), live_.as<int>(), fntot_, K_,
+                                             fnbl_, done);
+    });
+    const size_t knbl = (size_t)K_ * fnbl_;
+    launch(kFamOther, [&] {
+      contract_c_reduce_off<R><<<(unsigned)((knbl + 255) / 256), 256, 0, st_>>>(
+          fcpart_.as<double2>(), cvec_.as<C>(), fcsplit_, knbl, done, fnbl_, NB, fb0_);
+    });
+  }
+
+  void apply_freq(const C* v, C* out, const int* done) {
+    correlate_freq(v, done);
+    mask_crop(2, done);  // crops of the local-bin inverse DFTs, summed over ranks
+    launch(kFamMask, [&] { launch_filters(K_, st_, dd_.as<double>(), mh_, mw_, phat_.as<C>(), dtw_.as<C>()); });
+    launch(kFamContract, [&] {
+      contract_out<R, TBV><<<dim3(ftiles_, fntot_), TBV, 0, st_>>>(
+          zf_.as<C>(), phat_.as<C>() + fb0_, dwk_.as<double>(), live_.as<int>(), v, out, fpart_.as<double>(), fntot_,
+          K_, fnbl_, Wh, 0, done, nullptr, nullptr, 0.0, fb0_, NB);
+    });
+  }
+
+  // gamma_solve (learning.cpp:136-185) on the local bins of all images
+  void gamma_solve_freq(double bnorm, int& iters, bool& converged) {
+    iters = 0;
+    converged = false;
+    const size_t total = (size_t)fntot_ * fnbl_;
+    const unsigned vb = (unsigned)((total + TBV - 1) / TBV);
+    if (bnorm == 0.0) {
+      CK(cudaMemsetAsync(gf_.p, 0, gf_.bytes, st_));
+      converged = true;
+      return;
+    }
+    CgState init{};
+    init.bnorm = bnorm;
+    init.tol = cfg_.cg_tol;
+    init.max_iters = cfg_.cg_max;
+    CK(cudaMemcpyAsync(cg_.p, &init, sizeof(CgState), cudaMemcpyHostToDevice, st_));
+    apply_freq(gf_.as<C>(), apf_.as<C>(), nullptr);
+    launch(kFamOther, [&] {
+      cg_init<R, TBV><<<vb, TBV, 0, st_>>>(xf_.as<C>(), apf_.as<C>(), rf_.as<C>(), pf_.as<C>(),
+                                            fpart_.as<double>(), total, fnbl_, Wh, fb0_);
+    });
+    const double invD = 1.0 / D;
+    cg_step(fpart_.as<double>(), (int)vb, invD, 0);
+    const int* done = &cg_.as<CgState>()->done;
+    CgState s = read_cg();
+    int issued = 0, chunk = 2;
+    while (!s.done && issued < cfg_.cg_max) {
+      const int n = std::min(chunk, cfg_.cg_max - issued);
+      for (int c = 0; c < n; ++c) {
+        apply_freq(pf_.as<C>(), apf_.as<C>(), done);
+        cg_step(fpart_.as<double>(), fntot_ * ftiles_, invD, 1);
+        launch(kFamOther, [&] {
+          cg_update<R, TBV><<<vb, TBV, 0, st_>>>(gf_.as<C>(), rf_.as<C>(), pf_.as<C>(), apf_.as<C>(),
+                                                  cg_.as<CgState>(), fpart_.as<double>(), total, fnbl_, Wh, nullptr,
+                                                  invD, fb0_);
+        });
+        cg_step(fpart_.as<double>(), (int)vb, invD, 2);
+        launch(kFamOther, [&] {
+          cg_pupdate<R, TBV><<<vb, TBV, 0, st_>>>(rf_.as<C>(), pf_.as<C>(), cg_.as<CgState>(), total);
+        });
+      }
+      issued += n;
+      chunk = std::min(chunk * 2, 8);
+      s = read_cg();
+    }
+    iters = s.iters;
+    converged = s.converged != 0;
+  }
+
+  // solve_learning (learning.cpp:227-355), frequency-sharded (J = 1)
+  void learning_freq(double* d_out, dcsc_learning_stats* st) {
+    dcsc_learning_stats ls{};
+    if ((int)mu_.size() != K_) mu_.assign(K_, 1.0);
+    freq_operands();
+    CK(cudaMemsetAsync(cvec_.p, 0, cvec_.bytes, st_));  // bins outside [b0, b0 + nbl) stay zero
+    int n_live = 0;
+    for (int k = 0; k < K_; ++k) n_live += live_h_[k] ? 1 : 0;
+    ls.n_dead = K_ - n_live;
+    if (n_live == 0) {  // learning.cpp:258-270
+      ls.degenerate = 1;
+      CK(cudaMemsetAsync(gf_.p, 0, gf_.bytes, st_));
+      CK(cudaStreamSynchronize(st_));
+      std::fill(d_out, d_out + (size_t)K_ * M_, 0.0);
+      if (st) *st = ls;
+      return;
+    }
+    double bnorm = 0.0;
+    for (int n = 0; n < N_; ++n) bnorm += xnorm2c_[n];
+    reduce_host(&bnorm, 1);
+    bnorm = std::sqrt(bnorm);
+    std::vector<double> part, norms(K_, 0.0);
+    bool clamped = false;
+    for (int iter = 1; iter <= cfg_.max_mu_iters; ++iter) {
+      clamped = false;
+      for (int k = 0; k < K_; ++k)
+        if (mu_[k] < cfg_.mu_floor) {
+          mu_[k] = cfg_.mu_floor;
+          clamped = true;
+        }
+      upload_mu();
+      int cg_iters = 0;
+      bool cg_conv = false;
+      gamma_solve_freq(bnorm, cg_iters, cg_conv);
+      if (!cg_conv) ls.cg_budget_hit = 1;
+      ls.cg_iters += cg_iters;
+      if (iter == 1) ls.cg_iters_first = cg_iters;
+      correlate_freq(gf_.as<C>(), nullptr);  // d_recover (learning.cpp:187-216)
+      mask_crop(1, nullptr);
+      part.resize((size_t)K_ * M_);
+      CK(cudaMemcpyAsync(part.data(), dd_.p, sizeof(double) * K_ * M_, cudaMemcpyDeviceToHost, st_));
+      CK(cudaStreamSynchronize(st_));
+      for (int k = 0; k < K_; ++k) {
+        double sq = 0.0;
+        for (int i = 0; i < M_; ++i) sq += part[(size_t)k * M_ + i] * part[(size_t)k * M_ + i];
+        norms[k] = std::sqrt(sq);
+      }
+      ls.mu_iters = iter;
+      bool settled = true;
+      for (int k = 0; k < K_; ++k) {
+        const bool at_boundary = std::abs(norms[k] - 1.0) <= kFilterNormTol;
+        const bool inactive = mu_[k] <= cfg_.mu_floor * (1.0 + 1e-9) && norms[k] < 1.0;
+        if (!at_boundary && !inactive) {
+          settled = false;
+          break;
+        }
+      }
+      if (settled) {
+        ls.converged = 1;
+        break;
+      }
+      if (iter < cfg_.max_mu_iters)
+        for (int k = 0; k < K_; ++k) mu_[k] = std::max(mu_[k] * norms[k], cfg_.mu_floor);
+    }
+    ls.mu_clamped = clamped ? 1 : 0;
+    for (int k = 0; k < K_; ++k) {
+      double scale = 1.0;
+      if (norms[k] > 1.0) {
+        scale = 1.0 / norms[k];
+        ++ls.rescaled_filters;
+      }
+      for (int i = 0; i < M_; ++i) d_out[(size_t)k * M_ + i] = scale * part[(size_t)k * M_ + i];
+    }
+    if (st) *st = ls;
+  }
+
+  // per-image learning data terms (objective.cpp:83-95) of this rank's images
+  void data_terms_freq(const double* d, std::vector<double>& data) {
+    freq_operands();
+    upload_dict_spectra(d, dcand_.as<C>());
+    launch(kFamContract, [&] {
+      contract_out<R, TBV><<<dim3(ftiles_, fntot_), TBV, 0, st_>>>(
+          zf_.as<C>(), dcand_.as<C>() + fb0_, dwk_.as<double>(), live_.as<int>(), xf_.as<C>(), nullptr,
+          fpart_.as<double>(), fntot_, K_, fnbl_, Wh, 1, nullptr, nullptr, nullptr, 0.0, fb0_, NB);
+    });
+    launch(kFamOther, [&] {
+      per_image_reduce<<<fntot_, 256, 0, st_>>>(fpart_.as<double>(), ftiles_, 0.5 / D, fodata_.as<double>());
+    });
+    red_->allreduce(fodata_.as<double>(), fntot_, st_);
+    std::vector<double> all(fntot_);
+    CK(cudaMemcpyAsync(all.data(), fodata_.p, sizeof(double) * fntot_, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    data.assign(all.begin() + fnoff_, all.begin() + fnoff_ + N_);
   }
 
   // accept-only-descent for the coding half-step (pipeline.cpp:231-247)
@@ -1686,6 +1956,11 @@ class Engine final : public EngineBase {
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
       partial_, partial2_, l0_, zhat_, cpart_, hred_, ginv_, what_, cgcnt_, dhat_rb_, theta0_;
   std::vector<char> t0_pending_;  // per image: theta0_ holds a not ADMM-consistent warm theta
+  // frequency-sharded learning (set_learning_layout)
+  bool freq_ = false, zf_valid_ = false, xf_valid_ = false;
+  int fb0_ = 0, fnbl_ = 0, fntot_ = 0, fnoff_ = 0, ftiles_ = 0, fcsplit_ = 1;
+  std::vector<long> fn_rank_;
+  DevMem zf_, xf_, gf_, rf_, pf_, apf_, fsend_, fpart_, fodata_, fcpart_;
   bool use_theta0_ = false;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   std::vector<int> degen_;  // per image: normalisation met a constant input

@@ -24,9 +24,11 @@ struct InvErr : std::runtime_error { using std::runtime_error::runtime_error; };
     if (e_ != cudaSuccess) throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));     \
   } while (0)
 
-// Learning is image-sharded like coding (no z_hat all-to-all): the K x M
-// cropped correlations (each rank crops its own partial), the CG scalars and
-// the trace sums are all-reduced.
+// Learning is image-sharded like coding by default (no z_hat all-to-all): the
+// K x M cropped correlations (each rank crops its own partial), the CG scalars
+// and the trace sums are all-reduced. The frequency-sharded layout
+// (set_learning_layout(1)) moves z_hat and x_hat to frequency-major blocks by
+// one all-to-all per outer iteration and keeps the crop all-reduce.
 // NCCL is dlopen'ed (libnccl.so.2) so a process that already loaded torch's
 // NCCL shares it; the host-callback reducer lets ranks that share one GPU be
 // tested with host-side (gloo) reductions.
@@ -37,6 +39,11 @@ struct Reducer {
   bool forced = false;
   virtual ~Reducer() = default;
   virtual void allreduce(double* dev, size_t n, cudaStream_t st) = 0;  // in-place sum
+  // all-to-all of device byte blocks: `send` holds `world` consecutive blocks
+  // (block q -> rank q, sbytes[q]); `recv` gets `world` consecutive blocks
+  // (from rank q, rbytes[q]). Sizes are multiples of 8 bytes.
+  virtual void alltoall(const void* send, const size_t* sbytes, void* recv, const size_t* rbytes,
+                        cudaStream_t st) = 0;
 };
 
 // ---------------------------------------------------------------- interface
@@ -70,6 +77,7 @@ class EngineBase {
   virtual void run_begin() = 0;
   virtual int run_step(dcsc_trace_row* rows) = 0;
   virtual void run_accepts(int* image_accept, int* dict_accept) = 0;
+  virtual void set_learning_layout(int freq) = 0;
   virtual void synchronize() = 0;
   virtual void set_profiling(int on) = 0;
   virtual void kernel_time(int fam, double* ms, long long* n) = 0;

@@ -797,6 +797,40 @@ __global__ void contract_c_reduce(const double2* __restrict__ cpart, cx<R>* __re
   c[i] = mk<cx<R>>(R(ar), R(ai));
 }
 
+// frequency-sharded learning: the local-bin correlations (K x NBL) into the
+// full K x NBF spectra at bin offset b0 (the other bins stay zero)
+template <class R>
+__global__ void contract_c_reduce_off(const double2* __restrict__ cpart, cx<R>* __restrict__ c, int splits,
+                                      size_t KNBL, const int* done, int NBL, int NBF, int b0) {
+  if (done && *done) return;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= KNBL) return;
+  double ar = 0.0, ai = 0.0;
+  for (int s = 0; s < splits; ++s) {
+    const double2 p = cpart[(size_t)s * KNBL + i];
+    ar += p.x;
+    ai += p.y;
+  }
+  const size_t k = i / NBL, b = i % NBL;
+  c[k * NBF + b0 + b] = mk<cx<R>>(R(ar), R(ai));
+}
+
+// image-major spectra src [planes][NB] -> per-destination blocks for the
+// frequency all-to-all: bins [b0_q, b0_q + nbl_q) of every plane go to block q
+// (offset planes * b0_q, layout [planes][nbl_q]); b0_q = q NB / world
+template <class C>
+__global__ void pack_bins(const C* __restrict__ src, C* __restrict__ dst, size_t planes, int NB, int world) {
+  const size_t total = planes * (size_t)NB;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t p = i / NB;
+    const int b = (int)(i % NB);
+    int q = world - 1;
+    while ((long)q * NB / world > b) --q;
+    const int b0 = (int)((long)q * NB / world), nbl = (int)((long)(q + 1) * NB / world) - b0;
+    dst[planes * (size_t)b0 + p * (size_t)nbl + (b - b0)] = src[i];
+  }
+}
+
 // single-block fixed-order sum of block partials into out[0]
 static __global__ void sum_partials(const double* partial, int count, double* out) {
   __shared__ double red[32];
@@ -894,7 +928,9 @@ __global__ void __launch_bounds__(TB)
 contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const double* __restrict__ wk,
              const int* __restrict__ live, const cx<R>* __restrict__ v, cx<R>* __restrict__ out,
              double* __restrict__ partial, int N, int K, int NB, int Wh, int mode, const int* done,
-             CgState* cgst = nullptr, unsigned* cnt = nullptr, double invD = 0.0) {
+             CgState* cgst = nullptr, unsigned* cnt = nullptr, double invD = 0.0, int b0 = 0, int pstride = 0) {
+  // b0 / pstride (frequency-sharded learning): the NB bins are [b0, b0 + NB)
+  // of the full half spectrum, p points at bin b0 of K spectra pstride apart
   using C = cx<R>;
   __shared__ double red[TB / 32];
   if (done && *done) return;
@@ -920,6 +956,7 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
       ar[i] = ai[i] = 0.0;
     }
     const C* pp = p + b;
+    const size_t PS = pstride ? (size_t)pstride : (size_t)NB;
     constexpr int U = 8;
     int k = 0;
     for (; k + U <= K; k += U) {
@@ -928,7 +965,7 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
       for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int i = 0; i < NI; ++i) z[i][u] = __ldcs(zp[i] + (size_t)(k + u) * NB);  // streaming: keep p_hat in L2
-        q[u] = __ldg(pp + (size_t)(k + u) * NB);
+        q[u] = __ldg(pp + (size_t)(k + u) * PS);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -941,7 +978,7 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
       }
     }
     for (; k < K; ++k) {
-      const C q = __ldg(pp + (size_t)k * NB);
+      const C q = __ldg(pp + (size_t)k * PS);
       const double w = mode == 0 ? wk[k] : 1.0;
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
@@ -959,10 +996,10 @@ contract_out(const cx<R>* __restrict__ zhat, const cx<R>* __restrict__ p, const 
       if (mode == 0) {
         const C o = mk<C>(R((double)vv.x + ar[i]), R((double)vv.y + ai[i]));
         out[o_n] = o;
-        dot += bin_weight(b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
+        dot += bin_weight(b0 + b, Wh) * ((double)vv.x * (double)o.x + (double)vv.y * (double)o.y);
       } else {
         const double rr = ar[i] - (double)vv.x, ri = ai[i] - (double)vv.y;
-        dot += bin_weight(b, Wh) * (rr * rr + ri * ri);
+        dot += bin_weight(b0 + b, Wh) * (rr * rr + ri * ri);
       }
     }
   }
@@ -1003,7 +1040,7 @@ __device__ __forceinline__ void block_partial(double v, double* out_slot) {
 template <class R, int TB>
 __global__ void __launch_bounds__(TB)
 cg_init(const cx<R>* __restrict__ xhat, const cx<R>* __restrict__ ap, cx<R>* __restrict__ r,
-        cx<R>* __restrict__ p, double* partial, size_t total, int NB, int Wh) {
+        cx<R>* __restrict__ p, double* partial, size_t total, int NB, int Wh, int b0 = 0) {
   using C = cx<R>;
   const size_t i = (size_t)blockIdx.x * TB + threadIdx.x;
   double v = 0.0;
@@ -1012,7 +1049,7 @@ cg_init(const cx<R>* __restrict__ xhat, const cx<R>* __restrict__ ap, cx<R>* __r
     const C rv = mk<C>(-x.x - a.x, -x.y - a.y);
     r[i] = rv;
     p[i] = rv;
-    v = bin_weight((int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
+    v = bin_weight(b0 + (int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
   }
   block_partial<TB>(v, partial + blockIdx.x);
 }
@@ -1026,7 +1063,7 @@ template <class R, int TB>
 __global__ void __launch_bounds__(TB)
 cg_update(cx<R>* __restrict__ gam, cx<R>* __restrict__ r, const cx<R>* __restrict__ p,
           const cx<R>* __restrict__ ap, CgState* st, double* partial, size_t total, int NB,
-          int Wh, unsigned* cnt = nullptr, double invD = 0.0) {
+          int Wh, unsigned* cnt = nullptr, double invD = 0.0, int b0 = 0) {
   using C = cx<R>;
   if (st->done) return;
   double v = 0.0;
@@ -1036,7 +1073,7 @@ cg_update(cx<R>* __restrict__ gam, cx<R>* __restrict__ r, const cx<R>* __restric
     gam[i] = mk<C>(R(gv.x + al * pv.x), R(gv.y + al * pv.y));
     const C rv = mk<C>(R(rv0.x - al * av.x), R(rv0.y - al * av.y));
     r[i] = rv;
-    v += bin_weight((int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
+    v += bin_weight(b0 + (int)(i % (size_t)NB), Wh) * ((double)rv.x * rv.x + (double)rv.y * rv.y);
   }
   block_partial<TB>(v, partial + blockIdx.x);
   // single-rank CG: the last block turns the rr partials into beta / stop

@@ -140,6 +140,7 @@ EXPORTS = [
     "dcsc_synth_dataset", "dcsc_synth_generate_range", "dcsc_cuda_learning_correlation",
     "dcsc_cuda_dictionary_adjoint", "dcsc_cuda_lambda_update", "dcsc_cuda_gamma_solve", "dcsc_cuda_d_recover",
     "dcsc_cuda_run_begin", "dcsc_cuda_run_step", "dcsc_cuda_run_accepts", "dcsc_cuda_signal_flags",
+    "dcsc_cuda_set_learning_layout",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -428,6 +429,10 @@ class Context:
         _err(lib().dcsc_cuda_set_comm_callback(self._h, world, rank, self._cb, None))
 
     # -- measurement
+    def set_learning_layout(self, layout: str):
+        """'image' (default) or 'freq': frequency-sharded learning across ranks (after set_comm_*)."""
+        _err(lib().dcsc_cuda_set_learning_layout(self._h, {"image": 0, "freq": 1}[layout]))
+
     def synchronize(self):
         _err(lib().dcsc_cuda_synchronize(self._h))
 

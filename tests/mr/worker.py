@@ -32,12 +32,15 @@ def main():
         dist.destroy_process_group()
         return
     N, grid, K, m = 4, (20, 20), 6, 5
-    J = 2 if os.environ.get("MR_MODE") == "gpu_j" else 1
+    mode = os.environ.get("MR_MODE")
+    J = 2 if mode == "gpu_j" else 1
     x = mr_signals(dcsc, N, grid, K, m, J)
     n0, n1 = dcsc.shard_range(N, world, rank)
     cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
     with dcsc.Context(n1 - n0, grid, K, (m, m), cfg, 64, channels=J) as ctx:
         ctx.set_comm_callback(world, rank, dcsc.gloo_allreduce_fn())
+        if mode == "gpu_freq":  # frequency-sharded learning (one z_hat all-to-all per outer iteration)
+            ctx.set_learning_layout("freq")
         ctx.set_signals(x[n0:n1])
         trace, _ = ctx.run(cfg.max_outer)
         keys = ["total", "data_term", "l1_term", "admm_iters", "cg_iters", "mu_iters", "l0"]

@@ -138,3 +138,59 @@ print(json.dumps(out))
     assert cp == cn
     assert max(abs(a - b) / abs(b) for a, b in zip(tn, tp)) <= 1e-10
     assert np.abs(np.array(dn) - np.array(dp)).max() <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_frequency_sharded_learning_matches_single_rank(tmp_path, world):
+    """Frequency-sharded learning (BASELINE.json north_star): ranks own
+    contiguous bin ranges of every image's spectra after the z_hat / x_hat
+    all-to-all (here through the gloo callback, ranks sharing one GPU; 3 ranks:
+    uneven image and bin splits); the run equals the single-rank run (FP64)."""
+    res = launch(world, "gpu_freq", tmp_path)
+    N, grid, K, m = 4, (20, 20), 6, 5
+    x, _ = dcsc.synth_generate(N, grid, K, m, 0.05, 0.01, 7, False)
+    cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
+    one = dcsc.run_csc(x, K, (m, m), cfg, precision=64)
+    keys = ["total", "data_term", "l1_term", "admm_iters", "cg_iters", "mu_iters", "l0"]
+    single = np.array([[r[k] for k in keys] for r in one["trace"]], dtype=np.float64)
+    for r in res:
+        t = r["trace"]
+        assert t.shape == single.shape
+        assert np.all(np.abs(t[:, :3] - single[:, :3]) <= 1e-9 * np.abs(single[:, :3]))
+        assert np.array_equal(t[:, 3], single[:, 3]) and np.array_equal(t[:, 5], single[:, 5])
+        assert np.all(np.abs(t[:, 4] - single[:, 4]) <= 2)
+        assert np.abs(r["dict"] - one["dict"]).max() <= 1e-8 * np.abs(one["dict"]).max()
+
+
+@pytest.mark.gpu
+def test_nccl_frequency_sharded_one_rank_matches_single_rank():
+    """The NCCL all-to-all (grouped ncclSend / ncclRecv to itself) and the
+    frequency-sharded learning code path on a forced 1-rank communicator."""
+    code = r'''
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.getcwd())
+from paper_1709_09479_b200 import dcsc
+x, _ = dcsc.synth_generate(3, (20, 20), 5, 5, 0.05, 0.01, 17, False)
+cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=4, tol=1e-300)
+out = {}
+for mode in ("plain", "freq"):
+    with dcsc.Context(3, (20, 20), 5, (5, 5), cfg, 64) as ctx:
+        if mode == "freq":
+            ctx.set_comm_nccl(1, 0, dcsc.nccl_unique_id())
+            ctx.set_learning_layout("freq")
+        ctx.set_signals(x)
+        rows, _ = ctx.run(3)
+        out[mode] = ([r["total"] for r in rows], [r["cg_iters"] for r in rows], ctx.get_dictionary().tolist())
+print(json.dumps(out))
+'''
+    env = dict(os.environ, DCSC_FORCE_MULTI="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    import json
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    (tp, cp, dp), (tn, cn, dn) = out["plain"], out["freq"]
+    assert cp == cn
+    assert max(abs(a - b) / abs(b) for a, b in zip(tn, tp)) <= 1e-10
+    assert np.abs(np.array(dn) - np.array(dp)).max() <= 1e-9
