@@ -220,20 +220,51 @@ class Engine final : public EngineBase {
         coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
     }
   }
+  // persistent pipelined r2c / c2r (SmemPipe) when the staging buffer fits and
+  // the planes are 16-byte aligned storage-precision planes: grid = resident slots
+  static int pipe_grid(const void* fn, size_t smem, int count) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, T, smem) != cudaSuccess || per < 1) per = 1;
+    cudaGetLastError();
+    return std::max(1, std::min(count, sms * per));
+  }
+  static bool aligned16(const void* p, size_t stride_bytes) {
+    return (reinterpret_cast<uintptr_t>(p) % 16) == 0 && stride_bytes % 16 == 0;
+  }
   template <class SRC>
   static void launch_r2c(int count, cudaStream_t st, const SRC* src, size_t ss, C* dst, size_t ds, const C* tw,
                          int* live, int live_mod) {
-    if constexpr (CLU)
+    if constexpr (CLU) {
       r2c_planes_cl<P, SRC><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
-    else
+    } else {
+      if constexpr (std::is_same<SRC, R>::value && SmemPipe<P>::r2c_ok) {
+        if (!std::getenv("DCSC_NO_FFT_PIPE") && aligned16(src, ss * sizeof(R))) {
+          constexpr size_t sm = SmemPipe<P>::r2c;
+          const int g = pipe_grid((const void*)r2c_planes_pipe<P>, sm, count);
+          r2c_planes_pipe<P><<<g, T, sm, st>>>(src, ss, dst, ds, tw, live, live_mod, count);
+          return;
+        }
+      }
       r2c_planes<P, SRC><<<count, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
+    }
   }
   template <class DST>
   static void launch_c2r(int count, cudaStream_t st, const C* src, size_t ss, DST* dst, size_t ds, const C* tw) {
-    if constexpr (CLU)
+    if constexpr (CLU) {
       c2r_planes_cl<P, DST><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
-    else
+    } else {
+      if constexpr (std::is_same<DST, R>::value && SmemPipe<P>::c2r_ok) {
+        if (!std::getenv("DCSC_NO_FFT_PIPE") && aligned16(src, ss * sizeof(C)) && aligned16(dst, ds * sizeof(R))) {
+          constexpr size_t sm = SmemPipe<P>::c2r;
+          const int g = pipe_grid((const void*)c2r_planes_pipe<P>, sm, count);
+          c2r_planes_pipe<P><<<g, T, sm, st>>>(src, ss, dst, ds, tw, count);
+          return;
+        }
+      }
       c2r_planes<P, DST><<<count, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
+    }
   }
   static void launch_filters(int K, cudaStream_t st, const double* d, int mh, int mw, C* dst, const C* tw) {
     if constexpr (CLU)
@@ -281,6 +312,8 @@ class Engine final : public EngineBase {
       big((const void*)c2r_planes<P, double>, smem_plain());
       big((const void*)r2c_filters<P>, smem_plain());
       big((const void*)mask_step<P>, smem_plain());
+      if constexpr (SmemPipe<P>::r2c_ok) big((const void*)r2c_planes_pipe<P>, SmemPipe<P>::r2c);
+      if constexpr (SmemPipe<P>::c2r_ok) big((const void*)c2r_planes_pipe<P>, SmemPipe<P>::c2r);
     }
   }
 

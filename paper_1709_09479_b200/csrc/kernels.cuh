@@ -603,6 +603,125 @@ r2c_planes(const SRC* __restrict__ src, size_t src_stride, cx<typename P::R>* __
   forward_to_global<P>(B0, B1, TW, COL0, dst + (size_t)p * dst_stride);
 }
 
+// Persistent, pipelined batched transforms: one CTA per SM slot walks planes
+// p = blockIdx.x, + gridDim.x, ...; the next plane's input streams into a
+// staging buffer by one TMA bulk copy while the current plane transforms, so
+// the HBM read overlaps the FFT instead of preceding it (the one-CTA-per-plane
+// kernels above serialise load -> FFT -> store on each SM).
+template <class P>
+struct SmemPipe {
+  using R = typename P::R;
+  using C = typename P::C;
+  static constexpr size_t stg_off = (Smem<P>::two + 127) / 128 * 128;
+  static constexpr size_t r2c = stg_off + sizeof(R) * P::D;   // + real plane
+  static constexpr size_t c2r = stg_off + sizeof(C) * P::NB;  // + half spectrum
+  static constexpr bool r2c_ok = r2c <= 220 * 1024 && (sizeof(R) * P::D) % 16 == 0;
+  static constexpr bool c2r_ok = c2r <= 220 * 1024 && (sizeof(C) * P::NB) % 16 == 0;
+};
+
+template <class P>
+__global__ void __launch_bounds__(P::T)
+r2c_planes_pipe(const typename P::R* __restrict__ src, size_t src_stride, cx<typename P::R>* __restrict__ dst,
+                size_t dst_stride, const cx<typename P::R>* tw, int* live_flags, int live_mod, int count) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, Wh = P::Wh, NB = P::NB, T = P::T, M = P::M;
+  constexpr unsigned BYTES = sizeof(R) * P::D;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar_s;
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB;
+  C* COL0 = TW + P::TW_LEN;
+  const C* STG = reinterpret_cast<const C*>(smem_raw + SmemPipe<P>::stg_off);
+  unsigned long long* bar = &bar_s;
+  P::load_twiddles(TW, tw);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_async_smem();
+  }
+  __syncthreads();
+  int p = blockIdx.x;
+  if (threadIdx.x == 0 && p < count) {
+    mbar_expect_tx(bar, BYTES);
+    bulk_g2s((void*)STG, src + (size_t)p * src_stride, BYTES, bar);
+  }
+  unsigned phase = 0;
+  for (; p < count; p += gridDim.x) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    int any = 0;
+    for (int it = threadIdx.x; it < H * M; it += T) {  // pixel pairs -> [H][Wh]
+      const C v = STG[it];
+      any |= (v.x != R(0)) | (v.y != R(0));
+      B0[(it / M) * Wh + it % M] = v;
+    }
+    if (live_flags) {
+      any = __syncthreads_or(any);
+      if (threadIdx.x == 0 && any) atomicOr(live_flags + (p % live_mod), 1);
+    } else {
+      __syncthreads();
+    }
+    const int nx = p + gridDim.x;
+    if (threadIdx.x == 0 && nx < count) {  // staging consumed: the next plane streams in
+      fence_async_smem();
+      mbar_expect_tx(bar, BYTES);
+      bulk_g2s((void*)STG, src + (size_t)nx * src_stride, BYTES, bar);
+    }
+    forward_to_global<P>(B0, B1, TW, COL0, dst + (size_t)p * dst_stride);
+    __syncthreads();
+  }
+}
+
+template <class P>
+__global__ void __launch_bounds__(P::T)
+c2r_planes_pipe(const cx<typename P::R>* __restrict__ src, size_t src_stride, typename P::R* __restrict__ dst,
+                size_t dst_stride, const cx<typename P::R>* tw, int count) {
+  using R = typename P::R;
+  using C = typename P::C;
+  constexpr int H = P::H, Wh = P::Wh, NB = P::NB, T = P::T, D = P::D, M = P::M;
+  constexpr unsigned BYTES = sizeof(C) * NB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long bar_s;
+  C* B0 = reinterpret_cast<C*>(smem_raw);
+  C* B1 = B0 + NB;
+  C* TW = B1 + NB;
+  C* STG = reinterpret_cast<C*>(smem_raw + SmemPipe<P>::stg_off);
+  unsigned long long* bar = &bar_s;
+  P::load_twiddles(TW, tw);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_async_smem();
+  }
+  __syncthreads();
+  int p = blockIdx.x;
+  if (threadIdx.x == 0 && p < count) {
+    mbar_expect_tx(bar, BYTES);
+    bulk_g2s(STG, src + (size_t)p * src_stride, BYTES, bar);
+  }
+  unsigned phase = 0;
+  const R sc = R(1.0 / (double)D);
+  for (; p < count; p += gridDim.x) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    // the first column stage reads the staged spectrum; cols_inv syncs after it
+    C* c = P::template cols_inv<false>(B0, B1, TW, [&](int r, int cc) { return STG[r * Wh + cc]; });
+    const int nx = p + gridDim.x;
+    if (threadIdx.x == 0 && nx < count) {  // staging consumed: the next spectrum streams in
+      fence_async_smem();
+      mbar_expect_tx(bar, BYTES);
+      bulk_g2s(STG, src + (size_t)nx * src_stride, BYTES, bar);
+    }
+    C* sp = P::rows_inv(c, c == B0 ? B1 : B0, TW);
+    C* o = reinterpret_cast<C*>(dst + (size_t)p * dst_stride);
+    for (int it = threadIdx.x; it < H * M; it += T) {
+      const C v = sp[(it / M) * Wh + it % M];
+      o[it] = mk<C>(v.x * sc, v.y * sc);
+    }
+    __syncthreads();
+  }
+}
+
 // Zero-padded filters (corner placement, spectral.cpp:106-122) -> spectra.
 template <class P>
 __global__ void __launch_bounds__(P::T)
