@@ -158,6 +158,13 @@ void normalize_image(int mode, int H, int W, const double* in, double* out, int 
 constexpr int pick_threads(int H, int W) {
   return H * W == 128 * 128 ? DCSC_T128 : (H * W >= 100 * 100 ? 512 : (H * W >= 64 * 64 ? 256 : 128));
 }
+#ifndef DCSC_T100D
+#define DCSC_T100D 512  // threads per CTA of the FP64 100x100 family (experiment knob)
+#endif
+template <class R>
+constexpr int pick_threads_r(int H, int W) {
+  return (sizeof(R) == 8 && H * W == 100 * 100) ? DCSC_T100D : pick_threads(H, W);
+}
 
 // Kernel family per compiled grid: one CTA per plane (Plane), or a 4-CTA
 // cluster per plane (ClusterPlane) when the half spectrum exceeds smem.
@@ -165,7 +172,7 @@ template <class R, int H, int W>
 struct KernelFamily {
   static constexpr bool cluster = false;
   static constexpr int CL = 1;
-  using P = Plane<R, H, W, pick_threads(H, W)>;
+  using P = Plane<R, H, W, pick_threads_r<R>(H, W)>;
 };
 template <>
 struct KernelFamily<double, 128, 128> {  // FP64 128x128: 133 KB per plane buffer
