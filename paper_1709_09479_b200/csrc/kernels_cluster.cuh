@@ -199,7 +199,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   const bool DST = ADMM && a.dhat_rb != nullptr;
   const int k0s = (int)(blockIdx.x / CL) * a.kpg;
   // rank 0's packed generator column P(r) = t(r, 0) + i t(r, W/2), t = conj(d) lambda:
-  // one warp pre-packs conj(P) into the staged d_hat slot 0 per filter, and the
+  // rank 0 pre-packs conj(P) into the staged d_hat slot 0 per filter, and the
   // generator multiplies it by a lambda of ones, so no lane issues partner loads
   C* LAMC = reinterpret_cast<C*>(smem_raw + SM::lamc_off);
   if (DST && rank == 0 && threadIdx.x < H) {
@@ -255,11 +255,9 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         dphase ^= 1u;
         CLT(12)
         if (rank == 0) {
-          if (threadIdx.x < 32) {
-            for (int r = threadIdx.x; r < H; r += 32) {
-              const C p0 = cmulc(Y[r * CS], LAMC[r]), pm = cmulc(Y[r * CS + COLS], LAMC[H + r]);
-              Y[r * CS] = cconj(CP::pack_col0(p0, pm));
-            }
+          for (int r = threadIdx.x; r < H; r += T) {  // one row per thread
+            const C p0 = cmulc(Y[r * CS], LAMC[r]), pm = cmulc(Y[r * CS + COLS], LAMC[H + r]);
+            Y[r * CS] = cconj(CP::pack_col0(p0, pm));
           }
           __syncthreads();
         }
