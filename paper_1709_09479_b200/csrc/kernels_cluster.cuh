@@ -90,6 +90,27 @@ __device__ __forceinline__ void cl_issue_exchange(const typename CP::C* snd, typ
   }
 }
 
+// Exchange I in two row halves (rows [0, ROWS/2) of every block first, on
+// barA; the rest on barB), all first halves issued before any second half, so
+// the receiver's first inverse row stage starts on its first-half rows while
+// the second halves are in flight.
+template <class CP>
+__device__ __forceinline__ void cl_issue_exchange_split(const typename CP::C* snd, typename CP::C* stg,
+                                                        unsigned rank, unsigned long long* barA,
+                                                        unsigned long long* barB) {
+  constexpr int HALF = (CP::ROWS / 2) * CP::CS;
+  constexpr unsigned HB = sizeof(typename CP::C) * HALF;
+  static_assert(HB % 16 == 0, "bulk copies move multiples of 16 bytes");
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(barA, (CP::CL - 1) * HB);
+    mbar_expect_tx(barB, (CP::CL - 1) * HB);
+    for (unsigned q = 0; q < (unsigned)CP::CL; ++q)
+      if (q != rank) bulk_s2peer(stg + rank * CP::BLOCK, q, snd + q * CP::BLOCK, HB, barA);
+    for (unsigned q = 0; q < (unsigned)CP::CL; ++q)
+      if (q != rank) bulk_s2peer(stg + rank * CP::BLOCK + HALF, q, snd + q * CP::BLOCK + HALF, HB, barB);
+  }
+}
+
 // Fully synchronised exchange (single-plane helper kernels).
 template <class CP>
 __device__ __forceinline__ void cl_exchange_sync(const typename CP::C* snd, typename CP::C* stg, unsigned rank,
@@ -152,6 +173,10 @@ __global__ void cl_rank_block(const cx<typename CP::R>* __restrict__ dhat, cx<ty
 #define DCSC_CL_USTAGE 0  // u row block staged in smem by TMA (load during the last inverse row stage, store
                           // after the prox); A/B 1.229 vs 1.218 ms per c3s launch (the tight B_I wait costs the gain)
 #endif
+#ifndef DCSC_CL_XI_SPLIT
+#define DCSC_CL_XI_SPLIT 0  // exchange I in two row halves (first inverse row stage starts on the first half);
+                            // A/B 1.238 vs 1.205 ms per c3s launch (more copies, more spills): off
+#endif
 #ifndef DCSC_CL_PROX_UNROLL
 #define DCSC_CL_PROX_UNROLL 16
 #endif
@@ -208,6 +233,14 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     LAMC[H + threadIdx.x] = lamn[threadIdx.x * Wh + M];
   }
   if (DST && threadIdx.x == 0) mbar_init(dbar, 1);
+  __shared__ __align__(8) unsigned long long xbarA_s, xbarB_s;
+  unsigned long long* xbarA = &xbarA_s;
+  unsigned long long* xbarB = &xbarB_s;
+  unsigned xiphase = 0;
+  if (ADMM && DCSC_CL_XI_SPLIT && threadIdx.x == 0) {
+    mbar_init(xbarA, 1);
+    mbar_init(xbarB, 1);
+  }
   if (ADMM && DCSC_CL_USTAGE && threadIdx.x == 0) mbar_init(ubar, 1);
   cl_init_exchange<CP>(xbar);  // (fences the mbarrier inits, syncs the CTA)
   if (DST && threadIdx.x == 0 && k0s < a.K) {
@@ -283,11 +316,18 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       CLT(0)
       cluster_wait();  // B_F (previous filter): peers' Z free
       CLT(1)
+#if DCSC_CL_XI_SPLIT
+      cl_issue_exchange_split<CP>(Y, Z, rank, xbarA, xbarB);
+      CLT(2)
+      CP::rows_inv_first(Z, Y, rank, X, TW, [&](int rl) { mbar_wait(rl < ROWS / 2 ? xbarA : xbarB, xiphase); });
+      xiphase ^= 1u;
+#else
       cl_issue_exchange<CP>(Y, Z, rank, xbar);
       mbar_wait(xbar, xphase);
       CLT(2)
       xphase ^= 1u;
       CP::rows_inv_first(Z, Y, rank, X, TW);
+#endif
       __syncthreads();
       CLT(7)
       cluster_arrive();  // B_I: my Z consumed, my incoming blocks complete
