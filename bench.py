@@ -242,6 +242,7 @@ def ref_unit_costs(cfg, threads):
     x, d = make_data(cfg, 0, n_s, ref.synth_generate)
     if cfg.get("J", 1) > 1:
         raise RuntimeError("reference unit costs are for J = 1 configs")
+    ref.coding_batch(x[: min(2, n_s)], d, ref.Cfg(beta=cfg["beta"], max_admm=1, normalize=0))  # untimed: plans, threads
     tc = {}
     for cap in (1, 3):
         c = ref.Cfg(beta=cfg["beta"], max_admm=cap, normalize=0)
