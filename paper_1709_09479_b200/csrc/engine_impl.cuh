@@ -244,7 +244,20 @@ class Engine final : public EngineBase {
   static void launch_r2c(int count, cudaStream_t st, const SRC* src, size_t ss, C* dst, size_t ds, const C* tw,
                          int* live, int live_mod) {
     if constexpr (CLU) {
-      r2c_planes_cl<P, SRC><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod);
+      // persistent: as many clusters as fit at once, each walking planes
+      static int slots = 0;
+      if (!slots) {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(CLN, 1, 1);
+        lc.blockDim = dim3(T, 1, 1);
+        lc.dynamicSmemBytes = smem_plain();
+        int ncl = 0;
+        slots = (cudaOccupancyMaxActiveClusters(&ncl, (void*)r2c_planes_cl<P, SRC>, &lc) == cudaSuccess && ncl > 0)
+                    ? ncl : 32;
+        cudaGetLastError();
+      }
+      const int g = std::max(1, std::min(count, slots));
+      r2c_planes_cl<P, SRC><<<g * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, live, live_mod, count);
     } else {
       if constexpr (std::is_same<SRC, R>::value && SmemPipe<P>::r2c_ok) {
         if (!std::getenv("DCSC_NO_FFT_PIPE") && aligned16(src, ss * sizeof(R))) {
@@ -260,7 +273,19 @@ class Engine final : public EngineBase {
   template <class DST>
   static void launch_c2r(int count, cudaStream_t st, const C* src, size_t ss, DST* dst, size_t ds, const C* tw) {
     if constexpr (CLU) {
-      c2r_planes_cl<P, DST><<<count * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr);
+      static int slots = 0;
+      if (!slots) {
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(CLN, 1, 1);
+        lc.blockDim = dim3(T, 1, 1);
+        lc.dynamicSmemBytes = smem_plain();
+        int ncl = 0;
+        slots = (cudaOccupancyMaxActiveClusters(&ncl, (void*)c2r_planes_cl<P, DST>, &lc) == cudaSuccess && ncl > 0)
+                    ? ncl : 32;
+        cudaGetLastError();
+      }
+      const int g = std::max(1, std::min(count, slots));
+      c2r_planes_cl<P, DST><<<g * CLN, T, smem_plain(), st>>>(src, ss, dst, ds, tw, nullptr, count);
     } else {
       if constexpr (std::is_same<DST, R>::value && SmemPipe<P>::c2r_ok) {
         if (!std::getenv("DCSC_NO_FFT_PIPE") && aligned16(src, ss * sizeof(C)) && aligned16(dst, ds * sizeof(R))) {

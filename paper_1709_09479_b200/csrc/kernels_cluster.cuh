@@ -673,7 +673,7 @@ __device__ __forceinline__ void cl_inverse(ClBufs<CP>& b, unsigned rank, GEN&& g
 template <class CP, class SRC>
 __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     r2c_planes_cl(const SRC* __restrict__ src, size_t src_stride, cx<typename CP::R>* __restrict__ dst,
-                  size_t dst_stride, const cx<typename CP::R>* tw, int* live_flags, int live_mod) {
+                  size_t dst_stride, const cx<typename CP::R>* tw, int* live_flags, int live_mod, int count) {
   using R = typename CP::R;
   using C = typename CP::C;
   constexpr int W = CP::W, Wh = CP::Wh, T = CP::T, M = CP::M, ROWS = CP::ROWS;
@@ -681,20 +681,36 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   __shared__ __align__(8) unsigned long long bar_s;
   ClBufs<CP> b(smem_raw, &bar_s);
   const unsigned rank = cluster_rank();
-  const int p = blockIdx.x / CP::CL, r0 = rank * ROWS;
+  const int r0 = rank * ROWS;
   CP::load_twiddles(b.TW, tw);
   cl_init_exchange<CP>(b.bar);
-  const SRC* s = src + (size_t)p * src_stride;
-  int any = 0;
-  for (int it = threadIdx.x; it < ROWS * M; it += T) {
-    const int rl = it / M, m = it % M;
-    const R v0 = R(s[(r0 + rl) * W + 2 * m]), v1 = R(s[(r0 + rl) * W + 2 * m + 1]);
-    any |= (v0 != R(0)) | (v1 != R(0));
-    b.Z[rl * Wh + m] = mk<C>(v0, v1);
+  // persistent over planes (grid = resident clusters): the next plane's rows of
+  // this rank are prefetched into L2 while the current plane transforms
+  const int stride = gridDim.x / CP::CL;
+  for (int p = blockIdx.x / CP::CL; p < count; p += stride) {
+    const SRC* s = src + (size_t)p * src_stride + (size_t)r0 * W;
+    if (threadIdx.x == 0 && p + stride < count)
+      prefetch_l2_bulk(src + (size_t)(p + stride) * src_stride + (size_t)r0 * W, sizeof(SRC) * ROWS * W);
+    int any = 0;
+    for (int it = threadIdx.x; it < ROWS * M; it += T) {
+      const int rl = it / M, m = it % M;
+      R v0, v1;
+      if constexpr (std::is_same<SRC, R>::value) {  // pixel pair as one vector load
+        const C v = reinterpret_cast<const C*>(s)[it];
+        v0 = v.x;
+        v1 = v.y;
+      } else {
+        v0 = R(s[rl * W + 2 * m]);
+        v1 = R(s[rl * W + 2 * m + 1]);
+      }
+      any |= (v0 != R(0)) | (v1 != R(0));
+      b.Z[rl * Wh + m] = mk<C>(v0, v1);
+    }
+    any = __syncthreads_or(any);
+    if (live_flags && threadIdx.x == 0 && any) atomicOr(live_flags + (p % live_mod), 1);
+    cl_forward_to_global<CP>(b, rank, dst + (size_t)p * dst_stride);
+    __syncthreads();
   }
-  any = __syncthreads_or(any);
-  if (live_flags && threadIdx.x == 0 && any) atomicOr(live_flags + (p % live_mod), 1);
-  cl_forward_to_global<CP>(b, rank, dst + (size_t)p * dst_stride);
 }
 
 template <class CP>
@@ -726,7 +742,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
 template <class CP, class DST>
 __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     c2r_planes_cl(const cx<typename CP::R>* __restrict__ src, size_t src_stride, DST* __restrict__ dst,
-                  size_t dst_stride, const cx<typename CP::R>* tw, const double* scale) {
+                  size_t dst_stride, const cx<typename CP::R>* tw, const double* scale, int count) {
   using R = typename CP::R;
   using C = typename CP::C;
   constexpr int W = CP::W, Wh = CP::Wh, T = CP::T, M = CP::M, ROWS = CP::ROWS, D = CP::D;
@@ -734,18 +750,30 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   __shared__ __align__(8) unsigned long long bar_s;
   ClBufs<CP> b(smem_raw, &bar_s);
   const unsigned rank = cluster_rank();
-  const int p = blockIdx.x / CP::CL, r0 = rank * ROWS;
+  const int r0 = rank * ROWS;
   CP::load_twiddles(b.TW, tw);
   cl_init_exchange<CP>(b.bar);
-  const C* s = src + (size_t)p * src_stride;
-  cl_inverse<CP>(b, rank, [&](int r, int c) { return s[r * Wh + c]; });
-  const R sc = R((scale ? scale[p] : 1.0) / (double)D);
-  DST* o = dst + (size_t)p * dst_stride;
-  for (int it = threadIdx.x; it < ROWS * M; it += T) {
-    const int rl = it / M, m = it % M;
-    const C v = b.Z[rl * Wh + m];
-    o[(r0 + rl) * W + 2 * m] = DST(v.x * sc);
-    o[(r0 + rl) * W + 2 * m + 1] = DST(v.y * sc);
+  // persistent over planes; each rank prefetches a quarter (its row block) of
+  // the next plane's spectrum into L2 while the current plane transforms
+  const int stride = gridDim.x / CP::CL;
+  for (int p = blockIdx.x / CP::CL; p < count; p += stride) {
+    const C* s = src + (size_t)p * src_stride;
+    if (threadIdx.x == 0 && p + stride < count)
+      prefetch_l2_bulk(src + (size_t)(p + stride) * src_stride + (size_t)r0 * Wh, sizeof(C) * ROWS * Wh);
+    cl_inverse<CP>(b, rank, [&](int r, int c) { return s[r * Wh + c]; });
+    const R sc = R((scale ? scale[p] : 1.0) / (double)D);
+    DST* o = dst + (size_t)p * dst_stride + (size_t)r0 * W;
+    for (int it = threadIdx.x; it < ROWS * M; it += T) {
+      const int rl = it / M, m = it % M;
+      const C v = b.Z[rl * Wh + m];
+      if constexpr (std::is_same<DST, R>::value) {
+        reinterpret_cast<C*>(o)[it] = mk<C>(v.x * sc, v.y * sc);
+      } else {
+        o[rl * W + 2 * m] = DST(v.x * sc);
+        o[rl * W + 2 * m + 1] = DST(v.y * sc);
+      }
+    }
+    __syncthreads();
   }
 }
 
