@@ -154,17 +154,14 @@ struct ClusterPlane {
   // self-mirrored — so every staged element is loaded once.
   // The block of this rank itself is read from its own send buffer `self`
   // (it is not copied).
-  // wait(rl): called by each task before its loads (the split exchange-I hook)
-  template <class WAIT = void (*)(int)>
   __device__ static __forceinline__ void rows_inv_first(const C* stg, const C* self, unsigned rank, C* out,
-                                                        const C* tw, WAIT&& wait = [](int) {}) {
+                                                        const C* tw) {
     using S = Split<RowPlanI>;
     constexpr int R = S::first, J = M / R, TASKS = ROWS * (J / 2);
     static_assert(J % 2 == 0, "paired butterflies");
 #pragma unroll 1
     for (int task = threadIdx.x; task < TASKS; task += T) {
       const int rl = task % ROWS, t = task / ROWS;
-      wait(rl);
       const int ja = t == 0 ? 0 : t, jb = t == 0 ? J / 2 : J - t;
       C a[R], b[R];
 #pragma unroll

@@ -90,27 +90,6 @@ __device__ __forceinline__ void cl_issue_exchange(const typename CP::C* snd, typ
   }
 }
 
-// Exchange I in two row halves (rows [0, ROWS/2) of every block first, on
-// barA; the rest on barB), all first halves issued before any second half, so
-// the receiver's first inverse row stage starts on its first-half rows while
-// the second halves are in flight.
-template <class CP>
-__device__ __forceinline__ void cl_issue_exchange_split(const typename CP::C* snd, typename CP::C* stg,
-                                                        unsigned rank, unsigned long long* barA,
-                                                        unsigned long long* barB) {
-  constexpr int HALF = (CP::ROWS / 2) * CP::CS;
-  constexpr unsigned HB = sizeof(typename CP::C) * HALF;
-  static_assert(HB % 16 == 0, "bulk copies move multiples of 16 bytes");
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(barA, (CP::CL - 1) * HB);
-    mbar_expect_tx(barB, (CP::CL - 1) * HB);
-    for (unsigned q = 0; q < (unsigned)CP::CL; ++q)
-      if (q != rank) bulk_s2peer(stg + rank * CP::BLOCK, q, snd + q * CP::BLOCK, HB, barA);
-    for (unsigned q = 0; q < (unsigned)CP::CL; ++q)
-      if (q != rank) bulk_s2peer(stg + rank * CP::BLOCK + HALF, q, snd + q * CP::BLOCK + HALF, HB, barB);
-  }
-}
-
 // Fully synchronised exchange (single-plane helper kernels).
 template <class CP>
 __device__ __forceinline__ void cl_exchange_sync(const typename CP::C* snd, typename CP::C* stg, unsigned rank,
@@ -166,17 +145,6 @@ __global__ void cl_rank_block(const cx<typename CP::R>* __restrict__ dhat, cx<ty
   }
 }
 
-#ifndef DCSC_CL_PV_RB
-#define DCSC_CL_PV_RB 0  // last-stage d_hat from the rank-blocked slice (A/B: 1.313 vs 1.219 ms per c3s launch, off)
-#endif
-#ifndef DCSC_CL_USTAGE
-#define DCSC_CL_USTAGE 0  // u row block staged in smem by TMA (load during the last inverse row stage, store
-                          // after the prox); A/B 1.229 vs 1.218 ms per c3s launch (the tight B_I wait costs the gain)
-#endif
-#ifndef DCSC_CL_XI_SPLIT
-#define DCSC_CL_XI_SPLIT 0  // exchange I in two row halves (first inverse row stage starts on the first half);
-                            // A/B 1.238 vs 1.205 ms per c3s launch (more copies, more spills): off
-#endif
 #ifndef DCSC_CL_PROX_UNROLL
 #define DCSC_CL_PROX_UNROLL 16
 #endif
@@ -217,10 +185,9 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   // Y (rank-blocked layout) while the previous filter's last stage runs; Y is
   // free then (exchange F's blocks consumed) and no peer writes it before this
   // rank's own next-filter exchange (B_I). Only lambda_hat is read from L2.
-  __shared__ __align__(8) unsigned long long dbar_s, ubar_s;
+  __shared__ __align__(8) unsigned long long dbar_s;
   unsigned long long* dbar = &dbar_s;
-  unsigned long long* ubar = &ubar_s;
-  unsigned dphase = 0, uphase = 0;
+  unsigned dphase = 0;
   const bool DST = ADMM && a.dhat_rb != nullptr;
   const int k0s = (int)(blockIdx.x / CL) * a.kpg;
   // rank 0's packed generator column P(r) = t(r, 0) + i t(r, W/2), t = conj(d) lambda:
@@ -233,15 +200,6 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     LAMC[H + threadIdx.x] = lamn[threadIdx.x * Wh + M];
   }
   if (DST && threadIdx.x == 0) mbar_init(dbar, 1);
-  __shared__ __align__(8) unsigned long long xbarA_s, xbarB_s;
-  unsigned long long* xbarA = &xbarA_s;
-  unsigned long long* xbarB = &xbarB_s;
-  unsigned xiphase = 0;
-  if (ADMM && DCSC_CL_XI_SPLIT && threadIdx.x == 0) {
-    mbar_init(xbarA, 1);
-    mbar_init(xbarB, 1);
-  }
-  if (ADMM && DCSC_CL_USTAGE && threadIdx.x == 0) mbar_init(ubar, 1);
   cl_init_exchange<CP>(xbar);  // (fences the mbarrier inits, syncs the CTA)
   if (DST && threadIdx.x == 0 && k0s < a.K) {
     mbar_expect_tx(dbar, (unsigned)(sizeof(C) * BS));
@@ -281,7 +239,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       const C* __restrict__ lam = a.lamhat + (size_t)n * NB;
       if (threadIdx.x == 0) {
         prefetch_l2_bulk(uk, sizeof(C) * ROWS * M);
-        if (!(DST && DCSC_CL_PV_RB) && k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
+        if (k + 1 < k1) prefetch_l2_bulk(dk + NB, sizeof(C) * NB);
       }
       if (DST) {
         mbar_wait(dbar, dphase);
@@ -316,49 +274,21 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       CLT(0)
       cluster_wait();  // B_F (previous filter): peers' Z free
       CLT(1)
-#if DCSC_CL_XI_SPLIT
-      cl_issue_exchange_split<CP>(Y, Z, rank, xbarA, xbarB);
-      CLT(2)
-      CP::rows_inv_first(Z, Y, rank, X, TW, [&](int rl) { mbar_wait(rl < ROWS / 2 ? xbarA : xbarB, xiphase); });
-      xiphase ^= 1u;
-#else
       cl_issue_exchange<CP>(Y, Z, rank, xbar);
       mbar_wait(xbar, xphase);
       CLT(2)
       xphase ^= 1u;
       CP::rows_inv_first(Z, Y, rank, X, TW);
-#endif
       __syncthreads();
       CLT(7)
       cluster_arrive();  // B_I: my Z consumed, my incoming blocks complete
-#if DCSC_CL_USTAGE
-      // u staging: once every peer has received this rank's exchange-I blocks
-      // (B_I, awaited right away) Y is free; this filter's u row block (64 KB,
-      // contiguous) lands in Y by TMA while the last inverse row stage runs,
-      // and goes back to HBM by a TMA store after the prox
-      cluster_wait();  // B_I
-      if (threadIdx.x == 0) {
-        fence_async_smem();  // the rows_inv_first reads of Y precede the TMA writes
-        mbar_expect_tx(ubar, (unsigned)(sizeof(C) * ROWS * M));
-        bulk_g2s(Y, uk, (unsigned)(sizeof(C) * ROWS * M), ubar);
-      }
-#endif
       CP::rows_inv_rest(X, Z, TW);
       CLT(8)
-#if DCSC_CL_USTAGE
-      mbar_wait(ubar, uphase);
-      uphase ^= 1u;
-      C* const US = Y;  // u row block [ROWS][M] in smem
-#endif
       R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
 #pragma unroll kClProxUnroll
       for (int it = threadIdx.x; it < ROWS * M; it += T) {
         const int rl = it / M, m = it % M;
-#if DCSC_CL_USTAGE
-        const C uv = US[it];
-#else
         const C uv = __ldcs(uk + it);  // u streams through once: evict-first (keeps d_hat, lambda_hat in L2)
-#endif
         const C v = Z[rl * Wh + m];
         const R tv[2] = {v.x * invD, v.y * invD};
         const R uo[2] = {uv.x, uv.y};
@@ -386,11 +316,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
           wv[e] = R(2) * th - un;
           un2[e] = un;
         }
-#if DCSC_CL_USTAGE
-        US[it] = mk<C>(un2[0], un2[1]);
-#else
         __stcs(uk + it, mk<C>(un2[0], un2[1]));
-#endif
         Z[rl * Wh + m] = mk<C>(wv[0], wv[1]);
       }
 #pragma unroll
@@ -408,16 +334,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         ws[0] += (double)f0; ws[1] += (double)f1; ws[2] += (double)f2; ws[3] += (double)f3;
         ws[4] += (double)f4; ws[5] += (double)f5; ws[6] = fmax(ws[6], (double)f6);
       }
-#if DCSC_CL_USTAGE
-      fence_async_smem();  // the new u (generic stores) -> TMA store
       __syncthreads();
-      if (threadIdx.x == 0) {
-        bulk_s2g(uk, US, (unsigned)(sizeof(C) * ROWS * M));
-        bulk_commit();
-      }
-#else
-      __syncthreads();
-#endif
       CLT(9)
     } else {
       const C* __restrict__ src = reinterpret_cast<const C*>(
@@ -454,17 +371,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     fence_async_smem();
     __syncthreads();
     CLT(3)
-#if DCSC_CL_USTAGE
-    if constexpr (ADMM) {
-      // B_U: every rank's u store has read its Y, so exchange F may write peers' Y
-      if (threadIdx.x == 0) bulk_wait_read0();
-      __syncthreads();
-      cluster_arrive();
-      cluster_wait();
-    }
-#else
     if constexpr (ADMM) cluster_wait();  // B_I: peers' Y free (else covered by the wait at the filter start)
-#endif
     CLT(4)
     cl_issue_exchange<CP>(Z, Y, rank, xbar);
     mbar_wait(xbar, xphase);
@@ -483,12 +390,11 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     // so rank 0 does not trail its peers by an L2 round trip every filter
     // ADMM: the last stage's d_hat operands come from this rank's contiguous
     // slice of the rank-blocked copy (L2-hot: TMA'd for this filter's generator)
-    const bool PVRB = DST && DCSC_CL_PV_RB;
-    const C* __restrict__ dsl = PVRB ? a.dhat_rb + ((size_t)k * CL + rank) * BS : nullptr;
+
     C d0 = mk<C>(R(0), R(0)), dMv = mk<C>(R(0), R(0));
     if (rank == 0 && threadIdx.x < H) {
-      d0 = PVRB ? __ldg(dsl + threadIdx.x * CS) : __ldg(dk + threadIdx.x * Wh);
-      dMv = PVRB ? __ldg(dsl + threadIdx.x * CS + COLS) : __ldg(dk + threadIdx.x * Wh + M);
+      d0 = __ldg(dk + threadIdx.x * Wh);
+      dMv = __ldg(dk + threadIdx.x * Wh + M);
     }
     {
       const C* twc = TW + CP::TW_COL;
@@ -500,7 +406,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         if (col != 0) {
 #pragma unroll
           for (int s = 0; s < RL; ++s)
-            pv[s] = PVRB ? __ldg(dsl + (j + s * JL) * CS + cl) : __ldg(dk + (j + s * JL) * Wh + col);
+            pv[s] = __ldg(dk + (j + s * JL) * Wh + col);
         }
         C x[RL];
 #pragma unroll
@@ -534,8 +440,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
              tt[f][1], tt[f][2], tt[f][7], tt[f][8], tt[f][9], tt[f][3], tt[f][4], tt[f][5], tt[f][10], tt[f][11],
              tt[f][12], tt[f][13]);
 #endif
-  cluster_wait();  if (ADMM && DCSC_CL_USTAGE && threadIdx.x == 0) bulk_wait0();  // u stores complete before the CTA retires
-  // last B_F: every block delivered, no peer addresses this CTA's smem
+  cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
   {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
     const int it = threadIdx.x;
