@@ -213,7 +213,10 @@ class Engine final : public EngineBase {
   template <int MODE>
   static void launch_coding(int G, int cnt, cudaStream_t st, const CodingArgs<R>& a) {
     if constexpr (CLU) {
-      coding_pass_cl<P, MODE><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
+      if (a.J > 1)
+        coding_pass_cl<P, MODE, true><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
+      else
+        coding_pass_cl<P, MODE><<<dim3(G * CLN, cnt), T, smem_coding(), st>>>(a);
     } else {
       if (MODE == kPassAdmm && a.J == 2)  // common channel counts: compile-time loops
         coding_pass<P, MODE, true, 2><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
@@ -320,6 +323,10 @@ class Engine final : public EngineBase {
       big((const void*)coding_pass_cl<P, kPassPrologue>, smem_coding());
       big((const void*)coding_pass_cl<P, kPassObjective>, smem_coding());
       big((const void*)coding_pass_cl<P, kPassMaps>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassAdmm, true>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassPrologue, true>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassObjective, true>, smem_coding());
+      big((const void*)coding_pass_cl<P, kPassMaps, true>, smem_coding());
       big((const void*)r2c_planes_cl<P, R>, smem_plain());
       big((const void*)r2c_planes_cl<P, double>, smem_plain());
       big((const void*)c2r_planes_cl<P, R>, smem_plain());
@@ -354,7 +361,6 @@ class Engine final : public EngineBase {
     K_ = o.filters;
     J_ = std::max(1, o.channels);
     if (J_ > kMaxChannels) throw DimErr("at most " + std::to_string(kMaxChannels) + " channels are supported");
-    if (J_ > 1 && CLU) throw DimErr("multi-channel (TCSC) coding is not compiled for the cluster grid family");
     if constexpr (CLU) {  // the cropped support must sit in the first rank's row block
       if (o.support_h > P::ROWS)
         throw DimErr("filter support taller than " + std::to_string(P::ROWS) + " rows on the cluster grid family");

@@ -150,7 +150,12 @@ __global__ void cl_rank_block(const cx<typename CP::R>* __restrict__ dhat, cx<ty
 #endif
 constexpr int kClProxUnroll = DCSC_CL_PROX_UNROLL;  // u loads in flight per thread in the prox loop
 
-template <class CP, int MODE>
+// TC (multi-channel, J > 1, the reference's Joint mode, tcsc.cpp:101-171): the
+// generator forms t_hat_k = sum_j conj(d_hat_jk) lambda_hat_j from L2, and the
+// last forward column stage stores w_hat_k (z_hat_k in the objective / maps
+// passes) to a.what instead of accumulating; tc_lambda / tc_objective do the
+// per-bin J x J work (tcsc_kernels.cuh).
+template <class CP, int MODE, bool TC = false>
 __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     coding_pass_cl(CodingArgs<typename CP::R> a) {
   using R = typename CP::R;
@@ -188,7 +193,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   __shared__ __align__(8) unsigned long long dbar_s;
   unsigned long long* dbar = &dbar_s;
   unsigned dphase = 0;
-  const bool DST = ADMM && a.dhat_rb != nullptr;
+  const bool DST = ADMM && !TC && a.dhat_rb != nullptr;
   const int k0s = (int)(blockIdx.x / CL) * a.kpg;
   // rank 0's packed generator column P(r) = t(r, 0) + i t(r, W/2), t = conj(d) lambda:
   // rank 0 pre-packs conj(P) into the staged d_hat slot 0 per filter, and the
@@ -263,6 +268,16 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         });
         CLT(13)
         CP::cols_inv_rest(X, Y, TW);
+      } else if constexpr (TC) {
+        const int J = a.J;
+        CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
+          const int b = r * Wh + c;
+          C t = mk<C>(R(0), R(0));
+          for (int j = 0; j < J; ++j)
+            t = cadd(t, cmulc(__ldg(a.dhat + ((size_t)j * a.K + k) * NB + b),
+                              __ldg(a.lamhat + ((size_t)n * J + j) * NB + b)));
+          return t;
+        });
       } else {
         CP::cols_inv(X, Y, TW, rank, [&](int r, int c) {
           const int b = r * Wh + c;
@@ -388,14 +403,12 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
     }
     // column-0 epilogue operands (rank 0) fetched with the last stage's loads,
     // so rank 0 does not trail its peers by an L2 round trip every filter
-    // ADMM: the last stage's d_hat operands come from this rank's contiguous
-    // slice of the rank-blocked copy (L2-hot: TMA'd for this filter's generator)
-
     C d0 = mk<C>(R(0), R(0)), dMv = mk<C>(R(0), R(0));
-    if (rank == 0 && threadIdx.x < H) {
+    if (!TC && rank == 0 && threadIdx.x < H) {
       d0 = __ldg(dk + threadIdx.x * Wh);
       dMv = __ldg(dk + threadIdx.x * Wh + M);
     }
+    C* const wk = TC ? a.what + ((size_t)n * a.K + k) * NB : nullptr;
     {
       const C* twc = TW + CP::TW_COL;
       const int it = threadIdx.x;
@@ -403,7 +416,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         const int cl = it % COLS, j = it / COLS;
         const int col = CP::col_of(rank, cl);
         C pv[RL];
-        if (col != 0) {
+        if (!TC && col != 0) {
 #pragma unroll
           for (int s = 0; s < RL; ++s)
             pv[s] = __ldg(dk + (j + s * JL) * Wh + col);
@@ -416,6 +429,9 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         if (col == 0) {
 #pragma unroll
           for (int s = 0; s < RL; ++s) COL0[j + s * JL] = x[s];
+        } else if constexpr (TC) {  // w_hat_k (z_hat_k) at the natural bins of this rank's columns
+#pragma unroll
+          for (int s = 0; s < RL; ++s) wk[(j + s * JL) * Wh + col] = x[s];
         } else {
 #pragma unroll
           for (int s = 0; s < RL; ++s) acc[s] = cadd(acc[s], cmul(pv[s], x[s]));
@@ -428,8 +444,13 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       const int r = threadIdx.x;
       C x0, xn;
       CP::unpack_col0(COL0, r, x0, xn);
-      acc0 = cadd(acc0, cmul(d0, x0));
-      accN = cadd(accN, cmul(dMv, xn));
+      if constexpr (TC) {
+        wk[r * Wh] = x0;
+        wk[r * Wh + M] = xn;
+      } else {
+        acc0 = cadd(acc0, cmul(d0, x0));
+        accN = cadd(accN, cmul(dMv, xn));
+      }
     }
   }
 #ifdef DCSC_CL_TRACE
@@ -441,7 +462,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
              tt[f][12], tt[f][13]);
 #endif
   cluster_wait();  // last B_F: every block delivered, no peer addresses this CTA's smem
-  {
+  if constexpr (!TC) {
     C* dst = a.part + ((size_t)n * a.G + g) * NB;
     const int it = threadIdx.x;
     if (it < ITEMS_L) {
@@ -513,7 +534,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
         }
       }
     }
-    if (stop || (MODE == kPassAdmm && a.is_last)) return;
+    if (TC || stop || (MODE == kPassAdmm && a.is_last)) return;  // TC: lambda_hat from tc_lambda
     const R inv_rho = R(1) / rho;
     const C* pn = a.part + (size_t)n * a.G * NB;
     for (int b = threadIdx.x; b < NB; b += T) {

@@ -157,3 +157,41 @@ def test_encode_matches_reference_cli_path():
     assert rel(z, z_r) <= FP64_TOL
     o_r = ref.objective_j(xnorm, d, z_r, 0.1)
     assert abs(obj[2] - o_r[2]) <= FP64_TOL * abs(o_r[2])
+
+
+# ---------------------------------------------------------------- cluster grid families (J > 1)
+@pytest.mark.parametrize("J,grid,K,m,prec", [(2, (128, 128), 3, 11, 64), (3, (256, 256), 2, 11, 32)])
+def test_tcsc_coding_cluster_family_matches_reference(J, grid, K, m, prec):
+    """Joint mode on the 4-CTA cluster families (FP64 128x128, FP32 256x256): the
+    generator sums conj(d_hat_jk) lambda_hat_j over channels and the pass stores
+    w_hat_k for the per-bin J x J solves (tcsc.cpp:101-171)."""
+    x, d = problem(1, J, grid, K, m, seed=9, fp32=prec == 32)
+    cfg = ref.Cfg(beta=0.1, max_admm=40, normalize=0)
+    z_r, st_r, s_r = ref.solve_coding_tcsc(x[0], d, cfg)
+    sc = dcsc.SolverConfig(beta=0.1, max_admm=40, normalize=0)
+    z_g, st_g, s_g = dcsc.solve_coding_tcsc(x[0], d, sc, precision=prec)
+    if prec == 64:
+        assert s_g["admm_iters"] == s_r["admm_iters"]
+        assert rel(z_g, z_r) <= FP64_TOL
+        assert rel(st_g.lam, st_r[2]) <= FP64_TOL
+        assert abs(s_g["dual_objective"] - s_r["dual_objective"]) <= FP64_TOL * abs(s_r["dual_objective"])
+    else:
+        assert abs(s_g["dual_objective"] - s_r["dual_objective"]) <= 1e-4 * abs(s_r["dual_objective"])
+        og = dcsc.evaluate_objective(x[0], d, z_g, 0.1, precision=32)
+        orf = ref.objective_j(x[0], d, z_r, 0.1)
+        assert abs(og[2] - orf[2]) <= 1e-4 * abs(orf[2])
+
+
+def test_tcsc_run_cluster_family_fp64_matches_reference():
+    """run_csc in Joint mode (J = 2) on the FP64 128x128 cluster family: coding,
+    objective (tc_objective over the stored z_hat), learning, 2 outer iterations."""
+    x, _ = problem(2, 2, (128, 128), 3, 11, seed=12)
+    kw = dict(beta=0.1, max_outer=2, normalize=0, seed=7, tol=1e-300, max_admm=40, max_mu_iters=6, cg_max=40)
+    r = ref.run_j(x, 3, (11, 11), ref.Cfg(**kw))
+    g = dcsc.run_csc(x, 3, (11, 11), dcsc.SolverConfig(**kw), precision=64)
+    assert len(g["trace"]) == len(r["trace"])
+    for a, b in zip(g["trace"], r["trace"]):
+        assert a["admm_iters"] == b["admm_iters"]
+        for key in ("total", "data_term", "l1_term"):
+            assert abs(a[key] - b[key]) <= 1e-8 * abs(b[key]), (key, a, b)
+    assert rel(g["dict"], r["dicts"][-1]) <= 1e-7
