@@ -76,7 +76,13 @@ def test_channel_count_is_validated_before_touching_the_device():
         dcsc.Context(2, (20, 20), 4, (5, 5), dcsc.SolverConfig(normalize=0), 64, channels=9)
 
 
-def test_joint_mode_on_the_cluster_grid_is_a_dimension_error():
-    # the 256^2 (4-CTA cluster) family is single-channel in this round
+def test_cluster_grid_limits_are_dimension_errors():
+    # the 4-CTA cluster families crop the support inside rank 0's row block
+    # (H / 4 rows) and every family takes at most 8 channels: checked before
+    # any device work, so this runs without a GPU
     with pytest.raises(dcsc.DimensionError):
-        dcsc.Context(1, (256, 256), 4, (11, 11), dcsc.SolverConfig(normalize=0), 32, channels=3)
+        dcsc.Context(1, (256, 256), 4, (65, 65), dcsc.SolverConfig(normalize=0), 32)
+    with pytest.raises(dcsc.DimensionError):
+        dcsc.Context(1, (128, 128), 4, (33, 5), dcsc.SolverConfig(normalize=0), 64)
+    with pytest.raises(dcsc.DimensionError):
+        dcsc.Context(1, (64, 64), 4, (5, 5), dcsc.SolverConfig(normalize=0), 32, channels=9)
