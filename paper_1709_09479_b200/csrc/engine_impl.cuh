@@ -430,7 +430,7 @@ class Engine final : public EngineBase {
     dhat_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);    // J x K x NB (channel-major)
     dcand_.alloc(sizeof(C) * (size_t)J_ * K_ * NB);
     if constexpr (CLU) {
-      if (J_ == 1) dhat_rb_.alloc(sizeof(C) * (size_t)K_ * CLN * P::BUF);  // rank-blocked d_hat (cl_rank_block)
+      if (J_ == 1) dhat_rb_.alloc((size_t)K_ * CLN * P::buffer_bytes);  // rank-blocked d_hat (cl_rank_block)
     }
     sigma_.alloc(sizeof(R) * NB);
     u_.alloc(sizeof(R) * nD * K_);

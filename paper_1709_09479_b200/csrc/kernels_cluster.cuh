@@ -128,16 +128,18 @@ __global__ void cl_rank_block(const cx<typename CP::R>* __restrict__ dhat, cx<ty
                               int K) {
   using C = typename CP::C;
   constexpr int H = CP::H, CS = CP::CS, COLS = CP::COLS, CL = CP::CL, Wh = CP::Wh, M = CP::M, NB = CP::NB;
-  constexpr int BUF = CP::BUF;
-  static_assert(BUF == H * CS, "rank block = one column buffer");
-  const size_t total = (size_t)K * CL * BUF;
+  constexpr int RB = (int)(CP::buffer_bytes / sizeof(C));  // slice stride = the smem buffer stride
+  static_assert(CP::BUF == H * CS, "rank block = one column buffer");
+  const size_t total = (size_t)K * CL * RB;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int e = (int)(i % BUF);
-    const int c = (int)((i / BUF) % CL);
-    const size_t k = i / ((size_t)BUF * CL);
+    const int e = (int)(i % RB);
+    const int c = (int)((i / RB) % CL);
+    const size_t k = i / ((size_t)RB * CL);
     const int r = e / CS, cl = e % CS;
     C v = mk<C>(typename CP::R(0), typename CP::R(0));
-    if (cl < COLS)
+    if (e >= H * CS) {
+      // padding to the buffer stride
+    } else if (cl < COLS)
       v = dhat[k * NB + r * Wh + CP::col_of((unsigned)c, cl)];
     else if (c == 0)
       v = dhat[k * NB + r * Wh + M];
@@ -164,7 +166,7 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
   constexpr int H = CP::H, M = CP::M, Wh = CP::Wh, NB = CP::NB, D = CP::D, T = CP::T, CL = CP::CL;
   constexpr int ROWS = CP::ROWS, COLS = CP::COLS, CS = CP::CS;
   constexpr int BS = CP::buffer_bytes / sizeof(C);
-  static_assert(BS == CP::BUF, "rank-blocked d_hat stride (cl_rank_block) = buffer size");
+  static_assert(BS >= CP::BUF, "rank-blocked d_hat stride (cl_rank_block) = buffer stride");
   constexpr bool ADMM = MODE == kPassAdmm;
   using S = Split<typename CP::ColPlan>;
   static_assert(CountStages<typename CP::ColPlan>::value == 2, "two-stage column plan (X -> Y)");
