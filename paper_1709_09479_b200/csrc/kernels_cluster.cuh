@@ -302,39 +302,60 @@ __global__ void __cluster_dims__(CP::CL, 1, 1) __launch_bounds__(CP::T)
       CP::rows_inv_rest(X, Z, TW);
       CLT(8)
       R f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0, f6 = 0;
-#pragma unroll kClProxUnroll
-      for (int it = threadIdx.x; it < ROWS * M; it += T) {
-        const int rl = it / M, m = it % M;
-        const C uv = __ldcs(uk + it);  // u streams through once: evict-first (keeps d_hat, lambda_hat in L2)
-        const C v = Z[rl * Wh + m];
-        const R tv[2] = {v.x * invD, v.y * invD};
-        const R uo[2] = {uv.x, uv.y};
-        C t0v = mk<C>(R(0), R(0));
-        if (t0k) t0v = __ldg(t0k + it);
-        const R t0[2] = {t0v.x, t0v.y};
-        R wv[2], un2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const R t = tv[e];
-          const R th_o = t0k ? t0[e] : fmin(fmax(uo[e], -beta), beta);
-          const R un = t - (th_o - uo[e]);
-          const R th = fmin(fmax(un, -beta), beta);
-          const R zn = rho * (th - un);
-          const R d_tt = th - t;
-          const R dz = rho * d_tt;
-          const R dth = th - th_o;
-          f0 += d_tt * d_tt;
-          f1 += th * th;
-          f2 += t * t;
-          f3 += dz * dz;
-          f4 += zn * zn;
-          f5 += dth * dth;
-          f6 = fmax(f6, fabs(t));
-          wv[e] = R(2) * th - un;
-          un2[e] = un;
+      auto prox_elem = [&](const R t, const R u_old, const R t0e, R& w_out, R& u_out) {
+        const R th_o = t0k ? t0e : fmin(fmax(u_old, -beta), beta);
+        const R un = t - (th_o - u_old);
+        const R th = fmin(fmax(un, -beta), beta);
+        const R zn = rho * (th - un);
+        const R d_tt = th - t;
+        const R dz = rho * d_tt;
+        const R dth = th - th_o;
+        f0 += d_tt * d_tt;
+        f1 += th * th;
+        f2 += t * t;
+        f3 += dz * dz;
+        f4 += zn * zn;
+        f5 += dth * dth;
+        f6 = fmax(f6, fabs(t));
+        w_out = R(2) * th - un;
+        u_out = un;
+      };
+      if constexpr (sizeof(R) == 4) {
+        // FP32: two pixel pairs per item, u as 16-byte vectors (half the LDG /
+        // STG instructions of the 8-byte form)
+        float4* __restrict__ uk4 = reinterpret_cast<float4*>(uk);
+        const float4* __restrict__ t0k4 = reinterpret_cast<const float4*>(t0k);
+#pragma unroll 8
+        for (int it = threadIdx.x; it < ROWS * M / 2; it += T) {
+          const int rl = (2 * it) / M, m = (2 * it) % M;
+          const float4 u4 = __ldcs(uk4 + it);  // u streams through once: evict-first (keeps d_hat, lambda_hat in L2)
+          float4 t04 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (t0k) t04 = __ldg(t0k4 + it);
+          const C va = Z[rl * Wh + m], vb = Z[rl * Wh + m + 1];
+          float4 o4;
+          C wa, wb;
+          prox_elem(va.x * invD, u4.x, t04.x, wa.x, o4.x);
+          prox_elem(va.y * invD, u4.y, t04.y, wa.y, o4.y);
+          prox_elem(vb.x * invD, u4.z, t04.z, wb.x, o4.z);
+          prox_elem(vb.y * invD, u4.w, t04.w, wb.y, o4.w);
+          __stcs(uk4 + it, o4);
+          Z[rl * Wh + m] = wa;
+          Z[rl * Wh + m + 1] = wb;
         }
-        __stcs(uk + it, mk<C>(un2[0], un2[1]));
-        Z[rl * Wh + m] = mk<C>(wv[0], wv[1]);
+      } else {
+#pragma unroll kClProxUnroll
+        for (int it = threadIdx.x; it < ROWS * M; it += T) {
+          const int rl = it / M, m = it % M;
+          const C uv = __ldcs(uk + it);
+          C t0v = mk<C>(R(0), R(0));
+          if (t0k) t0v = __ldg(t0k + it);
+          const C v = Z[rl * Wh + m];
+          C w, un;
+          prox_elem(v.x * invD, uv.x, t0v.x, w.x, un.x);
+          prox_elem(v.y * invD, uv.y, t0v.y, w.y, un.y);
+          __stcs(uk + it, un);
+          Z[rl * Wh + m] = w;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
