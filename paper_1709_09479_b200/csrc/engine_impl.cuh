@@ -24,6 +24,7 @@
 #include "dcsc_cuda.h"
 #include "kernels.cuh"
 #include "kernels_cluster.cuh"
+#include "kernels_tc.cuh"
 #include "tcsc_kernels.cuh"
 
 using namespace dcsc_cuda;
@@ -230,6 +231,19 @@ class Engine final : public EngineBase {
         coding_pass<P, MODE><<<dim3(G, cnt), T, smem_coding(), st>>>(a);
     }
   }
+  // Tensor-core spatial coding iteration (kernels_tc.cuh): FP32 planes whose
+  // rows split into 128-pixel tiles, 11 x 11 supports, K <= 128, J = 1.
+  // (cluster families only: their u planes are row-major; the single-CTA
+  // family keeps u as column-major pixel pairs)
+  static constexpr bool kTcFamily = CLU && std::is_same<R, float>::value && W % 128 == 0 &&
+                                    (W / 128 == 1 || (W / 128) % 2 == 0) && H % 16 == 0;
+  template <int KF>
+  using TG = TcGeom<H, W, KF, 11, 11, 16>;
+  template <int KF>
+  static void set_tc_attr() {
+    CK(cudaFuncSetAttribute((const void*)coding_pass_tc<TG<KF>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)TG<KF>::smem));
+  }
   // persistent pipelined r2c / c2r (SmemPipe) when the staging buffer fits and
   // the planes are 16-byte aligned storage-precision planes: grid = resident slots
   static int pipe_grid(const void* fn, size_t smem, int count) {
@@ -318,6 +332,10 @@ class Engine final : public EngineBase {
     auto big = [](const void* fn, size_t bytes) {
       if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     };
+    if constexpr (kTcFamily) {
+      set_tc_attr<64>();
+      set_tc_attr<128>();
+    }
     if constexpr (CLU) {
       big((const void*)coding_pass_cl<P, kPassAdmm>, smem_coding());
       big((const void*)coding_pass_cl<P, kPassPrologue>, smem_coding());
@@ -501,6 +519,22 @@ class Engine final : public EngineBase {
                    maps_.bytes + lamhat_.bytes + lam_.bytes + part_.bytes + sums_.bytes + gam_.bytes +
                    3 * r_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes + ginv_.bytes + what_.bytes +
                    dhat_rb_.bytes;
+    if constexpr (kTcFamily) {
+      const char* e = std::getenv("DCSC_TC");
+      tc_ = J_ == 1 && mh_ == 11 && mw_ == 11 && K_ <= 128 && !(e && e[0] == '0');
+      if (tc_) {
+        using G = TG<128>;  // band geometry does not depend on the filter count
+        tc_kf_ = K_ <= 64 ? 64 : 128;
+        tlam16_.alloc(sizeof(uint32_t) * (size_t)N_ * D);
+        tlscale_.alloc(sizeof(float) * (size_t)N_);
+        tdsplit_.alloc((size_t)2 * tc_kf_ * kTcTaps * 2);
+        tspart_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::SR * W);
+        tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
+        device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes;
+        CK(cudaDeviceGetAttribute(&tc_grid_, cudaDevAttrMultiProcessorCount, o.device));
+        if (std::getenv("DCSC_VERBOSE")) std::fprintf(stderr, "dcsc: tensor-core coding pass (KF=%d)\n", tc_kf_);
+      }
+    }
     CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
     CK(cudaMemsetAsync(maps_.p, 0, maps_.bytes, st_));
     CK(cudaMemsetAsync(lam_.p, 0, lam_.bytes, st_));
@@ -594,6 +628,60 @@ class Engine final : public EngineBase {
     a.iter = iter;
     a.is_last = is_last;
     launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] { launch_coding<MODE>(G_, cnt, st_, a); });
+  }
+
+  // lambda_hat -> spatial lambda -> scaled f16 hi / lo planes for the tensor-core pass
+  void tc_lambda_spatial(int n0, int cnt) {
+    if constexpr (kTcFamily) {
+      c2r<R>(lamhat_.as<C>() + (size_t)n0 * NB, NB, lam_.as<R>() + (size_t)n0 * D, D, cnt);
+      launch(kFamLambda, [&] {
+        tc_lam_split<D><<<cnt, 512, 0, st_>>>(lam_.as<R>() + (size_t)n0 * D, tlam16_.as<uint32_t>() + (size_t)n0 * D,
+                                              tlscale_.as<float>() + n0);
+      });
+    }
+  }
+  // One ADMM iteration of images [n0, n0 + cnt) on the tensor-core path:
+  // spatial pass (t, prox, s = sum_k d_k * w_k) -> band sums -> DFT(s) ->
+  // stop test + lambda_hat (lambda_update, coding.cpp:264-283, :25-37) ->
+  // spatial lambda for the next iteration.
+  void tc_iteration(int n0, int cnt, int it, bool last) {
+    if constexpr (kTcFamily) {
+      using G = TG<128>;
+      TcArgs a;
+      a.lam16 = tlam16_.as<uint32_t>() + (size_t)n0 * D;
+      a.lam_scale = tlscale_.as<float>() + n0;
+      a.dsplit = tdsplit_.as<__half>();
+      a.d_scale = tc_dscale_;
+      a.u = u_.as<R>() + (size_t)n0 * K_ * D;
+      a.theta0 = use_theta0_ ? theta0_.as<R>() + (size_t)n0 * K_ * D : nullptr;
+      a.spart = tspart_.as<float>() + (size_t)n0 * G::NBANDS * G::SR * W;
+      a.bsums = tbsums_.as<double>() + (size_t)n0 * G::NBANDS * kSums;
+      a.conv = conv_.as<int>() + n0;
+      a.N = cnt;
+      a.K = K_;
+      a.rho = (float)cfg_.rho;
+      a.beta = (float)cfg_.beta;
+      const int grid = std::min(tc_grid_, cnt * G::NBANDS);
+      launch(kFamCoding, [&] {
+        if (tc_kf_ == 64)
+          coding_pass_tc<TG<64>><<<grid, kTcThreads, TG<64>::smem, st_>>>(a);
+        else
+          coding_pass_tc<TG<128>><<<grid, kTcThreads, TG<128>::smem, st_>>>(a);
+      });
+      R* s = lam_.as<R>() + (size_t)n0 * D;          // s reuses the spatial lambda planes
+      C* spec = part_.as<C>() + (size_t)n0 * NB;      // one partial spectrum per image (G = 1)
+      double* sm1 = sums_.as<double>() + (size_t)n0 * kSums;
+      launch(kFamLambda, [&] {
+        tc_band_reduce<G><<<dim3(16, cnt), 256, 0, st_>>>(a.spart, a.bsums, a.conv, s, sm1);
+      });
+      r2c(s, false, D, spec, NB, cnt);
+      launch(kFamLambda, [&] {
+        lambda_update<R><<<dim3((NB + 255) / 256, cnt), 256, 0, st_>>>(
+            spec, sm1, xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(), lamhat_.as<C>() + (size_t)n0 * NB,
+            conv_.as<int>() + n0, img_.as<ImageAdmm>() + n0, 1, NB, R(cfg_.rho), it, last ? 1 : 0, 0);
+      });
+      if (!last) tc_lambda_spatial(n0, cnt);
+    }
   }
 
   void r2c(const void* src, bool src_double, size_t src_stride, C* dst, size_t dst_stride, int count,
@@ -694,6 +782,19 @@ class Engine final : public EngineBase {
         launch(kFamOther, [&] {
           cl_rank_block<P><<<592, 256, 0, st_>>>(dhat_.as<C>(), dhat_rb_.as<C>(), K_);
         });
+    }
+    if constexpr (kTcFamily) {
+      if (tc_) {
+        float amax = 0.f;
+        for (double v : dict_) amax = std::max(amax, (float)std::fabs(v));
+        tc_dscale_ = umma::pow2_scale(amax);
+        launch(kFamOther, [&] {
+          if (tc_kf_ == 64)
+            tc_dsplit<64><<<32, 256, 0, st_>>>(ddict_.as<double>(), K_, M_, tc_dscale_, tdsplit_.as<__half>());
+          else
+            tc_dsplit<128><<<64, 256, 0, st_>>>(ddict_.as<double>(), K_, M_, tc_dscale_, tdsplit_.as<__half>());
+        });
+      }
     }
     if (J_ == 1) {
       launch(kFamOther, [&] {
@@ -940,13 +1041,17 @@ class Engine final : public EngineBase {
       });
     };
     if (all_zero && J_ == 1) lam_update(0, 0, 1);
+    if (tc_) tc_lambda_spatial(n0, cnt);
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     int pending = -1;  // iteration whose conv flags are in flight
     for (int it = 1; it <= cfg_.max_admm; ++it) {
       use_theta0_ = t0_pending && it == 1;
-      coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
+      if (tc_)
+        tc_iteration(n0, cnt, it, it == cfg_.max_admm);
+      else
+        coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
       use_theta0_ = false;
       if (J_ > 1 && it < cfg_.max_admm) tc_lam(K_, true);
       if (pending >= 0) {
@@ -2033,6 +2138,11 @@ class Engine final : public EngineBase {
   std::vector<long> fn_rank_;
   DevMem zf_, xf_, gf_, rf_, pf_, apf_, fsend_, fpart_, fodata_, fcpart_;
   bool use_theta0_ = false;
+  // tensor-core coding pass (kernels_tc.cuh)
+  bool tc_ = false;
+  int tc_kf_ = 128, tc_grid_ = 148;
+  float tc_dscale_ = 1.f;
+  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_;
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   std::vector<int> degen_;  // per image: normalisation met a constant input
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)

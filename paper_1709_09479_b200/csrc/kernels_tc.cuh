@@ -1,0 +1,485 @@
+// Spatial-domain ADMM coding iteration on the 5th-generation tensor cores.
+//
+// The reference forms, per ADMM iteration and filter k (coding.cpp:223-263),
+//   t_k = iDFT(conj(d_hat_k) lambda_hat)          (correlate, coding.cpp:77-86)
+//   prox on (theta, z) with t_k                    (coding.cpp:237-251)
+//   acc = sum_k d_hat_k DFT(theta_k + z_k / rho)   (lambda_from_w, coding.cpp:25-37)
+// With the filters' m x m support at the plane corner (filter_spectrum) the two
+// spectral products are circular correlations / convolutions with m*m taps:
+//   t_k[p] = sum_o d_k[o] lambda[p + o],  s[p] = sum_k sum_o d_k[o] w_k[p - o],
+// and DFT(s) = sum_k d_hat_k w_hat_k exactly. Over all filters at once they are
+// two GEMMs per tile of 128 pixels (one row segment):
+//   GEMM-1  T[p][k] = sum_o L[p][o] D[k][o]    L = im2col(lambda) (M=128, N=KF, K=128 taps)
+//   GEMM-2  Z[p][o] = sum_k W[p][k] D[k][o]    W = w of the tile   (M=128, N=128 taps, K=KF)
+// followed by the col2im sum s[p + o] += Z[p][o]. Both run on tcgen05 with the
+// pixel operand in tensor memory and the dictionary in shared memory (one
+// copy serves GEMM-1 K-major and GEMM-2 MN-major), accumulating in FP32; each
+// FP32 operand is split into two scaled f16 (x*s = hi + lo + O(2^-22 |x*s|)) and
+// three products (hi*hi + hi*lo + lo*hi) restore FP32-level accuracy. lambda
+// is scaled per image, the dictionary per dictionary, w per pixel (a row of W).
+// The per-image FFT work that remains is one r2c of s and one c2r of lambda_hat
+// per iteration instead of a c2r + r2c per filter.
+//
+// Persistent kernel, one CTA per SM, 9 warps: warp 0 issues the MMAs (one
+// thread); warps 1-8 are two epilogue groups of 4 warps (one per TMEM lane
+// quarter = 32 pixels), each owning one of two tensor-memory slots (256
+// columns: A operand = im2col then W; accumulator = T then Z) and alternate
+// tiles, so one group's epilogue overlaps the other group's GEMMs.
+// Work item = (image, band of RB tile rows); deterministic: every sum has a
+// fixed order (per-warp col2im strips, strips and bands summed in index order).
+#pragma once
+#include "kernels.cuh"
+#include "umma.cuh"
+
+namespace dcsc_cuda {
+
+constexpr int kTcTaps = 128;                       // GEMM-1 K / GEMM-2 N (taps padded)
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcThreads = 32 * (kTcEpiWarps + 1);  // 288
+constexpr int kTcStripW = 44;                      // col2im strip row stride (floats) >= 32 + MW - 1
+
+struct TcArgs {
+  const uint32_t* lam16;   // N x 2 x H x W/2 words: f16 pairs of lambda * lam_scale[n] (hi plane, lo plane)
+  const float* lam_scale;  // N
+  const __half* dsplit;    // 2 x KF x 128 f16 core-matrix grid of d * d_scale (hi, lo)
+  float d_scale;
+  float* u;                // N x K x H x W ADMM state u = t - z/rho
+  const float* theta0;     // N x K x H x W (first iteration's theta_old) or nullptr
+  float* spart;            // N x NBANDS x SR x W col2im band partials
+  double* bsums;           // N x NBANDS x kSums stop-test partial sums
+  const int* conv;         // N
+  int N, K;
+  float rho, beta;
+};
+
+template <int H_, int W_, int KF_, int MH_, int MW_, int RB_>
+struct TcGeom {
+  static constexpr int H = H_, W = W_, KF = KF_, MH = MH_, MW = MW_, RB = RB_;
+  static constexpr int D = H * W;
+  static constexpr int TPR = W / 128;              // tiles per image row
+  static constexpr int NBANDS = H / RB;
+  static constexpr int TPI = RB * TPR;             // tiles per work item
+  static constexpr int SR = RB + MH - 1;           // rows a band's col2im touches / lambda rows it reads
+  static constexpr int LWW = W / 2 + 8;            // lambda band row: W halves + 16 wrap halves, in words
+  static constexpr int NSS = TPR == 1 ? 2 : TPR;   // strip sets (per tile column; per epilogue group if TPR == 1)
+  static constexpr int NSTRIP = NSS * 4;
+  static constexpr int STRIP = SR * kTcStripW;
+  static constexpr int TAPS = MH * MW;
+  static_assert(W % 128 == 0 && (TPR == 1 || TPR % 2 == 0), "row tiles of 128 pixels: one or an even count per row");
+  static_assert(H % RB == 0 && RB >= MH - 1 && TPI % 2 == 0, "band geometry");
+  static_assert(TAPS <= kTcTaps && 32 + MW - 1 <= kTcStripW && MW <= 16, "filter support");
+  static_assert(KF % 32 == 0 && KF >= 32 && KF <= 128, "filters per pass");
+  static constexpr size_t d_bytes = (size_t)2 * KF * kTcTaps * 2;
+  static constexpr size_t lam_off = d_bytes;
+  static constexpr size_t lam_bytes = (size_t)2 * SR * LWW * 4;
+  static constexpr size_t strip_off = (lam_off + lam_bytes + 15) / 16 * 16;
+  static constexpr size_t strip_bytes = (size_t)NSTRIP * STRIP * 4;
+  static constexpr size_t red_off = strip_off + strip_bytes;
+  static constexpr size_t red_bytes = (size_t)8 * kTcEpiWarps * 8;
+  static constexpr size_t bar_off = red_off + red_bytes;
+  static constexpr size_t smem = bar_off + 16 * 8;
+};
+
+__device__ __forceinline__ void mbar_arrive1(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcEpiWarps) : "memory"); }
+__device__ __forceinline__ uint32_t lds_u16(const void* p) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(smem_addr(p)));
+  return v;
+}
+
+// im2col row of one pixel (tap o = oy*MW + ox, lambda[r + oy][c + ox]) as f16
+// pairs (o = 2j, 2j+1) -> tensor-memory columns j (hi) and 64 + j (lo).
+// `row` = this tile row's first band row (hi plane; the lo plane follows at
+// +SR*LWW words), cb = c >> 1, par = c & 1. Pairs inside one tap row are two
+// word loads + a byte permute; pairs across tap rows two half loads.
+template <class G>
+__device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint32_t A) {
+  constexpr int MW = G::MW, TAPS = G::TAPS, LWW = G::LWW, SR = G::SR;
+  const int cb = c >> 1, par = c & 1;
+  const uint32_t sel_e = par ? 0x5432u : 0x3210u;  // pair starting at an even tap column offset
+  const uint32_t sel_o = par ? 0x3210u : 0x5432u;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t vv[2][16];
+#pragma unroll
+    for (int pl = 0; pl < 2; ++pl) {
+      const uint32_t* rp = row + pl * SR * LWW;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        const int o0 = 2 * (ch * 16 + jj), o1 = o0 + 1;
+        uint32_t val = 0;
+        if (o0 < TAPS) {
+          const int oy0 = o0 / MW, ox0 = o0 % MW;
+          if (o1 < TAPS && o1 / MW == oy0) {
+            const uint32_t* p = rp + oy0 * LWW + cb;
+            if ((ox0 & 1) == 0) {
+              val = __byte_perm(p[ox0 / 2], p[ox0 / 2 + 1], sel_e);
+            } else {
+              val = __byte_perm(p[par + (ox0 - 1) / 2], p[par + (ox0 - 1) / 2 + 1], sel_o);
+            }
+          } else {
+            const unsigned short* hr = reinterpret_cast<const unsigned short*>(rp);
+            const uint32_t lo = lds_u16(hr + oy0 * 2 * LWW + c + ox0);
+            uint32_t hi = 0;
+            if (o1 < TAPS) hi = lds_u16(hr + (o1 / MW) * 2 * LWW + c + (o1 % MW));
+            val = lo | (hi << 16);
+          }
+        }
+        vv[pl][jj] = val;
+      }
+    }
+    umma::st16(A + ch * 16, vv[0]);
+    umma::st16(A + 64 + ch * 16, vv[1]);
+  }
+}
+
+template <class G>
+__global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
+  constexpr int H = G::H, W = G::W, KF = G::KF, MW = G::MW, RB = G::RB, D = G::D, TPR = G::TPR,
+                NBANDS = G::NBANDS, TPI = G::TPI, SR = G::SR, LWW = G::LWW, TAPS = G::TAPS;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const __half* Ds = reinterpret_cast<const __half*>(sm);
+  uint32_t* LAM = reinterpret_cast<uint32_t*>(sm + G::lam_off);
+  float* STR = reinterpret_cast<float*>(sm + G::strip_off);
+  double* RED = reinterpret_cast<double*>(sm + G::red_off);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + G::bar_off);
+  unsigned long long *a_full = bars, *t_full = bars + 2, *w_full = bars + 4, *z_full = bars + 6, *dbar = bars + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) umma::tmem_alloc<512>(tslot);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(a_full + i, 4);
+      mbar_init(w_full + i, 4);
+      mbar_init(t_full + i, 1);
+      mbar_init(z_full + i, 1);
+    }
+    mbar_init(dbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tbase = *tslot;
+  const int items = a.N * NBANDS;
+
+  if (warp == 0) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      mbar_expect_tx(dbar, (unsigned)G::d_bytes);
+      for (int i = 0; i < (int)(G::d_bytes / 16384); ++i)
+        bulk_g2s(const_cast<__half*>(Ds) + i * 8192, a.dsplit + i * 8192, 16384u, dbar);
+      mbar_wait(dbar, 0);
+      const uint32_t dh = umma::smem_u32(Ds), dl = dh + KF * kTcTaps * 2;
+      constexpr uint32_t id1 = umma::idesc_f16(128, KF, 0), id2 = umma::idesc_f16(128, kTcTaps, 1);
+      auto gemm1 = [&](uint32_t gg) {
+        const uint32_t s = gg & 1u, ph = (gg >> 1) & 1u;
+        mbar_wait(a_full + s, ph);
+        umma::fence_after_sync();
+        const uint32_t A = tbase + 256u * s, acc = A + 128u;
+#pragma unroll
+        for (int j = 0; j < kTcTaps / 16; ++j) {  // K = taps; B K-major: LBO 128 B (taps), SBO 2048 B (filters)
+          const uint64_t bh = umma::sdesc(dh + 256u * j, 128u, 2048u), bl = umma::sdesc(dl + 256u * j, 128u, 2048u);
+          umma::mma_ts(acc, A + 8u * j, bh, id1, j > 0);
+          umma::mma_ts(acc, A + 8u * j, bl, id1, 1u);
+          umma::mma_ts(acc, A + 64u + 8u * j, bh, id1, 1u);
+        }
+        umma::commit(t_full + s);
+      };
+      auto gemm2 = [&](uint32_t gg) {
+        const uint32_t s = gg & 1u, ph = (gg >> 1) & 1u;
+        mbar_wait(w_full + s, ph);
+        umma::fence_after_sync();
+        const uint32_t A = tbase + 256u * s, acc = A + 128u;
+#pragma unroll
+        for (int j = 0; j < KF / 16; ++j) {  // K = filters; B MN-major: LBO 2048 B (filters), SBO 128 B (taps)
+          const uint64_t bh = umma::sdesc(dh + 4096u * j, 2048u, 128u), bl = umma::sdesc(dl + 4096u * j, 2048u, 128u);
+          umma::mma_ts(acc, A + 8u * j, bh, id2, j > 0);
+          umma::mma_ts(acc, A + 8u * j, bl, id2, 1u);
+          umma::mma_ts(acc, A + 64u + 8u * j, bh, id2, 1u);
+        }
+        umma::commit(z_full + s);
+      };
+      // GEMM-2 of a tile is issued after GEMM-1 of the next one, but never
+      // across items: the epilogue groups meet at an item boundary.
+      uint32_t g = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        if (a.conv[item / NBANDS]) continue;
+        for (int t = 0; t < TPI; ++t) {
+          gemm1(g + t);
+          if (t > 0) gemm2(g + t - 1);
+        }
+        gemm2(g + TPI - 1);
+        g += TPI;
+      }
+    }
+  } else {
+    // ===== epilogue groups =====
+    const int ew = warp - 1, e = ew >> 2, q = warp & 3, p = 32 * q + lane, et = threadIdx.x - 32;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    const uint32_t A = tbase + 256u * e + lane_off, ACC = A + 128u;
+    const float rho = a.rho, beta = a.beta;
+    uint32_t g = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int n = item / NBANDS, b = item % NBANDS;
+      if (a.conv[n]) continue;
+      epi_sync();  // previous item's strips flushed
+      {            // lambda band rows b*RB .. b*RB + SR - 1 (mod H), wrap-padded by 16 halves
+        const uint32_t* src = a.lam16 + (size_t)n * 2 * (D / 2);
+        for (int i = et; i < 2 * SR * LWW; i += 32 * kTcEpiWarps) {
+          const int pl = i / (SR * LWW), rr = (i / LWW) % SR, wi = i % LWW;
+          const int gr = (b * RB + rr) % H, sc = wi < W / 2 ? wi : wi - W / 2;
+          LAM[i] = __ldg(src + ((size_t)pl * H + gr) * (W / 2) + sc);
+        }
+        float4* z4 = reinterpret_cast<float4*>(STR);
+        for (int i = et; i < G::NSTRIP * G::STRIP / 4; i += 32 * kTcEpiWarps) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      epi_sync();
+      const float tsc = 1.f / (__ldg(a.lam_scale + n) * a.d_scale);
+      const float dinv = 1.f / a.d_scale;
+      double st[7] = {0, 0, 0, 0, 0, 0, 0};
+      float* const ubase = a.u + (size_t)n * a.K * D;
+      const float* const t0base = a.theta0 ? a.theta0 + (size_t)n * a.K * D : nullptr;
+      auto prefetch_tile = [&](int t) {
+        if (t < TPI && p < a.K) {
+          const int r = b * RB + t / TPR, c0 = (t % TPR) * 128;
+          prefetch_l2_bulk(ubase + (size_t)p * D + r * W + c0, 512u);
+        }
+      };
+      prefetch_tile(e);
+      for (int t = e; t < TPI; t += 2) {
+        const uint32_t gg = g + t, ph = (gg >> 1) & 1u;
+        const int rl = t / TPR, tc = t % TPR;
+        const int r = b * RB + rl, c = tc * 128 + p;
+        prefetch_tile(t + 2);
+        // --- im2col(lambda) -> A
+        tc_build_im2col<G>(LAM + rl * LWW, c, A);
+        umma::wait_st();
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(a_full + e);
+        // --- prox on T, w -> A (two f16 planes, per-pixel scale)
+        float* const up = ubase + (size_t)r * W + c;
+        const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
+        float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f, f4 = 0.f, f5 = 0.f, f6 = 0.f, wmax = 0.f;
+        mbar_wait(t_full + e, ph);
+        umma::fence_after_sync();
+#pragma unroll 1
+        for (int ch = 0; ch < KF / 32; ++ch) {
+          float uo[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = ch * 32 + j;
+            uo[j] = k < a.K ? __ldcs(up + (size_t)k * D) : 0.f;
+          }
+          uint32_t v[32];
+          umma::ld32(ACC + ch * 32, v);
+          umma::wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = ch * 32 + j;
+            const float tv = __uint_as_float(v[j]) * tsc;
+            const float uv = uo[j];
+            const float th_o = t0p ? (k < a.K ? __ldg(t0p + (size_t)k * D) : 0.f) : fminf(fmaxf(uv, -beta), beta);
+            const float un = tv - (th_o - uv);
+            const float th = fminf(fmaxf(un, -beta), beta);
+            const float zn = rho * (th - un);
+            const float d_tt = th - tv;
+            const float dz = rho * d_tt;
+            const float dth = th - th_o;
+            f0 += d_tt * d_tt;
+            f1 += th * th;
+            f2 += tv * tv;
+            f3 += dz * dz;
+            f4 += zn * zn;
+            f5 += dth * dth;
+            f6 = fmaxf(f6, fabsf(tv));
+            const float w = 2.f * th - un;
+            wmax = fmaxf(wmax, fabsf(w));
+            if (k < a.K) __stcs(up + (size_t)k * D, un);
+            v[j] = __float_as_uint(w);
+          }
+          umma::st32(ACC + ch * 32, v);
+        }
+        umma::wait_st();
+        const float sw = umma::pow2_scale(wmax);
+#pragma unroll 1
+        for (int ch = 0; ch < KF / 32; ++ch) {
+          uint32_t v[32];
+          umma::ld32(ACC + ch * 32, v);
+          umma::wait_ld();
+          uint32_t vh[16], vl[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            __half h0, l0, h1, l1;
+            umma::split2(__uint_as_float(v[2 * jj]), sw, h0, l0);
+            umma::split2(__uint_as_float(v[2 * jj + 1]), sw, h1, l1);
+            vh[jj] = umma::pack2(h0, h1);
+            vl[jj] = umma::pack2(l0, l1);
+          }
+          umma::st16(A + ch * 16, vh);
+          umma::st16(A + 64 + ch * 16, vl);
+        }
+        umma::wait_st();
+        umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(w_full + e);
+        st[0] += (double)f0; st[1] += (double)f1; st[2] += (double)f2; st[3] += (double)f3;
+        st[4] += (double)f4; st[5] += (double)f5; st[6] = fmax(st[6], (double)f6);
+        // --- col2im: s[r + oy][c + ox] += Z[p][o] into this warp's strip
+        const float zsc = dinv / sw;
+        float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;
+        mbar_wait(z_full + e, ph);
+        umma::fence_after_sync();
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          if (ch * 32 >= TAPS) break;
+          uint32_t v[32];
+          umma::ld32(ACC + ch * 32, v);
+          umma::wait_ld();
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int o = ch * 32 + jj;
+            if (o < TAPS) {
+              float* sp = S + (o / MW) * kTcStripW + (o % MW);
+              *sp = fmaf(__uint_as_float(v[jj]), zsc, *sp);
+              __syncwarp();
+            }
+          }
+        }
+      }
+      g += TPI;
+      // --- stop-test partial sums of the item (fixed order)
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        double x = st[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double y = __shfl_xor_sync(0xffffffffu, x, o);
+          x = i == 6 ? fmax(x, y) : x + y;
+        }
+        if (lane == 0) RED[ew * 8 + i] = x;
+      }
+      epi_sync();
+      if (et == 0) {
+        double* o = a.bsums + ((size_t)n * NBANDS + b) * kSums;
+        for (int i = 0; i < 7; ++i) {
+          double x = 0.0;
+          for (int w2 = 0; w2 < kTcEpiWarps; ++w2) x = i == 6 ? fmax(x, RED[w2 * 8 + i]) : x + RED[w2 * 8 + i];
+          o[i] = x;
+        }
+        o[7] = 0.0;
+      }
+      // --- strips -> band partial (strips summed in index order)
+      float* dst = a.spart + ((size_t)n * NBANDS + b) * SR * W;
+      for (int i = et; i < SR * W; i += 32 * kTcEpiWarps) {
+        const int lr = i / W, col = i % W;
+        float v = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < G::NSS; ++s2)
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {
+            int off = col - ((TPR == 1 ? 0 : s2 * 128) + 32 * q2);
+            if (off < 0) off += W;
+            if (off < 32 + MW - 1) v += STR[(s2 * 4 + q2) * G::STRIP + lr * kTcStripW + off];
+          }
+        dst[i] = v;
+      }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) {
+    umma::fence_after_sync();
+    umma::tmem_free<512>(tbase);
+  }
+}
+
+// s[n] = sum of the band partials (each output row from its own band and the
+// previous one, in that order); stop-test sums over bands -> sums[n] (G = 1).
+template <class G>
+__global__ void tc_band_reduce(const float* __restrict__ spart, const double* __restrict__ bsums,
+                               const int* __restrict__ conv, float* __restrict__ s, double* __restrict__ sums) {
+  constexpr int H = G::H, W = G::W, RB = G::RB, SR = G::SR, NBANDS = G::NBANDS, D = G::D;
+  const int n = blockIdx.y;
+  if (conv[n]) return;
+  const float* sp = spart + (size_t)n * NBANDS * SR * W;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
+    const int r = i / W, c = i % W;
+    const int b0 = r / RB, lr0 = r - b0 * RB;
+    const int bp = (b0 + NBANDS - 1) % NBANDS, lrp = lr0 + RB;
+    float v = 0.f;
+    if (lrp < SR) v = sp[((size_t)bp * SR + lrp) * W + c];
+    v += sp[((size_t)b0 * SR + lr0) * W + c];
+    s[(size_t)n * D + i] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int bb = 0; bb < NBANDS; ++bb) {
+      const double* o = bsums + ((size_t)n * NBANDS + bb) * kSums;
+      for (int i = 0; i < 6; ++i) acc[i] += o[i];
+      acc[6] = fmax(acc[6], o[6]);
+    }
+    double* o = sums + (size_t)n * kSums;
+    for (int i = 0; i < 7; ++i) o[i] = acc[i];
+    o[7] = 0.0;
+  }
+}
+
+// lambda (spatial, per image) -> f16 hi / lo pair planes scaled by a power of
+// two that maps max|lambda| to [2^13, 2^14).
+template <int D>
+__global__ void tc_lam_split(const float* __restrict__ lam, uint32_t* __restrict__ lam16, float* __restrict__ scale) {
+  __shared__ float red[32];
+  const int n = blockIdx.x;
+  const float2* l2 = reinterpret_cast<const float2*>(lam + (size_t)n * D);
+  float m = 0.f;
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    const float2 v = l2[i];
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  const float sc = umma::pow2_scale(red[0]);
+  if (threadIdx.x == 0) scale[n] = sc;
+  uint32_t* hi = lam16 + (size_t)n * D;
+  uint32_t* lo = hi + D / 2;
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    const float2 v = l2[i];
+    __half h0, l0, h1, l1;
+    umma::split2(v.x, sc, h0, l0);
+    umma::split2(v.y, sc, h1, l1);
+    hi[i] = umma::pack2(h0, h1);
+    lo[i] = umma::pack2(l0, l1);
+  }
+}
+
+// dictionary K x TAPS (FP64, tap o = y*MW + x) -> f16 hi / lo core-matrix grid:
+// element (k, o) at ((k/8)*16 + o/8)*64 + (k%8)*8 + o%8 halves; zero padded to KF x 128.
+template <int KF>
+__global__ void tc_dsplit(const double* __restrict__ d, int K, int taps, float scale, __half* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KF * kTcTaps; i += gridDim.x * blockDim.x) {
+    const int k = i / kTcTaps, o = i % kTcTaps;
+    const float v = (k < K && o < taps) ? (float)d[(size_t)k * taps + o] : 0.f;
+    __half hi, lo;
+    umma::split2(v, scale, hi, lo);
+    const int idx = (((k >> 3) * 16 + (o >> 3)) * 8 + (k & 7)) * 8 + (o & 7);
+    out[idx] = hi;
+    out[KF * kTcTaps + idx] = lo;
+  }
+}
+
+}  // namespace dcsc_cuda
