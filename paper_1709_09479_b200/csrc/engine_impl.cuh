@@ -241,8 +241,28 @@ class Engine final : public EngineBase {
   using TG = TcGeom<H, W, KF, 11, 11, 16>;
   template <int KF>
   static void set_tc_attr() {
-    CK(cudaFuncSetAttribute((const void*)coding_pass_tc<TG<KF>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)TG<KF>::smem));
+    const int sm = (int)TG<KF>::smem;
+    CK(cudaFuncSetAttribute((const void*)coding_pass_tc<TG<KF>, true, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute((const void*)coding_pass_tc<TG<KF>, true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute((const void*)coding_pass_tc<TG<KF>, false, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute((const void*)coding_pass_tc<TG<KF>, false, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  }
+  template <int KF>
+  void launch_tc(int grid, const TcArgs& a) {
+    constexpr size_t sm = TG<KF>::smem;
+    const bool full = a.K == KF, t0 = a.theta0 != nullptr;
+    if (full && !t0)
+      coding_pass_tc<TG<KF>, true, false><<<grid, kTcThreads, sm, st_>>>(a);
+    else if (full)
+      coding_pass_tc<TG<KF>, true, true><<<grid, kTcThreads, sm, st_>>>(a);
+    else if (!t0)
+      coding_pass_tc<TG<KF>, false, false><<<grid, kTcThreads, sm, st_>>>(a);
+    else
+      coding_pass_tc<TG<KF>, false, true><<<grid, kTcThreads, sm, st_>>>(a);
   }
   // persistent pipelined r2c / c2r (SmemPipe) when the staging buffer fits and
   // the planes are 16-byte aligned storage-precision planes: grid = resident slots
@@ -664,9 +684,9 @@ class Engine final : public EngineBase {
       const int grid = std::min(tc_grid_, cnt * G::NBANDS);
       launch(kFamCoding, [&] {
         if (tc_kf_ == 64)
-          coding_pass_tc<TG<64>><<<grid, kTcThreads, TG<64>::smem, st_>>>(a);
+          launch_tc<64>(grid, a);
         else
-          coding_pass_tc<TG<128>><<<grid, kTcThreads, TG<128>::smem, st_>>>(a);
+          launch_tc<128>(grid, a);
       });
       R* s = lam_.as<R>() + (size_t)n0 * D;          // s reuses the spatial lambda planes
       C* spec = part_.as<C>() + (size_t)n0 * NB;      // one partial spectrum per image (G = 1)

@@ -136,7 +136,9 @@ __device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint
   }
 }
 
-template <class G>
+// FULL: K == KF (no padded filters); T0: a.theta0 is set (first iteration of a
+// warm state that is not ADMM-consistent).
+template <class G, bool FULL, bool T0>
 __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
   constexpr int H = G::H, W = G::W, KF = G::KF, MW = G::MW, RB = G::RB, D = G::D, TPR = G::TPR,
                 NBANDS = G::NBANDS, TPI = G::TPI, SR = G::SR, LWW = G::LWW, TAPS = G::TAPS;
@@ -265,16 +267,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
         // --- prox on T, w -> A (two f16 planes, per-pixel scale)
         float* const up = ubase + (size_t)r * W + c;
         const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
-        float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f, f4 = 0.f, f5 = 0.f, f6 = 0.f, wmax = 0.f;
+        // stop-test sums (coding.cpp:237-259): sum dz^2 = rho^2 sum (theta' - t)^2 and
+        // sum z'^2 = rho^2 sum (theta' - u')^2 are scaled once per tile
+        float f0 = 0.f, f1 = 0.f, f2 = 0.f, f4 = 0.f, f5 = 0.f, f6 = 0.f, wmax = 0.f;
         mbar_wait(t_full + e, ph);
         umma::fence_after_sync();
 #pragma unroll 1
         for (int ch = 0; ch < KF / 32; ++ch) {
-          float uo[32];
+          float uo[32], t0v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int k = ch * 32 + j;
-            uo[j] = k < a.K ? __ldcs(up + (size_t)k * D) : 0.f;
+            uo[j] = (FULL || k < a.K) ? __ldcs(up + (size_t)k * D) : 0.f;
+            if constexpr (T0) t0v[j] = (FULL || k < a.K) ? __ldg(t0p + (size_t)k * D) : 0.f;
           }
           uint32_t v[32];
           umma::ld32(ACC + ch * 32, v);
@@ -284,23 +289,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
             const int k = ch * 32 + j;
             const float tv = __uint_as_float(v[j]) * tsc;
             const float uv = uo[j];
-            const float th_o = t0p ? (k < a.K ? __ldg(t0p + (size_t)k * D) : 0.f) : fminf(fmaxf(uv, -beta), beta);
+            float th_o;
+            if constexpr (T0) th_o = t0v[j]; else th_o = fminf(fmaxf(uv, -beta), beta);
             const float un = tv - (th_o - uv);
             const float th = fminf(fmaxf(un, -beta), beta);
-            const float zn = rho * (th - un);
-            const float d_tt = th - tv;
-            const float dz = rho * d_tt;
-            const float dth = th - th_o;
-            f0 += d_tt * d_tt;
-            f1 += th * th;
-            f2 += tv * tv;
-            f3 += dz * dz;
-            f4 += zn * zn;
-            f5 += dth * dth;
+            const float d_tt = th - tv, d_z = th - un, dth = th - th_o;
+            f0 = fmaf(d_tt, d_tt, f0);
+            f1 = fmaf(th, th, f1);
+            f2 = fmaf(tv, tv, f2);
+            f4 = fmaf(d_z, d_z, f4);
+            f5 = fmaf(dth, dth, f5);
             f6 = fmaxf(f6, fabsf(tv));
-            const float w = 2.f * th - un;
+            const float w = fmaf(2.f, th, -un);
             wmax = fmaxf(wmax, fabsf(w));
-            if (k < a.K) __stcs(up + (size_t)k * D, un);
+            if (FULL || k < a.K) __stcs(up + (size_t)k * D, un);
             v[j] = __float_as_uint(w);
           }
           umma::st32(ACC + ch * 32, v);
@@ -314,13 +316,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
           umma::wait_ld();
           uint32_t vh[16], vl[16];
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            __half h0, l0, h1, l1;
-            umma::split2(__uint_as_float(v[2 * jj]), sw, h0, l0);
-            umma::split2(__uint_as_float(v[2 * jj + 1]), sw, h1, l1);
-            vh[jj] = umma::pack2(h0, h1);
-            vl[jj] = umma::pack2(l0, l1);
-          }
+          for (int jj = 0; jj < 16; ++jj)
+            umma::split2x2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1]), sw, vh[jj], vl[jj]);
           umma::st16(A + ch * 16, vh);
           umma::st16(A + 64 + ch * 16, vl);
         }
@@ -328,8 +325,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
         umma::fence_before_sync();
         __syncwarp();
         if (lane == 0) mbar_arrive1(w_full + e);
-        st[0] += (double)f0; st[1] += (double)f1; st[2] += (double)f2; st[3] += (double)f3;
-        st[4] += (double)f4; st[5] += (double)f5; st[6] = fmax(st[6], (double)f6);
+        const float rho2 = rho * rho;
+        st[0] += (double)f0; st[1] += (double)f1; st[2] += (double)f2; st[3] += (double)(rho2 * f0);
+        st[4] += (double)(rho2 * f4); st[5] += (double)f5; st[6] = fmax(st[6], (double)f6);
         // --- col2im: s[r + oy][c + ox] += Z[p][o] into this warp's strip
         const float zsc = dinv / sw;
         float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;
@@ -459,11 +457,7 @@ __global__ void tc_lam_split(const float* __restrict__ lam, uint32_t* __restrict
   uint32_t* lo = hi + D / 2;
   for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
     const float2 v = l2[i];
-    __half h0, l0, h1, l1;
-    umma::split2(v.x, sc, h0, l0);
-    umma::split2(v.y, sc, h1, l1);
-    hi[i] = umma::pack2(h0, h1);
-    lo[i] = umma::pack2(l0, l1);
+    umma::split2x2(v.x, v.y, sc, hi[i], lo[i]);
   }
 }
 

@@ -125,6 +125,17 @@ __device__ __forceinline__ void split2(float x, float scale, __half& hi, __half&
   hi = __float2half_rn(xs);
   lo = __float2half_rn(xs - __half2float(hi));
 }
+// Two values at once with packed conversions (F2FP / HADD2.F32 on the FMA and
+// ALU pipes; the scalar F2F conversions issue on the quarter-rate XU pipe):
+// hi / lo = f16 pairs (low half = a) of (a, b) * scale.
+__device__ __forceinline__ void split2x2(float a, float b, float scale, uint32_t& hi, uint32_t& lo) {
+  const float as = a * scale, bs = b * scale;
+  const __half2 h = __float22half2_rn(make_float2(as, bs));
+  const float2 hb = __half22float2(h);
+  const __half2 l = __float22half2_rn(make_float2(as - hb.x, bs - hb.y));
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 __device__ __forceinline__ uint32_t pack2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
