@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -552,6 +553,18 @@ class Engine final : public EngineBase {
         tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
         device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes;
         CK(cudaDeviceGetAttribute(&tc_grid_, cudaDevAttrMultiProcessorCount, o.device));
+        // TMA map of u as [N*K planes][D pixels] FP32, box 16 planes x 128 pixels
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+        if (!fn || qr != cudaDriverEntryPointSuccess) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        const cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)N_ * K_};
+        const cuuint64_t gstr[1] = {(cuuint64_t)D * sizeof(float)};
+        const cuuint32_t box[2] = {128u, 16u}, estr[2] = {1u, 1u};
+        const CUresult cr = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
+            &tc_umap_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, u_.p, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
         if (std::getenv("DCSC_VERBOSE")) std::fprintf(stderr, "dcsc: tensor-core coding pass (KF=%d)\n", tc_kf_);
       }
     }
@@ -681,6 +694,8 @@ class Engine final : public EngineBase {
       a.K = K_;
       a.rho = (float)cfg_.rho;
       a.beta = (float)cfg_.beta;
+      a.umap = tc_umap_;
+      a.plane0 = n0 * K_;
       const int grid = std::min(tc_grid_, cnt * G::NBANDS);
       launch(kFamCoding, [&] {
         if (tc_kf_ == 64)
@@ -2163,6 +2178,7 @@ class Engine final : public EngineBase {
   int tc_kf_ = 128, tc_grid_ = 148;
   float tc_dscale_ = 1.f;
   DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_;
+  CUtensorMap tc_umap_{};
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   std::vector<int> degen_;  // per image: normalisation met a constant input
   C* xh_ch_ = nullptr;   // learning view: x_hat of the current channel (N x NB)

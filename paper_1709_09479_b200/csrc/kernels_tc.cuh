@@ -28,17 +28,33 @@
 // Work item = (image, band of RB tile rows); deterministic: every sum has a
 // fixed order (per-warp col2im strips, strips and bands summed in index order).
 #pragma once
+#include <cuda.h>
+
 #include "kernels.cuh"
 #include "umma.cuh"
 
 namespace dcsc_cuda {
 
+#ifdef DCSC_TC_TRACE  // per-phase globaltimer trace of one epilogue warp (CTA 0, group 0, warp 1), a few tiles
+#define TCT(slot)                                                                              \
+  if (blockIdx.x == 0 && threadIdx.x == 32 && t >= 2 && t < 8) {                              \
+    unsigned long long tt_;                                                                    \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_));                                   \
+    tr[(t - 2) / 2][slot] = tt_;                                                               \
+  }
+#else
+#define TCT(slot)
+#endif
+
 constexpr int kTcTaps = 128;                       // GEMM-1 K / GEMM-2 N (taps padded)
 constexpr int kTcEpiWarps = 8;
-constexpr int kTcThreads = 32 * (kTcEpiWarps + 1);  // 288
-constexpr int kTcStripW = 44;                      // col2im strip row stride (floats) >= 32 + MW - 1
+constexpr int kTcThreads = 32 * (kTcEpiWarps + 2);  // 320: MMA warp, 8 epilogue warps, u streaming warp
+constexpr int kTcStripW = 44;
+constexpr int kTcUSlots = 4;                       // u staging ring depth per epilogue group                      // col2im strip row stride (floats) >= 32 + MW - 1
 
 struct TcArgs {
+  CUtensorMap umap;        // u as [N*K planes][D pixels] FP32, box [16 planes][128 pixels]
+  int plane0;              // umap plane of (image 0 of this launch, filter 0)
   const uint32_t* lam16;   // N x 2 x H x W/2 words: f16 pairs of lambda * lam_scale[n] (hi plane, lo plane)
   const float* lam_scale;  // N
   const __half* dsplit;    // 2 x KF x 128 f16 core-matrix grid of d * d_scale (hi, lo)
@@ -76,12 +92,24 @@ struct TcGeom {
   static constexpr size_t strip_bytes = (size_t)NSTRIP * STRIP * 4;
   static constexpr size_t red_off = strip_off + strip_bytes;
   static constexpr size_t red_bytes = (size_t)8 * kTcEpiWarps * 8;
-  static constexpr size_t bar_off = red_off + red_bytes;
-  static constexpr size_t smem = bar_off + 16 * 8;
+  // u staging: per epilogue group a ring of kTcUSlots chunks of 16 filter rows x 128 pixels (TMA bulk copies)
+  static constexpr size_t ubuf_off = (red_off + red_bytes + 127) / 128 * 128;
+  static constexpr size_t ubuf_bytes = (size_t)2 * kTcUSlots * 16 * 128 * 4;
+  static constexpr size_t bar_off = ubuf_off + ubuf_bytes;
+  static constexpr size_t smem = bar_off + 32 * 8;
 };
 
 __device__ __forceinline__ void mbar_arrive1(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcEpiWarps) : "memory"); }
 __device__ __forceinline__ uint32_t lds_u16(const void* p) {
@@ -139,7 +167,7 @@ __device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint
 // FULL: K == KF (no padded filters); T0: a.theta0 is set (first iteration of a
 // warm state that is not ADMM-consistent).
 template <class G, bool FULL, bool T0>
-__global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_constant__ TcArgs a) {
   constexpr int H = G::H, W = G::W, KF = G::KF, MW = G::MW, RB = G::RB, D = G::D, TPR = G::TPR,
                 NBANDS = G::NBANDS, TPI = G::TPI, SR = G::SR, LWW = G::LWW, TAPS = G::TAPS;
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -149,7 +177,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
   double* RED = reinterpret_cast<double*>(sm + G::red_off);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + G::bar_off);
   unsigned long long *a_full = bars, *t_full = bars + 2, *w_full = bars + 4, *z_full = bars + 6, *dbar = bars + 8;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
+  unsigned long long *ufull = bars + 9, *uempty = bars + 9 + 2 * kTcUSlots;  // [group][slot]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9 + 4 * kTcUSlots);
+  float* UB = reinterpret_cast<float*>(sm + G::ubuf_off);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) umma::tmem_alloc<512>(tslot);
@@ -161,6 +191,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
       mbar_init(z_full + i, 1);
     }
     mbar_init(dbar, 1);
+    for (int i = 0; i < 2 * kTcUSlots; ++i) {
+      mbar_init(ufull + i, 1);
+      mbar_init(uempty + i, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   umma::fence_before_sync();
@@ -169,54 +203,100 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
   const uint32_t tbase = *tslot;
   const int items = a.N * NBANDS;
 
-  if (warp == 0) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+  constexpr int NCU = KF / 16, NCHUNK = (TPI / 2) * NCU;  // u chunks per item and group
+  if (warp == 0 || warp == kTcEpiWarps + 1) {
+    // ===== producer warps: GEMM issue (warp 0, lane 0); u row streaming by TMA (last warp) =====
+    if (warp == 0 && lane == 0) {
       mbar_expect_tx(dbar, (unsigned)G::d_bytes);
       for (int i = 0; i < (int)(G::d_bytes / 16384); ++i)
         bulk_g2s(const_cast<__half*>(Ds) + i * 8192, a.dsplit + i * 8192, 16384u, dbar);
       mbar_wait(dbar, 0);
-      const uint32_t dh = umma::smem_u32(Ds), dl = dh + KF * kTcTaps * 2;
-      constexpr uint32_t id1 = umma::idesc_f16(128, KF, 0), id2 = umma::idesc_f16(128, kTcTaps, 1);
-      auto gemm1 = [&](uint32_t gg) {
-        const uint32_t s = gg & 1u, ph = (gg >> 1) & 1u;
-        mbar_wait(a_full + s, ph);
-        umma::fence_after_sync();
-        const uint32_t A = tbase + 256u * s, acc = A + 128u;
+    }
+    __syncwarp();
+    const uint32_t dh = umma::smem_u32(Ds), dl = dh + KF * kTcTaps * 2;
+    constexpr uint32_t id1 = umma::idesc_f16(128, KF, 0), id2 = umma::idesc_f16(128, kTcTaps, 1);
+    auto gemm1 = [&](uint32_t gg) {
+      const uint32_t s = gg & 1u;
+      umma::fence_after_sync();
+      const uint32_t A = tbase + 256u * s, acc = A + 128u;
 #pragma unroll
-        for (int j = 0; j < kTcTaps / 16; ++j) {  // K = taps; B K-major: LBO 128 B (taps), SBO 2048 B (filters)
-          const uint64_t bh = umma::sdesc(dh + 256u * j, 128u, 2048u), bl = umma::sdesc(dl + 256u * j, 128u, 2048u);
-          umma::mma_ts(acc, A + 8u * j, bh, id1, j > 0);
-          umma::mma_ts(acc, A + 8u * j, bl, id1, 1u);
-          umma::mma_ts(acc, A + 64u + 8u * j, bh, id1, 1u);
-        }
-        umma::commit(t_full + s);
-      };
-      auto gemm2 = [&](uint32_t gg) {
-        const uint32_t s = gg & 1u, ph = (gg >> 1) & 1u;
-        mbar_wait(w_full + s, ph);
-        umma::fence_after_sync();
-        const uint32_t A = tbase + 256u * s, acc = A + 128u;
+      for (int j = 0; j < kTcTaps / 16; ++j) {  // K = taps; B K-major: LBO 128 B (taps), SBO 2048 B (filters)
+        const uint64_t bh = umma::sdesc(dh + 256u * j, 128u, 2048u), bl = umma::sdesc(dl + 256u * j, 128u, 2048u);
+        umma::mma_ts(acc, A + 8u * j, bh, id1, j > 0);
+        umma::mma_ts(acc, A + 8u * j, bl, id1, 1u);
+        umma::mma_ts(acc, A + 64u + 8u * j, bh, id1, 1u);
+      }
+      umma::commit(t_full + s);
+    };
+    auto gemm2 = [&](uint32_t gg) {
+      const uint32_t s = gg & 1u;
+      umma::fence_after_sync();
+      const uint32_t A = tbase + 256u * s, acc = A + 128u;
 #pragma unroll
-        for (int j = 0; j < KF / 16; ++j) {  // K = filters; B MN-major: LBO 2048 B (filters), SBO 128 B (taps)
-          const uint64_t bh = umma::sdesc(dh + 4096u * j, 2048u, 128u), bl = umma::sdesc(dl + 4096u * j, 2048u, 128u);
-          umma::mma_ts(acc, A + 8u * j, bh, id2, j > 0);
-          umma::mma_ts(acc, A + 8u * j, bl, id2, 1u);
-          umma::mma_ts(acc, A + 64u + 8u * j, bh, id2, 1u);
+      for (int j = 0; j < KF / 16; ++j) {  // K = filters; B MN-major: LBO 2048 B (filters), SBO 128 B (taps)
+        const uint64_t bh = umma::sdesc(dh + 4096u * j, 2048u, 128u), bl = umma::sdesc(dl + 4096u * j, 2048u, 128u);
+        umma::mma_ts(acc, A + 8u * j, bh, id2, j > 0);
+        umma::mma_ts(acc, A + 8u * j, bl, id2, 1u);
+        umma::mma_ts(acc, A + 64u + 8u * j, bh, id2, 1u);
+      }
+      umma::commit(z_full + s);
+    };
+    int ntiles = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x)
+      if (!a.conv[item / NBANDS]) ntiles += TPI;
+    // per group: next chunk (item, index within the item) and its ring sequence number
+    int c_item[2], c_i[2];
+    uint32_t c_seq[2] = {0u, 0u};
+    auto next_active = [&](int item) {
+      while (item < items && a.conv[item / NBANDS]) item += gridDim.x;
+      return item;
+    };
+    c_item[0] = c_item[1] = next_active(blockIdx.x);
+    c_i[0] = c_i[1] = 0;
+    uint32_t n1 = 0, n2 = 0;
+    auto lane0_test = [&](unsigned long long* bar, unsigned par) {
+      int r = 0;
+      if (lane == 0) r = mbar_test(bar, par) ? 1 : 0;
+      return __shfl_sync(0xffffffffu, r, 0) != 0;
+    };
+    if (warp == 0) {
+      // GEMMs: whichever is ready first (GEMM-1 of the next tile, GEMM-2 of the oldest pending)
+      while (lane == 0 && (int)n2 < ntiles) {
+        if ((int)n1 < ntiles && mbar_test(a_full + (n1 & 1u), (n1 >> 1) & 1u)) {
+          gemm1(n1++);
+        } else if (n2 < n1 && mbar_test(w_full + (n2 & 1u), (n2 >> 1) & 1u)) {
+          gemm2(n2++);
         }
-        umma::commit(z_full + s);
-      };
-      // GEMM-2 of a tile is issued after GEMM-1 of the next one, but never
-      // across items: the epilogue groups meet at an item boundary.
-      uint32_t g = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        if (a.conv[item / NBANDS]) continue;
-        for (int t = 0; t < TPI; ++t) {
-          gemm1(g + t);
-          if (t > 0) gemm2(g + t - 1);
+      }
+    } else
+    while (c_item[0] < items || c_item[1] < items) {
+      // u rows: chunk i of an item = tile e + 2 (i / NCU), filter rows 16 (i % NCU) .. + 16
+      for (int e = 0; e < 2; ++e) {
+        while (c_item[e] < items) {  // every free ring slot
+        const uint32_t ci = c_seq[e], sl = ci % kTcUSlots;
+        if (ci >= (uint32_t)kTcUSlots && !lane0_test(uempty + e * kTcUSlots + sl, ((ci / kTcUSlots) - 1) & 1u))
+          break;
+        const int n = c_item[e] / NBANDS, b = c_item[e] % NBANDS, i = c_i[e];
+        const int t = e + 2 * (i / NCU), k0 = 16 * (i % NCU);
+        const int r = b * RB + t / TPR, c0 = (t % TPR) * 128;
+        const int nv = FULL ? 16 : max(0, min(16, a.K - k0));
+        unsigned long long* fb = ufull + e * kTcUSlots + sl;
+        (void)nv;
+        if (lane == 0) {  // one 2-D TMA: 16 planes x 128 pixels (rows past the last plane are zero-filled)
+          mbar_expect_tx(fb, 16u * 128u * 4u);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                  smem_addr(UB + (size_t)(e * kTcUSlots + sl) * 16 * 128)),
+              "l"(&a.umap), "r"(r * W + c0), "r"(a.plane0 + n * a.K + k0), "r"(smem_addr(fb))
+              : "memory");
         }
-        gemm2(g + TPI - 1);
-        g += TPI;
+        __syncwarp();
+        ++c_seq[e];
+        if (++c_i[e] == NCHUNK) {
+          c_i[e] = 0;
+          c_item[e] = next_active(c_item[e] + gridDim.x);
+        }
+        }
       }
     }
   } else {
@@ -225,7 +305,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     const uint32_t A = tbase + 256u * e + lane_off, ACC = A + 128u;
     const float rho = a.rho, beta = a.beta;
-    uint32_t g = 0;
+    uint32_t g = 0, uc = 0;  // tiles / u chunks (per group) of this CTA's earlier items
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int n = item / NBANDS, b = item % NBANDS;
       if (a.conv[n]) continue;
@@ -246,51 +326,67 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
       double st[7] = {0, 0, 0, 0, 0, 0, 0};
       float* const ubase = a.u + (size_t)n * a.K * D;
       const float* const t0base = a.theta0 ? a.theta0 + (size_t)n * a.K * D : nullptr;
-      auto prefetch_tile = [&](int t) {
-        if (t < TPI && p < a.K) {
-          const int r = b * RB + t / TPR, c0 = (t % TPR) * 128;
-          prefetch_l2_bulk(ubase + (size_t)p * D + r * W + c0, 512u);
-        }
+      // u rows arrive in this group's ring by TMA (producer warp); every warp
+      // releases a slot once it holds the chunk in registers
+      float* const ring = UB + (size_t)e * kTcUSlots * 16 * 128;
+      unsigned long long* const uf = ufull + e * kTcUSlots;
+      unsigned long long* const ue = uempty + e * kTcUSlots;
+      int ci_next = 0;  // next chunk this warp consumes (item-relative)
+      auto take_chunk = [&](float (&uo)[16]) {
+        const uint32_t ci = uc + (uint32_t)ci_next, sl = ci % kTcUSlots;
+        mbar_wait(uf + sl, (ci / kTcUSlots) & 1u);
+        const float* src = ring + (size_t)sl * 16 * 128 + p;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) uo[j] = src[j * 128];
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(ue + sl);
+        ++ci_next;
       };
-      prefetch_tile(e);
+#ifdef DCSC_TC_TRACE
+      unsigned long long tr[3][8] = {};
+#endif
       for (int t = e; t < TPI; t += 2) {
+        TCT(0)
         const uint32_t gg = g + t, ph = (gg >> 1) & 1u;
         const int rl = t / TPR, tc = t % TPR;
         const int r = b * RB + rl, c = tc * 128 + p;
-        prefetch_tile(t + 2);
+        float* const up = ubase + (size_t)r * W + c;
+        const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
         // --- im2col(lambda) -> A
         tc_build_im2col<G>(LAM + rl * LWW, c, A);
         umma::wait_st();
         umma::fence_before_sync();
         __syncwarp();
         if (lane == 0) mbar_arrive1(a_full + e);
+        TCT(1)
         // --- prox on T, w -> A (two f16 planes, per-pixel scale)
-        float* const up = ubase + (size_t)r * W + c;
-        const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
         // stop-test sums (coding.cpp:237-259): sum dz^2 = rho^2 sum (theta' - t)^2 and
         // sum z'^2 = rho^2 sum (theta' - u')^2 are scaled once per tile
         float f0 = 0.f, f1 = 0.f, f2 = 0.f, f4 = 0.f, f5 = 0.f, f6 = 0.f, wmax = 0.f;
         mbar_wait(t_full + e, ph);
         umma::fence_after_sync();
+        TCT(2)
 #pragma unroll 1
-        for (int ch = 0; ch < KF / 32; ++ch) {
-          float uo[32], t0v[32];
+        for (int ch = 0; ch < KF / 16; ++ch) {
+          float ucur[16], tcur[16];
+          take_chunk(ucur);
+          if constexpr (T0) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int k = ch * 32 + j;
-            uo[j] = (FULL || k < a.K) ? __ldcs(up + (size_t)k * D) : 0.f;
-            if constexpr (T0) t0v[j] = (FULL || k < a.K) ? __ldg(t0p + (size_t)k * D) : 0.f;
+            for (int j = 0; j < 16; ++j) {
+              const int k = ch * 16 + j;
+              tcur[j] = (FULL || k < a.K) ? __ldg(t0p + (size_t)k * D) : 0.f;
+            }
           }
-          uint32_t v[32];
-          umma::ld32(ACC + ch * 32, v);
+          uint32_t v[16];
+          umma::ld16(ACC + ch * 16, v);
           umma::wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int k = ch * 32 + j;
+          for (int j = 0; j < 16; ++j) {
+            const int k = ch * 16 + j;
             const float tv = __uint_as_float(v[j]) * tsc;
-            const float uv = uo[j];
+            const float uv = (FULL || k < a.K) ? ucur[j] : 0.f;
             float th_o;
-            if constexpr (T0) th_o = t0v[j]; else th_o = fminf(fmaxf(uv, -beta), beta);
+            if constexpr (T0) th_o = tcur[j]; else th_o = fminf(fmaxf(uv, -beta), beta);
             const float un = tv - (th_o - uv);
             const float th = fminf(fmaxf(un, -beta), beta);
             const float d_tt = th - tv, d_z = th - un, dth = th - th_o;
@@ -305,8 +401,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
             if (FULL || k < a.K) __stcs(up + (size_t)k * D, un);
             v[j] = __float_as_uint(w);
           }
-          umma::st32(ACC + ch * 32, v);
+          umma::st16(ACC + ch * 16, v);
         }
+        TCT(3)
         umma::wait_st();
         const float sw = umma::pow2_scale(wmax);
 #pragma unroll 1
@@ -325,6 +422,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
         umma::fence_before_sync();
         __syncwarp();
         if (lane == 0) mbar_arrive1(w_full + e);
+        TCT(4)
         const float rho2 = rho * rho;
         st[0] += (double)f0; st[1] += (double)f1; st[2] += (double)f2; st[3] += (double)(rho2 * f0);
         st[4] += (double)(rho2 * f4); st[5] += (double)f5; st[6] = fmax(st[6], (double)f6);
@@ -333,24 +431,37 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(TcArgs a) {
         float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;
         mbar_wait(z_full + e, ph);
         umma::fence_after_sync();
+        TCT(5)
+        {
+          uint32_t v[4][32];
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          if (ch * 32 >= TAPS) break;
-          uint32_t v[32];
-          umma::ld32(ACC + ch * 32, v);
+          for (int ch = 0; ch < 4; ++ch)
+            if (ch * 32 < TAPS) umma::ld32(ACC + ch * 32, v[ch]);
           umma::wait_ld();
+          // taps (oy, ox) of one ox touch distinct strip rows: 11 independent
+          // read-modify-writes between warp syncs (lanes overlap only along ox)
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const int o = ch * 32 + jj;
-            if (o < TAPS) {
-              float* sp = S + (o / MW) * kTcStripW + (o % MW);
-              *sp = fmaf(__uint_as_float(v[jj]), zsc, *sp);
-              __syncwarp();
+          for (int ox = 0; ox < MW; ++ox) {
+#pragma unroll
+            for (int oy = 0; oy < G::MH; ++oy) {
+              const int o = oy * MW + ox;
+              float* sp = S + oy * kTcStripW + ox;
+              *sp = fmaf(__uint_as_float(v[o / 32][o % 32]), zsc, *sp);
             }
+            __syncwarp();
           }
         }
+        TCT(6)
       }
+#ifdef DCSC_TC_TRACE
+      if (blockIdx.x == 0 && threadIdx.x == 32 && item == (int)blockIdx.x)
+        for (int f = 0; f < 3; ++f)
+          printf("TCT tile %d: build %llu waitG1 %llu epi1 %llu split %llu waitG2 %llu col2im %llu | next %llu\n", 2 + 2 * f,
+                 tr[f][1] - tr[f][0], tr[f][2] - tr[f][1], tr[f][3] - tr[f][2], tr[f][4] - tr[f][3],
+                 tr[f][5] - tr[f][4], tr[f][6] - tr[f][5], f < 2 ? tr[f + 1][0] - tr[f][6] : 0ull);
+#endif
       g += TPI;
+      uc += NCHUNK;
       // --- stop-test partial sums of the item (fixed order)
 #pragma unroll
       for (int i = 0; i < 7; ++i) {

@@ -109,6 +109,58 @@ __global__ void __launch_bounds__(128, 1)
   if (w == 0) umma::tmem_free<512>(base);
 }
 
+__global__ void __launch_bounds__(128, 1) probe_time(int reps, long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char dsm[];
+  __half* Dh = reinterpret_cast<__half*>(dsm);
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) unsigned long long bar;
+  const int p = threadIdx.x, w = p >> 5;
+  if (w == 0) umma::tmem_alloc<512>(&tslot);
+  if (p == 0) bar_init(&bar, 1);
+  for (int i = p; i < 2 * 128 * 128; i += 128) Dh[i] = __float2half(0.001f * (i % 7));
+  umma::fence_proxy_async();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t base = tslot;
+  if (p == 0) {
+    const uint32_t dh = umma::smem_u32(Dh), dl = dh + 128 * 128 * 2;
+    const uint32_t id1 = umma::idesc_f16(128, 128, 0), id2 = umma::idesc_f16(128, 128, 1);
+    unsigned ph = 0;
+    for (int mode = 0; mode < 2; ++mode) {
+      long long t0 = clock64();
+      for (int r = 0; r < reps; ++r) {
+        for (int j = 0; j < 8; ++j) {
+          const uint64_t bh = mode == 0 ? umma::sdesc(dh + j * 256, 128, 2048) : umma::sdesc(dh + j * 4096, 2048, 128);
+          const uint64_t bl = mode == 0 ? umma::sdesc(dl + j * 256, 128, 2048) : umma::sdesc(dl + j * 4096, 2048, 128);
+          const uint32_t id = mode == 0 ? id1 : id2;
+          umma::mma_ts(base + 256, base + j * 8, bh, id, j > 0);
+          umma::mma_ts(base + 256, base + j * 8, bl, id, 1);
+          umma::mma_ts(base + 256, base + 64 + j * 8, bh, id, 1);
+        }
+      }
+      umma::commit(&bar);
+      bar_wait(&bar, ph);
+      ph ^= 1;
+      cyc[mode] = clock64() - t0;
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (w == 0) umma::tmem_free<512>(base);
+}
+
+extern "C" int umma_time(int reps, long long* out) {
+  long long* d;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(probe_time, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  probe_time<<<1, 128, 65536>>>(reps, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(out, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return (int)e;
+}
+
 extern "C" int umma_probe(const float* hA1, const float* hD, const float* hW, float sA, float sD, float* hT,
                           float* hZ, int variant) {
   float *A1, *Dm, *Wm, *T, *Z;

@@ -51,6 +51,11 @@ def run():
             # diagnose layout: correlation with permuted references
             print("T[0,:8]", T[0, :8]); print("Tref[0,:8]", Tref[0, :8])
             print("Z[0,:8]", Z[0, :8]); print("Zref[0,:8]", Zref[0, :8])
+    out = (ctypes.c_longlong * 2)()
+    lib.umma_time.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)]
+    lib.umma_time(200, out)
+    per = [out[i] / (200 * 24) for i in range(2)]
+    print(f"cycles per 128x128x16 f16 MMA (A tmem): B K-major {per[0]:.1f}, B MN-major {per[1]:.1f}")
     # FP32 baseline error for comparison
     T32 = A1 @ Dm.T
     print("fp32 numpy T rel err", np.abs(T32 - Tref).max() / np.abs(Tref).max())
