@@ -266,10 +266,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
           gemm1(n1++);
         } else if (n2 < n1 && mbar_test(w_full + (n2 & 1u), (n2 >> 1) & 1u)) {
           gemm2(n2++);
+        } else {
+          __nanosleep(40);  // keep the polling off the epilogue warps' issue slots
         }
       }
     } else
     while (c_item[0] < items || c_item[1] < items) {
+      const uint32_t seq0 = c_seq[0] + c_seq[1];
       // u rows: chunk i of an item = tile e + 2 (i / NCU), filter rows 16 (i % NCU) .. + 16
       for (int e = 0; e < 2; ++e) {
         while (c_item[e] < items) {  // every free ring slot
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         }
         }
       }
+      if (c_seq[0] + c_seq[1] == seq0) __nanosleep(100);
     }
   } else {
     // ===== epilogue groups =====
