@@ -83,6 +83,15 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_tensor_peak():
+    """Dense f16/bf16 tensor peak (TFLOP/s): MEASURED_PEAKS.json burst figure, else the recipe's nominal."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    except Exception:
+        return 2250.0, "fallback"
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -468,6 +477,7 @@ def run_ours(args, cfg):
     sc = dcsc.SolverConfig(beta=cfg["beta"], max_admm=cfg["max_admm"], normalize=0, seed=SEED, tol=1e-300)
     ctx = dcsc.Context(nl, (cfg["H"], cfg["W"]), cfg["K"], (cfg["m"], cfg["m"]), sc, cfg["prec"],
                        device=dev, channels=cfg.get("J", 1))
+    coding_path = ctx.coding_path()
     nccl_ranks = None
     if world > 1 and not weak:
         import torch
@@ -577,6 +587,7 @@ def run_ours(args, cfg):
                                                              "device-resident by design)")),
                 "outer_iters": ([r["outer_iter"] for r in rows_e2e if r["phase"] == 0] if not weak else None)},
         "gpu_launches": launches,
+        "coding_path": coding_path,
     }
     if not weak:
         out["timed_outer_iters"] = timed_idx
@@ -597,11 +608,36 @@ def run_ours(args, cfg):
             algo_total = (admm_total / world * (4 * cfg["K"] * D * s + Dh * 2 * s)
                           + cod_n * cfg["K"] * Dh * 2 * s)
         achieved = algo_total / (cod_ms / 1000.0) / 1e9
-        out["roofline"] = {"bound": "hbm", "kernel": "coding_pass<ADMM> (coding_pass_cl at 256x256)",
-                           "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                           "frac": achieved / peak, "traffic": traffic_from_profiles(args.config),
-                           "algorithmic_bytes_per_launch": algo_total / cod_n, "avg_launch_ms": avg,
-                           "launches": cod_n, "share_of_step": cod_ms_all / ms}
+        if coding_path == "tensor":
+            # tcgen05 spatial pass: the u state (read + write) is the kernel's
+            # minimum HBM traffic (2 K D s per image-iteration, plus the f16
+            # lambda band and the col2im band partials, 13/8 of a plane each);
+            # SURVEY.md 8(d)'s formula charges theta and z separately (twice
+            # the bytes of u) and is kept as formula_bytes_per_launch
+            s_, D_, _ = sizes(cfg)
+            # image-iterations per launch (cold-start coding configs: every image, every launch)
+            img_it_launch = nl if weak else (admm_total / world) / cod_n
+            kern_bytes = img_it_launch * (2 * cfg["K"] * D_ * s_ + 2 * (26 / 16) * D_ * 4)
+            ach_b = kern_bytes / (avg / 1000.0) / 1e9
+            kf = 64 if cfg["K"] <= 64 else 128
+            flops = img_it_launch * D_ * 1536 * kf  # 2 GEMMs x 3 f16 products x 2 x 128 taps x KF per pixel
+            ach_f = flops / (avg / 1000.0) / 1e12
+            tpeak, tpk = load_tensor_peak()
+            out["roofline"] = {"bound": "hbm", "kernel": "coding_pass_tc (tcgen05 spatial ADMM iteration)",
+                               "achieved": ach_b, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                               "frac": ach_b / peak, "traffic": traffic_from_profiles(args.config + "_tc"),
+                               "algorithmic_bytes_per_launch": kern_bytes,
+                               "formula_bytes_per_launch": algo_total / cod_n,
+                               "avg_launch_ms": avg, "launches": cod_n, "share_of_step": cod_ms_all / ms}
+            out["roofline_tensor"] = {"bound": "tensor", "kernel": "coding_pass_tc (f16 x3 split GEMMs)",
+                                      "achieved": ach_f, "peak": tpeak, "peak_kind": tpk, "unit": "TFLOP/s",
+                                      "frac": ach_f / tpeak, "flops_per_launch": flops}
+        else:
+            out["roofline"] = {"bound": "hbm", "kernel": "coding_pass<ADMM> (coding_pass_cl at 256x256)",
+                               "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                               "frac": achieved / peak, "traffic": traffic_from_profiles(args.config),
+                               "algorithmic_bytes_per_launch": algo_total / cod_n, "avg_launch_ms": avg,
+                               "launches": cod_n, "share_of_step": cod_ms_all / ms}
     if learn_n and not weak:
         # z_hat streams: each CG apply (cg_iters + one warm-start residual apply per
         # mu iteration) is one contract_c + one contract_out, each d_recover one

@@ -226,6 +226,13 @@ int dcsc_cuda_event_elapsed(dcsc_cuda_ctx* ctx, int a, int b, double* ms);
 /* bytes of device memory held by the context */
 int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes);
 
+/* Which ADMM coding iteration the context runs (no reference counterpart:
+ * the reference has one, admm_coding, coding.cpp:166-329):
+ * 0 = the fused FFT pass (half-spectrum c2r / prox / r2c per filter),
+ * 1 = the tensor-core spatial pass (FP32 planes of 128-pixel row tiles,
+ *     11 x 11 supports, K <= 128, one channel; DCSC_TC=0 disables it). */
+int dcsc_cuda_coding_path(dcsc_cuda_ctx* ctx, int* path);
+
 /* multi-rank: one context per GPU holds its shard of images; learning sums
  * its K x NB correlations and the CG / trace scalars over ranks.
  * dcsc_cuda_nccl_unique_id: rank 0 creates the id (>= 128 bytes) and ships it

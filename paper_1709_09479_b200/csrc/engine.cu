@@ -483,4 +483,10 @@ int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes) {
   return DCSC_OK;
 }
 
+int dcsc_cuda_coding_path(dcsc_cuda_ctx* ctx, int* path) {
+  CTX_CHECK
+  *path = ctx->eng->coding_path;
+  return DCSC_OK;
+}
+
 }  // extern "C"

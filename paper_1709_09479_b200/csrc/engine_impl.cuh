@@ -566,6 +566,7 @@ class Engine final : public EngineBase {
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
         if (std::getenv("DCSC_VERBOSE")) std::fprintf(stderr, "dcsc: tensor-core coding pass (KF=%d)\n", tc_kf_);
+        coding_path = 1;
       }
     }
     CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));

@@ -90,6 +90,7 @@ class EngineBase {
   std::unique_ptr<Reducer> red_;
  public:
   size_t device_bytes = 0;
+  int coding_path = 0;  // ADMM coding iteration: 0 FFT pass (kernels*.cuh), 1 tensor-core spatial pass (kernels_tc.cuh)
 };
 
 // ---------------------------------------------------------------- size table

@@ -37,7 +37,7 @@ namespace dcsc_cuda {
 
 #ifdef DCSC_TC_TRACE  // per-phase globaltimer trace of one epilogue warp (CTA 0, group 0, warp 1), a few tiles
 #define TCT(slot)                                                                              \
-  if (blockIdx.x == 0 && threadIdx.x == 32 && t >= 2 && t < 8) {                              \
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && e == 0 && t >= 2 && t < 8) {              \
     unsigned long long tt_;                                                                    \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_));                                   \
     tr[(t - 2) / 2][slot] = tt_;                                                               \
@@ -458,11 +458,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         TCT(6)
       }
 #ifdef DCSC_TC_TRACE
-      if (blockIdx.x == 0 && threadIdx.x == 32 && item == (int)blockIdx.x)
+      if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && e == 0 && item == (int)blockIdx.x)
         for (int f = 0; f < 3; ++f)
-          printf("TCT tile %d: build %llu waitG1 %llu epi1 %llu split %llu waitG2 %llu col2im %llu | next %llu\n", 2 + 2 * f,
-                 tr[f][1] - tr[f][0], tr[f][2] - tr[f][1], tr[f][3] - tr[f][2], tr[f][4] - tr[f][3],
-                 tr[f][5] - tr[f][4], tr[f][6] - tr[f][5], f < 2 ? tr[f + 1][0] - tr[f][6] : 0ull);
+          printf("TCT warp %d tile %d: start %llu build %llu waitG1 %llu epi1 %llu split %llu waitG2 %llu col2im %llu\n",
+                 warp, 2 + 2 * f, tr[f][0] % 1000000, tr[f][1] - tr[f][0], tr[f][2] - tr[f][1], tr[f][3] - tr[f][2],
+                 tr[f][4] - tr[f][3], tr[f][5] - tr[f][4], tr[f][6] - tr[f][5]);
 #endif
       g += TPI;
       uc += NCHUNK;

@@ -140,7 +140,7 @@ EXPORTS = [
     "dcsc_synth_dataset", "dcsc_synth_generate_range", "dcsc_cuda_learning_correlation",
     "dcsc_cuda_dictionary_adjoint", "dcsc_cuda_lambda_update", "dcsc_cuda_gamma_solve", "dcsc_cuda_d_recover",
     "dcsc_cuda_run_begin", "dcsc_cuda_run_step", "dcsc_cuda_run_accepts", "dcsc_cuda_signal_flags",
-    "dcsc_cuda_set_learning_layout",
+    "dcsc_cuda_set_learning_layout", "dcsc_cuda_coding_path",
 ]
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -463,6 +463,12 @@ class Context:
         v = C.c_size_t()
         _err(lib().dcsc_cuda_device_bytes(self._h, C.byref(v)))
         return v.value
+
+    def coding_path(self) -> str:
+        """'fft' (fused FFT coding pass) or 'tensor' (tcgen05 spatial pass)."""
+        v = C.c_int()
+        _err(lib().dcsc_cuda_coding_path(self._h, C.byref(v)))
+        return "tensor" if v.value == 1 else "fft"
 
 
 # ---------------------------------------------------------------- reference-shaped API
