@@ -234,9 +234,10 @@ class Engine final : public EngineBase {
   }
   // Tensor-core spatial coding iteration (kernels_tc.cuh): FP32 planes whose
   // rows split into 128-pixel tiles, 11 x 11 supports, K <= 128, J = 1.
-  // (cluster families only: their u planes are row-major; the single-CTA
-  // family keeps u as column-major pixel pairs)
-  static constexpr bool kTcFamily = CLU && std::is_same<R, float>::value && W % 128 == 0 &&
+  // The pass works on row-major u planes: the cluster family's own layout; the
+  // single-CTA family (column-major pixel pairs) runs it on a row-major copy
+  // (tu_) converted once before and after each coding call.
+  static constexpr bool kTcFamily = std::is_same<R, float>::value && W % 128 == 0 &&
                                     (W / 128 == 1 || (W / 128) % 2 == 0) && H % 16 == 0;
   template <int KF>
   using TG = TcGeom<H, W, KF, 11, 11, 16>;
@@ -551,7 +552,8 @@ class Engine final : public EngineBase {
         tdsplit_.alloc((size_t)2 * tc_kf_ * kTcTaps * 2);
         tspart_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::SR * W);
         tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
-        device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes;
+        if (!CLU) tu_.alloc(sizeof(float) * (size_t)N_ * K_ * D);
+        device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes + tu_.bytes;
         CK(cudaDeviceGetAttribute(&tc_grid_, cudaDevAttrMultiProcessorCount, o.device));
         // TMA map of u as [N*K planes][D pixels] FP32, box 16 planes x 128 pixels
         void* fn = nullptr;
@@ -562,7 +564,8 @@ class Engine final : public EngineBase {
         const cuuint64_t gstr[1] = {(cuuint64_t)D * sizeof(float)};
         const cuuint32_t box[2] = {128u, 16u}, estr[2] = {1u, 1u};
         const CUresult cr = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn)(
-            &tc_umap_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, u_.p, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            &tc_umap_, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, CLU ? u_.p : tu_.p, gdim, gstr, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
         if (std::getenv("DCSC_VERBOSE")) std::fprintf(stderr, "dcsc: tensor-core coding pass (KF=%d)\n", tc_kf_);
@@ -664,6 +667,24 @@ class Engine final : public EngineBase {
     launch(MODE == kPassAdmm ? kFamCoding : kFamOther, [&] { launch_coding<MODE>(G_, cnt, st_, a); });
   }
 
+  // single-CTA family: u planes of images [n0, n0 + cnt) between the column-major
+  // pair layout (u_) and the row-major copy the tensor-core pass works on (tu_)
+  void tc_convert_u(int n0, int cnt, bool to_rows) {
+    if constexpr (kTcFamily && !CLU) {
+      const dim3 grid((std::max(W / 2, H) + 31) / 32, (std::max(W / 2, H) + 31) / 32, cnt * K_);
+      float2* u2 = reinterpret_cast<float2*>(u_.as<float>() + (size_t)n0 * K_ * D);
+      float2* t2 = reinterpret_cast<float2*>(tu_.as<float>() + (size_t)n0 * K_ * D);
+      launch(kFamOther, [&] {
+        if (to_rows)
+          tc_pair_transpose<true><<<dim3((H + 31) / 32, (W / 2 + 31) / 32, cnt * K_), dim3(32, 8), 0, st_>>>(
+              u2, t2, H, W / 2);
+        else
+          tc_pair_transpose<false><<<dim3((W / 2 + 31) / 32, (H + 31) / 32, cnt * K_), dim3(32, 8), 0, st_>>>(
+              t2, u2, H, W / 2);
+      });
+      (void)grid;
+    }
+  }
   // lambda_hat -> spatial lambda -> scaled f16 hi / lo planes for the tensor-core pass
   void tc_lambda_spatial(int n0, int cnt) {
     if constexpr (kTcFamily) {
@@ -686,8 +707,8 @@ class Engine final : public EngineBase {
       a.lam_scale = tlscale_.as<float>() + n0;
       a.dsplit = tdsplit_.as<__half>();
       a.d_scale = tc_dscale_;
-      a.u = u_.as<R>() + (size_t)n0 * K_ * D;
-      a.theta0 = use_theta0_ ? theta0_.as<R>() + (size_t)n0 * K_ * D : nullptr;
+      a.u = (CLU ? u_.as<float>() : tu_.as<float>()) + (size_t)n0 * K_ * D;
+      a.theta0 = use_theta0_ ? theta0_.as<float>() + (size_t)n0 * K_ * D : nullptr;
       a.spart = tspart_.as<float>() + (size_t)n0 * G::NBANDS * G::SR * W;
       a.bsums = tbsums_.as<double>() + (size_t)n0 * G::NBANDS * kSums;
       a.conv = conv_.as<int>() + n0;
@@ -1077,14 +1098,20 @@ class Engine final : public EngineBase {
       });
     };
     if (all_zero && J_ == 1) lam_update(0, 0, 1);
-    if (tc_) tc_lambda_spatial(n0, cnt);
+    // tensor-core pass for this call (the single-CTA family keeps a warm state that
+    // is not ADMM-consistent on the FFT pass: its theta0 is in the pair layout)
+    const bool tc = tc_ && (CLU || !t0_pending);
+    if (tc) {
+      if (!CLU) tc_convert_u(n0, cnt, true);
+      tc_lambda_spatial(n0, cnt);
+    }
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     int pending = -1;  // iteration whose conv flags are in flight
     for (int it = 1; it <= cfg_.max_admm; ++it) {
       use_theta0_ = t0_pending && it == 1;
-      if (tc_)
+      if (tc)
         tc_iteration(n0, cnt, it, it == cfg_.max_admm);
       else
         coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
@@ -1106,6 +1133,7 @@ class Engine final : public EngineBase {
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
+    if (tc && !CLU) tc_convert_u(n0, cnt, false);
     // exit: lambda = iDFT(lambda_hat), rescale, dual objective (coding.cpp:287-309)
     c2r<R>(lamhat_.as<C>() + (size_t)n0 * J_ * NB, NB, lam_.as<R>() + (size_t)n0 * J_ * D, D, cnt * J_);
     launch(kFamOther, [&] {
@@ -2178,7 +2206,7 @@ class Engine final : public EngineBase {
   bool tc_ = false;
   int tc_kf_ = 128, tc_grid_ = 148;
   float tc_dscale_ = 1.f;
-  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_;
+  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_, tu_;
   CUtensorMap tc_umap_{};
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   std::vector<int> degen_;  // per image: normalisation met a constant input

@@ -576,6 +576,27 @@ __global__ void tc_lam_split(const float* __restrict__ lam, uint32_t* __restrict
   }
 }
 
+// u planes of the single-CTA family (column-major pixel pairs: pair (r, m) at
+// m*H + r) <-> row-major planes for the tensor-core pass: a float2 transpose of
+// each [W/2][H] plane through 32 x 32 shared tiles. TO_ROWS: pairs -> rows.
+template <bool TO_ROWS>
+__global__ void tc_pair_transpose(const float2* __restrict__ src, float2* __restrict__ dst, int H, int W2) {
+  __shared__ float2 t[32][33];
+  const size_t plane = (size_t)blockIdx.z * H * W2;
+  // TO_ROWS: src [W2][H] -> dst [H][W2]; else src [H][W2] -> dst [W2][H]
+  const int R0 = TO_ROWS ? W2 : H, C0 = TO_ROWS ? H : W2;  // src rows x cols
+  const int br = blockIdx.y * 32, bc = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = br + i, c = bc + threadIdx.x;
+    if (r < R0 && c < C0) t[i][threadIdx.x] = src[plane + (size_t)r * C0 + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = bc + i, c = br + threadIdx.x;  // dst [C0][R0]
+    if (r < C0 && c < R0) dst[plane + (size_t)r * R0 + c] = t[threadIdx.x][i];
+  }
+}
+
 // dictionary K x TAPS (FP64, tap o = y*MW + x) -> f16 hi / lo core-matrix grid:
 // element (k, o) at ((k/8)*16 + o/8)*64 + (k%8)*8 + o%8 halves; zero padded to KF x 128.
 template <int KF>
