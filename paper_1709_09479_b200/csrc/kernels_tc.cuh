@@ -50,7 +50,8 @@ constexpr int kTcTaps = 128;                       // GEMM-1 K / GEMM-2 N (taps 
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcThreads = 32 * (kTcEpiWarps + 2);  // 320: MMA warp, 8 epilogue warps, u streaming warp
 constexpr int kTcStripW = 44;
-constexpr int kTcUSlots = 4;                       // u staging ring depth per epilogue group                      // col2im strip row stride (floats) >= 32 + MW - 1
+constexpr int kTcUSlots = 6;                       // u staging ring depth per epilogue group
+constexpr int kTcUPrefetch = 8;                    // chunks ahead an L2 prefetch of u rows is issued                      // col2im strip row stride (floats) >= 32 + MW - 1
 
 struct TcArgs {
   CUtensorMap umap;        // u as [N*K planes][D pixels] FP32, box [16 planes][128 pixels]
@@ -96,8 +97,48 @@ struct TcGeom {
   static constexpr size_t ubuf_off = (red_off + red_bytes + 127) / 128 * 128;
   static constexpr size_t ubuf_bytes = (size_t)2 * kTcUSlots * 16 * 128 * 4;
   static constexpr size_t bar_off = ubuf_off + ubuf_bytes;
-  static constexpr size_t smem = bar_off + 32 * 8;
+  static constexpr size_t smem = bar_off + (size_t)(10 + 4 * kTcUSlots) * 8;  // barriers + TMEM slot
 };
+
+// Packed FP32 pairs (FADD2 / FMUL2 / FFMA2): half the issue slots of scalar FP32.
+struct F2 {
+  unsigned long long u;
+};
+__device__ __forceinline__ F2 f2(float x, float y) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.u) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ float f2x(F2 a) {
+  float x, y;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.u));
+  return x;
+}
+__device__ __forceinline__ float f2y(F2 a) {
+  float x, y;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.u));
+  return y;
+}
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+  F2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u));
+  return r;
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+  F2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u));
+  return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+  F2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.u) : "l"(a.u), "l"(b.u));
+  return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.u) : "l"(a.u), "l"(b.u), "l"(c.u));
+  return r;
+}
 
 __device__ __forceinline__ void mbar_arrive1(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -285,6 +326,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         const int nv = FULL ? 16 : max(0, min(16, a.K - k0));
         unsigned long long* fb = ufull + e * kTcUSlots + sl;
         (void)nv;
+        if (lane == 0 && i + kTcUPrefetch < NCHUNK) {  // the same group's chunk kTcUPrefetch ahead -> L2
+          const int ip = i + kTcUPrefetch;
+          const int tp = e + 2 * (ip / NCU), kp = 16 * (ip % NCU);
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&a.umap),
+                       "r"((b * RB + tp / TPR) * W + (tp % TPR) * 128), "r"(a.plane0 + n * a.K + kp)
+                       : "memory");
+        }
         if (lane == 0) {  // one 2-D TMA: 16 planes x 128 pixels (rows past the last plane are zero-filled)
           mbar_expect_tx(fb, 16u * 128u * 4u);
           asm volatile(
@@ -301,7 +349,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         }
         }
       }
-      if (c_seq[0] + c_seq[1] == seq0) __nanosleep(100);
+      if (c_seq[0] + c_seq[1] == seq0) __nanosleep(32);
     }
   } else {
     // ===== epilogue groups =====
@@ -366,7 +414,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         // --- prox on T, w -> A (two f16 planes, per-pixel scale)
         // stop-test sums (coding.cpp:237-259): sum dz^2 = rho^2 sum (theta' - t)^2 and
         // sum z'^2 = rho^2 sum (theta' - u')^2 are scaled once per tile
-        float f0 = 0.f, f1 = 0.f, f2 = 0.f, f4 = 0.f, f5 = 0.f, f6 = 0.f, wmax = 0.f;
+        // per-pair accumulators (packed FP32), folded once per tile
+        F2 a0 = f2(0.f, 0.f), a1 = a0, a2 = a0, a4 = a0, a5 = a0;
+        float f6 = 0.f, wmax = 0.f;
+        const F2 tsc2 = f2(tsc, tsc);
         mbar_wait(t_full + e, ph);
         umma::fence_after_sync();
         TCT(2)
@@ -385,28 +436,42 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
           umma::ld16(ACC + ch * 16, v);
           umma::wait_ld();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int k = ch * 16 + j;
-            const float tv = __uint_as_float(v[j]) * tsc;
-            const float uv = (FULL || k < a.K) ? ucur[j] : 0.f;
-            float th_o;
-            if constexpr (T0) th_o = tcur[j]; else th_o = fminf(fmaxf(uv, -beta), beta);
-            const float un = tv - (th_o - uv);
-            const float th = fminf(fmaxf(un, -beta), beta);
-            const float d_tt = th - tv, d_z = th - un, dth = th - th_o;
-            f0 = fmaf(d_tt, d_tt, f0);
-            f1 = fmaf(th, th, f1);
-            f2 = fmaf(tv, tv, f2);
-            f4 = fmaf(d_z, d_z, f4);
-            f5 = fmaf(dth, dth, f5);
-            f6 = fmaxf(f6, fabsf(tv));
-            const float w = fmaf(2.f, th, -un);
-            wmax = fmaxf(wmax, fabsf(w));
-            if (FULL || k < a.K) __stcs(up + (size_t)k * D, un);
-            v[j] = __float_as_uint(w);
+          for (int jj = 0; jj < 8; ++jj) {
+            const int k0 = ch * 16 + 2 * jj;
+            const float u0 = (FULL || k0 < a.K) ? ucur[2 * jj] : 0.f;
+            const float u1 = (FULL || k0 + 1 < a.K) ? ucur[2 * jj + 1] : 0.f;
+            const F2 t = mul2(f2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1])), tsc2);
+            float o0, o1;
+            if constexpr (T0) {
+              o0 = tcur[2 * jj];
+              o1 = tcur[2 * jj + 1];
+            } else {
+              o0 = fminf(fmaxf(u0, -beta), beta);
+              o1 = fminf(fmaxf(u1, -beta), beta);
+            }
+            const F2 tho = f2(o0, o1);
+            const F2 un = sub2(t, sub2(tho, f2(u0, u1)));  // u' = t - (theta_old - u)
+            const float un0 = f2x(un), un1 = f2y(un);
+            const F2 th = f2(fminf(fmaxf(un0, -beta), beta), fminf(fmaxf(un1, -beta), beta));
+            const F2 d_tt = sub2(th, t), d_z = sub2(th, un), dth = sub2(th, tho);
+            a0 = fma2(d_tt, d_tt, a0);
+            a1 = fma2(th, th, a1);
+            a2 = fma2(t, t, a2);
+            a4 = fma2(d_z, d_z, a4);
+            a5 = fma2(dth, dth, a5);
+            f6 = fmaxf(f6, fmaxf(fabsf(f2x(t)), fabsf(f2y(t))));
+            const F2 w = add2(th, d_z);  // w = theta' + z'/rho = 2 theta' - u'
+            const float w0 = f2x(w), w1 = f2y(w);
+            wmax = fmaxf(wmax, fmaxf(fabsf(w0), fabsf(w1)));
+            if (FULL || k0 < a.K) __stcs(up + (size_t)k0 * D, un0);
+            if (FULL || k0 + 1 < a.K) __stcs(up + (size_t)(k0 + 1) * D, un1);
+            v[2 * jj] = __float_as_uint(w0);
+            v[2 * jj + 1] = __float_as_uint(w1);
           }
           umma::st16(ACC + ch * 16, v);
         }
+        const float f0 = f2x(a0) + f2y(a0), f1 = f2x(a1) + f2y(a1), f2_ = f2x(a2) + f2y(a2),
+                    f4 = f2x(a4) + f2y(a4), f5 = f2x(a5) + f2y(a5);
         TCT(3)
         umma::wait_st();
         const float sw = umma::pow2_scale(wmax);
@@ -428,7 +493,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         if (lane == 0) mbar_arrive1(w_full + e);
         TCT(4)
         const float rho2 = rho * rho;
-        st[0] += (double)f0; st[1] += (double)f1; st[2] += (double)f2; st[3] += (double)(rho2 * f0);
+        st[0] += (double)f0; st[1] += (double)f1; st[2] += (double)f2_; st[3] += (double)(rho2 * f0);
         st[4] += (double)(rho2 * f4); st[5] += (double)f5; st[6] = fmax(st[6], (double)f6);
         // --- col2im: s[r + oy][c + ox] += Z[p][o] into this warp's strip
         const float zsc = dinv / sw;
