@@ -30,6 +30,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "umma.cuh"
 
@@ -221,7 +223,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
   unsigned long long *ufull = bars + 9, *uempty = bars + 9 + 2 * kTcUSlots;  // [group][slot]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9 + 4 * kTcUSlots);
   float* UB = reinterpret_cast<float*>(sm + G::ubuf_off);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches keep
+  // the MMA operands in uniform registers (no per-instruction lane loops)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   if (warp == 0) umma::tmem_alloc<512>(tslot);
   if (threadIdx.x == 32) {
@@ -242,6 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tbase = *tslot;
+  if (tbase != 0u) __trap();  // 512 columns allocated by the only CTA on the SM start at column 0
   const int items = a.N * NBANDS;
 
   constexpr int NCU = KF / 16, NCHUNK = (TPI / 2) * NCU;  // u chunks per item and group
@@ -256,31 +261,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
     __syncwarp();
     const uint32_t dh = umma::smem_u32(Ds), dl = dh + KF * kTcTaps * 2;
     constexpr uint32_t id1 = umma::idesc_f16(128, KF, 0), id2 = umma::idesc_f16(128, kTcTaps, 1);
-    auto gemm1 = [&](uint32_t gg) {
-      const uint32_t s = gg & 1u;
+    // the CTA owns all 512 TMEM columns, so the allocation starts at address 0
+    // (checked below); slot addresses are then warp-uniform immediates
+    // slot as a compile-time constant: TMEM addresses become immediates
+    auto gemm1s = [&](auto S) {
+      constexpr uint32_t A = 256u * decltype(S)::value, acc = A + 128u;
       umma::fence_after_sync();
-      const uint32_t A = tbase + 256u * s, acc = A + 128u;
 #pragma unroll
       for (int j = 0; j < kTcTaps / 16; ++j) {  // K = taps; B K-major: LBO 128 B (taps), SBO 2048 B (filters)
         const uint64_t bh = umma::sdesc(dh + 256u * j, 128u, 2048u), bl = umma::sdesc(dl + 256u * j, 128u, 2048u);
-        umma::mma_ts(acc, A + 8u * j, bh, id1, j > 0);
-        umma::mma_ts(acc, A + 8u * j, bl, id1, 1u);
-        umma::mma_ts(acc, A + 64u + 8u * j, bh, id1, 1u);
+        umma::mma_ts_warp(acc, A + 8u * j, bh, id1, j > 0);
+        umma::mma_ts_warp(acc, A + 8u * j, bl, id1, 1u);
+        umma::mma_ts_warp(acc, A + 64u + 8u * j, bh, id1, 1u);
       }
-      umma::commit(t_full + s);
+      umma::commit_warp(t_full + decltype(S)::value);
     };
-    auto gemm2 = [&](uint32_t gg) {
-      const uint32_t s = gg & 1u;
+    auto gemm2s = [&](auto S) {
+      constexpr uint32_t A = 256u * decltype(S)::value, acc = A + 128u;
       umma::fence_after_sync();
-      const uint32_t A = tbase + 256u * s, acc = A + 128u;
 #pragma unroll
       for (int j = 0; j < KF / 16; ++j) {  // K = filters; B MN-major: LBO 2048 B (filters), SBO 128 B (taps)
         const uint64_t bh = umma::sdesc(dh + 4096u * j, 2048u, 128u), bl = umma::sdesc(dl + 4096u * j, 2048u, 128u);
-        umma::mma_ts(acc, A + 8u * j, bh, id2, j > 0);
-        umma::mma_ts(acc, A + 8u * j, bl, id2, 1u);
-        umma::mma_ts(acc, A + 64u + 8u * j, bh, id2, 1u);
+        umma::mma_ts_warp(acc, A + 8u * j, bh, id2, j > 0);
+        umma::mma_ts_warp(acc, A + 8u * j, bl, id2, 1u);
+        umma::mma_ts_warp(acc, A + 64u + 8u * j, bh, id2, 1u);
       }
-      umma::commit(z_full + s);
+      umma::commit_warp(z_full + decltype(S)::value);
+    };
+    auto gemm1 = [&](uint32_t gg) {
+      if (gg & 1u) gemm1s(std::integral_constant<uint32_t, 1>{}); else gemm1s(std::integral_constant<uint32_t, 0>{});
+    };
+    auto gemm2 = [&](uint32_t gg) {
+      if (gg & 1u) gemm2s(std::integral_constant<uint32_t, 1>{}); else gemm2s(std::integral_constant<uint32_t, 0>{});
     };
     int ntiles = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x)
@@ -302,10 +314,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
     };
     if (warp == 0) {
       // GEMMs: whichever is ready first (GEMM-1 of the next tile, GEMM-2 of the oldest pending)
-      while (lane == 0 && (int)n2 < ntiles) {
-        if ((int)n1 < ntiles && mbar_test(a_full + (n1 & 1u), (n1 >> 1) & 1u)) {
+      // whole warp, converged: decisions from lane 0's barrier tests, MMAs by an elected lane
+      while ((int)n2 < ntiles) {
+        if ((int)n1 < ntiles && lane0_test(a_full + (n1 & 1u), (n1 >> 1) & 1u)) {
           gemm1(n1++);
-        } else if (n2 < n1 && mbar_test(w_full + (n2 & 1u), (n2 >> 1) & 1u)) {
+        } else if (n2 < n1 && lane0_test(w_full + (n2 & 1u), (n2 >> 1) & 1u)) {
           gemm2(n2++);
         } else {
           __nanosleep(40);  // keep the polling off the epilogue warps' issue slots
