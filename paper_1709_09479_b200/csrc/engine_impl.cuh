@@ -552,6 +552,7 @@ class Engine final : public EngineBase {
         tdsplit_.alloc((size_t)2 * tc_kf_ * kTcTaps * 2);
         tspart_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::SR * W);
         tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
+        tupd_.alloc(sizeof(int) * (size_t)N_);
         if (!CLU) tu_.alloc(sizeof(float) * (size_t)N_ * K_ * D);
         device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes + tu_.bytes;
         CK(cudaDeviceGetAttribute(&tc_grid_, cudaDevAttrMultiProcessorCount, o.device));
@@ -728,16 +729,19 @@ class Engine final : public EngineBase {
       R* s = lam_.as<R>() + (size_t)n0 * D;          // s reuses the spatial lambda planes
       C* spec = part_.as<C>() + (size_t)n0 * NB;      // one partial spectrum per image (G = 1)
       double* sm1 = sums_.as<double>() + (size_t)n0 * kSums;
+      int* upd = tupd_.as<int>() + n0;
       launch(kFamLambda, [&] {
-        tc_band_reduce<G><<<dim3(16, cnt), 256, 0, st_>>>(a.spart, a.bsums, a.conv, s, sm1);
+        tc_band_reduce<G><<<dim3(16, cnt), 256, 0, st_>>>(a.spart, a.bsums, conv_.as<int>() + n0, s,
+                                                         img_.as<ImageAdmm>() + n0, upd, it, last ? 1 : 0);
       });
+      (void)sm1;
+      if (last) return;
       r2c(s, false, D, spec, NB, cnt);
       launch(kFamLambda, [&] {
-        lambda_update<R><<<dim3((NB + 255) / 256, cnt), 256, 0, st_>>>(
-            spec, sm1, xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(), lamhat_.as<C>() + (size_t)n0 * NB,
-            conv_.as<int>() + n0, img_.as<ImageAdmm>() + n0, 1, NB, R(cfg_.rho), it, last ? 1 : 0, 0);
+        tc_lambda_apply<R><<<dim3(32, cnt), 256, 0, st_>>>(spec, xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(),
+                                                          lamhat_.as<C>() + (size_t)n0 * NB, upd, NB, R(cfg_.rho));
       });
-      if (!last) tc_lambda_spatial(n0, cnt);
+      tc_lambda_spatial(n0, cnt);
     }
   }
 
@@ -2206,7 +2210,7 @@ class Engine final : public EngineBase {
   bool tc_ = false;
   int tc_kf_ = 128, tc_grid_ = 148;
   float tc_dscale_ = 1.f;
-  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_, tu_;
+  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_, tu_, tupd_;
   CUtensorMap tc_umap_{};
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   std::vector<int> degen_;  // per image: normalisation met a constant input

@@ -591,33 +591,67 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
 }
 
 // s[n] = sum of the band partials (each output row from its own band and the
-// previous one, in that order); stop-test sums over bands -> sums[n] (G = 1).
+// previous one, in that order). Block (0, n) also reduces the stop-test sums
+// over bands (fixed order) and runs the stop test of coding.cpp:264-283 once
+// per image: ImageAdmm stats, conv[n], and upd[n] = "form the next lambda_hat".
 template <class G>
-__global__ void tc_band_reduce(const float* __restrict__ spart, const double* __restrict__ bsums,
-                               const int* __restrict__ conv, float* __restrict__ s, double* __restrict__ sums) {
-  constexpr int H = G::H, W = G::W, RB = G::RB, SR = G::SR, NBANDS = G::NBANDS, D = G::D;
+__global__ void tc_band_reduce(const float* __restrict__ spart, const double* __restrict__ bsums, int* conv,
+                               float* __restrict__ s, ImageAdmm* img, int* upd, int iter, int is_last) {
+  constexpr int W = G::W, RB = G::RB, SR = G::SR, NBANDS = G::NBANDS, D = G::D;
   const int n = blockIdx.y;
-  if (conv[n]) return;
-  const float* sp = spart + (size_t)n * NBANDS * SR * W;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += gridDim.x * blockDim.x) {
-    const int r = i / W, c = i % W;
-    const int b0 = r / RB, lr0 = r - b0 * RB;
-    const int bp = (b0 + NBANDS - 1) % NBANDS, lrp = lr0 + RB;
-    float v = 0.f;
-    if (lrp < SR) v = sp[((size_t)bp * SR + lrp) * W + c];
-    v += sp[((size_t)b0 * SR + lr0) * W + c];
-    s[(size_t)n * D + i] = v;
+  if (conv[n]) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) upd[n] = 0;
+    return;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    double tt = 0, th = 0, t2 = 0, dz2 = 0, z2 = 0, dth = 0, tinf = 0;
     for (int bb = 0; bb < NBANDS; ++bb) {
       const double* o = bsums + ((size_t)n * NBANDS + bb) * kSums;
-      for (int i = 0; i < 6; ++i) acc[i] += o[i];
-      acc[6] = fmax(acc[6], o[6]);
+      tt += o[0]; th += o[1]; t2 += o[2]; dz2 += o[3]; z2 += o[4]; dth += o[5];
+      tinf = fmax(tinf, o[6]);
     }
-    double* o = sums + (size_t)n * kSums;
-    for (int i = 0; i < 7; ++i) o[i] = acc[i];
-    o[7] = 0.0;
+    const double denom = fmax(fmax(sqrt(th), sqrt(t2)), 1.0);
+    const double primal = sqrt(tt) / denom;
+    const double zc = sqrt(dz2) / fmax(sqrt(z2), 1.0);
+    const double thc = sqrt(dth) / fmax(sqrt(th), 1.0);
+    const bool stop = primal <= kAdmmRelTol && zc <= kAdmmRelTol && thc <= kAdmmRelTol;
+    ImageAdmm& m = img[n];
+    m.iters = iter;
+    m.primal = primal;
+    m.zc = zc;
+    m.thc = thc;
+    m.tinf = tinf;
+    if (stop) m.converged = 1;
+    upd[n] = (stop || is_last) ? 0 : 1;
+    if (stop) conv[n] = 1;  // blocks of this launch that miss it write an s nobody reads
+  }
+  const float4* sp = reinterpret_cast<const float4*>(spart + (size_t)n * NBANDS * SR * W);
+  float4* so = reinterpret_cast<float4*>(s + (size_t)n * D);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D / 4; i += gridDim.x * blockDim.x) {
+    const int r = (4 * i) / W, c4 = i % (W / 4);
+    const int b0 = r / RB, lr0 = r - b0 * RB;
+    const int bp = (b0 + NBANDS - 1) % NBANDS, lrp = lr0 + RB;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lrp < SR) v = sp[((size_t)bp * SR + lrp) * (W / 4) + c4];
+    const float4 w = sp[((size_t)b0 * SR + lr0) * (W / 4) + c4];
+    v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+    so[i] = v;
+  }
+}
+
+// lambda_hat = (DFT(s) - x_hat / rho) / sigma (lambda_from_w, coding.cpp:25-37) for
+// the images whose stop test asked for the next iteration (upd[n])
+template <class R>
+__global__ void tc_lambda_apply(const cx<R>* __restrict__ shat, const cx<R>* __restrict__ xhat,
+                                const R* __restrict__ sigma, cx<R>* __restrict__ lamhat, const int* __restrict__ upd,
+                                int NB, R rho) {
+  const int n = blockIdx.y;
+  if (!upd[n]) return;
+  const R inv_rho = R(1) / rho;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < NB; b += gridDim.x * blockDim.x) {
+    const cx<R> a = shat[(size_t)n * NB + b], xv = xhat[(size_t)n * NB + b];
+    const R sg = sigma[b];
+    lamhat[(size_t)n * NB + b] = mk<cx<R>>((a.x - xv.x * inv_rho) / sg, (a.y - xv.y * inv_rho) / sg);
   }
 }
 
