@@ -237,10 +237,13 @@ class Engine final : public EngineBase {
   // The pass works on row-major u planes: the cluster family's own layout; the
   // single-CTA family (column-major pixel pairs) runs it on a row-major copy
   // (tu_) converted once before and after each coding call.
-  static constexpr bool kTcFamily = std::is_same<R, float>::value && W % 128 == 0 &&
-                                    (W / 128 == 1 || (W / 128) % 2 == 0) && H % 16 == 0;
+  static constexpr bool kTcFamily = std::is_same<R, float>::value && H % 16 == 0 &&
+                                    ((W % 128 == 0 && (W / 128 == 1 || (W / 128) % 2 == 0)) || W == 64);
+  // compiled support (square) and filter-slot counts per family: 64 x 64 (C4) runs
+  // 7 x 7 supports with 32 / 64 filter slots, the wider grids 11 x 11 with 64 / 128
+  static constexpr int kTcM = W == 64 ? 7 : 11, kTcKFa = W == 64 ? 32 : 64, kTcKFb = W == 64 ? 64 : 128;
   template <int KF>
-  using TG = TcGeom<H, W, KF, 11, 11, 16>;
+  using TG = TcGeom<H, W, KF, kTcM, kTcM, 16>;
   template <int KF>
   static void set_tc_attr() {
     const int sm = (int)TG<KF>::smem;
@@ -355,8 +358,8 @@ class Engine final : public EngineBase {
       if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     };
     if constexpr (kTcFamily) {
-      set_tc_attr<64>();
-      set_tc_attr<128>();
+      set_tc_attr<kTcKFa>();
+      set_tc_attr<kTcKFb>();
     }
     if constexpr (CLU) {
       big((const void*)coding_pass_cl<P, kPassAdmm>, smem_coding());
@@ -543,13 +546,13 @@ class Engine final : public EngineBase {
                    dhat_rb_.bytes;
     if constexpr (kTcFamily) {
       const char* e = std::getenv("DCSC_TC");
-      tc_ = J_ == 1 && mh_ == 11 && mw_ == 11 && K_ <= 128 && !(e && e[0] == '0');
+      tc_ = J_ == 1 && mh_ == kTcM && mw_ == kTcM && K_ <= kTcKFb && !(e && e[0] == '0');
       if (tc_) {
-        using G = TG<128>;  // band geometry does not depend on the filter count
-        tc_kf_ = K_ <= 64 ? 64 : 128;
+        using G = TG<kTcKFb>;  // band geometry does not depend on the filter count
+        tc_kf_ = K_ <= kTcKFa ? kTcKFa : kTcKFb;
         tlam16_.alloc(sizeof(uint32_t) * (size_t)N_ * D);
         tlscale_.alloc(sizeof(float) * (size_t)N_);
-        tdsplit_.alloc((size_t)2 * tc_kf_ * kTcTaps * 2);
+        tdsplit_.alloc((size_t)2 * tc_kf_ * G::TP * 2);
         tspart_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::SR * W);
         tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
         tupd_.alloc(sizeof(int) * (size_t)N_);
@@ -672,18 +675,20 @@ class Engine final : public EngineBase {
   // pair layout (u_) and the row-major copy the tensor-core pass works on (tu_)
   void tc_convert_u(int n0, int cnt, bool to_rows) {
     if constexpr (kTcFamily && !CLU) {
-      const dim3 grid((std::max(W / 2, H) + 31) / 32, (std::max(W / 2, H) + 31) / 32, cnt * K_);
-      float2* u2 = reinterpret_cast<float2*>(u_.as<float>() + (size_t)n0 * K_ * D);
-      float2* t2 = reinterpret_cast<float2*>(tu_.as<float>() + (size_t)n0 * K_ * D);
-      launch(kFamOther, [&] {
-        if (to_rows)
-          tc_pair_transpose<true><<<dim3((H + 31) / 32, (W / 2 + 31) / 32, cnt * K_), dim3(32, 8), 0, st_>>>(
-              u2, t2, H, W / 2);
-        else
-          tc_pair_transpose<false><<<dim3((W / 2 + 31) / 32, (H + 31) / 32, cnt * K_), dim3(32, 8), 0, st_>>>(
-              t2, u2, H, W / 2);
-      });
-      (void)grid;
+      const long planes = (long)cnt * K_;
+      for (long p0 = 0; p0 < planes; p0 += 32768) {  // gridDim.z <= 65535
+        const int np = (int)std::min(32768L, planes - p0);
+        float2* u2 = reinterpret_cast<float2*>(u_.as<float>() + ((size_t)n0 * K_ + p0) * D);
+        float2* t2 = reinterpret_cast<float2*>(tu_.as<float>() + ((size_t)n0 * K_ + p0) * D);
+        launch(kFamOther, [&] {
+          if (to_rows)
+            tc_pair_transpose<true><<<dim3((H + 31) / 32, (W / 2 + 31) / 32, np), dim3(32, 8), 0, st_>>>(
+                u2, t2, H, W / 2);
+          else
+            tc_pair_transpose<false><<<dim3((W / 2 + 31) / 32, (H + 31) / 32, np), dim3(32, 8), 0, st_>>>(
+                t2, u2, H, W / 2);
+        });
+      }
     }
   }
   // lambda_hat -> spatial lambda -> scaled f16 hi / lo planes for the tensor-core pass
@@ -702,7 +707,7 @@ class Engine final : public EngineBase {
   // spatial lambda for the next iteration.
   void tc_iteration(int n0, int cnt, int it, bool last) {
     if constexpr (kTcFamily) {
-      using G = TG<128>;
+      using G = TG<kTcKFb>;
       TcArgs a;
       a.lam16 = tlam16_.as<uint32_t>() + (size_t)n0 * D;
       a.lam_scale = tlscale_.as<float>() + n0;
@@ -721,10 +726,10 @@ class Engine final : public EngineBase {
       a.plane0 = n0 * K_;
       const int grid = std::min(tc_grid_, cnt * G::NBANDS);
       launch(kFamCoding, [&] {
-        if (tc_kf_ == 64)
-          launch_tc<64>(grid, a);
+        if (tc_kf_ == kTcKFa)
+          launch_tc<kTcKFa>(grid, a);
         else
-          launch_tc<128>(grid, a);
+          launch_tc<kTcKFb>(grid, a);
       });
       R* s = lam_.as<R>() + (size_t)n0 * D;          // s reuses the spatial lambda planes
       C* spec = part_.as<C>() + (size_t)n0 * NB;      // one partial spectrum per image (G = 1)
@@ -850,10 +855,13 @@ class Engine final : public EngineBase {
         for (double v : dict_) amax = std::max(amax, (float)std::fabs(v));
         tc_dscale_ = umma::pow2_scale(amax);
         launch(kFamOther, [&] {
-          if (tc_kf_ == 64)
-            tc_dsplit<64><<<32, 256, 0, st_>>>(ddict_.as<double>(), K_, M_, tc_dscale_, tdsplit_.as<__half>());
+          constexpr int TP = TG<kTcKFb>::TP;
+          if (tc_kf_ == kTcKFa)
+            tc_dsplit<kTcKFa, TP><<<32, 256, 0, st_>>>(ddict_.as<double>(), K_, M_, tc_dscale_,
+                                                       tdsplit_.as<__half>());
           else
-            tc_dsplit<128><<<64, 256, 0, st_>>>(ddict_.as<double>(), K_, M_, tc_dscale_, tdsplit_.as<__half>());
+            tc_dsplit<kTcKFb, TP><<<64, 256, 0, st_>>>(ddict_.as<double>(), K_, M_, tc_dscale_,
+                                                       tdsplit_.as<__half>());
         });
       }
     }

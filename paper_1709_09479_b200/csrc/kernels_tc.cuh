@@ -75,20 +75,23 @@ template <int H_, int W_, int KF_, int MH_, int MW_, int RB_>
 struct TcGeom {
   static constexpr int H = H_, W = W_, KF = KF_, MH = MH_, MW = MW_, RB = RB_;
   static constexpr int D = H * W;
-  static constexpr int TPR = W / 128;              // tiles per image row
+  static constexpr int WT = W < 128 ? W : 128;     // tile width: a 128-pixel tile is RPT rows x WT pixels
+  static constexpr int RPT = 128 / WT;             // image rows per tile (2 at W = 64)
+  static constexpr int TPR = W / WT;               // tiles per row (tile rows of RPT image rows)
   static constexpr int NBANDS = H / RB;
-  static constexpr int TPI = RB * TPR;             // tiles per work item
+  static constexpr int TPI = (RB / RPT) * TPR;     // tiles per work item
   static constexpr int SR = RB + MH - 1;           // rows a band's col2im touches / lambda rows it reads
   static constexpr int LWW = W / 2 + 8;            // lambda band row: W halves + 16 wrap halves, in words
   static constexpr int NSS = TPR == 1 ? 2 : TPR;   // strip sets (per tile column; per epilogue group if TPR == 1)
   static constexpr int NSTRIP = NSS * 4;
   static constexpr int STRIP = SR * kTcStripW;
   static constexpr int TAPS = MH * MW;
-  static_assert(W % 128 == 0 && (TPR == 1 || TPR % 2 == 0), "row tiles of 128 pixels: one or an even count per row");
-  static_assert(H % RB == 0 && RB >= MH - 1 && TPI % 2 == 0, "band geometry");
-  static_assert(TAPS <= kTcTaps && 32 + MW - 1 <= kTcStripW && MW <= 16, "filter support");
+  static constexpr int TP = TAPS <= 64 ? 64 : 128;  // taps padded: GEMM-1 K, GEMM-2 N
+  static_assert((W % 128 == 0 && (TPR == 1 || TPR % 2 == 0)) || W == 64, "128-pixel tiles: row segments or row pairs");
+  static_assert(H % RB == 0 && RB % RPT == 0 && RB >= MH - 1 && TPI % 2 == 0, "band geometry");
+  static_assert(TAPS <= kTcTaps && 32 + MW - 1 <= kTcStripW && MW <= 16 && MW < W, "filter support");
   static_assert(KF % 32 == 0 && KF >= 32 && KF <= 128, "filters per pass");
-  static constexpr size_t d_bytes = (size_t)2 * KF * kTcTaps * 2;
+  static constexpr size_t d_bytes = (size_t)2 * KF * TP * 2;
   static constexpr size_t lam_off = d_bytes;
   static constexpr size_t lam_bytes = (size_t)2 * SR * LWW * 4;
   static constexpr size_t strip_off = (lam_off + lam_bytes + 15) / 16 * 16;
@@ -168,12 +171,12 @@ __device__ __forceinline__ uint32_t lds_u16(const void* p) {
 // word loads + a byte permute; pairs across tap rows two half loads.
 template <class G>
 __device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint32_t A) {
-  constexpr int MW = G::MW, TAPS = G::TAPS, LWW = G::LWW, SR = G::SR;
+  constexpr int MW = G::MW, TAPS = G::TAPS, LWW = G::LWW, SR = G::SR, TP = G::TP;
   const int cb = c >> 1, par = c & 1;
   const uint32_t sel_e = par ? 0x5432u : 0x3210u;  // pair starting at an even tap column offset
   const uint32_t sel_o = par ? 0x3210u : 0x5432u;
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
+  for (int ch = 0; ch < TP / 32; ++ch) {
     uint32_t vv[2][16];
 #pragma unroll
     for (int pl = 0; pl < 2; ++pl) {
@@ -211,7 +214,8 @@ __device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint
 // warm state that is not ADMM-consistent).
 template <class G, bool FULL, bool T0>
 __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_constant__ TcArgs a) {
-  constexpr int H = G::H, W = G::W, KF = G::KF, MW = G::MW, RB = G::RB, D = G::D, TPR = G::TPR,
+  constexpr int H = G::H, W = G::W, KF = G::KF, MW = G::MW, RB = G::RB, D = G::D, TPR = G::TPR, TP = G::TP,
+                WT = G::WT, RPT = G::RPT,
                 NBANDS = G::NBANDS, TPI = G::TPI, SR = G::SR, LWW = G::LWW, TAPS = G::TAPS;
   extern __shared__ __align__(1024) unsigned char sm[];
   const __half* Ds = reinterpret_cast<const __half*>(sm);
@@ -254,13 +258,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
     // ===== producer warps: GEMM issue (warp 0, lane 0); u row streaming by TMA (last warp) =====
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(dbar, (unsigned)G::d_bytes);
-      for (int i = 0; i < (int)(G::d_bytes / 16384); ++i)
-        bulk_g2s(const_cast<__half*>(Ds) + i * 8192, a.dsplit + i * 8192, 16384u, dbar);
+      static_assert(G::d_bytes % 8192 == 0, "dictionary split in 8 KB bulk copies");
+      for (int i = 0; i < (int)(G::d_bytes / 8192); ++i)
+        bulk_g2s(const_cast<__half*>(Ds) + i * 4096, a.dsplit + i * 4096, 8192u, dbar);
       mbar_wait(dbar, 0);
     }
     __syncwarp();
-    const uint32_t dh = umma::smem_u32(Ds), dl = dh + KF * kTcTaps * 2;
-    constexpr uint32_t id1 = umma::idesc_f16(128, KF, 0), id2 = umma::idesc_f16(128, kTcTaps, 1);
+    const uint32_t dh = umma::smem_u32(Ds), dl = dh + KF * TP * 2;
+    constexpr uint32_t id1 = umma::idesc_f16(128, KF, 0), id2 = umma::idesc_f16(128, TP, 1);
+    constexpr uint32_t FGS = (uint32_t)TP * 16u;  // bytes per filter group (8 filters x TP taps) in the D grid
     // the CTA owns all 512 TMEM columns, so the allocation starts at address 0
     // (checked below); slot addresses are then warp-uniform immediates
     // slot as a compile-time constant: TMEM addresses become immediates
@@ -268,8 +274,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
       constexpr uint32_t A = 256u * decltype(S)::value, acc = A + 128u;
       umma::fence_after_sync();
 #pragma unroll
-      for (int j = 0; j < kTcTaps / 16; ++j) {  // K = taps; B K-major: LBO 128 B (taps), SBO 2048 B (filters)
-        const uint64_t bh = umma::sdesc(dh + 256u * j, 128u, 2048u), bl = umma::sdesc(dl + 256u * j, 128u, 2048u);
+      for (int j = 0; j < TP / 16; ++j) {  // K = taps; B K-major: LBO 128 B (taps), SBO FGS (filters)
+        const uint64_t bh = umma::sdesc(dh + 256u * j, 128u, FGS), bl = umma::sdesc(dl + 256u * j, 128u, FGS);
         umma::mma_ts_warp(acc, A + 8u * j, bh, id1, j > 0);
         umma::mma_ts_warp(acc, A + 8u * j, bl, id1, 1u);
         umma::mma_ts_warp(acc, A + 64u + 8u * j, bh, id1, 1u);
@@ -280,8 +286,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
       constexpr uint32_t A = 256u * decltype(S)::value, acc = A + 128u;
       umma::fence_after_sync();
 #pragma unroll
-      for (int j = 0; j < KF / 16; ++j) {  // K = filters; B MN-major: LBO 2048 B (filters), SBO 128 B (taps)
-        const uint64_t bh = umma::sdesc(dh + 4096u * j, 2048u, 128u), bl = umma::sdesc(dl + 4096u * j, 2048u, 128u);
+      for (int j = 0; j < KF / 16; ++j) {  // K = filters; B MN-major: LBO FGS (filters), SBO 128 B (taps)
+        const uint64_t bh = umma::sdesc(dh + 2u * FGS * j, FGS, 128u), bl = umma::sdesc(dl + 2u * FGS * j, FGS, 128u);
         umma::mma_ts_warp(acc, A + 8u * j, bh, id2, j > 0);
         umma::mma_ts_warp(acc, A + 8u * j, bl, id2, 1u);
         umma::mma_ts_warp(acc, A + 64u + 8u * j, bh, id2, 1u);
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
           break;
         const int n = c_item[e] / NBANDS, b = c_item[e] % NBANDS, i = c_i[e];
         const int t = e + 2 * (i / NCU), k0 = 16 * (i % NCU);
-        const int r = b * RB + t / TPR, c0 = (t % TPR) * 128;
+        const int r = b * RB + (t / TPR) * RPT, c0 = (t % TPR) * 128;  // the tile's first pixel
         const int nv = FULL ? 16 : max(0, min(16, a.K - k0));
         unsigned long long* fb = ufull + e * kTcUSlots + sl;
         (void)nv;
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
           const int ip = i + kTcUPrefetch;
           const int tp = e + 2 * (ip / NCU), kp = 16 * (ip % NCU);
           asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&a.umap),
-                       "r"((b * RB + tp / TPR) * W + (tp % TPR) * 128), "r"(a.plane0 + n * a.K + kp)
+                       "r"((b * RB + (tp / TPR) * RPT) * W + (tp % TPR) * 128), "r"(a.plane0 + n * a.K + kp)
                        : "memory");
         }
         if (lane == 0) {  // one 2-D TMA: 16 planes x 128 pixels (rows past the last plane are zero-filled)
@@ -413,8 +419,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
       for (int t = e; t < TPI; t += 2) {
         TCT(0)
         const uint32_t gg = g + t, ph = (gg >> 1) & 1u;
-        const int rl = t / TPR, tc = t % TPR;
-        const int r = b * RB + rl, c = tc * 128 + p;
+        const int tc = t % TPR;
+        const int rl = (t / TPR) * RPT + p / WT;  // this pixel's band-local row
+        const int r = b * RB + rl, c = tc * 128 + p % WT;
         float* const up = ubase + (size_t)r * W + c;
         const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
         // --- im2col(lambda) -> A
@@ -510,14 +517,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         st[4] += (double)(rho2 * f4); st[5] += (double)f5; st[6] = fmax(st[6], (double)f6);
         // --- col2im: s[r + oy][c + ox] += Z[p][o] into this warp's strip
         const float zsc = dinv / sw;
-        float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;
+        float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;  // warp-uniform row
         mbar_wait(z_full + e, ph);
         umma::fence_after_sync();
         TCT(5)
         {
           uint32_t v[4][32];
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch)
+          for (int ch = 0; ch < TP / 32; ++ch)
             if (ch * 32 < TAPS) umma::ld32(ACC + ch * 32, v[ch]);
           umma::wait_ld();
           // taps (oy, ox) of one ox touch distinct strip rows: 11 independent
@@ -574,7 +581,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         for (int s2 = 0; s2 < G::NSS; ++s2)
 #pragma unroll
           for (int q2 = 0; q2 < 4; ++q2) {
-            int off = col - ((TPR == 1 ? 0 : s2 * 128) + 32 * q2);
+            int off = col - ((TPR == 1 ? 0 : s2 * 128) + (32 * q2) % WT);
             if (off < 0) off += W;
             if (off < 32 + MW - 1) v += STR[(s2 * 4 + q2) * G::STRIP + lr * kTcStripW + off];
           }
@@ -710,17 +717,17 @@ __global__ void tc_pair_transpose(const float2* __restrict__ src, float2* __rest
 }
 
 // dictionary K x TAPS (FP64, tap o = y*MW + x) -> f16 hi / lo core-matrix grid:
-// element (k, o) at ((k/8)*16 + o/8)*64 + (k%8)*8 + o%8 halves; zero padded to KF x 128.
-template <int KF>
+// element (k, o) at ((k/8)*(TP/8) + o/8)*64 + (k%8)*8 + o%8 halves; zero padded to KF x TP.
+template <int KF, int TP>
 __global__ void tc_dsplit(const double* __restrict__ d, int K, int taps, float scale, __half* __restrict__ out) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KF * kTcTaps; i += gridDim.x * blockDim.x) {
-    const int k = i / kTcTaps, o = i % kTcTaps;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KF * TP; i += gridDim.x * blockDim.x) {
+    const int k = i / TP, o = i % TP;
     const float v = (k < K && o < taps) ? (float)d[(size_t)k * taps + o] : 0.f;
     __half hi, lo;
     umma::split2(v, scale, hi, lo);
-    const int idx = (((k >> 3) * 16 + (o >> 3)) * 8 + (k & 7)) * 8 + (o & 7);
+    const int idx = (((k >> 3) * (TP / 8) + (o >> 3)) * 8 + (k & 7)) * 8 + (o & 7);
     out[idx] = hi;
-    out[KF * kTcTaps + idx] = lo;
+    out[KF * TP + idx] = lo;
   }
 }
 

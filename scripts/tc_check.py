@@ -12,11 +12,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1709_09479_b200 import dcsc  # noqa: E402
 
 
-def run(tc, grid, K, N, admm, seed=3):
+def run(tc, grid, K, N, admm, seed=3, m=11):
     os.environ["DCSC_TC"] = "1" if tc else "0"
     cfg = dcsc.SolverConfig(beta=0.5, rho=0.1, max_admm=admm, seed=seed)
-    x, dtrue = dcsc.synth_generate(N, grid, K, 11, 0.01, 0.01, seed, True)[:2]
-    with dcsc.Context(N, grid, K, (11, 11), cfg, precision=32) as ctx:
+    x, dtrue = dcsc.synth_generate(N, grid, K, m, 0.01, 0.01, seed, True)[:2]
+    with dcsc.Context(N, grid, K, (m, m), cfg, precision=32) as ctx:
         ctx.set_signals(x)
         ctx.init_variables()
         ctx.coding()  # warm (and the first call's setup)
@@ -32,9 +32,9 @@ def run(tc, grid, K, N, admm, seed=3):
 def main():
     N = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     admm = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-    for grid, K in (((256, 256), 128), ((128, 128), 64)):
-        a = run(True, grid, K, N, admm)
-        b = run(False, grid, K, N, admm)
+    for grid, K, m in (((256, 256), 128, 11), ((128, 128), 64, 11), ((64, 64), 32, 7), ((64, 64), 20, 7)):
+        a = run(True, grid, K, N, admm, m=m)
+        b = run(False, grid, K, N, admm, m=m)
         rel = lambda u, v: float(np.abs(u - v).max() / max(np.abs(v).max(), 1e-30))
         print(f"grid {grid} K={K} N={N} admm<={admm}: tc {a[4]*1e3:.1f} ms  fft {b[4]*1e3:.1f} ms")
         print("  iters tc ", [s["admm_iters"] for s in a[0]], " fft", [s["admm_iters"] for s in b[0]])

@@ -23,11 +23,11 @@ def rel(a, b):
     return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
 
 
-def run_coding(monkeypatch, tc, x, d, K, admm, theta=None, z=None):
+def run_coding(monkeypatch, tc, x, d, K, admm, theta=None, z=None, m=11):
     monkeypatch.setenv("DCSC_TC", "1" if tc else "0")
     N = x.shape[0]
     cfg = dcsc.SolverConfig(beta=0.5, rho=0.1, max_admm=admm, normalize=0)
-    with dcsc.Context(N, x.shape[1:], K, (11, 11), cfg, 32) as ctx:
+    with dcsc.Context(N, x.shape[1:], K, (m, m), cfg, 32) as ctx:
         assert ctx.coding_path() == ("tensor" if tc else "fft")
         ctx.set_signals(x)
         ctx.set_dictionary(d)
@@ -38,15 +38,16 @@ def run_coding(monkeypatch, tc, x, d, K, admm, theta=None, z=None):
     return st, th, zz, lam
 
 
-@pytest.mark.parametrize("grid,K", [((256, 256), 128), ((256, 256), 40), ((128, 128), 64), ((128, 128), 20)])
-def test_tc_pass_matches_fft_pass(monkeypatch, grid, K):
-    """256 x 256: the cluster family (row-major u); 128 x 128: the single-CTA
-    family, whose column-major pixel-pair u planes the pass converts around
-    each coding call."""
-    x, _ = dcsc.synth_generate(3, grid, K, 11, 0.01, 0.01, 11, True)
-    d = ref.init_dictionary(K, (11, 11), grid, seed=5)
-    a = run_coding(monkeypatch, True, x, d, K, 30)
-    b = run_coding(monkeypatch, False, x, d, K, 30)
+@pytest.mark.parametrize("grid,K,m", [((256, 256), 128, 11), ((256, 256), 40, 11), ((128, 128), 64, 11),
+                                      ((128, 128), 20, 11), ((64, 64), 32, 7), ((64, 64), 12, 7)])
+def test_tc_pass_matches_fft_pass(monkeypatch, grid, K, m):
+    """256 x 256: the cluster family (row-major u); 128 x 128 and 64 x 64 (tiles
+    of two rows, 7 x 7 supports padded to 64 taps): the single-CTA family, whose
+    column-major pixel-pair u planes the pass converts around each coding call."""
+    x, _ = dcsc.synth_generate(3, grid, K, m, 0.01, 0.01, 11, True)
+    d = ref.init_dictionary(K, (m, m), grid, seed=5)
+    a = run_coding(monkeypatch, True, x, d, K, 30, m=m)
+    b = run_coding(monkeypatch, False, x, d, K, 30, m=m)
     assert [s["admm_iters"] for s in a[0]] == [s["admm_iters"] for s in b[0]]
     for key in ("primal_residual", "z_change", "theta_change", "dual_objective", "dual_infeasibility"):
         va = np.array([s[key] for s in a[0]])
