@@ -229,8 +229,11 @@ int dcsc_cuda_device_bytes(dcsc_cuda_ctx* ctx, size_t* bytes);
 /* Which ADMM coding iteration the context runs (no reference counterpart:
  * the reference has one, admm_coding, coding.cpp:166-329):
  * 0 = the fused FFT pass (half-spectrum c2r / prox / r2c per filter),
- * 1 = the tensor-core spatial pass (FP32 planes of 128-pixel row tiles,
- *     11 x 11 supports, K <= 128, one channel; DCSC_TC=0 disables it). */
+ * 1 = the tensor-core spatial pass (FP32 grids 256^2, 128^2, 100^2, 80^2
+ *     with 11 x 11 supports and 64^2 with 7 x 7, K <= 128, one channel),
+ *     for a coding call over all the context's images. It runs for batches of
+ *     at least two work items per SM; DCSC_TC=1 forces it whenever it
+ *     applies, DCSC_TC=0 disables it. */
 int dcsc_cuda_coding_path(dcsc_cuda_ctx* ctx, int* path);
 
 /* multi-rank: one context per GPU holds its shard of images; learning sums

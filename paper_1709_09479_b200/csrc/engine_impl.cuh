@@ -237,13 +237,15 @@ class Engine final : public EngineBase {
   // The pass works on row-major u planes: the cluster family's own layout; the
   // single-CTA family (column-major pixel pairs) runs it on a row-major copy
   // (tu_) converted once before and after each coding call.
-  static constexpr bool kTcFamily = std::is_same<R, float>::value && H % 16 == 0 &&
-                                    ((W % 128 == 0 && (W / 128 == 1 || (W / 128) % 2 == 0)) || W == 64);
+  static constexpr int kTcRB = H % 16 == 0 ? 16 : 20;  // band rows (C2's 100 x 100: 20)
+  static constexpr bool kTcFamily = std::is_same<R, float>::value && H % kTcRB == 0 &&
+                                    ((W % 128 == 0 && (W / 128 == 1 || (W / 128) % 2 == 0)) || W == 64 ||
+                                     (W > 64 && W < 128 && W % 4 == 0));
   // compiled support (square) and filter-slot counts per family: 64 x 64 (C4) runs
   // 7 x 7 supports with 32 / 64 filter slots, the wider grids 11 x 11 with 64 / 128
   static constexpr int kTcM = W == 64 ? 7 : 11, kTcKFa = W == 64 ? 32 : 64, kTcKFb = W == 64 ? 64 : 128;
   template <int KF>
-  using TG = TcGeom<H, W, KF, kTcM, kTcM, 16>;
+  using TG = TcGeom<H, W, KF, kTcM, kTcM, kTcRB>;
   template <int KF>
   static void set_tc_attr() {
     const int sm = (int)TG<KF>::smem;
@@ -545,7 +547,11 @@ class Engine final : public EngineBase {
                    3 * r_.bytes + cvec_.bytes + phat_.bytes + partial_.bytes + ginv_.bytes + what_.bytes +
                    dhat_rb_.bytes;
     if constexpr (kTcFamily) {
+      // DCSC_TC: 0 = FFT pass, 1 = tensor-core pass whenever it applies; unset =
+      // tensor-core pass for coding calls with at least two work items per SM
+      // (smaller batches leave SMs idle and the FFT pass wins)
       const char* e = std::getenv("DCSC_TC");
+      tc_force_ = e && e[0] == '1';
       tc_ = J_ == 1 && mh_ == kTcM && mw_ == kTcM && K_ <= kTcKFb && !(e && e[0] == '0');
       if (tc_) {
         using G = TG<kTcKFb>;  // band geometry does not depend on the filter count
@@ -572,8 +578,10 @@ class Engine final : public EngineBase {
             CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
-        if (std::getenv("DCSC_VERBOSE")) std::fprintf(stderr, "dcsc: tensor-core coding pass (KF=%d)\n", tc_kf_);
-        coding_path = 1;
+        coding_path = tc_use(N_) ? 1 : 0;
+        if (std::getenv("DCSC_VERBOSE"))
+          std::fprintf(stderr, "dcsc: tensor-core coding pass available (KF=%d), used for all %d images: %d\n", tc_kf_,
+                       N_, coding_path);
       }
     }
     CK(cudaMemsetAsync(u_.p, 0, u_.bytes, st_));
@@ -690,6 +698,12 @@ class Engine final : public EngineBase {
         });
       }
     }
+  }
+  bool tc_use(int cnt) const {
+    if constexpr (kTcFamily) {
+      return tc_ && (tc_force_ || (long)cnt * TG<kTcKFb>::NBANDS >= 2L * tc_grid_);
+    }
+    return false;
   }
   // lambda_hat -> spatial lambda -> scaled f16 hi / lo planes for the tensor-core pass
   void tc_lambda_spatial(int n0, int cnt) {
@@ -1112,7 +1126,7 @@ class Engine final : public EngineBase {
     if (all_zero && J_ == 1) lam_update(0, 0, 1);
     // tensor-core pass for this call (the single-CTA family keeps a warm state that
     // is not ADMM-consistent on the FFT pass: its theta0 is in the pair layout)
-    const bool tc = tc_ && (CLU || !t0_pending);
+    const bool tc = tc_use(cnt) && (CLU || !t0_pending);
     if (tc) {
       if (!CLU) tc_convert_u(n0, cnt, true);
       tc_lambda_spatial(n0, cnt);
@@ -2215,7 +2229,7 @@ class Engine final : public EngineBase {
   DevMem zf_, xf_, gf_, rf_, pf_, apf_, fsend_, fpart_, fodata_, fcpart_;
   bool use_theta0_ = false;
   // tensor-core coding pass (kernels_tc.cuh)
-  bool tc_ = false;
+  bool tc_ = false, tc_force_ = false;
   int tc_kf_ = 128, tc_grid_ = 148;
   float tc_dscale_ = 1.f;
   DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_, tu_, tupd_;

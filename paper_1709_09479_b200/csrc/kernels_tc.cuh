@@ -75,8 +75,11 @@ template <int H_, int W_, int KF_, int MH_, int MW_, int RB_>
 struct TcGeom {
   static constexpr int H = H_, W = W_, KF = KF_, MH = MH_, MW = MW_, RB = RB_;
   static constexpr int D = H * W;
-  static constexpr int WT = W < 128 ? W : 128;     // tile width: a 128-pixel tile is RPT rows x WT pixels
-  static constexpr int RPT = 128 / WT;             // image rows per tile (2 at W = 64)
+  // a 128-lane tile is RPT image rows x WT pixels: row segments of 128 (W a multiple of 128),
+  // row pairs (W = 64), or one row with 128 - W idle lanes (64 < W < 128)
+  static constexpr int WT = W < 128 ? W : 128;
+  static constexpr int RPT = W <= 64 ? 128 / W : 1;
+  static constexpr int VALID = WT * RPT;           // live lanes of a tile
   static constexpr int TPR = W / WT;               // tiles per row (tile rows of RPT image rows)
   static constexpr int NBANDS = H / RB;
   static constexpr int TPI = (RB / RPT) * TPR;     // tiles per work item
@@ -87,7 +90,8 @@ struct TcGeom {
   static constexpr int STRIP = SR * kTcStripW;
   static constexpr int TAPS = MH * MW;
   static constexpr int TP = TAPS <= 64 ? 64 : 128;  // taps padded: GEMM-1 K, GEMM-2 N
-  static_assert((W % 128 == 0 && (TPR == 1 || TPR % 2 == 0)) || W == 64, "128-pixel tiles: row segments or row pairs");
+  static_assert((W % 128 == 0 && (TPR == 1 || TPR % 2 == 0)) || W == 64 || (W > 64 && W < 128 && W % 4 == 0),
+                "128-lane tiles: row segments, row pairs, or single rows");
   static_assert(H % RB == 0 && RB % RPT == 0 && RB >= MH - 1 && TPI % 2 == 0, "band geometry");
   static_assert(TAPS <= kTcTaps && 32 + MW - 1 <= kTcStripW && MW <= 16 && MW < W, "filter support");
   static_assert(KF % 32 == 0 && KF >= 32 && KF <= 128, "filters per pass");
@@ -420,8 +424,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         TCT(0)
         const uint32_t gg = g + t, ph = (gg >> 1) & 1u;
         const int tc = t % TPR;
-        const int rl = (t / TPR) * RPT + p / WT;  // this pixel's band-local row
-        const int r = b * RB + rl, c = tc * 128 + p % WT;
+        const bool live = p < G::VALID;           // lanes past a short row (64 < W < 128) carry zeros
+        const int pc = live ? p : p - G::VALID;   // in-row stand-in for a dead lane's addresses
+        const int rl = (t / TPR) * RPT + pc / WT;  // this pixel's band-local row
+        const int r = b * RB + rl, c = tc * 128 + pc % WT;
         float* const up = ubase + (size_t)r * W + c;
         const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
         // --- im2col(lambda) -> A
@@ -437,7 +443,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         // per-pair accumulators (packed FP32), folded once per tile
         F2 a0 = f2(0.f, 0.f), a1 = a0, a2 = a0, a4 = a0, a5 = a0;
         float f6 = 0.f, wmax = 0.f;
-        const F2 tsc2 = f2(tsc, tsc);
+        const float tsl = live ? tsc : 0.f;  // dead lanes: t = u = 0, so w = 0 and no stop-test share
+        const F2 tsc2 = f2(tsl, tsl);
         mbar_wait(t_full + e, ph);
         umma::fence_after_sync();
         TCT(2)
@@ -449,7 +456,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int k = ch * 16 + j;
-              tcur[j] = (FULL || k < a.K) ? __ldg(t0p + (size_t)k * D) : 0.f;
+              tcur[j] = ((FULL || k < a.K) && live) ? __ldg(t0p + (size_t)k * D) : 0.f;
             }
           }
           uint32_t v[16];
@@ -458,8 +465,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
             const int k0 = ch * 16 + 2 * jj;
-            const float u0 = (FULL || k0 < a.K) ? ucur[2 * jj] : 0.f;
-            const float u1 = (FULL || k0 + 1 < a.K) ? ucur[2 * jj + 1] : 0.f;
+            const float u0 = ((FULL || k0 < a.K) && live) ? ucur[2 * jj] : 0.f;
+            const float u1 = ((FULL || k0 + 1 < a.K) && live) ? ucur[2 * jj + 1] : 0.f;
             const F2 t = mul2(f2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1])), tsc2);
             float o0, o1;
             if constexpr (T0) {
@@ -483,8 +490,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
             const F2 w = add2(th, d_z);  // w = theta' + z'/rho = 2 theta' - u'
             const float w0 = f2x(w), w1 = f2y(w);
             wmax = fmaxf(wmax, fmaxf(fabsf(w0), fabsf(w1)));
-            if (FULL || k0 < a.K) __stcs(up + (size_t)k0 * D, un0);
-            if (FULL || k0 + 1 < a.K) __stcs(up + (size_t)(k0 + 1) * D, un1);
+            if ((FULL || k0 < a.K) && live) __stcs(up + (size_t)k0 * D, un0);
+            if ((FULL || k0 + 1 < a.K) && live) __stcs(up + (size_t)(k0 + 1) * D, un1);
             v[2 * jj] = __float_as_uint(w0);
             v[2 * jj + 1] = __float_as_uint(w1);
           }
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
             for (int oy = 0; oy < G::MH; ++oy) {
               const int o = oy * MW + ox;
               float* sp = S + oy * kTcStripW + ox;
-              *sp = fmaf(__uint_as_float(v[o / 32][o % 32]), zsc, *sp);
+              if (live) *sp = fmaf(__uint_as_float(v[o / 32][o % 32]), zsc, *sp);
             }
             __syncwarp();
           }

@@ -32,7 +32,12 @@ def run(tc, grid, K, N, admm, seed=3, m=11):
 def main():
     N = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     admm = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-    for grid, K, m in (((256, 256), 128, 11), ((128, 128), 64, 11), ((64, 64), 32, 7), ((64, 64), 20, 7)):
+    cases = (((256, 256), 128, 11), ((128, 128), 64, 11), ((100, 100), 100, 11), ((80, 80), 24, 11),
+             ((64, 64), 32, 7), ((64, 64), 20, 7))
+    only = os.environ.get("TC_ONLY")
+    for grid, K, m in cases:
+        if only and str(grid[0]) not in only.split(","):
+            continue
         a = run(True, grid, K, N, admm, m=m)
         b = run(False, grid, K, N, admm, m=m)
         rel = lambda u, v: float(np.abs(u - v).max() / max(np.abs(v).max(), 1e-30))

@@ -39,10 +39,12 @@ def run_coding(monkeypatch, tc, x, d, K, admm, theta=None, z=None, m=11):
 
 
 @pytest.mark.parametrize("grid,K,m", [((256, 256), 128, 11), ((256, 256), 40, 11), ((128, 128), 64, 11),
-                                      ((128, 128), 20, 11), ((64, 64), 32, 7), ((64, 64), 12, 7)])
+                                      ((128, 128), 20, 11), ((100, 100), 100, 11), ((80, 80), 24, 11),
+                                      ((64, 64), 32, 7), ((64, 64), 12, 7)])
 def test_tc_pass_matches_fft_pass(monkeypatch, grid, K, m):
-    """256 x 256: the cluster family (row-major u); 128 x 128 and 64 x 64 (tiles
-    of two rows, 7 x 7 supports padded to 64 taps): the single-CTA family, whose
+    """256 x 256: the cluster family (row-major u); 128 x 128, 100 x 100 and 80 x 80
+    (one row per 128-lane tile, idle lanes past the row) and 64 x 64 (tiles of two
+    rows, 7 x 7 supports padded to 64 taps): the single-CTA family, whose
     column-major pixel-pair u planes the pass converts around each coding call."""
     x, _ = dcsc.synth_generate(3, grid, K, m, 0.01, 0.01, 11, True)
     d = ref.init_dictionary(K, (m, m), grid, seed=5)
@@ -94,3 +96,19 @@ def test_tc_inconsistent_warm_state_matches_reference(monkeypatch, kind):
             assert abs(st[0][key] - s_r[key]) <= TOL * max(abs(s_r[key]), 1e-30), (admm, key)
         assert rel(z_g[0], z_r) <= TOL, admm
         assert rel(lam_g[0], lam_r) <= TOL, admm
+
+
+def test_tc_pass_is_chosen_for_large_batches_only(monkeypatch):
+    """Default (DCSC_TC unset): the tensor-core pass for batches of >= 2 work
+    items per SM (C3: 512 images), the FFT pass for small ones; DCSC_TC=0 never."""
+    monkeypatch.delenv("DCSC_TC", raising=False)
+    cfg = dcsc.SolverConfig(max_admm=1, normalize=0)
+    with dcsc.Context(512, (256, 256), 128, (11, 11), cfg, 32) as ctx:
+        assert ctx.coding_path() == "tensor"
+    with dcsc.Context(2, (256, 256), 128, (11, 11), cfg, 32) as ctx:
+        assert ctx.coding_path() == "fft"
+    with dcsc.Context(512, (128, 128), 64, (11, 11), cfg, 64) as ctx:  # FP64: FFT pass only
+        assert ctx.coding_path() == "fft"
+    monkeypatch.setenv("DCSC_TC", "0")
+    with dcsc.Context(512, (256, 256), 128, (11, 11), cfg, 32) as ctx:
+        assert ctx.coding_path() == "fft"
