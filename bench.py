@@ -64,9 +64,10 @@ CONFIGS = {
     # C1 with J = 3 channels (Joint mode / TCSC; not a BASELINE config)
     "c1j3": dict(N=256, H=128, W=128, K=64, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
                  max_admm=50, outer=1, J=3),
-    # C3-shaped coding slice for profiling only (not a BASELINE config)
+    # C3-shaped coding slice for profiling only (not a BASELINE config); 16 images are below the
+    # tensor-core pass's default batch threshold, so it is forced (DCSC_TC=1) to profile C3's kernel
     "c3s": dict(N=16, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
-                max_admm=10, outer=1),
+                max_admm=10, outer=1, env={"DCSC_TC": "1"}),
     "c4": dict(N=2048, H=64, W=64, K=32, m=7, prec=32, beta=0.5, p=0.005, sigma=0.05, coding_only=False,
                max_admm=500, outer=10),
 }
@@ -734,6 +735,8 @@ def main():
     if rc is not None:
         return rc
     cfg = CONFIGS[args.config]
+    for k, v in cfg.get("env", {}).items():
+        os.environ.setdefault(k, v)
     if args.dump_counts:
         return dump_counts(args, cfg)
     if args.impl == "reference":
