@@ -259,17 +259,17 @@ class Engine final : public EngineBase {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   }
   template <int KF>
-  void launch_tc(int grid, const TcArgs& a) {
+  void launch_tc(int grid, const TcArgs& a, cudaStream_t st) {
     constexpr size_t sm = TG<KF>::smem;
     const bool full = a.K == KF, t0 = a.theta0 != nullptr;
     if (full && !t0)
-      coding_pass_tc<TG<KF>, true, false><<<grid, kTcThreads, sm, st_>>>(a);
+      coding_pass_tc<TG<KF>, true, false><<<grid, kTcThreads, sm, st>>>(a);
     else if (full)
-      coding_pass_tc<TG<KF>, true, true><<<grid, kTcThreads, sm, st_>>>(a);
+      coding_pass_tc<TG<KF>, true, true><<<grid, kTcThreads, sm, st>>>(a);
     else if (!t0)
-      coding_pass_tc<TG<KF>, false, false><<<grid, kTcThreads, sm, st_>>>(a);
+      coding_pass_tc<TG<KF>, false, false><<<grid, kTcThreads, sm, st>>>(a);
     else
-      coding_pass_tc<TG<KF>, false, true><<<grid, kTcThreads, sm, st_>>>(a);
+      coding_pass_tc<TG<KF>, false, true><<<grid, kTcThreads, sm, st>>>(a);
   }
   // persistent pipelined r2c / c2r (SmemPipe) when the staging buffer fits and
   // the planes are 16-byte aligned storage-precision planes: grid = resident slots
@@ -578,6 +578,7 @@ class Engine final : public EngineBase {
             CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+        CK(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
         coding_path = tc_use(N_) ? 1 : 0;
         if (std::getenv("DCSC_VERBOSE"))
           std::fprintf(stderr, "dcsc: tensor-core coding pass available (KF=%d), used for all %d images: %d\n", tc_kf_,
@@ -607,6 +608,7 @@ class Engine final : public EngineBase {
     if (pin_) cudaFreeHost(pin_);
     if (xstage_) cudaFreeHost(xstage_);
     if (st_) cudaStreamDestroy(st_);
+    if (st2_) cudaStreamDestroy(st2_);
   }
 
   // ------------------------------------------------------------ launches
@@ -622,18 +624,19 @@ class Engine final : public EngineBase {
     return evpool_[evused_++];
   }
   template <class F>
-  void launch(int fam, F&& f) {
+  void launch(int fam, F&& f, cudaStream_t s = nullptr) {
+    if (!s) s = st_;
     cudaEvent_t a = nullptr, b = nullptr;
     const bool prof = profiling_ == 1 || (profiling_ >= 2 && fam == kFamCoding) || (profiling_ == 3 && fam == kFamContract);
     if (prof) {
       a = pooled_event();
       b = pooled_event();
-      CK(cudaEventRecord(a, st_));
+      CK(cudaEventRecord(a, s));
     }
     f();
     CK(cudaGetLastError());
     if (prof) {
-      CK(cudaEventRecord(b, st_));
+      CK(cudaEventRecord(b, s));
       prof_.push_back({fam, a, b});
     }
     ++launches;
@@ -706,21 +709,25 @@ class Engine final : public EngineBase {
     return false;
   }
   // lambda_hat -> spatial lambda -> scaled f16 hi / lo planes for the tensor-core pass
-  void tc_lambda_spatial(int n0, int cnt) {
+  void tc_lambda_spatial(int n0, int cnt, cudaStream_t s = nullptr) {
     if constexpr (kTcFamily) {
-      c2r<R>(lamhat_.as<C>() + (size_t)n0 * NB, NB, lam_.as<R>() + (size_t)n0 * D, D, cnt);
+      if (!s) s = st_;
+      launch(kFamOther, [&] {
+        launch_c2r<R>(cnt, s, lamhat_.as<C>() + (size_t)n0 * NB, NB, lam_.as<R>() + (size_t)n0 * D, D, dtw_.as<C>());
+      }, s);
       launch(kFamLambda, [&] {
-        tc_lam_split<D><<<cnt, 512, 0, st_>>>(lam_.as<R>() + (size_t)n0 * D, tlam16_.as<uint32_t>() + (size_t)n0 * D,
-                                              tlscale_.as<float>() + n0);
-      });
+        tc_lam_split<D><<<cnt, 512, 0, s>>>(lam_.as<R>() + (size_t)n0 * D, tlam16_.as<uint32_t>() + (size_t)n0 * D,
+                                            tlscale_.as<float>() + n0);
+      }, s);
     }
   }
   // One ADMM iteration of images [n0, n0 + cnt) on the tensor-core path:
   // spatial pass (t, prox, s = sum_k d_k * w_k) -> band sums -> DFT(s) ->
   // stop test + lambda_hat (lambda_update, coding.cpp:264-283, :25-37) ->
   // spatial lambda for the next iteration.
-  void tc_iteration(int n0, int cnt, int it, bool last) {
+  void tc_iteration(int n0, int cnt, int it, bool last, cudaStream_t st = nullptr) {
     if constexpr (kTcFamily) {
+      if (!st) st = st_;
       using G = TG<kTcKFb>;
       TcArgs a;
       a.lam16 = tlam16_.as<uint32_t>() + (size_t)n0 * D;
@@ -741,26 +748,28 @@ class Engine final : public EngineBase {
       const int grid = std::min(tc_grid_, cnt * G::NBANDS);
       launch(kFamCoding, [&] {
         if (tc_kf_ == kTcKFa)
-          launch_tc<kTcKFa>(grid, a);
+          launch_tc<kTcKFa>(grid, a, st);
         else
-          launch_tc<kTcKFb>(grid, a);
-      });
+          launch_tc<kTcKFb>(grid, a, st);
+      }, st);
       R* s = lam_.as<R>() + (size_t)n0 * D;          // s reuses the spatial lambda planes
       C* spec = part_.as<C>() + (size_t)n0 * NB;      // one partial spectrum per image (G = 1)
       double* sm1 = sums_.as<double>() + (size_t)n0 * kSums;
       int* upd = tupd_.as<int>() + n0;
       launch(kFamLambda, [&] {
-        tc_band_reduce<G><<<dim3(16, cnt), 256, 0, st_>>>(a.spart, a.bsums, conv_.as<int>() + n0, s,
-                                                         img_.as<ImageAdmm>() + n0, upd, it, last ? 1 : 0);
-      });
+        tc_band_reduce<G><<<dim3(16, cnt), 256, 0, st>>>(a.spart, a.bsums, conv_.as<int>() + n0, s,
+                                                        img_.as<ImageAdmm>() + n0, upd, it, last ? 1 : 0);
+      }, st);
       (void)sm1;
       if (last) return;
-      r2c(s, false, D, spec, NB, cnt);
+      launch(kFamOther, [&] {
+        launch_r2c<R>(cnt, st, s, D, spec, NB, dtw_.as<C>(), nullptr, 1);
+      }, st);
       launch(kFamLambda, [&] {
-        tc_lambda_apply<R><<<dim3(32, cnt), 256, 0, st_>>>(spec, xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(),
-                                                          lamhat_.as<C>() + (size_t)n0 * NB, upd, NB, R(cfg_.rho));
-      });
-      tc_lambda_spatial(n0, cnt);
+        tc_lambda_apply<R><<<dim3(32, cnt), 256, 0, st>>>(spec, xhat_.as<C>() + (size_t)n0 * NB, sigma_.as<R>(),
+                                                         lamhat_.as<C>() + (size_t)n0 * NB, upd, NB, R(cfg_.rho));
+      }, st);
+      tc_lambda_spatial(n0, cnt, st);
     }
   }
 
@@ -1134,28 +1143,58 @@ class Engine final : public EngineBase {
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    // tensor-core pass on large batches: the images in two halves on two streams,
+    // so each half's per-iteration neighbours (band reduction, lambda_hat
+    // update, the two FFTs, lambda split) run beside the other half's coding
+    // pass instead of between two full-width passes
+    const int half = (tc && tc_use(cnt / 2) && cnt >= 2) ? cnt / 2 : 0;
+    cudaEvent_t ev2[2] = {nullptr, nullptr};
+    if (half) {
+      CK(cudaEventCreateWithFlags(&ev2[0], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev2[1], cudaEventDisableTiming));
+      CK(cudaEventRecord(ev2[0], st_));  // prologue / lambda split / u conversion done
+      CK(cudaStreamWaitEvent(st2_, ev2[0], 0));
+    }
     int pending = -1;  // iteration whose conv flags are in flight
     for (int it = 1; it <= cfg_.max_admm; ++it) {
       use_theta0_ = t0_pending && it == 1;
-      if (tc)
+      if (half) {
+        tc_iteration(n0, half, it, it == cfg_.max_admm, st_);
+        tc_iteration(n0 + half, cnt - half, it, it == cfg_.max_admm, st2_);
+      } else if (tc) {
         tc_iteration(n0, cnt, it, it == cfg_.max_admm);
-      else
+      } else {
         coding_launch<kPassAdmm>(dhat_.as<C>(), n0, cnt, it, it == cfg_.max_admm);
+      }
       use_theta0_ = false;
       if (J_ > 1 && it < cfg_.max_admm) tc_lam(K_, true);
       if (pending >= 0) {
         // one-iteration look-ahead: iteration `it` is queued before we wait on it-1
         CK(cudaEventSynchronize(ev[pending & 1]));
+        if (half) CK(cudaEventSynchronize(ev2[pending & 1]));
         bool all = true;
         for (int i = 0; i < cnt; ++i) all = all && conv_h[(pending & 1) * 65536 + i];
         if (all) break;
       }
       if (cnt <= 65536) {
-        CK(cudaMemcpyAsync(conv_h + (it & 1) * 65536, conv_.as<int>() + n0, sizeof(int) * cnt,
+        const int c1 = half ? half : cnt;
+        CK(cudaMemcpyAsync(conv_h + (it & 1) * 65536, conv_.as<int>() + n0, sizeof(int) * c1,
                            cudaMemcpyDeviceToHost, st_));
         CK(cudaEventRecord(ev[it & 1], st_));
+        if (half) {
+          CK(cudaMemcpyAsync(conv_h + (it & 1) * 65536 + half, conv_.as<int>() + n0 + half,
+                             sizeof(int) * (cnt - half), cudaMemcpyDeviceToHost, st2_));
+          CK(cudaEventRecord(ev2[it & 1], st2_));
+        }
         pending = it;
       }
+    }
+    if (half) {  // join: the exit work on st_ sees both halves
+      CK(cudaEventRecord(ev2[0], st2_));
+      CK(cudaStreamWaitEvent(st_, ev2[0], 0));
+      CK(cudaStreamSynchronize(st2_));
+      cudaEventDestroy(ev2[0]);
+      cudaEventDestroy(ev2[1]);
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
@@ -2217,6 +2256,7 @@ class Engine final : public EngineBase {
   int N_, K_, J_ = 1, mh_, mw_, M_, G_, kpg_, tiles_, accept_chunks_, csplit_ = 1, fused_rows_ = 1184;
   bool no_cg_fuse_ = false;
   cudaStream_t st_ = nullptr;
+  cudaStream_t st2_ = nullptr;  // second half of a tensor-core coding batch
   void* pin_ = nullptr;
   DevMem dtw_, x_, xhat_, dhat_, dcand_, sigma_, u_, maps_, lamhat_, lam_, part_, sums_, conv_, img_, dual_,
       infeas_, resc_, cnt_, odata_, ol1_, accept_, gam_, r_, p_, ap_, cvec_, phat_, live_, dmu_, dwk_, dd_, ddict_, cg_,
