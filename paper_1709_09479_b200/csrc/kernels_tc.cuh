@@ -396,6 +396,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         for (int i = et; i < G::NSTRIP * G::STRIP / 4; i += 32 * kTcEpiWarps) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       epi_sync();
+      if (et == 0 && item + (int)gridDim.x < items) {  // next item's lambda band -> L2 (both f16 planes)
+        const int n2 = (item + gridDim.x) / NBANDS, b2 = (item + gridDim.x) % NBANDS;
+        const int rows = min(SR, H - b2 * RB);  // the wrapped rows (from row 0) are the next bands' anyway
+        for (int pl = 0; pl < 2; ++pl)
+          prefetch_l2_bulk(a.lam16 + ((size_t)(n2 * 2 + pl) * H + b2 * RB) * (W / 2), (unsigned)(rows * W * 2));
+      }
       const float tsc = 1.f / (__ldg(a.lam_scale + n) * a.d_scale);
       const float dinv = 1.f / a.d_scale;
       double st[7] = {0, 0, 0, 0, 0, 0, 0};
