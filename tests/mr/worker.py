@@ -34,10 +34,15 @@ def main():
     N, grid, K, m = 4, (20, 20), 6, 5
     mode = os.environ.get("MR_MODE")
     J = 2 if mode == "gpu_j" else 1
+    prec = 64
+    if mode == "gpu_tc":  # FP32 128 x 128, 11 x 11: the tensor-core coding pass (forced by the test's DCSC_TC=1)
+        N, grid, K, m, prec = 4, (128, 128), 8, 11, 32
     x = mr_signals(dcsc, N, grid, K, m, J)
     n0, n1 = dcsc.shard_range(N, world, rank)
     cfg = dcsc.SolverConfig(beta=0.2, max_outer=3, normalize=0, seed=11, tol=1e-300)
-    with dcsc.Context(n1 - n0, grid, K, (m, m), cfg, 64, channels=J) as ctx:
+    if mode == "gpu_tc":
+        cfg = dcsc.SolverConfig(beta=0.5, max_outer=3, max_admm=60, normalize=0, seed=11, tol=1e-300)
+    with dcsc.Context(n1 - n0, grid, K, (m, m), cfg, prec, channels=J) as ctx:
         ctx.set_comm_callback(world, rank, dcsc.gloo_allreduce_fn())
         if mode == "gpu_freq":  # frequency-sharded learning (one z_hat all-to-all per outer iteration)
             ctx.set_learning_layout("freq")

@@ -27,13 +27,13 @@ def free_port():
     return p
 
 
-def launch(world, mode, tmp_path):
+def launch(world, mode, tmp_path, extra_env=None):
     port = free_port()
     procs, outs = [], []
     for r in range(world):
         out = str(tmp_path / f"rank{r}.npz")
         env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port), MR_OUT=out, MR_MODE=mode)
+                   MASTER_PORT=str(port), MR_OUT=out, MR_MODE=mode, **(extra_env or {}))
         procs.append(subprocess.Popen([sys.executable, WORKER], env=env, stdout=subprocess.PIPE,
                                       stderr=subprocess.STDOUT, text=True))
         outs.append(out)
@@ -194,3 +194,24 @@ print(json.dumps(out))
     assert cp == cn
     assert max(abs(a - b) / abs(b) for a, b in zip(tn, tp)) <= 1e-10
     assert np.abs(np.array(dn) - np.array(dp)).max() <= 1e-9
+
+
+@pytest.mark.gpu
+def test_two_ranks_tensor_core_coding_match_single_rank(tmp_path, monkeypatch):
+    """Image-sharded coding on the tensor-core pass (each rank's images as two
+    half-batches on two streams) + sharded learning reproduce a single-rank FP32
+    run at the FP32 tolerance with equal ADMM iteration counts."""
+    res = launch(2, "gpu_tc", tmp_path, {"DCSC_TC": "1"})
+    monkeypatch.setenv("DCSC_TC", "1")
+    N, grid, K, m = 4, (128, 128), 8, 11
+    x, _ = dcsc.synth_generate(N, grid, K, m, 0.05, 0.01, 7, False)
+    cfg = dcsc.SolverConfig(beta=0.5, max_outer=3, max_admm=60, normalize=0, seed=11, tol=1e-300)
+    one = dcsc.run_csc(x, K, (m, m), cfg, precision=32)
+    keys = ["total", "data_term", "l1_term", "admm_iters", "cg_iters", "mu_iters", "l0"]
+    single = np.array([[r[k] for k in keys] for r in one["trace"]], dtype=np.float64)
+    for r in res:
+        t = r["trace"]
+        assert t.shape == single.shape
+        assert np.all(np.abs(t[:, :3] - single[:, :3]) <= 1e-4 * np.abs(single[:, :3]))
+        assert np.array_equal(t[:, 3], single[:, 3])
+        assert np.abs(r["dict"] - one["dict"]).max() <= 1e-4 * np.abs(one["dict"]).max()
