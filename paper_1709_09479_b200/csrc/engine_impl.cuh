@@ -243,7 +243,9 @@ class Engine final : public EngineBase {
                                      (W > 64 && W < 128 && W % 4 == 0));
   // compiled support (square) and filter-slot counts per family: 64 x 64 (C4) runs
   // 7 x 7 supports with 32 / 64 filter slots, the wider grids 11 x 11 with 64 / 128
-  static constexpr int kTcM = W == 64 ? 7 : 11, kTcKFa = W == 64 ? 32 : 64, kTcKFb = W == 64 ? 64 : 128;
+  // (single-row families 80 / 100: 112 slots for C2's K = 100)
+  static constexpr int kTcM = W == 64 ? 7 : 11, kTcKFa = W == 64 ? 32 : 64,
+                       kTcKFb = W == 64 ? 64 : ((W > 64 && W < 128) ? 112 : 128);
   template <int KF>
   using TG = TcGeom<H, W, KF, kTcM, kTcM, kTcRB>;
   template <int KF>

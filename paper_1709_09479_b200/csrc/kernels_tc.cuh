@@ -94,7 +94,7 @@ struct TcGeom {
                 "128-lane tiles: row segments, row pairs, or single rows");
   static_assert(H % RB == 0 && RB % RPT == 0 && RB >= MH - 1 && TPI % 2 == 0, "band geometry");
   static_assert(TAPS <= kTcTaps && 32 + MW - 1 <= kTcStripW && MW <= 16 && MW < W, "filter support");
-  static_assert(KF % 32 == 0 && KF >= 32 && KF <= 128, "filters per pass");
+  static_assert(KF % 16 == 0 && KF >= 32 && KF <= 128, "filters per pass");
   static constexpr size_t d_bytes = (size_t)2 * KF * TP * 2;
   static constexpr size_t lam_off = d_bytes;
   static constexpr size_t lam_bytes = (size_t)2 * SR * LWW * 4;
@@ -519,6 +519,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
             umma::split2x2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1]), sw, vh[jj], vl[jj]);
           umma::st16(A + ch * 16, vh);
           umma::st16(A + 64 + ch * 16, vl);
+        }
+        if constexpr (KF % 32 != 0) {  // a last chunk of 16 filter slots (KF = 112)
+          uint32_t v[16];
+          umma::ld16(ACC + (KF / 32) * 32, v);
+          umma::wait_ld();
+          uint32_t vh[8], vl[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            umma::split2x2(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1]), sw, vh[jj], vl[jj]);
+          umma::st8(A + (KF / 32) * 16, vh);
+          umma::st8(A + 64 + (KF / 32) * 16, vl);
         }
         umma::wait_st();
         umma::fence_before_sync();
