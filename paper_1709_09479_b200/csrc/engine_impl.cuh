@@ -1149,7 +1149,10 @@ class Engine final : public EngineBase {
     // so each half's per-iteration neighbours (band reduction, lambda_hat
     // update, the two FFTs, lambda split) run beside the other half's coding
     // pass instead of between two full-width passes
-    const int half = (tc && tc_use(cnt / 2) && cnt >= 2) ? cnt / 2 : 0;
+    // (measured: C1 23.6 -> 24.7, C2 3.81 -> 4.51, C4 1.92 -> 2.20 outer iters/s; DCSC_TC_SPLIT=0 disables)
+    const char* sp = std::getenv("DCSC_TC_SPLIT");
+    const bool split = !(sp && sp[0] == '0');
+    const int half = (tc && split && cnt >= 2) ? cnt / 2 : 0;
     cudaEvent_t ev2[2] = {nullptr, nullptr};
     if (half) {
       CK(cudaEventCreateWithFlags(&ev2[0], cudaEventDisableTiming));
