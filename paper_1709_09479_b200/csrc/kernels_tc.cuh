@@ -8,9 +8,10 @@
 // spectral products are circular correlations / convolutions with m*m taps:
 //   t_k[p] = sum_o d_k[o] lambda[p + o],  s[p] = sum_k sum_o d_k[o] w_k[p - o],
 // and DFT(s) = sum_k d_hat_k w_hat_k exactly. Over all filters at once they are
-// two GEMMs per tile of 128 pixels (one row segment):
-//   GEMM-1  T[p][k] = sum_o L[p][o] D[k][o]    L = im2col(lambda) (M=128, N=KF, K=128 taps)
-//   GEMM-2  Z[p][o] = sum_k W[p][k] D[k][o]    W = w of the tile   (M=128, N=128 taps, K=KF)
+// two GEMMs per tile of 128 pixels (a row segment, a row pair at W = 64, or one
+// row with idle lanes for 64 < W < 128):
+//   GEMM-1  T[p][k] = sum_o L[p][o] D[k][o]    L = im2col(lambda) (M=128, N=KF, K=TP taps)
+//   GEMM-2  Z[p][o] = sum_k W[p][k] D[k][o]    W = w of the tile   (M=128, N=TP taps, K=KF)
 // followed by the col2im sum s[p + o] += Z[p][o]. Both run on tcgen05 with the
 // pixel operand in tensor memory and the dictionary in shared memory (one
 // copy serves GEMM-1 K-major and GEMM-2 MN-major), accumulating in FP32; each
@@ -20,11 +21,13 @@
 // The per-image FFT work that remains is one r2c of s and one c2r of lambda_hat
 // per iteration instead of a c2r + r2c per filter.
 //
-// Persistent kernel, one CTA per SM, 9 warps: warp 0 issues the MMAs (one
-// thread); warps 1-8 are two epilogue groups of 4 warps (one per TMEM lane
-// quarter = 32 pixels), each owning one of two tensor-memory slots (256
-// columns: A operand = im2col then W; accumulator = T then Z) and alternate
-// tiles, so one group's epilogue overlaps the other group's GEMMs.
+// Persistent kernel, one CTA per SM, 10 warps: warp 0 issues the GEMMs (a
+// converged warp, one elected lane, uniform operands); warps 1-8 are two
+// epilogue groups of 4 warps (one per TMEM lane quarter = 32 pixels), each
+// owning one of two tensor-memory slots (256 columns: A operand = im2col then
+// W; accumulator = T then Z) and alternate tiles, so one group's epilogue
+// overlaps the other group's GEMMs; warp 9 streams u by 2-D TMA into one
+// shared-memory ring per group (plus L2 tensor prefetches ahead).
 // Work item = (image, band of RB tile rows); deterministic: every sum has a
 // fixed order (per-warp col2im strips, strips and bands summed in index order).
 #pragma once
