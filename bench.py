@@ -68,6 +68,9 @@ CONFIGS = {
     # tensor-core pass's default batch threshold, so it is forced (DCSC_TC=1) to profile C3's kernel
     "c3s": dict(N=16, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
                 max_admm=10, outer=1, env={"DCSC_TC": "1"}),
+    # a 128-image C3 coding slice for A/B timing of the coding pass under load (~14 work items per SM)
+    "c3m": dict(N=128, H=256, W=256, K=128, m=11, prec=32, beta=0.5, p=0.01, sigma=0.01, coding_only=True,
+                max_admm=20, outer=1),
     "c4": dict(N=2048, H=64, W=64, K=32, m=7, prec=32, beta=0.5, p=0.005, sigma=0.05, coding_only=False,
                max_admm=500, outer=10),
 }

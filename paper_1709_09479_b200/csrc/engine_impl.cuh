@@ -2319,10 +2319,21 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
   dtw.alloc(sizeof(C) * P::TW_LEN);
   CK(cudaMemcpy(dtw.p, tw.data(), dtw.bytes, cudaMemcpyHostToDevice));
   spec.alloc(sizeof(C) * (size_t)batch * NB);
+  // FP32 families run the storage-precision kernels the engine uses (the
+  // input rounded to float once, as set_signals does; the output widened)
+  constexpr bool narrow = !std::is_same<R, double>::value;
   if (!inverse) {
-    din.alloc(sizeof(double) * (size_t)batch * D);
-    CK(cudaMemcpy(din.p, in, din.bytes, cudaMemcpyHostToDevice));
-    E::template launch_r2c<double>(batch, 0, din.as<double>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+    if constexpr (narrow) {
+      std::vector<R> hin((size_t)batch * D);
+      for (size_t i = 0; i < hin.size(); ++i) hin[i] = R(in[i]);
+      din.alloc(sizeof(R) * hin.size());
+      CK(cudaMemcpy(din.p, hin.data(), din.bytes, cudaMemcpyHostToDevice));
+      E::template launch_r2c<R>(batch, 0, din.as<R>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+    } else {
+      din.alloc(sizeof(double) * (size_t)batch * D);
+      CK(cudaMemcpy(din.p, in, din.bytes, cudaMemcpyHostToDevice));
+      E::template launch_r2c<double>(batch, 0, din.as<double>(), D, spec.as<C>(), NB, dtw.as<C>(), nullptr, 1);
+    }
     CK(cudaGetLastError());
     std::vector<C> h((size_t)batch * NB);
     CK(cudaMemcpy(h.data(), spec.p, spec.bytes, cudaMemcpyDeviceToHost));
@@ -2334,10 +2345,19 @@ void dft_batch(bool inverse, int batch, const double* in, double* out) {
     std::vector<C> h((size_t)batch * NB);
     for (size_t i = 0; i < h.size(); ++i) h[i] = mk<C>(R(in[2 * i]), R(in[2 * i + 1]));
     CK(cudaMemcpy(spec.p, h.data(), spec.bytes, cudaMemcpyHostToDevice));
-    dout.alloc(sizeof(double) * (size_t)batch * D);
-    E::template launch_c2r<double>(batch, 0, spec.as<C>(), NB, dout.as<double>(), D, dtw.as<C>());
-    CK(cudaGetLastError());
-    CK(cudaMemcpy(out, dout.p, dout.bytes, cudaMemcpyDeviceToHost));
+    if constexpr (narrow) {
+      dout.alloc(sizeof(R) * (size_t)batch * D);
+      E::template launch_c2r<R>(batch, 0, spec.as<C>(), NB, dout.as<R>(), D, dtw.as<C>());
+      CK(cudaGetLastError());
+      std::vector<R> hout((size_t)batch * D);
+      CK(cudaMemcpy(hout.data(), dout.p, dout.bytes, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < hout.size(); ++i) out[i] = double(hout[i]);
+    } else {
+      dout.alloc(sizeof(double) * (size_t)batch * D);
+      E::template launch_c2r<double>(batch, 0, spec.as<C>(), NB, dout.as<double>(), D, dtw.as<C>());
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(out, dout.p, dout.bytes, cudaMemcpyDeviceToHost));
+    }
   }
   CK(cudaDeviceSynchronize());
 }
