@@ -564,8 +564,10 @@ class Engine final : public EngineBase {
         tspart_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::SR * W);
         tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
         tupd_.alloc(sizeof(int) * (size_t)N_);
+        tzmax_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::TPI * 4);
         if (!CLU) tu_.alloc(sizeof(float) * (size_t)N_ * K_ * D);
-        device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes + tu_.bytes;
+        device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes + tu_.bytes +
+                        tzmax_.bytes;
         CK(cudaDeviceGetAttribute(&tc_grid_, cudaDevAttrMultiProcessorCount, o.device));
         // TMA map of u as [N*K planes][D pixels] FP32, box 16 planes x 128 pixels
         void* fn = nullptr;
@@ -704,6 +706,17 @@ class Engine final : public EngineBase {
       }
     }
   }
+  // max |z/rho| per warp-tile of the stored u: the pass's bound for W's f16 scale
+  void tc_zmax(int n0, int cnt) {
+    if constexpr (kTcFamily) {
+      using G = TG<kTcKFb>;
+      launch(kFamOther, [&] {
+        tc_zmax_init<G><<<dim3(G::NBANDS * G::TPI, cnt), 128, 0, st_>>>(
+            (CLU ? u_.as<float>() : tu_.as<float>()) + (size_t)n0 * K_ * D,
+            tzmax_.as<float>() + (size_t)n0 * G::NBANDS * G::TPI * 4, K_, (float)cfg_.beta);
+      });
+    }
+  }
   bool tc_use(int cnt) const {
     if constexpr (kTcFamily) {
       return tc_ && (tc_force_ || (long)cnt * TG<kTcKFb>::NBANDS >= 2L * tc_grid_);
@@ -741,6 +754,8 @@ class Engine final : public EngineBase {
       a.spart = tspart_.as<float>() + (size_t)n0 * G::NBANDS * G::SR * W;
       a.bsums = tbsums_.as<double>() + (size_t)n0 * G::NBANDS * kSums;
       a.conv = conv_.as<int>() + n0;
+      a.zmax = tzmax_.as<float>() + (size_t)n0 * G::NBANDS * G::TPI * 4;
+      a.tbound = tc_tbound_;
       a.N = cnt;
       a.K = K_;
       a.rho = (float)cfg_.rho;
@@ -879,6 +894,13 @@ class Engine final : public EngineBase {
         float amax = 0.f;
         for (double v : dict_) amax = std::max(amax, (float)std::fabs(v));
         tc_dscale_ = umma::pow2_scale(amax);
+        double l1max = 0.0;  // max_k ||d_k||_1 (J = 1): the pass's bound on |t|
+        for (int k = 0; k < K_; ++k) {
+          double l1 = 0.0;
+          for (int o = 0; o < M_; ++o) l1 += std::fabs(dict_[(size_t)k * M_ + o]);
+          l1max = std::max(l1max, l1);
+        }
+        tc_tbound_ = (float)(2.0 * 16384.0 * l1max);
         launch(kFamOther, [&] {
           constexpr int TP = TG<kTcKFb>::TP;
           if (tc_kf_ == kTcKFa)
@@ -1141,6 +1163,7 @@ class Engine final : public EngineBase {
     if (tc) {
       if (!CLU) tc_convert_u(n0, cnt, true);
       tc_lambda_spatial(n0, cnt);
+      tc_zmax(n0, cnt);
     }
     cudaEvent_t ev[2];
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -2276,8 +2299,8 @@ class Engine final : public EngineBase {
   // tensor-core coding pass (kernels_tc.cuh)
   bool tc_ = false, tc_force_ = false;
   int tc_kf_ = 128, tc_grid_ = 148;
-  float tc_dscale_ = 1.f;
-  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_, tu_, tupd_;
+  float tc_dscale_ = 1.f, tc_tbound_ = 0.f;
+  DevMem tlam16_, tlscale_, tdsplit_, tspart_, tbsums_, tu_, tupd_, tzmax_;
   CUtensorMap tc_umap_{};
   std::vector<double> dict_, mu_, xnorm2_, xnorm2c_, xs_host_, dstage_;
   std::vector<int> degen_;  // per image: normalisation met a constant input

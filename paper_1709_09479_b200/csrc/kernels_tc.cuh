@@ -70,6 +70,8 @@ struct TcArgs {
   float* spart;            // N x NBANDS x SR x W col2im band partials
   double* bsums;           // N x NBANDS x kSums stop-test partial sums
   const int* conv;         // N
+  float* zmax;             // N x NBANDS x TPI x 4: per warp and tile, max_k |z/rho| of the stored u (written each pass)
+  float tbound;            // |t| <= tbound / lam_scale[n] (2 * 2^14 * max_k ||d_k||_1)
   int N, K;
   float rho, beta;
 };
@@ -405,7 +407,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         for (int pl = 0; pl < 2; ++pl)
           prefetch_l2_bulk(a.lam16 + ((size_t)(n2 * 2 + pl) * H + b2 * RB) * (W / 2), (unsigned)(rows * W * 2));
       }
-      const float tsc = 1.f / (__ldg(a.lam_scale + n) * a.d_scale);
+      const float lsc = __ldg(a.lam_scale + n);
+      const float tsc = 1.f / (lsc * a.d_scale);
+      const float tb = a.tbound / lsc;
       const float dinv = 1.f / a.d_scale;
       double st[7] = {0, 0, 0, 0, 0, 0, 0};
       float* const ubase = a.u + (size_t)n * a.K * D;
@@ -451,7 +455,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         // sum z'^2 = rho^2 sum (theta' - u')^2 are scaled once per tile
         // per-pair accumulators (packed FP32), folded once per tile
         F2 a0 = f2(0.f, 0.f), a1 = a0, a2 = a0, a4 = a0, a5 = a0;
-        float f6 = 0.f, wmax = 0.f;
+        float f6 = 0.f, wmax = 0.f, zm = 0.f;
+        // W's per-pixel f16 scale from a bound known before the prox (not T0):
+        // |w| = |2 theta' - u'| <= beta + |u'| <= beta + |t| + |z_old / rho|, with
+        // |t| <= ||d_k||_1 max|lambda| (tb) and max_k |z_old / rho| of this warp's
+        // pixels recorded by the previous pass (zmax) -> w is split as it is formed
+        float* const zslot = a.zmax + (((size_t)n * NBANDS + b) * TPI + t) * 4 + q;
+        const float sw_pred = T0 ? 1.f : umma::pow2_scale(beta + tb + *zslot);
         const float tsl = live ? tsc : 0.f;  // dead lanes: t = u = 0, so w = 0 and no stop-test share
         const F2 tsc2 = f2(tsl, tsl);
         mbar_wait(t_full + e, ph);
@@ -468,7 +478,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
               tcur[j] = ((FULL || k < a.K) && live) ? __ldg(t0p + (size_t)k * D) : 0.f;
             }
           }
-          uint32_t v[16];
+          uint32_t v[16], vh[8], vl[8];
           umma::ld16(ACC + ch * 16, v);
           umma::wait_ld();
 #pragma unroll
@@ -496,23 +506,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
             a4 = fma2(d_z, d_z, a4);
             a5 = fma2(dth, dth, a5);
             f6 = fmaxf(f6, fmaxf(fabsf(f2x(t)), fabsf(f2y(t))));
+            zm = fmaxf(zm, fmaxf(fabsf(f2x(d_z)), fabsf(f2y(d_z))));
             const F2 w = add2(th, d_z);  // w = theta' + z'/rho = 2 theta' - u'
             const float w0 = f2x(w), w1 = f2y(w);
-            wmax = fmaxf(wmax, fmaxf(fabsf(w0), fabsf(w1)));
+            if constexpr (T0) {
+              wmax = fmaxf(wmax, fmaxf(fabsf(w0), fabsf(w1)));
+            } else {
+              umma::split2x2(w0, w1, sw_pred, vh[jj], vl[jj]);
+            }
             if ((FULL || k0 < a.K) && live) __stcs(up + (size_t)k0 * D, un0);
             if ((FULL || k0 + 1 < a.K) && live) __stcs(up + (size_t)(k0 + 1) * D, un1);
             v[2 * jj] = __float_as_uint(w0);
             v[2 * jj + 1] = __float_as_uint(w1);
           }
-          umma::st16(ACC + ch * 16, v);
+          if constexpr (T0) {
+            umma::st16(ACC + ch * 16, v);
+          } else {  // filter pairs 8 ch .. 8 ch + 7 -> W columns (hi, lo)
+            umma::st8(A + ch * 8, vh);
+            umma::st8(A + 64 + ch * 8, vl);
+          }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) zm = fmaxf(zm, __shfl_xor_sync(0xffffffffu, zm, o));
+        if (lane == 0) *zslot = zm;
         const float f0 = f2x(a0) + f2y(a0), f1 = f2x(a1) + f2y(a1), f2_ = f2x(a2) + f2y(a2),
                     f4 = f2x(a4) + f2y(a4), f5 = f2x(a5) + f2y(a5);
         TCT(3)
         umma::wait_st();
-        const float sw = umma::pow2_scale(wmax);
+        const float sw = T0 ? umma::pow2_scale(wmax) : sw_pred;
 #pragma unroll 1
-        for (int ch = 0; ch < KF / 32; ++ch) {
+        for (int ch = 0; ch < (T0 ? KF / 32 : 0); ++ch) {
           uint32_t v[32];
           umma::ld32(ACC + ch * 32, v);
           umma::wait_ld();
@@ -523,7 +546,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
           umma::st16(A + ch * 16, vh);
           umma::st16(A + 64 + ch * 16, vl);
         }
-        if constexpr (KF % 32 != 0) {  // a last chunk of 16 filter slots (KF = 112)
+        if constexpr (T0 && KF % 32 != 0) {  // a last chunk of 16 filter slots (KF = 112)
           uint32_t v[16];
           umma::ld16(ACC + (KF / 32) * 32, v);
           umma::wait_ld();
@@ -622,6 +645,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
     umma::fence_after_sync();
     umma::tmem_free<512>(tbase);
   }
+}
+
+// zmax of a stored u (coding_pass_tc's per warp-tile record, recomputed at the
+// start of a coding call): max_k |clamp(u, beta) - u| over the 32 pixels that
+// epilogue warp q handles in tile t of band b. Block (b * TPI + t, n), 128 threads.
+template <class G>
+__global__ void __launch_bounds__(128) tc_zmax_init(const float* __restrict__ u, float* __restrict__ zmax, int K,
+                                                    float beta) {
+  constexpr int W = G::W, D = G::D, TPR = G::TPR, WT = G::WT, RPT = G::RPT, RB = G::RB, TPI = G::TPI;
+  const int n = blockIdx.y, b = blockIdx.x / TPI, t = blockIdx.x % TPI;
+  const int p = threadIdx.x, lane = p & 31, q = p >> 5;
+  const bool live = p < G::VALID;
+  const int pc = live ? p : p - G::VALID;
+  const int r = b * RB + (t / TPR) * RPT + pc / WT, c = (t % TPR) * 128 + pc % WT;
+  const float* up = u + (size_t)n * K * D + (size_t)r * W + c;
+  float m = 0.f;
+  if (live)
+    for (int k = 0; k < K; ++k) {
+      const float v = __ldg(up + (size_t)k * D);
+      m = fmaxf(m, fabsf(fminf(fmaxf(v, -beta), beta) - v));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) zmax[((size_t)n * gridDim.x + blockIdx.x) * 4 + q] = m;
 }
 
 // s[n] = sum of the band partials (each output row from its own band and the
