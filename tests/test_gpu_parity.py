@@ -117,8 +117,8 @@ def test_coding_fp32_matches_reference():
     cfg = ref.Cfg(beta=0.5, max_admm=50, normalize=0)
     z_r, st_r, s_r = ref.solve_coding(x[0], d, cfg)
     z_g, st_g, s_g = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=0.5, max_admm=50, normalize=0), precision=32)
-    assert abs(s_g["admm_iters"] - s_r["admm_iters"]) <= 1
-    assert rel(z_g, z_r) <= 1e-3  # element-wise maps; the objective below carries the 1e-4 bar
+    assert s_g["admm_iters"] == s_r["admm_iters"]
+    assert rel(z_g, z_r) <= FP32_TOL  # element-wise maps, relative to max|z|
     og = dcsc.evaluate_objective(x[0], d, z_g, 0.5, precision=64)
     orf = ref.objective(x[0], d, z_r, 0.5)
     assert abs(og[2] - orf[2]) <= FP32_TOL * abs(orf[2])
@@ -215,8 +215,8 @@ def test_cluster_plane_coding_fp32_matches_reference():
     cfg = ref.Cfg(beta=0.5, max_admm=25, normalize=0)
     z_r, st_r, s_r = ref.solve_coding(x[0], d, cfg)
     z_g, st_g, s_g = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=0.5, max_admm=25, normalize=0), precision=32)
-    assert abs(s_g["admm_iters"] - s_r["admm_iters"]) <= 1
-    assert rel(z_g, z_r) <= 1e-3
+    assert s_g["admm_iters"] == s_r["admm_iters"]
+    assert rel(z_g, z_r) <= FP32_TOL
     og = dcsc.evaluate_objective(x[0], d, z_g, 0.5, precision=32)
     orf = ref.objective(x[0], d, z_r, 0.5)
     assert abs(og[2] - orf[2]) <= FP32_TOL * abs(orf[2])
@@ -245,7 +245,7 @@ def test_cluster_plane_learning_fp32_matches_reference():
     d_g, _, s_g = dcsc.solve_learning(x, maps, (11, 11), dcsc.SolverConfig(beta=0.5, normalize=0, max_mu_iters=2,
                                                                            cg_max=12), precision=32)
     assert s_g["mu_iters"] == s_r["mu_iters"]
-    assert rel(d_g, d_r) <= 1e-3
+    assert rel(d_g, d_r) <= FP32_TOL
     # the learning data term of both dictionaries agrees to the FP32 bar
     with dcsc.Context(2, (256, 256), 3, (11, 11), dcsc.SolverConfig(normalize=0), 64 if False else 32) as ctx:
         ctx.set_signals(x)
@@ -263,7 +263,7 @@ def test_cluster_plane_run_fp32_matches_reference():
     r = ref.run(x, 3, (11, 11), ref.Cfg(**kw))
     g = dcsc.run_csc(x, 3, (11, 11), dcsc.SolverConfig(**kw), precision=32)
     compare_runs(g, r, FP32_TOL)
-    assert rel(g["dict"], r["dict"]) <= 1e-3
+    assert rel(g["dict"], r["dict"]) <= FP32_TOL
 
 
 @pytest.mark.parametrize("mode", [1, 2])
@@ -319,7 +319,11 @@ def test_huge_beta_gives_zero_maps_and_lambda_minus_x():
     x, d = problem(1, (20, 20), 4, 5)
     z, st, s = dcsc.solve_coding(x[0], d, dcsc.SolverConfig(beta=1e6, rho=1.0, max_admm=500, normalize=0))
     assert np.all(z == 0)
+    # a property of the converged iterate, not a reference comparison: ADMM stops at its
+    # relative tolerance (coding.cpp:264-283), so lambda equals -x to that tolerance only
     assert rel(st.lam, -x[0]) <= 1e-3
+    z_r, st_r, s_r = ref.solve_coding(x[0], d, ref.Cfg(beta=1e6, rho=1.0, max_admm=500, normalize=0))
+    assert s["admm_iters"] == s_r["admm_iters"] and rel(st.lam, st_r.lam) <= FP64_TOL
 
 
 def test_learning_correlation_fp64_matches_reference():
@@ -372,11 +376,11 @@ def test_stateless_learning_ops_fp64_match_reference():
 def test_c4_shaped_run_fp32_matches_reference():
     """A C4-shaped slice (BASELINE configs[4]: 64x64 FP32, K=32 filters 7x7,
     p=0.005, sigma=0.05) for 2 outer iterations of run_csc against the oracle on
-    the same FP32-rounded inputs: objectives <= 1e-4, dictionary <= 1e-3."""
+    the same FP32-rounded inputs: objectives and dictionary <= 1e-4."""
     x, _ = dcsc.synth_generate(12, (64, 64), 32, 7, 0.005, 0.05, 20250917, True)
     kw = dict(beta=0.5, max_outer=2, normalize=0, seed=20250917, tol=1e-300, max_admm=120, max_mu_iters=10,
               cg_max=60)
     r = ref.run(x, 32, (7, 7), ref.Cfg(**kw))
     g = dcsc.run_csc(x, 32, (7, 7), dcsc.SolverConfig(**kw), precision=32)
     compare_runs(g, r, FP32_TOL)
-    assert rel(g["dict"], r["dict"]) <= 1e-3
+    assert rel(g["dict"], r["dict"]) <= FP32_TOL
