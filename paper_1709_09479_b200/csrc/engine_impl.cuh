@@ -246,8 +246,15 @@ class Engine final : public EngineBase {
   // (single-row families 80 / 100: 112 slots for C2's K = 100)
   static constexpr int kTcM = W == 64 ? 7 : 11, kTcKFa = W == 64 ? 32 : 64,
                        kTcKFb = W == 64 ? 64 : ((W > 64 && W < 128) ? 112 : 128);
+  // epilogue warps: 16 (two per TMEM lane quarter) where the per-tile epilogue is long (256 x 256 with
+  // 128 filter slots, the single-row 100 / 80 families with 112), 8 at 128 x 128 and 64 x 64 (measured)
+#ifdef DCSC_TC_EW
+  static constexpr int kTcEW = DCSC_TC_EW;
+#else
+  static constexpr int kTcEW = (W == 128 || W == 64) ? 8 : 16;
+#endif
   template <int KF>
-  using TG = TcGeom<H, W, KF, kTcM, kTcM, kTcRB>;
+  using TG = TcGeom<H, W, KF, kTcM, kTcM, kTcRB, kTcEW>;
   template <int KF>
   static void set_tc_attr() {
     const int sm = (int)TG<KF>::smem;
@@ -265,13 +272,13 @@ class Engine final : public EngineBase {
     constexpr size_t sm = TG<KF>::smem;
     const bool full = a.K == KF, t0 = a.theta0 != nullptr;
     if (full && !t0)
-      coding_pass_tc<TG<KF>, true, false><<<grid, kTcThreads, sm, st>>>(a);
+      coding_pass_tc<TG<KF>, true, false><<<grid, TG<KF>::THREADS, sm, st>>>(a);
     else if (full)
-      coding_pass_tc<TG<KF>, true, true><<<grid, kTcThreads, sm, st>>>(a);
+      coding_pass_tc<TG<KF>, true, true><<<grid, TG<KF>::THREADS, sm, st>>>(a);
     else if (!t0)
-      coding_pass_tc<TG<KF>, false, false><<<grid, kTcThreads, sm, st>>>(a);
+      coding_pass_tc<TG<KF>, false, false><<<grid, TG<KF>::THREADS, sm, st>>>(a);
     else
-      coding_pass_tc<TG<KF>, false, true><<<grid, kTcThreads, sm, st>>>(a);
+      coding_pass_tc<TG<KF>, false, true><<<grid, TG<KF>::THREADS, sm, st>>>(a);
   }
   // persistent pipelined r2c / c2r (SmemPipe) when the staging buffer fits and
   // the planes are 16-byte aligned storage-precision planes: grid = resident slots
@@ -564,7 +571,7 @@ class Engine final : public EngineBase {
         tspart_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::SR * W);
         tbsums_.alloc(sizeof(double) * (size_t)N_ * G::NBANDS * kSums);
         tupd_.alloc(sizeof(int) * (size_t)N_);
-        tzmax_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::TPI * 4);
+        tzmax_.alloc(sizeof(float) * (size_t)N_ * G::NBANDS * G::TPI * 4 * G::HV);
         if (!CLU) tu_.alloc(sizeof(float) * (size_t)N_ * K_ * D);
         device_bytes += tlam16_.bytes + tlscale_.bytes + tdsplit_.bytes + tspart_.bytes + tbsums_.bytes + tu_.bytes +
                         tzmax_.bytes;
@@ -713,7 +720,7 @@ class Engine final : public EngineBase {
       launch(kFamOther, [&] {
         tc_zmax_init<G><<<dim3(G::NBANDS * G::TPI, cnt), 128, 0, st_>>>(
             (CLU ? u_.as<float>() : tu_.as<float>()) + (size_t)n0 * K_ * D,
-            tzmax_.as<float>() + (size_t)n0 * G::NBANDS * G::TPI * 4, K_, (float)cfg_.beta);
+            tzmax_.as<float>() + (size_t)n0 * G::NBANDS * G::TPI * 4 * G::HV, K_, (float)cfg_.beta);
       });
     }
   }
@@ -754,7 +761,7 @@ class Engine final : public EngineBase {
       a.spart = tspart_.as<float>() + (size_t)n0 * G::NBANDS * G::SR * W;
       a.bsums = tbsums_.as<double>() + (size_t)n0 * G::NBANDS * kSums;
       a.conv = conv_.as<int>() + n0;
-      a.zmax = tzmax_.as<float>() + (size_t)n0 * G::NBANDS * G::TPI * 4;
+      a.zmax = tzmax_.as<float>() + (size_t)n0 * G::NBANDS * G::TPI * 4 * G::HV;
       a.tbound = tc_tbound_;
       a.N = cnt;
       a.K = K_;

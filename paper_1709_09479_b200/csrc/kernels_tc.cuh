@@ -52,8 +52,8 @@ namespace dcsc_cuda {
 #endif
 
 constexpr int kTcTaps = 128;                       // GEMM-1 K / GEMM-2 N (taps padded)
-constexpr int kTcEpiWarps = 8;
-constexpr int kTcThreads = 32 * (kTcEpiWarps + 2);  // 320: MMA warp, 8 epilogue warps, u streaming warp
+// epilogue warps per CTA (TcGeom::EW): 8 = one warp per (group, TMEM lane quarter); 16 = two, which
+// split the filters (prox) and the taps (im2col, col2im) of the quarter's 32 pixels. DCSC_TC_EW forces one.
 constexpr int kTcStripW = 44;
 constexpr int kTcUSlots = 6;                       // u staging ring depth per epilogue group
 constexpr int kTcUPrefetch = 8;                    // chunks ahead an L2 prefetch of u rows is issued                      // col2im strip row stride (floats) >= 32 + MW - 1
@@ -70,15 +70,19 @@ struct TcArgs {
   float* spart;            // N x NBANDS x SR x W col2im band partials
   double* bsums;           // N x NBANDS x kSums stop-test partial sums
   const int* conv;         // N
-  float* zmax;             // N x NBANDS x TPI x 4: per warp and tile, max_k |z/rho| of the stored u (written each pass)
+  float* zmax;             // N x NBANDS x TPI x 4 x HV: per warp and tile, max_k |z/rho| of the stored u (written each pass)
   float tbound;            // |t| <= tbound / lam_scale[n] (2 * 2^14 * max_k ||d_k||_1)
   int N, K;
   float rho, beta;
 };
 
-template <int H_, int W_, int KF_, int MH_, int MW_, int RB_>
+template <int H_, int W_, int KF_, int MH_, int MW_, int RB_, int EW_>
 struct TcGeom {
   static constexpr int H = H_, W = W_, KF = KF_, MH = MH_, MW = MW_, RB = RB_;
+  static constexpr int EW = EW_;                   // epilogue warps: 8 or 16
+  static constexpr int HV = EW / 8;                // warps per (group, lane quarter)
+  static constexpr int THREADS = 32 * (EW + 2);    // MMA warp, epilogue warps, u streaming warp
+  static_assert(EW == 8 || EW == 16, "epilogue warps");
   static constexpr int D = H * W;
   // a 128-lane tile is RPT image rows x WT pixels: row segments of 128 (W a multiple of 128),
   // row pairs (W = 64), or one row with 128 - W idle lanes (64 < W < 128)
@@ -106,7 +110,7 @@ struct TcGeom {
   static constexpr size_t strip_off = (lam_off + lam_bytes + 15) / 16 * 16;
   static constexpr size_t strip_bytes = (size_t)NSTRIP * STRIP * 4;
   static constexpr size_t red_off = strip_off + strip_bytes;
-  static constexpr size_t red_bytes = (size_t)8 * kTcEpiWarps * 8;
+  static constexpr size_t red_bytes = (size_t)8 * EW * 8;
   // u staging: per epilogue group a ring of kTcUSlots chunks of 16 filter rows x 128 pixels (TMA bulk copies)
   static constexpr size_t ubuf_off = (red_off + red_bytes + 127) / 128 * 128;
   static constexpr size_t ubuf_bytes = (size_t)2 * kTcUSlots * 16 * 128 * 4;
@@ -166,7 +170,10 @@ __device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned pari
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcEpiWarps) : "memory"); }
+template <int THREADS>
+__device__ __forceinline__ void epi_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory");
+}
 __device__ __forceinline__ uint32_t lds_u16(const void* p) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(smem_addr(p)));
@@ -179,13 +186,14 @@ __device__ __forceinline__ uint32_t lds_u16(const void* p) {
 // +SR*LWW words), cb = c >> 1, par = c & 1. Pairs inside one tap row are two
 // word loads + a byte permute; pairs across tap rows two half loads.
 template <class G>
-__device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint32_t A) {
+__device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint32_t A, int h) {
   constexpr int MW = G::MW, TAPS = G::TAPS, LWW = G::LWW, SR = G::SR, TP = G::TP;
   const int cb = c >> 1, par = c & 1;
   const uint32_t sel_e = par ? 0x5432u : 0x3210u;  // pair starting at an even tap column offset
   const uint32_t sel_o = par ? 0x3210u : 0x5432u;
 #pragma unroll
   for (int ch = 0; ch < TP / 32; ++ch) {
+    if (G::HV > 1 && (ch % G::HV) != h) continue;  // 32-tap chunks alternate between the quarter's warps
     uint32_t vv[2][16];
 #pragma unroll
     for (int pl = 0; pl < 2; ++pl) {
@@ -219,10 +227,53 @@ __device__ __forceinline__ void tc_build_im2col(const uint32_t* row, int c, uint
   }
 }
 
+// tensor-memory columns [C0, C0 + N) of this warp's lanes -> v[0 .. N) (largest power-of-two pieces first)
+template <int N>
+__device__ __forceinline__ void tc_ld_cols(uint32_t taddr, uint32_t* v) {
+  if constexpr (N >= 32) {
+    umma::ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
+    tc_ld_cols<N - 32>(taddr + 32, v + 32);
+  } else if constexpr (N >= 16) {
+    umma::ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
+    tc_ld_cols<N - 16>(taddr + 16, v + 16);
+  } else if constexpr (N >= 8) {
+    umma::ld8(taddr, *reinterpret_cast<uint32_t(*)[8]>(v));
+    tc_ld_cols<N - 8>(taddr + 8, v + 8);
+  } else if constexpr (N >= 4) {
+    umma::ld4(taddr, *reinterpret_cast<uint32_t(*)[4]>(v));
+    tc_ld_cols<N - 4>(taddr + 4, v + 4);
+  } else if constexpr (N >= 2) {
+    umma::ld2(taddr, *reinterpret_cast<uint32_t(*)[2]>(v));
+    tc_ld_cols<N - 2>(taddr + 2, v + 2);
+  } else if constexpr (N == 1) {
+    umma::ld1(taddr, v[0]);
+  }
+}
+
+// col2im of tap rows [OY0, OY1): s[r + oy][c + ox] += Z[p][oy * MW + ox] * zsc into this warp's
+// strip rows. Taps (oy, ox) of one ox touch distinct strip rows: OY1 - OY0 independent
+// read-modify-writes between warp syncs (lanes overlap only along ox).
+template <class G, int OY0, int OY1>
+__device__ __forceinline__ void tc_col2im(uint32_t ACC, float* S, float zsc, bool live) {
+  constexpr int MW = G::MW, C0 = OY0 * MW, NV = (OY1 - OY0) * MW;
+  uint32_t v[NV];
+  tc_ld_cols<NV>(ACC + C0, v);
+  umma::wait_ld();
+#pragma unroll
+  for (int ox = 0; ox < MW; ++ox) {
+#pragma unroll
+    for (int oy = OY0; oy < OY1; ++oy) {
+      float* sp = S + oy * kTcStripW + ox;
+      if (live) *sp = fmaf(__uint_as_float(v[(oy - OY0) * MW + ox]), zsc, *sp);
+    }
+    __syncwarp();
+  }
+}
+
 // FULL: K == KF (no padded filters); T0: a.theta0 is set (first iteration of a
 // warm state that is not ADMM-consistent).
 template <class G, bool FULL, bool T0>
-__global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(G::THREADS, 1) coding_pass_tc(const __grid_constant__ TcArgs a) {
   constexpr int H = G::H, W = G::W, KF = G::KF, MW = G::MW, RB = G::RB, D = G::D, TPR = G::TPR, TP = G::TP,
                 WT = G::WT, RPT = G::RPT,
                 NBANDS = G::NBANDS, TPI = G::TPI, SR = G::SR, LWW = G::LWW, TAPS = G::TAPS;
@@ -243,8 +294,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
   if (warp == 0) umma::tmem_alloc<512>(tslot);
   if (threadIdx.x == 32) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(a_full + i, 4);
-      mbar_init(w_full + i, 4);
+      mbar_init(a_full + i, 4 * G::HV);
+      mbar_init(w_full + i, 4 * G::HV);
       mbar_init(t_full + i, 1);
       mbar_init(z_full + i, 1);
     }
@@ -263,7 +314,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
   const int items = a.N * NBANDS;
 
   constexpr int NCU = KF / 16, NCHUNK = (TPI / 2) * NCU;  // u chunks per item and group
-  if (warp == 0 || warp == kTcEpiWarps + 1) {
+  if (warp == 0 || warp == G::EW + 1) {
     // ===== producer warps: GEMM issue (warp 0, lane 0); u row streaming by TMA (last warp) =====
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(dbar, (unsigned)G::d_bytes);
@@ -381,7 +432,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
     }
   } else {
     // ===== epilogue groups =====
-    const int ew = warp - 1, e = ew >> 2, q = warp & 3, p = 32 * q + lane, et = threadIdx.x - 32;
+    // warp -> (group e, half h, lane quarter q = warp % 4: the TMEM lanes a warp may access)
+    const int ew = warp - 1, e = (ew >> 2) & 1, h = ew >> 3, q = warp & 3, p = 32 * q + lane, et = threadIdx.x - 32;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     const uint32_t A = tbase + 256u * e + lane_off, ACC = A + 128u;
     const float rho = a.rho, beta = a.beta;
@@ -389,18 +441,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int n = item / NBANDS, b = item % NBANDS;
       if (a.conv[n]) continue;
-      epi_sync();  // previous item's strips flushed
+      epi_sync<32 * G::EW>();  // previous item's strips flushed
       {            // lambda band rows b*RB .. b*RB + SR - 1 (mod H), wrap-padded by 16 halves
         const uint32_t* src = a.lam16 + (size_t)n * 2 * (D / 2);
-        for (int i = et; i < 2 * SR * LWW; i += 32 * kTcEpiWarps) {
+        for (int i = et; i < 2 * SR * LWW; i += 32 * G::EW) {
           const int pl = i / (SR * LWW), rr = (i / LWW) % SR, wi = i % LWW;
           const int gr = (b * RB + rr) % H, sc = wi < W / 2 ? wi : wi - W / 2;
           LAM[i] = __ldg(src + ((size_t)pl * H + gr) * (W / 2) + sc);
         }
         float4* z4 = reinterpret_cast<float4*>(STR);
-        for (int i = et; i < G::NSTRIP * G::STRIP / 4; i += 32 * kTcEpiWarps) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = et; i < G::NSTRIP * G::STRIP / 4; i += 32 * G::EW) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      epi_sync();
+      epi_sync<32 * G::EW>();
       if (et == 0 && item + (int)gridDim.x < items) {  // next item's lambda band -> L2 (both f16 planes)
         const int n2 = (item + gridDim.x) / NBANDS, b2 = (item + gridDim.x) % NBANDS;
         const int rows = min(SR, H - b2 * RB);  // the wrapped rows (from row 0) are the next bands' anyway
@@ -419,16 +471,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
       float* const ring = UB + (size_t)e * kTcUSlots * 16 * 128;
       unsigned long long* const uf = ufull + e * kTcUSlots;
       unsigned long long* const ue = uempty + e * kTcUSlots;
-      int ci_next = 0;  // next chunk this warp consumes (item-relative)
-      auto take_chunk = [&](float (&uo)[16]) {
-        const uint32_t ci = uc + (uint32_t)ci_next, sl = ci % kTcUSlots;
+      // chunk cix (item-relative, group order: tile-major, filter chunks inside); chunks
+      // alternate between the quarter's warps, each released by the four warps that read it
+      auto take_chunk = [&](float (&uo)[16], int cix) {
+        const uint32_t ci = uc + (uint32_t)cix, sl = ci % kTcUSlots;
         mbar_wait(uf + sl, (ci / kTcUSlots) & 1u);
         const float* src = ring + (size_t)sl * 16 * 128 + p;
 #pragma unroll
         for (int j = 0; j < 16; ++j) uo[j] = src[j * 128];
         __syncwarp();
         if (lane == 0) mbar_arrive1(ue + sl);
-        ++ci_next;
       };
 #ifdef DCSC_TC_TRACE
       unsigned long long tr[3][8] = {};
@@ -444,7 +496,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         float* const up = ubase + (size_t)r * W + c;
         const float* const t0p = t0base ? t0base + (size_t)r * W + c : nullptr;
         // --- im2col(lambda) -> A
-        tc_build_im2col<G>(LAM + rl * LWW, c, A);
+        tc_build_im2col<G>(LAM + rl * LWW, c, A, h);
         umma::wait_st();
         umma::fence_before_sync();
         __syncwarp();
@@ -460,17 +512,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         // |w| = |2 theta' - u'| <= beta + |u'| <= beta + |t| + |z_old / rho|, with
         // |t| <= ||d_k||_1 max|lambda| (tb) and max_k |z_old / rho| of this warp's
         // pixels recorded by the previous pass (zmax) -> w is split as it is formed
-        float* const zslot = a.zmax + (((size_t)n * NBANDS + b) * TPI + t) * 4 + q;
-        const float sw_pred = T0 ? 1.f : umma::pow2_scale(beta + tb + *zslot);
+        float* const zslot = a.zmax + ((((size_t)n * NBANDS + b) * TPI + t) * 4 + q) * G::HV;
+        const float zprev = G::HV > 1 ? fmaxf(zslot[0], zslot[G::HV - 1]) : zslot[0];
+        const float sw_pred = T0 ? 1.f : umma::pow2_scale(beta + tb + zprev);
         const float tsl = live ? tsc : 0.f;  // dead lanes: t = u = 0, so w = 0 and no stop-test share
         const F2 tsc2 = f2(tsl, tsl);
         mbar_wait(t_full + e, ph);
         umma::fence_after_sync();
         TCT(2)
 #pragma unroll 1
-        for (int ch = 0; ch < KF / 16; ++ch) {
+        // filter chunks alternate between the quarter's warps; the theta0 variant needs max|w| over
+        // all filters of a pixel, so there the first warp of the quarter takes every chunk
+        for (int ch = T0 ? (h == 0 ? 0 : KF / 16) : h; ch < KF / 16; ch += T0 ? 1 : G::HV) {
           float ucur[16], tcur[16];
-          take_chunk(ucur);
+          take_chunk(ucur, ((t - e) >> 1) * NCU + ch);
           if constexpr (T0) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -528,14 +583,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) zm = fmaxf(zm, __shfl_xor_sync(0xffffffffu, zm, o));
-        if (lane == 0) *zslot = zm;
         const float f0 = f2x(a0) + f2y(a0), f1 = f2x(a1) + f2y(a1), f2_ = f2x(a2) + f2y(a2),
                     f4 = f2x(a4) + f2y(a4), f5 = f2x(a5) + f2y(a5);
         TCT(3)
         umma::wait_st();
         const float sw = T0 ? umma::pow2_scale(wmax) : sw_pred;
 #pragma unroll 1
-        for (int ch = 0; ch < (T0 ? KF / 32 : 0); ++ch) {
+        for (int ch = 0; ch < (T0 && h == 0 ? KF / 32 : 0); ++ch) {
           uint32_t v[32];
           umma::ld32(ACC + ch * 32, v);
           umma::wait_ld();
@@ -546,7 +600,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
           umma::st16(A + ch * 16, vh);
           umma::st16(A + 64 + ch * 16, vl);
         }
-        if constexpr (T0 && KF % 32 != 0) {  // a last chunk of 16 filter slots (KF = 112)
+        if (T0 && KF % 32 != 0 && h == 0) {  // a last chunk of 16 filter slots (KF = 112)
           uint32_t v[16];
           umma::ld16(ACC + (KF / 32) * 32, v);
           umma::wait_ld();
@@ -570,25 +624,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;  // warp-uniform row
         mbar_wait(z_full + e, ph);
         umma::fence_after_sync();
+        if (lane == 0) zslot[h] = zm;  // both of the quarter's warps have read the previous record by now
         TCT(5)
-        {
-          uint32_t v[4][32];
-#pragma unroll
-          for (int ch = 0; ch < TP / 32; ++ch)
-            if (ch * 32 < TAPS) umma::ld32(ACC + ch * 32, v[ch]);
-          umma::wait_ld();
-          // taps (oy, ox) of one ox touch distinct strip rows: 11 independent
-          // read-modify-writes between warp syncs (lanes overlap only along ox)
-#pragma unroll
-          for (int ox = 0; ox < MW; ++ox) {
-#pragma unroll
-            for (int oy = 0; oy < G::MH; ++oy) {
-              const int o = oy * MW + ox;
-              float* sp = S + oy * kTcStripW + ox;
-              if (live) *sp = fmaf(__uint_as_float(v[o / 32][o % 32]), zsc, *sp);
-            }
-            __syncwarp();
-          }
+        // the quarter's warps split the tap rows (disjoint strip rows): oy in [0, MH0) and [MH0, MH)
+        // (theta0 variant: W's scale is known to the quarter's first warp only, which takes both parts)
+        if constexpr (G::HV == 1) {
+          tc_col2im<G, 0, G::MH>(ACC, S, zsc, live);
+        } else {
+          if (h == 0) tc_col2im<G, 0, (G::MH + 1) / 2>(ACC, S, zsc, live);
+          if (T0 ? h == 0 : h == 1) tc_col2im<G, (G::MH + 1) / 2, G::MH>(ACC, S, zsc, live);
         }
         TCT(6)
       }
@@ -612,19 +656,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) coding_pass_tc(const __grid_con
         }
         if (lane == 0) RED[ew * 8 + i] = x;
       }
-      epi_sync();
+      epi_sync<32 * G::EW>();
       if (et == 0) {
         double* o = a.bsums + ((size_t)n * NBANDS + b) * kSums;
         for (int i = 0; i < 7; ++i) {
           double x = 0.0;
-          for (int w2 = 0; w2 < kTcEpiWarps; ++w2) x = i == 6 ? fmax(x, RED[w2 * 8 + i]) : x + RED[w2 * 8 + i];
+          for (int w2 = 0; w2 < G::EW; ++w2) x = i == 6 ? fmax(x, RED[w2 * 8 + i]) : x + RED[w2 * 8 + i];
           o[i] = x;
         }
         o[7] = 0.0;
       }
       // --- strips -> band partial (strips summed in index order)
       float* dst = a.spart + ((size_t)n * NBANDS + b) * SR * W;
-      for (int i = et; i < SR * W; i += 32 * kTcEpiWarps) {
+      for (int i = et; i < SR * W; i += 32 * G::EW) {
         const int lr = i / W, col = i % W;
         float v = 0.f;
 #pragma unroll
@@ -668,7 +712,8 @@ __global__ void __launch_bounds__(128) tc_zmax_init(const float* __restrict__ u,
     }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) zmax[((size_t)n * gridDim.x + blockIdx.x) * 4 + q] = m;
+  if (lane == 0)
+    for (int hh = 0; hh < G::HV; ++hh) zmax[(((size_t)n * gridDim.x + blockIdx.x) * 4 + q) * G::HV + hh] = m;
 }
 
 // s[n] = sum of the band partials (each output row from its own band and the

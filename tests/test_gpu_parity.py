@@ -323,7 +323,7 @@ def test_huge_beta_gives_zero_maps_and_lambda_minus_x():
     # relative tolerance (coding.cpp:264-283), so lambda equals -x to that tolerance only
     assert rel(st.lam, -x[0]) <= 1e-3
     z_r, st_r, s_r = ref.solve_coding(x[0], d, ref.Cfg(beta=1e6, rho=1.0, max_admm=500, normalize=0))
-    assert s["admm_iters"] == s_r["admm_iters"] and rel(st.lam, st_r.lam) <= FP64_TOL
+    assert s["admm_iters"] == s_r["admm_iters"] and rel(st.lam, st_r[2]) <= FP64_TOL
 
 
 def test_learning_correlation_fp64_matches_reference():
