@@ -114,6 +114,13 @@ typedef struct {
 int dcsc_cuda_last_error(char* buf, size_t len);
 /* 1 when a kernel family for this grid / precision is compiled in */
 int dcsc_cuda_supported_grid(int height, int width, int precision);
+/* The reference plans any grid at run time (spectral.cpp:16-47, DftPlan). Here every grid is a
+ * compiled kernel family: the built-in ones (DCSC_SIZES), plus grid plugins - one shared library
+ * per (precision, H, W), any even W with H and W/2 factoring into 2, 3, 5 and a half-spectrum
+ * plane that fits shared memory - built by `python -m paper_1709_09479_b200.build --grid P H W`.
+ * A plugin named libdcsc_grid_f<P>_<H>x<W>.so in <library dir>/grids or $DCSC_GRID_DIR is found by
+ * dcsc_cuda_create on its own; dcsc_cuda_load_grid registers one from any path. */
+int dcsc_cuda_load_grid(const char* path);
 
 int dcsc_cuda_create(const dcsc_cuda_opts* opts, dcsc_cuda_ctx** out);
 int dcsc_cuda_destroy(dcsc_cuda_ctx* ctx);

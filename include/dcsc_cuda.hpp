@@ -10,9 +10,11 @@
 //                        -> dcsc::cuda::solve_coding_tcsc / solve_learning_tcsc
 //                                                        (tcsc.hpp:53-68)
 // Precision defaults to FP64 (the reference's arithmetic); FP32 is opt-in.
-// Grid support: 2-D, J <= 8 channels (J > 1 = Joint channel mode), sizes
-// compiled into the library (dcsc_cuda_supported_grid); anything else throws
-// dcsc::DimensionError.
+// Grid support: 2-D, J <= 8 channels (J > 1 = Joint channel mode); the grids
+// compiled into the library plus grid plugins (one library per grid, built by
+// `python -m paper_1709_09479_b200.build --grid P H W`, found by name next to
+// the library or registered with dcsc::cuda::load_grid); dcsc_cuda_supported_grid
+// answers for both, anything else throws dcsc::DimensionError.
 #pragma once
 
 #include <cmath>
@@ -29,6 +31,10 @@
 #include "dcsc_cuda.h"
 
 namespace dcsc::cuda {
+
+inline void check(int rc);
+// register a grid plugin library (dcsc_cuda_load_grid)
+inline void load_grid(const std::string& path) { check(dcsc_cuda_load_grid(path.c_str())); }
 
 inline void check(int rc) {
   if (rc == DCSC_OK) return;

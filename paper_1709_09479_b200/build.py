@@ -98,5 +98,59 @@ def build(verbose: bool = False, defines=(), tag=None, only=None) -> str:
     return lib
 
 
+GRIDDIR = os.path.join(LIBDIR, "grids")
+
+
+def _smooth(n: int) -> bool:
+    for p in (2, 3, 5):
+        while n % p == 0:
+            n //= p
+    return n == 1
+
+
+def grid_lib(precision: int, H: int, W: int) -> str:
+    return os.path.join(GRIDDIR, f"libdcsc_grid_f{precision}_{H}x{W}.so")
+
+
+def build_grid(precision: int, H: int, W: int, force: bool = False) -> str:
+    """Compile the engine for one more grid as a plugin library (DCSC_GRID_PLUGIN,
+    csrc/engine_impl.cuh): lib/grids/libdcsc_grid_f<P>_<H>x<W>.so, which the main library
+    finds by name (the reference plans any grid at run time, spectral.cpp:16-47; here a
+    grid is a compiled kernel family). One CTA holds a half-spectrum plane in shared
+    memory, so H x (W/2 + 1) complex values must fit; H and W/2 must factor into 2, 3, 5."""
+    if precision not in (32, 64):
+        raise ValueError("precision must be 32 or 64")
+    if H < 8 or W < 16 or W % 2 or not _smooth(H) or not _smooth(W // 2):
+        raise ValueError(f"grid {H}x{W}: W must be even, H >= 8, W >= 16, and H, W/2 must factor into 2, 3 and 5")
+    plane = H * (W // 2 + 1) * (8 if precision == 32 else 16)
+    limit = 66560 if precision == 32 else 81600  # the largest single-CTA families: FP32 128x128, FP64 100x100
+    if plane > limit:
+        raise ValueError(f"grid {H}x{W} FP{precision}: half-spectrum plane of {plane} bytes exceeds the "
+                         f"single-CTA family's {limit}")
+    lib = grid_lib(precision, H, W)
+    hdrs = _headers()
+    if not force and not _stale(lib, hdrs):
+        return lib
+    os.makedirs(GRIDDIR, exist_ok=True)
+    gdir = os.path.join(ROOT, "build", "grids")
+    os.makedirs(gdir, exist_ok=True)
+    rt = "float" if precision == 32 else "double"
+    src = os.path.join(gdir, f"grid_f{precision}_{H}x{W}.cu")
+    with open(src, "w") as f:
+        f.write(f"// generated by build.build_grid: engine plugin for {rt} {H}x{W}\n"
+                f'#include "engine_impl.cuh"\n\nDCSC_GRID_PLUGIN({rt}, {H}, {W})\n')
+    log = src + ".build.log"
+    cmd = [_nvcc(), "-shared", src, "-o", lib] + NVCC_FLAGS + ["-ccbin", HOST_CXX, "-lgomp"]
+    with open(log, "w") as f:
+        r = subprocess.run(cmd, stdout=f, stderr=subprocess.STDOUT)
+    if r.returncode != 0:
+        sys.stderr.write(open(log).read()[-20000:])
+        raise RuntimeError(f"grid plugin {rt} {H}x{W} failed to compile")
+    return lib
+
+
 if __name__ == "__main__":
-    print(build(verbose=True))
+    if len(sys.argv) >= 5 and sys.argv[1] == "--grid":
+        print(build_grid(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])))
+    else:
+        print(build(verbose=True))

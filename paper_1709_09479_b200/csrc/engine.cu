@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -180,13 +181,74 @@ struct HostReducer final : Reducer {
 };
 int prec_of(const char* t) { return std::strcmp(t, "double") == 0 ? 64 : 32; }
 
+// ---- grid plugins: one engine instantiation unit per shared library (DCSC_GRID_PLUGIN in
+// engine_impl.cuh, built by paper_1709_09479_b200/build.py build_grid) for grids outside
+// DCSC_SIZES. Loaded explicitly (dcsc_cuda_load_grid) or found by name next to this
+// library (<dir>/grids/libdcsc_grid_f{32,64}_{H}x{W}.so, or $DCSC_GRID_DIR).
+struct GridPlugin {
+  int prec, H, W;
+  void* (*make)(const dcsc_cuda_opts*);
+  void (*dft)(int, int, const double*, double*);
+  void (*fft_timing)(int, int, double*, double*);
+};
+std::vector<GridPlugin>& plugins() {
+  static std::vector<GridPlugin> v;
+  return v;
+}
+std::mutex& plugin_mutex() {
+  static std::mutex m;
+  return m;
+}
+const GridPlugin* load_plugin(const std::string& path, bool must_exist) {
+  void* h = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
+  if (!h) {
+    if (must_exist) throw InvErr("cannot load grid plugin " + path + ": " + dlerror());
+    return nullptr;
+  }
+  auto info = reinterpret_cast<void (*)(int*, int*, int*)>(dlsym(h, "dcsc_grid_info"));
+  GridPlugin g{};
+  g.make = reinterpret_cast<void* (*)(const dcsc_cuda_opts*)>(dlsym(h, "dcsc_grid_make"));
+  g.dft = reinterpret_cast<void (*)(int, int, const double*, double*)>(dlsym(h, "dcsc_grid_dft"));
+  g.fft_timing = reinterpret_cast<void (*)(int, int, double*, double*)>(dlsym(h, "dcsc_grid_fft_timing"));
+  if (!info || !g.make || !g.dft || !g.fft_timing) {
+    dlclose(h);
+    throw InvErr(path + " is not a dcsc grid plugin");
+  }
+  info(&g.prec, &g.H, &g.W);
+  for (const GridPlugin& q : plugins())
+    if (q.prec == g.prec && q.H == g.H && q.W == g.W) return &q;  // already registered
+  plugins().push_back(g);
+  return &plugins().back();
+}
+std::string own_dir() {
+  Dl_info di;
+  if (!dladdr(reinterpret_cast<const void*>(&prec_of), &di) || !di.dli_fname) return ".";
+  std::string p = di.dli_fname;
+  const size_t k = p.rfind('/');
+  return k == std::string::npos ? "." : p.substr(0, k);
+}
+const GridPlugin* find_plugin(int H, int W, int prec) {
+  std::lock_guard<std::mutex> lk(plugin_mutex());
+  for (const GridPlugin& q : plugins())
+    if (q.prec == prec && q.H == H && q.W == W) return &q;
+  const std::string name = "libdcsc_grid_f" + std::to_string(prec) + "_" + std::to_string(H) + "x" +
+                           std::to_string(W) + ".so";
+  if (const char* d = std::getenv("DCSC_GRID_DIR"))
+    if (const GridPlugin* g = load_plugin(std::string(d) + "/" + name, false)) return g;
+  return load_plugin(own_dir() + "/grids/" + name, false);
+}
+
 std::unique_ptr<EngineBase> make_engine(const dcsc_cuda_opts& o) {
 #define DCSC_MAKE(Rt, Hh, Ww) \
   if (o.precision == prec_of(#Rt) && o.height == Hh && o.width == Ww) return make_engine_##Rt##_##Hh##_##Ww(o);
   DCSC_SIZES(DCSC_MAKE)
 #undef DCSC_MAKE
+  if (const GridPlugin* g = find_plugin(o.height, o.width, o.precision))
+    return std::unique_ptr<EngineBase>(static_cast<EngineBase*>(g->make(&o)));
   throw DimErr("no compiled kernel family for grid " + std::to_string(o.height) + "x" + std::to_string(o.width) +
-               " at FP" + std::to_string(o.precision));
+               " at FP" + std::to_string(o.precision) +
+               " (build a grid plugin: python -m paper_1709_09479_b200.build --grid " + std::to_string(o.precision) +
+               " " + std::to_string(o.height) + " " + std::to_string(o.width) + ")");
 }
 
 bool supported(int H, int W, int prec) {
@@ -194,7 +256,7 @@ bool supported(int H, int W, int prec) {
   if (prec == prec_of(#Rt) && H == Hh && W == Ww) return true;
   DCSC_SIZES(DCSC_SUP)
 #undef DCSC_SUP
-  return false;
+  return find_plugin(H, W, prec) != nullptr;
 }
 
 void fft_timing_dispatch(int H, int W, int prec, int batch, int iters, double* r2c, double* c2r) {
@@ -205,6 +267,7 @@ void fft_timing_dispatch(int H, int W, int prec, int batch, int iters, double* r
   }
   DCSC_SIZES(DCSC_FT)
 #undef DCSC_FT
+  if (const GridPlugin* g = find_plugin(H, W, prec)) return g->fft_timing(batch, iters, r2c, c2r);
   throw DimErr("no compiled FFT for this grid/precision");
 }
 
@@ -216,6 +279,7 @@ void dft_dispatch(int H, int W, int prec, bool inverse, int batch, const double*
   }
   DCSC_SIZES(DCSC_DFT)
 #undef DCSC_DFT
+  if (const GridPlugin* g = find_plugin(H, W, prec)) return g->dft(inverse ? 1 : 0, batch, in, out);
   throw DimErr("no compiled FFT for this grid/precision");
 }
 
@@ -241,7 +305,19 @@ int dcsc_cuda_last_error(char* buf, size_t len) {
   return (int)g_err.size();
 }
 
-int dcsc_cuda_supported_grid(int height, int width, int precision) { return supported(height, width, precision) ? 1 : 0; }
+int dcsc_cuda_supported_grid(int height, int width, int precision) {
+  int ok = 0;
+  guarded([&] { ok = supported(height, width, precision) ? 1 : 0; });
+  return ok;
+}
+
+int dcsc_cuda_load_grid(const char* path) {
+  return guarded([&] {
+    if (!path) throw InvErr("null argument");
+    std::lock_guard<std::mutex> lk(plugin_mutex());
+    load_plugin(path, true);
+  });
+}
 
 int dcsc_cuda_create(const dcsc_cuda_opts* opts, dcsc_cuda_ctx** out) {
   return guarded([&] {

@@ -2448,3 +2448,22 @@ void fft_timing(int batch, int iters, double* ms_r2c, double* ms_c2r) {
     fft_timing<Rt, Hh, Ww>(batch, iters, ms_r2c, ms_c2r);                                      \
   }                                                                                            \
   }
+
+// A grid plugin: the engine of one more (precision, H, W) as its own shared library, found by
+// engine.cu's dispatcher (find_plugin) through these four C symbols.
+#define DCSC_GRID_PLUGIN(Rt, Hh, Ww)                                                              \
+  DCSC_ENGINE_INSTANTIATE(Rt, Hh, Ww)                                                              \
+  extern "C" void dcsc_grid_info(int* prec, int* h, int* w) {                                      \
+    *prec = sizeof(Rt) == 8 ? 64 : 32;                                                             \
+    *h = Hh;                                                                                       \
+    *w = Ww;                                                                                       \
+  }                                                                                                \
+  extern "C" void* dcsc_grid_make(const dcsc_cuda_opts* o) {                                       \
+    return static_cast<dcsc_engine::EngineBase*>(dcsc_engine::make_engine_##Rt##_##Hh##_##Ww(*o).release()); \
+  }                                                                                                \
+  extern "C" void dcsc_grid_dft(int inverse, int batch, const double* in, double* out) {           \
+    dcsc_engine::dft_batch_##Rt##_##Hh##_##Ww(inverse != 0, batch, in, out);                       \
+  }                                                                                                \
+  extern "C" void dcsc_grid_fft_timing(int batch, int iters, double* ms_r2c, double* ms_c2r) {     \
+    dcsc_engine::fft_timing_##Rt##_##Hh##_##Ww(batch, iters, ms_r2c, ms_c2r);                      \
+  }

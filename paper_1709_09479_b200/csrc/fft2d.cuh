@@ -180,7 +180,23 @@ __device__ __forceinline__ void dft(C* x) {
 // ---------------------------------------------------------------- radix plans
 template <int... Rs> struct RadixList {};
 
-template <int L> struct PlanFor;
+// Any length whose prime factors are 2, 3 and 5 has a plan: the tuned lists below for the
+// compiled families, otherwise greedy from the largest radix {16, 10, 8, 6, 5, 4, 3, 2} that
+// divides what is left (grid plugins, build.build_grid).
+template <int R, class L> struct PrependR;
+template <int R, int... Rs> struct PrependR<R, RadixList<Rs...>> { using type = RadixList<R, Rs...>; };
+constexpr int greedy_radix(int L) {
+  constexpr int rs[8] = {16, 10, 8, 6, 5, 4, 3, 2};
+  for (int i = 0; i < 8; ++i)
+    if (L % rs[i] == 0) return rs[i];
+  return 0;
+}
+template <int L> struct PlanFor {
+  static constexpr int R = greedy_radix(L);
+  static_assert(R != 0, "FFT length must factor into 2, 3 and 5");
+  using type = typename PrependR<R, typename PlanFor<L / R>::type>::type;
+};
+template <> struct PlanFor<1> { using type = RadixList<>; };
 template <> struct PlanFor<8> { using type = RadixList<8>; };
 template <> struct PlanFor<10> { using type = RadixList<10>; };
 template <> struct PlanFor<12> { using type = RadixList<4, 3>; };

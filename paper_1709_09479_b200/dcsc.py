@@ -124,7 +124,7 @@ class SolverConfig:
 
 _lib = None
 EXPORTS = [
-    "dcsc_cuda_last_error", "dcsc_cuda_supported_grid", "dcsc_cuda_create", "dcsc_cuda_destroy",
+    "dcsc_cuda_last_error", "dcsc_cuda_supported_grid", "dcsc_cuda_load_grid", "dcsc_cuda_create", "dcsc_cuda_destroy",
     "dcsc_cuda_synchronize", "dcsc_cuda_set_signals", "dcsc_cuda_get_signals",
     "dcsc_cuda_set_dictionary", "dcsc_cuda_get_dictionary", "dcsc_cuda_init_variables",
     "dcsc_cuda_set_coding_state", "dcsc_cuda_get_coding_state", "dcsc_cuda_coding",
@@ -209,7 +209,23 @@ def _f64(a) -> np.ndarray:
 
 
 def supported_grid(h: int, w: int, precision: int) -> bool:
+    """True when a kernel family for this grid is compiled in or a grid plugin for it is found."""
     return bool(lib().dcsc_cuda_supported_grid(h, w, precision))
+
+
+def build_grid(h: int, w: int, precision: int = 64) -> str:
+    """Compile (once; needs nvcc) and register the engine plugin for a grid outside the built-in
+    families: any even w with h and w/2 factoring into 2, 3 and 5 whose half-spectrum plane fits
+    one CTA's shared memory. The reference plans any grid at run time (spectral.cpp:16-47)."""
+    from . import build as _build
+    path = _build.build_grid(precision, h, w)
+    load_grid(path)
+    return path
+
+
+def load_grid(path: str):
+    """Register a grid plugin library built elsewhere (dcsc_cuda_load_grid)."""
+    _err(lib().dcsc_cuda_load_grid(path.encode()))
 
 
 class Context:
