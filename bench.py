@@ -354,6 +354,7 @@ def run_reference(args, cfg):
         "scaling": "weak" if cfg["coding_only"] else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json generator)", "config": config_block(cfg, args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                         "extrapolated": True, "sample_seconds_per_step": round(statistics.median(samples), 2),
                          "seconds_per_outer_breakdown": {k: round(v, 2) for k, v in parts.items()},
                          "unit_costs": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in uc.items()}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -698,6 +699,7 @@ def run_ours(args, cfg):
             secs = [ref_outer_seconds(cfg, uc, cfg["N"], c)[0] for c in counts]
             out["cpu_baseline"] = {
                 "value": len(secs) / sum(secs), "unit": UNIT, "cores": threads, "kind": "reference",
+                "extrapolated": True, "sample_seconds": round(wall, 2),
                 "sample": (f"reference unit costs measured on {uc['n_sample']}-image samples ({wall:.1f}s wall on "
                            f"{threads} threads: coding capped at 1 and 3 ADMM iters, one objective"
                            + (", learning operator build/apply at two sizes" if not weak else "")
