@@ -98,7 +98,9 @@ def test_operator_is_the_identity_on_zero_maps():
     v = rng.standard_normal((1, 16, 16))
     with learning_ctx(np.zeros((1, 16, 16)), np.zeros((1, 2, 16, 16)), 3) as ctx:
         out = ctx.learning_apply(np.ones(2), v)
-    assert np.array_equal(out, v)
+    # the reference returns v bit for bit (its zero contribution is added in the signal domain); the GPU
+    # operator carries v through its r2c / c2r pair, so the identity holds to FP64 rounding
+    assert np.abs(out - v).max() <= 1e-14 * np.abs(v).max()
 
 
 def test_operator_approaches_the_identity_for_huge_multipliers():
