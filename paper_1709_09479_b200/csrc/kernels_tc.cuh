@@ -54,9 +54,15 @@ namespace dcsc_cuda {
 constexpr int kTcTaps = 128;                       // GEMM-1 K / GEMM-2 N (taps padded)
 // epilogue warps per CTA (TcGeom::EW): 8 = one warp per (group, TMEM lane quarter); 16 = two, which
 // split the filters (prox) and the taps (im2col, col2im) of the quarter's 32 pixels. DCSC_TC_EW forces one.
-constexpr int kTcStripW = 44;
+constexpr int kTcStripW = 44;                      // col2im strip row stride (floats) >= 32 + MW - 1
 constexpr int kTcUSlots = 6;                       // u staging ring depth per epilogue group
-constexpr int kTcUPrefetch = 8;                    // chunks ahead an L2 prefetch of u rows is issued                      // col2im strip row stride (floats) >= 32 + MW - 1
+#ifndef DCSC_TC_UPREFETCH  // experiment overrides (build.build(defines=[...]))
+#define DCSC_TC_UPREFETCH 8
+#endif
+#ifndef DCSC_TC_MMA_SLEEP
+#define DCSC_TC_MMA_SLEEP 40
+#endif
+constexpr int kTcUPrefetch = DCSC_TC_UPREFETCH;    // chunks ahead an L2 prefetch of u rows is issued
 
 struct TcArgs {
   CUtensorMap umap;        // u as [N*K planes][D pixels] FP32, box [16 planes][128 pixels]
@@ -387,7 +393,7 @@ __global__ void __launch_bounds__(G::THREADS, 1) coding_pass_tc(const __grid_con
         } else if (n2 < n1 && lane0_test(w_full + (n2 & 1u), (n2 >> 1) & 1u)) {
           gemm2(n2++);
         } else {
-          __nanosleep(40);  // keep the polling off the epilogue warps' issue slots
+          __nanosleep(DCSC_TC_MMA_SLEEP);  // keep the polling off the epilogue warps' issue slots
         }
       }
     } else
