@@ -183,6 +183,32 @@ __device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned pari
       : "memory");
   return ok != 0;
 }
+// Wait for a GEMM's commit (1-2 us): a plain try_wait loop re-issues every ~36 cycles (ncu: 12% of the
+// pass's executed warp instructions were these two spin loops). DCSC_TC_WAIT: 0 plain loop, 1 try_wait with a
+// suspend-time hint, 2 nanosleep back-off between tries.
+#ifndef DCSC_TC_WAIT
+#define DCSC_TC_WAIT 0
+#endif
+#ifndef DCSC_TC_WAIT_NS
+#define DCSC_TC_WAIT_NS 200
+#endif
+__device__ __forceinline__ void mbar_wait_gemm(unsigned long long* bar, unsigned parity) {
+#if DCSC_TC_WAIT == 1
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITG_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITG_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"((unsigned)DCSC_TC_WAIT_NS)
+      : "memory");
+#elif DCSC_TC_WAIT == 2
+  while (!mbar_test(bar, parity)) __nanosleep(DCSC_TC_WAIT_NS);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 template <int THREADS>
 __device__ __forceinline__ void epi_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory");
@@ -530,7 +556,7 @@ __global__ void __launch_bounds__(G::THREADS, 1) coding_pass_tc(const __grid_con
         const float sw_pred = T0 ? 1.f : umma::pow2_scale(beta + tb + zprev);
         const float tsl = live ? tsc : 0.f;  // dead lanes: t = u = 0, so w = 0 and no stop-test share
         const F2 tsc2 = f2(tsl, tsl);
-        mbar_wait(t_full + e, ph);
+        mbar_wait_gemm(t_full + e, ph);
         umma::fence_after_sync();
         TCT(2)
 #pragma unroll 1
@@ -645,7 +671,7 @@ __global__ void __launch_bounds__(G::THREADS, 1) coding_pass_tc(const __grid_con
         // --- col2im: s[r + oy][c + ox] += Z[p][o] into this warp's strip
         const float zsc = dinv / sw;
         float* const S = STR + ((TPR == 1 ? e : tc) * 4 + q) * G::STRIP + rl * kTcStripW + lane;  // warp-uniform row
-        mbar_wait(z_full + e, ph);
+        mbar_wait_gemm(z_full + e, ph);
         umma::fence_after_sync();
         if (lane == 0) zslot[h] = zm;  // both of the quarter's warps have read the previous record by now
         TCT(5)
