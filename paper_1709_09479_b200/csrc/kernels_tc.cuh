@@ -717,6 +717,21 @@ __global__ void __launch_bounds__(G::THREADS, 1) coding_pass_tc(const __grid_con
       }
       // --- strips -> band partial (strips summed in index order)
       float* dst = a.spart + ((size_t)n * NBANDS + b) * SR * W;
+#ifndef DCSC_TC_STRIP_GENERIC  // build override: the general loop everywhere (bit-identity check)
+      if constexpr (TPR >= 2) {
+        // row segments of 128: strip j = s2 * 4 + q2 starts at column 32 j, so a column reads its own strip
+        // and, in its first MW - 1 columns, the spill-over of the previous one (cyclic). Two terms: the sum
+        // (0 + a) + b equals the index-order sum of the general loop below bit for bit.
+        static_assert(G::NSTRIP * 32 == W, "one strip per 32 columns");
+        for (int i = et; i < SR * W; i += 32 * G::EW) {
+          const int lr = i / W, col = i % W, j = col >> 5, off = col & 31;
+          const float* sp = STR + lr * kTcStripW + off;
+          float v = 0.f + sp[j * G::STRIP];
+          if (off < MW - 1) v += sp[((j + G::NSTRIP - 1) % G::NSTRIP) * G::STRIP + 32];
+          dst[i] = v;
+        }
+      } else
+#endif
       for (int i = et; i < SR * W; i += 32 * G::EW) {
         const int lr = i / W, col = i % W;
         float v = 0.f;
